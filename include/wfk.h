@@ -1,0 +1,199 @@
+/* libwfk — B200-native (sm_100a) non-rigid alignment solver, deformed-TSDF
+ * fusion and projective association of VolumeDeform (arXiv 1603.08161).
+ *
+ * Drop-in boundary for the reference's hot path (warpfuse, namespace wf).
+ * Each entry point below names the reference function it replaces; the C++
+ * adapter a maintainer adds on the reference side wraps a
+ * wf::DeformableVolume / std::vector<wf::Correspondence> around these calls and
+ * re-throws the reference's exception types from the returned status.
+ *
+ * Conventions
+ *   - Every function returns WFK_OK (0) or a negative WFK_E_* status;
+ *     wfk_last_error(ctx) describes the last failure.  No exception crosses.
+ *   - Calls are synchronous (results are ready on return, like the reference)
+ *     and not re-entrant per context; use one context per thread / GPU.
+ *   - The context owns a device-resident copy of ONE DeformableVolume; host
+ *     arrays are only touched by wfk_volume_upload / wfk_volume_download and
+ *     the explicit download helpers, so a caller that keeps the volume resident
+ *     pays no host<->device traffic between calls.
+ *   - Exec arguments are accepted for interface parity; the device path is
+ *     deterministic (run-to-run identical) for both values.
+ */
+#pragma once
+
+#include "wfk_types.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct wfk_ctx wfk_ctx;
+
+typedef struct wfk_config {
+  int32_t device;   /* CUDA ordinal */
+  int32_t reserved_[7];
+} wfk_config;
+
+/* ---- context ------------------------------------------------------------- */
+int wfk_create(const wfk_config* cfg, wfk_ctx** out);
+void wfk_destroy(wfk_ctx* ctx);
+const char* wfk_last_error(const wfk_ctx* ctx);
+int wfk_version(void);
+/* kernel launches issued by this context so far (for bench accounting) */
+int64_t wfk_launch_count(const wfk_ctx* ctx);
+/* total PCG iterations run by this context so far */
+int64_t wfk_pcg_iteration_count(const wfk_ctx* ctx);
+
+/* ---- volume residency (DeformableVolume, volume.hpp:29-112) --------------- */
+/* (Re)allocates the device lattice when dims change; copies the fields in
+ * `fields` (WFK_VOL_* mask). */
+int wfk_volume_upload(wfk_ctx* ctx, const wfk_volume_view* v, uint32_t fields);
+int wfk_volume_download(wfk_ctx* ctx, wfk_volume_view* v, uint32_t fields);
+
+/* ---- solver (proj/include/wf/solver.hpp) ------------------------------------- */
+/* compute_active_set (solver.hpp:40, solver.cpp:32-69): grow-only.  Writes the
+ * ascending active list to out (may be NULL) and its length to n_out. */
+int wfk_compute_active_set(wfk_ctx* ctx, int32_t* out, int64_t cap, int64_t* n_out);
+
+/* Constraints for the next solve / energy call (the std::vector<Correspondence>
+ * argument of solver.hpp:89-119).  Anchors must be the trilinear anchors of a
+ * lattice cell (anchor k = anchor 0 + corner offset k), as
+ * DeformableVolume::trilinear_anchors produces them; anything else is
+ * WFK_E_INVALID_ARG, an index outside the lattice WFK_E_OUT_OF_RANGE. */
+int wfk_constraints_upload(wfk_ctx* ctx, const wfk_correspondence* c, int64_t n);
+/* download the constraints the context currently holds (e.g. after
+ * wfk_find_dense_correspondences); n_out = count */
+int wfk_constraints_download(wfk_ctx* ctx, wfk_correspondence* out, int64_t cap, int64_t* n_out);
+
+/* evaluate_energy (solver.hpp:88-90, solver.cpp:345-383) */
+int wfk_evaluate_energy(wfk_ctx* ctx, const wfk_pose* pose, const wfk_solver_params* p,
+                        wfk_energy* out);
+/* update_rotations (solver.hpp:94, solver.cpp:385-417) */
+int wfk_update_rotations(wfk_ctx* ctx, int32_t exec);
+/* flip_flop_solve (solver.hpp:97-101, solver.cpp:419-453) on the volume */
+int wfk_flip_flop_solve(wfk_ctx* ctx, const wfk_pose* pose, const wfk_solver_params* p,
+                        int32_t level, wfk_trace_entry* trace, int32_t cap, int32_t* n_out);
+/* solve_coarse_to_fine (solver.hpp:117-119, solver.cpp:505-534) */
+int wfk_solve_coarse_to_fine(wfk_ctx* ctx, const wfk_pose* pose, const wfk_solver_params* p,
+                             wfk_trace_entry* trace, int32_t cap, int32_t* n_out);
+
+/* build_normal_equations (solver.hpp:62-66, solver.cpp:108-280), materialised
+ * on the host in the reference layout.  Two-call: pass NULL arrays to get
+ * rows_out, then call again with arrays sized rows*27*9 (blocks, row-major
+ * 3x3), rows*27 (cols), rows*3 (rhs), rows (rows, frozen), n (node_row). */
+typedef struct wfk_ne_host {
+  int32_t* rows;
+  int32_t* node_row;
+  double* blocks;
+  int32_t* cols;
+  double* rhs;
+  uint8_t* frozen;
+} wfk_ne_host;
+int wfk_build_normal_equations(wfk_ctx* ctx, const wfk_pose* pose, const wfk_solver_params* p,
+                               wfk_ne_host* out, int32_t* rows_out);
+
+/* pcg_solve (solver.hpp:83-86, solver.cpp:282-343) on an explicit assembled
+ * NormalEquations (host arrays as above, `rows` rows); x is in/out (rows*3). */
+int wfk_pcg_solve(wfk_ctx* ctx, int32_t rows, const double* blocks, const int32_t* cols,
+                  const double* rhs, double* x, double tol, int32_t max_iters, int32_t exec,
+                  wfk_pcg_result* out);
+/* NormalEquations::multiply (solver.cpp:71-89) on an explicit system */
+int wfk_ne_multiply(wfk_ctx* ctx, int32_t rows, const double* blocks, const int32_t* cols,
+                    const double* x, double* y);
+
+/* hierarchy shape (build_hierarchy, solver.cpp:455-503): dims and active count
+ * of each level for the current volume + constraints. */
+int wfk_hierarchy_info(wfk_ctx* ctx, int32_t levels, int32_t* dims_out, int64_t* active_out);
+
+/* ---- fusion (proj/include/wf/fusion.hpp) ---------------------------------- */
+/* Uploads the frame used by integrate / backproject / association. */
+int wfk_frame_upload(wfk_ctx* ctx, const wfk_frame_view* frame);
+/* integrate_frame (fusion.hpp:26-28, fusion.cpp:7-83) with the uploaded frame */
+int wfk_integrate_frame(wfk_ctx* ctx, const wfk_pose* pose, const wfk_fusion_params* p,
+                        int32_t exec, wfk_fusion_stats* out);
+/* expand_grid (fusion.hpp:37, fusion.cpp:85-122) */
+int wfk_expand_grid(wfk_ctx* ctx, wfk_expansion_stats* out);
+/* advance_ages (fusion.hpp:40, fusion.cpp:124-126) */
+int wfk_advance_ages(wfk_ctx* ctx, const int32_t* idx, int64_t n);
+/* advance_ages over exactly the active set (pipeline.cpp:249-252) */
+int wfk_advance_active_ages(wfk_ctx* ctx);
+
+/* ---- association / "raycast" (correspond.hpp, isosurface.hpp) ------------ */
+/* backproject_depth (correspond.hpp:44, correspond.cpp:7-57) of the uploaded
+ * frame; out may be NULL (maps stay on the device). */
+int wfk_backproject_depth(wfk_ctx* ctx, int32_t exec, wfk_point_normal_map* out);
+/* extract_mesh (isosurface.hpp:49, isosurface.cpp:39-97); sizes returned */
+int wfk_extract_mesh(wfk_ctx* ctx, const wfk_pose* pose, int64_t* nv, int64_t* nt);
+/* re-warp the mesh's canonical vertices through the current field (the
+ * `redeform` step of pipeline.cpp:167-169) */
+int wfk_mesh_warp(wfk_ctx* ctx, const wfk_pose* pose);
+/* compute_normals (isosurface.hpp:52, isosurface.cpp:99-112) */
+int wfk_compute_normals(wfk_ctx* ctx);
+/* replace / read the device mesh */
+int wfk_mesh_upload(wfk_ctx* ctx, const wfk_mesh_view* m);
+int wfk_mesh_download(wfk_ctx* ctx, wfk_mesh_view* m);
+/* rasterize (isosurface.hpp:56-57, rasterize.cpp:29-137); out may be NULL */
+int wfk_rasterize(wfk_ctx* ctx, const wfk_intrinsics* intr, int32_t exec,
+                  wfk_geometry_buffer* out);
+int wfk_gbuffer_upload(wfk_ctx* ctx, const wfk_geometry_buffer* b);
+/* find_dense_correspondences (correspond.hpp:61-64, correspond.cpp:114-150) from
+ * the device geometry buffer and maps; the result replaces the context's
+ * constraints.  With drop_inactive != 0 constraints with an inactive anchor
+ * are removed as pipeline.cpp:220-229 does.  n_out = count. */
+int wfk_find_dense_correspondences(wfk_ctx* ctx, const wfk_intrinsics* intr,
+                                   const wfk_correspond_params* p, int32_t drop_inactive,
+                                   int64_t* n_out);
+/* append caller-supplied constraints (e.g. sparse feature constraints) to the
+ * context's constraints; with drop_inactive != 0 keeps only fully active ones */
+int wfk_constraints_append(wfk_ctx* ctx, const wfk_correspondence* c, int64_t n,
+                           int32_t drop_inactive, int64_t* kept);
+
+/* ---- per-frame hot path (Reconstructor::process_frame, pipeline.cpp:143-262,
+ * without ICP and the feature front-end) --------------------------------------- */
+typedef struct wfk_pipeline_config {
+  wfk_solver_params solver;
+  wfk_correspond_params correspond;
+  wfk_fusion_params fusion;
+  int32_t reassociations;
+  int32_t reserved_;
+} wfk_pipeline_config;
+
+typedef struct wfk_frame_record {
+  wfk_energy energy;
+  int32_t dense_count;
+  int32_t sparse_count;
+  int32_t anomalies;
+  int32_t trace_len;
+  int32_t pcg_iterations;
+  int32_t bootstrap;
+  wfk_fusion_stats fusion;
+  wfk_expansion_stats expansion;
+} wfk_frame_record;
+
+/* frame_index 0 bootstraps (pipeline.cpp:150-159).  sparse may be NULL. */
+int wfk_process_frame(wfk_ctx* ctx, const wfk_frame_view* frame, const wfk_pose* pose,
+                      const wfk_pipeline_config* cfg, const wfk_correspondence* sparse,
+                      int64_t nsparse, int32_t frame_index, wfk_frame_record* rec);
+
+/* ---- synthetic test-bed (NOT the hot path) --------------------------------------
+ * Sphere-traced depth + color of a sphere under the reference's bend warp
+ * (synthcam.cpp:141-159, 252-316), rendered on the device for benchmarks. */
+typedef struct wfk_synth_scene {
+  double center[3];
+  double radius;
+  double pivot[3];
+  double amplitude;      /* rad/m, already multiplied by the warp phase */
+  int32_t driver_axis;
+  int32_t rot_axis;
+  double t_min, t_max;
+  uint32_t texture_seed;
+  int32_t reserved_;
+  double texture_scale;
+  double dot_radius;
+} wfk_synth_scene;
+int wfk_synth_render(wfk_ctx* ctx, const wfk_synth_scene* s, const wfk_intrinsics* intr,
+                     float* depth_out, float* color_out);
+
+#ifdef __cplusplus
+}
+#endif

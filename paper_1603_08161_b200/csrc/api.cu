@@ -1,0 +1,550 @@
+// extern "C" boundary of libwfk (include/wfk.h).  Every entry point validates
+// its arguments, runs on the context's stream and returns a status; C++
+// exceptions never cross the ABI.
+#include <cstring>
+#include <vector>
+
+#include "wfk_context.cuh"
+#include "wfk_solver.cuh"
+
+using namespace wfk;
+
+namespace {
+
+template <class F>
+int guard(wfk_ctx* c, F&& f) {
+  if (!c) return WFK_E_INVALID_ARG;
+  try {
+    WFK_CUDA(cudaSetDevice(c->device));
+    f();
+    return WFK_OK;
+  } catch (const Error& e) {
+    c->err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    c->err = e.what();
+    return WFK_E_CUDA;
+  }
+}
+
+void check_params(const wfk_solver_params* p) {
+  if (!p) throw Error(WFK_E_INVALID_ARG, "null solver params");
+}
+
+int export_trace(wfk_ctx* c, const std::vector<wfk_trace_entry>& t, wfk_trace_entry* out, int32_t cap, int32_t* n_out) {
+  if (n_out) *n_out = int32_t(t.size());
+  if (int64_t(t.size()) > cap || (!out && !t.empty())) {
+    c->err = "trace buffer too small";
+    return WFK_E_CAPACITY;
+  }
+  if (!t.empty()) std::memcpy(out, t.data(), t.size() * sizeof(wfk_trace_entry));
+  return WFK_OK;
+}
+
+// constraints -> device (SoA), validating the trilinear anchor layout
+void upload_constraints(wfk_ctx* c, const wfk_correspondence* h, int64_t n, bool append, bool drop_inactive,
+                        int64_t* kept) {
+  if (n < 0 || (n > 0 && !h)) throw Error(WFK_E_INVALID_ARG, "bad constraint array");
+  const Grid& g = c->vol.g;
+  const int64_t npts = c->vol.n;
+  std::vector<uint8_t> act;
+  if (drop_inactive) {
+    act.resize(size_t(npts));
+    WFK_CUDA(cudaMemcpyAsync(act.data(), c->vol.active, size_t(npts), cudaMemcpyDeviceToHost, c->stream));
+    WFK_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  std::vector<int32_t> kind, anchor;
+  std::vector<double> can, w, tgt, nrm, conf;
+  kind.reserve(size_t(n));
+  for (int64_t i = 0; i < n; ++i) {
+    const wfk_correspondence& r = h[i];
+    const int a0 = r.anchor_index[0];
+    for (int k = 0; k < 8; ++k)
+      if (r.anchor_index[k] < 0 || r.anchor_index[k] >= npts)
+        throw Error(WFK_E_OUT_OF_RANGE, "constraint anchor outside the lattice");
+    int x, y, z;
+    g.idx3(a0, x, y, z);
+    if (x > g.nx - 2 || y > g.ny - 2 || z > g.nz - 2)
+      throw Error(WFK_E_INVALID_ARG, "anchor 0 is not the min corner of a lattice cell");
+    for (int k = 0; k < 8; ++k)
+      if (r.anchor_index[k] != g.lin(x + (k & 1), y + ((k >> 1) & 1), z + (k >> 2)))
+        throw Error(WFK_E_INVALID_ARG, "anchors are not trilinear cell anchors");
+    if (r.kind != WFK_DENSE_PLANE && r.kind != WFK_SPARSE_POINT)
+      throw Error(WFK_E_INVALID_ARG, "unknown correspondence kind");
+    if (drop_inactive) {
+      bool all = true;
+      for (int k = 0; k < 8; ++k) all = all && act[size_t(r.anchor_index[k])];
+      if (!all) continue;
+    }
+    kind.push_back(r.kind);
+    for (int k = 0; k < 3; ++k) {
+      can.push_back(r.canonical[k]);
+      tgt.push_back(r.target[k]);
+      nrm.push_back(r.target_normal[k]);
+    }
+    for (int k = 0; k < 8; ++k) {
+      anchor.push_back(r.anchor_index[k]);
+      w.push_back(r.anchor_weight[k]);
+    }
+    conf.push_back(r.confidence);
+  }
+  const int64_t m = int64_t(kind.size());
+  if (kept) *kept = m;
+  ConIn& ci = c->cons;
+  const int64_t base = append ? ci.count : 0;
+  const int64_t total = base + m;
+  const size_t cap = size_t(total) + 1;
+  cudaStream_t s = c->stream;
+  ci.kind.grow_keep(cap, s);
+  ci.canonical.grow_keep(3 * cap, s);
+  ci.anchor.grow_keep(8 * cap, s);
+  ci.weight.grow_keep(8 * cap, s);
+  ci.target.grow_keep(3 * cap, s);
+  ci.normal.grow_keep(3 * cap, s);
+  ci.conf.grow_keep(cap, s);
+  if (m > 0) {
+    WFK_CUDA(cudaMemcpyAsync(ci.kind.p + base, kind.data(), size_t(m) * 4, cudaMemcpyHostToDevice, s));
+    WFK_CUDA(cudaMemcpyAsync(ci.canonical.p + 3 * base, can.data(), size_t(m) * 24, cudaMemcpyHostToDevice, s));
+    WFK_CUDA(cudaMemcpyAsync(ci.anchor.p + 8 * base, anchor.data(), size_t(m) * 32, cudaMemcpyHostToDevice, s));
+    WFK_CUDA(cudaMemcpyAsync(ci.weight.p + 8 * base, w.data(), size_t(m) * 64, cudaMemcpyHostToDevice, s));
+    WFK_CUDA(cudaMemcpyAsync(ci.target.p + 3 * base, tgt.data(), size_t(m) * 24, cudaMemcpyHostToDevice, s));
+    WFK_CUDA(cudaMemcpyAsync(ci.normal.p + 3 * base, nrm.data(), size_t(m) * 24, cudaMemcpyHostToDevice, s));
+    WFK_CUDA(cudaMemcpyAsync(ci.conf.p + base, conf.data(), size_t(m) * 8, cudaMemcpyHostToDevice, s));
+  }
+  WFK_CUDA(cudaStreamSynchronize(s));  // host staging vectors die on return
+  ci.count = total;
+}
+
+}  // namespace
+
+extern "C" {
+
+int wfk_version(void) { return 1; }
+
+int wfk_create(const wfk_config* cfg, wfk_ctx** out) {
+  if (!out) return WFK_E_INVALID_ARG;
+  *out = nullptr;
+  auto* c = new wfk_ctx;
+  c->device = cfg ? cfg->device : 0;
+  try {
+    int n = 0;
+    WFK_CUDA(cudaGetDeviceCount(&n));
+    if (c->device < 0 || c->device >= n) throw Error(WFK_E_INVALID_ARG, "no such CUDA device");
+    WFK_CUDA(cudaSetDevice(c->device));
+    cudaDeviceProp prop;
+    WFK_CUDA(cudaGetDeviceProperties(&prop, c->device));
+    if (prop.major < 10) throw Error(WFK_E_CUDA, "libwfk is built for sm_100a (B200)");
+    c->num_sms = prop.multiProcessorCount;
+    WFK_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    WFK_CUDA(cudaMallocHost(&c->h_pinned, 4096));
+  } catch (const Error& e) {
+    delete c;
+    return e.code;
+  }
+  *out = c;
+  return WFK_OK;
+}
+
+void wfk_destroy(wfk_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->h_pinned) cudaFreeHost(c->h_pinned);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* wfk_last_error(const wfk_ctx* c) { return c ? c->err.c_str() : "null context"; }
+int64_t wfk_launch_count(const wfk_ctx* c) { return c ? c->stats.kernel_launches : 0; }
+int64_t wfk_pcg_iteration_count(const wfk_ctx* c) { return c ? c->stats.pcg_iterations : 0; }
+
+int wfk_volume_upload(wfk_ctx* c, const wfk_volume_view* v, uint32_t fields) {
+  return guard(c, [&] {
+    if (!v) throw Error(WFK_E_INVALID_ARG, "null volume");
+    if (v->dims[0] < 2 || v->dims[1] < 2 || v->dims[2] < 2)
+      throw Error(WFK_E_INVALID_ARG, "DeformableVolume: each dim must be >= 2");
+    if (!(v->voxel_size > 0)) throw Error(WFK_E_INVALID_ARG, "DeformableVolume: voxel_size must be > 0");
+    VolumeDev& d = c->vol;
+    const Grid g{v->dims[0], v->dims[1], v->dims[2], v->voxel_size, v->origin[0], v->origin[1], v->origin[2]};
+    const int64_t n = g.n();
+    if (n >= (int64_t(1) << 31)) throw Error(WFK_E_INVALID_ARG, "lattice too large for 32-bit indices");
+    const bool realloc = !d.valid || d.n != n;
+    if (realloc) fields = WFK_VOL_ALL;
+    d.g = g;
+    d.n = n;
+    d.mu = v->truncation;
+    d.tsdf.ensure(size_t(n));
+    d.weight.ensure(size_t(n));
+    d.color.ensure(3 * size_t(n));
+    d.deformed.ensure(3 * size_t(n));
+    d.euler.ensure(3 * size_t(n));
+    d.age.ensure(size_t(n));
+    d.active.ensure(size_t(n));
+    cudaStream_t s = c->stream;
+    auto up = [&](uint32_t bit, void* dst, const void* src, size_t bytes) {
+      if (!(fields & bit)) return;
+      if (!src) throw Error(WFK_E_INVALID_ARG, "volume field pointer is null");
+      WFK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    };
+    up(WFK_VOL_TSDF, d.tsdf, v->tsdf, size_t(n) * 4);
+    up(WFK_VOL_WEIGHT, d.weight, v->weight, size_t(n) * 4);
+    up(WFK_VOL_COLOR, d.color, v->color, size_t(n) * 12);
+    up(WFK_VOL_DEFORMED, d.deformed, v->deformed, size_t(n) * 24);
+    up(WFK_VOL_EULER, d.euler, v->euler, size_t(n) * 24);
+    up(WFK_VOL_AGE, d.age, v->age, size_t(n) * 4);
+    up(WFK_VOL_ACTIVE, d.active, v->active, size_t(n));
+    WFK_CUDA(cudaStreamSynchronize(s));
+    d.valid = true;
+  });
+}
+
+int wfk_volume_download(wfk_ctx* c, wfk_volume_view* v, uint32_t fields) {
+  return guard(c, [&] {
+    VolumeDev& d = c->vol;
+    if (!d.valid) throw Error(WFK_E_INVALID_ARG, "no volume uploaded");
+    if (!v || int64_t(v->dims[0]) * v->dims[1] * v->dims[2] != d.n)
+      throw Error(WFK_E_INVALID_ARG, "volume view does not match the device lattice");
+    cudaStream_t s = c->stream;
+    auto down = [&](uint32_t bit, void* dst, const void* src, size_t bytes) {
+      if (!(fields & bit) || !dst) return;
+      WFK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+    };
+    const size_t n = size_t(d.n);
+    down(WFK_VOL_TSDF, v->tsdf, d.tsdf, n * 4);
+    down(WFK_VOL_WEIGHT, v->weight, d.weight, n * 4);
+    down(WFK_VOL_COLOR, v->color, d.color, n * 12);
+    down(WFK_VOL_DEFORMED, v->deformed, d.deformed, n * 24);
+    down(WFK_VOL_EULER, v->euler, d.euler, n * 24);
+    down(WFK_VOL_AGE, v->age, d.age, n * 4);
+    down(WFK_VOL_ACTIVE, v->active, d.active, n);
+    WFK_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int wfk_compute_active_set(wfk_ctx* c, int32_t* out, int64_t cap, int64_t* n_out) {
+  return guard(c, [&] { fusion_compute_active_set(c, out, cap, n_out); });
+}
+
+int wfk_constraints_upload(wfk_ctx* c, const wfk_correspondence* h, int64_t n) {
+  return guard(c, [&] {
+    if (!c->vol.valid) throw Error(WFK_E_INVALID_ARG, "upload the volume before its constraints");
+    upload_constraints(c, h, n, false, false, nullptr);
+  });
+}
+
+int wfk_constraints_append(wfk_ctx* c, const wfk_correspondence* h, int64_t n, int32_t drop_inactive, int64_t* kept) {
+  return guard(c, [&] {
+    if (!c->vol.valid) throw Error(WFK_E_INVALID_ARG, "upload the volume before its constraints");
+    upload_constraints(c, h, n, true, drop_inactive != 0, kept);
+  });
+}
+
+int wfk_constraints_download(wfk_ctx* c, wfk_correspondence* out, int64_t cap, int64_t* n_out) {
+  return guard(c, [&] {
+    ConIn& ci = c->cons;
+    const int64_t n = ci.count;
+    if (n_out) *n_out = n;
+    if (!out) return;
+    if (n > cap) throw Error(WFK_E_CAPACITY, "constraint buffer too small");
+    if (n == 0) return;
+    cudaStream_t s = c->stream;
+    const size_t nn = static_cast<size_t>(n);
+    std::vector<int32_t> kind(nn), anchor(8 * nn);
+    std::vector<double> can(3 * nn), w(8 * nn), tgt(3 * nn), nrm(3 * nn), conf(nn);
+    WFK_CUDA(cudaMemcpyAsync(kind.data(), ci.kind, size_t(n) * 4, cudaMemcpyDeviceToHost, s));
+    WFK_CUDA(cudaMemcpyAsync(anchor.data(), ci.anchor, size_t(n) * 32, cudaMemcpyDeviceToHost, s));
+    WFK_CUDA(cudaMemcpyAsync(can.data(), ci.canonical, size_t(n) * 24, cudaMemcpyDeviceToHost, s));
+    WFK_CUDA(cudaMemcpyAsync(w.data(), ci.weight, size_t(n) * 64, cudaMemcpyDeviceToHost, s));
+    WFK_CUDA(cudaMemcpyAsync(tgt.data(), ci.target, size_t(n) * 24, cudaMemcpyDeviceToHost, s));
+    WFK_CUDA(cudaMemcpyAsync(nrm.data(), ci.normal, size_t(n) * 24, cudaMemcpyDeviceToHost, s));
+    WFK_CUDA(cudaMemcpyAsync(conf.data(), ci.conf, size_t(n) * 8, cudaMemcpyDeviceToHost, s));
+    WFK_CUDA(cudaStreamSynchronize(s));
+    for (int64_t i = 0; i < n; ++i) {
+      wfk_correspondence& r = out[i];
+      std::memset(&r, 0, sizeof(r));
+      r.kind = kind[size_t(i)];
+      for (int k = 0; k < 3; ++k) {
+        r.canonical[k] = can[size_t(3 * i + k)];
+        r.target[k] = tgt[size_t(3 * i + k)];
+        r.target_normal[k] = nrm[size_t(3 * i + k)];
+      }
+      for (int k = 0; k < 8; ++k) {
+        r.anchor_index[k] = anchor[size_t(8 * i + k)];
+        r.anchor_weight[k] = w[size_t(8 * i + k)];
+      }
+      r.confidence = conf[size_t(i)];
+    }
+  });
+}
+
+int wfk_evaluate_energy(wfk_ctx* c, const wfk_pose* pose, const wfk_solver_params* p, wfk_energy* out) {
+  return guard(c, [&] {
+    check_params(p);
+    wfk_energy e{};
+    solver_energy(c, pose, *p, &e);
+    if (out) *out = e;
+  });
+}
+
+int wfk_update_rotations(wfk_ctx* c, int32_t) {
+  return guard(c, [&] { solver_rotations(c); });
+}
+
+int wfk_flip_flop_solve(wfk_ctx* c, const wfk_pose* pose, const wfk_solver_params* p, int32_t level,
+                        wfk_trace_entry* trace, int32_t cap, int32_t* n_out) {
+  std::vector<wfk_trace_entry> t;
+  const int rc = guard(c, [&] {
+    check_params(p);
+    solver_flip_flop(c, pose, *p, level, t);
+  });
+  if (rc != WFK_OK) return rc;
+  return export_trace(c, t, trace, cap, n_out);
+}
+
+int wfk_solve_coarse_to_fine(wfk_ctx* c, const wfk_pose* pose, const wfk_solver_params* p, wfk_trace_entry* trace,
+                             int32_t cap, int32_t* n_out) {
+  std::vector<wfk_trace_entry> t;
+  const int rc = guard(c, [&] {
+    check_params(p);
+    solver_c2f(c, pose, *p, t);
+  });
+  if (rc != WFK_OK) return rc;
+  return export_trace(c, t, trace, cap, n_out);
+}
+
+int wfk_build_normal_equations(wfk_ctx* c, const wfk_pose* pose, const wfk_solver_params* p, wfk_ne_host* out,
+                               int32_t* rows_out) {
+  return guard(c, [&] {
+    check_params(p);
+    const int n = solver_build_ne(c, pose, *p, out);
+    if (rows_out) *rows_out = n;
+  });
+}
+
+int wfk_pcg_solve(wfk_ctx* c, int32_t rows, const double* blocks, const int32_t* cols, const double* rhs, double* x,
+                  double tol, int32_t max_iters, int32_t, wfk_pcg_result* out) {
+  return guard(c, [&] {
+    if (rows < 0 || (rows > 0 && (!blocks || !cols || !rhs || !x))) throw Error(WFK_E_INVALID_ARG, "bad system");
+    solver_pcg_assembled(c, rows, blocks, cols, rhs, x, tol, max_iters, 0, out, nullptr);
+  });
+}
+
+int wfk_ne_multiply(wfk_ctx* c, int32_t rows, const double* blocks, const int32_t* cols, const double* x, double* y) {
+  return guard(c, [&] {
+    if (rows < 0 || (rows > 0 && (!blocks || !cols || !x || !y))) throw Error(WFK_E_INVALID_ARG, "bad system");
+    std::vector<double> xc(x, x + 3 * size_t(rows));
+    solver_pcg_assembled(c, rows, blocks, cols, nullptr, xc.data(), 0, 0, 1, nullptr, y);
+  });
+}
+
+int wfk_hierarchy_info(wfk_ctx* c, int32_t levels, int32_t* dims_out, int64_t* active_out) {
+  return guard(c, [&] { solver_hierarchy_info(c, levels, dims_out, active_out); });
+}
+
+int wfk_frame_upload(wfk_ctx* c, const wfk_frame_view* f) {
+  return guard(c, [&] {
+    if (!f || !f->depth) throw Error(WFK_E_INVALID_ARG, "null frame");
+    const wfk_intrinsics& K = f->intrinsics;
+    if (!(K.fx > 0 && K.fy > 0 && K.width > 0 && K.height > 0))
+      throw Error(WFK_E_INVALID_ARG, "frame has invalid intrinsics");
+    FrameDev& d = c->frame;
+    const size_t npx = size_t(K.width) * size_t(K.height);
+    d.K = K;
+    d.depth.ensure(npx);
+    WFK_CUDA(cudaMemcpyAsync(d.depth, f->depth, npx * 4, cudaMemcpyHostToDevice, c->stream));
+    d.has_color = f->color != nullptr;
+    if (d.has_color) {
+      d.color.ensure(3 * npx);
+      WFK_CUDA(cudaMemcpyAsync(d.color, f->color, 3 * npx * 4, cudaMemcpyHostToDevice, c->stream));
+    }
+    d.maps_valid = false;
+    WFK_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int wfk_integrate_frame(wfk_ctx* c, const wfk_pose* pose, const wfk_fusion_params* p, int32_t, wfk_fusion_stats* out) {
+  return guard(c, [&] {
+    if (!p) throw Error(WFK_E_INVALID_ARG, "null fusion params");
+    fusion_integrate(c, pose, *p, out);
+  });
+}
+
+int wfk_expand_grid(wfk_ctx* c, wfk_expansion_stats* out) {
+  return guard(c, [&] { fusion_expand(c, out); });
+}
+
+int wfk_advance_ages(wfk_ctx* c, const int32_t* idx, int64_t n) {
+  return guard(c, [&] {
+    for (int64_t k = 0; k < n; ++k)
+      if (idx[k] < 0 || idx[k] >= c->vol.n) throw Error(WFK_E_OUT_OF_RANGE, "advance_ages: index outside the lattice");
+    fusion_advance_ages(c, idx, n);
+  });
+}
+
+int wfk_advance_active_ages(wfk_ctx* c) {
+  return guard(c, [&] { fusion_advance_active_ages(c); });
+}
+
+int wfk_backproject_depth(wfk_ctx* c, int32_t, wfk_point_normal_map* out) {
+  return guard(c, [&] { assoc_backproject(c, out); });
+}
+
+int wfk_extract_mesh(wfk_ctx* c, const wfk_pose* pose, int64_t* nv, int64_t* nt) {
+  return guard(c, [&] { assoc_extract_mesh(c, pose, nv, nt); });
+}
+
+int wfk_mesh_warp(wfk_ctx* c, const wfk_pose* pose) {
+  return guard(c, [&] { assoc_mesh_warp(c, pose); });
+}
+
+int wfk_compute_normals(wfk_ctx* c) {
+  return guard(c, [&] { assoc_compute_normals(c); });
+}
+
+int wfk_mesh_upload(wfk_ctx* c, const wfk_mesh_view* m) {
+  return guard(c, [&] {
+    if (!m || m->num_vertices < 0 || m->num_triangles < 0) throw Error(WFK_E_INVALID_ARG, "bad mesh");
+    MeshDev& d = c->mesh;
+    const size_t V = size_t(m->num_vertices), T = size_t(m->num_triangles);
+    for (size_t t = 0; t < 3 * T; ++t)
+      if (m->triangles[t] < 0 || size_t(m->triangles[t]) >= V) throw Error(WFK_E_OUT_OF_RANGE, "triangle index");
+    cudaStream_t s = c->stream;
+    d.can.ensure(3 * V + 3);
+    d.def.ensure(3 * V + 3);
+    d.nrm.ensure(3 * V + 3);
+    d.col.ensure(3 * V + 3);
+    d.tri.ensure(3 * T + 3);
+    if (V) {
+      WFK_CUDA(cudaMemcpyAsync(d.can, m->vertices_canonical, 24 * V, cudaMemcpyHostToDevice, s));
+      WFK_CUDA(cudaMemcpyAsync(d.def, m->vertices_deformed, 24 * V, cudaMemcpyHostToDevice, s));
+      if (m->colors) WFK_CUDA(cudaMemcpyAsync(d.col, m->colors, 12 * V, cudaMemcpyHostToDevice, s));
+      if (m->normals_deformed) WFK_CUDA(cudaMemcpyAsync(d.nrm, m->normals_deformed, 24 * V, cudaMemcpyHostToDevice, s));
+    }
+    if (T) WFK_CUDA(cudaMemcpyAsync(d.tri, m->triangles, 12 * T, cudaMemcpyHostToDevice, s));
+    WFK_CUDA(cudaStreamSynchronize(s));
+    d.V = int64_t(V);
+    d.T = int64_t(T);
+    d.normals_valid = m->normals_deformed != nullptr;
+    d.adj_valid = false;
+  });
+}
+
+int wfk_mesh_download(wfk_ctx* c, wfk_mesh_view* m) {
+  return guard(c, [&] {
+    MeshDev& d = c->mesh;
+    if (!m) throw Error(WFK_E_INVALID_ARG, "null mesh view");
+    const bool sizes_only = !m->vertices_canonical && !m->vertices_deformed && !m->triangles && !m->colors &&
+                            !m->normals_deformed;
+    if (!sizes_only && (m->num_vertices < d.V || m->num_triangles < d.T))
+      throw Error(WFK_E_CAPACITY, "mesh view too small");
+    m->num_vertices = d.V;
+    m->num_triangles = d.T;
+    if (sizes_only) return;
+    cudaStream_t s = c->stream;
+    const size_t V = size_t(d.V), T = size_t(d.T);
+    if (V && m->vertices_canonical) WFK_CUDA(cudaMemcpyAsync(m->vertices_canonical, d.can, 24 * V, cudaMemcpyDeviceToHost, s));
+    if (V && m->vertices_deformed) WFK_CUDA(cudaMemcpyAsync(m->vertices_deformed, d.def, 24 * V, cudaMemcpyDeviceToHost, s));
+    if (V && m->normals_deformed && d.normals_valid)
+      WFK_CUDA(cudaMemcpyAsync(m->normals_deformed, d.nrm, 24 * V, cudaMemcpyDeviceToHost, s));
+    if (V && m->colors) WFK_CUDA(cudaMemcpyAsync(m->colors, d.col, 12 * V, cudaMemcpyDeviceToHost, s));
+    if (T && m->triangles) WFK_CUDA(cudaMemcpyAsync(m->triangles, d.tri, 12 * T, cudaMemcpyDeviceToHost, s));
+    WFK_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int wfk_rasterize(wfk_ctx* c, const wfk_intrinsics* intr, int32_t, wfk_geometry_buffer* out) {
+  return guard(c, [&] {
+    if (!intr) throw Error(WFK_E_INVALID_ARG, "null intrinsics");
+    assoc_rasterize(c, *intr, out);
+  });
+}
+
+int wfk_gbuffer_upload(wfk_ctx* c, const wfk_geometry_buffer* b) {
+  return guard(c, [&] {
+    if (!b || b->width <= 0 || b->height <= 0) throw Error(WFK_E_INVALID_ARG, "bad geometry buffer");
+    GBufDev& d = c->gbuf;
+    const size_t npx = size_t(b->width) * size_t(b->height);
+    d.w = b->width;
+    d.h = b->height;
+    d.depth.ensure(npx);
+    d.point.ensure(3 * npx);
+    d.normal.ensure(3 * npx);
+    d.canonical.ensure(3 * npx);
+    cudaStream_t s = c->stream;
+    WFK_CUDA(cudaMemcpyAsync(d.depth, b->depth, npx * 4, cudaMemcpyHostToDevice, s));
+    WFK_CUDA(cudaMemcpyAsync(d.point, b->point, npx * 24, cudaMemcpyHostToDevice, s));
+    WFK_CUDA(cudaMemcpyAsync(d.normal, b->normal, npx * 24, cudaMemcpyHostToDevice, s));
+    WFK_CUDA(cudaMemcpyAsync(d.canonical, b->canonical, npx * 24, cudaMemcpyHostToDevice, s));
+    WFK_CUDA(cudaStreamSynchronize(s));
+    d.valid = true;
+  });
+}
+
+int wfk_find_dense_correspondences(wfk_ctx* c, const wfk_intrinsics* intr, const wfk_correspond_params* p,
+                                   int32_t drop_inactive, int64_t* n_out) {
+  return guard(c, [&] {
+    if (!intr || !p) throw Error(WFK_E_INVALID_ARG, "null argument");
+    if (!c->vol.valid) throw Error(WFK_E_INVALID_ARG, "no volume uploaded");
+    assoc_find_dense(c, *intr, *p, drop_inactive != 0, n_out);
+  });
+}
+
+// Reconstructor::process_frame (pipeline.cpp:143-262) without ICP/features
+int wfk_process_frame(wfk_ctx* c, const wfk_frame_view* frame, const wfk_pose* pose, const wfk_pipeline_config* cfg,
+                      const wfk_correspondence* sparse, int64_t nsparse, int32_t frame_index, wfk_frame_record* rec) {
+  const int rc0 = wfk_frame_upload(c, frame);
+  if (rc0 != WFK_OK) return rc0;
+  return guard(c, [&] {
+    if (!cfg || !rec) throw Error(WFK_E_INVALID_ARG, "null argument");
+    if (!c->vol.valid) throw Error(WFK_E_INVALID_ARG, "no volume uploaded");
+    std::memset(rec, 0, sizeof(*rec));
+    const wfk_intrinsics& K = frame->intrinsics;
+    assoc_backproject(c, nullptr);
+    if (frame_index == 0) {  // pipeline.cpp:150-159
+      wfk_fusion_params boot = cfg->fusion;
+      boot.bootstrap = 1;
+      fusion_integrate(c, pose, boot, &rec->fusion);
+      fusion_compute_active_set(c, nullptr, 0, nullptr);
+      rec->bootstrap = 1;
+      return;
+    }
+    int64_t nv = 0, nt = 0;
+    assoc_extract_mesh(c, pose, &nv, &nt);
+    if (nt == 0) throw Error(WFK_E_LOGIC, "empty isosurface before frame");
+    assoc_compute_normals(c);
+    assoc_rasterize(c, K, nullptr);
+    std::vector<wfk_trace_entry> trace;
+    for (int outer = 0; outer < cfg->reassociations; ++outer) {  // pipeline.cpp:226-247
+      int64_t nd = 0;
+      assoc_find_dense(c, K, cfg->correspond, true, &nd);
+      rec->dense_count = int32_t(nd);
+      int64_t kept = 0;
+      if (nsparse > 0) upload_constraints(c, sparse, nsparse, true, true, &kept);
+      rec->sparse_count = int32_t(kept);
+      if (c->cons.count == 0) break;
+      trace.clear();
+      solver_c2f(c, pose, cfg->solver, trace);
+      for (const wfk_trace_entry& e : trace) {
+        rec->anomalies += e.anomaly ? 1 : 0;
+        rec->pcg_iterations += e.pcg_iterations;
+        ++rec->trace_len;
+      }
+      if (!trace.empty()) rec->energy = trace.back().energy;
+      assoc_mesh_warp(c, pose);  // redeform (pipeline.cpp:167-172)
+      assoc_compute_normals(c);
+      assoc_rasterize(c, K, nullptr);
+    }
+    fusion_advance_active_ages(c);                      // pipeline.cpp:249-252
+    fusion_integrate(c, pose, cfg->fusion, &rec->fusion);  // :254
+    fusion_expand(c, &rec->expansion);                  // :255
+  });
+}
+
+int wfk_synth_render(wfk_ctx* c, const wfk_synth_scene* s, const wfk_intrinsics* intr, float* depth, float* color) {
+  return guard(c, [&] {
+    if (!s || !intr || !depth) throw Error(WFK_E_INVALID_ARG, "null argument");
+    synth_render(c, *s, *intr, depth, color);
+  });
+}
+
+}  // extern "C"

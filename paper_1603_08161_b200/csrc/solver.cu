@@ -1,0 +1,1262 @@
+// Non-rigid alignment solver on sm_100a: the reference's flip-flop
+// position-PCG / Procrustes loop over the deformation lattice, coarse to fine
+// (proj/src/solver.cpp:32-534), as
+//
+//   * per-level setup kernels: active-row compaction (ascending lattice order,
+//     solver.cpp:115-119), 6-neighbour row table, lock-free union-find for the
+//     frozen components (solver.cpp:124-144), constraint preparation and a
+//     row-major transpose of the constraint->anchor incidence built with a
+//     stable radix sort, so each row gathers its data term without atomics
+//     in exactly the reference's accumulation order (solver.cpp:185-195);
+//   * ONE cooperative persistent kernel per flip_flop_solve (solver.cpp:419-453)
+//     that runs energy, rhs/diagonal assembly, the Jacobi-PCG loop, write-back,
+//     the Procrustes rotation fit and the energy trace with grid-wide barriers
+//     instead of kernel launches.  The PCG operator is matrix-free: per
+//     iteration one pass over the constraints (q_c = sum_k a_k p[a_k],
+//     u_c = coef (g.q_c) g) and one pass over rows (sum of a_i u_c over the
+//     row's incidence list + the 6-neighbour ARAP Laplacian), replacing the
+//     27 x 3x3 fp64 block rows the reference stores (2,081 B per row).
+//     Dot products are deterministic two-level reductions (warp shuffle ->
+//     per-block partial -> fixed-order sum).
+#include <cooperative_groups.h>
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
+
+#include "wfk_context.cuh"
+#include "wfk_solver.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace wfk {
+
+// ============================================================================
+// setup kernels
+// ============================================================================
+
+__global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void k_scatter_node_row(const int32_t* rows, int N, int32_t* node_row) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x) node_row[rows[r]] = r;
+}
+
+// 6 face neighbours per row in the reference's kFaceNeighbors order
+// (solver.cpp:17-18); -1 when outside the grid or inactive.
+__global__ void k_row_neighbours(Grid g, const int32_t* rows, int N, const int32_t* node_row, int32_t* nbr,
+                                 int32_t* uf) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x) {
+    int x, y, z;
+    g.idx3(rows[r], x, y, z);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      const int a = x + kFace[k][0], b = y + kFace[k][1], c = z + kFace[k][2];
+      nbr[int64_t(k) * N + r] = g.in_grid(a, b, c) ? node_row[g.lin(a, b, c)] : -1;
+    }
+    uf[r] = r;
+  }
+}
+
+// lock-free union-find; a set's root is always its smallest row, so the final
+// partition and labels are independent of the race order.
+__device__ int uf_find(volatile int32_t* uf, int a) {
+  int p = uf[a];
+  while (p != a) {
+    a = p;
+    p = uf[a];
+  }
+  return a;
+}
+__global__ void k_union(const int32_t* nbr, int N, int32_t* uf) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < 6; k += 2) {  // +x, +y, +z edges cover every edge once
+      const int j = nbr[int64_t(k) * N + r];
+      if (j < 0) continue;
+      int a = r, b = j;
+      while (true) {
+        a = uf_find(uf, a);
+        b = uf_find(uf, b);
+        if (a == b) break;
+        if (a < b) {
+          int t = a;
+          a = b;
+          b = t;
+        }
+        const int old = atomicCAS(&uf[a], a, b);
+        if (old == a) break;
+        a = old;
+      }
+    }
+  }
+}
+__global__ void k_uf_compress(int N, int32_t* uf, uint8_t* comp_flag) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x) {
+    uf[r] = uf_find(uf, r);
+    comp_flag[r] = 0;
+  }
+}
+
+// Per-constraint preparation at one level: anchor rows, g = R^T n and the
+// constant of the rhs (solver.cpp:203-226), constrained-component marks
+// (solver.cpp:136-141) and the incidence keys of the row transpose.
+__global__ void k_con_prepare(int64_t C, const int32_t* kind, const double* target, const double* normal,
+                              const double* conf, const int32_t* c_node, const double* c_w,
+                              const int32_t* node_row, const int32_t* uf, PoseD pose, double w_d, double w_s,
+                              int N, int32_t* c_row, double* c_g, double* c_b, int32_t* c_kind,
+                              uint8_t* comp_flag, int32_t* key, int32_t* val, int32_t* cnt, int32_t* n_ent) {
+  const M3 rt = transpose(pose.r);
+  for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < C; c += int64_t(gridDim.x) * blockDim.x) {
+    const bool dense = kind[c] == WFK_DENSE_PLANE;
+    c_kind[c] = kind[c];
+    const V3 n = ld3(normal, c), f = ld3(target, c);
+    if (dense) {
+      const V3 g = mul(rt, n);
+      c_g[4 * c] = g.x;
+      c_g[4 * c + 1] = g.y;
+      c_g[4 * c + 2] = g.z;
+      c_g[4 * c + 3] = w_d * conf[c];
+      c_b[c] = dot(n, pose.t - f);
+    } else {
+      const V3 v = mul(rt, f - pose.t);
+      c_g[4 * c] = v.x;
+      c_g[4 * c + 1] = v.y;
+      c_g[4 * c + 2] = v.z;
+      c_g[4 * c + 3] = w_s * conf[c];
+      c_b[c] = 0.0;
+    }
+    int local = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int row = node_row[c_node[8 * c + k]];
+      const double w = c_w[8 * c + k];
+      c_row[8 * c + k] = row;
+      if (row >= 0 && w > 0) comp_flag[uf[row]] = 1;
+      // incidence entry unless alpha_i == 0 (solver.cpp:202)
+      if (row >= 0 && w != 0) {
+        key[8 * c + k] = row * 8 + (7 - k);  // cell order of solver.cpp:185-187
+        val[8 * c + k] = int32_t(8 * c + k);
+        atomicAdd(&cnt[row], 1);
+        ++local;
+      } else {
+        key[8 * c + k] = N * 8;  // sentinel, sorts last
+        val[8 * c + k] = int32_t(8 * c + k);
+      }
+    }
+    if (local) atomicAdd(n_ent, local);
+  }
+}
+
+__global__ void k_frozen(int N, const int32_t* uf, const uint8_t* comp_flag, uint8_t* frozen) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x)
+    frozen[r] = comp_flag[uf[r]] ? 0 : 1;
+}
+
+__global__ void k_entries(int64_t E, const int32_t* sorted_val, const double* c_w, int32_t* ent_con,
+                          double* ent_w) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < E; e += int64_t(gridDim.x) * blockDim.x) {
+    const int v = sorted_val[e];
+    ent_con[e] = v >> 3;
+    ent_w[e] = c_w[v];
+  }
+}
+
+// ConstraintCache (solver.hpp:66-70): constraint part of the rhs and of the
+// Jacobi diagonal, accumulated in the reference's order (solver.cpp:196-226).
+__global__ void k_constraint_cache(int N, const int32_t* row_ptr, const int32_t* ent_con, const double* ent_w,
+                                   const int32_t* c_kind, const double* c_g, const double* c_b, double* crhs,
+                                   double* cdiag) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x) {
+    V3 rhs{0, 0, 0}, diag{0, 0, 0};
+    for (int e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
+      const int c = ent_con[e];
+      const double a = ent_w[e];
+      const V3 g{c_g[4 * c], c_g[4 * c + 1], c_g[4 * c + 2]};
+      const double coef = c_g[4 * c + 3];
+      const double s = coef * a * a;
+      if (c_kind[c] == WFK_DENSE_PLANE) {
+        diag.x += s * (g.x * g.x);
+        diag.y += s * (g.y * g.y);
+        diag.z += s * (g.z * g.z);
+        rhs -= (coef * a * c_b[c]) * g;
+      } else {
+        diag.x += s * 1.0;
+        diag.y += s * 1.0;
+        diag.z += s * 1.0;
+        rhs += (coef * a) * g;
+      }
+    }
+    st3(crhs, r, rhs);
+    st3(cdiag, r, diag);
+  }
+}
+
+// ============================================================================
+// hierarchy (solver.cpp:455-534)
+// ============================================================================
+
+// coarse field from the fine one (solver.cpp:470-483), every coarse point
+__global__ void k_coarse_init(Grid fine, Grid coarse, const double* f_def, const double* f_eul, double* c_def,
+                              double* c_eul, uint8_t* c_act) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < coarse.n();
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const V3 xc = coarse.canonical(int(i));
+    V3 xq = xc;
+    double q[3] = {xq.x, xq.y, xq.z};
+    for (int k = 0; k < 3; ++k) q[k] = clampd(q[k], fine.org(k), fine.org(k) + fine.voxel * (fine.dim(k) - 1));
+    xq = V3{q[0], q[1], q[2]};
+    st3(c_def, i, fine.interpolate(f_def, xq) + (xc - xq));
+    int nearest[3];
+    for (int k = 0; k < 3; ++k)
+      nearest[k] = clampi(int(llround((q[k] - fine.org(k)) / fine.voxel)), 0, fine.dim(k) - 1);
+    st3(c_eul, i, ld3(f_eul, fine.lin(nearest[0], nearest[1], nearest[2])));
+    c_act[i] = 0;
+  }
+}
+
+// coarse activity: all 8 coarse anchors of every active fine node (solver.cpp:485-490)
+__global__ void k_coarse_activity(Grid fine, Grid coarse, const uint8_t* f_act, uint8_t* c_act, int32_t* err) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < fine.n(); i += int64_t(gridDim.x) * blockDim.x) {
+    if (!f_act[i]) continue;
+    const V3 x = fine.canonical(int(i));
+    if (!coarse.contains(x)) {
+      atomicOr(err, 2);
+      continue;
+    }
+    int idx[8];
+    double w[8];
+    coarse.anchors(x, idx, w);
+    for (int k = 0; k < 8; ++k) c_act[idx[k]] = 1;
+  }
+}
+
+// re-anchor every constraint on a coarse lattice (solver.cpp:492-499)
+__global__ void k_reanchor(int64_t C, Grid coarse, const double* canonical, int32_t* c_node, double* c_w,
+                           uint8_t* c_act, int32_t* err) {
+  for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < C; c += int64_t(gridDim.x) * blockDim.x) {
+    const V3 x = ld3(canonical, c);
+    if (!coarse.contains(x)) {
+      atomicOr(err, 2);
+      for (int k = 0; k < 8; ++k) {
+        c_node[8 * c + k] = 0;
+        c_w[8 * c + k] = 0;
+      }
+      continue;
+    }
+    int idx[8];
+    double w[8];
+    coarse.anchors(x, idx, w);
+    for (int k = 0; k < 8; ++k) {
+      c_node[8 * c + k] = idx[k];
+      c_w[8 * c + k] = w[k];
+      if (w[k] > 0) c_act[idx[k]] = 1;
+    }
+  }
+}
+
+// prolongation coarse -> fine over active fine nodes (solver.cpp:518-529)
+__global__ void k_prolong(Grid fine, Grid coarse, const uint8_t* f_act, double* f_def, double* f_eul,
+                          const double* c_def, const double* c_eul) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < fine.n(); i += int64_t(gridDim.x) * blockDim.x) {
+    if (!f_act[i]) continue;
+    const V3 x = fine.canonical(int(i));
+    st3(f_def, i, coarse.interpolate(c_def, x));
+    const double q[3] = {x.x, x.y, x.z};
+    int nearest[3];
+    for (int k = 0; k < 3; ++k)
+      nearest[k] = clampi(int(llround((q[k] - coarse.org(k)) / coarse.voxel)), 0, coarse.dim(k) - 1);
+    st3(f_eul, i, ld3(c_eul, coarse.lin(nearest[0], nearest[1], nearest[2])));
+  }
+}
+
+// ============================================================================
+// the cooperative flip-flop kernel
+// ============================================================================
+
+struct FFArgs {
+  Grid g;
+  int N;
+  int64_t C;
+  int mode;  // 0 = flip-flop, 1 = energy only, 2 = rotations only
+  int level;
+  // params
+  double w_d, w_s, w_r, ff_rel_tol, pcg_tol;
+  int ff_iters, pcg_max;
+  PoseD pose;
+  // rows
+  const int32_t* rows;
+  const int32_t* nbr;
+  const uint8_t* frozen;
+  // field (node indexed)
+  double* field_def;
+  double* field_eul;
+  // row state
+  double *t, *x, *rhs, *r, *p, *ap, *dinv, *rot;
+  const double *crhs, *cdiag;
+  // constraints
+  const int32_t* c_row;
+  const double* c_w;
+  const double* c_g;
+  const int32_t* c_kind;
+  const double* target;
+  const double* normal;
+  const double* conf;
+  double* c_u;
+  const int32_t* row_ptr;
+  const int32_t* ent_con;
+  const double* ent_w;
+  // outputs
+  double* partials;  // 2 regions x 4 slots x gridDim
+  wfk_trace_entry* trace;
+  int32_t* status;   // [0] trace length, [1] error bits, [2] total pcg iterations
+  double* energy_out;
+};
+
+struct Red {
+  // rotating partial regions: see the note on double buffering in k_flip_flop
+  int region = 0;
+};
+
+template <int NV>
+__device__ void grid_reduce(const FFArgs& a, cg::grid_group& grid, Red& rs, double (&v)[NV]) {
+  __shared__ double smem[4 * 32];
+  block_sum<NV>(v, smem);
+  double* base = a.partials + size_t(rs.region) * 4 * gridDim.x;
+  if (threadIdx.x == 0)
+    for (int k = 0; k < NV; ++k) base[size_t(k) * gridDim.x + blockIdx.x] = v[k];
+  grid.sync();
+  for (int k = 0; k < NV; ++k) v[k] = sum_partials(base + size_t(k) * gridDim.x, gridDim.x);
+  rs.region ^= 1;
+}
+
+__device__ __forceinline__ int64_t gtid() { return blockIdx.x * int64_t(blockDim.x) + threadIdx.x; }
+__device__ __forceinline__ int64_t gstride() { return int64_t(gridDim.x) * blockDim.x; }
+
+// E_sparse, E_dense, E_reg partials (solver.cpp:345-383)
+__device__ void energy_partials(const FFArgs& a, double& es, double& ed, double& er, int& bad) {
+  es = ed = er = 0;
+  for (int64_t c = gtid(); c < a.C; c += gstride()) {
+    V3 q{0, 0, 0};
+    for (int k = 0; k < 8; ++k) {
+      const double w = a.c_w[8 * c + k];
+      const int row = a.c_row[8 * c + k];
+      if (w > 0 && row < 0) bad = 1;
+      if (w != 0 && row >= 0) q += w * ld3(a.t, row);
+    }
+    const V3 s = a.pose.apply(q);
+    const V3 f = ld3(a.target, c);
+    if (a.c_kind[c] == WFK_DENSE_PLANE) {
+      const double rr = dot(s - f, ld3(a.normal, c));
+      ed += a.conf[c] * rr * rr;
+    } else {
+      es += a.conf[c] * sqnorm(s - f);
+    }
+  }
+  for (int r = int(gtid()); r < a.N; r += int(gstride())) {
+    const M3 ri = ld_m3(a.rot, r);
+    const int node = a.rows[r];
+    const V3 can_i = a.g.canonical(node);
+    const V3 ti = ld3(a.t, r);
+    for (int k = 0; k < 6; ++k) {
+      const int j = a.nbr[int64_t(k) * a.N + r];
+      if (j < 0) continue;
+      const V3 can_j = a.g.canonical(a.rows[j]);
+      const V3 resid = (ti - ld3(a.t, j)) - mul(ri, can_i - can_j);
+      er += sqnorm(resid);
+    }
+  }
+}
+
+__device__ wfk_energy energy(const FFArgs& a, cg::grid_group& grid, Red& rs, bool& logic_error) {
+  double es, ed, er;
+  int bad = 0;
+  energy_partials(a, es, ed, er, bad);
+  double v[4] = {es, ed, er, double(bad)};
+  grid_reduce<4>(a, grid, rs, v);
+  wfk_energy e;
+  e.sparse = v[0];
+  e.dense = v[1];
+  e.reg = v[2];
+  e.total = a.w_s * e.sparse + a.w_d * e.dense + a.w_r * e.reg;
+  logic_error = v[3] > 0;
+  return e;
+}
+
+// matrix-free A*v, pass 1: u_c = coef (g . q_c) g  |  coef q_c
+__device__ void matvec_constraints(const FFArgs& a, const double* v) {
+  for (int64_t c = gtid(); c < a.C; c += gstride()) {
+    V3 q{0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int row = a.c_row[8 * c + k];
+      if (row >= 0) q += a.c_w[8 * c + k] * ld3(v, row);
+    }
+    const double coef = a.c_g[4 * c + 3];
+    V3 u;
+    if (a.c_kind[c] == WFK_DENSE_PLANE) {
+      const V3 g{a.c_g[4 * c], a.c_g[4 * c + 1], a.c_g[4 * c + 2]};
+      u = (coef * dot(g, q)) * g;
+    } else {
+      u = coef * q;
+    }
+    st3(a.c_u, c, u);
+  }
+}
+
+// matrix-free A*v, pass 2, one row
+__device__ __forceinline__ V3 matvec_row(const FFArgs& a, const double* v, int r) {
+  const V3 vr = ld3(v, r);
+  if (a.frozen[r]) return vr;
+  V3 acc{0, 0, 0};
+  for (int e = a.row_ptr[r]; e < a.row_ptr[r + 1]; ++e) acc += a.ent_w[e] * ld3(a.c_u, a.ent_con[e]);
+  const double w2 = 2.0 * a.w_r;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    const int j = a.nbr[int64_t(k) * a.N + r];
+    if (j < 0) continue;
+    acc += w2 * (vr - ld3(v, j));
+  }
+  return acc;
+}
+
+// finish_row (solver.cpp:240-269) + Jacobi diagonal (solver.cpp:289-294)
+__device__ void assemble_rows(const FFArgs& a) {
+  for (int r = int(gtid()); r < a.N; r += int(gstride())) {
+    const int node = a.rows[r];
+    if (a.frozen[r]) {
+      st3(a.rhs, r, ld3(a.t, r));
+      st3(a.dinv, r, V3{1.0, 1.0, 1.0});
+      continue;
+    }
+    V3 rhs = ld3(a.crhs, r);
+    V3 diag = ld3(a.cdiag, r);
+    const M3 ri = ld_m3(a.rot, r);
+    const V3 can_i = a.g.canonical(node);
+    const double w2 = 2.0 * a.w_r;
+    for (int k = 0; k < 6; ++k) {
+      const int j = a.nbr[int64_t(k) * a.N + r];
+      if (j < 0) continue;
+      const V3 dij = can_i - a.g.canonical(a.rows[j]);
+      diag.x += w2 * 1.0;
+      diag.y += w2 * 1.0;
+      diag.z += w2 * 1.0;
+      rhs += a.w_r * mul(add(ri, ld_m3(a.rot, j)), dij);
+      if (a.frozen[j]) rhs += w2 * ld3(a.t, j);
+    }
+    st3(a.rhs, r, rhs);
+    st3(a.dinv, r, V3{diag.x > 1e-300 ? 1.0 / diag.x : 1.0, diag.y > 1e-300 ? 1.0 / diag.y : 1.0,
+                      diag.z > 1e-300 ? 1.0 / diag.z : 1.0});
+  }
+}
+
+// pcg_solve (solver.cpp:282-343) on the matrix-free operator; x in/out
+__device__ void pcg(const FFArgs& a, cg::grid_group& grid, Red& rs, int& iters, double& relres) {
+  iters = 0;
+  relres = 0;
+  // r = b - A x ; z = D^-1 r ; p = z
+  matvec_constraints(a, a.x);
+  grid.sync();
+  double v3[3] = {0, 0, 0};
+  for (int r = int(gtid()); r < a.N; r += int(gstride())) {
+    const V3 b = ld3(a.rhs, r);
+    const V3 rr = b - matvec_row(a, a.x, r);
+    const V3 z = cmul(ld3(a.dinv, r), rr);
+    st3(a.r, r, rr);
+    st3(a.p, r, z);
+    v3[0] += dot(rr, z);
+    v3[1] += dot(rr, rr);
+    v3[2] += sqnorm(b);
+  }
+  grid_reduce<3>(a, grid, rs, v3);
+  double rz = v3[0];
+  double r_norm = sqrt(v3[1]);
+  const double b_norm = sqrt(v3[2]);
+  if (b_norm == 0) {
+    for (int r = int(gtid()); r < a.N; r += int(gstride())) st3(a.x, r, V3{0, 0, 0});
+    grid.sync();
+    return;
+  }
+  relres = r_norm / b_norm;
+  const double stop = fmax(a.pcg_tol * r_norm, 1e-13 * b_norm);
+  for (int it = 0; it < a.pcg_max && r_norm > stop; ++it) {
+    matvec_constraints(a, a.p);
+    grid.sync();
+    double v1[1] = {0};
+    for (int r = int(gtid()); r < a.N; r += int(gstride())) {
+      const V3 apr = matvec_row(a, a.p, r);
+      st3(a.ap, r, apr);
+      v1[0] += dot(ld3(a.p, r), apr);
+    }
+    grid_reduce<1>(a, grid, rs, v1);
+    const double pap = v1[0];
+    if (pap <= 0) break;
+    const double alpha = rz / pap;
+    double v2[2] = {0, 0};
+    for (int r = int(gtid()); r < a.N; r += int(gstride())) {
+      const V3 pr = ld3(a.p, r);
+      st3(a.x, r, ld3(a.x, r) + alpha * pr);
+      const V3 rr = ld3(a.r, r) - alpha * ld3(a.ap, r);
+      st3(a.r, r, rr);
+      const V3 z = cmul(ld3(a.dinv, r), rr);
+      v2[0] += dot(rr, z);
+      v2[1] += dot(rr, rr);
+    }
+    grid_reduce<2>(a, grid, rs, v2);
+    const double rz_new = v2[0];
+    const double beta = rz_new / rz;
+    rz = rz_new;
+    for (int r = int(gtid()); r < a.N; r += int(gstride())) {
+      const V3 z = cmul(ld3(a.dinv, r), ld3(a.r, r));
+      st3(a.p, r, z + beta * ld3(a.p, r));
+    }
+    grid.sync();
+    r_norm = sqrt(v2[1]);
+    relres = r_norm / b_norm;
+    iters = it + 1;
+  }
+}
+
+// update_rotations (solver.cpp:385-417) for every row; rot[] follows euler.
+__device__ void rotations(const FFArgs& a) {
+  for (int r = int(gtid()); r < a.N; r += int(gstride())) {
+    const int node = a.rows[r];
+    const V3 can_i = a.g.canonical(node);
+    const V3 ti = ld3(a.t, r);
+    M3 h = m3_zero();
+    for (int k = 0; k < 6; ++k) {
+      const int j = a.nbr[int64_t(k) * a.N + r];
+      if (j < 0) continue;
+      const V3 rest = can_i - a.g.canonical(a.rows[j]);
+      const V3 cur = ti - ld3(a.t, j);
+      for (int p = 0; p < 3; ++p)
+        for (int q = 0; q < 3; ++q) h.a[p][q] += comp(rest, p) * comp(cur, q);
+    }
+    M3 u, v;
+    double sv[3];
+    svd3(h, u, sv, v);
+    if (sv[1] < 1e-14) continue;
+    M3 rm = mul(v, transpose(u));
+    if (det(rm) < 0) {
+      M3 flip = m3_identity();
+      flip.a[2][2] = -1;
+      rm = mul(mul(v, flip), transpose(u));
+    }
+    const V3 e = matrix_to_euler(rm);
+    st3(a.field_eul, node, e);
+    st_m3(a.rot, r, euler_to_matrix(e));
+  }
+}
+
+__global__ void __launch_bounds__(kBlock, 2) k_flip_flop(FFArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  Red rs;
+  // load the row state from the field
+  for (int r = int(gtid()); r < a.N; r += int(gstride())) {
+    const int node = a.rows[r];
+    st3(a.t, r, ld3(a.field_def, node));
+    st_m3(a.rot, r, euler_to_matrix(ld3(a.field_eul, node)));
+  }
+  grid.sync();
+  if (a.mode == 2) {
+    rotations(a);
+    return;
+  }
+  bool logic = false;
+  wfk_energy prev = energy(a, grid, rs, logic);
+  if (a.mode == 1 || logic) {
+    if (gtid() == 0) {
+      a.energy_out[0] = prev.total;
+      a.energy_out[1] = prev.sparse;
+      a.energy_out[2] = prev.dense;
+      a.energy_out[3] = prev.reg;
+      a.status[0] = 0;
+      if (logic) a.status[1] |= 1;
+    }
+    return;
+  }
+  int n_trace = 0;
+  int total_pcg = 0;
+  if (prev.total != 0) {
+    for (int it = 0; it < a.ff_iters; ++it) {
+      // assemble rhs / diagonal with the current rotations; x0 = t
+      assemble_rows(a);
+      for (int r = int(gtid()); r < a.N; r += int(gstride())) st3(a.x, r, ld3(a.t, r));
+      grid.sync();
+      int iters;
+      double relres;
+      pcg(a, grid, rs, iters, relres);
+      total_pcg += iters;
+      // write back non-frozen rows (solver.cpp:436-437)
+      for (int r = int(gtid()); r < a.N; r += int(gstride())) {
+        if (a.frozen[r]) continue;
+        const V3 xr = ld3(a.x, r);
+        st3(a.t, r, xr);
+        st3(a.field_def, a.rows[r], xr);
+      }
+      grid.sync();
+      rotations(a);
+      grid.sync();
+      bool dummy;
+      const wfk_energy e = energy(a, grid, rs, dummy);
+      const bool anomaly = e.total > prev.total + 1e-9 * prev.total;
+      if (gtid() == 0) {
+        wfk_trace_entry& t = a.trace[n_trace];
+        t.level = a.level;
+        t.iteration = it;
+        t.energy = e;
+        t.pcg_iterations = iters;
+        t.anomaly = anomaly ? 1 : 0;
+        t.pcg_residual = relres;
+      }
+      ++n_trace;
+      const double rel = (prev.total - e.total) / fmax(prev.total, 1e-300);
+      prev = e;
+      if (rel >= 0 && rel < a.ff_rel_tol) break;
+    }
+  }
+  if (gtid() == 0) {
+    a.status[0] = n_trace;
+    a.status[2] = total_pcg;
+    a.energy_out[0] = prev.total;
+    a.energy_out[1] = prev.sparse;
+    a.energy_out[2] = prev.dense;
+    a.energy_out[3] = prev.reg;
+  }
+}
+
+// ============================================================================
+// assembled-system PCG (pcg_solve on an explicit NormalEquations)
+// ============================================================================
+struct AsmArgs {
+  int N;
+  const double* blocks;  // N x 27 x 9
+  const int32_t* cols;   // N x 27
+  const double* rhs;
+  double *x, *r, *p, *ap, *dinv;
+  double tol;
+  int max_iters;
+  int mode;  // 0 = pcg, 1 = multiply x -> ap
+  double* partials;
+  int32_t* status;
+  double* relres_out;
+};
+
+__device__ __forceinline__ V3 asm_row(const AsmArgs& a, const double* v, int r) {
+  V3 acc{0, 0, 0};
+  for (int s = 0; s < 27; ++s) {
+    const int c = a.cols[27 * int64_t(r) + s];
+    if (c >= 0) acc += mul(ld_m3(a.blocks, 27 * int64_t(r) + s), ld3(v, c));
+  }
+  return acc;
+}
+
+template <int NV>
+__device__ void grid_reduce_asm(const AsmArgs& a, cg::grid_group& grid, int& region, double (&v)[NV]) {
+  __shared__ double smem[4 * 32];
+  block_sum<NV>(v, smem);
+  double* base = a.partials + size_t(region) * 4 * gridDim.x;
+  if (threadIdx.x == 0)
+    for (int k = 0; k < NV; ++k) base[size_t(k) * gridDim.x + blockIdx.x] = v[k];
+  grid.sync();
+  for (int k = 0; k < NV; ++k) v[k] = sum_partials(base + size_t(k) * gridDim.x, gridDim.x);
+  region ^= 1;
+}
+
+__global__ void __launch_bounds__(kBlock, 2) k_pcg_assembled(AsmArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  int region = 0;
+  if (a.mode == 1) {
+    for (int r = int(gtid()); r < a.N; r += int(gstride())) st3(a.ap, r, asm_row(a, a.x, r));
+    return;
+  }
+  for (int r = int(gtid()); r < a.N; r += int(gstride())) {
+    const M3 d = ld_m3(a.blocks, 27 * int64_t(r) + kCenter);
+    st3(a.dinv, r, V3{d.a[0][0] > 1e-300 ? 1.0 / d.a[0][0] : 1.0, d.a[1][1] > 1e-300 ? 1.0 / d.a[1][1] : 1.0,
+                      d.a[2][2] > 1e-300 ? 1.0 / d.a[2][2] : 1.0});
+  }
+  double v3[3] = {0, 0, 0};
+  for (int r = int(gtid()); r < a.N; r += int(gstride())) {
+    const V3 b = ld3(a.rhs, r);
+    const V3 rr = b - asm_row(a, a.x, r);
+    const V3 dv{1, 1, 1};
+    (void)dv;
+    st3(a.r, r, rr);
+  }
+  grid.sync();
+  for (int r = int(gtid()); r < a.N; r += int(gstride())) {
+    const V3 rr = ld3(a.r, r);
+    const V3 z = cmul(ld3(a.dinv, r), rr);
+    st3(a.p, r, z);
+    v3[0] += dot(rr, z);
+    v3[1] += dot(rr, rr);
+    v3[2] += sqnorm(ld3(a.rhs, r));
+  }
+  grid_reduce_asm<3>(a, grid, region, v3);
+  double rz = v3[0];
+  double r_norm = sqrt(v3[1]);
+  const double b_norm = sqrt(v3[2]);
+  int iters = 0;
+  double relres = 0;
+  if (b_norm == 0) {
+    for (int r = int(gtid()); r < a.N; r += int(gstride())) st3(a.x, r, V3{0, 0, 0});
+  } else {
+    relres = r_norm / b_norm;
+    const double stop = fmax(a.tol * r_norm, 1e-13 * b_norm);
+    for (int it = 0; it < a.max_iters && r_norm > stop; ++it) {
+      double v1[1] = {0};
+      for (int r = int(gtid()); r < a.N; r += int(gstride())) {
+        const V3 apr = asm_row(a, a.p, r);
+        st3(a.ap, r, apr);
+        v1[0] += dot(ld3(a.p, r), apr);
+      }
+      grid_reduce_asm<1>(a, grid, region, v1);
+      const double pap = v1[0];
+      if (pap <= 0) break;
+      const double alpha = rz / pap;
+      double v2[2] = {0, 0};
+      for (int r = int(gtid()); r < a.N; r += int(gstride())) {
+        st3(a.x, r, ld3(a.x, r) + alpha * ld3(a.p, r));
+        const V3 rr = ld3(a.r, r) - alpha * ld3(a.ap, r);
+        st3(a.r, r, rr);
+        const V3 z = cmul(ld3(a.dinv, r), rr);
+        v2[0] += dot(rr, z);
+        v2[1] += dot(rr, rr);
+      }
+      grid_reduce_asm<2>(a, grid, region, v2);
+      const double beta = v2[0] / rz;
+      rz = v2[0];
+      for (int r = int(gtid()); r < a.N; r += int(gstride())) {
+        const V3 z = cmul(ld3(a.dinv, r), ld3(a.r, r));
+        st3(a.p, r, z + beta * ld3(a.p, r));
+      }
+      grid.sync();
+      r_norm = sqrt(v2[1]);
+      relres = r_norm / b_norm;
+      iters = it + 1;
+    }
+  }
+  if (gtid() == 0) {
+    a.status[0] = iters;
+    a.relres_out[0] = relres;
+  }
+}
+
+// ============================================================================
+// NormalEquations materialisation (test-facing build_normal_equations)
+// ============================================================================
+__global__ void k_ne_assemble(Grid g, int N, const int32_t* rows, const int32_t* node_row, const int32_t* nbr,
+                              const uint8_t* frozen, const int32_t* row_ptr, const int32_t* ent_con,
+                              const double* ent_w, const int32_t* c_node, const double* c_w, const int32_t* c_kind,
+                              const double* c_g, const double* rot, const double* t, const double* crhs,
+                              double w_r, double* blocks, int32_t* cols, double* rhs) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x) {
+    const int node = rows[r];
+    int x, y, z;
+    g.idx3(node, x, y, z);
+    double* B = blocks + int64_t(r) * 27 * 9;
+    for (int s = 0; s < 27 * 9; ++s) B[s] = 0.0;
+    for (int dz = -1; dz <= 1; ++dz)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          const int s = stencil_slot(dx, dy, dz);
+          cols[27 * int64_t(r) + s] =
+              g.in_grid(x + dx, y + dy, z + dz) ? node_row[g.lin(x + dx, y + dy, z + dz)] : -1;
+        }
+    if (frozen[r]) {
+      B[kCenter * 9 + 0] = B[kCenter * 9 + 4] = B[kCenter * 9 + 8] = 1.0;
+      st3(rhs, r, ld3(t, r));
+      continue;
+    }
+    for (int e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
+      const int c = ent_con[e];
+      const double ai = ent_w[e];
+      const double coef = c_g[4 * c + 3];
+      const V3 gg{c_g[4 * c], c_g[4 * c + 1], c_g[4 * c + 2]};
+      for (int k = 0; k < 8; ++k) {
+        int a, b, cz;
+        g.idx3(c_node[8 * c + k], a, b, cz);
+        const int s = stencil_slot(a - x, b - y, cz - z);
+        const double sc = coef * ai * c_w[8 * c + k];
+        if (c_kind[c] == WFK_DENSE_PLANE) {
+          for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) B[s * 9 + i * 3 + j] += sc * (comp(gg, i) * comp(gg, j));
+        } else {
+          for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) B[s * 9 + i * 3 + j] += sc * (i == j ? 1.0 : 0.0);
+        }
+      }
+    }
+    V3 rv = ld3(crhs, r);
+    const M3 ri = ld_m3(rot, r);
+    const V3 can_i = g.canonical(node);
+    const double w2 = 2.0 * w_r;
+    for (int k = 0; k < 6; ++k) {
+      const int j = nbr[int64_t(k) * N + r];
+      if (j < 0) continue;
+      const V3 dij = can_i - g.canonical(rows[j]);
+      for (int i = 0; i < 3; ++i) B[kCenter * 9 + i * 4] += w2 * 1.0;
+      rv += w_r * mul(add(ri, ld_m3(rot, j)), dij);
+      if (frozen[j]) {
+        rv += w2 * ld3(t, j);
+      } else {
+        const int s = stencil_slot(kFace[k][0], kFace[k][1], kFace[k][2]);
+        for (int i = 0; i < 3; ++i) B[s * 9 + i * 4] -= w2 * 1.0;
+      }
+    }
+    st3(rhs, r, rv);
+  }
+}
+
+__global__ void k_load_rows(int N, const int32_t* rows, const double* f_def, const double* f_eul, double* t,
+                            double* rot) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x) {
+    st3(t, r, ld3(f_def, rows[r]));
+    st_m3(rot, r, euler_to_matrix(ld3(f_eul, rows[r])));
+  }
+}
+
+// ============================================================================
+// host orchestration
+// ============================================================================
+
+static void sync_check(wfk_ctx* c) { WFK_CUDA(cudaStreamSynchronize(c->stream)); }
+
+// Compacts the level's active mask into rows (ascending), builds node_row,
+// neighbours and the union-find labels.
+static void level_rows(wfk_ctx* c, Level& L) {
+  const int64_t n = L.g.n();
+  cudaStream_t s = c->stream;
+  L.rows.ensure(size_t(n));
+  L.node_row.ensure(size_t(n));
+  int32_t* d_count = c->ivec.ensure(16);
+  size_t tmp = 0;
+  thrust::counting_iterator<int32_t> it(0);
+  cub::DeviceSelect::Flagged(nullptr, tmp, it, L.active, L.rows.p, d_count, int(n), s);
+  c->temp.ensure(tmp);
+  WFK_CUDA(cub::DeviceSelect::Flagged(c->temp.p, tmp, it, L.active, L.rows.p, d_count, int(n), s));
+  count_launch(c);
+  WFK_CUDA(cudaMemcpyAsync(c->h_pinned, d_count, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  WFK_CUDA(cudaMemsetAsync(L.node_row.p, 0xff, size_t(n) * sizeof(int32_t), s));
+  sync_check(c);
+  L.N = c->h_pinned[0];
+  const int N = L.N;
+  const size_t Nc = size_t(N > 0 ? N : 1);
+  L.nbr.ensure(6 * Nc);
+  L.uf.ensure(Nc);
+  L.frozen.ensure(Nc);
+  L.comp_flag.ensure(Nc);
+  for (DevBuf<double>* b : {&L.t, &L.x, &L.rhs, &L.r, &L.p, &L.ap, &L.dinv, &L.crhs, &L.cdiag}) b->ensure(3 * Nc);
+  L.rot.ensure(9 * Nc);
+  L.row_ptr.ensure(Nc + 1);
+  L.cnt.ensure(Nc + 1);
+  if (N == 0) return;
+  k_scatter_node_row<<<grid_for(N), kBlock, 0, s>>>(L.rows, N, L.node_row);
+  k_row_neighbours<<<grid_for(N), kBlock, 0, s>>>(L.g, L.rows, N, L.node_row, L.nbr, L.uf);
+  k_union<<<grid_for(N), kBlock, 0, s>>>(L.nbr, N, L.uf);
+  k_uf_compress<<<grid_for(N), kBlock, 0, s>>>(N, L.uf, L.comp_flag);
+  count_launch(c, 4);
+  WFK_CUDA(cudaGetLastError());
+}
+
+// Prepares the level's constraints (anchors in c_node/c_w) for the solve:
+// rows, frozen rows, incidence transpose and the constraint cache.
+static void level_constraints(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_params& p) {
+  cudaStream_t s = c->stream;
+  const int64_t C = L.C;
+  const int N = L.N;
+  const size_t Cc = size_t(C > 0 ? C : 1);
+  L.c_row.ensure(8 * Cc);
+  L.c_g.ensure(4 * Cc);
+  L.c_b.ensure(Cc);
+  L.c_u.ensure(3 * Cc);
+  L.c_kind.ensure(Cc);
+  L.key_in.ensure(8 * Cc);
+  L.key_out.ensure(8 * Cc);
+  L.val_in.ensure(8 * Cc);
+  L.val_out.ensure(8 * Cc);
+  L.ent_con.ensure(8 * Cc);
+  L.ent_w.ensure(8 * Cc);
+  int32_t* d_ne = c->ivec.ensure(16) + 1;
+  WFK_CUDA(cudaMemsetAsync(d_ne, 0, sizeof(int32_t), s));
+  WFK_CUDA(cudaMemsetAsync(L.cnt.p, 0, size_t(N + 1) * sizeof(int32_t), s));
+  if (C > 0) {
+    k_con_prepare<<<grid_for(C), kBlock, 0, s>>>(C, c->cons.kind, c->cons.target, c->cons.normal, c->cons.conf,
+                                                 L.c_node, L.c_w, L.node_row, L.uf, pose, p.w_d, p.w_s, N, L.c_row,
+                                                 L.c_g, L.c_b, L.c_kind, L.comp_flag, L.key_in, L.val_in, L.cnt,
+                                                 d_ne);
+    count_launch(c);
+  }
+  if (N == 0) {
+    L.E = 0;
+    WFK_CUDA(cudaMemsetAsync(L.row_ptr.p, 0, sizeof(int32_t), s));
+    return;
+  }
+  k_frozen<<<grid_for(N), kBlock, 0, s>>>(N, L.uf, L.comp_flag, L.frozen);
+  count_launch(c);
+  // row_ptr = exclusive scan of per-row counts
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, L.cnt.p, L.row_ptr.p, N + 1, s);
+  size_t tmp2 = 0;
+  if (C > 0) {
+    int bits = 1;
+    while ((int64_t(1) << bits) <= int64_t(N) * 8) ++bits;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp2, L.key_in.p, L.key_out.p, L.val_in.p, L.val_out.p, int(8 * C), 0,
+                                    bits, s);
+    c->temp.ensure(std::max(tmp, tmp2));
+    WFK_CUDA(cub::DeviceRadixSort::SortPairs(c->temp.p, tmp2, L.key_in.p, L.key_out.p, L.val_in.p, L.val_out.p,
+                                             int(8 * C), 0, bits, s));
+    count_launch(c);
+  }
+  c->temp.ensure(std::max(tmp, tmp2));
+  WFK_CUDA(cub::DeviceScan::ExclusiveSum(c->temp.p, tmp, L.cnt.p, L.row_ptr.p, N + 1, s));
+  count_launch(c);
+  WFK_CUDA(cudaMemcpyAsync(c->h_pinned + 1, d_ne, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  sync_check(c);
+  L.E = c->h_pinned[1];
+  if (L.E > 0) {
+    k_entries<<<grid_for(L.E), kBlock, 0, s>>>(L.E, L.val_out, L.c_w, L.ent_con, L.ent_w);
+    count_launch(c);
+  }
+  k_constraint_cache<<<grid_for(N), kBlock, 0, s>>>(N, L.row_ptr, L.ent_con, L.ent_w, L.c_kind, L.c_g, L.c_b,
+                                                    L.crhs, L.cdiag);
+  count_launch(c);
+  WFK_CUDA(cudaGetLastError());
+}
+
+PoseD pose_dev(const wfk_pose* p) {
+  PoseD q;
+  for (int i = 0; i < 9; ++i) q.r.a[i / 3][i % 3] = p ? p->rotation[i] : (i % 4 == 0 ? 1.0 : 0.0);
+  q.t = p ? V3{p->translation[0], p->translation[1], p->translation[2]} : V3{0, 0, 0};
+  return q;
+}
+
+static int coop_blocks(wfk_ctx* c) {
+  if (c->coop_blocks == 0) {
+    int per_sm = 0;
+    WFK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_flip_flop, kBlock, 0));
+    int per_sm2 = 0;
+    WFK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_pcg_assembled, kBlock, 0));
+    per_sm = std::min(per_sm, per_sm2);
+    if (per_sm < 1) throw Error(WFK_E_CUDA, "cooperative kernel does not fit on an SM");
+    c->coop_blocks = c->num_sms * std::min(per_sm, 2);
+  }
+  return c->coop_blocks;
+}
+
+// Runs the cooperative kernel on a prepared level.  mode 0 = flip-flop,
+// 1 = energy, 2 = rotations.  Returns trace entries appended to `out`.
+static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_params& p, int mode, int level_tag,
+                      std::vector<wfk_trace_entry>* out, wfk_energy* e_out) {
+  cudaStream_t s = c->stream;
+  const int G = coop_blocks(c);
+  FFArgs a;
+  a.g = L.g;
+  a.N = L.N;
+  a.C = L.C;
+  a.mode = mode;
+  a.level = level_tag;
+  a.w_d = p.w_d;
+  a.w_s = p.w_s;
+  a.w_r = p.w_r;
+  a.ff_rel_tol = p.flip_flop_rel_tol;
+  a.pcg_tol = p.pcg_tol;
+  a.ff_iters = p.flip_flop_iters;
+  a.pcg_max = p.pcg_max_iters;
+  a.pose = pose;
+  a.rows = L.rows;
+  a.nbr = L.nbr;
+  a.frozen = L.frozen;
+  a.field_def = L.deformed;
+  a.field_eul = L.euler;
+  a.t = L.t;
+  a.x = L.x;
+  a.rhs = L.rhs;
+  a.r = L.r;
+  a.p = L.p;
+  a.ap = L.ap;
+  a.dinv = L.dinv;
+  a.rot = L.rot;
+  a.crhs = L.crhs;
+  a.cdiag = L.cdiag;
+  a.c_row = L.c_row;
+  a.c_w = L.c_w;
+  a.c_g = L.c_g;
+  a.c_kind = L.c_kind;
+  a.target = c->cons.target;
+  a.normal = c->cons.normal;
+  a.conf = c->cons.conf;
+  a.c_u = L.c_u;
+  a.row_ptr = L.row_ptr;
+  a.ent_con = L.ent_con;
+  a.ent_w = L.ent_w;
+  a.partials = c->partials.ensure(size_t(8) * G);
+  a.trace = c->trace.ensure(size_t(std::max(p.flip_flop_iters, 1)));
+  int32_t* status = c->ivec.ensure(16) + 4;
+  double* eout = c->eout.ensure(8);
+  a.status = status;
+  a.energy_out = eout;
+  WFK_CUDA(cudaMemsetAsync(status, 0, 4 * sizeof(int32_t), s));
+  if (L.N == 0 && L.C == 0 && mode != 2) {
+    // nothing to solve: energy is exactly zero
+    if (e_out) *e_out = wfk_energy{0, 0, 0, 0};
+    return;
+  }
+  void* args[] = {&a};
+  WFK_CUDA(cudaLaunchCooperativeKernel((void*)k_flip_flop, dim3(G), dim3(kBlock), args, 0, s));
+  count_launch(c);
+  int32_t st[4];
+  double en[4];
+  WFK_CUDA(cudaMemcpyAsync(c->h_pinned + 8, status, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  WFK_CUDA(cudaMemcpyAsync(reinterpret_cast<double*>(c->h_pinned + 16), eout, 4 * sizeof(double),
+                           cudaMemcpyDeviceToHost, s));
+  sync_check(c);
+  for (int i = 0; i < 4; ++i) st[i] = c->h_pinned[8 + i];
+  for (int i = 0; i < 4; ++i) en[i] = reinterpret_cast<double*>(c->h_pinned + 16)[i];
+  if (st[1] & 1) throw Error(WFK_E_LOGIC, "evaluate_energy: constraint anchors an inactive point");
+  if (e_out) *e_out = wfk_energy{en[0], en[1], en[2], en[3]};
+  c->stats.pcg_iterations += st[2];
+  if (out && st[0] > 0) {
+    const size_t k = out->size();
+    out->resize(k + size_t(st[0]));
+    WFK_CUDA(cudaMemcpyAsync(out->data() + k, a.trace, size_t(st[0]) * sizeof(wfk_trace_entry),
+                             cudaMemcpyDeviceToHost, s));
+    sync_check(c);
+  }
+}
+
+// level 0 aliases the volume and the uploaded anchors
+static void bind_level0(wfk_ctx* c) {
+  Level& L = c->lv[0];
+  L.g = c->vol.g;
+  L.deformed = c->vol.deformed;
+  L.euler = c->vol.euler;
+  L.active = c->vol.active;
+  L.C = c->cons.count;
+  const size_t Cc = size_t(std::max<int64_t>(L.C, 1));
+  L.c_node.ensure(8 * Cc);
+  L.c_w.ensure(8 * Cc);
+  if (L.C > 0) {
+    WFK_CUDA(cudaMemcpyAsync(L.c_node.p, c->cons.anchor.p, size_t(8 * L.C) * sizeof(int32_t),
+                             cudaMemcpyDeviceToDevice, c->stream));
+    WFK_CUDA(cudaMemcpyAsync(L.c_w.p, c->cons.weight.p, size_t(8 * L.C) * sizeof(double), cudaMemcpyDeviceToDevice,
+                             c->stream));
+  }
+}
+
+static void require_volume(wfk_ctx* c) {
+  if (!c->vol.valid) throw Error(WFK_E_INVALID_ARG, "no volume uploaded");
+}
+
+// build_hierarchy (solver.cpp:455-503): levels 1..L-1 from level 0
+static void build_hierarchy(wfk_ctx* c, int levels) {
+  if (levels < 1) throw Error(WFK_E_INVALID_ARG, "build_hierarchy: levels must be >= 1");
+  if (levels > kMaxLevels) throw Error(WFK_E_INVALID_ARG, "build_hierarchy: too many levels");
+  cudaStream_t s = c->stream;
+  int32_t* err = c->ivec.ensure(16) + 12;
+  WFK_CUDA(cudaMemsetAsync(err, 0, sizeof(int32_t), s));
+  for (int l = 1; l < levels; ++l) {
+    Level& F = c->lv[l - 1];
+    Level& Cl = c->lv[l];
+    Grid cg_ = F.g;
+    cg_.nx = (F.g.nx - 1 + 1) / 2 + 1;
+    cg_.ny = (F.g.ny - 1 + 1) / 2 + 1;
+    cg_.nz = (F.g.nz - 1 + 1) / 2 + 1;
+    if (cg_.nx < 2 || cg_.ny < 2 || cg_.nz < 2)
+      throw Error(WFK_E_INVALID_ARG, "build_hierarchy: coarsest level below 2^3");
+    cg_.voxel = F.g.voxel * 2.0;
+    Cl.g = cg_;
+    const size_t n = size_t(cg_.n());
+    Cl.deformed = Cl.own_deformed.ensure(3 * n);
+    Cl.euler = Cl.own_euler.ensure(3 * n);
+    Cl.active = Cl.own_active.ensure(n);
+    Cl.owns_field = true;
+    k_coarse_init<<<grid_for(int64_t(n)), kBlock, 0, s>>>(F.g, cg_, F.deformed, F.euler, Cl.deformed, Cl.euler,
+                                                          Cl.active);
+    k_coarse_activity<<<grid_for(F.g.n()), kBlock, 0, s>>>(F.g, cg_, F.active, Cl.active, err);
+    Cl.C = c->cons.count;
+    const size_t Cc = size_t(std::max<int64_t>(Cl.C, 1));
+    Cl.c_node.ensure(8 * Cc);
+    Cl.c_w.ensure(8 * Cc);
+    if (Cl.C > 0)
+      k_reanchor<<<grid_for(Cl.C), kBlock, 0, s>>>(Cl.C, cg_, c->cons.canonical, Cl.c_node, Cl.c_w, Cl.active, err);
+    count_launch(c, 3);
+  }
+  WFK_CUDA(cudaMemcpyAsync(c->h_pinned + 2, err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  sync_check(c);
+  if (c->h_pinned[2] & 2) throw Error(WFK_E_OUT_OF_RANGE, "trilinear_anchors: point outside grid");
+}
+
+static void prolong(wfk_ctx* c, int l) {
+  Level& Cl = c->lv[l];
+  Level& F = c->lv[l - 1];
+  k_prolong<<<grid_for(F.g.n()), kBlock, 0, c->stream>>>(F.g, Cl.g, F.active, F.deformed, F.euler, Cl.deformed,
+                                                         Cl.euler);
+  count_launch(c);
+}
+
+void solve_level(wfk_ctx* c, int l, const PoseD& pose, const wfk_solver_params& p, int mode,
+                 std::vector<wfk_trace_entry>* trace, wfk_energy* e) {
+  Level& L = c->lv[l];
+  level_rows(c, L);
+  level_constraints(c, L, pose, p);
+  run_level(c, L, pose, p, mode, l, trace, e);
+}
+
+// --------------------------------------------------------------------------
+// entry points used by api.cu
+// --------------------------------------------------------------------------
+void solver_flip_flop(wfk_ctx* c, const wfk_pose* pose, const wfk_solver_params& p, int level_tag,
+                      std::vector<wfk_trace_entry>& trace) {
+  require_volume(c);
+  bind_level0(c);
+  Level& L = c->lv[0];
+  const PoseD pd = pose_dev(pose);
+  level_rows(c, L);
+  level_constraints(c, L, pd, p);
+  run_level(c, L, pd, p, 0, level_tag, &trace, nullptr);
+}
+
+void solver_energy(wfk_ctx* c, const wfk_pose* pose, const wfk_solver_params& p, wfk_energy* e) {
+  require_volume(c);
+  bind_level0(c);
+  solve_level(c, 0, pose_dev(pose), p, 1, nullptr, e);
+}
+
+void solver_rotations(wfk_ctx* c) {
+  require_volume(c);
+  bind_level0(c);
+  wfk_solver_params p{};
+  Level& L = c->lv[0];
+  level_rows(c, L);
+  if (L.N == 0) return;
+  const int64_t Csave = L.C;
+  L.C = 0;
+  run_level(c, L, pose_dev(nullptr), p, 2, 0, nullptr, nullptr);
+  L.C = Csave;
+}
+
+void solver_c2f(wfk_ctx* c, const wfk_pose* pose, const wfk_solver_params& p, std::vector<wfk_trace_entry>& trace) {
+  require_volume(c);
+  bind_level0(c);
+  const PoseD pd = pose_dev(pose);
+  build_hierarchy(c, p.levels);
+  for (int l = p.levels - 1; l >= 1; --l) {
+    solve_level(c, l, pd, p, 0, &trace, nullptr);
+    prolong(c, l);
+  }
+  solve_level(c, 0, pd, p, 0, &trace, nullptr);
+}
+
+void solver_hierarchy_info(wfk_ctx* c, int levels, int32_t* dims, int64_t* active) {
+  require_volume(c);
+  bind_level0(c);
+  build_hierarchy(c, levels);
+  for (int l = 0; l < levels; ++l) {
+    Level& L = c->lv[l];
+    if (dims) {
+      dims[3 * l] = L.g.nx;
+      dims[3 * l + 1] = L.g.ny;
+      dims[3 * l + 2] = L.g.nz;
+    }
+    if (active) {
+      level_rows(c, L);
+      active[l] = L.N;
+    }
+  }
+}
+
+int solver_build_ne(wfk_ctx* c, const wfk_pose* pose, const wfk_solver_params& p, wfk_ne_host* out) {
+  require_volume(c);
+  bind_level0(c);
+  Level& L = c->lv[0];
+  const PoseD pd = pose_dev(pose);
+  level_rows(c, L);
+  level_constraints(c, L, pd, p);
+  const int N = L.N;
+  if (!out || N == 0) return N;
+  cudaStream_t s = c->stream;
+  double* t = L.t;
+  k_load_rows<<<grid_for(N), kBlock, 0, s>>>(N, L.rows, L.deformed, L.euler, t, L.rot);
+  DevBuf<double> blocks;
+  DevBuf<int32_t> cols;
+  DevBuf<double> rhs;
+  blocks.ensure(size_t(N) * 27 * 9);
+  cols.ensure(size_t(N) * 27);
+  rhs.ensure(size_t(N) * 3);
+  k_ne_assemble<<<grid_for(N), kBlock, 0, s>>>(L.g, N, L.rows, L.node_row, L.nbr, L.frozen, L.row_ptr, L.ent_con,
+                                               L.ent_w, L.c_node, L.c_w, L.c_kind, L.c_g, L.rot, t, L.crhs, p.w_r,
+                                               blocks, cols, rhs);
+  count_launch(c, 2);
+  WFK_CUDA(cudaGetLastError());
+  if (out->rows) WFK_CUDA(cudaMemcpyAsync(out->rows, L.rows, size_t(N) * 4, cudaMemcpyDeviceToHost, s));
+  if (out->node_row)
+    WFK_CUDA(cudaMemcpyAsync(out->node_row, L.node_row, size_t(L.g.n()) * 4, cudaMemcpyDeviceToHost, s));
+  if (out->blocks)
+    WFK_CUDA(cudaMemcpyAsync(out->blocks, blocks, size_t(N) * 27 * 9 * 8, cudaMemcpyDeviceToHost, s));
+  if (out->cols) WFK_CUDA(cudaMemcpyAsync(out->cols, cols, size_t(N) * 27 * 4, cudaMemcpyDeviceToHost, s));
+  if (out->rhs) WFK_CUDA(cudaMemcpyAsync(out->rhs, rhs, size_t(N) * 3 * 8, cudaMemcpyDeviceToHost, s));
+  if (out->frozen) WFK_CUDA(cudaMemcpyAsync(out->frozen, L.frozen, size_t(N), cudaMemcpyDeviceToHost, s));
+  sync_check(c);
+  return N;
+}
+
+void solver_pcg_assembled(wfk_ctx* c, int N, const double* blocks, const int32_t* cols, const double* rhs, double* x,
+                          double tol, int max_iters, int mode, wfk_pcg_result* res, double* y) {
+  cudaStream_t s = c->stream;
+  if (N <= 0) {
+    if (res) *res = wfk_pcg_result{0, 0, 0.0};
+    return;
+  }
+  DevBuf<double> B, X, R, P, AP, D, RHS;
+  DevBuf<int32_t> CL;
+  B.ensure(size_t(N) * 27 * 9);
+  CL.ensure(size_t(N) * 27);
+  X.ensure(size_t(N) * 3);
+  R.ensure(size_t(N) * 3);
+  P.ensure(size_t(N) * 3);
+  AP.ensure(size_t(N) * 3);
+  D.ensure(size_t(N) * 3);
+  RHS.ensure(size_t(N) * 3);
+  WFK_CUDA(cudaMemcpyAsync(B.p, blocks, size_t(N) * 27 * 9 * 8, cudaMemcpyHostToDevice, s));
+  WFK_CUDA(cudaMemcpyAsync(CL.p, cols, size_t(N) * 27 * 4, cudaMemcpyHostToDevice, s));
+  WFK_CUDA(cudaMemcpyAsync(X.p, x, size_t(N) * 3 * 8, cudaMemcpyHostToDevice, s));
+  if (rhs) WFK_CUDA(cudaMemcpyAsync(RHS.p, rhs, size_t(N) * 3 * 8, cudaMemcpyHostToDevice, s));
+  const int G = coop_blocks(c);
+  AsmArgs a;
+  a.N = N;
+  a.blocks = B;
+  a.cols = CL;
+  a.rhs = RHS;
+  a.x = X;
+  a.r = R;
+  a.p = P;
+  a.ap = AP;
+  a.dinv = D;
+  a.tol = tol;
+  a.max_iters = max_iters;
+  a.mode = mode;
+  a.partials = c->partials.ensure(size_t(8) * G);
+  a.status = c->ivec.ensure(16) + 8;
+  a.relres_out = c->dvec.ensure(8);
+  void* args[] = {&a};
+  WFK_CUDA(cudaLaunchCooperativeKernel((void*)k_pcg_assembled, dim3(G), dim3(kBlock), args, 0, s));
+  count_launch(c);
+  if (mode == 1) {
+    WFK_CUDA(cudaMemcpyAsync(y, AP.p, size_t(N) * 3 * 8, cudaMemcpyDeviceToHost, s));
+    sync_check(c);
+    return;
+  }
+  WFK_CUDA(cudaMemcpyAsync(x, X.p, size_t(N) * 3 * 8, cudaMemcpyDeviceToHost, s));
+  WFK_CUDA(cudaMemcpyAsync(c->h_pinned + 8, a.status, 4, cudaMemcpyDeviceToHost, s));
+  WFK_CUDA(cudaMemcpyAsync(reinterpret_cast<double*>(c->h_pinned + 16), a.relres_out, 8, cudaMemcpyDeviceToHost, s));
+  sync_check(c);
+  if (res) {
+    res->iterations = c->h_pinned[8];
+    res->relative_residual = reinterpret_cast<double*>(c->h_pinned + 16)[0];
+  }
+  c->stats.pcg_iterations += c->h_pinned[8];
+}
+
+}  // namespace wfk

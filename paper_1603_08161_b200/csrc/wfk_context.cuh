@@ -1,0 +1,207 @@
+// Device context of libwfk: one per (process, GPU).  Owns the device-resident
+// deformation lattice, the per-level solver workspaces, the frame / map /
+// mesh / geometry-buffer buffers and the CUDA stream every call runs on.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/wfk.h"
+#include "wfk_common.cuh"
+
+namespace wfk {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define WFK_CUDA(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      throw ::wfk::Error(e_ == cudaErrorMemoryAllocation ? WFK_E_OOM : WFK_E_CUDA,       \
+                         std::string(#call) + ": " + cudaGetErrorString(e_));            \
+  } while (0)
+
+// Growable device buffer (capacity only grows; contents not preserved).
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  T* ensure(size_t n) {
+    if (n == 0) n = 1;
+    if (n > cap) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      size_t want = n + n / 4;
+      WFK_CUDA(cudaMalloc(&p, want * sizeof(T)));
+      cap = want;
+    }
+    return p;
+  }
+  // exact-size ensure keeping the old contents
+  T* grow_keep(size_t n, cudaStream_t s) {
+    if (n <= cap) return p;
+    T* q = nullptr;
+    size_t want = n + n / 4;
+    WFK_CUDA(cudaMalloc(&q, want * sizeof(T)));
+    if (p) {
+      WFK_CUDA(cudaMemcpyAsync(q, p, cap * sizeof(T), cudaMemcpyDeviceToDevice, s));
+      WFK_CUDA(cudaStreamSynchronize(s));
+      cudaFree(p);
+    }
+    p = q;
+    cap = want;
+    return p;
+  }
+  operator T*() const { return p; }
+};
+
+// Device copy of one wf::Correspondence (input constraints of a solve).
+struct ConIn {
+  DevBuf<int32_t> kind;     // C
+  DevBuf<double> canonical; // 3C
+  DevBuf<int32_t> anchor;   // 8C   (node indices, level-0 grid)
+  DevBuf<double> weight;    // 8C
+  DevBuf<double> target;    // 3C
+  DevBuf<double> normal;    // 3C
+  DevBuf<double> conf;      // C
+  int64_t count = 0;
+};
+
+// Per-level solver workspace (one lattice of the coarse-to-fine hierarchy).
+struct Level {
+  Grid g{};
+  bool owns_field = false;
+  // node-indexed deformation field (level 0: aliases the volume)
+  DevBuf<double> own_deformed, own_euler;
+  DevBuf<uint8_t> own_active;
+  double* deformed = nullptr;
+  double* euler = nullptr;
+  uint8_t* active = nullptr;
+  // rows
+  int N = 0;
+  DevBuf<int32_t> rows, node_row, nbr, uf;  // nbr: 6 x Ncap SoA
+  DevBuf<uint8_t> frozen, comp_flag;
+  // per-row state (AoS double3 / row-major 3x3)
+  DevBuf<double> t, x, rhs, r, p, ap, dinv, crhs, cdiag, rot;
+  // level constraints
+  int64_t C = 0;
+  DevBuf<int32_t> c_node;   // 8C anchors at this level
+  DevBuf<double> c_w;       // 8C
+  DevBuf<int32_t> c_row;    // 8C (row or -1)
+  DevBuf<double> c_g;       // 4C: g = R^T n (dense) and coef
+  DevBuf<double> c_b;       // 3C: constraint rhs vector before alpha
+  DevBuf<double> c_u;       // 3C: matvec scratch
+  DevBuf<int32_t> c_kind;   // C
+  // CSR transpose: row -> (constraint, alpha)
+  int64_t E = 0;
+  DevBuf<int32_t> row_ptr, ent_con, key_in, key_out, val_in, val_out;
+  DevBuf<double> ent_w;
+  DevBuf<int32_t> cnt;
+};
+
+struct VolumeDev {
+  Grid g{};
+  double mu = 0;
+  int64_t n = 0;
+  DevBuf<float> tsdf, weight, color;
+  DevBuf<double> deformed, euler;
+  DevBuf<int32_t> age;
+  DevBuf<uint8_t> active;
+  bool valid = false;
+};
+
+struct FrameDev {
+  wfk_intrinsics K{};
+  bool has_color = false;
+  DevBuf<float> depth, color;
+  // PointNormalMap (correspond.hpp:34-42)
+  DevBuf<double> point, normal;
+  DevBuf<uint8_t> pvalid, nvalid;
+  bool maps_valid = false;
+};
+
+struct MeshDev {
+  int64_t V = 0, T = 0;
+  DevBuf<double> can, def, nrm;
+  DevBuf<float> col;
+  DevBuf<int32_t> tri;
+  // marching-cubes scratch
+  DevBuf<int32_t> cell_case, cell_tri_off, cell_vert_off, edge_vertex;
+  DevBuf<uint8_t> tri_keep;
+  DevBuf<int32_t> tri_pos;
+  // vertex -> incident triangles (ascending), for compute_normals
+  DevBuf<int32_t> adj_ptr, adj_tri;
+  bool adj_valid = false;
+  bool normals_valid = false;
+};
+
+struct GBufDev {
+  int w = 0, h = 0;
+  DevBuf<float> depth;
+  DevBuf<double> point, normal, canonical;
+  DevBuf<unsigned long long> zkey;
+  // triangle setup scratch
+  DevBuf<double> setup;
+  DevBuf<int32_t> setup_tri;
+  DevBuf<int32_t> assoc_pos;
+  bool valid = false;
+};
+
+constexpr int kMaxLevels = 8;
+
+struct Stats {
+  int64_t pcg_iterations = 0;
+  int64_t kernel_launches = 0;
+};
+
+}  // namespace wfk
+
+struct wfk_ctx {
+  int device = 0;
+  int num_sms = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  wfk::VolumeDev vol;
+  wfk::ConIn cons;
+  wfk::Level lv[wfk::kMaxLevels];
+  wfk::FrameDev frame;
+  wfk::MeshDev mesh;
+  wfk::GBufDev gbuf;
+  wfk::Stats stats;
+  // scratch
+  wfk::DevBuf<double> partials;
+  wfk::DevBuf<int32_t> flags;   // device status words
+  wfk::DevBuf<uint8_t> temp;    // cub temp storage
+  wfk::DevBuf<wfk_trace_entry> trace;
+  wfk::DevBuf<int32_t> ivec;    // misc int scratch
+  wfk::DevBuf<int64_t> lvec;    // misc int64 scratch
+  wfk::DevBuf<double> dvec;     // misc double scratch
+  wfk::DevBuf<double> eout;     // energy readback
+  wfk::DevBuf<uint8_t> mask;    // misc byte scratch
+  int32_t* h_pinned = nullptr;  // small pinned readback area (4 KB)
+  int coop_blocks = 0;          // resident blocks for cooperative kernels
+};
+
+namespace wfk {
+// launch-count bookkeeping (bench.py reports gpu_launches from this)
+inline void count_launch(wfk_ctx* c, int n = 1) { c->stats.kernel_launches += n; }
+inline int grid_for(int64_t n, int block = kBlock) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > (1 << 30)) g = 1 << 30;
+  return int(g);
+}
+}  // namespace wfk

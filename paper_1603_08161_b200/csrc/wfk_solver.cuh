@@ -1,0 +1,38 @@
+// Host-side entry points of the device solver (solver.cu), used by api.cu.
+#pragma once
+
+#include <vector>
+
+#include "wfk_context.cuh"
+
+namespace wfk {
+
+PoseD pose_dev(const wfk_pose* p);
+void solver_flip_flop(wfk_ctx* c, const wfk_pose* pose, const wfk_solver_params& p, int level_tag,
+                      std::vector<wfk_trace_entry>& trace);
+void solver_energy(wfk_ctx* c, const wfk_pose* pose, const wfk_solver_params& p, wfk_energy* e);
+void solver_rotations(wfk_ctx* c);
+void solver_c2f(wfk_ctx* c, const wfk_pose* pose, const wfk_solver_params& p, std::vector<wfk_trace_entry>& trace);
+void solver_hierarchy_info(wfk_ctx* c, int levels, int32_t* dims, int64_t* active);
+int solver_build_ne(wfk_ctx* c, const wfk_pose* pose, const wfk_solver_params& p, wfk_ne_host* out);
+void solver_pcg_assembled(wfk_ctx* c, int N, const double* blocks, const int32_t* cols, const double* rhs, double* x,
+                          double tol, int max_iters, int mode, wfk_pcg_result* res, double* y);
+
+// fusion.cu
+void fusion_compute_active_set(wfk_ctx* c, int32_t* out, int64_t cap, int64_t* n_out);
+void fusion_integrate(wfk_ctx* c, const wfk_pose* pose, const wfk_fusion_params& p, wfk_fusion_stats* out);
+void fusion_expand(wfk_ctx* c, wfk_expansion_stats* out);
+void fusion_advance_ages(wfk_ctx* c, const int32_t* idx, int64_t n);
+void fusion_advance_active_ages(wfk_ctx* c);
+
+// assoc.cu
+void assoc_backproject(wfk_ctx* c, wfk_point_normal_map* out);
+void assoc_extract_mesh(wfk_ctx* c, const wfk_pose* pose, int64_t* nv, int64_t* nt);
+void assoc_mesh_warp(wfk_ctx* c, const wfk_pose* pose);
+void assoc_compute_normals(wfk_ctx* c);
+void assoc_rasterize(wfk_ctx* c, const wfk_intrinsics& K, wfk_geometry_buffer* out);
+void assoc_find_dense(wfk_ctx* c, const wfk_intrinsics& K, const wfk_correspond_params& p, bool drop_inactive,
+                      int64_t* n_out);
+void synth_render(wfk_ctx* c, const wfk_synth_scene& s, const wfk_intrinsics& K, float* depth, float* color);
+
+}  // namespace wfk

@@ -1,0 +1,342 @@
+"""ctypes front end of libwfk.so (include/wfk.h) -- the B200 path.
+
+``Context`` owns one device (its CUDA stream, the device-resident lattice and
+work buffers).  Its methods are one-to-one with the C ABI; ``paper_1603_08161_b200.wf``
+layers the reference's stateless ``wf::`` functions on top.
+
+There is no CPU fallback: if libwfk.so is missing or no B200 is visible the
+constructor raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+from .abi import (CORR_DTYPE, CorrespondParams, Energy, ExpansionStats, FrameView, FusionParams,
+                  FusionStats, GeometryBufferView, Intrinsics, MeshView, PcgResult,
+                  PointNormalMapView, Pose, SolverParams, TraceEntry, Volume, VolumeView, ptr,
+                  trace_to_list, VOL_ALL, WFK_OK)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libwfk.so")
+CSRC = os.path.join(HERE, "csrc")
+
+
+def build(jobs: int = 4) -> str:
+    """Compile libwfk.so for sm_100a in-tree (nvcc cross-compiles without a GPU)."""
+    subprocess.run(["make", "-s", f"-j{jobs}", "-C", CSRC], check=True)
+    return LIB_PATH
+
+
+class WfkError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"libwfk error {code}: {msg}")
+        self.code = code
+
+
+class PipelineConfig(C.Structure):
+    _fields_ = [("solver", SolverParams), ("correspond", CorrespondParams), ("fusion", FusionParams),
+                ("reassociations", C.c_int32), ("reserved_", C.c_int32)]
+
+
+class FrameRecord(C.Structure):
+    _fields_ = [("energy", Energy), ("dense_count", C.c_int32), ("sparse_count", C.c_int32),
+                ("anomalies", C.c_int32), ("trace_len", C.c_int32), ("pcg_iterations", C.c_int32),
+                ("bootstrap", C.c_int32), ("fusion", FusionStats), ("expansion", ExpansionStats)]
+
+
+class NeHost(C.Structure):
+    _fields_ = [("rows", C.c_void_p), ("node_row", C.c_void_p), ("blocks", C.c_void_p),
+                ("cols", C.c_void_p), ("rhs", C.c_void_p), ("frozen", C.c_void_p)]
+
+
+class SynthScene(C.Structure):
+    _fields_ = [("center", C.c_double * 3), ("radius", C.c_double), ("pivot", C.c_double * 3),
+                ("amplitude", C.c_double), ("driver_axis", C.c_int32), ("rot_axis", C.c_int32),
+                ("t_min", C.c_double), ("t_max", C.c_double), ("texture_seed", C.c_uint32),
+                ("reserved_", C.c_int32), ("texture_scale", C.c_double), ("dot_radius", C.c_double)]
+
+
+class Config(C.Structure):
+    _fields_ = [("device", C.c_int32), ("reserved_", C.c_int32 * 7)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libwfk.so not built ({LIB_PATH}); run __graft_entry__.build()")
+        _lib = C.CDLL(LIB_PATH)
+        _lib.wfk_last_error.restype = C.c_char_p
+        _lib.wfk_last_error.argtypes = [C.c_void_p]
+        _lib.wfk_launch_count.restype = C.c_int64
+        _lib.wfk_launch_count.argtypes = [C.c_void_p]
+        _lib.wfk_pcg_iteration_count.restype = C.c_int64
+        _lib.wfk_pcg_iteration_count.argtypes = [C.c_void_p]
+        _lib.wfk_destroy.argtypes = [C.c_void_p]
+    return _lib
+
+
+def _cptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+class Context:
+    """One libwfk context on one CUDA device (wfk_create / wfk_destroy)."""
+
+    def __init__(self, device: int = 0):
+        cfg = Config()
+        cfg.device = device
+        h = C.c_void_p()
+        rc = lib().wfk_create(C.byref(cfg), C.byref(h))
+        if rc != WFK_OK:
+            raise WfkError(rc, "wfk_create failed (no B200 / CUDA device visible?)")
+        self.h = h
+        self.dims = None
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().wfk_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def _check(self, rc):
+        if rc != WFK_OK:
+            raise WfkError(rc, lib().wfk_last_error(self.h).decode())
+
+    @property
+    def launch_count(self) -> int:
+        return int(lib().wfk_launch_count(self.h))
+
+    @property
+    def pcg_iteration_count(self) -> int:
+        return int(lib().wfk_pcg_iteration_count(self.h))
+
+    # ---- volume ------------------------------------------------------------
+    def upload_volume(self, vol: Volume, fields: int = VOL_ALL):
+        vv = vol.view()
+        self._check(lib().wfk_volume_upload(self.h, C.byref(vv), C.c_uint32(fields)))
+        self.dims = vol.dims
+
+    def download_volume(self, vol: Volume, fields: int = VOL_ALL):
+        vv = vol.view()
+        self._check(lib().wfk_volume_download(self.h, C.byref(vv), C.c_uint32(fields)))
+
+    # ---- solver ------------------------------------------------------------
+    def compute_active_set(self, want_list: bool = True):
+        n = C.c_int64()
+        if not want_list:
+            self._check(lib().wfk_compute_active_set(self.h, None, C.c_int64(0), C.byref(n)))
+            return n.value
+        cap = int(np.prod(self.dims))
+        out = np.zeros(cap, np.int32)
+        self._check(lib().wfk_compute_active_set(self.h, _cptr(out), C.c_int64(cap), C.byref(n)))
+        return out[: n.value].copy()
+
+    def upload_constraints(self, cons):
+        cons = np.ascontiguousarray(cons if cons is not None else np.zeros(0, CORR_DTYPE), dtype=CORR_DTYPE)
+        self._check(lib().wfk_constraints_upload(self.h, _cptr(cons), C.c_int64(len(cons))))
+
+    def append_constraints(self, cons, drop_inactive=True) -> int:
+        cons = np.ascontiguousarray(cons, dtype=CORR_DTYPE)
+        kept = C.c_int64()
+        self._check(lib().wfk_constraints_append(self.h, _cptr(cons), C.c_int64(len(cons)),
+                                                 C.c_int32(1 if drop_inactive else 0), C.byref(kept)))
+        return kept.value
+
+    def download_constraints(self):
+        n = C.c_int64()
+        self._check(lib().wfk_constraints_download(self.h, None, C.c_int64(0), C.byref(n)))
+        out = np.zeros(max(n.value, 1), CORR_DTYPE)
+        self._check(lib().wfk_constraints_download(self.h, _cptr(out), C.c_int64(len(out)), C.byref(n)))
+        return out[: n.value].copy()
+
+    def evaluate_energy(self, pose: Pose, params: SolverParams) -> dict:
+        e = Energy()
+        self._check(lib().wfk_evaluate_energy(self.h, C.byref(pose), C.byref(params), C.byref(e)))
+        return e.as_dict()
+
+    def update_rotations(self):
+        self._check(lib().wfk_update_rotations(self.h, C.c_int32(1)))
+
+    def _trace(self, fn, *args, cap=4096):
+        buf = (TraceEntry * cap)()
+        n = C.c_int32()
+        self._check(fn(self.h, *args, buf, C.c_int32(cap), C.byref(n)))
+        return trace_to_list(buf, n.value)
+
+    def flip_flop_solve(self, pose: Pose, params: SolverParams, level: int = 0):
+        return self._trace(lib().wfk_flip_flop_solve, C.byref(pose), C.byref(params), C.c_int32(level))
+
+    def solve_coarse_to_fine(self, pose: Pose, params: SolverParams):
+        return self._trace(lib().wfk_solve_coarse_to_fine, C.byref(pose), C.byref(params))
+
+    def hierarchy_info(self, levels: int):
+        dims = np.zeros((levels, 3), np.int32)
+        act = np.zeros(levels, np.int64)
+        self._check(lib().wfk_hierarchy_info(self.h, C.c_int32(levels), _cptr(dims), _cptr(act)))
+        return dims, act
+
+    def build_normal_equations(self, pose: Pose, params: SolverParams) -> dict:
+        rows = C.c_int32()
+        self._check(lib().wfk_build_normal_equations(self.h, C.byref(pose), C.byref(params), None,
+                                                     C.byref(rows)))
+        n = rows.value
+        npts = int(np.prod(self.dims))
+        out = dict(rows=np.zeros(n, np.int32), node_row=np.zeros(npts, np.int32),
+                   blocks=np.zeros((n, 27, 3, 3)), cols=np.zeros((n, 27), np.int32),
+                   rhs=np.zeros((n, 3)), frozen=np.zeros(n, np.uint8))
+        ne = NeHost(*(_cptr(out[k]) for k in ("rows", "node_row", "blocks", "cols", "rhs", "frozen")))
+        self._check(lib().wfk_build_normal_equations(self.h, C.byref(pose), C.byref(params), C.byref(ne),
+                                                     C.byref(rows)))
+        return out
+
+    def pcg_solve(self, blocks, cols, rhs, x, tol, max_iters):
+        blocks = np.ascontiguousarray(blocks, np.float64)
+        cols = np.ascontiguousarray(cols, np.int32)
+        rhs = np.ascontiguousarray(rhs, np.float64)
+        x = np.ascontiguousarray(x, np.float64).copy()
+        res = PcgResult()
+        self._check(lib().wfk_pcg_solve(self.h, C.c_int32(len(cols)), _cptr(blocks), _cptr(cols), _cptr(rhs),
+                                        _cptr(x), C.c_double(tol), C.c_int32(max_iters), C.c_int32(1),
+                                        C.byref(res)))
+        return x, res.iterations, res.relative_residual
+
+    def ne_multiply(self, blocks, cols, x):
+        blocks = np.ascontiguousarray(blocks, np.float64)
+        cols = np.ascontiguousarray(cols, np.int32)
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.zeros_like(x)
+        self._check(lib().wfk_ne_multiply(self.h, C.c_int32(len(cols)), _cptr(blocks), _cptr(cols), _cptr(x),
+                                          _cptr(y)))
+        return y
+
+    # ---- fusion ------------------------------------------------------------
+    def upload_frame(self, frame):
+        fv = frame.view()
+        self._check(lib().wfk_frame_upload(self.h, C.byref(fv)))
+        self._frame_wh = (frame.intrinsics.width, frame.intrinsics.height)
+
+    def integrate_frame(self, pose: Pose, params: FusionParams) -> FusionStats:
+        s = FusionStats()
+        self._check(lib().wfk_integrate_frame(self.h, C.byref(pose), C.byref(params), C.c_int32(1), C.byref(s)))
+        return s
+
+    def expand_grid(self) -> ExpansionStats:
+        s = ExpansionStats()
+        self._check(lib().wfk_expand_grid(self.h, C.byref(s)))
+        return s
+
+    def advance_ages(self, idx):
+        idx = np.ascontiguousarray(idx, np.int32)
+        self._check(lib().wfk_advance_ages(self.h, _cptr(idx), C.c_int64(idx.size)))
+
+    def advance_active_ages(self):
+        self._check(lib().wfk_advance_active_ages(self.h))
+
+    # ---- association -------------------------------------------------------
+    def backproject_depth(self, download: bool = True):
+        from types import SimpleNamespace
+        if not download:
+            self._check(lib().wfk_backproject_depth(self.h, C.c_int32(1), None))
+            return None
+        # sizes come from the uploaded frame; caller passes dims via last upload
+        w, h = self._frame_wh
+        m = SimpleNamespace(width=w, height=h, point=np.zeros((w * h, 3)), normal=np.zeros((w * h, 3)),
+                            point_valid=np.zeros(w * h, np.uint8), normal_valid=np.zeros(w * h, np.uint8))
+        v = PointNormalMapView(w, h, ptr(m.point, C.c_double), ptr(m.normal, C.c_double),
+                               ptr(m.point_valid, C.c_uint8), ptr(m.normal_valid, C.c_uint8))
+        self._check(lib().wfk_backproject_depth(self.h, C.c_int32(1), C.byref(v)))
+        return m
+
+    def extract_mesh(self, pose: Pose):
+        nv, nt = C.c_int64(), C.c_int64()
+        self._check(lib().wfk_extract_mesh(self.h, C.byref(pose), C.byref(nv), C.byref(nt)))
+        return nv.value, nt.value
+
+    def mesh_warp(self, pose: Pose):
+        self._check(lib().wfk_mesh_warp(self.h, C.byref(pose)))
+
+    def compute_normals(self):
+        self._check(lib().wfk_compute_normals(self.h))
+
+    def download_mesh(self):
+        from types import SimpleNamespace
+        mv = MeshView()
+        self._check(lib().wfk_mesh_download(self.h, C.byref(mv)))
+        V, T = mv.num_vertices, mv.num_triangles
+        m = SimpleNamespace(vertices_canonical=np.zeros((V, 3)), vertices_deformed=np.zeros((V, 3)),
+                            normals_deformed=np.zeros((V, 3)), colors=np.zeros((V, 3), np.float32),
+                            triangles=np.zeros((T, 3), np.int32))
+        mv = MeshView(V, T, ptr(m.vertices_canonical, C.c_double), ptr(m.vertices_deformed, C.c_double),
+                      ptr(m.normals_deformed, C.c_double), ptr(m.colors, C.c_float), ptr(m.triangles, C.c_int32))
+        self._check(lib().wfk_mesh_download(self.h, C.byref(mv)))
+        return m
+
+    def upload_mesh(self, m):
+        def a(x, dt):
+            return None if x is None else np.ascontiguousarray(x, dt)
+        can, de = a(m.vertices_canonical, np.float64), a(m.vertices_deformed, np.float64)
+        nr = a(getattr(m, "normals_deformed", None), np.float64)
+        col, tri = a(m.colors, np.float32), a(m.triangles, np.int32)
+        mv = MeshView(len(can), len(tri), ptr(can, C.c_double), ptr(de, C.c_double), ptr(nr, C.c_double),
+                      ptr(col, C.c_float), ptr(tri, C.c_int32))
+        self._check(lib().wfk_mesh_upload(self.h, C.byref(mv)))
+
+    def rasterize(self, intr: Intrinsics, download: bool = True):
+        from types import SimpleNamespace
+        if not download:
+            self._check(lib().wfk_rasterize(self.h, C.byref(intr), C.c_int32(1), None))
+            return None
+        w, h = intr.width, intr.height
+        b = SimpleNamespace(width=w, height=h, depth=np.zeros(w * h, np.float32), point=np.zeros((w * h, 3)),
+                            normal=np.zeros((w * h, 3)), canonical=np.zeros((w * h, 3)))
+        v = GeometryBufferView(w, h, ptr(b.depth, C.c_float), ptr(b.point, C.c_double), ptr(b.normal, C.c_double),
+                               ptr(b.canonical, C.c_double))
+        self._check(lib().wfk_rasterize(self.h, C.byref(intr), C.c_int32(1), C.byref(v)))
+        return b
+
+    def upload_gbuffer(self, b):
+        v = GeometryBufferView(b.width, b.height, ptr(np.ascontiguousarray(b.depth, np.float32), C.c_float),
+                               ptr(np.ascontiguousarray(b.point), C.c_double),
+                               ptr(np.ascontiguousarray(b.normal), C.c_double),
+                               ptr(np.ascontiguousarray(b.canonical), C.c_double))
+        self._check(lib().wfk_gbuffer_upload(self.h, C.byref(v)))
+
+    def find_dense_correspondences(self, intr: Intrinsics, params: CorrespondParams, drop_inactive=False) -> int:
+        n = C.c_int64()
+        self._check(lib().wfk_find_dense_correspondences(self.h, C.byref(intr), C.byref(params),
+                                                         C.c_int32(1 if drop_inactive else 0), C.byref(n)))
+        return n.value
+
+    # ---- per-frame pipeline --------------------------------------------------
+    def process_frame(self, frame, pose: Pose, cfg: PipelineConfig, frame_index: int, sparse=None) -> FrameRecord:
+        rec = FrameRecord()
+        s = None if sparse is None or len(sparse) == 0 else np.ascontiguousarray(sparse, CORR_DTYPE)
+        fv = frame.view()
+        self._check(lib().wfk_process_frame(self.h, C.byref(fv), C.byref(pose), C.byref(cfg), _cptr(s),
+                                            C.c_int64(0 if s is None else len(s)), C.c_int32(frame_index),
+                                            C.byref(rec)))
+        return rec
+
+    def synth_render(self, scene: SynthScene, intr: Intrinsics):
+        depth = np.zeros((intr.height, intr.width), np.float32)
+        color = np.zeros((intr.height, intr.width, 3), np.float32)
+        self._check(lib().wfk_synth_render(self.h, C.byref(scene), C.byref(intr), _cptr(depth), _cptr(color)))
+        return depth, color
+
+
+def pipeline_config(solver=None, correspond=None, fusion=None, reassociations=3) -> PipelineConfig:
+    cfg = PipelineConfig()
+    cfg.solver = solver or SolverParams.make()
+    cfg.correspond = correspond or CorrespondParams.make()
+    cfg.fusion = fusion or FusionParams.make()
+    cfg.reassociations = reassociations
+    return cfg

@@ -1,0 +1,298 @@
+"""Parity of the B200 solver (libwfk.so via its C ABI) against the oracle.
+
+Integer and index work must be bit-exact (rows, node_row, stencil columns,
+frozen rows, active sets).  Floating-point work is compared against the oracle
+with the tolerances of BASELINE.json's north_star: <= 1e-4 relative on final
+energy and <= 1e-3 voxel on deformed positions; the assembled quantities that
+are computed in the reference's own operation order are held to 1e-12."""
+import numpy as np
+import pytest
+
+from oracle import pyoracle as O
+from paper_1603_08161_b200.abi import CORR_DTYPE, Pose, SolverParams, Volume
+from tests.fixtures import (acceptance_sphere_volume, active_sphere_volume, make_volume, node_constraints,
+                            random_dense_constraints, rigid_motion_constraints)
+
+pytestmark = pytest.mark.gpu
+
+ENERGY_RTOL = 1e-4     # north_star: final energy
+POS_TOL_VOXEL = 1e-3   # north_star: deformed positions, in voxels
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_1603_08161_b200.wfk import Context
+    c = Context(0)
+    yield c
+    c.close()
+
+
+def jittered_sphere(n=12, voxel=0.05, seed=21, amp=0.02, euler_amp=0.0):
+    v = active_sphere_volume(n, voxel)
+    rng = O.Rng(seed)
+    for i in range(v.num_points):
+        v.deformed[i] += rng.vec3(-amp, amp)
+        if euler_amp:
+            v.euler[i] = euler_amp * rng.vec3(-1, 1)
+    return v
+
+
+def test_active_set_bit_exact(ctx):
+    v = Volume((20, 20, 20), 0.05, (-0.475, -0.475, 1.0))
+    from tests.fixtures import sphere_tsdf
+    sphere_tsdf(v, v.origin + 0.475, 0.31)
+    v.weight[::7] = 0  # unobserved corners
+    ref = v.copy()
+    exp = O.compute_active_set(ref)
+    ctx.upload_volume(v)
+    got = ctx.compute_active_set()
+    assert np.array_equal(got, exp)
+    ctx.download_volume(v)
+    assert np.array_equal(v.active, ref.active)
+    # grow-only
+    v.tsdf += np.float32(0.05)
+    ref.tsdf += np.float32(0.05)
+    ctx.upload_volume(v)
+    assert np.array_equal(ctx.compute_active_set(), O.compute_active_set(ref))
+
+
+def test_normal_equations_match_reference_layout(ctx):
+    v = jittered_sphere(euler_amp=0.05)
+    cons = np.concatenate([rigid_motion_constraints(v, np.eye(3), (0.01, 0, 0)),
+                           random_dense_constraints(v, 150, seed=3)])
+    p = SolverParams.make()
+    pose = Pose.make(O.euler_to_matrix((0.01, -0.02, 0.03)), (0.01, 0.0, -0.02))
+    ref = O.NormalEquations(v, pose, cons, p)
+    ctx.upload_volume(v)
+    ctx.upload_constraints(cons)
+    got = ctx.build_normal_equations(pose, p)
+    assert np.array_equal(got["rows"], ref.rows)
+    assert np.array_equal(got["node_row"], ref.node_row)
+    assert np.array_equal(got["cols"], ref.cols)
+    assert np.array_equal(got["frozen"], ref.frozen)
+    scale = np.max(np.abs(ref.blocks))
+    assert np.max(np.abs(got["blocks"] - ref.blocks)) <= 1e-12 * scale
+    assert np.max(np.abs(got["rhs"] - ref.rhs)) <= 1e-12 * np.max(np.abs(ref.rhs))
+
+
+def test_frozen_component_detection(ctx):
+    # two disjoint shells; constraints only on one -> the other is frozen
+    v = Volume((24, 12, 12), 0.05, (0, 0, 1.0))
+    c = v.canonical_positions()
+    d1 = np.linalg.norm(c - (0.275, 0.275, 1.275), axis=1) - 0.15
+    d2 = np.linalg.norm(c - (0.875, 0.275, 1.275), axis=1) - 0.15
+    v.tsdf[:] = np.minimum(d1, d2).astype(np.float32)
+    v.weight[:] = 1
+    O.compute_active_set(v)
+    cons = node_constraints(v, 3, lambda x: x + 0.01)
+    cons = cons[cons["canonical"][:, 0] < 0.55]
+    ref = O.NormalEquations(v, Pose.make(), cons, SolverParams.make())
+    assert 0 < ref.frozen.sum() < ref.num_rows
+    ctx.upload_volume(v)
+    ctx.upload_constraints(cons)
+    got = ctx.build_normal_equations(Pose.make(), SolverParams.make())
+    assert np.array_equal(got["frozen"], ref.frozen)
+
+
+def test_assembled_pcg_and_multiply(ctx):
+    v = active_sphere_volume(8, 0.07)
+    r = O.euler_to_matrix((0.02, -0.03, 0.05))
+    cons = rigid_motion_constraints(v, r, (0.02, -0.01, 0.005))
+    ref = O.NormalEquations(v, Pose.make(), cons, SolverParams.make())
+    x = np.random.default_rng(1).uniform(-1, 1, (ref.num_rows, 3))
+    y = ctx.ne_multiply(ref.blocks, ref.cols, x)
+    assert np.max(np.abs(y - ref.multiply(x))) <= 1e-12 * np.max(np.abs(y))
+    # PCG against a dense solve (test_solver.cpp:98-130)
+    xg, it, res = ctx.pcg_solve(ref.blocks, ref.cols, ref.rhs, np.zeros((ref.num_rows, 3)), 1e-12, 4000)
+    n = ref.num_rows
+    a = np.zeros((3 * n, 3 * n))
+    e = np.zeros((n, 3))
+    for j in range(3 * n):
+        e[j // 3, j % 3] = 1
+        a[:, j] = ref.multiply(e).reshape(-1)
+        e[j // 3, j % 3] = 0
+    xd = np.linalg.solve(a, ref.rhs.reshape(-1))
+    assert np.sqrt(np.sum((xg.reshape(-1) - xd) ** 2) / np.sum(xd ** 2)) < 1e-8
+    xo, ito, reso = ref.pcg_solve(np.zeros((n, 3)), 1e-12, 4000)
+    assert abs(it - ito) <= 2
+
+
+def test_energy_parity(ctx):
+    v = jittered_sphere(euler_amp=0.1)
+    cons = np.concatenate([rigid_motion_constraints(v, np.eye(3), (0.01, 0, 0)),
+                           random_dense_constraints(v, 200, seed=4)])
+    p = SolverParams.make()
+    pose = Pose.make(O.euler_to_matrix((0.01, 0.0, 0.02)), (0.0, 0.01, 0.0))
+    exp = O.evaluate_energy(v, pose, cons, p)
+    ctx.upload_volume(v)
+    ctx.upload_constraints(cons)
+    got = ctx.evaluate_energy(pose, p)
+    for k in ("total", "sparse", "dense", "reg"):
+        assert got[k] == pytest.approx(exp[k], rel=1e-11, abs=1e-300)
+
+
+def test_energy_identity_field_is_zero(ctx):  # test_solver.cpp:213-221
+    v = active_sphere_volume()
+    cons = rigid_motion_constraints(v, np.eye(3), np.zeros(3))
+    ctx.upload_volume(v)
+    ctx.upload_constraints(cons)
+    e = ctx.evaluate_energy(Pose.make(), SolverParams.make())
+    assert e["reg"] == 0.0 and e["total"] < 1e-28
+
+
+def test_energy_rejects_inactive_anchor(ctx):  # solver.cpp:352-353
+    from paper_1603_08161_b200.wfk import WfkError
+    v = active_sphere_volume()
+    cons = rigid_motion_constraints(v, np.eye(3), np.zeros(3))
+    v.active[cons["anchor_index"][0][0]] = 0
+    ctx.upload_volume(v)
+    ctx.upload_constraints(cons)
+    with pytest.raises(WfkError) as ei:
+        ctx.evaluate_energy(Pose.make(), SolverParams.make())
+    assert ei.value.code == -3
+
+
+def test_bad_anchor_layout_rejected(ctx):
+    from paper_1603_08161_b200.wfk import WfkError
+    v = active_sphere_volume()
+    cons = rigid_motion_constraints(v, np.eye(3), np.zeros(3)).copy()
+    ctx.upload_volume(v)
+    bad = cons[:1].copy()
+    bad["anchor_index"][0][3] += 1
+    with pytest.raises(WfkError) as ei:
+        ctx.upload_constraints(bad)
+    assert ei.value.code == -1
+    bad = cons[:1].copy()
+    bad["anchor_index"][0][:] = v.num_points + 5
+    with pytest.raises(WfkError) as ei:
+        ctx.upload_constraints(bad)
+    assert ei.value.code == -2
+
+
+def test_update_rotations_parity(ctx):
+    v = jittered_sphere(amp=0.01)
+    r = O.euler_to_matrix((0.3, -0.2, 0.5))
+    v.deformed[:] = (v.canonical_positions() + np.random.default_rng(2).uniform(-0.003, 0.003, (v.num_points, 3))) @ r.T
+    ref = v.copy()
+    O.update_rotations(ref)
+    ctx.upload_volume(v)
+    ctx.update_rotations()
+    ctx.download_volume(v)
+    act = v.active.astype(bool)
+    d = np.abs(v.euler[act] - ref.euler[act])
+    assert np.max(d) < 1e-11
+    assert np.array_equal(v.euler[~act], ref.euler[~act])
+
+
+def test_rotation_fit_recovers_rigid_motion(ctx):  # test_solver.cpp:144-162
+    v = active_sphere_volume()
+    r = O.euler_to_matrix((0.3, -0.2, 0.5))
+    v.deformed[:] = v.canonical_positions() @ r.T + (0.1, 0.05, -0.07)
+    ctx.upload_volume(v)
+    ctx.update_rotations()
+    ctx.download_volume(v)
+    for i in np.nonzero(v.active)[0]:
+        assert np.linalg.norm(O.euler_to_matrix(v.euler[i]) - r) < 1e-12
+
+
+def compare_solves(v_gpu, v_ref, trace_gpu, trace_ref):
+    assert len(trace_gpu) == len(trace_ref)
+    for a, b in zip(trace_gpu, trace_ref):
+        assert a["level"] == b["level"] and a["iteration"] == b["iteration"]
+        assert a["energy"]["total"] == pytest.approx(b["energy"]["total"], rel=ENERGY_RTOL)
+        assert a["anomaly"] == b["anomaly"]
+    act = v_ref.active.astype(bool)
+    assert np.array_equal(v_gpu.active, v_ref.active)
+    dev = np.max(np.linalg.norm(v_gpu.deformed[act] - v_ref.deformed[act], axis=1)) / v_ref.voxel_size
+    assert dev <= POS_TOL_VOXEL, dev
+
+
+def test_flip_flop_parity(ctx):
+    v = jittered_sphere(amp=0.015, seed=24)
+    r = O.euler_to_matrix((0.05, -0.08, 0.1))
+    t = np.array([0.02, 0.01, -0.015])
+    cons = np.concatenate([rigid_motion_constraints(v, r, t), random_dense_constraints(v, 300, seed=5)])
+    p = SolverParams.make(flip_flop_iters=6, flip_flop_rel_tol=0.0)
+    ref = v.copy()
+    tr = O.flip_flop_solve(ref, Pose.make(), cons, p)
+    ctx.upload_volume(v)
+    ctx.upload_constraints(cons)
+    tg = ctx.flip_flop_solve(Pose.make(), p)
+    ctx.download_volume(v)
+    compare_solves(v, ref, tg, tr)
+    # the descent property of test_solver.cpp:224-251
+    for a, b in zip(tg, tg[1:]):
+        assert b["energy"]["total"] <= a["energy"]["total"] * (1 + 1e-9)
+
+
+def test_flip_flop_defaults_parity(ctx):
+    v = jittered_sphere(n=16, voxel=0.04, amp=0.01, seed=7, euler_amp=0.02)
+    cons = random_dense_constraints(v, 600, seed=8, normal_jitter=0.5)
+    p = SolverParams.make()
+    ref = v.copy()
+    tr = O.flip_flop_solve(ref, Pose.make(), cons, p)
+    ctx.upload_volume(v)
+    ctx.upload_constraints(cons)
+    tg = ctx.flip_flop_solve(Pose.make(), p)
+    ctx.download_volume(v)
+    compare_solves(v, ref, tg, tr)
+
+
+def test_hierarchy_shape(ctx):  # test_solver.cpp:253-262
+    v = active_sphere_volume()
+    cons = rigid_motion_constraints(v, O.euler_to_matrix((0, 0.06, -0.04)), (0.015, -0.01, 0.02))
+    dims_ref, act_ref, _ = O.hierarchy_info(v, cons, 3)
+    ctx.upload_volume(v)
+    ctx.upload_constraints(cons)
+    dims, act = ctx.hierarchy_info(3)
+    assert np.array_equal(dims, dims_ref)
+    assert np.array_equal(act, act_ref)
+
+
+def test_coarse_to_fine_parity(ctx):  # test_solver.cpp:253-272
+    v = active_sphere_volume()
+    r = O.euler_to_matrix((0, 0.06, -0.04))
+    t = np.array([0.015, -0.01, 0.02])
+    cons = rigid_motion_constraints(v, r, t)
+    p = SolverParams.make(flip_flop_iters=20, pcg_tol=1e-8, pcg_max_iters=500)
+    ref = v.copy()
+    tr = O.solve_coarse_to_fine(ref, Pose.make(), cons, p)
+    ctx.upload_volume(v)
+    ctx.upload_constraints(cons)
+    tg = ctx.solve_coarse_to_fine(Pose.make(), p)
+    ctx.download_volume(v)
+    compare_solves(v, ref, tg, tr)
+    for c in cons:
+        assert np.linalg.norm(O.warp_point(v, Pose.make(), c["canonical"]) - c["target"]) < 1e-3
+
+
+def test_coarse_to_fine_bench_fixture(ctx):
+    # kernel_bench.cpp:15-29 fixture with dense constraints, default params
+    v = make_volume(32)
+    cons = random_dense_constraints(v, 2000, seed=9)
+    p = SolverParams.make()
+    pose = Pose.make(O.euler_to_matrix((0.0, 0.01, 0.0)), (0.005, 0, 0))
+    ref = v.copy()
+    tr = O.solve_coarse_to_fine(ref, pose, cons, p)
+    ctx.upload_volume(v)
+    ctx.upload_constraints(cons)
+    tg = ctx.solve_coarse_to_fine(pose, p)
+    ctx.download_volume(v)
+    compare_solves(v, ref, tg, tr)
+
+
+def test_solve_is_deterministic(ctx):
+    v = jittered_sphere(amp=0.015, seed=24)
+    cons = random_dense_constraints(v, 300, seed=5)
+    p = SolverParams.make()
+    out = []
+    for _ in range(2):
+        w = v.copy()
+        ctx.upload_volume(w)
+        ctx.upload_constraints(cons)
+        tr = ctx.solve_coarse_to_fine(Pose.make(), p)
+        ctx.download_volume(w)
+        out.append((w.deformed.copy(), w.euler.copy(), [e["energy"]["total"] for e in tr]))
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1])
+    assert out[0][2] == out[1][2]
