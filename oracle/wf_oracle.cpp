@@ -2105,3 +2105,116 @@ int wfo_recon_process_frame(wfo_recon* r, const wfk_frame_view* frame, const wfk
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// synthetic test-bed: SyntheticScene::render_frame (synthcam.cpp:252-316) for
+// one sphere under the bend warp (synthcam.cpp:141-147, 164-201) with the Dots
+// texture (synthcam.cpp:98-112).  Used only to make benchmark inputs for the
+// CPU reference arm.
+// ---------------------------------------------------------------------------
+namespace {
+M3 axis_unit(int axis, double ang) {
+  M3 r = M3::identity();
+  const double c = std::cos(ang), s = std::sin(ang);
+  if (axis == 0) { r.a[1][1] = c; r.a[1][2] = -s; r.a[2][1] = s; r.a[2][2] = c; }
+  else if (axis == 1) { r.a[0][0] = c; r.a[0][2] = s; r.a[2][0] = -s; r.a[2][2] = c; }
+  else { r.a[0][0] = c; r.a[0][1] = -s; r.a[1][0] = s; r.a[1][1] = c; }
+  return r;
+}
+uint64_t smix(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+uint64_t hcell(int64_t x, int64_t y, int64_t z, uint32_t seed) {
+  uint64_t h = seed;
+  h = smix(h ^ uint64_t(x));
+  h = smix(h ^ uint64_t(y));
+  h = smix(h ^ uint64_t(z));
+  return h;
+}
+double r01(uint64_t h) { return double(h >> 11) * (1.0 / 9007199254740992.0); }
+}  // namespace
+
+extern "C" int wfo_synth_render(const double center[3], double radius, const double pivot[3], double amplitude,
+                                int driver_axis, int rot_axis, uint32_t tex_seed, double tex_scale,
+                                double dot_radius, const wfk_intrinsics* K, float* depth, float* color) {
+  const V3 c0{center[0], center[1], center[2]}, pv{pivot[0], pivot[1], pivot[2]};
+  auto inverse_warp = [&](const V3& world) {
+    if (amplitude == 0) return world;
+    const V3 p = world - pv;
+    auto g = [&](double s) { return (transpose(axis_unit(rot_axis, amplitude * s)) * p)[driver_axis] - s; };
+    double s = p[driver_axis];
+    bool ok = false;
+    for (int it = 0; it < 50; ++it) {
+      const double gs = g(s);
+      if (std::abs(gs) < 1e-12) { ok = true; break; }
+      const double h = 1e-7;
+      const double dg = (g(s + h) - g(s - h)) / (2 * h);
+      if (std::abs(dg) < 1e-12) break;
+      s -= gs / dg;
+    }
+    if (!ok && std::abs(g(s)) > 1e-10) {
+      double lo = -(norm(p) + 1), hi = norm(p) + 1;
+      for (int it = 0; it < 200; ++it) {
+        const double mid = 0.5 * (lo + hi);
+        if (g(lo) * g(mid) <= 0) hi = mid; else lo = mid;
+      }
+      s = 0.5 * (lo + hi);
+    }
+    return pv + axis_unit(rot_axis, -amplitude * s) * p;
+  };
+  const int W = K->width, H = K->height;
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int y = 0; y < H; ++y)
+    for (int x = 0; x < W; ++x) {
+      const size_t i = size_t(y) * size_t(W) + size_t(x);
+      depth[i] = 0.f;
+      color[3 * i] = color[3 * i + 1] = color[3 * i + 2] = 0.f;
+      const V3 dir = normalized(V3{(double(x) - K->cx) / K->fx, (double(y) - K->cy) / K->fy, 1.0});
+      auto field = [&](double t) { return norm(inverse_warp(t * dir) - c0) - radius; };
+      double t = 0.05, f = field(t);
+      if (f <= 0) continue;
+      double hit = -1;
+      for (int it = 0; it < 2000 && t < 6.0; ++it) {
+        const double step = std::clamp(0.7 * f, 5e-5, 0.25);
+        const double tn = t + step;
+        const double fn = field(tn);
+        if (fn <= 1e-7) {
+          if (fn < 0) {
+            double lo = t, hi = tn;
+            for (int b = 0; b < 60; ++b) {
+              const double mid = 0.5 * (lo + hi);
+              if (field(mid) > 0) lo = mid; else hi = mid;
+            }
+            hit = 0.5 * (lo + hi);
+          } else {
+            hit = tn;
+          }
+          break;
+        }
+        t = tn;
+        f = fn;
+      }
+      if (hit < 0) continue;
+      const V3 pc = hit * dir;
+      depth[i] = float(pc.z);
+      const V3 can = inverse_warp(pc);
+      const V3 cell = can / tex_scale;
+      const V3 fl{std::floor(cell.x), std::floor(cell.y), std::floor(cell.z)};
+      const uint64_t h = hcell(int64_t(fl.x), int64_t(fl.y), int64_t(fl.z), tex_seed);
+      const double margin = dot_radius + 0.05;
+      const V3 jit{margin + r01(h) * (1 - 2 * margin), margin + r01(smix(h)) * (1 - 2 * margin),
+                   margin + r01(smix(smix(h))) * (1 - 2 * margin)};
+      if (norm(cell - (fl + jit)) < dot_radius) {
+        const uint64_t hc = smix(h ^ 0xd0d5u);
+        color[3 * i] = 20 + 160 * float(r01(hc));
+        color[3 * i + 1] = 20 + 160 * float(r01(smix(hc)));
+        color[3 * i + 2] = 20 + 160 * float(r01(smix(smix(hc))));
+      } else {
+        color[3 * i] = color[3 * i + 1] = color[3 * i + 2] = 210.f;
+      }
+    }
+  return WFK_OK;
+}
