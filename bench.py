@@ -1,0 +1,437 @@
+#!/usr/bin/env python
+"""Benchmark of the VolumeDeform hot path on B200 (BASELINE.json metric:
+"non-rigid solve ms/frame & PCG iters/s at named lattice; HBM GB/s vs peak").
+
+Workload (BASELINE.json configs[2], concrete form in SURVEY.md 8(d) row 3):
+640x480 depth, 128^3 deformation lattice, 3-level coarse-to-fine flip-flop
+solve + deformed-TSDF fusion + association ("raycast") per frame, on a synthetic
+deforming sphere (r 0.3 m at z 1.2 m, bend 2.0 rad/m oscillating with
+frequency 2 over a 300-frame sequence).  One step = one
+Reconstructor::process_frame (pipeline.cpp:143-262) with the reference's
+default solver / correspondence / fusion parameters and 3 re-associations.
+The ICP global pose and the SIFT feature front-end are outside the scope of
+this path and are off in both arms.
+
+  python bench.py [--gpus N --steps K --warmup W]        B200 arm (libwfk.so)
+  python bench.py --impl reference [...]                  CPU arm (the oracle port)
+
+Frame 0 bootstraps the volume (untimed); W warm-up frames follow; K frames
+are timed.  `value` times K frames whose inputs are staged in HBM beforehand;
+`e2e` re-runs the same K frames from the same checkpointed volume through
+wfk_process_frame with pinned HOST frame buffers (H2D of depth + color and
+the D2H of the frame record inside the timed region).  L2 is flushed (256 MB
+write) before every timed frame.  All times are CUDA events on the context's
+stream.  With --gpus N > 1 (torchrun) every rank runs an independent replica
+(the 128^3 path does not shard) and the timing is the max over
+ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "non-rigid solve ms/frame & PCG iters/s at named lattice; HBM GB/s vs peak"
+N_LATTICE = 128
+W_PX, H_PX = 640, 480
+FX, FY, CX, CY = 560.0, 560.0, 319.5, 239.5
+FRAMES_TOTAL = 300
+AMPLITUDE = 2.0
+FREQUENCY = 2.0
+
+
+def log(*a):
+    print("[bench]", *a, file=sys.stderr, flush=True)
+
+
+def workload_config(n_gpus):
+    return {
+        "workload": "VolumeDeform per-frame hot path, BASELINE configs[2]: 640x480 depth, 128^3 lattice, "
+                    "3-level coarse-to-fine flip-flop GN/PCG + deformed-TSDF fusion + association",
+        "lattice": [N_LATTICE] * 3,
+        "depth_resolution": [W_PX, H_PX],
+        "levels": 3, "flip_flop_iters": 4, "pcg_tol": 1e-4, "pcg_max_iters": 50, "reassociations": 3,
+        "scene": "sphere r=0.3 m @ z=1.2 m, bend 2.0 rad/m, oscillating freq 2 over 300 frames",
+        "icp": "off (out of scope)", "sparse_features": "off (front-end out of scope)",
+        "l2": "flushed (256 MB write) before every timed frame",
+        "parallelism": f"replicas x{n_gpus}" if n_gpus > 1 else "single GPU",
+    }
+
+
+def frame_amplitude(f):
+    # SyntheticScene::warp_phase with frequency > 0 (synthcam.cpp:131-136)
+    return AMPLITUDE * math.sin(2 * math.pi * FREQUENCY * f / FRAMES_TOTAL)
+
+
+def lattice_geometry():
+    voxel = 0.7 / (N_LATTICE - 1)
+    return (N_LATTICE,) * 3, voxel, (-0.35, -0.35, 0.85)
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md "clocks" line)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """dram bytes per flip-flop launch from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_flip_flop.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d
+    except (OSError, ValueError):
+        return None, None
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing (torchrun; replicas only)
+# ---------------------------------------------------------------------------
+class Dist:
+    def __init__(self, n_gpus):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl")
+            self.torch, self.dist = torch, dist
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, x):
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x):
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+def run_b200(args):
+    from paper_1603_08161_b200.abi import Frame, Intrinsics, Pose, SolverParams, Volume
+    from paper_1603_08161_b200.wfk import Context, SynthScene, pinned_array, pipeline_config
+
+    d = Dist(args.gpus)
+    ctx = Context(d.local)
+    K = Intrinsics.make(FX, FY, CX, CY, W_PX, H_PX)
+    n_frames = 1 + args.warmup + args.steps
+
+    # synthetic input sequence, rendered on the device, kept in pinned host memory
+    frames = []
+    for f in range(n_frames):
+        s = SynthScene()
+        s.center[:] = [0.0, 0.0, 1.2]
+        s.radius = 0.3
+        s.pivot[:] = [0.0, 0.0, 1.2]
+        s.amplitude = frame_amplitude(f)
+        s.driver_axis, s.rot_axis = 0, 1
+        s.t_min, s.t_max = 0.05, 6.0
+        s.texture_seed, s.texture_scale, s.dot_radius = 7, 0.06, 0.3
+        depth, color = ctx.synth_render(s, K)
+        pd = pinned_array((H_PX, W_PX), np.float32)
+        pc = pinned_array((H_PX, W_PX, 3), np.float32)
+        pd[:] = depth
+        pc[:] = color
+        frames.append(Frame(K, pd, pc))
+    log(f"rendered {n_frames} frames; valid depth px of frame 1: {int((frames[min(1, n_frames - 1)].depth > 0).sum())}")
+
+    dims, voxel, origin = lattice_geometry()
+    vol = Volume(dims, voxel, origin)
+    ctx.upload_volume(vol)
+    cfg = pipeline_config(solver=SolverParams.make(), reassociations=3)
+    pose = Pose.make()
+    for f in range(1, n_frames):
+        ctx.stage_frame(f, frames[f])
+
+    log("staged frames")
+    rec0 = ctx.process_frame(frames[0], pose, cfg, 0)  # bootstrap
+    log(f"bootstrap: fused {rec0.fusion.fused}")
+    assert rec0.bootstrap == 1
+    for f in range(1, 1 + args.warmup):
+        ctx.process_staged_frame(f, pose, cfg, f)
+
+    # checkpoint so the e2e pass repeats exactly the same K frames
+    log("warm-up done")
+    ckpt = Volume(dims, voxel, origin)
+    ctx.download_volume(ckpt)
+    timed = list(range(1 + args.warmup, n_frames))
+
+    # ---- value: inputs resident in HBM ---------------------------------------
+    ctx.profile_enable(True)
+    launches0 = ctx.launch_count
+    recs = []
+    total_ms = 0.0
+    d.barrier()
+    with ClockSampler(d.local) as clocks:
+        for f in timed:
+            ctx.flush_l2()
+            ctx.timer_mark(0)
+            recs.append(ctx.process_staged_frame(f, pose, cfg, f))
+            ctx.timer_mark(1)
+            total_ms += ctx.timer_elapsed_ms(0, 1)
+    d.barrier()
+    launches = ctx.launch_count - launches0
+    prof = ctx.profile_read()
+    ctx.profile_enable(False)
+
+    log(f"timed: {total_ms / len(timed):.3f} ms/frame")
+    # ---- e2e: same frames through the public call with host buffers -----------
+    ctx.upload_volume(ckpt)
+    e2e_ms = 0.0
+    d.barrier()
+    for f in timed:
+        ctx.flush_l2()
+        ctx.timer_mark(2)
+        r = ctx.process_frame(frames[f], pose, cfg, f)   # H2D frame + D2H record inside
+        ctx.timer_mark(3)
+        e2e_ms += ctx.timer_elapsed_ms(2, 3)
+        _ = (r.energy.total, r.dense_count)
+    d.barrier()
+
+    k = len(timed)
+    ms_frame = d.max(total_ms) / k
+    e2e_frame = d.max(e2e_ms) / k
+    pcg_iters = sum(r.pcg_iterations for r in recs)
+    pcg_iters_all = d.sum(pcg_iters)
+    peak, peak_src = measured_peak()
+    achieved = prof.flip_flop_bytes / (prof.flip_flop_ms * 1e-3) / 1e9 if prof.flip_flop_ms > 0 else 0.0
+    achieved_impl = prof.flip_flop_bytes_impl / (prof.flip_flop_ms * 1e-3) / 1e9 if prof.flip_flop_ms > 0 else 0.0
+    traffic, ncu_doc = ncu_traffic()
+    clk = clocks.summary()
+
+    cpu = None
+    if d.rank == 0 and d.world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(frames, args.cpu_frames)
+
+    if d.rank == 0:
+        out = {
+            "metric": METRIC,
+            "value": ms_frame / d.world,
+            "unit": "ms/frame",
+            "n_gpus": d.world,
+            "steps": k,
+            "warmup": args.warmup,
+            "ms_per_step": ms_frame,
+            "higher_is_better": False,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (device-rendered deforming sphere sequence)",
+            "config": workload_config(d.world),
+            "pcg_iters_per_s": pcg_iters_all / (d.max(total_ms) * 1e-3),
+            "pcg_iterations_per_frame": pcg_iters / k,
+            "frame_breakdown_ms": {kk: v / k for kk, v in prof.as_dict()["stage_ms"].items()},
+            "dense_constraints_per_frame": float(np.mean([r.dense_count for r in recs])),
+            "gpu_launches": int(launches),
+            "roofline": {
+                "bound": "hbm",
+                "kernel": "k_flip_flop (cooperative flip-flop solve: energy, rhs/diag, matrix-free Jacobi-PCG, "
+                          "write-back, Procrustes, energy)",
+                "achieved": achieved,
+                "peak": peak,
+                "peak_source": peak_src,
+                "unit": "GB/s",
+                "frac": achieved / peak,
+                "traffic": traffic,
+                "bytes_model": "SURVEY.md 8(d): PCG 160 N + 32 C_d + 20 C_s per iteration, rhs/diag 52 N, "
+                               "rotation 28 N, energy 28 N + 44 C",
+                "achieved_fp64_layout": achieved_impl,
+                "launches": prof.flip_flop_launches,
+                "avg_launch_ms": prof.flip_flop_ms / max(prof.flip_flop_launches, 1),
+                "share_of_frame": prof.flip_flop_ms / max(total_ms, 1e-9),
+            },
+            "e2e": {
+                "value": e2e_frame / d.world,
+                "unit": "ms/frame",
+                "h2d_bytes_per_step": int(frames[0].depth.nbytes + frames[0].color.nbytes),
+                "d2h_bytes_per_step": int(__import__("ctypes").sizeof(type(recs[0]))),
+            },
+            "clocks": clk,
+        }
+        if cpu is not None:
+            out["cpu_baseline"] = cpu
+        print(json.dumps(out), flush=True)
+    ctx.close()
+    d.close()
+
+
+def cpu_baseline_sample(frames, n_frames):
+    """The oracle port on this host's cores, frames 1..n of the same sequence
+    after the (untimed) bootstrap frame 0; reports the median ms/frame."""
+    from oracle import pyoracle as O
+    from paper_1603_08161_b200.abi import SolverParams
+    dims, voxel, origin = lattice_geometry()
+    rec = O.Reconstructor(dims, voxel, origin, solver=SolverParams.make(), reassociations=3)
+    rec.process_frame(frames[0])
+    times = []
+    for f in range(1, 1 + n_frames):
+        t0 = time.perf_counter()
+        rec.process_frame(frames[f])
+        times.append((time.perf_counter() - t0) * 1e3)
+    return {"value": float(np.median(times)), "unit": "ms/frame", "cores": int(O.lib().wfo_num_threads()),
+            "kind": "port",
+            "sample": f"oracle Reconstructor, frames 1..{n_frames} of the same sequence after the bootstrap "
+                      f"frame (median of {n_frames}), OpenMP threads = {int(O.lib().wfo_num_threads())}"}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the CPU implementation of the path (oracle port) on this host
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    from oracle import pyoracle as O
+    from paper_1603_08161_b200.abi import Frame, Intrinsics, SolverParams
+    K = Intrinsics.make(FX, FY, CX, CY, W_PX, H_PX)
+    n_frames = 1 + args.warmup + args.steps
+    frames = []
+    for f in range(n_frames):
+        depth, color = O.synth_render(K, amplitude=frame_amplitude(f))
+        frames.append(Frame(K, depth, color))
+    dims, voxel, origin = lattice_geometry()
+    rec = O.Reconstructor(dims, voxel, origin, solver=SolverParams.make(), reassociations=3)
+    rec.process_frame(frames[0])
+    for f in range(1, 1 + args.warmup):
+        rec.process_frame(frames[f])
+    t0 = time.perf_counter()
+    pcg = 0
+    for f in range(1 + args.warmup, n_frames):
+        r = rec.process_frame(frames[f])
+        pcg += r.pcg_iterations
+    dt = time.perf_counter() - t0
+    ms = dt * 1e3 / args.steps
+    cores = int(O.lib().wfo_num_threads())
+    out = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": ms,
+        "unit": "ms/frame",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (CPU-rendered deforming sphere sequence)",
+        "config": workload_config(1),
+        "pcg_iters_per_s": pcg / dt,
+        "cpu_baseline": {"value": ms, "unit": "ms/frame", "cores": cores, "kind": "port",
+                         "sample": f"oracle port of the reference path (oracle/wf_oracle.cpp, OpenMP {cores} "
+                                   f"threads), {args.steps} full frames after bootstrap + {args.warmup} warm-up"},
+        "e2e": {"value": ms, "unit": "ms/frame", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-frames", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        print("warning: W >= 3 warm-up steps are required for a valid number", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -175,6 +175,37 @@ int wfk_process_frame(wfk_ctx* ctx, const wfk_frame_view* frame, const wfk_pose*
                       const wfk_pipeline_config* cfg, const wfk_correspondence* sparse,
                       int64_t nsparse, int32_t frame_index, wfk_frame_record* rec);
 
+/* Stage a frame in device memory (slot >= 0), then run the per-frame path on it
+ * with no host->device traffic (HBM-resident benchmark inputs). */
+int wfk_frame_stage(wfk_ctx* ctx, int32_t slot, const wfk_frame_view* frame);
+int wfk_process_staged_frame(wfk_ctx* ctx, int32_t slot, const wfk_pose* pose,
+                             const wfk_pipeline_config* cfg, const wfk_correspondence* sparse,
+                             int64_t nsparse, int32_t frame_index, wfk_frame_record* rec);
+
+/* ---- measurement --------------------------------------------------------------
+ * Device-event profiling of the context's stream: every flip-flop kernel
+ * launch (the dominant kernel) with its algorithmic bytes, and the stages of
+ * wfk_process_frame.  Enabling resets the counters. */
+typedef struct wfk_profile {
+  int64_t flip_flop_launches;
+  int64_t pcg_iterations;
+  double flip_flop_ms;          /* summed CUDA-event durations of the launches */
+  double flip_flop_bytes;       /* algorithmic bytes, SURVEY.md 8(d) model */
+  double flip_flop_bytes_impl;  /* algorithmic bytes of the fp64 layout */
+  double stage_ms[8];           /* maps+mesh+raster, associate, solve, redeform, fuse, frame */
+  int64_t launches;             /* kernel launches so far */
+} wfk_profile;
+int wfk_profile_enable(wfk_ctx* ctx, int32_t on);
+int wfk_profile_read(wfk_ctx* ctx, wfk_profile* out);
+/* CUDA events on the context's stream (16 slots) */
+int wfk_timer_mark(wfk_ctx* ctx, int32_t slot);
+int wfk_timer_elapsed_ms(wfk_ctx* ctx, int32_t a, int32_t b, double* ms);
+/* write 256 MB on the context's stream so the next call starts with a cold L2 */
+int wfk_flush_l2(wfk_ctx* ctx);
+/* page-locked host memory for frame buffers (cudaMallocHost) */
+int wfk_host_alloc(size_t bytes, void** out);
+void wfk_host_free(void* p);
+
 /* ---- synthetic test-bed (NOT the hot path) --------------------------------------
  * Sphere-traced depth + color of a sphere under the reference's bend warp
  * (synthcam.cpp:141-159, 252-316), rendered on the device for benchmarks. */

@@ -422,6 +422,23 @@ def extract_mesh(vol, pose=None) -> Mesh:
     return Mesh(h)
 
 
+def synth_render(intr, center=(0.0, 0.0, 1.2), radius=0.3, pivot=(0.0, 0.0, 1.2), amplitude=0.0,
+                 driver_axis=0, rot_axis=1, tex_seed=7, tex_scale=0.06, dot_radius=0.3):
+    """SyntheticScene::render_frame for a sphere under the bend warp (test-bed)."""
+    depth = np.zeros((intr.height, intr.width), np.float32)
+    color = np.zeros((intr.height, intr.width, 3), np.float32)
+    c = np.asarray(center, np.float64).copy()
+    pv = np.asarray(pivot, np.float64).copy()
+    l = lib()
+    l.wfo_synth_render.argtypes = [C.POINTER(C.c_double), C.c_double, C.POINTER(C.c_double), C.c_double,
+                                   C.c_int, C.c_int, C.c_uint32, C.c_double, C.c_double,
+                                   C.POINTER(Intrinsics), C.c_void_p, C.c_void_p]
+    _check(l.wfo_synth_render(ptr(c, C.c_double), radius, ptr(pv, C.c_double), amplitude, driver_axis,
+                              rot_axis, tex_seed, tex_scale, dot_radius, C.byref(intr), _cptr(depth),
+                              _cptr(color)))
+    return depth, color
+
+
 # --- per-frame pipeline (pipeline.cpp:143-262, hot-path subset) -------------------
 class ReconConfig(C.Structure):
     _fields_ = [("dims", C.c_int32 * 3), ("reassociations", C.c_int32), ("voxel_size", C.c_double),

@@ -112,7 +112,17 @@ void upload_constraints(wfk_ctx* c, const wfk_correspondence* h, int64_t n, bool
     WFK_CUDA(cudaMemcpyAsync(ci.conf.p + base, conf.data(), size_t(m) * 8, cudaMemcpyHostToDevice, s));
   }
   WFK_CUDA(cudaStreamSynchronize(s));  // host staging vectors die on return
+  int64_t ns = 0;
+  for (int32_t k : kind) ns += k == WFK_SPARSE_POINT ? 1 : 0;
+  ci.n_sparse = (append ? ci.n_sparse : 0) + ns;
   ci.count = total;
+}
+
+void run_frame(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose* pose, const wfk_pipeline_config* cfg,
+               const wfk_correspondence* sparse, int64_t nsparse, int32_t frame_index, wfk_frame_record* rec);
+
+void stage_mark(wfk_ctx* c, int k) {
+  if (c->prof.on) WFK_CUDA(cudaEventRecord(c->prof.ev[2 + k], c->stream));
 }
 
 }  // namespace
@@ -137,6 +147,8 @@ int wfk_create(const wfk_config* cfg, wfk_ctx** out) {
     c->num_sms = prop.multiProcessorCount;
     WFK_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     WFK_CUDA(cudaMallocHost(&c->h_pinned, 4096));
+    for (cudaEvent_t& e : c->prof.ev) WFK_CUDA(cudaEventCreate(&e));
+    for (cudaEvent_t& e : c->prof.timer) WFK_CUDA(cudaEventCreate(&e));
   } catch (const Error& e) {
     delete c;
     return e.code;
@@ -150,6 +162,14 @@ void wfk_destroy(wfk_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
+  for (cudaEvent_t e : c->prof.ev)
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->prof.timer)
+    if (e) cudaEventDestroy(e);
+  for (float* p : c->staged_depth)
+    if (p) cudaFree(p);
+  for (float* p : c->staged_color)
+    if (p) cudaFree(p);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -350,12 +370,12 @@ int wfk_frame_upload(wfk_ctx* c, const wfk_frame_view* f) {
     FrameDev& d = c->frame;
     const size_t npx = size_t(K.width) * size_t(K.height);
     d.K = K;
-    d.depth.ensure(npx);
-    WFK_CUDA(cudaMemcpyAsync(d.depth, f->depth, npx * 4, cudaMemcpyHostToDevice, c->stream));
+    d.depth = d.depth_buf.ensure(npx);
+    WFK_CUDA(cudaMemcpyAsync(d.depth_buf.p, f->depth, npx * 4, cudaMemcpyHostToDevice, c->stream));
     d.has_color = f->color != nullptr;
     if (d.has_color) {
-      d.color.ensure(3 * npx);
-      WFK_CUDA(cudaMemcpyAsync(d.color, f->color, 3 * npx * 4, cudaMemcpyHostToDevice, c->stream));
+      d.color = d.color_buf.ensure(3 * npx);
+      WFK_CUDA(cudaMemcpyAsync(d.color_buf.p, f->color, 3 * npx * 4, cudaMemcpyHostToDevice, c->stream));
     }
     d.maps_valid = false;
     WFK_CUDA(cudaStreamSynchronize(c->stream));
@@ -499,6 +519,45 @@ int wfk_process_frame(wfk_ctx* c, const wfk_frame_view* frame, const wfk_pose* p
     if (!c->vol.valid) throw Error(WFK_E_INVALID_ARG, "no volume uploaded");
     std::memset(rec, 0, sizeof(*rec));
     const wfk_intrinsics& K = frame->intrinsics;
+    run_frame(c, K, pose, cfg, sparse, nsparse, frame_index, rec);
+  });
+}
+
+// frame already on the device (wfk_frame_stage slot)
+int wfk_process_staged_frame(wfk_ctx* c, int32_t slot, const wfk_pose* pose, const wfk_pipeline_config* cfg,
+                             const wfk_correspondence* sparse, int64_t nsparse, int32_t frame_index,
+                             wfk_frame_record* rec) {
+  return guard(c, [&] {
+    if (!cfg || !rec) throw Error(WFK_E_INVALID_ARG, "null argument");
+    if (!c->vol.valid) throw Error(WFK_E_INVALID_ARG, "no volume uploaded");
+    if (slot < 0 || size_t(slot) >= c->staged_depth.size() || !c->staged_depth[size_t(slot)])
+      throw Error(WFK_E_INVALID_ARG, "no frame staged in this slot");
+    FrameDev& d = c->frame;
+    d.K = c->staged_K[size_t(slot)];
+    d.depth = c->staged_depth[size_t(slot)];
+    d.color = c->staged_color[size_t(slot)];
+    d.has_color = d.color != nullptr;
+    d.maps_valid = false;
+    std::memset(rec, 0, sizeof(*rec));
+    run_frame(c, d.K, pose, cfg, sparse, nsparse, frame_index, rec);
+  });
+}
+
+}  // extern "C"
+
+namespace {
+void run_frame(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose* pose, const wfk_pipeline_config* cfg,
+               const wfk_correspondence* sparse, int64_t nsparse, int32_t frame_index, wfk_frame_record* rec) {
+    Prof& pf = c->prof;
+    double stage[kStages] = {0, 0, 0, 0, 0, 0};
+    auto lap = [&](int k, int a, int b) {
+      if (!pf.on) return;
+      WFK_CUDA(cudaEventSynchronize(pf.ev[2 + b]));
+      float ms = 0;
+      WFK_CUDA(cudaEventElapsedTime(&ms, pf.ev[2 + a], pf.ev[2 + b]));
+      stage[k] += ms;
+    };
+    stage_mark(c, 0);
     assoc_backproject(c, nullptr);
     if (frame_index == 0) {  // pipeline.cpp:150-159
       wfk_fusion_params boot = cfg->fusion;
@@ -513,17 +572,24 @@ int wfk_process_frame(wfk_ctx* c, const wfk_frame_view* frame, const wfk_pose* p
     if (nt == 0) throw Error(WFK_E_LOGIC, "empty isosurface before frame");
     assoc_compute_normals(c);
     assoc_rasterize(c, K, nullptr);
+    stage_mark(c, 1);
+    lap(0, 0, 1);
     std::vector<wfk_trace_entry> trace;
     for (int outer = 0; outer < cfg->reassociations; ++outer) {  // pipeline.cpp:226-247
+      stage_mark(c, 2);
       int64_t nd = 0;
       assoc_find_dense(c, K, cfg->correspond, true, &nd);
       rec->dense_count = int32_t(nd);
       int64_t kept = 0;
       if (nsparse > 0) upload_constraints(c, sparse, nsparse, true, true, &kept);
       rec->sparse_count = int32_t(kept);
+      stage_mark(c, 3);
+      lap(1, 2, 3);
       if (c->cons.count == 0) break;
       trace.clear();
       solver_c2f(c, pose, cfg->solver, trace);
+      stage_mark(c, 4);
+      lap(2, 3, 4);
       for (const wfk_trace_entry& e : trace) {
         rec->anomalies += e.anomaly ? 1 : 0;
         rec->pcg_iterations += e.pcg_iterations;
@@ -533,18 +599,126 @@ int wfk_process_frame(wfk_ctx* c, const wfk_frame_view* frame, const wfk_pose* p
       assoc_mesh_warp(c, pose);  // redeform (pipeline.cpp:167-172)
       assoc_compute_normals(c);
       assoc_rasterize(c, K, nullptr);
+      stage_mark(c, 5);
+      lap(3, 4, 5);
     }
+    stage_mark(c, 6);
     fusion_advance_active_ages(c);                      // pipeline.cpp:249-252
     fusion_integrate(c, pose, cfg->fusion, &rec->fusion);  // :254
     fusion_expand(c, &rec->expansion);                  // :255
-  });
+    stage_mark(c, 7);
+    lap(4, 6, 7);
+    lap(5, 0, 7);
+    for (int k = 0; k < kStages; ++k) pf.stage_ms[k] += stage[k];
 }
+}  // namespace
+
+extern "C" {
 
 int wfk_synth_render(wfk_ctx* c, const wfk_synth_scene* s, const wfk_intrinsics* intr, float* depth, float* color) {
   return guard(c, [&] {
     if (!s || !intr || !depth) throw Error(WFK_E_INVALID_ARG, "null argument");
     synth_render(c, *s, *intr, depth, color);
   });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int wfk_profile_enable(wfk_ctx* c, int32_t on) {
+  return guard(c, [&] {
+    Prof& p = c->prof;
+    p.on = on != 0;
+    p.ff_launches = p.pcg_iterations = 0;
+    p.ff_ms = p.ff_bytes = p.ff_bytes_impl = 0;
+    for (double& s : p.stage_ms) s = 0;
+  });
+}
+
+int wfk_profile_read(wfk_ctx* c, wfk_profile* out) {
+  return guard(c, [&] {
+    if (!out) throw Error(WFK_E_INVALID_ARG, "null profile");
+    const Prof& p = c->prof;
+    out->flip_flop_launches = p.ff_launches;
+    out->pcg_iterations = p.pcg_iterations;
+    out->flip_flop_ms = p.ff_ms;
+    out->flip_flop_bytes = p.ff_bytes;
+    out->flip_flop_bytes_impl = p.ff_bytes_impl;
+    for (int k = 0; k < 6; ++k) out->stage_ms[k] = p.stage_ms[k];
+    out->stage_ms[6] = out->stage_ms[7] = 0;
+    out->launches = c->stats.kernel_launches;
+  });
+}
+
+int wfk_timer_mark(wfk_ctx* c, int32_t slot) {
+  return guard(c, [&] {
+    if (slot < 0 || slot >= 16) throw Error(WFK_E_INVALID_ARG, "timer slot out of range");
+    WFK_CUDA(cudaEventRecord(c->prof.timer[slot], c->stream));
+  });
+}
+
+int wfk_timer_elapsed_ms(wfk_ctx* c, int32_t a, int32_t b, double* ms) {
+  return guard(c, [&] {
+    if (a < 0 || a >= 16 || b < 0 || b >= 16 || !ms) throw Error(WFK_E_INVALID_ARG, "bad timer slots");
+    WFK_CUDA(cudaEventSynchronize(c->prof.timer[b]));
+    float f = 0;
+    WFK_CUDA(cudaEventElapsedTime(&f, c->prof.timer[a], c->prof.timer[b]));
+    *ms = f;
+  });
+}
+
+int wfk_flush_l2(wfk_ctx* c) {
+  return guard(c, [&] {
+    const size_t bytes = size_t(256) << 20;  // 2x the 126 MB L2
+    uint8_t* p = c->l2_flush.ensure(bytes);
+    WFK_CUDA(cudaMemsetAsync(p, c->stats.kernel_launches & 0xff, bytes, c->stream));
+    WFK_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int wfk_frame_stage(wfk_ctx* c, int32_t slot, const wfk_frame_view* f) {
+  return guard(c, [&] {
+    if (slot < 0 || slot > 4096 || !f || !f->depth) throw Error(WFK_E_INVALID_ARG, "bad slot or frame");
+    const wfk_intrinsics& K = f->intrinsics;
+    if (!(K.fx > 0 && K.fy > 0 && K.width > 0 && K.height > 0))
+      throw Error(WFK_E_INVALID_ARG, "frame has invalid intrinsics");
+    const size_t need = size_t(slot) + 1;
+    if (c->staged_depth.size() < need) {
+      c->staged_depth.resize(need, nullptr);
+      c->staged_color.resize(need, nullptr);
+      c->staged_K.resize(need);
+    }
+    const size_t npx = size_t(K.width) * size_t(K.height);
+    float*& d = c->staged_depth[size_t(slot)];
+    float*& col = c->staged_color[size_t(slot)];
+    if (d) cudaFree(d);
+    if (col) cudaFree(col);
+    d = col = nullptr;
+    WFK_CUDA(cudaMalloc(&d, npx * 4));
+    WFK_CUDA(cudaMemcpyAsync(d, f->depth, npx * 4, cudaMemcpyHostToDevice, c->stream));
+    if (f->color) {
+      WFK_CUDA(cudaMalloc(&col, npx * 12));
+      WFK_CUDA(cudaMemcpyAsync(col, f->color, npx * 12, cudaMemcpyHostToDevice, c->stream));
+    }
+    c->staged_K[size_t(slot)] = K;
+    WFK_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int wfk_host_alloc(size_t bytes, void** out) {
+  if (!out) return WFK_E_INVALID_ARG;
+  *out = nullptr;
+  const cudaError_t e = cudaMallocHost(out, bytes ? bytes : 1);
+  return e == cudaSuccess ? WFK_OK : (e == cudaErrorMemoryAllocation ? WFK_E_OOM : WFK_E_CUDA);
+}
+
+void wfk_host_free(void* p) {
+  if (p) cudaFreeHost(p);
 }
 
 }  // extern "C"

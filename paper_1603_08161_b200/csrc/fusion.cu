@@ -193,7 +193,7 @@ void fusion_integrate(wfk_ctx* c, const wfk_pose* pose, const wfk_fusion_params&
   a.pose = pose_dev(pose);
   a.K = c->frame.K;
   a.depth = c->frame.depth;
-  a.color = c->frame.has_color ? c->frame.color.p : nullptr;
+  a.color = c->frame.has_color ? c->frame.color : nullptr;
   a.k_min = p.k_min;
   a.bootstrap = p.bootstrap;
   a.w_max = p.w_max;

@@ -1004,7 +1004,10 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
     return;
   }
   void* args[] = {&a};
+  Prof& pf = c->prof;
+  if (pf.on) WFK_CUDA(cudaEventRecord(pf.ev[0], s));
   WFK_CUDA(cudaLaunchCooperativeKernel((void*)k_flip_flop, dim3(G), dim3(kBlock), args, 0, s));
+  if (pf.on) WFK_CUDA(cudaEventRecord(pf.ev[1], s));
   count_launch(c);
   int32_t st[4];
   double en[4];
@@ -1017,6 +1020,25 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   if (st[1] & 1) throw Error(WFK_E_LOGIC, "evaluate_energy: constraint anchors an inactive point");
   if (e_out) *e_out = wfk_energy{en[0], en[1], en[2], en[3]};
   c->stats.pcg_iterations += st[2];
+  if (pf.on && mode == 0) {
+    float ms = 0;
+    WFK_CUDA(cudaEventElapsedTime(&ms, pf.ev[0], pf.ev[1]));
+    pf.ff_launches += 1;
+    pf.ff_ms += ms;
+    pf.pcg_iterations += st[2];
+    // algorithmic bytes of this launch.  SURVEY.md 8(d): PCG iteration
+    // 160 N + 32 C_d + 20 C_s; rotation fit 28 N; energy 28 N + 44 C;
+    // rhs/diagonal 52 N per flip-flop iteration (+ the initial energy).
+    const double N = L.N, Cs = double(std::min<int64_t>(c->cons.n_sparse, L.C)), Cd = double(L.C) - Cs;
+    const double iters = st[0], pcg = st[2];
+    pf.ff_bytes += pcg * (160 * N + 32 * Cd + 20 * Cs) + iters * (52 * N + 28 * N + 28 * N + 44 * (Cd + Cs)) +
+                   (28 * N + 44 * (Cd + Cs));
+    // the same traffic for this fp64 layout:
+    // 4-phase PCG 365 N + 276 C per iteration; rhs/diag 153 N, write-back 48 N,
+    // rotation fit 201 N, energy 177 N + 232 C per flip-flop iteration.
+    pf.ff_bytes_impl += pcg * (365 * N + 276 * (Cd + Cs)) + iters * ((153 + 48 + 201 + 177) * N + 232 * (Cd + Cs)) +
+                        (177 * N + 232 * (Cd + Cs));
+  }
   if (out && st[0] > 0) {
     const size_t k = out->size();
     out->resize(k + size_t(st[0]));

@@ -78,6 +78,7 @@ struct ConIn {
   DevBuf<double> normal;    // 3C
   DevBuf<double> conf;      // C
   int64_t count = 0;
+  int64_t n_sparse = 0;     // SparsePoint records among them (byte model)
 };
 
 // Per-level solver workspace (one lattice of the coarse-to-fine hierarchy).
@@ -126,7 +127,10 @@ struct VolumeDev {
 struct FrameDev {
   wfk_intrinsics K{};
   bool has_color = false;
-  DevBuf<float> depth, color;
+  DevBuf<float> depth_buf, color_buf;
+  // the frame the kernels read: the upload buffers or a staged slot
+  const float* depth = nullptr;
+  const float* color = nullptr;
   // PointNormalMap (correspond.hpp:34-42)
   DevBuf<double> point, normal;
   DevBuf<uint8_t> pvalid, nvalid;
@@ -167,6 +171,22 @@ struct Stats {
   int64_t kernel_launches = 0;
 };
 
+// Optional device-event profiling (wfk_profile_enable): per-launch duration of
+// the flip-flop kernel with its algorithmic bytes, and per-stage durations of
+// wfk_process_frame.
+constexpr int kStages = 6;  // 0 maps+mesh+raster, 1 associate, 2 solve, 3 redeform, 4 fuse, 5 total
+struct Prof {
+  bool on = false;
+  int64_t ff_launches = 0;
+  int64_t pcg_iterations = 0;
+  double ff_ms = 0;
+  double ff_bytes = 0;       // SURVEY.md 8(d) model (fp32 state, 3-phase PCG)
+  double ff_bytes_impl = 0;  // this implementation's fp64 layout
+  double stage_ms[kStages] = {0, 0, 0, 0, 0, 0};
+  cudaEvent_t ev[2 + 2 * kStages] = {};
+  cudaEvent_t timer[16] = {};
+};
+
 }  // namespace wfk
 
 struct wfk_ctx {
@@ -181,6 +201,11 @@ struct wfk_ctx {
   wfk::MeshDev mesh;
   wfk::GBufDev gbuf;
   wfk::Stats stats;
+  wfk::Prof prof;
+  // frames staged in device memory (wfk_frame_stage)
+  std::vector<wfk_intrinsics> staged_K;
+  std::vector<float*> staged_depth, staged_color;
+  wfk::DevBuf<uint8_t> l2_flush;
   // scratch
   wfk::DevBuf<double> partials;
   wfk::DevBuf<int32_t> flags;   // device status words

@@ -60,6 +60,19 @@ class SynthScene(C.Structure):
                 ("reserved_", C.c_int32), ("texture_scale", C.c_double), ("dot_radius", C.c_double)]
 
 
+class Profile(C.Structure):
+    _fields_ = [("flip_flop_launches", C.c_int64), ("pcg_iterations", C.c_int64), ("flip_flop_ms", C.c_double),
+                ("flip_flop_bytes", C.c_double), ("flip_flop_bytes_impl", C.c_double),
+                ("stage_ms", C.c_double * 8), ("launches", C.c_int64)]
+
+    STAGES = ("maps_mesh_raster", "associate", "solve", "redeform", "fuse", "frame")
+
+    def as_dict(self):
+        d = {f: getattr(self, f) for f, _ in self._fields_ if f != "stage_ms"}
+        d["stage_ms"] = {k: self.stage_ms[i] for i, k in enumerate(self.STAGES)}
+        return d
+
+
 class Config(C.Structure):
     _fields_ = [("device", C.c_int32), ("reserved_", C.c_int32 * 7)]
 
@@ -80,11 +93,43 @@ def lib():
         _lib.wfk_pcg_iteration_count.restype = C.c_int64
         _lib.wfk_pcg_iteration_count.argtypes = [C.c_void_p]
         _lib.wfk_destroy.argtypes = [C.c_void_p]
+        _lib.wfk_host_alloc.argtypes = [C.c_size_t, C.POINTER(C.c_void_p)]
+        _lib.wfk_host_free.argtypes = [C.c_void_p]
+        _lib.wfk_host_free.restype = None
     return _lib
 
 
 def _cptr(a):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+class _Pinned:
+    def __init__(self, nbytes):
+        p = C.c_void_p()
+        rc = lib().wfk_host_alloc(C.c_size_t(nbytes), C.byref(p))
+        if rc != WFK_OK:
+            raise WfkError(rc, "wfk_host_alloc failed")
+        self.p = p
+
+    def __del__(self):
+        if getattr(self, "p", None):
+            lib().wfk_host_free(self.p)
+            self.p = None
+
+
+def pinned_array(shape, dtype) -> np.ndarray:
+    """numpy array over page-locked host memory (wfk_host_alloc)."""
+    dtype = np.dtype(dtype)
+    n = int(np.prod(shape)) * dtype.itemsize
+    buf = _Pinned(n)
+    raw = (C.c_uint8 * n).from_address(buf.p.value)
+    arr = np.frombuffer(raw, dtype=dtype).reshape(shape)
+    arr.setflags(write=True)
+    _PINNED_KEEP.append(buf)  # lifetime tied to the process (bench buffers)
+    return arr
+
+
+_PINNED_KEEP = []
 
 
 class Context:
@@ -325,6 +370,39 @@ class Context:
                                             C.c_int64(0 if s is None else len(s)), C.c_int32(frame_index),
                                             C.byref(rec)))
         return rec
+
+    def stage_frame(self, slot: int, frame):
+        fv = frame.view()
+        self._check(lib().wfk_frame_stage(self.h, C.c_int32(slot), C.byref(fv)))
+
+    def process_staged_frame(self, slot: int, pose: Pose, cfg: PipelineConfig, frame_index: int,
+                             sparse=None) -> FrameRecord:
+        rec = FrameRecord()
+        s = None if sparse is None or len(sparse) == 0 else np.ascontiguousarray(sparse, CORR_DTYPE)
+        self._check(lib().wfk_process_staged_frame(self.h, C.c_int32(slot), C.byref(pose), C.byref(cfg), _cptr(s),
+                                                   C.c_int64(0 if s is None else len(s)),
+                                                   C.c_int32(frame_index), C.byref(rec)))
+        return rec
+
+    # ---- measurement ---------------------------------------------------------
+    def profile_enable(self, on: bool = True):
+        self._check(lib().wfk_profile_enable(self.h, C.c_int32(1 if on else 0)))
+
+    def profile_read(self) -> Profile:
+        p = Profile()
+        self._check(lib().wfk_profile_read(self.h, C.byref(p)))
+        return p
+
+    def timer_mark(self, slot: int):
+        self._check(lib().wfk_timer_mark(self.h, C.c_int32(slot)))
+
+    def timer_elapsed_ms(self, a: int, b: int) -> float:
+        ms = C.c_double()
+        self._check(lib().wfk_timer_elapsed_ms(self.h, C.c_int32(a), C.c_int32(b), C.byref(ms)))
+        return ms.value
+
+    def flush_l2(self):
+        self._check(lib().wfk_flush_l2(self.h))
 
     def synth_render(self, scene: SynthScene, intr: Intrinsics):
         depth = np.zeros((intr.height, intr.width), np.float32)
