@@ -155,11 +155,52 @@ __global__ void k_frozen(int N, const int32_t* uf, const uint8_t* comp_flag, uin
 }
 
 __global__ void k_entries(int64_t E, const int32_t* sorted_val, const double* c_w, int32_t* ent_con,
-                          double* ent_w) {
+                          uint8_t* ent_k, double* ent_w) {
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < E; e += int64_t(gridDim.x) * blockDim.x) {
     const int v = sorted_val[e];
     ent_con[e] = v >> 3;
+    ent_k[e] = uint8_t(v & 7);
     ent_w[e] = c_w[v];
+  }
+}
+
+// Cached B^T B of one (row, stencil slot): sum over the row's incidences of
+// coef a_i a_k (g g^T | I) for the anchor k at that slot, in the reference's
+// accumulation order (solver.cpp:196-226); symmetric 3x3 stored as 6 values.
+// Columns follow solver.cpp:149-160.
+__global__ void k_assemble_btb(Grid g, int N, const int32_t* rows, const int32_t* node_row, const int32_t* row_ptr,
+                               const int32_t* ent_con, const uint8_t* ent_k, const double* ent_w, const double* c_w,
+                               const double* c_g, const int32_t* c_kind, double* blk, int32_t* cols) {
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < int64_t(N) * 27;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const int r = int(t / 27), s = int(t % 27);
+    const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = s / 9 - 1;
+    int x, y, z;
+    g.idx3(rows[r], x, y, z);
+    cols[t] = g.in_grid(x + dx, y + dy, z + dz) ? node_row[g.lin(x + dx, y + dy, z + dz)] : -1;
+    double b[6] = {0, 0, 0, 0, 0, 0};
+    for (int e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
+      const int ki = ent_k[e];
+      const int ox = (ki & 1) + dx, oy = ((ki >> 1) & 1) + dy, oz = (ki >> 2) + dz;
+      if (ox < 0 || ox > 1 || oy < 0 || oy > 1 || oz < 0 || oz > 1) continue;
+      const int c = ent_con[e];
+      const int k = ox + 2 * oy + 4 * oz;
+      const double sc = c_g[4 * c + 3] * ent_w[e] * c_w[8 * int64_t(c) + k];
+      if (c_kind[c] == WFK_DENSE_PLANE) {
+        const double gx = c_g[4 * c], gy = c_g[4 * c + 1], gz = c_g[4 * c + 2];
+        b[0] += sc * (gx * gx);
+        b[1] += sc * (gx * gy);
+        b[2] += sc * (gx * gz);
+        b[3] += sc * (gy * gy);
+        b[4] += sc * (gy * gz);
+        b[5] += sc * (gz * gz);
+      } else {
+        b[0] += sc * 1.0;
+        b[3] += sc * 1.0;
+        b[5] += sc * 1.0;
+      }
+    }
+    for (int m = 0; m < 6; ++m) blk[t * 6 + m] = b[m];
   }
 }
 
@@ -293,7 +334,11 @@ struct FFArgs {
   double* field_def;
   double* field_eul;
   // row state
-  double *t, *x, *rhs, *r, *p, *ap, *dinv, *rot;
+  double *t, *x, *rhs, *r, *p, *p2, *ap, *dinv, *rot;
+  // assembled B^T B (levels with many incidences per row)
+  int assembled;
+  const double* blk;     // N x 27 x 6 (xx xy xz yy yz zz)
+  const int32_t* cols;   // N x 27
   const double *crhs, *cdiag;
   // constraints
   const int32_t* c_row;
@@ -319,15 +364,30 @@ struct Red {
   int region = 0;
 };
 
+// Grid-wide deterministic sum of NV values: block tree -> one partial per block
+// -> grid barrier -> warp 0 of every block sums the partials in a fixed order
+// and broadcasts through shared memory.  Partial regions alternate between
+// calls, so a region is never rewritten before every block has read it (one
+// grid barrier always separates the two).
 template <int NV>
 __device__ void grid_reduce(const FFArgs& a, cg::grid_group& grid, Red& rs, double (&v)[NV]) {
   __shared__ double smem[4 * 32];
+  __shared__ double bcast[4];
   block_sum<NV>(v, smem);
   double* base = a.partials + size_t(rs.region) * 4 * gridDim.x;
   if (threadIdx.x == 0)
     for (int k = 0; k < NV; ++k) base[size_t(k) * gridDim.x + blockIdx.x] = v[k];
   grid.sync();
-  for (int k = 0; k < NV; ++k) v[k] = sum_partials(base + size_t(k) * gridDim.x, gridDim.x);
+  if (threadIdx.x < 32) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const double s = sum_partials(base + size_t(k) * gridDim.x, gridDim.x);
+      if (threadIdx.x == 0) bcast[k] = s;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = bcast[k];
   rs.region ^= 1;
 }
 
@@ -384,14 +444,28 @@ __device__ wfk_energy energy(const FFArgs& a, cg::grid_group& grid, Red& rs, boo
   return e;
 }
 
+// Vector fetchers for the operator: a stored vector, or the PCG direction
+// p_new = D^-1 r + beta p_old evaluated on the fly (solver.cpp:332, 337), so
+// the p update needs no grid barrier of its own.
+struct FetchVec {
+  const double* v;
+  WF_D V3 operator()(int i) const { return ld3(v, i); }
+};
+struct FetchP {
+  const double *dinv, *r, *pold;
+  double beta;
+  WF_D V3 operator()(int i) const { return cmul(ld3(dinv, i), ld3(r, i)) + beta * ld3(pold, i); }
+};
+
 // matrix-free A*v, pass 1: u_c = coef (g . q_c) g  |  coef q_c
-__device__ void matvec_constraints(const FFArgs& a, const double* v) {
+template <class F>
+__device__ void matvec_constraints(const FFArgs& a, const F& v) {
   for (int64_t c = gtid(); c < a.C; c += gstride()) {
     V3 q{0, 0, 0};
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int row = a.c_row[8 * c + k];
-      if (row >= 0) q += a.c_w[8 * c + k] * ld3(v, row);
+      if (row >= 0) q += a.c_w[8 * c + k] * v(row);
     }
     const double coef = a.c_g[4 * c + 3];
     V3 u;
@@ -405,20 +479,53 @@ __device__ void matvec_constraints(const FFArgs& a, const double* v) {
   }
 }
 
-// matrix-free A*v, pass 2, one row
-__device__ __forceinline__ V3 matvec_row(const FFArgs& a, const double* v, int r) {
-  const V3 vr = ld3(v, r);
-  if (a.frozen[r]) return vr;
-  V3 acc{0, 0, 0};
-  for (int e = a.row_ptr[r]; e < a.row_ptr[r + 1]; ++e) acc += a.ent_w[e] * ld3(a.c_u, a.ent_con[e]);
+template <class F>
+__device__ __forceinline__ V3 laplacian(const FFArgs& a, const F& v, int r, V3 vr, V3 acc) {
   const double w2 = 2.0 * a.w_r;
 #pragma unroll
   for (int k = 0; k < 6; ++k) {
     const int j = a.nbr[int64_t(k) * a.N + r];
     if (j < 0) continue;
-    acc += w2 * (vr - ld3(v, j));
+    acc += w2 * (vr - v(j));
   }
   return acc;
+}
+
+// A*v for one row.  Matrix-free: gather of a_i u_c over the row's incidence
+// list.  Assembled (levels whose rows carry many constraints): the cached
+// symmetric B^T B blocks of the 27-point stencil (solver.cpp:163-237).
+template <bool ASM, class F>
+__device__ __forceinline__ V3 matvec_row(const FFArgs& a, const F& v, int r, V3 vr) {
+  if (a.frozen[r]) return vr;
+  V3 acc{0, 0, 0};
+  if (ASM) {
+    const double* B = a.blk + int64_t(r) * 27 * 6;
+    const int32_t* cl = a.cols + int64_t(r) * 27;
+#pragma unroll 3
+    for (int s = 0; s < 27; ++s) {
+      const int c = cl[s];
+      if (c < 0) continue;
+      const V3 x = v(c);
+      const double* b = B + 6 * s;  // xx xy xz yy yz zz
+      acc.x += b[0] * x.x + b[1] * x.y + b[2] * x.z;
+      acc.y += b[1] * x.x + b[3] * x.y + b[4] * x.z;
+      acc.z += b[2] * x.x + b[4] * x.y + b[5] * x.z;
+    }
+  } else {
+    const int e0 = a.row_ptr[r], e1 = a.row_ptr[r + 1];
+    int e = e0;
+    for (; e + 4 <= e1; e += 4) {
+      const int c0 = a.ent_con[e], c1 = a.ent_con[e + 1], c2 = a.ent_con[e + 2], c3 = a.ent_con[e + 3];
+      const double w0 = a.ent_w[e], w1 = a.ent_w[e + 1], w2 = a.ent_w[e + 2], w3 = a.ent_w[e + 3];
+      const V3 u0 = ld3(a.c_u, c0), u1 = ld3(a.c_u, c1), u2 = ld3(a.c_u, c2), u3 = ld3(a.c_u, c3);
+      acc += w0 * u0;
+      acc += w1 * u1;
+      acc += w2 * u2;
+      acc += w3 * u3;
+    }
+    for (; e < e1; ++e) acc += a.ent_w[e] * ld3(a.c_u, a.ent_con[e]);
+  }
+  return laplacian(a, v, r, vr, acc);
 }
 
 // finish_row (solver.cpp:240-269) + Jacobi diagonal (solver.cpp:289-294)
@@ -451,20 +558,30 @@ __device__ void assemble_rows(const FFArgs& a) {
   }
 }
 
-// pcg_solve (solver.cpp:282-343) on the matrix-free operator; x in/out
+// pcg_solve (solver.cpp:282-343); x in/out.  Per iteration: [constraint pass
+// of A p -> barrier] (matrix-free levels only) -> row pass: p = z + beta p_old
+// on the fly, A p, p.Ap -> reduce -> x, r update, r.z, r.r -> reduce.  The
+// arithmetic of every vector element is the reference's; only where it is
+// evaluated moves.
+template <bool ASM>
 __device__ void pcg(const FFArgs& a, cg::grid_group& grid, Red& rs, int& iters, double& relres) {
   iters = 0;
   relres = 0;
-  // r = b - A x ; z = D^-1 r ; p = z
-  matvec_constraints(a, a.x);
-  grid.sync();
+  double* pold = a.p;
+  double* pnew = a.p2;
+  // r = b - A x (solver.cpp:305-310)
+  const FetchVec fx{a.x};
+  if (!ASM) {
+    matvec_constraints(a, fx);
+    grid.sync();
+  }
   double v3[3] = {0, 0, 0};
   for (int r = int(gtid()); r < a.N; r += int(gstride())) {
     const V3 b = ld3(a.rhs, r);
-    const V3 rr = b - matvec_row(a, a.x, r);
+    const V3 rr = b - matvec_row<ASM>(a, fx, r, ld3(a.x, r));
     const V3 z = cmul(ld3(a.dinv, r), rr);
     st3(a.r, r, rr);
-    st3(a.p, r, z);
+    st3(pold, r, V3{0, 0, 0});
     v3[0] += dot(rr, z);
     v3[1] += dot(rr, rr);
     v3[2] += sqnorm(b);
@@ -480,14 +597,20 @@ __device__ void pcg(const FFArgs& a, cg::grid_group& grid, Red& rs, int& iters, 
   }
   relres = r_norm / b_norm;
   const double stop = fmax(a.pcg_tol * r_norm, 1e-13 * b_norm);
+  double beta = 0.0;  // first direction: p = z
   for (int it = 0; it < a.pcg_max && r_norm > stop; ++it) {
-    matvec_constraints(a, a.p);
-    grid.sync();
+    const FetchP fp{a.dinv, a.r, pold, beta};
+    if (!ASM) {
+      matvec_constraints(a, fp);
+      grid.sync();
+    }
     double v1[1] = {0};
     for (int r = int(gtid()); r < a.N; r += int(gstride())) {
-      const V3 apr = matvec_row(a, a.p, r);
+      const V3 pr = fp(r);
+      const V3 apr = matvec_row<ASM>(a, fp, r, pr);
+      st3(pnew, r, pr);
       st3(a.ap, r, apr);
-      v1[0] += dot(ld3(a.p, r), apr);
+      v1[0] += dot(pr, apr);
     }
     grid_reduce<1>(a, grid, rs, v1);
     const double pap = v1[0];
@@ -495,7 +618,7 @@ __device__ void pcg(const FFArgs& a, cg::grid_group& grid, Red& rs, int& iters, 
     const double alpha = rz / pap;
     double v2[2] = {0, 0};
     for (int r = int(gtid()); r < a.N; r += int(gstride())) {
-      const V3 pr = ld3(a.p, r);
+      const V3 pr = ld3(pnew, r);
       st3(a.x, r, ld3(a.x, r) + alpha * pr);
       const V3 rr = ld3(a.r, r) - alpha * ld3(a.ap, r);
       st3(a.r, r, rr);
@@ -505,13 +628,11 @@ __device__ void pcg(const FFArgs& a, cg::grid_group& grid, Red& rs, int& iters, 
     }
     grid_reduce<2>(a, grid, rs, v2);
     const double rz_new = v2[0];
-    const double beta = rz_new / rz;
+    beta = rz_new / rz;
     rz = rz_new;
-    for (int r = int(gtid()); r < a.N; r += int(gstride())) {
-      const V3 z = cmul(ld3(a.dinv, r), ld3(a.r, r));
-      st3(a.p, r, z + beta * ld3(a.p, r));
-    }
-    grid.sync();
+    double* t = pold;
+    pold = pnew;
+    pnew = t;
     r_norm = sqrt(v2[1]);
     relres = r_norm / b_norm;
     iters = it + 1;
@@ -549,7 +670,7 @@ __device__ void rotations(const FFArgs& a) {
   }
 }
 
-__global__ void __launch_bounds__(kBlock, 2) k_flip_flop(FFArgs a) {
+__global__ void __launch_bounds__(kCoopBlock, 1) k_flip_flop(FFArgs a) {
   cg::grid_group grid = cg::this_grid();
   Red rs;
   // load the row state from the field
@@ -586,7 +707,10 @@ __global__ void __launch_bounds__(kBlock, 2) k_flip_flop(FFArgs a) {
       grid.sync();
       int iters;
       double relres;
-      pcg(a, grid, rs, iters, relres);
+      if (a.assembled)
+        pcg<true>(a, grid, rs, iters, relres);
+      else
+        pcg<false>(a, grid, rs, iters, relres);
       total_pcg += iters;
       // write back non-frozen rows (solver.cpp:436-437)
       for (int r = int(gtid()); r < a.N; r += int(gstride())) {
@@ -664,7 +788,7 @@ __device__ void grid_reduce_asm(const AsmArgs& a, cg::grid_group& grid, int& reg
   region ^= 1;
 }
 
-__global__ void __launch_bounds__(kBlock, 2) k_pcg_assembled(AsmArgs a) {
+__global__ void __launch_bounds__(kCoopBlock, 1) k_pcg_assembled(AsmArgs a) {
   cg::grid_group grid = cg::this_grid();
   int region = 0;
   if (a.mode == 1) {
@@ -847,7 +971,8 @@ static void level_rows(wfk_ctx* c, Level& L) {
   L.uf.ensure(Nc);
   L.frozen.ensure(Nc);
   L.comp_flag.ensure(Nc);
-  for (DevBuf<double>* b : {&L.t, &L.x, &L.rhs, &L.r, &L.p, &L.ap, &L.dinv, &L.crhs, &L.cdiag}) b->ensure(3 * Nc);
+  for (DevBuf<double>* b : {&L.t, &L.x, &L.rhs, &L.r, &L.p, &L.p2, &L.ap, &L.dinv, &L.crhs, &L.cdiag})
+    b->ensure(3 * Nc);
   L.rot.ensure(9 * Nc);
   L.row_ptr.ensure(Nc + 1);
   L.cnt.ensure(Nc + 1);
@@ -916,12 +1041,25 @@ static void level_constraints(wfk_ctx* c, Level& L, const PoseD& pose, const wfk
   sync_check(c);
   L.E = c->h_pinned[1];
   if (L.E > 0) {
-    k_entries<<<grid_for(L.E), kBlock, 0, s>>>(L.E, L.val_out, L.c_w, L.ent_con, L.ent_w);
+    L.ent_k.ensure(size_t(L.E));
+    k_entries<<<grid_for(L.E), kBlock, 0, s>>>(L.E, L.val_out, L.c_w, L.ent_con, L.ent_k, L.ent_w);
     count_launch(c);
   }
   k_constraint_cache<<<grid_for(N), kBlock, 0, s>>>(N, L.row_ptr, L.ent_con, L.ent_w, L.c_kind, L.c_g, L.c_b,
                                                     L.crhs, L.cdiag);
   count_launch(c);
+  // Rows carrying many constraint incidences (coarse levels, where every
+  // constraint of the frame lands on a few thousand nodes) get their B^T B
+  // assembled once per solve, so the PCG row pass is a fixed 27-block stencil.
+  L.assembled = L.E > int64_t(kAssembleRatio) * N;
+  if (L.assembled) {
+    L.blk.ensure(size_t(N) * 27 * 6);
+    L.cols.ensure(size_t(N) * 27);
+    k_assemble_btb<<<grid_for(int64_t(N) * 27), kBlock, 0, s>>>(L.g, N, L.rows, L.node_row, L.row_ptr, L.ent_con,
+                                                                 L.ent_k, L.ent_w, L.c_w, L.c_g, L.c_kind, L.blk,
+                                                                 L.cols);
+    count_launch(c);
+  }
   WFK_CUDA(cudaGetLastError());
 }
 
@@ -935,12 +1073,13 @@ PoseD pose_dev(const wfk_pose* p) {
 static int coop_blocks(wfk_ctx* c) {
   if (c->coop_blocks == 0) {
     int per_sm = 0;
-    WFK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_flip_flop, kBlock, 0));
+    WFK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_flip_flop, kCoopBlock, 0));
     int per_sm2 = 0;
-    WFK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_pcg_assembled, kBlock, 0));
+    WFK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_pcg_assembled, kCoopBlock, 0));
     per_sm = std::min(per_sm, per_sm2);
     if (per_sm < 1) throw Error(WFK_E_CUDA, "cooperative kernel does not fit on an SM");
-    c->coop_blocks = c->num_sms * std::min(per_sm, 2);
+    // one persistent block per SM: fewest partials and barrier arrivals
+    c->coop_blocks = std::min(c->num_sms, kMaxCoopBlocks);
   }
   return c->coop_blocks;
 }
@@ -975,6 +1114,10 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   a.rhs = L.rhs;
   a.r = L.r;
   a.p = L.p;
+  a.p2 = L.p2;
+  a.assembled = L.assembled ? 1 : 0;
+  a.blk = L.blk;
+  a.cols = L.cols;
   a.ap = L.ap;
   a.dinv = L.dinv;
   a.rot = L.rot;
@@ -1006,7 +1149,7 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   void* args[] = {&a};
   Prof& pf = c->prof;
   if (pf.on) WFK_CUDA(cudaEventRecord(pf.ev[0], s));
-  WFK_CUDA(cudaLaunchCooperativeKernel((void*)k_flip_flop, dim3(G), dim3(kBlock), args, 0, s));
+  WFK_CUDA(cudaLaunchCooperativeKernel((void*)k_flip_flop, dim3(G), dim3(kCoopBlock), args, 0, s));
   if (pf.on) WFK_CUDA(cudaEventRecord(pf.ev[1], s));
   count_launch(c);
   int32_t st[4];
@@ -1263,7 +1406,7 @@ void solver_pcg_assembled(wfk_ctx* c, int N, const double* blocks, const int32_t
   a.status = c->ivec.ensure(16) + 8;
   a.relres_out = c->dvec.ensure(8);
   void* args[] = {&a};
-  WFK_CUDA(cudaLaunchCooperativeKernel((void*)k_pcg_assembled, dim3(G), dim3(kBlock), args, 0, s));
+  WFK_CUDA(cudaLaunchCooperativeKernel((void*)k_pcg_assembled, dim3(G), dim3(kCoopBlock), args, 0, s));
   count_launch(c);
   if (mode == 1) {
     WFK_CUDA(cudaMemcpyAsync(y, AP.p, size_t(N) * 3 * 8, cudaMemcpyDeviceToHost, s));

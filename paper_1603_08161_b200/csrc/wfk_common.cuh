@@ -18,6 +18,8 @@
 namespace wfk {
 
 constexpr int kBlock = 256;
+constexpr int kCoopBlock = 512;     // persistent cooperative kernels: 1 block / SM
+constexpr int kAssembleRatio = 32;  // incidences per row above which B^T B is assembled
 constexpr int kCenter = 13;
 
 struct V3 {
@@ -350,12 +352,20 @@ WF_D void block_sum(double (&v)[NV], double* smem /* >= NV * 32 */) {
   __syncthreads();
 }
 
-// Sum of partials[k * stride + b] over b < nblocks, fixed order; every thread
-// of the calling warp gets the result.
+// Sum of partials[b] over b < nblocks (<= 512), fixed order; every lane of the
+// calling warp gets the result.  All loads are issued before the adds.
+constexpr int kMaxCoopBlocks = 512;
 WF_D double sum_partials(const double* partials, int nblocks) {
   const int lane = threadIdx.x & 31;
+  double v[kMaxCoopBlocks / 32];
+#pragma unroll
+  for (int j = 0; j < kMaxCoopBlocks / 32; ++j) {
+    const int b = lane + 32 * j;
+    v[j] = b < nblocks ? __ldcg(partials + b) : 0.0;
+  }
   double s = 0.0;
-  for (int b = lane; b < nblocks; b += 32) s += __ldcg(partials + b);
+#pragma unroll
+  for (int j = 0; j < kMaxCoopBlocks / 32; ++j) s += v[j];
   return warp_sum(s);
 }
 

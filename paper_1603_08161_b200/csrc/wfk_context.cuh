@@ -96,7 +96,12 @@ struct Level {
   DevBuf<int32_t> rows, node_row, nbr, uf;  // nbr: 6 x Ncap SoA
   DevBuf<uint8_t> frozen, comp_flag;
   // per-row state (AoS double3 / row-major 3x3)
-  DevBuf<double> t, x, rhs, r, p, ap, dinv, crhs, cdiag, rot;
+  DevBuf<double> t, x, rhs, r, p, p2, ap, dinv, crhs, cdiag, rot;
+  // assembled B^T B for rows with many incidences (see kAssembleRatio)
+  bool assembled = false;
+  DevBuf<double> blk;      // N x 27 x 6
+  DevBuf<int32_t> cols;    // N x 27
+  DevBuf<uint8_t> ent_k;   // corner of the row inside each incident constraint
   // level constraints
   int64_t C = 0;
   DevBuf<int32_t> c_node;   // 8C anchors at this level
