@@ -155,13 +155,19 @@ __global__ void k_frozen(int N, const int32_t* uf, const uint8_t* comp_flag, uin
 }
 
 __global__ void k_entries(int64_t E, const int32_t* sorted_val, const double* c_w, int32_t* ent_con,
-                          uint8_t* ent_k, double* ent_w) {
+                          uint8_t* ent_k, double* ent_w, int32_t* c_pos) {
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < E; e += int64_t(gridDim.x) * blockDim.x) {
     const int v = sorted_val[e];
     ent_con[e] = v >> 3;
     ent_k[e] = uint8_t(v & 7);
     ent_w[e] = c_w[v];
+    c_pos[v] = int32_t(e);
   }
+}
+
+__global__ void k_heavy_flags(int N, const int32_t* row_ptr, uint8_t* flag) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x)
+    flag[r] = row_ptr[r + 1] - row_ptr[r] > kHeavyRow ? 1 : 0;
 }
 
 // Cached B^T B of one (row, stencil slot): sum over the row's incidences of
@@ -207,8 +213,8 @@ __global__ void k_assemble_btb(Grid g, int N, const int32_t* rows, const int32_t
 // ConstraintCache (solver.hpp:66-70): constraint part of the rhs and of the
 // Jacobi diagonal, accumulated in the reference's order (solver.cpp:196-226).
 __global__ void k_constraint_cache(int N, const int32_t* row_ptr, const int32_t* ent_con, const double* ent_w,
-                                   const int32_t* c_kind, const double* c_g, const double* c_b, double* crhs,
-                                   double* cdiag) {
+                                   const int32_t* c_kind, const double* c_g, const double* c_b, double4* crhs,
+                                   double4* cdiag) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x) {
     V3 rhs{0, 0, 0}, diag{0, 0, 0};
     for (int e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
@@ -229,8 +235,8 @@ __global__ void k_constraint_cache(int N, const int32_t* row_ptr, const int32_t*
         rhs += (coef * a) * g;
       }
     }
-    st3(crhs, r, rhs);
-    st3(cdiag, r, diag);
+    crhs[r] = make_double4(rhs.x, rhs.y, rhs.z, 0.0);
+    cdiag[r] = make_double4(diag.x, diag.y, diag.z, 0.0);
   }
 }
 
@@ -330,59 +336,105 @@ struct FFArgs {
   const int32_t* rows;
   const int32_t* nbr;
   const uint8_t* frozen;
-  // field (node indexed)
+  // field (node indexed, the volume's AoS layout)
   double* field_def;
   double* field_eul;
-  // row state
-  double *t, *x, *rhs, *r, *p, *p2, *ap, *dinv, *rot;
+  // row state: 32-byte padded 3-vectors, one 256-bit access each
+  double4 *t, *x, *rhs, *r, *p, *ap, *dinv;
+  const double4 *crhs, *cdiag;
+  double* rot;  // 9 per row
   // assembled B^T B (levels with many incidences per row)
   int assembled;
   const double* blk;     // N x 27 x 6 (xx xy xz yy yz zz)
   const int32_t* cols;   // N x 27
-  const double *crhs, *cdiag;
   // constraints
-  const int32_t* c_row;
-  const double* c_w;
-  const double* c_g;
+  const int4* c_row;     // 2 per constraint: anchor rows (-1 inactive)
+  const double4* c_w;    // 2 per constraint: anchor weights
+  const double4* c_g;    // g = R^T n (dense) | R^T (f - t) (sparse), coef
   const int32_t* c_kind;
   const double* target;
   const double* normal;
   const double* conf;
-  double* c_u;
   const int32_t* row_ptr;
-  const int32_t* ent_con;
-  const double* ent_w;
+  const int4* c_pos;     // 2 per constraint: incidence slot of each corner or -1
+  double4* contrib;      // E: a_k u_c per incidence slot (row-sorted)
+  const int32_t* heavy;  // rows with more than kHeavyRow incidences
+  int n_heavy;
   // outputs
   double* partials;  // 2 regions x 4 slots x gridDim
   wfk_trace_entry* trace;
   int32_t* status;   // [0] trace length, [1] error bits, [2] total pcg iterations
+  unsigned long long* dbg;  // per-block phase cycles (WFK_PHASE_TIMING=1), else null
   double* energy_out;
 };
 
 struct Red {
-  // rotating partial regions: see the note on double buffering in k_flip_flop
+  // rotating partial regions: see the note on double buffering in grid_reduce
   int region = 0;
 };
 
-// Grid-wide deterministic sum of NV values: block tree -> one partial per block
-// -> grid barrier -> warp 0 of every block sums the partials in a fixed order
-// and broadcasts through shared memory.  Partial regions alternate between
-// calls, so a region is never rewritten before every block has read it (one
-// grid barrier always separates the two).
+// Diagnostic phase clock: thread 0 of every block accumulates SM cycles per
+// phase (enabled with WFK_PHASE_TIMING=1; a null sink compiles to a branch).
+__device__ __forceinline__ long long sm_cycles() {
+#ifdef __CUDA_ARCH__
+  return clock64();
+#else
+  return 0;
+#endif
+}
+struct PhaseClock {
+  unsigned long long* acc;
+  long long t;
+  __device__ explicit PhaseClock(unsigned long long* sink)
+      : acc((threadIdx.x == 0 && sink) ? sink + 16 * blockIdx.x : nullptr), t(sm_cycles()) {}
+  __device__ void lap(int k) {
+    if (acc) {
+      const long long n = sm_cycles();
+      acc[k] += (unsigned long long)(n - t);
+      t = n;
+    }
+  }
+  __device__ void count(int k) {
+    if (acc) acc[k] += 1;
+  }
+};
+
+WF_D V3 ld4(const double4* p, int64_t i) {
+  const double4 v = p[i];
+  return {v.x, v.y, v.z};
+}
+WF_D void st4(double4* p, int64_t i, V3 v) { p[i] = make_double4(v.x, v.y, v.z, 0.0); }
+
+// Grid-wide deterministic sum of NV values: warp shuffle -> per-block partial
+// (warp 0) -> grid barrier -> warp 0 of every block sums the partials in a
+// fixed order and broadcasts through shared memory.  Partial regions alternate
+// between calls, so a region is never rewritten before every block has read
+// it (one grid barrier always separates the two).
 template <int NV>
 __device__ void grid_reduce(const FFArgs& a, cg::grid_group& grid, Red& rs, double (&v)[NV]) {
   __shared__ double smem[4 * 32];
   __shared__ double bcast[4];
-  block_sum<NV>(v, smem);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double* base = a.partials + size_t(rs.region) * 4 * gridDim.x;
-  if (threadIdx.x == 0)
-    for (int k = 0; k < NV; ++k) base[size_t(k) * gridDim.x + blockIdx.x] = v[k];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) smem[k * 32 + warp] = v[k];
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const double s = warp_sum(lane < nw ? smem[k * 32 + lane] : 0.0);
+      if (lane == 0) base[size_t(k) * gridDim.x + blockIdx.x] = s;
+    }
+  }
   grid.sync();
-  if (threadIdx.x < 32) {
+  if (warp == 0) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       const double s = sum_partials(base + size_t(k) * gridDim.x, gridDim.x);
-      if (threadIdx.x == 0) bcast[k] = s;
+      if (lane == 0) bcast[k] = s;
     }
   }
   __syncthreads();
@@ -391,19 +443,36 @@ __device__ void grid_reduce(const FFArgs& a, cg::grid_group& grid, Red& rs, doub
   rs.region ^= 1;
 }
 
-__device__ __forceinline__ int64_t gtid() { return blockIdx.x * int64_t(blockDim.x) + threadIdx.x; }
+// Work distribution of the persistent kernel: chunks of 32 consecutive items
+// (one per warp, coalesced) interleaved across the blocks, so even a few
+// thousand rows spread over every SM instead of the first few blocks.
+__device__ __forceinline__ int64_t gtid() {
+  return (int64_t((threadIdx.x >> 5) * gridDim.x + blockIdx.x) << 5) + (threadIdx.x & 31);
+}
 __device__ __forceinline__ int64_t gstride() { return int64_t(gridDim.x) * blockDim.x; }
+__device__ __forceinline__ int gwarp() { return (threadIdx.x >> 5) * gridDim.x + blockIdx.x; }
+__device__ __forceinline__ int nwarps() { return (blockDim.x >> 5) * gridDim.x; }
+
+WF_D void ld_anchors(const FFArgs& a, int64_t c, int rows[8], double w[8]) {
+  const int4 r0 = a.c_row[2 * c], r1 = a.c_row[2 * c + 1];
+  const double4 w0 = a.c_w[2 * c], w1 = a.c_w[2 * c + 1];
+  rows[0] = r0.x; rows[1] = r0.y; rows[2] = r0.z; rows[3] = r0.w;
+  rows[4] = r1.x; rows[5] = r1.y; rows[6] = r1.z; rows[7] = r1.w;
+  w[0] = w0.x; w[1] = w0.y; w[2] = w0.z; w[3] = w0.w;
+  w[4] = w1.x; w[5] = w1.y; w[6] = w1.z; w[7] = w1.w;
+}
 
 // E_sparse, E_dense, E_reg partials (solver.cpp:345-383)
 __device__ void energy_partials(const FFArgs& a, double& es, double& ed, double& er, int& bad) {
   es = ed = er = 0;
   for (int64_t c = gtid(); c < a.C; c += gstride()) {
+    int rows[8];
+    double w[8];
+    ld_anchors(a, c, rows, w);
     V3 q{0, 0, 0};
     for (int k = 0; k < 8; ++k) {
-      const double w = a.c_w[8 * c + k];
-      const int row = a.c_row[8 * c + k];
-      if (w > 0 && row < 0) bad = 1;
-      if (w != 0 && row >= 0) q += w * ld3(a.t, row);
+      if (w[k] > 0 && rows[k] < 0) bad = 1;
+      if (w[k] != 0 && rows[k] >= 0) q += w[k] * ld4(a.t, rows[k]);
     }
     const V3 s = a.pose.apply(q);
     const V3 f = ld3(a.target, c);
@@ -418,12 +487,12 @@ __device__ void energy_partials(const FFArgs& a, double& es, double& ed, double&
     const M3 ri = ld_m3(a.rot, r);
     const int node = a.rows[r];
     const V3 can_i = a.g.canonical(node);
-    const V3 ti = ld3(a.t, r);
+    const V3 ti = ld4(a.t, r);
     for (int k = 0; k < 6; ++k) {
       const int j = a.nbr[int64_t(k) * a.N + r];
       if (j < 0) continue;
       const V3 can_j = a.g.canonical(a.rows[j]);
-      const V3 resid = (ti - ld3(a.t, j)) - mul(ri, can_i - can_j);
+      const V3 resid = (ti - ld4(a.t, j)) - mul(ri, can_i - can_j);
       er += sqnorm(resid);
     }
   }
@@ -444,68 +513,62 @@ __device__ wfk_energy energy(const FFArgs& a, cg::grid_group& grid, Red& rs, boo
   return e;
 }
 
-// Vector fetchers for the operator: a stored vector, or the PCG direction
-// p_new = D^-1 r + beta p_old evaluated on the fly (solver.cpp:332, 337), so
-// the p update needs no grid barrier of its own.
-struct FetchVec {
-  const double* v;
-  WF_D V3 operator()(int i) const { return ld3(v, i); }
-};
-struct FetchP {
-  const double *dinv, *r, *pold;
-  double beta;
-  WF_D V3 operator()(int i) const { return cmul(ld3(dinv, i), ld3(r, i)) + beta * ld3(pold, i); }
-};
-
-// matrix-free A*v, pass 1: u_c = coef (g . q_c) g  |  coef q_c
-template <class F>
-__device__ void matvec_constraints(const FFArgs& a, const F& v) {
+// matrix-free A*v, pass 1: u_c = coef (g . q_c) g | coef q_c with
+// q_c = sum_k a_k v[a_k], and a_k u_c scattered to the incidence slot of each
+// anchor row (row-sorted order), so pass 2 sums a contiguous range per row.
+__device__ void matvec_constraints(const FFArgs& a, const double4* v) {
   for (int64_t c = gtid(); c < a.C; c += gstride()) {
+    int rows[8];
+    double w[8];
+    ld_anchors(a, c, rows, w);
     V3 q{0, 0, 0};
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int row = a.c_row[8 * c + k];
-      if (row >= 0) q += a.c_w[8 * c + k] * v(row);
-    }
-    const double coef = a.c_g[4 * c + 3];
+    for (int k = 0; k < 8; ++k)
+      if (rows[k] >= 0) q += w[k] * ld4(v, rows[k]);
+    const double4 gc = a.c_g[c];
     V3 u;
     if (a.c_kind[c] == WFK_DENSE_PLANE) {
-      const V3 g{a.c_g[4 * c], a.c_g[4 * c + 1], a.c_g[4 * c + 2]};
-      u = (coef * dot(g, q)) * g;
+      const V3 g{gc.x, gc.y, gc.z};
+      u = (gc.w * dot(g, q)) * g;
     } else {
-      u = coef * q;
+      u = gc.w * q;
     }
-    st3(a.c_u, c, u);
+    const int4 p0 = a.c_pos[2 * c], p1 = a.c_pos[2 * c + 1];
+    const int pos[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (pos[k] >= 0) st4(a.contrib, pos[k], w[k] * u);
   }
 }
 
-template <class F>
-__device__ __forceinline__ V3 laplacian(const FFArgs& a, const F& v, int r, V3 vr, V3 acc) {
+__device__ __forceinline__ V3 laplacian(const FFArgs& a, const double4* v, int r, V3 vr, V3 acc) {
   const double w2 = 2.0 * a.w_r;
 #pragma unroll
   for (int k = 0; k < 6; ++k) {
     const int j = a.nbr[int64_t(k) * a.N + r];
     if (j < 0) continue;
-    acc += w2 * (vr - v(j));
+    acc += w2 * (vr - ld4(v, j));
   }
   return acc;
 }
 
-// A*v for one row.  Matrix-free: gather of a_i u_c over the row's incidence
-// list.  Assembled (levels whose rows carry many constraints): the cached
-// symmetric B^T B blocks of the 27-point stencil (solver.cpp:163-237).
-template <bool ASM, class F>
-__device__ __forceinline__ V3 matvec_row(const FFArgs& a, const F& v, int r, V3 vr) {
+// A*v for one row.  Matrix-free: the row's contiguous incidence
+// contributions.  Assembled (levels whose rows carry many constraints): the
+// cached symmetric B^T B blocks of the 27-point stencil (solver.cpp:163-237).
+template <bool ASM>
+__device__ __forceinline__ V3 matvec_row(const FFArgs& a, const double4* v, int r, V3 vr) {
   if (a.frozen[r]) return vr;
   V3 acc{0, 0, 0};
   if (ASM) {
     const double* B = a.blk + int64_t(r) * 27 * 6;
-    const int32_t* cl = a.cols + int64_t(r) * 27;
-#pragma unroll 3
+    const int32_t* cp = a.cols + int64_t(r) * 27;
+    int cl[27];
+#pragma unroll
+    for (int s = 0; s < 27; ++s) cl[s] = cp[s];
+#pragma unroll
     for (int s = 0; s < 27; ++s) {
-      const int c = cl[s];
-      if (c < 0) continue;
-      const V3 x = v(c);
+      if (cl[s] < 0) continue;
+      const V3 x = ld4(v, cl[s]);
       const double* b = B + 6 * s;  // xx xy xz yy yz zz
       acc.x += b[0] * x.x + b[1] * x.y + b[2] * x.z;
       acc.y += b[1] * x.x + b[3] * x.y + b[4] * x.z;
@@ -513,19 +576,42 @@ __device__ __forceinline__ V3 matvec_row(const FFArgs& a, const F& v, int r, V3 
     }
   } else {
     const int e0 = a.row_ptr[r], e1 = a.row_ptr[r + 1];
-    int e = e0;
-    for (; e + 4 <= e1; e += 4) {
-      const int c0 = a.ent_con[e], c1 = a.ent_con[e + 1], c2 = a.ent_con[e + 2], c3 = a.ent_con[e + 3];
-      const double w0 = a.ent_w[e], w1 = a.ent_w[e + 1], w2 = a.ent_w[e + 2], w3 = a.ent_w[e + 3];
-      const V3 u0 = ld3(a.c_u, c0), u1 = ld3(a.c_u, c1), u2 = ld3(a.c_u, c2), u3 = ld3(a.c_u, c3);
-      acc += w0 * u0;
-      acc += w1 * u1;
-      acc += w2 * u2;
-      acc += w3 * u3;
-    }
-    for (; e < e1; ++e) acc += a.ent_w[e] * ld3(a.c_u, a.ent_con[e]);
+#pragma unroll 4
+    for (int e = e0; e < e1; ++e) acc += ld4(a.contrib, e);
   }
   return laplacian(a, v, r, vr, acc);
+}
+
+// (A v)_r for every row, delivered once per row to sink(r, v_r, (A v)_r).
+// Matrix-free levels hand rows with more than kHeavyRow incidences to a whole
+// warp: lanes stride the row's contiguous contributions (coalesced 256-bit
+// loads), lanes 0-5 take one stencil neighbour each, fixed shuffle tree.
+template <bool ASM, class Sink>
+__device__ __forceinline__ void row_pass(const FFArgs& a, const double4* v, Sink& sink) {
+  for (int r = int(gtid()); r < a.N; r += int(gstride())) {
+    if (!ASM && a.row_ptr[r + 1] - a.row_ptr[r] > kHeavyRow) continue;
+    const V3 vr = ld4(v, r);
+    sink(r, vr, matvec_row<ASM>(a, v, r, vr));
+  }
+  if (!ASM) {
+    const int lane = threadIdx.x & 31;
+    const double w2 = 2.0 * a.w_r;
+    for (int h = gwarp(); h < a.n_heavy; h += nwarps()) {
+      const int r = a.heavy[h];
+      const int e0 = a.row_ptr[r], e1 = a.row_ptr[r + 1];
+      const V3 vr = ld4(v, r);
+      V3 acc{0, 0, 0};
+      for (int e = e0 + lane; e < e1; e += 32) acc += ld4(a.contrib, e);
+      if (lane < 6) {
+        const int j = a.nbr[int64_t(lane) * a.N + r];
+        if (j >= 0) acc += w2 * (vr - ld4(v, j));
+      }
+      acc.x = warp_sum(acc.x);
+      acc.y = warp_sum(acc.y);
+      acc.z = warp_sum(acc.z);
+      if (lane == 0) sink(r, vr, a.frozen[r] ? vr : acc);
+    }
+  }
 }
 
 // finish_row (solver.cpp:240-269) + Jacobi diagonal (solver.cpp:289-294)
@@ -533,12 +619,12 @@ __device__ void assemble_rows(const FFArgs& a) {
   for (int r = int(gtid()); r < a.N; r += int(gstride())) {
     const int node = a.rows[r];
     if (a.frozen[r]) {
-      st3(a.rhs, r, ld3(a.t, r));
-      st3(a.dinv, r, V3{1.0, 1.0, 1.0});
+      a.rhs[r] = a.t[r];
+      a.dinv[r] = make_double4(1.0, 1.0, 1.0, 0.0);
       continue;
     }
-    V3 rhs = ld3(a.crhs, r);
-    V3 diag = ld3(a.cdiag, r);
+    V3 rhs = ld4(a.crhs, r);
+    V3 diag = ld4(a.cdiag, r);
     const M3 ri = ld_m3(a.rot, r);
     const V3 can_i = a.g.canonical(node);
     const double w2 = 2.0 * a.w_r;
@@ -550,89 +636,100 @@ __device__ void assemble_rows(const FFArgs& a) {
       diag.y += w2 * 1.0;
       diag.z += w2 * 1.0;
       rhs += a.w_r * mul(add(ri, ld_m3(a.rot, j)), dij);
-      if (a.frozen[j]) rhs += w2 * ld3(a.t, j);
+      if (a.frozen[j]) rhs += w2 * ld4(a.t, j);
     }
-    st3(a.rhs, r, rhs);
-    st3(a.dinv, r, V3{diag.x > 1e-300 ? 1.0 / diag.x : 1.0, diag.y > 1e-300 ? 1.0 / diag.y : 1.0,
+    st4(a.rhs, r, rhs);
+    st4(a.dinv, r, V3{diag.x > 1e-300 ? 1.0 / diag.x : 1.0, diag.y > 1e-300 ? 1.0 / diag.y : 1.0,
                       diag.z > 1e-300 ? 1.0 / diag.z : 1.0});
   }
 }
 
-// pcg_solve (solver.cpp:282-343); x in/out.  Per iteration: [constraint pass
-// of A p -> barrier] (matrix-free levels only) -> row pass: p = z + beta p_old
-// on the fly, A p, p.Ap -> reduce -> x, r update, r.z, r.r -> reduce.  The
-// arithmetic of every vector element is the reference's; only where it is
+// pcg_solve (solver.cpp:282-343); x in/out.  Per iteration:
+//   P  p = z + beta p (own rows)                              -> barrier
+//   A  constraint pass of A p  (matrix-free levels only)       -> barrier
+//   B  row pass: A p, p.Ap                                     -> reduction
+//   C  x += alpha p, r -= alpha Ap, r.z, r.r                   -> reduction
+// The arithmetic of every vector element is the reference's; only where it is
 // evaluated moves.
 template <bool ASM>
 __device__ void pcg(const FFArgs& a, cg::grid_group& grid, Red& rs, int& iters, double& relres) {
   iters = 0;
   relres = 0;
-  double* pold = a.p;
-  double* pnew = a.p2;
+  PhaseClock pc(a.dbg);
   // r = b - A x (solver.cpp:305-310)
-  const FetchVec fx{a.x};
   if (!ASM) {
-    matvec_constraints(a, fx);
+    matvec_constraints(a, a.x);
     grid.sync();
   }
   double v3[3] = {0, 0, 0};
-  for (int r = int(gtid()); r < a.N; r += int(gstride())) {
-    const V3 b = ld3(a.rhs, r);
-    const V3 rr = b - matvec_row<ASM>(a, fx, r, ld3(a.x, r));
-    const V3 z = cmul(ld3(a.dinv, r), rr);
-    st3(a.r, r, rr);
-    st3(pold, r, V3{0, 0, 0});
+  auto init_sink = [&](int r, V3, V3 ax) {
+    const V3 b = ld4(a.rhs, r);
+    const V3 rr = b - ax;
+    const V3 z = cmul(ld4(a.dinv, r), rr);
+    st4(a.r, r, rr);
+    st4(a.p, r, V3{0, 0, 0});
     v3[0] += dot(rr, z);
     v3[1] += dot(rr, rr);
     v3[2] += sqnorm(b);
-  }
+  };
+  row_pass<ASM>(a, a.x, init_sink);
   grid_reduce<3>(a, grid, rs, v3);
   double rz = v3[0];
   double r_norm = sqrt(v3[1]);
   const double b_norm = sqrt(v3[2]);
   if (b_norm == 0) {
-    for (int r = int(gtid()); r < a.N; r += int(gstride())) st3(a.x, r, V3{0, 0, 0});
+    for (int r = int(gtid()); r < a.N; r += int(gstride())) st4(a.x, r, V3{0, 0, 0});
     grid.sync();
     return;
   }
   relres = r_norm / b_norm;
   const double stop = fmax(a.pcg_tol * r_norm, 1e-13 * b_norm);
   double beta = 0.0;  // first direction: p = z
+  pc.lap(12);
   for (int it = 0; it < a.pcg_max && r_norm > stop; ++it) {
-    const FetchP fp{a.dinv, a.r, pold, beta};
+    for (int r = int(gtid()); r < a.N; r += int(gstride())) {
+      const V3 z = cmul(ld4(a.dinv, r), ld4(a.r, r));
+      st4(a.p, r, z + beta * ld4(a.p, r));
+    }
+    pc.lap(6);
+    grid.sync();
+    pc.lap(7);
     if (!ASM) {
-      matvec_constraints(a, fp);
+      matvec_constraints(a, a.p);
+      pc.lap(0);
       grid.sync();
+      pc.lap(1);
     }
     double v1[1] = {0};
-    for (int r = int(gtid()); r < a.N; r += int(gstride())) {
-      const V3 pr = fp(r);
-      const V3 apr = matvec_row<ASM>(a, fp, r, pr);
-      st3(pnew, r, pr);
-      st3(a.ap, r, apr);
+    auto ap_sink = [&](int r, V3 pr, V3 apr) {
+      st4(a.ap, r, apr);
       v1[0] += dot(pr, apr);
-    }
+    };
+    row_pass<ASM>(a, a.p, ap_sink);
+    pc.lap(2);
     grid_reduce<1>(a, grid, rs, v1);
+    pc.lap(3);
     const double pap = v1[0];
     if (pap <= 0) break;
     const double alpha = rz / pap;
     double v2[2] = {0, 0};
     for (int r = int(gtid()); r < a.N; r += int(gstride())) {
-      const V3 pr = ld3(pnew, r);
-      st3(a.x, r, ld3(a.x, r) + alpha * pr);
-      const V3 rr = ld3(a.r, r) - alpha * ld3(a.ap, r);
-      st3(a.r, r, rr);
-      const V3 z = cmul(ld3(a.dinv, r), rr);
+      const double4 x4 = a.x[r], p4 = a.p[r], r4 = a.r[r], ap4 = a.ap[r], d4 = a.dinv[r];
+      const V3 xn = V3{x4.x, x4.y, x4.z} + alpha * V3{p4.x, p4.y, p4.z};
+      const V3 rr = V3{r4.x, r4.y, r4.z} - alpha * V3{ap4.x, ap4.y, ap4.z};
+      st4(a.x, r, xn);
+      st4(a.r, r, rr);
+      const V3 z = cmul(V3{d4.x, d4.y, d4.z}, rr);
       v2[0] += dot(rr, z);
       v2[1] += dot(rr, rr);
     }
+    pc.lap(4);
     grid_reduce<2>(a, grid, rs, v2);
+    pc.lap(5);
+    pc.count(15);
     const double rz_new = v2[0];
     beta = rz_new / rz;
     rz = rz_new;
-    double* t = pold;
-    pold = pnew;
-    pnew = t;
     r_norm = sqrt(v2[1]);
     relres = r_norm / b_norm;
     iters = it + 1;
@@ -644,13 +741,13 @@ __device__ void rotations(const FFArgs& a) {
   for (int r = int(gtid()); r < a.N; r += int(gstride())) {
     const int node = a.rows[r];
     const V3 can_i = a.g.canonical(node);
-    const V3 ti = ld3(a.t, r);
+    const V3 ti = ld4(a.t, r);
     M3 h = m3_zero();
     for (int k = 0; k < 6; ++k) {
       const int j = a.nbr[int64_t(k) * a.N + r];
       if (j < 0) continue;
       const V3 rest = can_i - a.g.canonical(a.rows[j]);
-      const V3 cur = ti - ld3(a.t, j);
+      const V3 cur = ti - ld4(a.t, j);
       for (int p = 0; p < 3; ++p)
         for (int q = 0; q < 3; ++q) h.a[p][q] += comp(rest, p) * comp(cur, q);
     }
@@ -676,7 +773,7 @@ __global__ void __launch_bounds__(kCoopBlock, 1) k_flip_flop(FFArgs a) {
   // load the row state from the field
   for (int r = int(gtid()); r < a.N; r += int(gstride())) {
     const int node = a.rows[r];
-    st3(a.t, r, ld3(a.field_def, node));
+    st4(a.t, r, ld3(a.field_def, node));
     st_m3(a.rot, r, euler_to_matrix(ld3(a.field_eul, node)));
   }
   grid.sync();
@@ -700,11 +797,13 @@ __global__ void __launch_bounds__(kCoopBlock, 1) k_flip_flop(FFArgs a) {
   int n_trace = 0;
   int total_pcg = 0;
   if (prev.total != 0) {
+    PhaseClock pc(a.dbg);
     for (int it = 0; it < a.ff_iters; ++it) {
       // assemble rhs / diagonal with the current rotations; x0 = t
       assemble_rows(a);
-      for (int r = int(gtid()); r < a.N; r += int(gstride())) st3(a.x, r, ld3(a.t, r));
+      for (int r = int(gtid()); r < a.N; r += int(gstride())) a.x[r] = a.t[r];
       grid.sync();
+      pc.lap(8);
       int iters;
       double relres;
       if (a.assembled)
@@ -712,18 +811,21 @@ __global__ void __launch_bounds__(kCoopBlock, 1) k_flip_flop(FFArgs a) {
       else
         pcg<false>(a, grid, rs, iters, relres);
       total_pcg += iters;
+      pc.lap(9);
       // write back non-frozen rows (solver.cpp:436-437)
       for (int r = int(gtid()); r < a.N; r += int(gstride())) {
         if (a.frozen[r]) continue;
-        const V3 xr = ld3(a.x, r);
-        st3(a.t, r, xr);
+        const V3 xr = ld4(a.x, r);
+        st4(a.t, r, xr);
         st3(a.field_def, a.rows[r], xr);
       }
       grid.sync();
       rotations(a);
       grid.sync();
+      pc.lap(10);
       bool dummy;
       const wfk_energy e = energy(a, grid, rs, dummy);
+      pc.lap(11);
       const bool anomaly = e.total > prev.total + 1e-9 * prev.total;
       if (gtid() == 0) {
         wfk_trace_entry& t = a.trace[n_trace];
@@ -873,7 +975,7 @@ __global__ void __launch_bounds__(kCoopBlock, 1) k_pcg_assembled(AsmArgs a) {
 __global__ void k_ne_assemble(Grid g, int N, const int32_t* rows, const int32_t* node_row, const int32_t* nbr,
                               const uint8_t* frozen, const int32_t* row_ptr, const int32_t* ent_con,
                               const double* ent_w, const int32_t* c_node, const double* c_w, const int32_t* c_kind,
-                              const double* c_g, const double* rot, const double* t, const double* crhs,
+                              const double* c_g, const double* rot, const double4* t, const double4* crhs,
                               double w_r, double* blocks, int32_t* cols, double* rhs) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x) {
     const int node = rows[r];
@@ -890,7 +992,7 @@ __global__ void k_ne_assemble(Grid g, int N, const int32_t* rows, const int32_t*
         }
     if (frozen[r]) {
       B[kCenter * 9 + 0] = B[kCenter * 9 + 4] = B[kCenter * 9 + 8] = 1.0;
-      st3(rhs, r, ld3(t, r));
+      st3(rhs, r, V3{t[r].x, t[r].y, t[r].z});
       continue;
     }
     for (int e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
@@ -912,7 +1014,7 @@ __global__ void k_ne_assemble(Grid g, int N, const int32_t* rows, const int32_t*
         }
       }
     }
-    V3 rv = ld3(crhs, r);
+    V3 rv{crhs[r].x, crhs[r].y, crhs[r].z};
     const M3 ri = ld_m3(rot, r);
     const V3 can_i = g.canonical(node);
     const double w2 = 2.0 * w_r;
@@ -923,7 +1025,7 @@ __global__ void k_ne_assemble(Grid g, int N, const int32_t* rows, const int32_t*
       for (int i = 0; i < 3; ++i) B[kCenter * 9 + i * 4] += w2 * 1.0;
       rv += w_r * mul(add(ri, ld_m3(rot, j)), dij);
       if (frozen[j]) {
-        rv += w2 * ld3(t, j);
+        rv += w2 * V3{t[j].x, t[j].y, t[j].z};
       } else {
         const int s = stencil_slot(kFace[k][0], kFace[k][1], kFace[k][2]);
         for (int i = 0; i < 3; ++i) B[s * 9 + i * 4] -= w2 * 1.0;
@@ -933,10 +1035,11 @@ __global__ void k_ne_assemble(Grid g, int N, const int32_t* rows, const int32_t*
   }
 }
 
-__global__ void k_load_rows(int N, const int32_t* rows, const double* f_def, const double* f_eul, double* t,
+__global__ void k_load_rows(int N, const int32_t* rows, const double* f_def, const double* f_eul, double4* t,
                             double* rot) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x) {
-    st3(t, r, ld3(f_def, rows[r]));
+    const V3 v = ld3(f_def, rows[r]);
+    t[r] = make_double4(v.x, v.y, v.z, 0.0);
     st_m3(rot, r, euler_to_matrix(ld3(f_eul, rows[r])));
   }
 }
@@ -971,8 +1074,7 @@ static void level_rows(wfk_ctx* c, Level& L) {
   L.uf.ensure(Nc);
   L.frozen.ensure(Nc);
   L.comp_flag.ensure(Nc);
-  for (DevBuf<double>* b : {&L.t, &L.x, &L.rhs, &L.r, &L.p, &L.p2, &L.ap, &L.dinv, &L.crhs, &L.cdiag})
-    b->ensure(3 * Nc);
+  for (DevBuf<double4>* b : {&L.t, &L.x, &L.rhs, &L.r, &L.p, &L.ap, &L.dinv, &L.crhs, &L.cdiag}) b->ensure(Nc);
   L.rot.ensure(9 * Nc);
   L.row_ptr.ensure(Nc + 1);
   L.cnt.ensure(Nc + 1);
@@ -1040,9 +1142,11 @@ static void level_constraints(wfk_ctx* c, Level& L, const PoseD& pose, const wfk
   WFK_CUDA(cudaMemcpyAsync(c->h_pinned + 1, d_ne, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   sync_check(c);
   L.E = c->h_pinned[1];
+  L.c_pos.ensure(8 * size_t(std::max<int64_t>(C, 1)));
+  if (C > 0) WFK_CUDA(cudaMemsetAsync(L.c_pos.p, 0xff, 8 * size_t(C) * sizeof(int32_t), s));
   if (L.E > 0) {
     L.ent_k.ensure(size_t(L.E));
-    k_entries<<<grid_for(L.E), kBlock, 0, s>>>(L.E, L.val_out, L.c_w, L.ent_con, L.ent_k, L.ent_w);
+    k_entries<<<grid_for(L.E), kBlock, 0, s>>>(L.E, L.val_out, L.c_w, L.ent_con, L.ent_k, L.ent_w, L.c_pos);
     count_launch(c);
   }
   k_constraint_cache<<<grid_for(N), kBlock, 0, s>>>(N, L.row_ptr, L.ent_con, L.ent_w, L.c_kind, L.c_g, L.c_b,
@@ -1052,6 +1156,23 @@ static void level_constraints(wfk_ctx* c, Level& L, const PoseD& pose, const wfk
   // constraint of the frame lands on a few thousand nodes) get their B^T B
   // assembled once per solve, so the PCG row pass is a fixed 27-block stencil.
   L.assembled = L.E > int64_t(kAssembleRatio) * N;
+  L.n_heavy = 0;
+  if (!L.assembled && L.E > 0) {
+    L.contrib.ensure(size_t(L.E));
+    L.heavy.ensure(size_t(N) + 1);
+    uint8_t* flag = c->mask.ensure(size_t(std::max<int64_t>(2 * c->vol.n, N)) + 1);
+    k_heavy_flags<<<grid_for(N), kBlock, 0, s>>>(N, L.row_ptr, flag);
+    int32_t* d_nh = c->ivec.ensure(16) + 3;
+    size_t tmp3 = 0;
+    thrust::counting_iterator<int32_t> it(0);
+    cub::DeviceSelect::Flagged(nullptr, tmp3, it, flag, L.heavy.p, d_nh, N, s);
+    c->temp.ensure(tmp3);
+    WFK_CUDA(cub::DeviceSelect::Flagged(c->temp.p, tmp3, it, flag, L.heavy.p, d_nh, N, s));
+    count_launch(c, 2);
+    WFK_CUDA(cudaMemcpyAsync(c->h_pinned + 3, d_nh, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    sync_check(c);
+    L.n_heavy = c->h_pinned[3];
+  }
   if (L.assembled) {
     L.blk.ensure(size_t(N) * 27 * 6);
     L.cols.ensure(size_t(N) * 27);
@@ -1114,7 +1235,6 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   a.rhs = L.rhs;
   a.r = L.r;
   a.p = L.p;
-  a.p2 = L.p2;
   a.assembled = L.assembled ? 1 : 0;
   a.blk = L.blk;
   a.cols = L.cols;
@@ -1123,23 +1243,30 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   a.rot = L.rot;
   a.crhs = L.crhs;
   a.cdiag = L.cdiag;
-  a.c_row = L.c_row;
-  a.c_w = L.c_w;
-  a.c_g = L.c_g;
+  a.c_row = reinterpret_cast<const int4*>(L.c_row.p);
+  a.c_w = reinterpret_cast<const double4*>(L.c_w.p);
+  a.c_g = reinterpret_cast<const double4*>(L.c_g.p);
   a.c_kind = L.c_kind;
   a.target = c->cons.target;
   a.normal = c->cons.normal;
   a.conf = c->cons.conf;
-  a.c_u = L.c_u;
   a.row_ptr = L.row_ptr;
-  a.ent_con = L.ent_con;
-  a.ent_w = L.ent_w;
+  a.c_pos = reinterpret_cast<const int4*>(L.c_pos.p);
+  a.contrib = L.contrib;
+  a.heavy = L.heavy;
+  a.n_heavy = L.n_heavy;
   a.partials = c->partials.ensure(size_t(8) * G);
   a.trace = c->trace.ensure(size_t(std::max(p.flip_flop_iters, 1)));
   int32_t* status = c->ivec.ensure(16) + 4;
   double* eout = c->eout.ensure(8);
   a.status = status;
   a.energy_out = eout;
+  static const bool phase_timing = getenv("WFK_PHASE_TIMING") != nullptr;
+  a.dbg = nullptr;
+  if (phase_timing) {
+    a.dbg = reinterpret_cast<unsigned long long*>(c->lvec.ensure(size_t(16) * G));
+    WFK_CUDA(cudaMemsetAsync(a.dbg, 0, size_t(16) * G * sizeof(unsigned long long), s));
+  }
   WFK_CUDA(cudaMemsetAsync(status, 0, 4 * sizeof(int32_t), s));
   if (L.N == 0 && L.C == 0 && mode != 2) {
     // nothing to solve: energy is exactly zero
@@ -1163,6 +1290,30 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   if (st[1] & 1) throw Error(WFK_E_LOGIC, "evaluate_energy: constraint anchors an inactive point");
   if (e_out) *e_out = wfk_energy{en[0], en[1], en[2], en[3]};
   c->stats.pcg_iterations += st[2];
+  if (phase_timing) {
+    std::vector<unsigned long long> d(size_t(16) * G);
+    WFK_CUDA(cudaMemcpy(d.data(), a.dbg, d.size() * 8, cudaMemcpyDeviceToHost));
+    const double it = double(d[15]) + 1e-9;
+    auto stat = [&](int k, double& mean, double& mx) {
+      mean = 0;
+      mx = 0;
+      for (int b = 0; b < G; ++b) {
+        const double v = double(d[size_t(b) * 16 + k]) / it;
+        mean += v / G;
+        mx = std::max(mx, v);
+      }
+    };
+    const char* names[8] = {"A", "Async", "B", "red1", "C", "red2", "P", "Psync"};
+    fprintf(stderr, "[wfk phase] level %d N %d C %lld asm %d heavy %d iters %.0f | cycles/iter mean/max:", level_tag,
+            L.N, (long long)L.C, int(L.assembled), L.n_heavy, it);
+    for (int k = 0; k < 8; ++k) {
+      double m, x;
+      stat(k, m, x);
+      fprintf(stderr, " %s %.0f/%.0f", names[k], m, x);
+    }
+    fprintf(stderr, " | blk0 Mcyc/launch: assemble %.2f pcg %.2f rot %.2f energy %.2f\n", d[8] * 1e-6, d[9] * 1e-6,
+            d[10] * 1e-6, d[11] * 1e-6);
+  }
   if (pf.on && mode == 0) {
     float ms = 0;
     WFK_CUDA(cudaEventElapsedTime(&ms, pf.ev[0], pf.ev[1]));
@@ -1342,7 +1493,7 @@ int solver_build_ne(wfk_ctx* c, const wfk_pose* pose, const wfk_solver_params& p
   const int N = L.N;
   if (!out || N == 0) return N;
   cudaStream_t s = c->stream;
-  double* t = L.t;
+  double4* t = L.t;
   k_load_rows<<<grid_for(N), kBlock, 0, s>>>(N, L.rows, L.deformed, L.euler, t, L.rot);
   DevBuf<double> blocks;
   DevBuf<int32_t> cols;

@@ -20,6 +20,7 @@ namespace wfk {
 constexpr int kBlock = 256;
 constexpr int kCoopBlock = 512;     // persistent cooperative kernels: 1 block / SM
 constexpr int kAssembleRatio = 32;  // incidences per row above which B^T B is assembled
+constexpr int kHeavyRow = 16;       // incidences above which a row is summed by a whole warp
 constexpr int kCenter = 13;
 
 struct V3 {

@@ -96,12 +96,17 @@ struct Level {
   DevBuf<int32_t> rows, node_row, nbr, uf;  // nbr: 6 x Ncap SoA
   DevBuf<uint8_t> frozen, comp_flag;
   // per-row state (AoS double3 / row-major 3x3)
-  DevBuf<double> t, x, rhs, r, p, p2, ap, dinv, crhs, cdiag, rot;
+  DevBuf<double4> t, x, rhs, r, p, ap, dinv, crhs, cdiag;  // 32 B padded 3-vectors
+  DevBuf<double> rot;
   // assembled B^T B for rows with many incidences (see kAssembleRatio)
   bool assembled = false;
   DevBuf<double> blk;      // N x 27 x 6
   DevBuf<int32_t> cols;    // N x 27
   DevBuf<uint8_t> ent_k;   // corner of the row inside each incident constraint
+  DevBuf<int32_t> c_pos;   // 8C: incidence slot of (constraint, corner), -1 if none
+  DevBuf<double4> contrib; // E: per-incidence matvec contributions
+  DevBuf<int32_t> heavy;   // rows summed by a whole warp
+  int n_heavy = 0;
   // level constraints
   int64_t C = 0;
   DevBuf<int32_t> c_node;   // 8C anchors at this level
