@@ -1,6 +1,7 @@
 // extern "C" boundary of libwfk (include/wfk.h).  Every entry point validates
 // its arguments, runs on the context's stream and returns a status; C++
 // exceptions never cross the ABI.
+#include <chrono>
 #include <cstring>
 #include <vector>
 
@@ -568,10 +569,21 @@ void run_frame(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose* pose, const 
       return;
     }
     int64_t nv = 0, nt = 0;
-    assoc_extract_mesh(c, pose, &nv, &nt);
+    static const bool dbg = getenv("WFK_STAGE_DEBUG") != nullptr;
+    auto timed = [&](const char* name, auto&& fn) {
+      if (!dbg) return fn();
+      WFK_CUDA(cudaStreamSynchronize(c->stream));
+      const auto t0 = std::chrono::steady_clock::now();
+      fn();
+      WFK_CUDA(cudaStreamSynchronize(c->stream));
+      const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      fprintf(stderr, "[wfk stage] frame %d %-10s %8.3f ms  (V %lld T %lld)\n", frame_index, name, ms, (long long)nv,
+              (long long)nt);
+    };
+    timed("mc", [&] { assoc_extract_mesh(c, pose, &nv, &nt); });
     if (nt == 0) throw Error(WFK_E_LOGIC, "empty isosurface before frame");
-    assoc_compute_normals(c);
-    assoc_rasterize(c, K, nullptr);
+    timed("normals", [&] { assoc_compute_normals(c); });
+    timed("raster", [&] { assoc_rasterize(c, K, nullptr); });
     stage_mark(c, 1);
     lap(0, 0, 1);
     std::vector<wfk_trace_entry> trace;
@@ -596,9 +608,9 @@ void run_frame(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose* pose, const 
         ++rec->trace_len;
       }
       if (!trace.empty()) rec->energy = trace.back().energy;
-      assoc_mesh_warp(c, pose);  // redeform (pipeline.cpp:167-172)
-      assoc_compute_normals(c);
-      assoc_rasterize(c, K, nullptr);
+      timed("warp", [&] { assoc_mesh_warp(c, pose); });  // redeform (pipeline.cpp:167-172)
+      timed("normals2", [&] { assoc_compute_normals(c); });
+      timed("raster2", [&] { assoc_rasterize(c, K, nullptr); });
       stage_mark(c, 5);
       lap(3, 4, 5);
     }

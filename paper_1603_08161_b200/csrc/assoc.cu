@@ -467,7 +467,10 @@ void assoc_compute_normals(wfk_ctx* c) {
     const int64_t E = 3 * m.T;
     m.adj_ptr.ensure(size_t(m.V) + 1);
     m.adj_tri.ensure(size_t(E) + 1);
-    DevBuf<int32_t> key, val, key2, cnt;
+    DevBuf<int32_t>& key = m.adj_key;
+    DevBuf<int32_t>& val = m.adj_val;
+    DevBuf<int32_t>& key2 = m.adj_key2;
+    DevBuf<int32_t>& cnt = m.adj_cnt;
     key.ensure(size_t(E) + 1);
     val.ensure(size_t(E) + 1);
     key2.ensure(size_t(E) + 1);
@@ -485,7 +488,6 @@ void assoc_compute_normals(wfk_ctx* c) {
       count_launch(c);
     }
     exclusive_scan(c, cnt.p, m.adj_ptr.p, m.V + 1);
-    WFK_CUDA(cudaStreamSynchronize(s));  // scratch buffers are freed on return
     m.adj_valid = true;
   }
   k_normals<<<grid_for(m.V), kBlock, 0, s>>>(m.V, m.adj_ptr, m.adj_tri, m.tri, m.def, m.nrm);

@@ -165,6 +165,21 @@ __global__ void k_entries(int64_t E, const int32_t* sorted_val, const double* c_
   }
 }
 
+// work items of the balanced matrix-free row pass (see item_pass)
+__global__ void k_item_count(int N, const int32_t* row_ptr, int32_t* n_items) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x) {
+    const int cnt = row_ptr[r + 1] - row_ptr[r];
+    n_items[r] = cnt > 0 ? (cnt + kItemLen - 1) / kItemLen : 1;
+  }
+}
+__global__ void k_item_write(int N, const int32_t* row_ptr, const int32_t* item_ptr, int4* items) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x) {
+    const int e0 = row_ptr[r], e1 = row_ptr[r + 1];
+    for (int i = item_ptr[r], k = 0; i < item_ptr[r + 1]; ++i, ++k)
+      items[i] = make_int4(r, e0 + k * kItemLen, min(e1, e0 + (k + 1) * kItemLen), k == 0 ? 1 : 0);
+  }
+}
+
 __global__ void k_heavy_flags(int N, const int32_t* row_ptr, uint8_t* flag) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x)
     flag[r] = row_ptr[r + 1] - row_ptr[r] > kHeavyRow ? 1 : 0;
@@ -340,7 +355,7 @@ struct FFArgs {
   double* field_def;
   double* field_eul;
   // row state: 32-byte padded 3-vectors, one 256-bit access each
-  double4 *t, *x, *rhs, *r, *p, *ap, *dinv;
+  double4 *t, *x, *rhs, *r, *p, *ap, *dinv, *u, *w;  // ap holds s = A p
   const double4 *crhs, *cdiag;
   double* rot;  // 9 per row
   // assembled B^T B (levels with many incidences per row)
@@ -360,8 +375,15 @@ struct FFArgs {
   double4* contrib;      // E: a_k u_c per incidence slot (row-sorted)
   const int32_t* heavy;  // rows with more than kHeavyRow incidences
   int n_heavy;
+  const int4* items;     // matrix-free work items: row, e_begin, e_end, first
+  int n_items;
+  const int32_t* item_ptr;  // N+1: items of each row
+  double4* wpart;        // per-item partial (A v)
   // outputs
-  double* partials;  // 2 regions x 4 slots x gridDim
+  double* partials;  // 4 slots x gridDim
+  unsigned* sync_count;  // grid barrier arrival counter (own 128 B line)
+  unsigned* sync_gen;    // grid barrier generation (own 128 B line)
+  double* sync_total;    // reduction totals published by the last arriver
   wfk_trace_entry* trace;
   int32_t* status;   // [0] trace length, [1] error bits, [2] total pcg iterations
   unsigned long long* dbg;  // per-block phase cycles (WFK_PHASE_TIMING=1), else null
@@ -369,8 +391,7 @@ struct FFArgs {
 };
 
 struct Red {
-  // rotating partial regions: see the note on double buffering in grid_reduce
-  int region = 0;
+  unsigned gen = 0;  // generation of the grid barrier this block has passed
 };
 
 // Diagnostic phase clock: thread 0 of every block accumulates SM cycles per
@@ -383,19 +404,27 @@ __device__ __forceinline__ long long sm_cycles() {
 #endif
 }
 struct PhaseClock {
-  unsigned long long* acc;
+  unsigned long long* sink;
+  unsigned long long acc[16];
   long long t;
-  __device__ explicit PhaseClock(unsigned long long* sink)
-      : acc((threadIdx.x == 0 && sink) ? sink + 16 * blockIdx.x : nullptr), t(sm_cycles()) {}
+  __device__ explicit PhaseClock(unsigned long long* s)
+      : sink((threadIdx.x == 0 && s) ? s + 16 * blockIdx.x : nullptr), t(sm_cycles()) {
+    for (int k = 0; k < 16; ++k) acc[k] = 0;
+  }
   __device__ void lap(int k) {
-    if (acc) {
+    if (sink) {
       const long long n = sm_cycles();
       acc[k] += (unsigned long long)(n - t);
       t = n;
     }
   }
   __device__ void count(int k) {
-    if (acc) acc[k] += 1;
+    if (sink) acc[k] += 1;
+  }
+  __device__ ~PhaseClock() {
+    if (sink)
+      for (int k = 0; k < 16; ++k)
+        if (acc[k]) sink[k] += acc[k];
   }
 };
 
@@ -405,42 +434,97 @@ WF_D V3 ld4(const double4* p, int64_t i) {
 }
 WF_D void st4(double4* p, int64_t i, V3 v) { p[i] = make_double4(v.x, v.y, v.z, 0.0); }
 
-// Grid-wide deterministic sum of NV values: warp shuffle -> per-block partial
-// (warp 0) -> grid barrier -> warp 0 of every block sums the partials in a
-// fixed order and broadcasts through shared memory.  Partial regions alternate
-// between calls, so a region is never rewritten before every block has read
-// it (one grid barrier always separates the two).
+// ---- grid synchronisation of the persistent kernel -------------------------
+// One arrival counter and one generation word (separate 128 B lines).  A block
+// arrives with a single acq_rel atomic from thread 0 after a block barrier; the
+// last of the G arrivals resets the counter and releases the next generation;
+// the others poll the generation word.
+//
+// grid_reduce fuses that barrier with a deterministic sum: every block
+// publishes its partials before arriving, and ONLY the last arriving block
+// reads them (fixed order, so the value does not depend on who is last),
+// stores the totals and then releases the generation -- the other blocks read
+// one line of totals instead of all G partials.  A partial or total slot is
+// never rewritten before every block has passed the barrier that consumed it.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned atom_add_acq_rel_u32(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+__device__ __forceinline__ void grid_barrier(const FFArgs& a, Red& rs) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned old = atom_add_acq_rel_u32(a.sync_count, 1u);
+    if (old == gridDim.x - 1) {
+      *a.sync_count = 0;
+      st_release_u32(a.sync_gen, rs.gen + 1);
+    } else {
+      while (ld_acquire_u32(a.sync_gen) == rs.gen) {
+      }
+    }
+  }
+  rs.gen += 1;
+  __syncthreads();
+}
+
 template <int NV>
-__device__ void grid_reduce(const FFArgs& a, cg::grid_group& grid, Red& rs, double (&v)[NV]) {
+__device__ void grid_reduce(const FFArgs& a, Red& rs, double (&v)[NV], PhaseClock* pc = nullptr) {
   __shared__ double smem[4 * 32];
   __shared__ double bcast[4];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  double* base = a.partials + size_t(rs.region) * 4 * gridDim.x;
 #pragma unroll
   for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
   if (lane == 0)
 #pragma unroll
     for (int k = 0; k < NV; ++k) smem[k * 32 + warp] = v[k];
   __syncthreads();
+  if (pc) pc->lap(6);
   if (warp == 0) {
+    double s[NV];
 #pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      const double s = warp_sum(lane < nw ? smem[k * 32 + lane] : 0.0);
-      if (lane == 0) base[size_t(k) * gridDim.x + blockIdx.x] = s;
-    }
-  }
-  grid.sync();
-  if (warp == 0) {
+    for (int k = 0; k < NV; ++k) s[k] = warp_sum(lane < nw ? smem[k * 32 + lane] : 0.0);
+    unsigned last = 0;
+    if (lane == 0) {
 #pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      const double s = sum_partials(base + size_t(k) * gridDim.x, gridDim.x);
-      if (lane == 0) bcast[k] = s;
+      for (int k = 0; k < NV; ++k) a.partials[size_t(k) * gridDim.x + blockIdx.x] = s[k];
+      __threadfence();
+      last = atom_add_acq_rel_u32(a.sync_count, 1u) == gridDim.x - 1 ? 1u : 0u;
     }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+      __threadfence();
+#pragma unroll
+      for (int k = 0; k < NV; ++k) s[k] = sum_partials(a.partials + size_t(k) * gridDim.x, gridDim.x);
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) a.sync_total[k] = s[k];
+        *a.sync_count = 0;
+        st_release_u32(a.sync_gen, rs.gen + 1);
+      }
+    } else if (lane == 0) {
+      while (ld_acquire_u32(a.sync_gen) == rs.gen) {
+      }
+    }
+    if (lane == 0)
+#pragma unroll
+      for (int k = 0; k < NV; ++k) bcast[k] = __ldcg(a.sync_total + k);
   }
+  rs.gen += 1;
+  if (pc) pc->lap(7);
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < NV; ++k) v[k] = bcast[k];
-  rs.region ^= 1;
+  if (pc) pc->lap(13);
 }
 
 // Work distribution of the persistent kernel: chunks of 32 consecutive items
@@ -503,7 +587,7 @@ __device__ wfk_energy energy(const FFArgs& a, cg::grid_group& grid, Red& rs, boo
   int bad = 0;
   energy_partials(a, es, ed, er, bad);
   double v[4] = {es, ed, er, double(bad)};
-  grid_reduce<4>(a, grid, rs, v);
+  grid_reduce<4>(a, rs, v);
   wfk_energy e;
   e.sparse = v[0];
   e.dense = v[1];
@@ -582,35 +666,69 @@ __device__ __forceinline__ V3 matvec_row(const FFArgs& a, const double4* v, int 
   return laplacian(a, v, r, vr, acc);
 }
 
-// (A v)_r for every row, delivered once per row to sink(r, v_r, (A v)_r).
-// Matrix-free levels hand rows with more than kHeavyRow incidences to a whole
-// warp: lanes stride the row's contiguous contributions (coalesced 256-bit
-// loads), lanes 0-5 take one stencil neighbour each, fixed shuffle tree.
+// (A v)_r for every row, delivered once per row to the group leader as
+// sink(r, v_r, (A v)_r).
+//  * Assembled levels: a group of kAsmLanes lanes per row, each lane a few of
+//    the 27 stencil slots (one parallel round of gathers), folding the ARAP
+//    Laplacian into the six face slots, then a sub-warp shuffle tree.
+//  * Matrix-free levels: one thread per light row summing its contiguous
+//    incidence contributions; rows with more than kHeavyRow incidences go to
+//    a whole warp (coalesced 256-bit loads, lanes 0-5 one face neighbour each).
 template <bool ASM, class Sink>
 __device__ __forceinline__ void row_pass(const FFArgs& a, const double4* v, Sink& sink) {
-  for (int r = int(gtid()); r < a.N; r += int(gstride())) {
-    if (!ASM && a.row_ptr[r + 1] - a.row_ptr[r] > kHeavyRow) continue;
-    const V3 vr = ld4(v, r);
-    sink(r, vr, matvec_row<ASM>(a, v, r, vr));
-  }
-  if (!ASM) {
-    const int lane = threadIdx.x & 31;
-    const double w2 = 2.0 * a.w_r;
-    for (int h = gwarp(); h < a.n_heavy; h += nwarps()) {
-      const int r = a.heavy[h];
-      const int e0 = a.row_ptr[r], e1 = a.row_ptr[r + 1];
-      const V3 vr = ld4(v, r);
+  const int lane = threadIdx.x & 31;
+  const double w2 = 2.0 * a.w_r;
+  if (ASM) {
+    constexpr int L = kAsmLanes, RPW = 32 / L;
+    const int sub = lane % L, grp = lane / L;
+    for (int base = gwarp() * RPW; base < a.N; base += nwarps() * RPW) {
+      const int r = base + grp;
+      const bool live = r < a.N;
+      const bool frozen = live && a.frozen[r];
+      const V3 vr = live ? ld4(v, r) : V3{0, 0, 0};
       V3 acc{0, 0, 0};
-      for (int e = e0 + lane; e < e1; e += 32) acc += ld4(a.contrib, e);
-      if (lane < 6) {
-        const int j = a.nbr[int64_t(lane) * a.N + r];
-        if (j >= 0) acc += w2 * (vr - ld4(v, j));
+      if (live && !frozen) {
+#pragma unroll
+        for (int s = sub; s < 27; s += L) {
+          const int col = a.cols[int64_t(r) * 27 + s];
+          if (col < 0) continue;
+          const V3 x = ld4(v, col);
+          const double* b = a.blk + (int64_t(r) * 27 + s) * 6;  // xx xy xz yy yz zz
+          acc.x += b[0] * x.x + b[1] * x.y + b[2] * x.z;
+          acc.y += b[1] * x.x + b[3] * x.y + b[4] * x.z;
+          acc.z += b[2] * x.x + b[4] * x.y + b[5] * x.z;
+          if (s == 4 || s == 10 || s == 12 || s == 14 || s == 16 || s == 22) acc += w2 * (vr - x);
+        }
       }
-      acc.x = warp_sum(acc.x);
-      acc.y = warp_sum(acc.y);
-      acc.z = warp_sum(acc.z);
-      if (lane == 0) sink(r, vr, a.frozen[r] ? vr : acc);
+#pragma unroll
+      for (int o = L / 2; o > 0; o >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+        acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+      }
+      if (live && sub == 0) sink(r, vr, frozen ? vr : acc);
     }
+    return;
+  }
+  for (int r = int(gtid()); r < a.N; r += int(gstride())) {
+    if (a.row_ptr[r + 1] - a.row_ptr[r] > kHeavyRow) continue;
+    const V3 vr = ld4(v, r);
+    sink(r, vr, matvec_row<false>(a, v, r, vr));
+  }
+  for (int h = gwarp(); h < a.n_heavy; h += nwarps()) {
+    const int r = a.heavy[h];
+    const int e0 = a.row_ptr[r], e1 = a.row_ptr[r + 1];
+    const V3 vr = ld4(v, r);
+    V3 acc{0, 0, 0};
+    for (int e = e0 + lane; e < e1; e += 32) acc += ld4(a.contrib, e);
+    if (lane < 6) {
+      const int j = a.nbr[int64_t(lane) * a.N + r];
+      if (j >= 0) acc += w2 * (vr - ld4(v, j));
+    }
+    acc.x = warp_sum(acc.x);
+    acc.y = warp_sum(acc.y);
+    acc.z = warp_sum(acc.z);
+    if (lane == 0) sink(r, vr, a.frozen[r] ? vr : acc);
   }
 }
 
@@ -644,93 +762,160 @@ __device__ void assemble_rows(const FFArgs& a) {
   }
 }
 
-// pcg_solve (solver.cpp:282-343); x in/out.  Per iteration:
-//   P  p = z + beta p (own rows)                              -> barrier
-//   A  constraint pass of A p  (matrix-free levels only)       -> barrier
-//   B  row pass: A p, p.Ap                                     -> reduction
-//   C  x += alpha p, r -= alpha Ap, r.z, r.r                   -> reduction
-// The arithmetic of every vector element is the reference's; only where it is
-// evaluated moves.
+// Matrix-free row pass, load-balanced: every row's contiguous incidence
+// contributions are cut into work items of at most kItemLen entries (fixed
+// per solve).  Item 0 of a row also carries the ARAP Laplacian.  Each item
+// writes its partial (A v) into wpart[item]; the update phase adds a row's
+// items in order, and the p.Ap / w.u dot is accumulated per item (it is
+// linear), so no row waits on another's long list.
+template <class Sink>
+__device__ __forceinline__ void item_pass(const FFArgs& a, const double4* v, Sink& sink) {
+  const double w2 = 2.0 * a.w_r;
+  for (int i = int(gtid()); i < a.n_items; i += int(gstride())) {
+    const int4 it = a.items[i];  // row, e_begin, e_end, first
+    const int r = it.x;
+    const V3 vr = ld4(v, r);
+    V3 acc{0, 0, 0};
+    if (a.frozen[r]) {
+      acc = vr;  // frozen rows: A = I (solver.cpp:241-246); they carry no incidences
+    } else {
+#pragma unroll 4
+      for (int e = it.y; e < it.z; ++e) acc += ld4(a.contrib, e);
+      if (it.w) {
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+          const int j = a.nbr[int64_t(k) * a.N + r];
+          if (j >= 0) acc += w2 * (vr - ld4(v, j));
+        }
+      }
+    }
+    st4(a.wpart, i, acc);
+    sink(r, vr, acc);
+  }
+}
+
+// (A v)_r of one row from its items (fixed order)
+WF_D V3 row_from_items(const FFArgs& a, int r) {
+  V3 acc{0, 0, 0};
+  for (int i = a.item_ptr[r]; i < a.item_ptr[r + 1]; ++i) acc += ld4(a.wpart, i);
+  return acc;
+}
+
+// pcg_solve (solver.cpp:282-343) in the Chronopoulos-Gear arrangement: the
+// same Krylov iterates (p = u + beta p, x += alpha p, r -= alpha A p with
+// u = D^-1 r, alpha = r.u / p.Ap, beta = r.u / r.u_prev), but s = A p and
+// w = A u are carried as vectors, so p.Ap = w.u - beta r.u / alpha_prev and
+// every iteration needs ONE grid reduction {r.u, w.u, r.r}:
+//   U  w from its items, p, s, x, r, u update (own rows)  -> barrier
+//   A  constraint pass of A u (matrix-free levels only)    -> barrier
+//   B  item pass (matrix-free) | row pass (assembled)      -> reduction
+// The stopping rule, breakdown test and iteration count are the reference's.
 template <bool ASM>
 __device__ void pcg(const FFArgs& a, cg::grid_group& grid, Red& rs, int& iters, double& relres) {
   iters = 0;
   relres = 0;
   PhaseClock pc(a.dbg);
-  // r = b - A x (solver.cpp:305-310)
-  if (!ASM) {
-    matvec_constraints(a, a.x);
-    grid.sync();
-  }
-  double v3[3] = {0, 0, 0};
-  auto init_sink = [&](int r, V3, V3 ax) {
+  auto none = [](int, V3, V3) {};
+  // r0 = b - A x0, u0 = D^-1 r0 (solver.cpp:305-310)
+  double acc_rr = 0, acc_bb = 0;
+  auto init_row = [&](int r, V3 ax) {
     const V3 b = ld4(a.rhs, r);
     const V3 rr = b - ax;
-    const V3 z = cmul(ld4(a.dinv, r), rr);
     st4(a.r, r, rr);
-    st4(a.p, r, V3{0, 0, 0});
-    v3[0] += dot(rr, z);
-    v3[1] += dot(rr, rr);
-    v3[2] += sqnorm(b);
+    st4(a.u, r, cmul(ld4(a.dinv, r), rr));
+    a.p[r] = make_double4(0, 0, 0, 0);
+    a.ap[r] = make_double4(0, 0, 0, 0);
+    acc_rr += dot(rr, rr);
+    acc_bb += sqnorm(b);
   };
-  row_pass<ASM>(a, a.x, init_sink);
-  grid_reduce<3>(a, grid, rs, v3);
-  double rz = v3[0];
-  double r_norm = sqrt(v3[1]);
-  const double b_norm = sqrt(v3[2]);
+  if (ASM) {
+    auto init_sink = [&](int r, V3, V3 ax) { init_row(r, ax); };
+    row_pass<true>(a, a.x, init_sink);
+  } else {
+    matvec_constraints(a, a.x);
+    grid_barrier(a, rs);
+    item_pass(a, a.x, none);
+    grid_barrier(a, rs);
+    for (int r = int(gtid()); r < a.N; r += int(gstride())) init_row(r, row_from_items(a, r));
+  }
+  grid_barrier(a, rs);
+  // w0 = A u0
+  double v4[4] = {0, 0, acc_rr, acc_bb};
+  if (ASM) {
+    auto w_sink = [&](int r, V3 ur, V3 wr) {
+      st4(a.w, r, wr);
+      v4[0] += dot(ld4(a.r, r), ur);
+      v4[1] += dot(wr, ur);
+    };
+    row_pass<true>(a, a.u, w_sink);
+  } else {
+    matvec_constraints(a, a.u);
+    grid_barrier(a, rs);
+    auto w_sink = [&](int, V3 ur, V3 wpart) { v4[1] += dot(wpart, ur); };
+    item_pass(a, a.u, w_sink);
+    for (int r = int(gtid()); r < a.N; r += int(gstride())) v4[0] += dot(ld4(a.r, r), ld4(a.u, r));
+  }
+  grid_reduce<4>(a, rs, v4);
+  double gamma = v4[0], delta = v4[1];
+  double r_norm = sqrt(v4[2]);
+  const double b_norm = sqrt(v4[3]);
   if (b_norm == 0) {
     for (int r = int(gtid()); r < a.N; r += int(gstride())) st4(a.x, r, V3{0, 0, 0});
-    grid.sync();
+    grid_barrier(a, rs);
     return;
   }
   relres = r_norm / b_norm;
   const double stop = fmax(a.pcg_tol * r_norm, 1e-13 * b_norm);
-  double beta = 0.0;  // first direction: p = z
+  double gamma_prev = 0, alpha_prev = 0;
   pc.lap(12);
   for (int it = 0; it < a.pcg_max && r_norm > stop; ++it) {
+    const double beta = it == 0 ? 0.0 : gamma / gamma_prev;
+    const double pap = it == 0 ? delta : delta - beta * gamma / alpha_prev;
+    if (pap <= 0) break;  // solver.cpp:327
+    const double alpha = gamma / pap;
+    double v3[3] = {0, 0, 0};
     for (int r = int(gtid()); r < a.N; r += int(gstride())) {
-      const V3 z = cmul(ld4(a.dinv, r), ld4(a.r, r));
-      st4(a.p, r, z + beta * ld4(a.p, r));
-    }
-    pc.lap(6);
-    grid.sync();
-    pc.lap(7);
-    if (!ASM) {
-      matvec_constraints(a, a.p);
-      pc.lap(0);
-      grid.sync();
-      pc.lap(1);
-    }
-    double v1[1] = {0};
-    auto ap_sink = [&](int r, V3 pr, V3 apr) {
-      st4(a.ap, r, apr);
-      v1[0] += dot(pr, apr);
-    };
-    row_pass<ASM>(a, a.p, ap_sink);
-    pc.lap(2);
-    grid_reduce<1>(a, grid, rs, v1);
-    pc.lap(3);
-    const double pap = v1[0];
-    if (pap <= 0) break;
-    const double alpha = rz / pap;
-    double v2[2] = {0, 0};
-    for (int r = int(gtid()); r < a.N; r += int(gstride())) {
-      const double4 x4 = a.x[r], p4 = a.p[r], r4 = a.r[r], ap4 = a.ap[r], d4 = a.dinv[r];
-      const V3 xn = V3{x4.x, x4.y, x4.z} + alpha * V3{p4.x, p4.y, p4.z};
-      const V3 rr = V3{r4.x, r4.y, r4.z} - alpha * V3{ap4.x, ap4.y, ap4.z};
-      st4(a.x, r, xn);
+      const V3 w = ASM ? ld4(a.w, r) : row_from_items(a, r);
+      const double4 u4 = a.u[r], p4 = a.p[r], s4 = a.ap[r], x4 = a.x[r], r4 = a.r[r], d4 = a.dinv[r];
+      const V3 p = V3{u4.x, u4.y, u4.z} + beta * V3{p4.x, p4.y, p4.z};
+      const V3 sv = w + beta * V3{s4.x, s4.y, s4.z};
+      const V3 x = V3{x4.x, x4.y, x4.z} + alpha * p;
+      const V3 rr = V3{r4.x, r4.y, r4.z} - alpha * sv;
+      const V3 u = cmul(V3{d4.x, d4.y, d4.z}, rr);
+      st4(a.p, r, p);
+      st4(a.ap, r, sv);
+      st4(a.x, r, x);
       st4(a.r, r, rr);
-      const V3 z = cmul(V3{d4.x, d4.y, d4.z}, rr);
-      v2[0] += dot(rr, z);
-      v2[1] += dot(rr, rr);
+      st4(a.u, r, u);
+      v3[0] += dot(rr, u);
+      v3[2] += dot(rr, rr);
     }
     pc.lap(4);
-    grid_reduce<2>(a, grid, rs, v2);
+    grid_barrier(a, rs);
     pc.lap(5);
+    if (ASM) {
+      auto w_sink2 = [&](int r, V3 ur, V3 wr) {
+        st4(a.w, r, wr);
+        v3[1] += dot(wr, ur);
+      };
+      row_pass<true>(a, a.u, w_sink2);
+    } else {
+      matvec_constraints(a, a.u);
+      pc.lap(0);
+      grid_barrier(a, rs);
+      pc.lap(1);
+      auto w_sink2 = [&](int, V3 ur, V3 wpart) { v3[1] += dot(wpart, ur); };
+      item_pass(a, a.u, w_sink2);
+    }
+    pc.lap(2);
+    grid_reduce<3>(a, rs, v3, &pc);
+    pc.lap(3);
     pc.count(15);
-    const double rz_new = v2[0];
-    beta = rz_new / rz;
-    rz = rz_new;
-    r_norm = sqrt(v2[1]);
+    gamma_prev = gamma;
+    alpha_prev = alpha;
+    gamma = v3[0];
+    delta = v3[1];
+    r_norm = sqrt(v3[2]);
     relres = r_norm / b_norm;
     iters = it + 1;
   }
@@ -776,7 +961,7 @@ __global__ void __launch_bounds__(kCoopBlock, 1) k_flip_flop(FFArgs a) {
     st4(a.t, r, ld3(a.field_def, node));
     st_m3(a.rot, r, euler_to_matrix(ld3(a.field_eul, node)));
   }
-  grid.sync();
+  grid_barrier(a, rs);
   if (a.mode == 2) {
     rotations(a);
     return;
@@ -802,7 +987,7 @@ __global__ void __launch_bounds__(kCoopBlock, 1) k_flip_flop(FFArgs a) {
       // assemble rhs / diagonal with the current rotations; x0 = t
       assemble_rows(a);
       for (int r = int(gtid()); r < a.N; r += int(gstride())) a.x[r] = a.t[r];
-      grid.sync();
+      grid_barrier(a, rs);
       pc.lap(8);
       int iters;
       double relres;
@@ -819,9 +1004,9 @@ __global__ void __launch_bounds__(kCoopBlock, 1) k_flip_flop(FFArgs a) {
         st4(a.t, r, xr);
         st3(a.field_def, a.rows[r], xr);
       }
-      grid.sync();
+      grid_barrier(a, rs);
       rotations(a);
-      grid.sync();
+      grid_barrier(a, rs);
       pc.lap(10);
       bool dummy;
       const wfk_energy e = energy(a, grid, rs, dummy);
@@ -1074,7 +1259,8 @@ static void level_rows(wfk_ctx* c, Level& L) {
   L.uf.ensure(Nc);
   L.frozen.ensure(Nc);
   L.comp_flag.ensure(Nc);
-  for (DevBuf<double4>* b : {&L.t, &L.x, &L.rhs, &L.r, &L.p, &L.ap, &L.dinv, &L.crhs, &L.cdiag}) b->ensure(Nc);
+  for (DevBuf<double4>* b : {&L.t, &L.x, &L.rhs, &L.r, &L.p, &L.ap, &L.dinv, &L.u, &L.w, &L.crhs, &L.cdiag})
+    b->ensure(Nc);
   L.rot.ensure(9 * Nc);
   L.row_ptr.ensure(Nc + 1);
   L.cnt.ensure(Nc + 1);
@@ -1157,21 +1343,24 @@ static void level_constraints(wfk_ctx* c, Level& L, const PoseD& pose, const wfk
   // assembled once per solve, so the PCG row pass is a fixed 27-block stencil.
   L.assembled = L.E > int64_t(kAssembleRatio) * N;
   L.n_heavy = 0;
-  if (!L.assembled && L.E > 0) {
-    L.contrib.ensure(size_t(L.E));
-    L.heavy.ensure(size_t(N) + 1);
-    uint8_t* flag = c->mask.ensure(size_t(std::max<int64_t>(2 * c->vol.n, N)) + 1);
-    k_heavy_flags<<<grid_for(N), kBlock, 0, s>>>(N, L.row_ptr, flag);
-    int32_t* d_nh = c->ivec.ensure(16) + 3;
-    size_t tmp3 = 0;
-    thrust::counting_iterator<int32_t> it(0);
-    cub::DeviceSelect::Flagged(nullptr, tmp3, it, flag, L.heavy.p, d_nh, N, s);
-    c->temp.ensure(tmp3);
-    WFK_CUDA(cub::DeviceSelect::Flagged(c->temp.p, tmp3, it, flag, L.heavy.p, d_nh, N, s));
-    count_launch(c, 2);
-    WFK_CUDA(cudaMemcpyAsync(c->h_pinned + 3, d_nh, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  if (!L.assembled && L.E > 0) L.contrib.ensure(size_t(L.E));
+  L.n_items = 0;
+  if (!L.assembled) {
+    L.item_ptr.ensure(size_t(N) + 1);
+    int32_t* cnt_items = L.cnt.p;  // per-row item counts (cnt is free after the row_ptr scan)
+    k_item_count<<<grid_for(N), kBlock, 0, s>>>(N, L.row_ptr, cnt_items);
+    WFK_CUDA(cudaMemsetAsync(cnt_items + N, 0, sizeof(int32_t), s));
+    size_t tmp4 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp4, cnt_items, L.item_ptr.p, N + 1, s);
+    c->temp.ensure(tmp4);
+    WFK_CUDA(cub::DeviceScan::ExclusiveSum(c->temp.p, tmp4, cnt_items, L.item_ptr.p, N + 1, s));
+    WFK_CUDA(cudaMemcpyAsync(c->h_pinned + 5, L.item_ptr.p + N, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     sync_check(c);
-    L.n_heavy = c->h_pinned[3];
+    L.n_items = c->h_pinned[5];
+    L.items.ensure(size_t(L.n_items) + 1);
+    L.wpart.ensure(size_t(L.n_items) + 1);
+    k_item_write<<<grid_for(N), kBlock, 0, s>>>(N, L.row_ptr, L.item_ptr, L.items);
+    count_launch(c, 3);
   }
   if (L.assembled) {
     L.blk.ensure(size_t(N) * 27 * 6);
@@ -1235,6 +1424,8 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   a.rhs = L.rhs;
   a.r = L.r;
   a.p = L.p;
+  a.u = L.u;
+  a.w = L.w;
   a.assembled = L.assembled ? 1 : 0;
   a.blk = L.blk;
   a.cols = L.cols;
@@ -1255,7 +1446,17 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   a.contrib = L.contrib;
   a.heavy = L.heavy;
   a.n_heavy = L.n_heavy;
+  a.items = L.items;
+  a.n_items = L.n_items;
+  a.item_ptr = L.item_ptr;
+  a.wpart = L.wpart;
   a.partials = c->partials.ensure(size_t(8) * G);
+  // barrier state: count, generation, totals on separate 128 B lines
+  unsigned* sync = reinterpret_cast<unsigned*>(c->sync_words.ensure(128));
+  WFK_CUDA(cudaMemsetAsync(sync, 0, 3 * 128, s));
+  a.sync_count = sync;
+  a.sync_gen = sync + 32;
+  a.sync_total = reinterpret_cast<double*>(sync + 64);
   a.trace = c->trace.ensure(size_t(std::max(p.flip_flop_iters, 1)));
   int32_t* status = c->ivec.ensure(16) + 4;
   double* eout = c->eout.ensure(8);
@@ -1303,7 +1504,7 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
         mx = std::max(mx, v);
       }
     };
-    const char* names[8] = {"A", "Async", "B", "red1", "C", "red2", "P", "Psync"};
+    const char* names[8] = {"A", "Async", "B", "red-", "U", "Usync", "redblk", "redsync"};
     fprintf(stderr, "[wfk phase] level %d N %d C %lld asm %d heavy %d iters %.0f | cycles/iter mean/max:", level_tag,
             L.N, (long long)L.C, int(L.assembled), L.n_heavy, it);
     for (int k = 0; k < 8; ++k) {
@@ -1311,8 +1512,10 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
       stat(k, m, x);
       fprintf(stderr, " %s %.0f/%.0f", names[k], m, x);
     }
-    fprintf(stderr, " | blk0 Mcyc/launch: assemble %.2f pcg %.2f rot %.2f energy %.2f\n", d[8] * 1e-6, d[9] * 1e-6,
-            d[10] * 1e-6, d[11] * 1e-6);
+    double m13, x13;
+    stat(13, m13, x13);
+    fprintf(stderr, " redsum %.0f/%.0f | blk0 Mcyc/launch: assemble %.2f pcg %.2f rot %.2f energy %.2f\n", m13, x13,
+            d[8] * 1e-6, d[9] * 1e-6, d[10] * 1e-6, d[11] * 1e-6);
   }
   if (pf.on && mode == 0) {
     float ms = 0;

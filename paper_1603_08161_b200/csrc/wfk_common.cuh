@@ -21,6 +21,8 @@ constexpr int kBlock = 256;
 constexpr int kCoopBlock = 512;     // persistent cooperative kernels: 1 block / SM
 constexpr int kAssembleRatio = 32;  // incidences per row above which B^T B is assembled
 constexpr int kHeavyRow = 16;       // incidences above which a row is summed by a whole warp
+constexpr int kAsmLanes = 8;        // lanes per row on assembled levels (27 stencil slots)
+constexpr int kItemLen = 8;         // incidences per work item of the matrix-free row pass
 constexpr int kCenter = 13;
 
 struct V3 {

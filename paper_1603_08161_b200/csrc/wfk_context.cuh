@@ -96,7 +96,7 @@ struct Level {
   DevBuf<int32_t> rows, node_row, nbr, uf;  // nbr: 6 x Ncap SoA
   DevBuf<uint8_t> frozen, comp_flag;
   // per-row state (AoS double3 / row-major 3x3)
-  DevBuf<double4> t, x, rhs, r, p, ap, dinv, crhs, cdiag;  // 32 B padded 3-vectors
+  DevBuf<double4> t, x, rhs, r, p, ap, dinv, u, w, crhs, cdiag;  // 32 B padded 3-vectors
   DevBuf<double> rot;
   // assembled B^T B for rows with many incidences (see kAssembleRatio)
   bool assembled = false;
@@ -107,6 +107,10 @@ struct Level {
   DevBuf<double4> contrib; // E: per-incidence matvec contributions
   DevBuf<int32_t> heavy;   // rows summed by a whole warp
   int n_heavy = 0;
+  DevBuf<int4> items;      // balanced matrix-free work items
+  DevBuf<int32_t> item_ptr;
+  DevBuf<double4> wpart;
+  int n_items = 0;
   // level constraints
   int64_t C = 0;
   DevBuf<int32_t> c_node;   // 8C anchors at this level
@@ -157,7 +161,7 @@ struct MeshDev {
   DevBuf<uint8_t> tri_keep;
   DevBuf<int32_t> tri_pos;
   // vertex -> incident triangles (ascending), for compute_normals
-  DevBuf<int32_t> adj_ptr, adj_tri;
+  DevBuf<int32_t> adj_ptr, adj_tri, adj_key, adj_val, adj_key2, adj_cnt;
   bool adj_valid = false;
   bool normals_valid = false;
 };
@@ -218,6 +222,7 @@ struct wfk_ctx {
   wfk::DevBuf<uint8_t> l2_flush;
   // scratch
   wfk::DevBuf<double> partials;
+  wfk::DevBuf<uint32_t> sync_words;  // grid barrier state of the persistent kernel
   wfk::DevBuf<int32_t> flags;   // device status words
   wfk::DevBuf<uint8_t> temp;    // cub temp storage
   wfk::DevBuf<wfk_trace_entry> trace;
