@@ -214,6 +214,7 @@ int wfk_volume_upload(wfk_ctx* c, const wfk_volume_view* v, uint32_t fields) {
     up(WFK_VOL_EULER, d.euler, v->euler, size_t(n) * 24);
     up(WFK_VOL_AGE, d.age, v->age, size_t(n) * 4);
     up(WFK_VOL_ACTIVE, d.active, v->active, size_t(n));
+    if (fields & WFK_VOL_ACTIVE) ++d.active_gen;
     WFK_CUDA(cudaStreamSynchronize(s));
     d.valid = true;
   });

@@ -65,6 +65,7 @@ static void active_set_device(wfk_ctx* c) {
   k_surface_cells<<<grid_for(ncell), kBlock, 0, s>>>(v.g, v.tsdf, v.weight, on);
   k_dilate<<<grid_for(v.n), kBlock, 0, s>>>(v.g, on, v.active);
   count_launch(c, 2);
+  ++v.active_gen;
   WFK_CUDA(cudaGetLastError());
 }
 

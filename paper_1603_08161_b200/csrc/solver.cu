@@ -55,19 +55,31 @@ __global__ void k_row_neighbours(Grid g, const int32_t* rows, int N, const int32
       const int a = x + kFace[k][0], b = y + kFace[k][1], c = z + kFace[k][2];
       nbr[int64_t(k) * N + r] = g.in_grid(a, b, c) ? node_row[g.lin(a, b, c)] : -1;
     }
-    uf[r] = r;
+    int m = r;  // hook to the smallest neighbour: parents stay <= children
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      const int j = nbr[int64_t(k) * N + r];
+      if (j >= 0 && j < m) m = j;
+    }
+    uf[r] = m;
   }
 }
 
-// lock-free union-find; a set's root is always its smallest row, so the final
-// partition and labels are independent of the race order.
-__device__ int uf_find(volatile int32_t* uf, int a) {
-  int p = uf[a];
-  while (p != a) {
-    a = p;
-    p = uf[a];
+// Lock-free union-find (ECL-CC style): a parent is never larger than its
+// child, so a set's root is its smallest row and the final labels are
+// independent of the race order.  find() halves paths as it walks.
+__device__ __forceinline__ int uf_find(int32_t* uf_, int x) {
+  volatile int32_t* uf = uf_;
+  int cur = uf[x];
+  if (cur != x) {
+    int next, prev = x;
+    while (cur > (next = uf[cur])) {
+      uf[prev] = next;
+      prev = cur;
+      cur = next;
+    }
   }
-  return a;
+  return cur;
 }
 __global__ void k_union(const int32_t* nbr, int N, int32_t* uf) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x) {
@@ -75,19 +87,17 @@ __global__ void k_union(const int32_t* nbr, int N, int32_t* uf) {
     for (int k = 0; k < 6; k += 2) {  // +x, +y, +z edges cover every edge once
       const int j = nbr[int64_t(k) * N + r];
       if (j < 0) continue;
-      int a = r, b = j;
-      while (true) {
-        a = uf_find(uf, a);
-        b = uf_find(uf, b);
-        if (a == b) break;
+      int a = uf_find(uf, r), b = uf_find(uf, j);
+      while (a != b) {
         if (a < b) {
-          int t = a;
+          const int t = a;
           a = b;
           b = t;
         }
         const int old = atomicCAS(&uf[a], a, b);
         if (old == a) break;
-        a = old;
+        a = uf_find(uf, old);
+        b = uf_find(uf, b);
       }
     }
   }
@@ -166,17 +176,19 @@ __global__ void k_entries(int64_t E, const int32_t* sorted_val, const double* c_
 }
 
 // work items of the balanced matrix-free row pass (see item_pass)
-__global__ void k_item_count(int N, const int32_t* row_ptr, int32_t* n_items) {
+__global__ void k_item_count(int N, const int32_t* row_ptr, int32_t* n_extra) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x) {
     const int cnt = row_ptr[r + 1] - row_ptr[r];
-    n_items[r] = cnt > 0 ? (cnt + kItemLen - 1) / kItemLen : 1;
+    n_extra[r] = cnt > kItemLen ? (cnt - 1) / kItemLen : 0;  // items beyond the row's first
   }
 }
-__global__ void k_item_write(int N, const int32_t* row_ptr, const int32_t* item_ptr, int4* items) {
+__global__ void k_item_write(int N, const int32_t* row_ptr, const int32_t* xptr, int4* xitems, int2* xrange) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x) {
     const int e0 = row_ptr[r], e1 = row_ptr[r + 1];
-    for (int i = item_ptr[r], k = 0; i < item_ptr[r + 1]; ++i, ++k)
-      items[i] = make_int4(r, e0 + k * kItemLen, min(e1, e0 + (k + 1) * kItemLen), k == 0 ? 1 : 0);
+    const int x0 = xptr[r], x1 = xptr[r + 1];
+    for (int i = x0, k = 1; i < x1; ++i, ++k)
+      xitems[i] = make_int4(r, e0 + k * kItemLen, min(e1, e0 + (k + 1) * kItemLen), 0);
+    xrange[r] = make_int2(x0, x1 - x0);
   }
 }
 
@@ -186,21 +198,20 @@ __global__ void k_heavy_flags(int N, const int32_t* row_ptr, uint8_t* flag) {
 }
 
 // Cached B^T B of one (row, stencil slot): sum over the row's incidences of
-// coef a_i a_k (g g^T | I) for the anchor k at that slot, in the reference's
-// accumulation order (solver.cpp:196-226); symmetric 3x3 stored as 6 values.
-// Columns follow solver.cpp:149-160.
+// coef a_i a_k (g g^T | I) for the anchor k at that slot (solver.cpp:196-226),
+// symmetric 3x3 stored as 6 values; columns follow solver.cpp:149-160.  One
+// warp per (row, slot): lanes stride the row's incidence list (thousands on
+// the coarse levels), fixed shuffle tree.
 __global__ void k_assemble_btb(Grid g, int N, const int32_t* rows, const int32_t* node_row, const int32_t* row_ptr,
                                const int32_t* ent_con, const uint8_t* ent_k, const double* ent_w, const double* c_w,
                                const double* c_g, const int32_t* c_kind, double* blk, int32_t* cols) {
-  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < int64_t(N) * 27;
-       t += int64_t(gridDim.x) * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t t = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; t < int64_t(N) * 27; t += warps) {
     const int r = int(t / 27), s = int(t % 27);
     const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = s / 9 - 1;
-    int x, y, z;
-    g.idx3(rows[r], x, y, z);
-    cols[t] = g.in_grid(x + dx, y + dy, z + dz) ? node_row[g.lin(x + dx, y + dy, z + dz)] : -1;
     double b[6] = {0, 0, 0, 0, 0, 0};
-    for (int e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
+    for (int e = row_ptr[r] + lane; e < row_ptr[r + 1]; e += 32) {
       const int ki = ent_k[e];
       const int ox = (ki & 1) + dx, oy = ((ki >> 1) & 1) + dy, oz = (ki >> 2) + dz;
       if (ox < 0 || ox > 1 || oy < 0 || oy > 1 || oz < 0 || oz > 1) continue;
@@ -221,37 +232,71 @@ __global__ void k_assemble_btb(Grid g, int N, const int32_t* rows, const int32_t
         b[5] += sc * 1.0;
       }
     }
-    for (int m = 0; m < 6; ++m) blk[t * 6 + m] = b[m];
+#pragma unroll
+    for (int m = 0; m < 6; ++m) b[m] = warp_sum(b[m]);
+    if (lane == 0) {
+      int x, y, z;
+      g.idx3(rows[r], x, y, z);
+      cols[t] = g.in_grid(x + dx, y + dy, z + dz) ? node_row[g.lin(x + dx, y + dy, z + dz)] : -1;
+      for (int m = 0; m < 6; ++m) blk[t * 6 + m] = b[m];
+    }
   }
 }
 
 // ConstraintCache (solver.hpp:66-70): constraint part of the rhs and of the
-// Jacobi diagonal, accumulated in the reference's order (solver.cpp:196-226).
+// Jacobi diagonal.  Rows with at most kCacheWarpRow incidences accumulate in
+// the reference's order (solver.cpp:196-226) on one thread; longer rows (the
+// coarse levels) are summed by a warp with a fixed shuffle tree.
+WF_D void cache_term(int c, double a, const int32_t* c_kind, const double* c_g, const double* c_b, V3& rhs,
+                     V3& diag) {
+  const V3 g{c_g[4 * c], c_g[4 * c + 1], c_g[4 * c + 2]};
+  const double coef = c_g[4 * c + 3];
+  const double s = coef * a * a;
+  if (c_kind[c] == WFK_DENSE_PLANE) {
+    diag.x += s * (g.x * g.x);
+    diag.y += s * (g.y * g.y);
+    diag.z += s * (g.z * g.z);
+    rhs -= (coef * a * c_b[c]) * g;
+  } else {
+    diag.x += s * 1.0;
+    diag.y += s * 1.0;
+    diag.z += s * 1.0;
+    rhs += (coef * a) * g;
+  }
+}
+
 __global__ void k_constraint_cache(int N, const int32_t* row_ptr, const int32_t* ent_con, const double* ent_w,
                                    const int32_t* c_kind, const double* c_g, const double* c_b, double4* crhs,
                                    double4* cdiag) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x) {
+    if (row_ptr[r + 1] - row_ptr[r] > kCacheWarpRow) continue;
     V3 rhs{0, 0, 0}, diag{0, 0, 0};
-    for (int e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
-      const int c = ent_con[e];
-      const double a = ent_w[e];
-      const V3 g{c_g[4 * c], c_g[4 * c + 1], c_g[4 * c + 2]};
-      const double coef = c_g[4 * c + 3];
-      const double s = coef * a * a;
-      if (c_kind[c] == WFK_DENSE_PLANE) {
-        diag.x += s * (g.x * g.x);
-        diag.y += s * (g.y * g.y);
-        diag.z += s * (g.z * g.z);
-        rhs -= (coef * a * c_b[c]) * g;
-      } else {
-        diag.x += s * 1.0;
-        diag.y += s * 1.0;
-        diag.z += s * 1.0;
-        rhs += (coef * a) * g;
-      }
-    }
+    for (int e = row_ptr[r]; e < row_ptr[r + 1]; ++e) cache_term(ent_con[e], ent_w[e], c_kind, c_g, c_b, rhs, diag);
     crhs[r] = make_double4(rhs.x, rhs.y, rhs.z, 0.0);
     cdiag[r] = make_double4(diag.x, diag.y, diag.z, 0.0);
+  }
+}
+
+__global__ void k_constraint_cache_warp(int N, const int32_t* row_ptr, const int32_t* ent_con, const double* ent_w,
+                                        const int32_t* c_kind, const double* c_g, const double* c_b, double4* crhs,
+                                        double4* cdiag) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < N; r += warps) {
+    if (row_ptr[r + 1] - row_ptr[r] <= kCacheWarpRow) continue;
+    V3 rhs{0, 0, 0}, diag{0, 0, 0};
+    for (int e = row_ptr[r] + lane; e < row_ptr[r + 1]; e += 32)
+      cache_term(ent_con[e], ent_w[e], c_kind, c_g, c_b, rhs, diag);
+    rhs.x = warp_sum(rhs.x);
+    rhs.y = warp_sum(rhs.y);
+    rhs.z = warp_sum(rhs.z);
+    diag.x = warp_sum(diag.x);
+    diag.y = warp_sum(diag.y);
+    diag.z = warp_sum(diag.z);
+    if (lane == 0) {
+      crhs[r] = make_double4(rhs.x, rhs.y, rhs.z, 0.0);
+      cdiag[r] = make_double4(diag.x, diag.y, diag.z, 0.0);
+    }
   }
 }
 
@@ -375,10 +420,10 @@ struct FFArgs {
   double4* contrib;      // E: a_k u_c per incidence slot (row-sorted)
   const int32_t* heavy;  // rows with more than kHeavyRow incidences
   int n_heavy;
-  const int4* items;     // matrix-free work items: row, e_begin, e_end, first
-  int n_items;
-  const int32_t* item_ptr;  // N+1: items of each row
-  double4* wpart;        // per-item partial (A v)
+  const int4* xitems;    // matrix-free extra work items (row, e_begin, e_end)
+  int n_xitems;
+  const int2* xrange;    // N: first extra item and count of each row
+  double4* wpart;        // per-item partial (A v): rows first, then extra items
   // outputs
   double* partials;  // 4 slots x gridDim
   unsigned* sync_count;  // grid barrier arrival counter (own 128 B line)
@@ -763,25 +808,39 @@ __device__ void assemble_rows(const FFArgs& a) {
 }
 
 // Matrix-free row pass, load-balanced: every row's contiguous incidence
-// contributions are cut into work items of at most kItemLen entries (fixed
-// per solve).  Item 0 of a row also carries the ARAP Laplacian.  Each item
-// writes its partial (A v) into wpart[item]; the update phase adds a row's
-// items in order, and the p.Ap / w.u dot is accumulated per item (it is
-// linear), so no row waits on another's long list.
+// contributions are cut into work items of at most kItemLen entries.  Item r
+// (r < N) is row r's first item and also carries the ARAP Laplacian, so its
+// loads need no item record; rows with more incidences own extra items
+// (stored after the first N).  Each item writes its partial (A v) to
+// wpart[item]; the update phase adds a row's items in order, and the w.u dot
+// is accumulated per item (it is linear), so no row waits on a long list.
 template <class Sink>
 __device__ __forceinline__ void item_pass(const FFArgs& a, const double4* v, Sink& sink) {
   const double w2 = 2.0 * a.w_r;
-  for (int i = int(gtid()); i < a.n_items; i += int(gstride())) {
-    const int4 it = a.items[i];  // row, e_begin, e_end, first
-    const int r = it.x;
+  const int total = a.N + a.n_xitems;
+  for (int i = int(gtid()); i < total; i += int(gstride())) {
+    int r, e0, e1;
+    bool first;
+    if (i < a.N) {
+      r = i;
+      e0 = a.row_ptr[r];
+      e1 = min(a.row_ptr[r + 1], e0 + kItemLen);
+      first = true;
+    } else {
+      const int4 it = a.xitems[i - a.N];
+      r = it.x;
+      e0 = it.y;
+      e1 = it.z;
+      first = false;
+    }
     const V3 vr = ld4(v, r);
     V3 acc{0, 0, 0};
-    if (a.frozen[r]) {
+    if (first && a.frozen[r]) {
       acc = vr;  // frozen rows: A = I (solver.cpp:241-246); they carry no incidences
     } else {
 #pragma unroll 4
-      for (int e = it.y; e < it.z; ++e) acc += ld4(a.contrib, e);
-      if (it.w) {
+      for (int e = e0; e < e1; ++e) acc += ld4(a.contrib, e);
+      if (first) {
 #pragma unroll
         for (int k = 0; k < 6; ++k) {
           const int j = a.nbr[int64_t(k) * a.N + r];
@@ -796,8 +855,9 @@ __device__ __forceinline__ void item_pass(const FFArgs& a, const double4* v, Sin
 
 // (A v)_r of one row from its items (fixed order)
 WF_D V3 row_from_items(const FFArgs& a, int r) {
-  V3 acc{0, 0, 0};
-  for (int i = a.item_ptr[r]; i < a.item_ptr[r + 1]; ++i) acc += ld4(a.wpart, i);
+  V3 acc = ld4(a.wpart, r);
+  const int2 xr = a.xrange[r];
+  for (int i = 0; i < xr.y; ++i) acc += ld4(a.wpart, a.N + xr.x + i);
   return acc;
 }
 
@@ -1240,6 +1300,14 @@ static void sync_check(wfk_ctx* c) { WFK_CUDA(cudaStreamSynchronize(c->stream));
 static void level_rows(wfk_ctx* c, Level& L) {
   const int64_t n = L.g.n();
   cudaStream_t s = c->stream;
+  // Level 0 mirrors the volume's active mask, which no solve changes: its rows,
+  // neighbour table and component labels are reused until the mask changes
+  // (compute_active_set / expand_grid / an ACTIVE upload bump active_gen).
+  const bool level0 = &L == &c->lv[0];
+  if (level0 && L.rows_gen == c->vol.active_gen && L.rows_gen != 0) {
+    if (L.N > 0) WFK_CUDA(cudaMemsetAsync(L.comp_flag.p, 0, size_t(L.N), s));
+    return;
+  }
   L.rows.ensure(size_t(n));
   L.node_row.ensure(size_t(n));
   int32_t* d_count = c->ivec.ensure(16);
@@ -1264,6 +1332,7 @@ static void level_rows(wfk_ctx* c, Level& L) {
   L.rot.ensure(9 * Nc);
   L.row_ptr.ensure(Nc + 1);
   L.cnt.ensure(Nc + 1);
+  L.rows_gen = 0;
   if (N == 0) return;
   k_scatter_node_row<<<grid_for(N), kBlock, 0, s>>>(L.rows, N, L.node_row);
   k_row_neighbours<<<grid_for(N), kBlock, 0, s>>>(L.g, L.rows, N, L.node_row, L.nbr, L.uf);
@@ -1271,6 +1340,7 @@ static void level_rows(wfk_ctx* c, Level& L) {
   k_uf_compress<<<grid_for(N), kBlock, 0, s>>>(N, L.uf, L.comp_flag);
   count_launch(c, 4);
   WFK_CUDA(cudaGetLastError());
+  L.rows_gen = level0 ? c->vol.active_gen : 0;
 }
 
 // Prepares the level's constraints (anchors in c_node/c_w) for the solve:
@@ -1337,35 +1407,39 @@ static void level_constraints(wfk_ctx* c, Level& L, const PoseD& pose, const wfk
   }
   k_constraint_cache<<<grid_for(N), kBlock, 0, s>>>(N, L.row_ptr, L.ent_con, L.ent_w, L.c_kind, L.c_g, L.c_b,
                                                     L.crhs, L.cdiag);
-  count_launch(c);
+  if (L.E > int64_t(kCacheWarpRow) * 2)
+    k_constraint_cache_warp<<<std::min(grid_for(int64_t(N) * 32), c->num_sms * 16), kBlock, 0, s>>>(
+        N, L.row_ptr, L.ent_con, L.ent_w, L.c_kind, L.c_g, L.c_b, L.crhs, L.cdiag);
+  count_launch(c, 2);
   // Rows carrying many constraint incidences (coarse levels, where every
   // constraint of the frame lands on a few thousand nodes) get their B^T B
   // assembled once per solve, so the PCG row pass is a fixed 27-block stencil.
   L.assembled = L.E > int64_t(kAssembleRatio) * N;
   L.n_heavy = 0;
   if (!L.assembled && L.E > 0) L.contrib.ensure(size_t(L.E));
-  L.n_items = 0;
+  L.n_xitems = 0;
   if (!L.assembled) {
-    L.item_ptr.ensure(size_t(N) + 1);
-    int32_t* cnt_items = L.cnt.p;  // per-row item counts (cnt is free after the row_ptr scan)
-    k_item_count<<<grid_for(N), kBlock, 0, s>>>(N, L.row_ptr, cnt_items);
-    WFK_CUDA(cudaMemsetAsync(cnt_items + N, 0, sizeof(int32_t), s));
+    L.xptr.ensure(size_t(N) + 1);
+    L.xrange.ensure(size_t(N) + 1);
+    int32_t* n_extra = L.cnt.p;  // per-row extra item counts (cnt is free after the row_ptr scan)
+    k_item_count<<<grid_for(N), kBlock, 0, s>>>(N, L.row_ptr, n_extra);
+    WFK_CUDA(cudaMemsetAsync(n_extra + N, 0, sizeof(int32_t), s));
     size_t tmp4 = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tmp4, cnt_items, L.item_ptr.p, N + 1, s);
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp4, n_extra, L.xptr.p, N + 1, s);
     c->temp.ensure(tmp4);
-    WFK_CUDA(cub::DeviceScan::ExclusiveSum(c->temp.p, tmp4, cnt_items, L.item_ptr.p, N + 1, s));
-    WFK_CUDA(cudaMemcpyAsync(c->h_pinned + 5, L.item_ptr.p + N, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    WFK_CUDA(cub::DeviceScan::ExclusiveSum(c->temp.p, tmp4, n_extra, L.xptr.p, N + 1, s));
+    WFK_CUDA(cudaMemcpyAsync(c->h_pinned + 5, L.xptr.p + N, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     sync_check(c);
-    L.n_items = c->h_pinned[5];
-    L.items.ensure(size_t(L.n_items) + 1);
-    L.wpart.ensure(size_t(L.n_items) + 1);
-    k_item_write<<<grid_for(N), kBlock, 0, s>>>(N, L.row_ptr, L.item_ptr, L.items);
+    L.n_xitems = c->h_pinned[5];
+    L.xitems.ensure(size_t(L.n_xitems) + 1);
+    L.wpart.ensure(size_t(N) + size_t(L.n_xitems) + 1);
+    k_item_write<<<grid_for(N), kBlock, 0, s>>>(N, L.row_ptr, L.xptr, L.xitems, L.xrange);
     count_launch(c, 3);
   }
   if (L.assembled) {
     L.blk.ensure(size_t(N) * 27 * 6);
     L.cols.ensure(size_t(N) * 27);
-    k_assemble_btb<<<grid_for(int64_t(N) * 27), kBlock, 0, s>>>(L.g, N, L.rows, L.node_row, L.row_ptr, L.ent_con,
+    k_assemble_btb<<<std::min(grid_for(int64_t(N) * 27 * 32), c->num_sms * 32), kBlock, 0, s>>>(L.g, N, L.rows, L.node_row, L.row_ptr, L.ent_con,
                                                                  L.ent_k, L.ent_w, L.c_w, L.c_g, L.c_kind, L.blk,
                                                                  L.cols);
     count_launch(c);
@@ -1400,6 +1474,7 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
                       std::vector<wfk_trace_entry>* out, wfk_energy* e_out) {
   cudaStream_t s = c->stream;
   const int G = coop_blocks(c);
+
   FFArgs a;
   a.g = L.g;
   a.N = L.N;
@@ -1446,9 +1521,9 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   a.contrib = L.contrib;
   a.heavy = L.heavy;
   a.n_heavy = L.n_heavy;
-  a.items = L.items;
-  a.n_items = L.n_items;
-  a.item_ptr = L.item_ptr;
+  a.xitems = L.xitems;
+  a.n_xitems = L.n_xitems;
+  a.xrange = L.xrange;
   a.wpart = L.wpart;
   a.partials = c->partials.ensure(size_t(8) * G);
   // barrier state: count, generation, totals on separate 128 B lines

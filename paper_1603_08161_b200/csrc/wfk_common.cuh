@@ -23,6 +23,7 @@ constexpr int kAssembleRatio = 32;  // incidences per row above which B^T B is a
 constexpr int kHeavyRow = 16;       // incidences above which a row is summed by a whole warp
 constexpr int kAsmLanes = 8;        // lanes per row on assembled levels (27 stencil slots)
 constexpr int kItemLen = 8;         // incidences per work item of the matrix-free row pass
+constexpr int kCacheWarpRow = 32;   // incidences above which the constraint cache sums a row by warp
 constexpr int kCenter = 13;
 
 struct V3 {

@@ -93,6 +93,7 @@ struct Level {
   uint8_t* active = nullptr;
   // rows
   int N = 0;
+  uint64_t rows_gen = 0;  // level 0: volume active_gen the row structures were built for
   DevBuf<int32_t> rows, node_row, nbr, uf;  // nbr: 6 x Ncap SoA
   DevBuf<uint8_t> frozen, comp_flag;
   // per-row state (AoS double3 / row-major 3x3)
@@ -107,10 +108,11 @@ struct Level {
   DevBuf<double4> contrib; // E: per-incidence matvec contributions
   DevBuf<int32_t> heavy;   // rows summed by a whole warp
   int n_heavy = 0;
-  DevBuf<int4> items;      // balanced matrix-free work items
-  DevBuf<int32_t> item_ptr;
+  DevBuf<int4> xitems;     // extra work items of the balanced matrix-free row pass
+  DevBuf<int32_t> xptr;
+  DevBuf<int2> xrange;
   DevBuf<double4> wpart;
-  int n_items = 0;
+  int n_xitems = 0;
   // level constraints
   int64_t C = 0;
   DevBuf<int32_t> c_node;   // 8C anchors at this level
@@ -135,6 +137,7 @@ struct VolumeDev {
   DevBuf<double> deformed, euler;
   DevBuf<int32_t> age;
   DevBuf<uint8_t> active;
+  uint64_t active_gen = 1;  // bumped whenever the active mask may change
   bool valid = false;
 };
 
