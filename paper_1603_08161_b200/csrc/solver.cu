@@ -201,10 +201,12 @@ __global__ void k_heavy_flags(int N, const int32_t* row_ptr, uint8_t* flag) {
 // coef a_i a_k (g g^T | I) for the anchor k at that slot (solver.cpp:196-226),
 // symmetric 3x3 stored as 6 values; columns follow solver.cpp:149-160.  One
 // warp per (row, slot): lanes stride the row's incidence list (thousands on
-// the coarse levels), fixed shuffle tree.
+// the coarse levels), fixed shuffle tree.  Stored slot-major (SoA over rows:
+// blk[(slot * 6 + m) * N + row], cols[slot * N + row]) so the thread-per-row
+// stencil loads are coalesced.
 __global__ void k_assemble_btb(Grid g, int N, const int32_t* rows, const int32_t* node_row, const int32_t* row_ptr,
                                const int32_t* ent_con, const uint8_t* ent_k, const double* ent_w, const double* c_w,
-                               const double* c_g, const int32_t* c_kind, double* blk, int32_t* cols) {
+                               const double* c_g, const int32_t* c_kind, double* blk, int32_t* cols, int soa) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   for (int64_t t = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; t < int64_t(N) * 27; t += warps) {
@@ -237,9 +239,56 @@ __global__ void k_assemble_btb(Grid g, int N, const int32_t* rows, const int32_t
     if (lane == 0) {
       int x, y, z;
       g.idx3(rows[r], x, y, z);
-      cols[t] = g.in_grid(x + dx, y + dy, z + dz) ? node_row[g.lin(x + dx, y + dy, z + dz)] : -1;
-      for (int m = 0; m < 6; ++m) blk[t * 6 + m] = b[m];
+      const int col = g.in_grid(x + dx, y + dy, z + dz) ? node_row[g.lin(x + dx, y + dy, z + dz)] : -1;
+      if (soa) {
+        cols[int64_t(s) * N + r] = col;
+        for (int m = 0; m < 6; ++m) blk[(int64_t(s) * 6 + m) * N + r] = b[m];
+      } else {
+        cols[t] = col;
+        for (int m = 0; m < 6; ++m) blk[t * 6 + m] = b[m];
+      }
     }
+  }
+}
+
+// Same, one thread per (row, slot) in the reference's accumulation order --
+// for levels whose rows carry few incidences.
+__global__ void k_assemble_btb_thread(Grid g, int N, const int32_t* rows, const int32_t* node_row,
+                                      const int32_t* row_ptr, const int32_t* ent_con, const uint8_t* ent_k,
+                                      const double* ent_w, const double* c_w, const double* c_g,
+                                      const int32_t* c_kind, double* blk, int32_t* cols, int soa) {
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < int64_t(N) * 27;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const int s = int(t / N), r = int(t % N);  // slot-major: consecutive threads, consecutive rows
+    const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = s / 9 - 1;
+    double b[6] = {0, 0, 0, 0, 0, 0};
+    for (int e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
+      const int ki = ent_k[e];
+      const int ox = (ki & 1) + dx, oy = ((ki >> 1) & 1) + dy, oz = (ki >> 2) + dz;
+      if (ox < 0 || ox > 1 || oy < 0 || oy > 1 || oz < 0 || oz > 1) continue;
+      const int c = ent_con[e];
+      const int k = ox + 2 * oy + 4 * oz;
+      const double sc = c_g[4 * c + 3] * ent_w[e] * c_w[8 * int64_t(c) + k];
+      if (c_kind[c] == WFK_DENSE_PLANE) {
+        const double gx = c_g[4 * c], gy = c_g[4 * c + 1], gz = c_g[4 * c + 2];
+        b[0] += sc * (gx * gx);
+        b[1] += sc * (gx * gy);
+        b[2] += sc * (gx * gz);
+        b[3] += sc * (gy * gy);
+        b[4] += sc * (gy * gz);
+        b[5] += sc * (gz * gz);
+      } else {
+        b[0] += sc * 1.0;
+        b[3] += sc * 1.0;
+        b[5] += sc * 1.0;
+      }
+    }
+    int x, y, z;
+    g.idx3(rows[r], x, y, z);
+    const int col = g.in_grid(x + dx, y + dy, z + dz) ? node_row[g.lin(x + dx, y + dy, z + dz)] : -1;
+    const int64_t ta = int64_t(r) * 27 + s;
+    cols[soa ? int64_t(s) * N + r : ta] = col;
+    for (int m = 0; m < 6; ++m) blk[soa ? (int64_t(s) * 6 + m) * N + r : ta * 6 + m] = b[m];
   }
 }
 
@@ -405,6 +454,7 @@ struct FFArgs {
   double* rot;  // 9 per row
   // assembled B^T B (levels with many incidences per row)
   int assembled;
+  int asm_rows_on_lanes;  // rows on lanes (large levels) vs kAsmLanes lanes per row
   const double* blk;     // N x 27 x 6 (xx xy xz yy yz zz)
   const int32_t* cols;   // N x 27
   // constraints
@@ -689,19 +739,16 @@ __device__ __forceinline__ V3 matvec_row(const FFArgs& a, const double4* v, int 
   if (a.frozen[r]) return vr;
   V3 acc{0, 0, 0};
   if (ASM) {
-    const double* B = a.blk + int64_t(r) * 27 * 6;
-    const int32_t* cp = a.cols + int64_t(r) * 27;
-    int cl[27];
-#pragma unroll
-    for (int s = 0; s < 27; ++s) cl[s] = cp[s];
-#pragma unroll
+    const int64_t n = a.N;
+#pragma unroll 9
     for (int s = 0; s < 27; ++s) {
-      if (cl[s] < 0) continue;
-      const V3 x = ld4(v, cl[s]);
-      const double* b = B + 6 * s;  // xx xy xz yy yz zz
-      acc.x += b[0] * x.x + b[1] * x.y + b[2] * x.z;
-      acc.y += b[1] * x.x + b[3] * x.y + b[4] * x.z;
-      acc.z += b[2] * x.x + b[4] * x.y + b[5] * x.z;
+      const int col = a.cols[int64_t(s) * n + r];
+      if (col < 0) continue;
+      const V3 x = ld4(v, col);
+      const double* b = a.blk + int64_t(s) * 6 * n + r;  // xx xy xz yy yz zz, stride N
+      acc.x += b[0] * x.x + b[n] * x.y + b[2 * n] * x.z;
+      acc.y += b[n] * x.x + b[3 * n] * x.y + b[4 * n] * x.z;
+      acc.z += b[2 * n] * x.x + b[4 * n] * x.y + b[5 * n] * x.z;
     }
   } else {
     const int e0 = a.row_ptr[r], e1 = a.row_ptr[r + 1];
@@ -723,6 +770,33 @@ template <bool ASM, class Sink>
 __device__ __forceinline__ void row_pass(const FFArgs& a, const double4* v, Sink& sink) {
   const int lane = threadIdx.x & 31;
   const double w2 = 2.0 * a.w_r;
+  if (ASM && a.asm_rows_on_lanes) {
+    // large assembled levels: rows on lanes, slot loop, coalesced SoA loads
+    const int N = a.N;
+    for (int r = int(gtid()); r < N; r += int(gstride())) {
+      const V3 vr = ld4(v, r);
+      if (a.frozen[r]) {
+        sink(r, vr, vr);
+        continue;
+      }
+      V3 acc{0, 0, 0};
+#pragma unroll 9
+      for (int s = 0; s < 27; ++s) {
+        const int col = a.cols[int64_t(s) * N + r];
+        if (col < 0) continue;
+        const V3 x = ld4(v, col);
+        const double* b = a.blk + int64_t(s) * 6 * N + r;
+        const double b0 = b[0], b1 = b[N], b2 = b[2 * int64_t(N)], b3 = b[3 * int64_t(N)],
+                     b4 = b[4 * int64_t(N)], b5 = b[5 * int64_t(N)];
+        acc.x += b0 * x.x + b1 * x.y + b2 * x.z;
+        acc.y += b1 * x.x + b3 * x.y + b4 * x.z;
+        acc.z += b2 * x.x + b4 * x.y + b5 * x.z;
+        if (s == 4 || s == 10 || s == 12 || s == 14 || s == 16 || s == 22) acc += w2 * (vr - x);
+      }
+      sink(r, vr, acc);
+    }
+    return;
+  }
   if (ASM) {
     constexpr int L = kAsmLanes, RPW = 32 / L;
     const int sub = lane % L, grp = lane / L;
@@ -1437,11 +1511,17 @@ static void level_constraints(wfk_ctx* c, Level& L, const PoseD& pose, const wfk
     count_launch(c, 3);
   }
   if (L.assembled) {
+    const int soa = N >= kAsmThreadRows ? 1 : 0;  // rows on lanes read slot-major blocks
     L.blk.ensure(size_t(N) * 27 * 6);
     L.cols.ensure(size_t(N) * 27);
+    if (L.E <= int64_t(kCacheWarpRow) * N)
+      k_assemble_btb_thread<<<grid_for(int64_t(N) * 27), kBlock, 0, s>>>(L.g, N, L.rows, L.node_row, L.row_ptr,
+                                                                        L.ent_con, L.ent_k, L.ent_w, L.c_w, L.c_g,
+                                                                        L.c_kind, L.blk, L.cols, soa);
+    else
     k_assemble_btb<<<std::min(grid_for(int64_t(N) * 27 * 32), c->num_sms * 32), kBlock, 0, s>>>(L.g, N, L.rows, L.node_row, L.row_ptr, L.ent_con,
                                                                  L.ent_k, L.ent_w, L.c_w, L.c_g, L.c_kind, L.blk,
-                                                                 L.cols);
+                                                                 L.cols, soa);
     count_launch(c);
   }
   WFK_CUDA(cudaGetLastError());
@@ -1502,6 +1582,7 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   a.u = L.u;
   a.w = L.w;
   a.assembled = L.assembled ? 1 : 0;
+  a.asm_rows_on_lanes = L.N >= kAsmThreadRows ? 1 : 0;
   a.blk = L.blk;
   a.cols = L.cols;
   a.ap = L.ap;
