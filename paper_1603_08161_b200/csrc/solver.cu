@@ -450,6 +450,10 @@ struct FFArgs {
   double* field_eul;
   // row state: 32-byte padded 3-vectors, one 256-bit access each
   double4 *t, *x, *rhs, *r, *p, *ap, *dinv, *u, *w;  // ap holds s = A p
+  double4 *z, *m0, *m1;  // pipelined PCG: z = A D s, m = D w (double-buffered)
+  double4* nbuf;         // pipelined PCG: n = A m of the rows a thread leads
+  unsigned long long* sync_ll;  // split-reduction totals (flag-embedded words)
+  int pcg_variant;       // 0 pipelined (one reduction, overlapped), 1 Chronopoulos-Gear
   const double4 *crhs, *cdiag;
   double* rot;  // 9 per row
   // assembled B^T B (levels with many incidences per row)
@@ -558,10 +562,12 @@ __device__ __forceinline__ unsigned atom_add_acq_rel_u32(unsigned* p, unsigned v
 __device__ __forceinline__ void grid_barrier(const FFArgs& a, Red& rs) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
+    // the arrival counter only grows (reset at launch): the last arrival of
+    // generation g reads G (g + 1) - 1.  The acq_rel arrival releases the
+    // block's writes (ordered before it by the block barrier) and, for the
+    // last block, acquires everyone else's.
     const unsigned old = atom_add_acq_rel_u32(a.sync_count, 1u);
-    if (old == gridDim.x - 1) {
-      *a.sync_count = 0;
+    if (old == gridDim.x * (rs.gen + 1) - 1) {
       st_release_u32(a.sync_gen, rs.gen + 1);
     } else {
       while (ld_acquire_u32(a.sync_gen) == rs.gen) {
@@ -592,18 +598,15 @@ __device__ void grid_reduce(const FFArgs& a, Red& rs, double (&v)[NV], PhaseCloc
     if (lane == 0) {
 #pragma unroll
       for (int k = 0; k < NV; ++k) a.partials[size_t(k) * gridDim.x + blockIdx.x] = s[k];
-      __threadfence();
-      last = atom_add_acq_rel_u32(a.sync_count, 1u) == gridDim.x - 1 ? 1u : 0u;
+      last = atom_add_acq_rel_u32(a.sync_count, 1u) == gridDim.x * (rs.gen + 1) - 1 ? 1u : 0u;
     }
     last = __shfl_sync(0xffffffffu, last, 0);
     if (last) {
-      __threadfence();
 #pragma unroll
       for (int k = 0; k < NV; ++k) s[k] = sum_partials(a.partials + size_t(k) * gridDim.x, gridDim.x);
       if (lane == 0) {
 #pragma unroll
         for (int k = 0; k < NV; ++k) a.sync_total[k] = s[k];
-        *a.sync_count = 0;
         st_release_u32(a.sync_gen, rs.gen + 1);
       }
     } else if (lane == 0) {
@@ -695,8 +698,10 @@ __device__ wfk_energy energy(const FFArgs& a, cg::grid_group& grid, Red& rs, boo
 // matrix-free A*v, pass 1: u_c = coef (g . q_c) g | coef q_c with
 // q_c = sum_k a_k v[a_k], and a_k u_c scattered to the incidence slot of each
 // anchor row (row-sorted order), so pass 2 sums a contiguous range per row.
-__device__ void matvec_constraints(const FFArgs& a, const double4* v) {
-  for (int64_t c = gtid(); c < a.C; c += gstride()) {
+__device__ void matvec_constraints(const FFArgs& a, const double4* v, int skip = 0) {
+  const int64_t c0 = gtid() - 32 * skip;
+  if (c0 < 0) return;
+  for (int64_t c = c0; c < a.C; c += gstride() - 32 * skip) {
     int rows[8];
     double w[8];
     ld_anchors(a, c, rows, w);
@@ -767,13 +772,14 @@ __device__ __forceinline__ V3 matvec_row(const FFArgs& a, const double4* v, int 
 //    incidence contributions; rows with more than kHeavyRow incidences go to
 //    a whole warp (coalesced 256-bit loads, lanes 0-5 one face neighbour each).
 template <bool ASM, class Sink>
-__device__ __forceinline__ void row_pass(const FFArgs& a, const double4* v, Sink& sink) {
+__device__ __forceinline__ void row_pass(const FFArgs& a, const double4* v, Sink& sink, int skip = 0) {
   const int lane = threadIdx.x & 31;
   const double w2 = 2.0 * a.w_r;
+  if (gwarp() < skip) return;  // warps reserved for the split reduction
   if (ASM && a.asm_rows_on_lanes) {
     // large assembled levels: rows on lanes, slot loop, coalesced SoA loads
     const int N = a.N;
-    for (int r = int(gtid()); r < N; r += int(gstride())) {
+    for (int r = int(gtid()) - 32 * skip; r < N; r += int(gstride()) - 32 * skip) {
       const V3 vr = ld4(v, r);
       if (a.frozen[r]) {
         sink(r, vr, vr);
@@ -800,7 +806,7 @@ __device__ __forceinline__ void row_pass(const FFArgs& a, const double4* v, Sink
   if (ASM) {
     constexpr int L = kAsmLanes, RPW = 32 / L;
     const int sub = lane % L, grp = lane / L;
-    for (int base = gwarp() * RPW; base < a.N; base += nwarps() * RPW) {
+    for (int base = (gwarp() - skip) * RPW; base < a.N; base += (nwarps() - skip) * RPW) {
       const int r = base + grp;
       const bool live = r < a.N;
       const bool frozen = live && a.frozen[r];
@@ -1055,6 +1061,310 @@ __device__ void pcg(const FFArgs& a, cg::grid_group& grid, Red& rs, int& iters, 
   }
 }
 
+// Matrix-free row pass with kMfLanes lanes per row: the row's contiguous
+// incidence contributions and its six face neighbours are strided over the
+// lanes, a sub-warp shuffle tree sums them (fixed order), and the group
+// leader receives (A v)_r -- so a row is complete inside one warp and its
+// update can follow without another grid barrier.
+template <class Sink>
+__device__ __forceinline__ void row_pass_mf(const FFArgs& a, const double4* v, Sink& sink, int skip = 0) {
+  constexpr int L = kMfLanes, RPW = 32 / L;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane % L, grp = lane / L;
+  const double w2 = 2.0 * a.w_r;
+  if (gwarp() < skip) return;
+  for (int base = (gwarp() - skip) * RPW; base < a.N; base += (nwarps() - skip) * RPW) {
+    const int r = base + grp;
+    const bool live = r < a.N;
+    const bool frozen = live && a.frozen[r];
+    const V3 vr = live ? ld4(v, r) : V3{0, 0, 0};
+    V3 acc{0, 0, 0};
+    if (live && !frozen) {
+      const int e0 = a.row_ptr[r], e1 = a.row_ptr[r + 1];
+      for (int e = e0 + sub; e < e1; e += L) acc += ld4(a.contrib, e);
+#pragma unroll
+      for (int k = sub; k < 6; k += L) {
+        const int j = a.nbr[int64_t(k) * a.N + r];
+        if (j >= 0) acc += w2 * (vr - ld4(v, j));
+      }
+    }
+#pragma unroll
+    for (int o = L / 2; o > 0; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+      acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+    }
+    if (live && sub == 0) sink(r, vr, frozen ? vr : acc);
+  }
+}
+
+// ---- split reduction --------------------------------------------------------
+// The pipelined iteration needs its dot products only after the next matvec,
+// so the reduction is split off the barrier: every block publishes its block
+// partials and passes a plain grid barrier; then global warp 0 (block 0,
+// warp 0, which the PCG passes leave without rows) sums the partials in fixed
+// block order and publishes the totals as flag-embedded words {32-bit half,
+// 32-bit tag} (single-copy atomic 64-bit stores, so a reader that sees the tag
+// sees the value), while every other warp proceeds with the matvec.  Blocks
+// poll the totals only when the update needs them.  Partials and totals are
+// double-buffered by the reduction sequence number, which a block can only
+// reuse two reductions later -- after every block has consumed the older one.
+constexpr int kSplitNV = 3;
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ double* split_partials(const FFArgs& a, unsigned seq) {
+  return a.partials + size_t(seq & 1) * kSplitNV * gridDim.x;
+}
+__device__ __forceinline__ unsigned long long* split_totals(const FFArgs& a, unsigned seq) {
+  return a.sync_ll + (seq & 1) * 8;
+}
+// block sum of v -> partials[seq], then a grid barrier (publishes all writes)
+__device__ void split_arrive(const FFArgs& a, Red& rs, double (&v)[kSplitNV], unsigned seq) {
+  __shared__ double smem[kSplitNV * 32];
+  block_sum<kSplitNV>(v, smem);
+  if (threadIdx.x < kSplitNV) split_partials(a, seq)[threadIdx.x * gridDim.x + blockIdx.x] = v[threadIdx.x];
+  grid_barrier(a, rs);
+}
+// global warp 0 only, after split_arrive's barrier
+__device__ void split_total(const FFArgs& a, unsigned seq) {
+  const int lane = threadIdx.x & 31;
+  const double* part = split_partials(a, seq);
+  double t[kSplitNV];
+#pragma unroll
+  for (int k = 0; k < kSplitNV; ++k) t[k] = 0;
+  // fixed order: lane l sums blocks l, l + 32, ... then a fixed shuffle tree
+  // one batch of loads for up to 160 blocks (B200: 148), then any remainder
+  constexpr int J = 5;
+  double x[kSplitNV][J];
+#pragma unroll
+  for (int j = 0; j < J; ++j)
+#pragma unroll
+    for (int k = 0; k < kSplitNV; ++k) {
+      const int b = lane + 32 * j;
+      x[k][j] = b < int(gridDim.x) ? __ldcg(part + k * gridDim.x + b) : 0.0;
+    }
+#pragma unroll
+  for (int j = 0; j < J; ++j)
+#pragma unroll
+    for (int k = 0; k < kSplitNV; ++k) t[k] += x[k][j];
+  for (int b = lane + 32 * J; b < int(gridDim.x); b += 32)
+#pragma unroll
+    for (int k = 0; k < kSplitNV; ++k) t[k] += __ldcg(part + k * gridDim.x + b);
+#pragma unroll
+  for (int k = 0; k < kSplitNV; ++k) t[k] = warp_sum(t[k]);
+  if (lane < 2 * kSplitNV) {
+    double tv = t[0];
+#pragma unroll
+    for (int k = 1; k < kSplitNV; ++k)
+      if ((lane >> 1) == k) tv = t[k];
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(tv);
+    const unsigned half = (lane & 1) ? unsigned(bits >> 32) : unsigned(bits);
+    st_relaxed_u64(split_totals(a, seq) + lane, (unsigned long long)half << 32 | (seq + 1u));
+  }
+}
+// every block: wait for the totals of reduction seq
+__device__ void split_wait(const FFArgs& a, unsigned seq, double (&v)[kSplitNV]) {
+  __shared__ double bc[kSplitNV];
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 32) {
+    unsigned half = 0;
+    if (lane < 2 * kSplitNV) {
+      const unsigned long long* w = split_totals(a, seq) + lane;
+      unsigned long long x;
+      do {
+        x = ld_relaxed_u64(w);
+      } while (unsigned(x) != seq + 1u);
+      half = unsigned(x >> 32);
+    }
+    const unsigned hi = __shfl_down_sync(0xffffffffu, half, 1);
+    if (lane < 2 * kSplitNV && !(lane & 1))
+      bc[lane >> 1] = __longlong_as_double((long long)((unsigned long long)hi << 32 | half));
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kSplitNV; ++k) v[k] = bc[k];
+}
+
+// The rows a warp received from row_pass / row_pass_mf (L lanes per row: RPW
+// rows per round, rounds nw apart), revisited with every lane busy: lane l
+// takes row l % RPW of round l / RPW, 32 / RPW rounds per step.  The matvec
+// results were stored by lanes of the same warp, so a __syncwarp orders them.
+template <int L, class F>
+__device__ __forceinline__ void for_warp_rows(int N, int skip, F f) {
+  constexpr int RPW = 32 / L, RPS = 32 / RPW;
+  if (gwarp() < skip) return;
+  __syncwarp();
+  const int lane = threadIdx.x & 31;
+  const int gw = gwarp() - skip, nw = nwarps() - skip;
+  for (int k = lane / RPW;; k += RPS) {
+    const int r = (gw + k * nw) * RPW + lane % RPW;
+    if (r >= N) break;  // rows grow with k
+    f(r);
+  }
+}
+
+// pcg_solve (solver.cpp:282-343) as pipelined Jacobi-PCG (Ghysels & Vanroose
+// 2014): the same Krylov iterates as the reference's PCG in exact arithmetic,
+// with w = A u, s = A p and z = A D s carried by recurrences, so the one grid
+// reduction {r.u, w.u, r.r} of an iteration is not needed until after the
+// next matvec n = A m (m = D w).  Per iteration:
+//   assembled:    row pass n = A m | totals (global warp 0)
+//                 update own rows  -> partials + barrier         (1 barrier)
+//   matrix-free:  constraint pass of A m | totals -> barrier
+//                 row pass n = A m, update own rows -> partials + barrier
+// The update: z = n + beta z, s = w + beta s, p = u + beta p, x += alpha p,
+// r -= alpha s, w -= alpha z, u = D r, m' = D w (into the other m buffer, as
+// slower blocks may still gather the current one).  alpha and beta are the
+// reference's: alpha = r.u / p.Ap with p.Ap = w.u - beta r.u / alpha_prev.
+// Stopping rule, breakdown test and iteration count are the reference's.
+template <bool ASM>
+__device__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, double& relres) {
+  iters = 0;
+  relres = 0;
+  PhaseClock pc(a.dbg);
+  // r0 = b - A x0, u0 = D^-1 r0 (solver.cpp:305-310) -- all warps, classic reductions
+  double acc_rr = 0, acc_bb = 0;
+  auto init_sink = [&](int r, V3, V3 ax) {
+    const V3 b = ld4(a.rhs, r);
+    const V3 rr = b - ax;
+    st4(a.r, r, rr);
+    st4(a.u, r, cmul(ld4(a.dinv, r), rr));
+    const double4 zero = make_double4(0, 0, 0, 0);
+    a.p[r] = zero;
+    a.ap[r] = zero;
+    a.z[r] = zero;
+    acc_rr += dot(rr, rr);
+    acc_bb += sqnorm(b);
+  };
+  auto matvec_all = [&](const double4* v, auto& sink) {
+    if (ASM) {
+      row_pass<true>(a, v, sink);
+    } else {
+      matvec_constraints(a, v);
+      grid_barrier(a, rs);
+      row_pass_mf(a, v, sink);
+    }
+  };
+  matvec_all(a.x, init_sink);
+  grid_barrier(a, rs);
+  // w0 = A u0, m0 = D w0
+  double v4[4] = {0, 0, 0, 0};
+  auto w_sink = [&](int r, V3 ur, V3 wr) {
+    st4(a.w, r, wr);
+    st4(a.m0, r, cmul(ld4(a.dinv, r), wr));
+    v4[0] += dot(ld4(a.r, r), ur);
+    v4[1] += dot(wr, ur);
+  };
+  matvec_all(a.u, w_sink);
+  v4[2] = acc_rr;
+  v4[3] = acc_bb;
+  grid_reduce<4>(a, rs, v4);
+  double gamma = v4[0], delta = v4[1];
+  double r_norm = sqrt(v4[2]);
+  const double b_norm = sqrt(v4[3]);
+  if (b_norm == 0) {
+    for (int r = int(gtid()); r < a.N; r += int(gstride())) st4(a.x, r, V3{0, 0, 0});
+    grid_barrier(a, rs);
+    return;
+  }
+  relres = r_norm / b_norm;
+  const double stop = fmax(a.pcg_tol * r_norm, 1e-13 * b_norm);
+  double gamma_prev = 0, alpha_prev = 0;
+  constexpr int kSkip = 1;  // global warp 0 sums the split reductions
+  const bool comm = gwarp() == 0;
+  constexpr int LM = ASM ? kAsmLanes : kMfLanes;
+  const bool rows_on_lanes = ASM && a.asm_rows_on_lanes;
+  unsigned seq = 0;
+  bool pending = false;  // totals of reduction seq - 1 not yet read
+  pc.lap(12);
+  for (int it = 0; it < a.pcg_max; ++it) {
+    const double4* mcur = (it & 1) ? a.m1 : a.m0;
+    double4* mnext = (it & 1) ? a.m0 : a.m1;
+    // n = A m for own rows (stored by the row's leader lane), overlapped
+    // with the totals of the previous update
+    auto n_sink = [&](int r, V3, V3 n) { st4(a.nbuf, r, n); };
+    if (ASM) {
+      if (comm && pending) split_total(a, seq - 1);
+      row_pass<true>(a, mcur, n_sink, kSkip);
+    } else {
+      matvec_constraints(a, mcur, kSkip);
+      if (comm && pending) split_total(a, seq - 1);
+      pc.lap(0);
+      grid_barrier(a, rs);
+      pc.lap(1);
+      row_pass_mf(a, mcur, n_sink, kSkip);
+    }
+    pc.lap(2);
+    if (pending) {
+      double v3[3];
+      split_wait(a, seq - 1, v3);
+      gamma_prev = gamma;
+      gamma = v3[0];
+      delta = v3[1];
+      r_norm = sqrt(v3[2]);
+      relres = r_norm / b_norm;
+      pending = false;
+    }
+    pc.lap(6);
+    if (!(r_norm > stop)) break;
+    const double beta = it == 0 ? 0.0 : gamma / gamma_prev;
+    const double pap = it == 0 ? delta : delta - beta * gamma / alpha_prev;
+    if (pap <= 0) break;  // solver.cpp:327
+    const double alpha = gamma / pap;
+    double v3[3] = {0, 0, 0};
+    auto upd = [&](int r) {
+      const double4 n4 = a.nbuf[r], w4 = a.w[r], s4 = a.ap[r], z4 = a.z[r], p4 = a.p[r], x4 = a.x[r],
+                    r4 = a.r[r], d4 = a.dinv[r];
+      const V3 d{d4.x, d4.y, d4.z};
+      const V3 w{w4.x, w4.y, w4.z};
+      V3 rr{r4.x, r4.y, r4.z};
+      const V3 z = V3{n4.x, n4.y, n4.z} + beta * V3{z4.x, z4.y, z4.z};
+      const V3 sv = w + beta * V3{s4.x, s4.y, s4.z};
+      const V3 p = cmul(d, rr) + beta * V3{p4.x, p4.y, p4.z};
+      const V3 x = V3{x4.x, x4.y, x4.z} + alpha * p;
+      rr = rr - alpha * sv;
+      const V3 wn = w - alpha * z;
+      const V3 u = cmul(d, rr);
+      st4(a.z, r, z);
+      st4(a.ap, r, sv);
+      st4(a.p, r, p);
+      st4(a.x, r, x);
+      st4(a.r, r, rr);
+      st4(a.w, r, wn);
+      st4(mnext, r, cmul(d, wn));
+      v3[0] += dot(rr, u);
+      v3[1] += dot(wn, u);
+      v3[2] += dot(rr, rr);
+    };
+    if (rows_on_lanes)
+      for_warp_rows<1>(a.N, kSkip, upd);
+    else
+      for_warp_rows<LM>(a.N, kSkip, upd);
+    pc.lap(4);
+    split_arrive(a, rs, v3, seq);
+    pc.lap(7);
+    pc.count(15);
+    alpha_prev = alpha;
+    ++seq;
+    pending = true;
+    iters = it + 1;
+  }
+  if (pending) {
+    // totals of the last update: residual of the returned iterate
+    if (comm) split_total(a, seq - 1);
+    double v3[3];
+    split_wait(a, seq - 1, v3);
+    r_norm = sqrt(v3[2]);
+    relres = r_norm / b_norm;
+  }
+}
+
 // update_rotations (solver.cpp:385-417) for every row; rot[] follows euler.
 __device__ void rotations(const FFArgs& a) {
   for (int r = int(gtid()); r < a.N; r += int(gstride())) {
@@ -1125,10 +1435,17 @@ __global__ void __launch_bounds__(kCoopBlock, 1) k_flip_flop(FFArgs a) {
       pc.lap(8);
       int iters;
       double relres;
-      if (a.assembled)
-        pcg<true>(a, grid, rs, iters, relres);
-      else
-        pcg<false>(a, grid, rs, iters, relres);
+      if (a.pcg_variant == 1) {
+        if (a.assembled)
+          pcg<true>(a, grid, rs, iters, relres);
+        else
+          pcg<false>(a, grid, rs, iters, relres);
+      } else {
+        if (a.assembled)
+          pcg_pipe<true>(a, rs, iters, relres);
+        else
+          pcg_pipe<false>(a, rs, iters, relres);
+      }
       total_pcg += iters;
       pc.lap(9);
       // write back non-frozen rows (solver.cpp:436-437)
@@ -1401,8 +1718,10 @@ static void level_rows(wfk_ctx* c, Level& L) {
   L.uf.ensure(Nc);
   L.frozen.ensure(Nc);
   L.comp_flag.ensure(Nc);
-  for (DevBuf<double4>* b : {&L.t, &L.x, &L.rhs, &L.r, &L.p, &L.ap, &L.dinv, &L.u, &L.w, &L.crhs, &L.cdiag})
+  for (DevBuf<double4>* b : {&L.t, &L.x, &L.rhs, &L.r, &L.p, &L.ap, &L.dinv, &L.u, &L.w, &L.crhs, &L.cdiag, &L.z})
     b->ensure(Nc);
+  L.mbuf.ensure(2 * Nc);
+  L.nbuf.ensure(Nc);
   L.rot.ensure(9 * Nc);
   L.row_ptr.ensure(Nc + 1);
   L.cnt.ensure(Nc + 1);
@@ -1581,6 +1900,15 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   a.p = L.p;
   a.u = L.u;
   a.w = L.w;
+  a.z = L.z;
+  a.m0 = L.mbuf.p;
+  a.m1 = L.mbuf.p + std::max(L.N, 1);
+  a.nbuf = L.nbuf.p;
+  static const int pcg_variant = [] {
+    const char* v = getenv("WFK_PCG");
+    return v && std::string(v) == "cg" ? 1 : 0;
+  }();
+  a.pcg_variant = pcg_variant;
   a.assembled = L.assembled ? 1 : 0;
   a.asm_rows_on_lanes = L.N >= kAsmThreadRows ? 1 : 0;
   a.blk = L.blk;
@@ -1607,12 +1935,13 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   a.xrange = L.xrange;
   a.wpart = L.wpart;
   a.partials = c->partials.ensure(size_t(8) * G);
-  // barrier state: count, generation, totals on separate 128 B lines
+  // barrier state: count, generation, totals, split totals on separate 128 B lines
   unsigned* sync = reinterpret_cast<unsigned*>(c->sync_words.ensure(128));
-  WFK_CUDA(cudaMemsetAsync(sync, 0, 3 * 128, s));
+  WFK_CUDA(cudaMemsetAsync(sync, 0, 4 * 128, s));
   a.sync_count = sync;
   a.sync_gen = sync + 32;
   a.sync_total = reinterpret_cast<double*>(sync + 64);
+  a.sync_ll = reinterpret_cast<unsigned long long*>(sync + 96);
   a.trace = c->trace.ensure(size_t(std::max(p.flip_flop_iters, 1)));
   int32_t* status = c->ivec.ensure(16) + 4;
   double* eout = c->eout.ensure(8);

@@ -97,7 +97,9 @@ struct Level {
   DevBuf<int32_t> rows, node_row, nbr, uf;  // nbr: 6 x Ncap SoA
   DevBuf<uint8_t> frozen, comp_flag;
   // per-row state (AoS double3 / row-major 3x3)
-  DevBuf<double4> t, x, rhs, r, p, ap, dinv, u, w, crhs, cdiag;  // 32 B padded 3-vectors
+  DevBuf<double4> t, x, rhs, r, p, ap, dinv, u, w, crhs, cdiag, z;  // 32 B padded 3-vectors
+  DevBuf<double4> mbuf;  // 2 x N: pipelined PCG m = D w, double-buffered
+  DevBuf<double4> nbuf;  // N: pipelined PCG n = A m
   DevBuf<double> rot;
   // assembled B^T B for rows with many incidences (see kAssembleRatio)
   bool assembled = false;
