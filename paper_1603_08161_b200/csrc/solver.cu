@@ -20,6 +20,7 @@
 //     per-block partial -> fixed-order sum).
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
+#include <type_traits>
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
 
@@ -453,6 +454,7 @@ struct FFArgs {
   double4 *z, *m0, *m1;  // pipelined PCG: z = A D s, m = D w (double-buffered)
   double4* nbuf;         // pipelined PCG: n = A m of the rows a thread leads
   unsigned long long* sync_ll;  // split-reduction totals (flag-embedded words)
+  int meta_rows, meta_cons;     // pipelined matrix-free levels: metadata cached in shared memory
   int pcg_variant;       // 0 pipelined (one reduction, overlapped), 1 Chronopoulos-Gear
   const double4 *crhs, *cdiag;
   double* rot;  // 9 per row
@@ -527,11 +529,22 @@ struct PhaseClock {
   }
 };
 
+// Padded 3-vectors are accessed as one 32-byte-aligned unit: CUDA's double4
+// is only 16-byte aligned (two 128-bit accesses, two L2 sector requests);
+// through this type the compiler emits single 256-bit LDG/STG.E.ENL2.256.
+struct __align__(32) D4 {
+  double x, y, z, w;
+};
 WF_D V3 ld4(const double4* p, int64_t i) {
-  const double4 v = p[i];
+  const D4 v = reinterpret_cast<const D4*>(p)[i];
   return {v.x, v.y, v.z};
 }
-WF_D void st4(double4* p, int64_t i, V3 v) { p[i] = make_double4(v.x, v.y, v.z, 0.0); }
+WF_D void st4(double4* p, int64_t i, V3 v) { reinterpret_cast<D4*>(p)[i] = D4{v.x, v.y, v.z, 0.0}; }
+WF_D double4 ld4w(const double4* p, int64_t i) {
+  const D4 v = reinterpret_cast<const D4*>(p)[i];
+  return make_double4(v.x, v.y, v.z, v.w);
+}
+WF_D void st4w(double4* p, int64_t i, double4 v) { reinterpret_cast<D4*>(p)[i] = D4{v.x, v.y, v.z, v.w}; }
 
 // ---- grid synchronisation of the persistent kernel -------------------------
 // One arrival counter and one generation word (separate 128 B lines).  A block
@@ -637,7 +650,7 @@ __device__ __forceinline__ int nwarps() { return (blockDim.x >> 5) * gridDim.x; 
 
 WF_D void ld_anchors(const FFArgs& a, int64_t c, int rows[8], double w[8]) {
   const int4 r0 = a.c_row[2 * c], r1 = a.c_row[2 * c + 1];
-  const double4 w0 = a.c_w[2 * c], w1 = a.c_w[2 * c + 1];
+  const double4 w0 = ld4w(a.c_w, 2 * c), w1 = ld4w(a.c_w, 2 * c + 1);
   rows[0] = r0.x; rows[1] = r0.y; rows[2] = r0.z; rows[3] = r0.w;
   rows[4] = r1.x; rows[5] = r1.y; rows[6] = r1.z; rows[7] = r1.w;
   w[0] = w0.x; w[1] = w0.y; w[2] = w0.z; w[3] = w0.w;
@@ -698,26 +711,53 @@ __device__ wfk_energy energy(const FFArgs& a, cg::grid_group& grid, Red& rs, boo
 // matrix-free A*v, pass 1: u_c = coef (g . q_c) g | coef q_c with
 // q_c = sum_k a_k v[a_k], and a_k u_c scattered to the incidence slot of each
 // anchor row (row-sorted order), so pass 2 sums a contiguous range per row.
-__device__ void matvec_constraints(const FFArgs& a, const double4* v, int skip = 0) {
+template <class Meta = std::nullptr_t>
+__device__ void matvec_constraints(const FFArgs& a, const double4* v, int skip = 0, const Meta* mm = nullptr) {
   const int64_t c0 = gtid() - 32 * skip;
   if (c0 < 0) return;
-  for (int64_t c = c0; c < a.C; c += gstride() - 32 * skip) {
+  int k_round = 0;
+  for (int64_t c = c0; c < a.C; c += gstride() - 32 * skip, ++k_round) {
     int rows[8];
     double w[8];
-    ld_anchors(a, c, rows, w);
+    double4 gc;
+    int kind;
+    int4 p0, p1;
+    bool cached = false;
+    if constexpr (!std::is_same<Meta, std::nullptr_t>::value) {
+      if (mm && mm->cons) {
+        cached = true;
+        const int q = k_round * int(blockDim.x) + threadIdx.x;
+        const int SC = int(blockDim.x) * ((a.C + (gstride() - 32 * skip) - 1) / (gstride() - 32 * skip));
+        const int4 r0 = mm->crow[q], r1 = mm->crow[SC + q];
+        const double4 w0 = mm->cw[q], w1 = mm->cw[SC + q];
+        rows[0] = r0.x; rows[1] = r0.y; rows[2] = r0.z; rows[3] = r0.w;
+        rows[4] = r1.x; rows[5] = r1.y; rows[6] = r1.z; rows[7] = r1.w;
+        w[0] = w0.x; w[1] = w0.y; w[2] = w0.z; w[3] = w0.w;
+        w[4] = w1.x; w[5] = w1.y; w[6] = w1.z; w[7] = w1.w;
+        gc = mm->cg[q];
+        kind = mm->ckind[q];
+        p0 = mm->cpos[q];
+        p1 = mm->cpos[SC + q];
+      }
+    }
+    if (!cached) {
+      ld_anchors(a, c, rows, w);
+      gc = ld4w(a.c_g, c);
+      kind = a.c_kind[c];
+      p0 = a.c_pos[2 * c];
+      p1 = a.c_pos[2 * c + 1];
+    }
     V3 q{0, 0, 0};
 #pragma unroll
     for (int k = 0; k < 8; ++k)
       if (rows[k] >= 0) q += w[k] * ld4(v, rows[k]);
-    const double4 gc = a.c_g[c];
     V3 u;
-    if (a.c_kind[c] == WFK_DENSE_PLANE) {
+    if (kind == WFK_DENSE_PLANE) {
       const V3 g{gc.x, gc.y, gc.z};
       u = (gc.w * dot(g, q)) * g;
     } else {
       u = gc.w * q;
     }
-    const int4 p0 = a.c_pos[2 * c], p1 = a.c_pos[2 * c + 1];
     const int pos[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
 #pragma unroll
     for (int k = 0; k < 8; ++k)
@@ -1016,7 +1056,8 @@ __device__ void pcg(const FFArgs& a, cg::grid_group& grid, Red& rs, int& iters, 
     double v3[3] = {0, 0, 0};
     for (int r = int(gtid()); r < a.N; r += int(gstride())) {
       const V3 w = ASM ? ld4(a.w, r) : row_from_items(a, r);
-      const double4 u4 = a.u[r], p4 = a.p[r], s4 = a.ap[r], x4 = a.x[r], r4 = a.r[r], d4 = a.dinv[r];
+      const double4 u4 = ld4w(a.u, r), p4 = ld4w(a.p, r), s4 = ld4w(a.ap, r), x4 = ld4w(a.x, r), r4 = ld4w(a.r, r),
+                    d4 = ld4w(a.dinv, r);
       const V3 p = V3{u4.x, u4.y, u4.z} + beta * V3{p4.x, p4.y, p4.z};
       const V3 sv = w + beta * V3{s4.x, s4.y, s4.z};
       const V3 x = V3{x4.x, x4.y, x4.z} + alpha * p;
@@ -1066,8 +1107,9 @@ __device__ void pcg(const FFArgs& a, cg::grid_group& grid, Red& rs, int& iters, 
 // lanes, a sub-warp shuffle tree sums them (fixed order), and the group
 // leader receives (A v)_r -- so a row is complete inside one warp and its
 // update can follow without another grid barrier.
-template <class Sink>
-__device__ __forceinline__ void row_pass_mf(const FFArgs& a, const double4* v, Sink& sink, int skip = 0) {
+template <class Sink, class Meta = std::nullptr_t, class Sl = std::nullptr_t>
+__device__ __forceinline__ void row_pass_mf(const FFArgs& a, const double4* v, Sink& sink, int skip = 0,
+                                            const Meta* mm = nullptr, const Sl* sl = nullptr) {
   constexpr int L = kMfLanes, RPW = 32 / L;
   const int lane = threadIdx.x & 31;
   const int sub = lane % L, grp = lane / L;
@@ -1076,15 +1118,37 @@ __device__ __forceinline__ void row_pass_mf(const FFArgs& a, const double4* v, S
   for (int base = (gwarp() - skip) * RPW; base < a.N; base += (nwarps() - skip) * RPW) {
     const int r = base + grp;
     const bool live = r < a.N;
-    const bool frozen = live && a.frozen[r];
+    int e0 = 0, e1 = 0, nb[6] = {-1, -1, -1, -1, -1, -1};
+    bool frozen = false;
+    bool cached = false;
+    if constexpr (!std::is_same<Meta, std::nullptr_t>::value) {
+      if (mm && mm->rows) {
+        cached = true;
+        if (live) {
+          const int q = sl->of(r);
+          const int4 m0 = mm->rm[q], m1 = mm->rn[q];
+          e0 = m0.x;
+          e1 = m0.y;
+          frozen = m0.z != 0;
+          nb[0] = m0.w; nb[1] = m1.x; nb[2] = m1.y; nb[3] = m1.z; nb[4] = m1.w;
+          nb[5] = mm->rn5[q];
+        }
+      }
+    }
+    if (!cached && live) {
+      frozen = a.frozen[r];
+      e0 = a.row_ptr[r];
+      e1 = a.row_ptr[r + 1];
+#pragma unroll
+      for (int k = sub; k < 6; k += L) nb[k] = a.nbr[int64_t(k) * a.N + r];
+    }
     const V3 vr = live ? ld4(v, r) : V3{0, 0, 0};
     V3 acc{0, 0, 0};
     if (live && !frozen) {
-      const int e0 = a.row_ptr[r], e1 = a.row_ptr[r + 1];
       for (int e = e0 + sub; e < e1; e += L) acc += ld4(a.contrib, e);
 #pragma unroll
       for (int k = sub; k < 6; k += L) {
-        const int j = a.nbr[int64_t(k) * a.N + r];
+        const int j = nb[k];
         if (j >= 0) acc += w2 * (vr - ld4(v, j));
       }
     }
@@ -1209,6 +1273,86 @@ __device__ __forceinline__ void for_warp_rows(int N, int skip, F f) {
   }
 }
 
+// Shared-memory row slots of the pipelined PCG.  The rows a warp receives
+// from the row pass (L lanes per row: RPW rows per round, rounds nw warps
+// apart) are always the same, so their Krylov state lives in the block's
+// shared memory for the whole solve: slot (warp-in-block, round, row-in-round),
+// vector-major (SoA) so consecutive lanes hit consecutive 32-byte words.
+enum { kSx, kSr, kSw, kSp, kSs, kSz, kSd, kSn, kSlotVecs };
+struct Slots {
+  double4* sm;  // kSlotVecs x S
+  int S;        // slots per block = warps per block x K x RPW
+  int K;        // rounds per warp
+  int RPW, gw, nw;
+  __device__ __forceinline__ int of(int r) const {
+    return int(threadIdx.x >> 5) * K * RPW + ((r / RPW - gw) / nw) * RPW + r % RPW;
+  }
+  __device__ __forceinline__ double4& at(int v, int slot) const { return sm[v * S + slot]; }
+};
+__host__ __device__ constexpr int pipe_rpw(bool asm_level, bool rows_on_lanes) {
+  return rows_on_lanes ? 32 : 32 / (asm_level ? kAsmLanes : kMfLanes);
+}
+// Shared-memory layout of one pipelined solve (host and device compute it
+// alike): the row-state slots; on matrix-free levels optionally each row
+// slot's metadata {e0, e1, frozen, 6 neighbours} (36 B) and each constraint
+// slot's anchors, weights, g, incidence slots and kind (164 B), which are
+// fixed for the whole solve and so cost one gather chain per iteration less.
+struct PipeLayout {
+  int K, S;      // rounds per warp, row slots per block
+  int KC, SC;    // constraint rounds per thread, constraint slots per block
+  size_t rmeta, cmeta, total;  // byte offsets / size
+};
+__host__ __device__ inline PipeLayout pipe_layout(int N, int64_t C, int rpw, int G, int tpb, int skip, bool rows,
+                                                  bool cons) {
+  PipeLayout l;
+  const int wpb = tpb / 32;
+  const int nw = G * wpb - skip;
+  l.K = (N + nw * rpw - 1) / (nw * rpw);
+  l.S = wpb * l.K * rpw;
+  const int64_t nt = int64_t(G) * tpb - 32 * skip;
+  l.KC = cons ? int((C + nt - 1) / nt) : 0;
+  l.SC = tpb * l.KC;
+  size_t off = size_t(kSlotVecs) * l.S * sizeof(double4);
+  l.rmeta = off;
+  if (rows) off += size_t(l.S) * (2 * sizeof(int4) + sizeof(int));
+  off = (off + 31) / 32 * 32;
+  l.cmeta = off;
+  if (cons) off += size_t(l.SC) * (4 * sizeof(int4) + 3 * sizeof(double4) + sizeof(int));
+  l.total = off;
+  return l;
+}
+// SMEM views of the cached metadata
+struct MfMeta {
+  const int4* rm;   // S: e0, e1, frozen, nbr0
+  const int4* rn;   // S: nbr1..nbr4
+  const int* rn5;   // S: nbr5
+  const int4* crow; // 2 SC
+  const int4* cpos; // 2 SC
+  const double4* cw;  // 2 SC
+  const double4* cg;  // SC
+  const int* ckind;   // SC
+  bool rows, cons;
+};
+__device__ inline MfMeta mf_meta(char* base, const PipeLayout& l, bool rows, bool cons) {
+  MfMeta m;
+  m.rows = rows;
+  m.cons = cons;
+  char* r = base + l.rmeta;
+  m.rm = reinterpret_cast<const int4*>(r);
+  m.rn = reinterpret_cast<const int4*>(r + size_t(l.S) * sizeof(int4));
+  m.rn5 = reinterpret_cast<const int*>(r + size_t(l.S) * 2 * sizeof(int4));
+  char* c = base + l.cmeta;
+  const size_t SC = size_t(l.SC);
+  m.cw = reinterpret_cast<const double4*>(c);
+  m.cg = reinterpret_cast<const double4*>(c + 2 * SC * sizeof(double4));
+  m.crow = reinterpret_cast<const int4*>(c + 3 * SC * sizeof(double4));
+  m.cpos = reinterpret_cast<const int4*>(c + 3 * SC * sizeof(double4) + 2 * SC * sizeof(int4));
+  m.ckind = reinterpret_cast<const int*>(c + 3 * SC * sizeof(double4) + 4 * SC * sizeof(int4));
+  return m;
+}
+constexpr int kPipeSkip = 1;  // global warp 0 sums the split reductions
+constexpr size_t kPipeSmemMax = 220 * 1024;  // dynamic shared memory for the row slots
+
 // pcg_solve (solver.cpp:282-343) as pipelined Jacobi-PCG (Ghysels & Vanroose
 // 2014): the same Krylov iterates as the reference's PCG in exact arithmetic,
 // with w = A u, s = A p and z = A D s carried by recurrences, so the one grid
@@ -1222,46 +1366,106 @@ __device__ __forceinline__ void for_warp_rows(int N, int skip, F f) {
 // r -= alpha s, w -= alpha z, u = D r, m' = D w (into the other m buffer, as
 // slower blocks may still gather the current one).  alpha and beta are the
 // reference's: alpha = r.u / p.Ap with p.Ap = w.u - beta r.u / alpha_prev.
+// Only m (gathered by neighbours) lives in global memory; x, r, w, p, s, z,
+// D^-1 and n stay in the shared-memory slots of the warp that owns the row.
 // Stopping rule, breakdown test and iteration count are the reference's.
 template <bool ASM>
 __device__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, double& relres) {
+  extern __shared__ double4 dyn_smem[];
   iters = 0;
   relres = 0;
   PhaseClock pc(a.dbg);
-  // r0 = b - A x0, u0 = D^-1 r0 (solver.cpp:305-310) -- all warps, classic reductions
+  constexpr int kSkip = kPipeSkip;
+  const bool comm = gwarp() == 0;
+  constexpr int LM = ASM ? kAsmLanes : kMfLanes;
+  const bool rows_on_lanes = ASM && a.asm_rows_on_lanes;
+  Slots sl;
+  sl.sm = dyn_smem;
+  sl.RPW = pipe_rpw(ASM, rows_on_lanes);
+  const PipeLayout lay =
+      pipe_layout(a.N, a.C, sl.RPW, gridDim.x, blockDim.x, kSkip, !ASM && a.meta_rows, !ASM && a.meta_cons);
+  sl.K = lay.K;
+  sl.S = lay.S;
+  sl.gw = gwarp() - kSkip;
+  sl.nw = nwarps() - kSkip;
+  const MfMeta mm = mf_meta(reinterpret_cast<char*>(dyn_smem), lay, !ASM && a.meta_rows, !ASM && a.meta_cons);
+  const MfMeta* mmp = ASM ? nullptr : &mm;
+  auto matvec = [&](const double4* v, auto& sink) {
+    if (ASM) {
+      row_pass<true>(a, v, sink, kSkip);
+    } else {
+      matvec_constraints(a, v, kSkip, mmp);
+      grid_barrier(a, rs);
+      row_pass_mf(a, v, sink, kSkip, mmp, &sl);
+    }
+  };
+  auto each_row = [&](auto f) {
+    if (rows_on_lanes)
+      for_warp_rows<1>(a.N, kSkip, f);
+    else
+      for_warp_rows<LM>(a.N, kSkip, f);
+  };
+  if (!ASM && (mm.rows || mm.cons)) {
+    // the solve's fixed row / constraint metadata into shared memory
+    if (mm.rows)
+      each_row([&](int r) {
+        const int q = sl.of(r);
+        int nb[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) nb[k] = a.nbr[int64_t(k) * a.N + r];
+        const_cast<int4*>(mm.rm)[q] = make_int4(a.row_ptr[r], a.row_ptr[r + 1], a.frozen[r], nb[0]);
+        const_cast<int4*>(mm.rn)[q] = make_int4(nb[1], nb[2], nb[3], nb[4]);
+        const_cast<int*>(mm.rn5)[q] = nb[5];
+      });
+    if (mm.cons) {
+      const int64_t c0 = gtid() - 32 * kSkip;
+      if (c0 >= 0)
+        for (int64_t c = c0, k = 0; c < a.C; c += gstride() - 32 * kSkip, ++k) {
+          const int q = int(k) * blockDim.x + threadIdx.x;
+          const int SC = lay.SC;
+          const_cast<int4*>(mm.crow)[q] = a.c_row[2 * c];
+          const_cast<int4*>(mm.crow)[SC + q] = a.c_row[2 * c + 1];
+          const_cast<double4*>(mm.cw)[q] = a.c_w[2 * c];
+          const_cast<double4*>(mm.cw)[SC + q] = a.c_w[2 * c + 1];
+          const_cast<int4*>(mm.cpos)[q] = a.c_pos[2 * c];
+          const_cast<int4*>(mm.cpos)[SC + q] = a.c_pos[2 * c + 1];
+          const_cast<double4*>(mm.cg)[q] = a.c_g[c];
+          const_cast<int*>(mm.ckind)[q] = a.c_kind[c];
+        }
+    }
+    __syncthreads();
+  }
+  // r0 = b - A x0, u0 = D^-1 r0 (solver.cpp:305-310)
   double acc_rr = 0, acc_bb = 0;
-  auto init_sink = [&](int r, V3, V3 ax) {
+  auto init_sink = [&](int r, V3 xr, V3 ax) {
     const V3 b = ld4(a.rhs, r);
     const V3 rr = b - ax;
-    st4(a.r, r, rr);
-    st4(a.u, r, cmul(ld4(a.dinv, r), rr));
+    const double4 d4 = ld4w(a.dinv, r);
+    st4(a.u, r, cmul(V3{d4.x, d4.y, d4.z}, rr));
+    const int q = sl.of(r);
     const double4 zero = make_double4(0, 0, 0, 0);
-    a.p[r] = zero;
-    a.ap[r] = zero;
-    a.z[r] = zero;
+    sl.at(kSx, q) = make_double4(xr.x, xr.y, xr.z, 0.0);
+    sl.at(kSr, q) = make_double4(rr.x, rr.y, rr.z, 0.0);
+    sl.at(kSp, q) = zero;
+    sl.at(kSs, q) = zero;
+    sl.at(kSz, q) = zero;
+    sl.at(kSd, q) = d4;
     acc_rr += dot(rr, rr);
     acc_bb += sqnorm(b);
   };
-  auto matvec_all = [&](const double4* v, auto& sink) {
-    if (ASM) {
-      row_pass<true>(a, v, sink);
-    } else {
-      matvec_constraints(a, v);
-      grid_barrier(a, rs);
-      row_pass_mf(a, v, sink);
-    }
-  };
-  matvec_all(a.x, init_sink);
+  matvec(a.x, init_sink);
   grid_barrier(a, rs);
   // w0 = A u0, m0 = D w0
   double v4[4] = {0, 0, 0, 0};
   auto w_sink = [&](int r, V3 ur, V3 wr) {
-    st4(a.w, r, wr);
-    st4(a.m0, r, cmul(ld4(a.dinv, r), wr));
-    v4[0] += dot(ld4(a.r, r), ur);
+    const int q = sl.of(r);
+    const double4 d4 = sl.at(kSd, q), r4 = sl.at(kSr, q);
+    sl.at(kSw, q) = make_double4(wr.x, wr.y, wr.z, 0.0);
+    st4(a.m0, r, cmul(V3{d4.x, d4.y, d4.z}, wr));
+    v4[0] += dot(V3{r4.x, r4.y, r4.z}, ur);
     v4[1] += dot(wr, ur);
   };
-  matvec_all(a.u, w_sink);
+  matvec(a.u, w_sink);
   v4[2] = acc_rr;
   v4[3] = acc_bb;
   grid_reduce<4>(a, rs, v4);
@@ -1276,29 +1480,25 @@ __device__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, double& relres) {
   relres = r_norm / b_norm;
   const double stop = fmax(a.pcg_tol * r_norm, 1e-13 * b_norm);
   double gamma_prev = 0, alpha_prev = 0;
-  constexpr int kSkip = 1;  // global warp 0 sums the split reductions
-  const bool comm = gwarp() == 0;
-  constexpr int LM = ASM ? kAsmLanes : kMfLanes;
-  const bool rows_on_lanes = ASM && a.asm_rows_on_lanes;
   unsigned seq = 0;
   bool pending = false;  // totals of reduction seq - 1 not yet read
   pc.lap(12);
   for (int it = 0; it < a.pcg_max; ++it) {
     const double4* mcur = (it & 1) ? a.m1 : a.m0;
     double4* mnext = (it & 1) ? a.m0 : a.m1;
-    // n = A m for own rows (stored by the row's leader lane), overlapped
-    // with the totals of the previous update
-    auto n_sink = [&](int r, V3, V3 n) { st4(a.nbuf, r, n); };
+    // n = A m for own rows (into the leader's slot), overlapped with the
+    // totals of the previous update
+    auto n_sink = [&](int r, V3, V3 n) { sl.at(kSn, sl.of(r)) = make_double4(n.x, n.y, n.z, 0.0); };
     if (ASM) {
       if (comm && pending) split_total(a, seq - 1);
-      row_pass<true>(a, mcur, n_sink, kSkip);
+      matvec(mcur, n_sink);
     } else {
-      matvec_constraints(a, mcur, kSkip);
+      matvec_constraints(a, mcur, kSkip, mmp);
       if (comm && pending) split_total(a, seq - 1);
       pc.lap(0);
       grid_barrier(a, rs);
       pc.lap(1);
-      row_pass_mf(a, mcur, n_sink, kSkip);
+      row_pass_mf(a, mcur, n_sink, kSkip, mmp, &sl);
     }
     pc.lap(2);
     if (pending) {
@@ -1319,8 +1519,9 @@ __device__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, double& relres) {
     const double alpha = gamma / pap;
     double v3[3] = {0, 0, 0};
     auto upd = [&](int r) {
-      const double4 n4 = a.nbuf[r], w4 = a.w[r], s4 = a.ap[r], z4 = a.z[r], p4 = a.p[r], x4 = a.x[r],
-                    r4 = a.r[r], d4 = a.dinv[r];
+      const int q = sl.of(r);
+      const double4 n4 = sl.at(kSn, q), w4 = sl.at(kSw, q), s4 = sl.at(kSs, q), z4 = sl.at(kSz, q),
+                    p4 = sl.at(kSp, q), x4 = sl.at(kSx, q), r4 = sl.at(kSr, q), d4 = sl.at(kSd, q);
       const V3 d{d4.x, d4.y, d4.z};
       const V3 w{w4.x, w4.y, w4.z};
       V3 rr{r4.x, r4.y, r4.z};
@@ -1331,21 +1532,18 @@ __device__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, double& relres) {
       rr = rr - alpha * sv;
       const V3 wn = w - alpha * z;
       const V3 u = cmul(d, rr);
-      st4(a.z, r, z);
-      st4(a.ap, r, sv);
-      st4(a.p, r, p);
-      st4(a.x, r, x);
-      st4(a.r, r, rr);
-      st4(a.w, r, wn);
+      sl.at(kSz, q) = make_double4(z.x, z.y, z.z, 0.0);
+      sl.at(kSs, q) = make_double4(sv.x, sv.y, sv.z, 0.0);
+      sl.at(kSp, q) = make_double4(p.x, p.y, p.z, 0.0);
+      sl.at(kSx, q) = make_double4(x.x, x.y, x.z, 0.0);
+      sl.at(kSr, q) = make_double4(rr.x, rr.y, rr.z, 0.0);
+      sl.at(kSw, q) = make_double4(wn.x, wn.y, wn.z, 0.0);
       st4(mnext, r, cmul(d, wn));
       v3[0] += dot(rr, u);
       v3[1] += dot(wn, u);
       v3[2] += dot(rr, rr);
     };
-    if (rows_on_lanes)
-      for_warp_rows<1>(a.N, kSkip, upd);
-    else
-      for_warp_rows<LM>(a.N, kSkip, upd);
+    each_row(upd);
     pc.lap(4);
     split_arrive(a, rs, v3, seq);
     pc.lap(7);
@@ -1363,6 +1561,9 @@ __device__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, double& relres) {
     r_norm = sqrt(v3[2]);
     relres = r_norm / b_norm;
   }
+  // the solution back to global memory for the write-back phase
+  each_row([&](int r) { st4w(a.x, r, sl.at(kSx, sl.of(r))); });
+  grid_barrier(a, rs);
 }
 
 // update_rotations (solver.cpp:385-417) for every row; rot[] follows euler.
@@ -1959,10 +2160,37 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
     if (e_out) *e_out = wfk_energy{0, 0, 0, 0};
     return;
   }
+  // pipelined PCG keeps the row state in shared memory; levels too large for
+  // it use the Chronopoulos-Gear variant (state in global memory)
+  size_t smem = 0;
+  a.meta_rows = a.meta_cons = 0;
+  if (a.pcg_variant == 0) {
+    const int rpw = pipe_rpw(L.assembled, a.asm_rows_on_lanes);
+    auto bytes = [&](bool rows, bool cons) {
+      return pipe_layout(L.N, L.C, rpw, G, kCoopBlock, kPipeSkip, rows, cons).total;
+    };
+    static const bool no_meta = getenv("WFK_PIPE_NO_META") != nullptr;
+    if (!L.assembled && !no_meta && bytes(true, true) <= kPipeSmemMax) {
+      a.meta_rows = a.meta_cons = 1;
+    } else if (!L.assembled && !no_meta && bytes(true, false) <= kPipeSmemMax) {
+      a.meta_rows = 1;
+    }
+    smem = bytes(a.meta_rows, a.meta_cons);
+    if (smem > kPipeSmemMax) {
+      a.pcg_variant = 1;
+      a.meta_rows = a.meta_cons = 0;
+      smem = 0;
+    }
+  }
+  static bool smem_attr = false;
+  if (!smem_attr) {
+    WFK_CUDA(cudaFuncSetAttribute(k_flip_flop, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPipeSmemMax)));
+    smem_attr = true;
+  }
   void* args[] = {&a};
   Prof& pf = c->prof;
   if (pf.on) WFK_CUDA(cudaEventRecord(pf.ev[0], s));
-  WFK_CUDA(cudaLaunchCooperativeKernel((void*)k_flip_flop, dim3(G), dim3(kCoopBlock), args, 0, s));
+  WFK_CUDA(cudaLaunchCooperativeKernel((void*)k_flip_flop, dim3(G), dim3(kCoopBlock), args, smem, s));
   if (pf.on) WFK_CUDA(cudaEventRecord(pf.ev[1], s));
   count_launch(c);
   int32_t st[4];

@@ -23,7 +23,10 @@ constexpr int kAssembleRatio = 32; // incidences per row above which B^T B is as
 constexpr int kHeavyRow = 16;       // incidences above which a row is summed by a whole warp
 constexpr int kAsmLanes = 8;        // lanes per row on small assembled levels (27 stencil slots)
 constexpr int kAsmThreadRows = 16384;  // rows from which assembled levels put one row per lane
-constexpr int kMfLanes = 4;         // lanes per row of the matrix-free row pass (pipelined PCG)
+#ifndef WFK_MF_LANES
+#define WFK_MF_LANES 2
+#endif
+constexpr int kMfLanes = WFK_MF_LANES;  // lanes per row of the matrix-free row pass (pipelined PCG)
 constexpr int kItemLen = 8;         // incidences per work item of the matrix-free row pass
 constexpr int kCacheWarpRow = 32;   // incidences above which the constraint cache sums a row by warp
 constexpr int kCenter = 13;

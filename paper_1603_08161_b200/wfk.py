@@ -21,7 +21,8 @@ from .abi import (CORR_DTYPE, CorrespondParams, Energy, ExpansionStats, FrameVie
                   trace_to_list, VOL_ALL, WFK_OK)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libwfk.so")
+# WFK_LIBRARY: an alternate build of the same library (kernel-variant experiments)
+LIB_PATH = os.environ.get("WFK_LIBRARY") or os.path.join(HERE, "_lib", "libwfk.so")
 CSRC = os.path.join(HERE, "csrc")
 
 
