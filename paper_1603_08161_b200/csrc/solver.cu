@@ -455,6 +455,7 @@ struct FFArgs {
   double4* nbuf;         // pipelined PCG: n = A m of the rows a thread leads
   unsigned long long* sync_ll;  // split-reduction totals (flag-embedded words)
   int meta_rows, meta_cons;     // pipelined matrix-free levels: metadata cached in shared memory
+  int asm_smem;                 // pipelined assembled levels: B^T B rows cached in shared memory
   int pcg_variant;       // 0 pipelined (one reduction, overlapped), 1 Chronopoulos-Gear
   const double4 *crhs, *cdiag;
   double* rot;  // 9 per row
@@ -811,8 +812,10 @@ __device__ __forceinline__ V3 matvec_row(const FFArgs& a, const double4* v, int 
 //  * Matrix-free levels: one thread per light row summing its contiguous
 //    incidence contributions; rows with more than kHeavyRow incidences go to
 //    a whole warp (coalesced 256-bit loads, lanes 0-5 one face neighbour each).
-template <bool ASM, class Sink>
-__device__ __forceinline__ void row_pass(const FFArgs& a, const double4* v, Sink& sink, int skip = 0) {
+template <bool ASM, class Sink, class Sl = std::nullptr_t>
+__device__ __forceinline__ void row_pass(const FFArgs& a, const double4* v, Sink& sink, int skip = 0,
+                                         const Sl* sl = nullptr, const double* smb = nullptr,
+                                         const int* smc = nullptr) {
   const int lane = threadIdx.x & 31;
   const double w2 = 2.0 * a.w_r;
   if (gwarp() < skip) return;  // warps reserved for the split reduction
@@ -852,13 +855,22 @@ __device__ __forceinline__ void row_pass(const FFArgs& a, const double4* v, Sink
       const bool frozen = live && a.frozen[r];
       const V3 vr = live ? ld4(v, r) : V3{0, 0, 0};
       V3 acc{0, 0, 0};
+      const double* bb = a.blk + int64_t(r) * 27 * 6;
+      const int* cc = a.cols + int64_t(r) * 27;
+      if constexpr (!std::is_same<Sl, std::nullptr_t>::value) {
+        if (smb && live) {  // the solve's blocks of this warp's rows, cached in shared memory
+          const int q = sl->of(r);
+          bb = smb + q * 27 * 6;
+          cc = smc + q * 27;
+        }
+      }
       if (live && !frozen) {
 #pragma unroll
         for (int s = sub; s < 27; s += L) {
-          const int col = a.cols[int64_t(r) * 27 + s];
+          const int col = cc[s];
           if (col < 0) continue;
           const V3 x = ld4(v, col);
-          const double* b = a.blk + (int64_t(r) * 27 + s) * 6;  // xx xy xz yy yz zz
+          const double* b = bb + s * 6;  // xx xy xz yy yz zz
           acc.x += b[0] * x.x + b[1] * x.y + b[2] * x.z;
           acc.y += b[1] * x.x + b[3] * x.y + b[4] * x.z;
           acc.z += b[2] * x.x + b[4] * x.y + b[5] * x.z;
@@ -1300,10 +1312,10 @@ __host__ __device__ constexpr int pipe_rpw(bool asm_level, bool rows_on_lanes) {
 struct PipeLayout {
   int K, S;      // rounds per warp, row slots per block
   int KC, SC;    // constraint rounds per thread, constraint slots per block
-  size_t rmeta, cmeta, total;  // byte offsets / size
+  size_t rmeta, cmeta, amat, total;  // byte offsets / size
 };
 __host__ __device__ inline PipeLayout pipe_layout(int N, int64_t C, int rpw, int G, int tpb, int skip, bool rows,
-                                                  bool cons) {
+                                                  bool cons, bool amat = false) {
   PipeLayout l;
   const int wpb = tpb / 32;
   const int nw = G * wpb - skip;
@@ -1318,6 +1330,9 @@ __host__ __device__ inline PipeLayout pipe_layout(int N, int64_t C, int rpw, int
   off = (off + 31) / 32 * 32;
   l.cmeta = off;
   if (cons) off += size_t(l.SC) * (4 * sizeof(int4) + 3 * sizeof(double4) + sizeof(int));
+  off = (off + 31) / 32 * 32;
+  l.amat = off;  // assembled levels: 27 x 6 block values + 27 columns per row slot
+  if (amat) off += size_t(l.S) * 27 * (6 * sizeof(double) + sizeof(int));
   l.total = off;
   return l;
 }
@@ -1382,17 +1397,36 @@ __device__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, double& relres) {
   Slots sl;
   sl.sm = dyn_smem;
   sl.RPW = pipe_rpw(ASM, rows_on_lanes);
+  const bool amat = ASM && a.asm_smem && !rows_on_lanes;
   const PipeLayout lay =
-      pipe_layout(a.N, a.C, sl.RPW, gridDim.x, blockDim.x, kSkip, !ASM && a.meta_rows, !ASM && a.meta_cons);
+      pipe_layout(a.N, a.C, sl.RPW, gridDim.x, blockDim.x, kSkip, !ASM && a.meta_rows, !ASM && a.meta_cons, amat);
   sl.K = lay.K;
   sl.S = lay.S;
   sl.gw = gwarp() - kSkip;
   sl.nw = nwarps() - kSkip;
   const MfMeta mm = mf_meta(reinterpret_cast<char*>(dyn_smem), lay, !ASM && a.meta_rows, !ASM && a.meta_cons);
   const MfMeta* mmp = ASM ? nullptr : &mm;
+  double* smb = amat ? reinterpret_cast<double*>(reinterpret_cast<char*>(dyn_smem) + lay.amat) : nullptr;
+  int* smc = amat ? reinterpret_cast<int*>(reinterpret_cast<char*>(dyn_smem) + lay.amat + size_t(lay.S) * 27 * 48)
+                  : nullptr;
+  if (amat && gwarp() >= kSkip) {
+    // this warp's rows of B^T B into shared memory (fixed for the whole solve)
+    const int lane = threadIdx.x & 31;
+    for (int idx = 0; idx < sl.K * sl.RPW; ++idx) {
+      const int r = (sl.gw + (idx / sl.RPW) * sl.nw) * sl.RPW + idx % sl.RPW;
+      if (r >= a.N) break;
+      const int q = sl.of(r);
+      for (int t = lane; t < 27 * 6; t += 32) smb[q * 27 * 6 + t] = a.blk[int64_t(r) * 27 * 6 + t];
+      if (lane < 27) smc[q * 27 + lane] = a.cols[int64_t(r) * 27 + lane];
+    }
+    __syncwarp();
+  }
   auto matvec = [&](const double4* v, auto& sink) {
     if (ASM) {
-      row_pass<true>(a, v, sink, kSkip);
+      if (amat)
+        row_pass<true>(a, v, sink, kSkip, &sl, smb, smc);
+      else
+        row_pass<true>(a, v, sink, kSkip);
     } else {
       matvec_constraints(a, v, kSkip, mmp);
       grid_barrier(a, rs);
@@ -2164,18 +2198,24 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   // it use the Chronopoulos-Gear variant (state in global memory)
   size_t smem = 0;
   a.meta_rows = a.meta_cons = 0;
+  a.asm_smem = 0;
   if (a.pcg_variant == 0) {
     const int rpw = pipe_rpw(L.assembled, a.asm_rows_on_lanes);
     auto bytes = [&](bool rows, bool cons) {
       return pipe_layout(L.N, L.C, rpw, G, kCoopBlock, kPipeSkip, rows, cons).total;
     };
     static const bool no_meta = getenv("WFK_PIPE_NO_META") != nullptr;
+    a.asm_smem = 0;
+    if (L.assembled && !a.asm_rows_on_lanes && !no_meta &&
+        pipe_layout(L.N, L.C, rpw, G, kCoopBlock, kPipeSkip, false, false, true).total <= kPipeSmemMax)
+      a.asm_smem = 1;
     if (!L.assembled && !no_meta && bytes(true, true) <= kPipeSmemMax) {
       a.meta_rows = a.meta_cons = 1;
     } else if (!L.assembled && !no_meta && bytes(true, false) <= kPipeSmemMax) {
       a.meta_rows = 1;
     }
-    smem = bytes(a.meta_rows, a.meta_cons);
+    smem = a.asm_smem ? pipe_layout(L.N, L.C, rpw, G, kCoopBlock, kPipeSkip, false, false, true).total
+                      : bytes(a.meta_rows, a.meta_cons);
     if (smem > kPipeSmemMax) {
       a.pcg_variant = 1;
       a.meta_rows = a.meta_cons = 0;
