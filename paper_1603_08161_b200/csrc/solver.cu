@@ -117,7 +117,7 @@ __global__ void k_con_prepare(int64_t C, const int32_t* kind, const double* targ
                               const double* conf, const int32_t* c_node, const double* c_w,
                               const int32_t* node_row, const int32_t* uf, PoseD pose, double w_d, double w_s,
                               int N, int32_t* c_row, double* c_g, double* c_b, int32_t* c_kind,
-                              uint8_t* comp_flag, int32_t* key, int32_t* val, int32_t* cnt, int32_t* n_ent) {
+                              uint8_t* comp_flag, int32_t* key, int32_t* val) {
   const M3 rt = transpose(pose.r);
   for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < C; c += int64_t(gridDim.x) * blockDim.x) {
     const bool dense = kind[c] == WFK_DENSE_PLANE;
@@ -138,7 +138,6 @@ __global__ void k_con_prepare(int64_t C, const int32_t* kind, const double* targ
       c_g[4 * c + 3] = w_s * conf[c];
       c_b[c] = 0.0;
     }
-    int local = 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int row = node_row[c_node[8 * c + k]];
@@ -149,14 +148,22 @@ __global__ void k_con_prepare(int64_t C, const int32_t* kind, const double* targ
       if (row >= 0 && w != 0) {
         key[8 * c + k] = row * 8 + (7 - k);  // cell order of solver.cpp:185-187
         val[8 * c + k] = int32_t(8 * c + k);
-        atomicAdd(&cnt[row], 1);
-        ++local;
       } else {
         key[8 * c + k] = N * 8;  // sentinel, sorts last
         val[8 * c + k] = int32_t(8 * c + k);
       }
     }
-    if (local) atomicAdd(n_ent, local);
+  }
+}
+
+// row_ptr from the sorted incidence keys (row * 8 + corner; sentinel N * 8):
+// position e starts every row in (row(e - 1), row(e)], position E8 closes the
+// rest, so row_ptr[N] = E (the sentinels sort last).
+__global__ void k_row_ptr_from_keys(int64_t E8, const int32_t* key, int N, int32_t* row_ptr) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e <= E8; e += int64_t(gridDim.x) * blockDim.x) {
+    const int row = e < E8 ? min(key[e] >> 3, N) : N;
+    const int prev = e > 0 ? min(key[e - 1] >> 3, N) : -1;
+    for (int r = prev + 1; r <= row; ++r) row_ptr[r] = int32_t(e);
   }
 }
 
@@ -165,8 +172,9 @@ __global__ void k_frozen(int N, const int32_t* uf, const uint8_t* comp_flag, uin
     frozen[r] = comp_flag[uf[r]] ? 0 : 1;
 }
 
-__global__ void k_entries(int64_t E, const int32_t* sorted_val, const double* c_w, int32_t* ent_con,
+__global__ void k_entries(const int32_t* n_ent, const int32_t* sorted_val, const double* c_w, int32_t* ent_con,
                           uint8_t* ent_k, double* ent_w, int32_t* c_pos) {
+  const int64_t E = *n_ent;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < E; e += int64_t(gridDim.x) * blockDim.x) {
     const int v = sorted_val[e];
     ent_con[e] = v >> 3;
@@ -293,6 +301,80 @@ __global__ void k_assemble_btb_thread(Grid g, int N, const int32_t* rows, const 
   }
 }
 
+// Same blocks, one warp per row: lanes stage 32 incidences at a time in
+// shared memory (corner, coef * a_i, g, kind, the constraint's 8 weights),
+// then lane s < 27 accumulates its stencil slot over the staged incidences in
+// incidence order -- the reference's accumulation order (as the thread
+// variant), with the row's incidence data loaded once per warp instead of
+// once per slot.
+constexpr int kAsmWarpBlock = 256;
+__global__ void __launch_bounds__(kAsmWarpBlock) k_assemble_btb_rowwarp(
+    Grid g, int N, const int32_t* rows, const int32_t* node_row, const int32_t* row_ptr, const int32_t* ent_con,
+    const uint8_t* ent_k, const double* ent_w, const double* c_w, const double* c_g, const int32_t* c_kind,
+    double* blk, int32_t* cols, int soa) {
+  struct Stage {
+    double sc[32], gx[32], gy[32], gz[32];
+    double w[8][33];  // padded: lane j writes w[k][j]
+    int k[32], dense[32];
+  };
+  __shared__ Stage st_all[kAsmWarpBlock / 32];
+  Stage& st = st_all[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int s = lane;  // stencil slot of this lane (lanes 27..31 only stage)
+  const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = s / 9 - 1;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < N; r += warps) {
+    double b[6] = {0, 0, 0, 0, 0, 0};
+    const int e0 = row_ptr[r], e1 = row_ptr[r + 1];
+    for (int base = e0; base < e1; base += 32) {
+      const int e = base + lane;
+      if (e < e1) {
+        const int c = ent_con[e];
+        st.k[lane] = ent_k[e];
+        st.sc[lane] = c_g[4 * c + 3] * ent_w[e];
+        st.gx[lane] = c_g[4 * c];
+        st.gy[lane] = c_g[4 * c + 1];
+        st.gz[lane] = c_g[4 * c + 2];
+        st.dense[lane] = c_kind[c] == WFK_DENSE_PLANE;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) st.w[k][lane] = c_w[8 * int64_t(c) + k];
+      }
+      __syncwarp();
+      const int cnt = min(32, e1 - base);
+      if (s < 27) {
+        for (int j = 0; j < cnt; ++j) {
+          const int ki = st.k[j];
+          const int ox = (ki & 1) + dx, oy = ((ki >> 1) & 1) + dy, oz = (ki >> 2) + dz;
+          if (ox < 0 || ox > 1 || oy < 0 || oy > 1 || oz < 0 || oz > 1) continue;
+          const double sc = st.sc[j] * st.w[ox + 2 * oy + 4 * oz][j];
+          if (st.dense[j]) {
+            const double gx = st.gx[j], gy = st.gy[j], gz = st.gz[j];
+            b[0] += sc * (gx * gx);
+            b[1] += sc * (gx * gy);
+            b[2] += sc * (gx * gz);
+            b[3] += sc * (gy * gy);
+            b[4] += sc * (gy * gz);
+            b[5] += sc * (gz * gz);
+          } else {
+            b[0] += sc * 1.0;
+            b[3] += sc * 1.0;
+            b[5] += sc * 1.0;
+          }
+        }
+      }
+      __syncwarp();
+    }
+    if (s < 27) {
+      int x, y, z;
+      g.idx3(rows[r], x, y, z);
+      const int col = g.in_grid(x + dx, y + dy, z + dz) ? node_row[g.lin(x + dx, y + dy, z + dz)] : -1;
+      const int64_t ta = int64_t(r) * 27 + s;
+      cols[soa ? int64_t(s) * N + r : ta] = col;
+      for (int m = 0; m < 6; ++m) blk[soa ? (int64_t(s) * 6 + m) * N + r : ta * 6 + m] = b[m];
+    }
+  }
+}
+
 // ConstraintCache (solver.hpp:66-70): constraint part of the rhs and of the
 // Jacobi diagonal.  Rows with at most kCacheWarpRow incidences accumulate in
 // the reference's order (solver.cpp:196-226) on one thread; longer rows (the
@@ -414,6 +496,19 @@ __global__ void k_reanchor(int64_t C, Grid coarse, const double* canonical, int3
 }
 
 // prolongation coarse -> fine over active fine nodes (solver.cpp:518-529)
+// prev <- cur, and flag |= bit if any element differed
+__global__ void k_mask_update(int64_t n, const uint8_t* cur, uint8_t* prev, int32_t* flag, int32_t bit) {
+  bool diff = false;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const uint8_t v = cur[i];
+    if (prev[i] != v) {
+      diff = true;
+      prev[i] = v;
+    }
+  }
+  if (__any_sync(0xffffffffu, diff) && (threadIdx.x & 31) == 0) atomicOr(flag, bit);
+}
+
 __global__ void k_prolong(Grid fine, Grid coarse, const uint8_t* f_act, double* f_def, double* f_eul,
                           const double* c_def, const double* c_eul) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < fine.n(); i += int64_t(gridDim.x) * blockDim.x) {
@@ -1929,11 +2024,15 @@ static void level_rows(wfk_ctx* c, Level& L) {
   // Level 0 mirrors the volume's active mask, which no solve changes: its rows,
   // neighbour table and component labels are reused until the mask changes
   // (compute_active_set / expand_grid / an ACTIVE upload bump active_gen).
+  // Coarse levels: reused while build_hierarchy finds their activity mask
+  // unchanged (it compares against the mask the rows were built from).
   const bool level0 = &L == &c->lv[0];
-  if (level0 && L.rows_gen == c->vol.active_gen && L.rows_gen != 0) {
+  const bool cached = level0 ? (L.rows_gen == c->vol.active_gen && L.rows_gen != 0) : (L.mask_same && L.rows_valid);
+  if (cached) {
     if (L.N > 0) WFK_CUDA(cudaMemsetAsync(L.comp_flag.p, 0, size_t(L.N), s));
     return;
   }
+  L.rows_valid = false;
   L.rows.ensure(size_t(n));
   L.node_row.ensure(size_t(n));
   int32_t* d_count = c->ivec.ensure(16);
@@ -1961,7 +2060,11 @@ static void level_rows(wfk_ctx* c, Level& L) {
   L.row_ptr.ensure(Nc + 1);
   L.cnt.ensure(Nc + 1);
   L.rows_gen = 0;
-  if (N == 0) return;
+  if (N == 0) {
+    L.rows_gen = level0 ? c->vol.active_gen : 0;
+    L.rows_valid = true;
+    return;
+  }
   k_scatter_node_row<<<grid_for(N), kBlock, 0, s>>>(L.rows, N, L.node_row);
   k_row_neighbours<<<grid_for(N), kBlock, 0, s>>>(L.g, L.rows, N, L.node_row, L.nbr, L.uf);
   k_union<<<grid_for(N), kBlock, 0, s>>>(L.nbr, N, L.uf);
@@ -1969,15 +2072,21 @@ static void level_rows(wfk_ctx* c, Level& L) {
   count_launch(c, 4);
   WFK_CUDA(cudaGetLastError());
   L.rows_gen = level0 ? c->vol.active_gen : 0;
+  L.rows_valid = true;
 }
 
 // Prepares the level's constraints (anchors in c_node/c_w) for the solve:
 // rows, frozen rows, incidence transpose and the constraint cache.
+// Prepares the level's constraints (anchors in c_node/c_w) for the solve:
+// rows, frozen rows, incidence transpose and the constraint cache.  No host
+// synchronisation: the incidence count E stays on the device (row_ptr[N]) and
+// every launch is sized by the bound 8C.
 static void level_constraints(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_params& p) {
   cudaStream_t s = c->stream;
   const int64_t C = L.C;
   const int N = L.N;
   const size_t Cc = size_t(C > 0 ? C : 1);
+  const int64_t E8 = 8 * C;  // bound on the incidence count
   L.c_row.ensure(8 * Cc);
   L.c_g.ensure(4 * Cc);
   L.c_b.ensure(Cc);
@@ -1989,96 +2098,91 @@ static void level_constraints(wfk_ctx* c, Level& L, const PoseD& pose, const wfk
   L.val_out.ensure(8 * Cc);
   L.ent_con.ensure(8 * Cc);
   L.ent_w.ensure(8 * Cc);
-  int32_t* d_ne = c->ivec.ensure(16) + 1;
-  WFK_CUDA(cudaMemsetAsync(d_ne, 0, sizeof(int32_t), s));
-  WFK_CUDA(cudaMemsetAsync(L.cnt.p, 0, size_t(N + 1) * sizeof(int32_t), s));
+  L.ent_k.ensure(8 * Cc);
+  L.c_pos.ensure(8 * Cc);
+  L.items_built = false;
   if (C > 0) {
     k_con_prepare<<<grid_for(C), kBlock, 0, s>>>(C, c->cons.kind, c->cons.target, c->cons.normal, c->cons.conf,
                                                  L.c_node, L.c_w, L.node_row, L.uf, pose, p.w_d, p.w_s, N, L.c_row,
-                                                 L.c_g, L.c_b, L.c_kind, L.comp_flag, L.key_in, L.val_in, L.cnt,
-                                                 d_ne);
+                                                 L.c_g, L.c_b, L.c_kind, L.comp_flag, L.key_in, L.val_in);
     count_launch(c);
   }
+  // E upper bound for the host-side decisions; the kernels use row_ptr[N]
+  L.E = E8;
   if (N == 0) {
-    L.E = 0;
     WFK_CUDA(cudaMemsetAsync(L.row_ptr.p, 0, sizeof(int32_t), s));
     return;
   }
   k_frozen<<<grid_for(N), kBlock, 0, s>>>(N, L.uf, L.comp_flag, L.frozen);
   count_launch(c);
-  // row_ptr = exclusive scan of per-row counts
-  size_t tmp = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp, L.cnt.p, L.row_ptr.p, N + 1, s);
-  size_t tmp2 = 0;
   if (C > 0) {
+    // incidences sorted by (row, cell order); rows' ranges from the sorted keys
     int bits = 1;
     while ((int64_t(1) << bits) <= int64_t(N) * 8) ++bits;
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp2, L.key_in.p, L.key_out.p, L.val_in.p, L.val_out.p, int(8 * C), 0,
-                                    bits, s);
-    c->temp.ensure(std::max(tmp, tmp2));
-    WFK_CUDA(cub::DeviceRadixSort::SortPairs(c->temp.p, tmp2, L.key_in.p, L.key_out.p, L.val_in.p, L.val_out.p,
-                                             int(8 * C), 0, bits, s));
-    count_launch(c);
-  }
-  c->temp.ensure(std::max(tmp, tmp2));
-  WFK_CUDA(cub::DeviceScan::ExclusiveSum(c->temp.p, tmp, L.cnt.p, L.row_ptr.p, N + 1, s));
-  count_launch(c);
-  WFK_CUDA(cudaMemcpyAsync(c->h_pinned + 1, d_ne, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  sync_check(c);
-  L.E = c->h_pinned[1];
-  L.c_pos.ensure(8 * size_t(std::max<int64_t>(C, 1)));
-  if (C > 0) WFK_CUDA(cudaMemsetAsync(L.c_pos.p, 0xff, 8 * size_t(C) * sizeof(int32_t), s));
-  if (L.E > 0) {
-    L.ent_k.ensure(size_t(L.E));
-    k_entries<<<grid_for(L.E), kBlock, 0, s>>>(L.E, L.val_out, L.c_w, L.ent_con, L.ent_k, L.ent_w, L.c_pos);
-    count_launch(c);
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, L.key_in.p, L.key_out.p, L.val_in.p, L.val_out.p, int(E8), 0, bits,
+                                    s);
+    c->temp.ensure(tmp);
+    WFK_CUDA(cub::DeviceRadixSort::SortPairs(c->temp.p, tmp, L.key_in.p, L.key_out.p, L.val_in.p, L.val_out.p,
+                                             int(E8), 0, bits, s));
+    k_row_ptr_from_keys<<<grid_for(E8 + 1), kBlock, 0, s>>>(E8, L.key_out, N, L.row_ptr);
+    WFK_CUDA(cudaMemsetAsync(L.c_pos.p, 0xff, size_t(E8) * sizeof(int32_t), s));
+    k_entries<<<grid_for(E8), kBlock, 0, s>>>(L.row_ptr + N, L.val_out, L.c_w, L.ent_con, L.ent_k, L.ent_w,
+                                              L.c_pos);
+    count_launch(c, 3);
+  } else {
+    WFK_CUDA(cudaMemsetAsync(L.row_ptr.p, 0, size_t(N + 1) * sizeof(int32_t), s));
   }
   k_constraint_cache<<<grid_for(N), kBlock, 0, s>>>(N, L.row_ptr, L.ent_con, L.ent_w, L.c_kind, L.c_g, L.c_b,
                                                     L.crhs, L.cdiag);
-  if (L.E > int64_t(kCacheWarpRow) * 2)
+  count_launch(c);
+  if (E8 > int64_t(kCacheWarpRow) * 2) {
     k_constraint_cache_warp<<<std::min(grid_for(int64_t(N) * 32), c->num_sms * 16), kBlock, 0, s>>>(
         N, L.row_ptr, L.ent_con, L.ent_w, L.c_kind, L.c_g, L.c_b, L.crhs, L.cdiag);
-  count_launch(c, 2);
+    count_launch(c);
+  }
   // Rows carrying many constraint incidences (coarse levels, where every
   // constraint of the frame lands on a few thousand nodes) get their B^T B
   // assembled once per solve, so the PCG row pass is a fixed 27-block stencil.
-  L.assembled = L.E > int64_t(kAssembleRatio) * N;
+  L.assembled = E8 > int64_t(kAssembleRatio) * N;
   L.n_heavy = 0;
-  if (!L.assembled && L.E > 0) L.contrib.ensure(size_t(L.E));
   L.n_xitems = 0;
-  if (!L.assembled) {
-    L.xptr.ensure(size_t(N) + 1);
-    L.xrange.ensure(size_t(N) + 1);
-    int32_t* n_extra = L.cnt.p;  // per-row extra item counts (cnt is free after the row_ptr scan)
-    k_item_count<<<grid_for(N), kBlock, 0, s>>>(N, L.row_ptr, n_extra);
-    WFK_CUDA(cudaMemsetAsync(n_extra + N, 0, sizeof(int32_t), s));
-    size_t tmp4 = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tmp4, n_extra, L.xptr.p, N + 1, s);
-    c->temp.ensure(tmp4);
-    WFK_CUDA(cub::DeviceScan::ExclusiveSum(c->temp.p, tmp4, n_extra, L.xptr.p, N + 1, s));
-    WFK_CUDA(cudaMemcpyAsync(c->h_pinned + 5, L.xptr.p + N, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    sync_check(c);
-    L.n_xitems = c->h_pinned[5];
-    L.xitems.ensure(size_t(L.n_xitems) + 1);
-    L.wpart.ensure(size_t(N) + size_t(L.n_xitems) + 1);
-    k_item_write<<<grid_for(N), kBlock, 0, s>>>(N, L.row_ptr, L.xptr, L.xitems, L.xrange);
-    count_launch(c, 3);
-  }
+  if (!L.assembled) L.contrib.ensure(size_t(std::max<int64_t>(E8, 1)));
   if (L.assembled) {
     const int soa = N >= kAsmThreadRows ? 1 : 0;  // rows on lanes read slot-major blocks
     L.blk.ensure(size_t(N) * 27 * 6);
     L.cols.ensure(size_t(N) * 27);
-    if (L.E <= int64_t(kCacheWarpRow) * N)
-      k_assemble_btb_thread<<<grid_for(int64_t(N) * 27), kBlock, 0, s>>>(L.g, N, L.rows, L.node_row, L.row_ptr,
-                                                                        L.ent_con, L.ent_k, L.ent_w, L.c_w, L.c_g,
-                                                                        L.c_kind, L.blk, L.cols, soa);
-    else
-    k_assemble_btb<<<std::min(grid_for(int64_t(N) * 27 * 32), c->num_sms * 32), kBlock, 0, s>>>(L.g, N, L.rows, L.node_row, L.row_ptr, L.ent_con,
-                                                                 L.ent_k, L.ent_w, L.c_w, L.c_g, L.c_kind, L.blk,
-                                                                 L.cols, soa);
+    k_assemble_btb_rowwarp<<<grid_for(int64_t(N) * 32, kAsmWarpBlock), kAsmWarpBlock, 0, s>>>(
+        L.g, N, L.rows, L.node_row, L.row_ptr, L.ent_con, L.ent_k, L.ent_w, L.c_w, L.c_g, L.c_kind, L.blk, L.cols,
+        soa);
     count_launch(c);
   }
   WFK_CUDA(cudaGetLastError());
+}
+
+// Work items of the balanced matrix-free item pass (Chronopoulos-Gear PCG
+// only; built on first use per prepared level).
+static void level_items(wfk_ctx* c, Level& L) {
+  if (L.items_built || L.assembled || L.N == 0) return;
+  cudaStream_t s = c->stream;
+  const int N = L.N;
+  L.xptr.ensure(size_t(N) + 1);
+  L.xrange.ensure(size_t(N) + 1);
+  int32_t* n_extra = L.cnt.p;  // per-row extra item counts
+  k_item_count<<<grid_for(N), kBlock, 0, s>>>(N, L.row_ptr, n_extra);
+  WFK_CUDA(cudaMemsetAsync(n_extra + N, 0, sizeof(int32_t), s));
+  size_t tmp4 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp4, n_extra, L.xptr.p, N + 1, s);
+  c->temp.ensure(tmp4);
+  WFK_CUDA(cub::DeviceScan::ExclusiveSum(c->temp.p, tmp4, n_extra, L.xptr.p, N + 1, s));
+  WFK_CUDA(cudaMemcpyAsync(c->h_pinned + 5, L.xptr.p + N, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  sync_check(c);
+  L.n_xitems = c->h_pinned[5];
+  L.xitems.ensure(size_t(L.n_xitems) + 1);
+  L.wpart.ensure(size_t(N) + size_t(L.n_xitems) + 1);
+  k_item_write<<<grid_for(N), kBlock, 0, s>>>(N, L.row_ptr, L.xptr, L.xitems, L.xrange);
+  count_launch(c, 3);
+  L.items_built = true;
 }
 
 PoseD pose_dev(const wfk_pose* p) {
@@ -2222,6 +2326,13 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
       smem = 0;
     }
   }
+  if (a.pcg_variant == 1 && mode == 0) {
+    level_items(c, L);  // the Chronopoulos-Gear item pass needs its work items
+    a.xitems = L.xitems;
+    a.n_xitems = L.n_xitems;
+    a.xrange = L.xrange;
+    a.wpart = L.wpart;
+  }
   static bool smem_attr = false;
   if (!smem_attr) {
     WFK_CUDA(cudaFuncSetAttribute(k_flip_flop, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPipeSmemMax)));
@@ -2238,6 +2349,13 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   WFK_CUDA(cudaMemcpyAsync(c->h_pinned + 8, status, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   WFK_CUDA(cudaMemcpyAsync(reinterpret_cast<double*>(c->h_pinned + 16), eout, 4 * sizeof(double),
                            cudaMemcpyDeviceToHost, s));
+  // the trace rides along with the status when it fits the pinned area
+  wfk_trace_entry* h_trace = reinterpret_cast<wfk_trace_entry*>(c->h_pinned + 256);
+  const size_t trace_cap = (4096 - 256 * sizeof(int32_t)) / sizeof(wfk_trace_entry);
+  const size_t n_trace_max = size_t(std::max(p.flip_flop_iters, 1));
+  const bool trace_inline = out && n_trace_max <= trace_cap;
+  if (trace_inline)
+    WFK_CUDA(cudaMemcpyAsync(h_trace, a.trace, n_trace_max * sizeof(wfk_trace_entry), cudaMemcpyDeviceToHost, s));
   sync_check(c);
   for (int i = 0; i < 4; ++i) st[i] = c->h_pinned[8 + i];
   for (int i = 0; i < 4; ++i) en[i] = reinterpret_cast<double*>(c->h_pinned + 16)[i];
@@ -2292,9 +2410,13 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   if (out && st[0] > 0) {
     const size_t k = out->size();
     out->resize(k + size_t(st[0]));
-    WFK_CUDA(cudaMemcpyAsync(out->data() + k, a.trace, size_t(st[0]) * sizeof(wfk_trace_entry),
-                             cudaMemcpyDeviceToHost, s));
-    sync_check(c);
+    if (trace_inline) {
+      std::copy(h_trace, h_trace + st[0], out->data() + k);
+    } else {
+      WFK_CUDA(cudaMemcpyAsync(out->data() + k, a.trace, size_t(st[0]) * sizeof(wfk_trace_entry),
+                               cudaMemcpyDeviceToHost, s));
+      sync_check(c);
+    }
   }
 }
 
@@ -2353,11 +2475,26 @@ static void build_hierarchy(wfk_ctx* c, int levels) {
     Cl.c_w.ensure(8 * Cc);
     if (Cl.C > 0)
       k_reanchor<<<grid_for(Cl.C), kBlock, 0, s>>>(Cl.C, cg_, c->cons.canonical, Cl.c_node, Cl.c_w, Cl.active, err);
-    count_launch(c, 3);
+    // did the activity mask change since the level's rows were built?
+    const bool same_grid = Cl.prev_n == n && Cl.prev_dims[0] == cg_.nx && Cl.prev_dims[1] == cg_.ny &&
+                           Cl.prev_dims[2] == cg_.nz;
+    Cl.prev_active.ensure(n);
+    if (!same_grid) WFK_CUDA(cudaMemsetAsync(Cl.prev_active.p, 0xff, n, s));
+    k_mask_update<<<grid_for(int64_t(n)), kBlock, 0, s>>>(int64_t(n), Cl.active, Cl.prev_active, err, 1 << (8 + l));
+    Cl.prev_n = n;
+    Cl.prev_dims[0] = cg_.nx;
+    Cl.prev_dims[1] = cg_.ny;
+    Cl.prev_dims[2] = cg_.nz;
+    count_launch(c, 4);
   }
   WFK_CUDA(cudaMemcpyAsync(c->h_pinned + 2, err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   sync_check(c);
   if (c->h_pinned[2] & 2) throw Error(WFK_E_OUT_OF_RANGE, "trilinear_anchors: point outside grid");
+  for (int l = 1; l < levels; ++l) {
+    Level& Cl = c->lv[l];
+    Cl.mask_same = !(c->h_pinned[2] & (1 << (8 + l)));
+    if (!Cl.mask_same) Cl.rows_valid = false;  // rows were built from an older mask
+  }
 }
 
 static void prolong(wfk_ctx* c, int l) {
@@ -2368,12 +2505,53 @@ static void prolong(wfk_ctx* c, int l) {
   count_launch(c);
 }
 
+// WFK_SETUP_TRACE=1: device-timeline breakdown of each coarse-to-fine solve
+// (events between the host steps; gaps where the device waits for the host
+// are attributed to the step that follows them).
+struct SetupTrace {
+  bool on = false;
+  cudaStream_t s = nullptr;
+  std::vector<cudaEvent_t> ev;
+  std::vector<const char*> name;
+  void mark(const char* n) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    ev.push_back(e);
+    name.push_back(n);
+  }
+  void report() {
+    if (!on || ev.size() < 2) return;
+    cudaEventSynchronize(ev.back());
+    fprintf(stderr, "[wfk setup]");
+    for (size_t i = 1; i < ev.size(); ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+      fprintf(stderr, " %s %.3f", name[i], ms);
+    }
+    float tot = 0;
+    cudaEventElapsedTime(&tot, ev.front(), ev.back());
+    fprintf(stderr, " | total %.3f ms\n", tot);
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    ev.clear();
+    name.clear();
+  }
+};
+static SetupTrace* g_trace = nullptr;
+static void trace_mark(const char* n) {
+  if (g_trace) g_trace->mark(n);
+}
+
 void solve_level(wfk_ctx* c, int l, const PoseD& pose, const wfk_solver_params& p, int mode,
                  std::vector<wfk_trace_entry>* trace, wfk_energy* e) {
   Level& L = c->lv[l];
   level_rows(c, L);
+  trace_mark(l == 0 ? "L0rows" : l == 1 ? "L1rows" : "L2rows");
   level_constraints(c, L, pose, p);
+  trace_mark(l == 0 ? "L0cons" : l == 1 ? "L1cons" : "L2cons");
   run_level(c, L, pose, p, mode, l, trace, e);
+  trace_mark(l == 0 ? "L0ff" : l == 1 ? "L1ff" : "L2ff");
 }
 
 // --------------------------------------------------------------------------
@@ -2413,12 +2591,26 @@ void solver_c2f(wfk_ctx* c, const wfk_pose* pose, const wfk_solver_params& p, st
   require_volume(c);
   bind_level0(c);
   const PoseD pd = pose_dev(pose);
+  static const bool tracing = getenv("WFK_SETUP_TRACE") != nullptr;
+  SetupTrace tr;
+  if (tracing) {
+    tr.on = true;
+    tr.s = c->stream;
+    g_trace = &tr;
+    tr.mark("start");
+  }
   build_hierarchy(c, p.levels);
+  trace_mark("hier");
   for (int l = p.levels - 1; l >= 1; --l) {
     solve_level(c, l, pd, p, 0, &trace, nullptr);
     prolong(c, l);
+    trace_mark("prolong");
   }
   solve_level(c, 0, pd, p, 0, &trace, nullptr);
+  if (tracing) {
+    tr.report();
+    g_trace = nullptr;
+  }
 }
 
 void solver_hierarchy_info(wfk_ctx* c, int levels, int32_t* dims, int64_t* active) {

@@ -94,6 +94,11 @@ struct Level {
   // rows
   int N = 0;
   uint64_t rows_gen = 0;  // level 0: volume active_gen the row structures were built for
+  bool rows_valid = false;   // row structures built (coarse levels: for prev_active)
+  bool mask_same = false;    // coarse levels: build_hierarchy found the activity mask unchanged
+  DevBuf<uint8_t> prev_active;  // coarse levels: mask the rows were last built from
+  size_t prev_n = 0;
+  int prev_dims[3] = {0, 0, 0};
   DevBuf<int32_t> rows, node_row, nbr, uf;  // nbr: 6 x Ncap SoA
   DevBuf<uint8_t> frozen, comp_flag;
   // per-row state (AoS double3 / row-major 3x3)
@@ -115,6 +120,7 @@ struct Level {
   DevBuf<int2> xrange;
   DevBuf<double4> wpart;
   int n_xitems = 0;
+  bool items_built = false;
   // level constraints
   int64_t C = 0;
   DevBuf<int32_t> c_node;   // 8C anchors at this level
