@@ -118,41 +118,38 @@ __global__ void k_con_prepare(int64_t C, const int32_t* kind, const double* targ
                               const int32_t* node_row, const int32_t* uf, PoseD pose, double w_d, double w_s,
                               int N, int32_t* c_row, double* c_g, double* c_b, int32_t* c_kind,
                               uint8_t* comp_flag, int32_t* key, int32_t* val) {
-  const M3 rt = transpose(pose.r);
-  for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < C; c += int64_t(gridDim.x) * blockDim.x) {
-    const bool dense = kind[c] == WFK_DENSE_PLANE;
-    c_kind[c] = kind[c];
-    const V3 n = ld3(normal, c), f = ld3(target, c);
-    if (dense) {
-      const V3 g = mul(rt, n);
-      c_g[4 * c] = g.x;
-      c_g[4 * c + 1] = g.y;
-      c_g[4 * c + 2] = g.z;
-      c_g[4 * c + 3] = w_d * conf[c];
-      c_b[c] = dot(n, pose.t - f);
-    } else {
-      const V3 v = mul(rt, f - pose.t);
-      c_g[4 * c] = v.x;
-      c_g[4 * c + 1] = v.y;
-      c_g[4 * c + 2] = v.z;
-      c_g[4 * c + 3] = w_s * conf[c];
-      c_b[c] = 0.0;
-    }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int row = node_row[c_node[8 * c + k]];
-      const double w = c_w[8 * c + k];
-      c_row[8 * c + k] = row;
-      if (row >= 0 && w > 0) comp_flag[uf[row]] = 1;
-      // incidence entry unless alpha_i == 0 (solver.cpp:202)
-      if (row >= 0 && w != 0) {
-        key[8 * c + k] = row * 8 + (7 - k);  // cell order of solver.cpp:185-187
-        val[8 * c + k] = int32_t(8 * c + k);
+  // one thread per (constraint, corner); corner 0 also does the constraint's g
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < 8 * C; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t c = i >> 3;
+    const int k = int(i & 7);
+    if (k == 0) {
+      const M3 rt = transpose(pose.r);
+      const bool dense = kind[c] == WFK_DENSE_PLANE;
+      c_kind[c] = kind[c];
+      const V3 n = ld3(normal, c), f = ld3(target, c);
+      if (dense) {
+        const V3 gv = mul(rt, n);
+        c_g[4 * c] = gv.x;
+        c_g[4 * c + 1] = gv.y;
+        c_g[4 * c + 2] = gv.z;
+        c_g[4 * c + 3] = w_d * conf[c];
+        c_b[c] = dot(n, pose.t - f);
       } else {
-        key[8 * c + k] = N * 8;  // sentinel, sorts last
-        val[8 * c + k] = int32_t(8 * c + k);
+        const V3 v = mul(rt, f - pose.t);
+        c_g[4 * c] = v.x;
+        c_g[4 * c + 1] = v.y;
+        c_g[4 * c + 2] = v.z;
+        c_g[4 * c + 3] = w_s * conf[c];
+        c_b[c] = 0.0;
       }
     }
+    const int row = node_row[c_node[i]];
+    const double w = c_w[i];
+    c_row[i] = row;
+    if (row >= 0 && w > 0) comp_flag[uf[row]] = 1;
+    // incidence entry unless alpha_i == 0 (solver.cpp:202)
+    key[i] = (row >= 0 && w != 0) ? row * 8 + (7 - k) : N * 8;  // cell order of solver.cpp:185-187; sentinel last
+    val[i] = int32_t(i);
   }
 }
 
@@ -301,40 +298,44 @@ __global__ void k_assemble_btb_thread(Grid g, int N, const int32_t* rows, const 
   }
 }
 
-// Same blocks, one warp per row: lanes stage 32 incidences at a time in
-// shared memory (corner, coef * a_i, g, kind, the constraint's 8 weights),
-// then lane s < 27 accumulates its stencil slot over the staged incidences in
-// incidence order -- the reference's accumulation order (as the thread
-// variant), with the row's incidence data loaded once per warp instead of
-// once per slot.
-constexpr int kAsmWarpBlock = 256;
-__global__ void __launch_bounds__(kAsmWarpBlock) k_assemble_btb_rowwarp(
+// Assembled levels: B^T B (solver.cpp:196-226) and the ConstraintCache
+// (solver.hpp:66-70) of one row per block.  Warp w takes the row's incidence
+// chunks w, w + 8, ... (32 incidences each): its lanes stage a chunk in shared
+// memory (corner, coef a_i, a_i, g, c_b, kind, the constraint's 8 weights),
+// then lane s < 27 accumulates stencil slot s and lane 27 the cache terms over
+// the staged incidences in incidence order; the 8 warps' partials are summed
+// in warp order (deterministic).  The row's incidence data is read once.
+template <int W>
+__global__ void __launch_bounds__(W * 32) k_assemble_rows(
     Grid g, int N, const int32_t* rows, const int32_t* node_row, const int32_t* row_ptr, const int32_t* ent_con,
-    const uint8_t* ent_k, const double* ent_w, const double* c_w, const double* c_g, const int32_t* c_kind,
-    double* blk, int32_t* cols, int soa) {
+    const uint8_t* ent_k, const double* ent_w, const double* c_w, const double* c_g, const double* c_b,
+    const int32_t* c_kind, double* blk, int32_t* cols, int soa, double4* crhs, double4* cdiag) {
   struct Stage {
-    double sc[32], gx[32], gy[32], gz[32];
-    double w[8][33];  // padded: lane j writes w[k][j]
+    double sc[32], a[32], gx[32], gy[32], gz[32], cb[32];
+    double w[8][33];
     int k[32], dense[32];
   };
-  __shared__ Stage st_all[kAsmWarpBlock / 32];
-  Stage& st = st_all[threadIdx.x >> 5];
-  const int lane = threadIdx.x & 31;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
-  const int s = lane;  // stencil slot of this lane (lanes 27..31 only stage)
+  __shared__ Stage st_all[W];
+  __shared__ double part[W][28][6];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  Stage& st = st_all[warp];
+  const int s = lane;
   const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = s / 9 - 1;
-  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < N; r += warps) {
-    double b[6] = {0, 0, 0, 0, 0, 0};
+  for (int r = blockIdx.x; r < N; r += gridDim.x) {
+    double b[6] = {0, 0, 0, 0, 0, 0};  // slot block (s < 27) | rhs xyz, diag xyz (s == 27)
     const int e0 = row_ptr[r], e1 = row_ptr[r + 1];
-    for (int base = e0; base < e1; base += 32) {
+    for (int base = e0 + 32 * warp; base < e1; base += 32 * W) {
       const int e = base + lane;
       if (e < e1) {
         const int c = ent_con[e];
+        const double ai = ent_w[e];
         st.k[lane] = ent_k[e];
-        st.sc[lane] = c_g[4 * c + 3] * ent_w[e];
+        st.a[lane] = ai;
+        st.sc[lane] = c_g[4 * c + 3] * ai;
         st.gx[lane] = c_g[4 * c];
         st.gy[lane] = c_g[4 * c + 1];
         st.gz[lane] = c_g[4 * c + 2];
+        st.cb[lane] = c_b[c];
         st.dense[lane] = c_kind[c] == WFK_DENSE_PLANE;
 #pragma unroll
         for (int k = 0; k < 8; ++k) st.w[k][lane] = c_w[8 * int64_t(c) + k];
@@ -361,17 +362,53 @@ __global__ void __launch_bounds__(kAsmWarpBlock) k_assemble_btb_rowwarp(
             b[5] += sc * 1.0;
           }
         }
+      } else if (s == 27) {
+        // cache_term (solver.cpp:203-226): coef a^2 diag, rhs
+        for (int j = 0; j < cnt; ++j) {
+          const double coef_a = st.sc[j], sd = coef_a * st.a[j];
+          const double gx = st.gx[j], gy = st.gy[j], gz = st.gz[j];
+          if (st.dense[j]) {
+            b[3] += sd * (gx * gx);
+            b[4] += sd * (gy * gy);
+            b[5] += sd * (gz * gz);
+            const double f = coef_a * st.cb[j];
+            b[0] -= f * gx;
+            b[1] -= f * gy;
+            b[2] -= f * gz;
+          } else {
+            b[3] += sd * 1.0;
+            b[4] += sd * 1.0;
+            b[5] += sd * 1.0;
+            b[0] += coef_a * gx;
+            b[1] += coef_a * gy;
+            b[2] += coef_a * gz;
+          }
+        }
       }
       __syncwarp();
     }
-    if (s < 27) {
-      int x, y, z;
-      g.idx3(rows[r], x, y, z);
-      const int col = g.in_grid(x + dx, y + dy, z + dz) ? node_row[g.lin(x + dx, y + dy, z + dz)] : -1;
-      const int64_t ta = int64_t(r) * 27 + s;
-      cols[soa ? int64_t(s) * N + r : ta] = col;
-      for (int m = 0; m < 6; ++m) blk[soa ? (int64_t(s) * 6 + m) * N + r : ta * 6 + m] = b[m];
+    if (s < 28)
+#pragma unroll
+      for (int m = 0; m < 6; ++m) part[warp][s][m] = b[m];
+    __syncthreads();
+    if (warp == 0 && s < 28) {
+      double t[6] = {0, 0, 0, 0, 0, 0};
+      for (int w = 0; w < W; ++w)
+#pragma unroll
+        for (int m = 0; m < 6; ++m) t[m] += part[w][s][m];
+      if (s < 27) {
+        int x, y, z;
+        g.idx3(rows[r], x, y, z);
+        const int col = g.in_grid(x + dx, y + dy, z + dz) ? node_row[g.lin(x + dx, y + dy, z + dz)] : -1;
+        const int64_t ta = int64_t(r) * 27 + s;
+        cols[soa ? int64_t(s) * N + r : ta] = col;
+        for (int m = 0; m < 6; ++m) blk[soa ? (int64_t(s) * 6 + m) * N + r : ta * 6 + m] = t[m];
+      } else {
+        crhs[r] = make_double4(t[0], t[1], t[2], 0.0);
+        cdiag[r] = make_double4(t[3], t[4], t[5], 0.0);
+      }
     }
+    __syncthreads();
   }
 }
 
@@ -2102,7 +2139,7 @@ static void level_constraints(wfk_ctx* c, Level& L, const PoseD& pose, const wfk
   L.c_pos.ensure(8 * Cc);
   L.items_built = false;
   if (C > 0) {
-    k_con_prepare<<<grid_for(C), kBlock, 0, s>>>(C, c->cons.kind, c->cons.target, c->cons.normal, c->cons.conf,
+    k_con_prepare<<<grid_for(8 * C), kBlock, 0, s>>>(C, c->cons.kind, c->cons.target, c->cons.normal, c->cons.conf,
                                                  L.c_node, L.c_w, L.node_row, L.uf, pose, p.w_d, p.w_s, N, L.c_row,
                                                  L.c_g, L.c_b, L.c_kind, L.comp_flag, L.key_in, L.val_in);
     count_launch(c);
@@ -2133,28 +2170,42 @@ static void level_constraints(wfk_ctx* c, Level& L, const PoseD& pose, const wfk
   } else {
     WFK_CUDA(cudaMemsetAsync(L.row_ptr.p, 0, size_t(N + 1) * sizeof(int32_t), s));
   }
-  k_constraint_cache<<<grid_for(N), kBlock, 0, s>>>(N, L.row_ptr, L.ent_con, L.ent_w, L.c_kind, L.c_g, L.c_b,
-                                                    L.crhs, L.cdiag);
-  count_launch(c);
-  if (E8 > int64_t(kCacheWarpRow) * 2) {
-    k_constraint_cache_warp<<<std::min(grid_for(int64_t(N) * 32), c->num_sms * 16), kBlock, 0, s>>>(
-        N, L.row_ptr, L.ent_con, L.ent_w, L.c_kind, L.c_g, L.c_b, L.crhs, L.cdiag);
-    count_launch(c);
-  }
   // Rows carrying many constraint incidences (coarse levels, where every
   // constraint of the frame lands on a few thousand nodes) get their B^T B
-  // assembled once per solve, so the PCG row pass is a fixed 27-block stencil.
+  // assembled once per solve, so the PCG row pass is a fixed 27-block stencil;
+  // the same pass produces their constraint cache.
   L.assembled = E8 > int64_t(kAssembleRatio) * N;
   L.n_heavy = 0;
   L.n_xitems = 0;
-  if (!L.assembled) L.contrib.ensure(size_t(std::max<int64_t>(E8, 1)));
-  if (L.assembled) {
+  if (!L.assembled) {
+    L.contrib.ensure(size_t(std::max<int64_t>(E8, 1)));
+    k_constraint_cache<<<grid_for(N), kBlock, 0, s>>>(N, L.row_ptr, L.ent_con, L.ent_w, L.c_kind, L.c_g, L.c_b,
+                                                      L.crhs, L.cdiag);
+    count_launch(c);
+    if (E8 > int64_t(kCacheWarpRow) * 2) {
+      k_constraint_cache_warp<<<std::min(grid_for(int64_t(N) * 32), c->num_sms * 16), kBlock, 0, s>>>(
+          N, L.row_ptr, L.ent_con, L.ent_w, L.c_kind, L.c_g, L.c_b, L.crhs, L.cdiag);
+      count_launch(c);
+    }
+  } else {
     const int soa = N >= kAsmThreadRows ? 1 : 0;  // rows on lanes read slot-major blocks
     L.blk.ensure(size_t(N) * 27 * 6);
     L.cols.ensure(size_t(N) * 27);
-    k_assemble_btb_rowwarp<<<grid_for(int64_t(N) * 32, kAsmWarpBlock), kAsmWarpBlock, 0, s>>>(
-        L.g, N, L.rows, L.node_row, L.row_ptr, L.ent_con, L.ent_k, L.ent_w, L.c_w, L.c_g, L.c_kind, L.blk, L.cols,
-        soa);
+    // warps per row ~ incidence chunks per row (bound 8C / N)
+    const int64_t chunks = (E8 / std::max(N, 1) + 31) / 32;
+    auto launch = [&](auto kern, int W) {
+      kern<<<std::min(N, c->num_sms * (64 / W)), W * 32, 0, s>>>(L.g, N, L.rows, L.node_row, L.row_ptr, L.ent_con,
+                                                                 L.ent_k, L.ent_w, L.c_w, L.c_g, L.c_b, L.c_kind,
+                                                                 L.blk, L.cols, soa, L.crhs, L.cdiag);
+    };
+    if (chunks <= 1)
+      launch(k_assemble_rows<1>, 1);
+    else if (chunks <= 2)
+      launch(k_assemble_rows<2>, 2);
+    else if (chunks <= 4)
+      launch(k_assemble_rows<4>, 4);
+    else
+      launch(k_assemble_rows<8>, 8);
     count_launch(c);
   }
   WFK_CUDA(cudaGetLastError());
