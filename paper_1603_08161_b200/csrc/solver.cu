@@ -153,6 +153,14 @@ __global__ void k_con_prepare(int64_t C, const int32_t* kind, const double* targ
   }
 }
 
+// sort keys of the pipelined row order: incidences per row (clamped to 16 bits)
+__global__ void k_row_count_keys(int N, const int32_t* row_ptr, int32_t* key, int32_t* val) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x) {
+    key[r] = min(row_ptr[r + 1] - row_ptr[r], 65535);
+    val[r] = r;
+  }
+}
+
 // row_ptr from the sorted incidence keys (row * 8 + corner; sentinel N * 8):
 // position e starts every row in (row(e - 1), row(e)], position E8 closes the
 // rest, so row_ptr[N] = E (the sentinels sort last).
@@ -588,6 +596,7 @@ struct FFArgs {
   unsigned long long* sync_ll;  // split-reduction totals (flag-embedded words)
   int meta_rows, meta_cons;     // pipelined matrix-free levels: metadata cached in shared memory
   int asm_smem;                 // pipelined assembled levels: B^T B rows cached in shared memory
+  const int32_t* perm;          // pipelined matrix-free levels: row order (decreasing incidences), or null
   int pcg_variant;       // 0 pipelined (one reduction, overlapped), 1 Chronopoulos-Gear
   const double4 *crhs, *cdiag;
   double* rot;  // 9 per row
@@ -1246,6 +1255,13 @@ __device__ void pcg(const FFArgs& a, cg::grid_group& grid, Red& rs, int& iters, 
   }
 }
 
+// Round k of warp gw (of nw): rounds are dealt to the warps in order, or --
+// when the rows are sorted by decreasing incidence count -- in snake order
+// (0..nw-1, nw-1..0, ...), so every warp gets a heavy and a light share.
+__device__ __forceinline__ int mf_round(int k, int gw, int nw, bool snake) {
+  return k * nw + ((snake && (k & 1)) ? nw - 1 - gw : gw);
+}
+
 // Matrix-free row pass with kMfLanes lanes per row: the row's contiguous
 // incidence contributions and its six face neighbours are strided over the
 // lanes, a sub-warp shuffle tree sums them (fixed order), and the group
@@ -1259,40 +1275,44 @@ __device__ __forceinline__ void row_pass_mf(const FFArgs& a, const double4* v, S
   const int sub = lane % L, grp = lane / L;
   const double w2 = 2.0 * a.w_r;
   if (gwarp() < skip) return;
-  for (int base = (gwarp() - skip) * RPW; base < a.N; base += (nwarps() - skip) * RPW) {
-    const int r = base + grp;
-    const bool live = r < a.N;
-    int e0 = 0, e1 = 0, nb[6] = {-1, -1, -1, -1, -1, -1};
+  const int gw = gwarp() - skip, nw = nwarps() - skip;
+  for (int k = 0;; ++k) {
+    const int pos = mf_round(k, gw, nw, a.perm != nullptr) * RPW + grp;
+    if (pos - grp >= a.N) break;  // rounds only grow with k
+    const bool live = pos < a.N;
+    const int q = int(threadIdx.x >> 5) * (sl ? sl->K : 0) * RPW + k * RPW + grp;  // row slot
+    int r = pos, e0 = 0, e1 = 0, nb[6] = {-1, -1, -1, -1, -1, -1};
     bool frozen = false;
     bool cached = false;
     if constexpr (!std::is_same<Meta, std::nullptr_t>::value) {
       if (mm && mm->rows) {
         cached = true;
         if (live) {
-          const int q = sl->of(r);
           const int4 m0 = mm->rm[q], m1 = mm->rn[q];
           e0 = m0.x;
           e1 = m0.y;
           frozen = m0.z != 0;
           nb[0] = m0.w; nb[1] = m1.x; nb[2] = m1.y; nb[3] = m1.z; nb[4] = m1.w;
           nb[5] = mm->rn5[q];
+          r = mm->rid[q];
         }
       }
     }
     if (!cached && live) {
+      if (a.perm) r = a.perm[pos];
       frozen = a.frozen[r];
       e0 = a.row_ptr[r];
       e1 = a.row_ptr[r + 1];
 #pragma unroll
-      for (int k = sub; k < 6; k += L) nb[k] = a.nbr[int64_t(k) * a.N + r];
+      for (int k2 = sub; k2 < 6; k2 += L) nb[k2] = a.nbr[int64_t(k2) * a.N + r];
     }
     const V3 vr = live ? ld4(v, r) : V3{0, 0, 0};
     V3 acc{0, 0, 0};
     if (live && !frozen) {
       for (int e = e0 + sub; e < e1; e += L) acc += ld4(a.contrib, e);
 #pragma unroll
-      for (int k = sub; k < 6; k += L) {
-        const int j = nb[k];
+      for (int k2 = sub; k2 < 6; k2 += L) {
+        const int j = nb[k2];
         if (j >= 0) acc += w2 * (vr - ld4(v, j));
       }
     }
@@ -1302,7 +1322,7 @@ __device__ __forceinline__ void row_pass_mf(const FFArgs& a, const double4* v, S
       acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
       acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
     }
-    if (live && sub == 0) sink(r, vr, frozen ? vr : acc);
+    if (live && sub == 0) sink(r, q, vr, frozen ? vr : acc);
   }
 }
 
@@ -1404,16 +1424,17 @@ __device__ void split_wait(const FFArgs& a, unsigned seq, double (&v)[kSplitNV])
 // takes row l % RPW of round l / RPW, 32 / RPW rounds per step.  The matvec
 // results were stored by lanes of the same warp, so a __syncwarp orders them.
 template <int L, class F>
-__device__ __forceinline__ void for_warp_rows(int N, int skip, F f) {
+__device__ __forceinline__ void for_warp_rows(int N, int skip, int K, const int32_t* perm, const int* rid, F f) {
   constexpr int RPW = 32 / L, RPS = 32 / RPW;
   if (gwarp() < skip) return;
   __syncwarp();
   const int lane = threadIdx.x & 31;
   const int gw = gwarp() - skip, nw = nwarps() - skip;
   for (int k = lane / RPW;; k += RPS) {
-    const int r = (gw + k * nw) * RPW + lane % RPW;
-    if (r >= N) break;  // rows grow with k
-    f(r);
+    const int pos = mf_round(k, gw, nw, perm != nullptr) * RPW + lane % RPW;
+    if (pos >= N) break;  // positions grow with k
+    const int q = int(threadIdx.x >> 5) * K * RPW + k * RPW + lane % RPW;
+    f(rid ? rid[q] : perm ? perm[pos] : pos, q);
   }
 }
 
@@ -1458,7 +1479,7 @@ __host__ __device__ inline PipeLayout pipe_layout(int N, int64_t C, int rpw, int
   l.SC = tpb * l.KC;
   size_t off = size_t(kSlotVecs) * l.S * sizeof(double4);
   l.rmeta = off;
-  if (rows) off += size_t(l.S) * (2 * sizeof(int4) + sizeof(int));
+  if (rows) off += size_t(l.S) * (2 * sizeof(int4) + 2 * sizeof(int));
   off = (off + 31) / 32 * 32;
   l.cmeta = off;
   if (cons) off += size_t(l.SC) * (4 * sizeof(int4) + 3 * sizeof(double4) + sizeof(int));
@@ -1473,6 +1494,7 @@ struct MfMeta {
   const int4* rm;   // S: e0, e1, frozen, nbr0
   const int4* rn;   // S: nbr1..nbr4
   const int* rn5;   // S: nbr5
+  const int* rid;   // S: row id of the slot
   const int4* crow; // 2 SC
   const int4* cpos; // 2 SC
   const double4* cw;  // 2 SC
@@ -1488,6 +1510,7 @@ __device__ inline MfMeta mf_meta(char* base, const PipeLayout& l, bool rows, boo
   m.rm = reinterpret_cast<const int4*>(r);
   m.rn = reinterpret_cast<const int4*>(r + size_t(l.S) * sizeof(int4));
   m.rn5 = reinterpret_cast<const int*>(r + size_t(l.S) * 2 * sizeof(int4));
+  m.rid = reinterpret_cast<const int*>(r + size_t(l.S) * (2 * sizeof(int4) + sizeof(int)));
   char* c = base + l.cmeta;
   const size_t SC = size_t(l.SC);
   m.cw = reinterpret_cast<const double4*>(c);
@@ -1553,29 +1576,32 @@ __device__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, double& relres) {
     }
     __syncwarp();
   }
-  auto matvec = [&](const double4* v, auto& sink) {
+  // sinks receive (row, slot, v_r, (A v)_r)
+  auto matvec = [&](const double4* v, auto& sink4) {
     if (ASM) {
+      auto sink3 = [&](int r, V3 vr, V3 av) { sink4(r, sl.of(r), vr, av); };
       if (amat)
-        row_pass<true>(a, v, sink, kSkip, &sl, smb, smc);
+        row_pass<true>(a, v, sink3, kSkip, &sl, smb, smc);
       else
-        row_pass<true>(a, v, sink, kSkip);
+        row_pass<true>(a, v, sink3, kSkip);
     } else {
       matvec_constraints(a, v, kSkip, mmp);
       grid_barrier(a, rs);
-      row_pass_mf(a, v, sink, kSkip, mmp, &sl);
+      row_pass_mf(a, v, sink4, kSkip, mmp, &sl);
     }
   };
-  auto each_row = [&](auto f) {
+  const int* rid_sm = (!ASM && mm.rows) ? mm.rid : nullptr;
+  auto each_row = [&](auto f) {  // f(row, slot)
     if (rows_on_lanes)
-      for_warp_rows<1>(a.N, kSkip, f);
+      for_warp_rows<1>(a.N, kSkip, sl.K, nullptr, nullptr, f);
     else
-      for_warp_rows<LM>(a.N, kSkip, f);
+      for_warp_rows<LM>(a.N, kSkip, sl.K, ASM ? nullptr : a.perm, rid_sm, f);
   };
   if (!ASM && (mm.rows || mm.cons)) {
     // the solve's fixed row / constraint metadata into shared memory
     if (mm.rows)
-      each_row([&](int r) {
-        const int q = sl.of(r);
+      for_warp_rows<LM>(a.N, kSkip, sl.K, a.perm, nullptr, [&](int r, int q) {
+        const_cast<int*>(mm.rid)[q] = r;
         int nb[6];
 #pragma unroll
         for (int k = 0; k < 6; ++k) nb[k] = a.nbr[int64_t(k) * a.N + r];
@@ -1603,12 +1629,11 @@ __device__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, double& relres) {
   }
   // r0 = b - A x0, u0 = D^-1 r0 (solver.cpp:305-310)
   double acc_rr = 0, acc_bb = 0;
-  auto init_sink = [&](int r, V3 xr, V3 ax) {
+  auto init_sink = [&](int r, int q, V3 xr, V3 ax) {
     const V3 b = ld4(a.rhs, r);
     const V3 rr = b - ax;
     const double4 d4 = ld4w(a.dinv, r);
     st4(a.u, r, cmul(V3{d4.x, d4.y, d4.z}, rr));
-    const int q = sl.of(r);
     const double4 zero = make_double4(0, 0, 0, 0);
     sl.at(kSx, q) = make_double4(xr.x, xr.y, xr.z, 0.0);
     sl.at(kSr, q) = make_double4(rr.x, rr.y, rr.z, 0.0);
@@ -1623,8 +1648,7 @@ __device__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, double& relres) {
   grid_barrier(a, rs);
   // w0 = A u0, m0 = D w0
   double v4[4] = {0, 0, 0, 0};
-  auto w_sink = [&](int r, V3 ur, V3 wr) {
-    const int q = sl.of(r);
+  auto w_sink = [&](int r, int q, V3 ur, V3 wr) {
     const double4 d4 = sl.at(kSd, q), r4 = sl.at(kSr, q);
     sl.at(kSw, q) = make_double4(wr.x, wr.y, wr.z, 0.0);
     st4(a.m0, r, cmul(V3{d4.x, d4.y, d4.z}, wr));
@@ -1654,7 +1678,7 @@ __device__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, double& relres) {
     double4* mnext = (it & 1) ? a.m0 : a.m1;
     // n = A m for own rows (into the leader's slot), overlapped with the
     // totals of the previous update
-    auto n_sink = [&](int r, V3, V3 n) { sl.at(kSn, sl.of(r)) = make_double4(n.x, n.y, n.z, 0.0); };
+    auto n_sink = [&](int, int q, V3, V3 n) { sl.at(kSn, q) = make_double4(n.x, n.y, n.z, 0.0); };
     if (ASM) {
       if (comm && pending) split_total(a, seq - 1);
       matvec(mcur, n_sink);
@@ -1684,8 +1708,7 @@ __device__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, double& relres) {
     if (pap <= 0) break;  // solver.cpp:327
     const double alpha = gamma / pap;
     double v3[3] = {0, 0, 0};
-    auto upd = [&](int r) {
-      const int q = sl.of(r);
+    auto upd = [&](int r, int q) {
       const double4 n4 = sl.at(kSn, q), w4 = sl.at(kSw, q), s4 = sl.at(kSs, q), z4 = sl.at(kSz, q),
                     p4 = sl.at(kSp, q), x4 = sl.at(kSx, q), r4 = sl.at(kSr, q), d4 = sl.at(kSd, q);
       const V3 d{d4.x, d4.y, d4.z};
@@ -1728,7 +1751,7 @@ __device__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, double& relres) {
     relres = r_norm / b_norm;
   }
   // the solution back to global memory for the write-back phase
-  each_row([&](int r) { st4w(a.x, r, sl.at(kSx, sl.of(r))); });
+  each_row([&](int r, int q) { st4w(a.x, r, sl.at(kSx, q)); });
   grid_barrier(a, rs);
 }
 
@@ -2179,6 +2202,18 @@ static void level_constraints(wfk_ctx* c, Level& L, const PoseD& pose, const wfk
   L.n_xitems = 0;
   if (!L.assembled) {
     L.contrib.ensure(size_t(std::max<int64_t>(E8, 1)));
+    // row order of the pipelined row pass: decreasing incidence count (stable)
+    L.perm.ensure(size_t(N));
+    L.perm_key.ensure(2 * size_t(N));
+    L.perm_val.ensure(size_t(N));
+    k_row_count_keys<<<grid_for(N), kBlock, 0, s>>>(N, L.row_ptr, L.perm_key.p, L.perm_val.p);
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, L.perm_key.p, L.perm_key.p + N, L.perm_val.p, L.perm.p,
+                                              N, 0, 16, s);
+    c->temp.ensure(tmp);
+    WFK_CUDA(cub::DeviceRadixSort::SortPairsDescending(c->temp.p, tmp, L.perm_key.p, L.perm_key.p + N,
+                                                       L.perm_val.p, L.perm.p, N, 0, 16, s));
+    count_launch(c, 2);
     k_constraint_cache<<<grid_for(N), kBlock, 0, s>>>(N, L.row_ptr, L.ent_con, L.ent_w, L.c_kind, L.c_g, L.c_b,
                                                       L.crhs, L.cdiag);
     count_launch(c);
@@ -2377,6 +2412,8 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
       smem = 0;
     }
   }
+  static const bool no_perm = getenv("WFK_NO_PERM") != nullptr;
+  a.perm = (a.pcg_variant == 0 && !L.assembled && L.N > 0 && !no_perm) ? L.perm.p : nullptr;
   if (a.pcg_variant == 1 && mode == 0) {
     level_items(c, L);  // the Chronopoulos-Gear item pass needs its work items
     a.xitems = L.xitems;
