@@ -2463,7 +2463,11 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
         mx = std::max(mx, v);
       }
     };
-    const char* names[8] = {"A", "Async", "B", "red-", "U", "Usync", "redblk", "redsync"};
+    // pipelined PCG: A constraint pass, Abar its barrier, B row pass, U update,
+    // wait = totals poll (incl. intra-block skew), bar = partials + grid barrier
+    const char* names_cg[8] = {"A", "Async", "B", "red-", "U", "Usync", "redblk", "redsync"};
+    const char* names_pipe[8] = {"A", "Abar", "B", "-", "U", "-", "wait", "bar"};
+    const char* const* names = a.pcg_variant == 0 ? names_pipe : names_cg;
     fprintf(stderr, "[wfk phase] level %d N %d C %lld asm %d heavy %d iters %.0f | cycles/iter mean/max:", level_tag,
             L.N, (long long)L.C, int(L.assembled), L.n_heavy, it);
     for (int k = 0; k < 8; ++k) {
@@ -2489,10 +2493,19 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
     const double iters = st[0], pcg = st[2];
     pf.ff_bytes += pcg * (160 * N + 32 * Cd + 20 * Cs) + iters * (52 * N + 28 * N + 28 * N + 44 * (Cd + Cs)) +
                    (28 * N + 44 * (Cd + Cs));
-    // the same traffic for this fp64 layout:
-    // 4-phase PCG 365 N + 276 C per iteration; rhs/diag 153 N, write-back 48 N,
-    // rotation fit 201 N, energy 177 N + 232 C per flip-flop iteration.
-    pf.ff_bytes_impl += pcg * (365 * N + 276 * (Cd + Cs)) + iters * ((153 + 48 + 201 + 177) * N + 232 * (Cd + Cs)) +
+    // the global-memory traffic of this fp64 implementation:
+    // pipelined PCG iteration, state in shared memory -- matrix-free 256 N + 768 C
+    // (m gathers at 8 anchors + 8 contribution writes per constraint, contribution
+    // reads, m_r + 6 neighbour gathers + m write per row), assembled 896 N (27 m
+    // gathers + m write per row; + 1404 N when B^T B is not shared-memory resident);
+    // Chronopoulos-Gear 365 N + 276 C.  Per flip-flop iteration rhs/diag 153 N,
+    // write-back 48 N, rotation fit 201 N, energy 177 N + 232 C.
+    double per_it;
+    if (a.pcg_variant == 0)
+      per_it = L.assembled ? (896 + (a.asm_smem ? 0 : 1404)) * N : 256 * N + 768 * (Cd + Cs);
+    else
+      per_it = 365 * N + 276 * (Cd + Cs);
+    pf.ff_bytes_impl += pcg * per_it + iters * ((153 + 48 + 201 + 177) * N + 232 * (Cd + Cs)) +
                         (177 * N + 232 * (Cd + Cs));
   }
   if (out && st[0] > 0) {
