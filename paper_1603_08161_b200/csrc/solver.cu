@@ -650,8 +650,8 @@ struct PhaseClock {
   unsigned long long* sink;
   unsigned long long acc[16];
   long long t;
-  __device__ explicit PhaseClock(unsigned long long* s)
-      : sink((threadIdx.x == 0 && s) ? s + 16 * blockIdx.x : nullptr), t(sm_cycles()) {
+  __device__ explicit PhaseClock(unsigned long long* s, unsigned owner = 0)
+      : sink((threadIdx.x == owner && s) ? s + 16 * blockIdx.x : nullptr), t(sm_cycles()) {
     for (int k = 0; k < 16; ++k) acc[k] = 0;
   }
   __device__ void lap(int k) {
@@ -1786,6 +1786,10 @@ __device__ void rotations(const FFArgs& a) {
   }
 }
 
+// One instantiation per (PCG variant, level kind): each carries only the PCG
+// code it runs, so the register allocation of one variant does not spill
+// another's hot loops.
+template <int V, bool ASM>
 __global__ void __launch_bounds__(kCoopBlock, 1) k_flip_flop(FFArgs a) {
   cg::grid_group grid = cg::this_grid();
   Red rs;
@@ -1825,17 +1829,10 @@ __global__ void __launch_bounds__(kCoopBlock, 1) k_flip_flop(FFArgs a) {
       pc.lap(8);
       int iters;
       double relres;
-      if (a.pcg_variant == 1) {
-        if (a.assembled)
-          pcg<true>(a, grid, rs, iters, relres);
-        else
-          pcg<false>(a, grid, rs, iters, relres);
-      } else {
-        if (a.assembled)
-          pcg_pipe<true>(a, rs, iters, relres);
-        else
-          pcg_pipe<false>(a, rs, iters, relres);
-      }
+      if (V == 1)
+        pcg<ASM>(a, grid, rs, iters, relres);
+      else
+        pcg_pipe<ASM>(a, rs, iters, relres);
       total_pcg += iters;
       pc.lap(9);
       // write back non-frozen rows (solver.cpp:436-437)
@@ -2281,7 +2278,7 @@ PoseD pose_dev(const wfk_pose* p) {
 static int coop_blocks(wfk_ctx* c) {
   if (c->coop_blocks == 0) {
     int per_sm = 0;
-    WFK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_flip_flop, kCoopBlock, 0));
+    WFK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_flip_flop<0, false>, kCoopBlock, 0));
     int per_sm2 = 0;
     WFK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_pcg_assembled, kCoopBlock, 0));
     per_sm = std::min(per_sm, per_sm2);
@@ -2331,7 +2328,9 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   a.nbuf = L.nbuf.p;
   static const int pcg_variant = [] {
     const char* v = getenv("WFK_PCG");
-    return v && std::string(v) == "cg" ? 1 : 0;
+    if (v && std::string(v) == "cg") return 1;
+    if (v && std::string(v) == "pipe") return 0;
+    return 0;
   }();
   a.pcg_variant = pcg_variant;
   a.assembled = L.assembled ? 1 : 0;
@@ -2421,15 +2420,23 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
     a.xrange = L.xrange;
     a.wpart = L.wpart;
   }
+  void (*kern)(FFArgs) = nullptr;
+  const bool asm_k = L.assembled;
+  if (a.pcg_variant == 1)
+    kern = asm_k ? k_flip_flop<1, true> : k_flip_flop<1, false>;
+  else
+    kern = asm_k ? k_flip_flop<0, true> : k_flip_flop<0, false>;
   static bool smem_attr = false;
   if (!smem_attr) {
-    WFK_CUDA(cudaFuncSetAttribute(k_flip_flop, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPipeSmemMax)));
+    for (void (*k)(FFArgs) : {k_flip_flop<0, false>, k_flip_flop<0, true>, k_flip_flop<1, false>,
+                              k_flip_flop<1, true>})
+      WFK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPipeSmemMax)));
     smem_attr = true;
   }
   void* args[] = {&a};
   Prof& pf = c->prof;
   if (pf.on) WFK_CUDA(cudaEventRecord(pf.ev[0], s));
-  WFK_CUDA(cudaLaunchCooperativeKernel((void*)k_flip_flop, dim3(G), dim3(kCoopBlock), args, smem, s));
+  WFK_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(G), dim3(kCoopBlock), args, smem, s));
   if (pf.on) WFK_CUDA(cudaEventRecord(pf.ev[1], s));
   count_launch(c);
   int32_t st[4];
