@@ -1442,7 +1442,9 @@ __device__ __forceinline__ void for_warp_rows(int N, int skip, int K, const int3
 // from the row pass (L lanes per row: RPW rows per round, rounds nw warps
 // apart) are always the same, so their Krylov state lives in the block's
 // shared memory for the whole solve: slot (warp-in-block, round, row-in-round),
-// vector-major (SoA) so consecutive lanes hit consecutive 32-byte words.
+// stored component-major (vector, component, slot): consecutive lanes hit
+// consecutive 8-byte words, 24 bytes per 3-vector (WFK_SLOT_SOA=0 selects the
+// padded vector-major layout, 32 bytes per 3-vector).
 enum { kSx, kSr, kSw, kSp, kSs, kSz, kSd, kSn, kSlotVecs };
 struct Slots {
   double4* sm;  // kSlotVecs x S
@@ -1452,7 +1454,25 @@ struct Slots {
   __device__ __forceinline__ int of(int r) const {
     return int(threadIdx.x >> 5) * K * RPW + ((r / RPW - gw) / nw) * RPW + r % RPW;
   }
-  __device__ __forceinline__ double4& at(int v, int slot) const { return sm[v * S + slot]; }
+#ifndef WFK_SLOT_SOA
+#define WFK_SLOT_SOA 1
+#endif
+#if WFK_SLOT_SOA
+  // component-major: (vector, component, slot) -- 24 bytes per 3-vector
+  __device__ __forceinline__ double4 get(int v, int q) const {
+    const double* b = reinterpret_cast<const double*>(sm) + size_t(3 * v) * S + q;
+    return make_double4(b[0], b[S], b[2 * S], 0.0);
+  }
+  __device__ __forceinline__ void put(int v, int q, double4 x) const {
+    double* b = reinterpret_cast<double*>(sm) + size_t(3 * v) * S + q;
+    b[0] = x.x;
+    b[S] = x.y;
+    b[2 * S] = x.z;
+  }
+#else
+  __device__ __forceinline__ double4 get(int v, int q) const { return sm[v * S + q]; }
+  __device__ __forceinline__ void put(int v, int q, double4 x) const { sm[v * S + q] = x; }
+#endif
 };
 __host__ __device__ constexpr int pipe_rpw(bool asm_level, bool rows_on_lanes) {
   return rows_on_lanes ? 32 : 32 / (asm_level ? kAsmLanes : kMfLanes);
@@ -1477,7 +1497,7 @@ __host__ __device__ inline PipeLayout pipe_layout(int N, int64_t C, int rpw, int
   const int64_t nt = int64_t(G) * tpb - 32 * skip;
   l.KC = cons ? int((C + nt - 1) / nt) : 0;
   l.SC = tpb * l.KC;
-  size_t off = size_t(kSlotVecs) * l.S * sizeof(double4);
+  size_t off = size_t(kSlotVecs) * l.S * (WFK_SLOT_SOA ? 3 * sizeof(double) : sizeof(double4));
   l.rmeta = off;
   if (rows) off += size_t(l.S) * (2 * sizeof(int4) + 2 * sizeof(int));
   off = (off + 31) / 32 * 32;
@@ -1635,12 +1655,12 @@ __device__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, double& relres) {
     const double4 d4 = ld4w(a.dinv, r);
     st4(a.u, r, cmul(V3{d4.x, d4.y, d4.z}, rr));
     const double4 zero = make_double4(0, 0, 0, 0);
-    sl.at(kSx, q) = make_double4(xr.x, xr.y, xr.z, 0.0);
-    sl.at(kSr, q) = make_double4(rr.x, rr.y, rr.z, 0.0);
-    sl.at(kSp, q) = zero;
-    sl.at(kSs, q) = zero;
-    sl.at(kSz, q) = zero;
-    sl.at(kSd, q) = d4;
+    sl.put(kSx, q, make_double4(xr.x, xr.y, xr.z, 0.0));
+    sl.put(kSr, q, make_double4(rr.x, rr.y, rr.z, 0.0));
+    sl.put(kSp, q, zero);
+    sl.put(kSs, q, zero);
+    sl.put(kSz, q, zero);
+    sl.put(kSd, q, d4);
     acc_rr += dot(rr, rr);
     acc_bb += sqnorm(b);
   };
@@ -1649,8 +1669,8 @@ __device__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, double& relres) {
   // w0 = A u0, m0 = D w0
   double v4[4] = {0, 0, 0, 0};
   auto w_sink = [&](int r, int q, V3 ur, V3 wr) {
-    const double4 d4 = sl.at(kSd, q), r4 = sl.at(kSr, q);
-    sl.at(kSw, q) = make_double4(wr.x, wr.y, wr.z, 0.0);
+    const double4 d4 = sl.get(kSd, q), r4 = sl.get(kSr, q);
+    sl.put(kSw, q, make_double4(wr.x, wr.y, wr.z, 0.0));
     st4(a.m0, r, cmul(V3{d4.x, d4.y, d4.z}, wr));
     v4[0] += dot(V3{r4.x, r4.y, r4.z}, ur);
     v4[1] += dot(wr, ur);
@@ -1678,7 +1698,7 @@ __device__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, double& relres) {
     double4* mnext = (it & 1) ? a.m0 : a.m1;
     // n = A m for own rows (into the leader's slot), overlapped with the
     // totals of the previous update
-    auto n_sink = [&](int, int q, V3, V3 n) { sl.at(kSn, q) = make_double4(n.x, n.y, n.z, 0.0); };
+    auto n_sink = [&](int, int q, V3, V3 n) { sl.put(kSn, q, make_double4(n.x, n.y, n.z, 0.0)); };
     if (ASM) {
       if (comm && pending) split_total(a, seq - 1);
       matvec(mcur, n_sink);
@@ -1709,8 +1729,8 @@ __device__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, double& relres) {
     const double alpha = gamma / pap;
     double v3[3] = {0, 0, 0};
     auto upd = [&](int r, int q) {
-      const double4 n4 = sl.at(kSn, q), w4 = sl.at(kSw, q), s4 = sl.at(kSs, q), z4 = sl.at(kSz, q),
-                    p4 = sl.at(kSp, q), x4 = sl.at(kSx, q), r4 = sl.at(kSr, q), d4 = sl.at(kSd, q);
+      const double4 n4 = sl.get(kSn, q), w4 = sl.get(kSw, q), s4 = sl.get(kSs, q), z4 = sl.get(kSz, q),
+                    p4 = sl.get(kSp, q), x4 = sl.get(kSx, q), r4 = sl.get(kSr, q), d4 = sl.get(kSd, q);
       const V3 d{d4.x, d4.y, d4.z};
       const V3 w{w4.x, w4.y, w4.z};
       V3 rr{r4.x, r4.y, r4.z};
@@ -1721,12 +1741,12 @@ __device__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, double& relres) {
       rr = rr - alpha * sv;
       const V3 wn = w - alpha * z;
       const V3 u = cmul(d, rr);
-      sl.at(kSz, q) = make_double4(z.x, z.y, z.z, 0.0);
-      sl.at(kSs, q) = make_double4(sv.x, sv.y, sv.z, 0.0);
-      sl.at(kSp, q) = make_double4(p.x, p.y, p.z, 0.0);
-      sl.at(kSx, q) = make_double4(x.x, x.y, x.z, 0.0);
-      sl.at(kSr, q) = make_double4(rr.x, rr.y, rr.z, 0.0);
-      sl.at(kSw, q) = make_double4(wn.x, wn.y, wn.z, 0.0);
+      sl.put(kSz, q, make_double4(z.x, z.y, z.z, 0.0));
+      sl.put(kSs, q, make_double4(sv.x, sv.y, sv.z, 0.0));
+      sl.put(kSp, q, make_double4(p.x, p.y, p.z, 0.0));
+      sl.put(kSx, q, make_double4(x.x, x.y, x.z, 0.0));
+      sl.put(kSr, q, make_double4(rr.x, rr.y, rr.z, 0.0));
+      sl.put(kSw, q, make_double4(wn.x, wn.y, wn.z, 0.0));
       st4(mnext, r, cmul(d, wn));
       v3[0] += dot(rr, u);
       v3[1] += dot(wn, u);
@@ -1751,7 +1771,7 @@ __device__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, double& relres) {
     relres = r_norm / b_norm;
   }
   // the solution back to global memory for the write-back phase
-  each_row([&](int r, int q) { st4w(a.x, r, sl.at(kSx, q)); });
+  each_row([&](int r, int q) { st4w(a.x, r, sl.get(kSx, q)); });
   grid_barrier(a, rs);
 }
 
@@ -2398,7 +2418,8 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
     if (L.assembled && !a.asm_rows_on_lanes && !no_meta &&
         pipe_layout(L.N, L.C, rpw, G, kCoopBlock, kPipeSkip, false, false, true).total <= kPipeSmemMax)
       a.asm_smem = 1;
-    if (!L.assembled && !no_meta && bytes(true, true) <= kPipeSmemMax) {
+    static const bool cmeta = getenv("WFK_PIPE_CMETA") != nullptr;
+    if (!L.assembled && !no_meta && cmeta && bytes(true, true) <= kPipeSmemMax) {
       a.meta_rows = a.meta_cons = 1;
     } else if (!L.assembled && !no_meta && bytes(true, false) <= kPipeSmemMax) {
       a.meta_rows = 1;
@@ -2430,7 +2451,11 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   if (!smem_attr) {
     for (void (*k)(FFArgs) : {k_flip_flop<0, false>, k_flip_flop<0, true>, k_flip_flop<1, false>,
                               k_flip_flop<1, true>})
+    {
       WFK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPipeSmemMax)));
+      static const int carve = getenv("WFK_CARVEOUT") ? atoi(getenv("WFK_CARVEOUT")) : -1;
+      if (carve >= 0) WFK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+    }
     smem_attr = true;
   }
   void* args[] = {&a};
