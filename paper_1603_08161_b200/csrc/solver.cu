@@ -2415,7 +2415,8 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
     };
     static const bool no_meta = getenv("WFK_PIPE_NO_META") != nullptr;
     a.asm_smem = 0;
-    if (L.assembled && !a.asm_rows_on_lanes && !no_meta &&
+    static const bool no_asm_smem = getenv("WFK_NO_ASM_SMEM") != nullptr;
+    if (L.assembled && !a.asm_rows_on_lanes && !no_meta && !no_asm_smem &&
         pipe_layout(L.N, L.C, rpw, G, kCoopBlock, kPipeSkip, false, false, true).total <= kPipeSmemMax)
       a.asm_smem = 1;
     static const bool cmeta = getenv("WFK_PIPE_CMETA") != nullptr;
