@@ -148,14 +148,25 @@ int wfk_find_dense_correspondences(wfk_ctx* ctx, const wfk_intrinsics* intr,
 int wfk_constraints_append(wfk_ctx* ctx, const wfk_correspondence* c, int64_t n,
                            int32_t drop_inactive, int64_t* kept);
 
+/* ---- global pose ---------------------------------------------------------------
+ * estimate_global_pose (solver.cpp:536-614; replaces solver.hpp:144-147): dense
+ * projective point-to-plane ICP.  Sources are the valid samples of the context's
+ * geometry buffer (the last wfk_rasterize) re-warped through the context's
+ * volume; targets are looked up projectively in the context's frame maps (the
+ * last wfk_backproject_depth).  Runs on the device without host round trips
+ * (per iteration: one accumulation launch and one single-block update). */
+int wfk_estimate_global_pose(wfk_ctx* ctx, const wfk_intrinsics* intr, const wfk_pose* initial,
+                             const wfk_icp_params* params, wfk_icp_result* out);
+
 /* ---- per-frame hot path (Reconstructor::process_frame, pipeline.cpp:143-262,
- * without ICP and the feature front-end) --------------------------------------- */
+ * without the feature front-end; sparse constraints may be passed in) --------- */
 typedef struct wfk_pipeline_config {
   wfk_solver_params solver;
   wfk_correspond_params correspond;
   wfk_fusion_params fusion;
   int32_t reassociations;
-  int32_t reserved_;
+  int32_t estimate_pose;  /* global ICP before the solve (config.hpp:45, default on) */
+  wfk_icp_params icp;     /* its corr is replaced by `correspond` (pipeline.cpp:176) */
 } wfk_pipeline_config;
 
 typedef struct wfk_frame_record {
@@ -168,9 +179,15 @@ typedef struct wfk_frame_record {
   int32_t bootstrap;
   wfk_fusion_stats fusion;
   wfk_expansion_stats expansion;
+  wfk_pose pose;           /* the frame's global pose (after ICP) -- pass it to the next frame */
+  int32_t icp_degraded;    /* FrameRecord::icp_degraded */
+  int32_t icp_iterations;
+  double icp_rms;          /* FrameRecord::icp_rms */
 } wfk_frame_record;
 
-/* frame_index 0 bootstraps (pipeline.cpp:150-159).  sparse may be NULL. */
+/* frame_index 0 bootstraps (pipeline.cpp:150-159).  sparse may be NULL.  `pose`
+ * is the pose entering the frame (the Reconstructor's pose_); the frame's pose,
+ * refined by ICP when cfg->estimate_pose, is returned in rec->pose. */
 int wfk_process_frame(wfk_ctx* ctx, const wfk_frame_view* frame, const wfk_pose* pose,
                       const wfk_pipeline_config* cfg, const wfk_correspondence* sparse,
                       int64_t nsparse, int32_t frame_index, wfk_frame_record* rec);

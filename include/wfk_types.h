@@ -148,6 +148,25 @@ typedef struct wfk_correspond_params {
   double eps_d, eps_n, eps_v;
 } wfk_correspond_params;
 
+/* wf::IcpParams (solver.hpp:121-131) */
+typedef struct wfk_icp_params {
+  wfk_correspond_params corr;   /* the pipeline copies its CorrespondenceParams in (pipeline.cpp:176) */
+  int32_t max_iters;            /* 20 */
+  int32_t min_correspondences;  /* 6 */
+  double rel_tol;               /* 1e-6 */
+  double min_improvement;       /* 0 */
+} wfk_icp_params;
+
+/* wf::IcpResult (solver.hpp:133-139) */
+typedef struct wfk_icp_result {
+  wfk_pose pose;
+  int32_t converged;
+  int32_t degraded;  /* too few correspondences, pose unchanged */
+  double rms;
+  int32_t iterations;
+  int32_t reserved_;
+} wfk_icp_result;
+
 /* wf::Frame (image.hpp:31-35): depth in meters (0 = invalid), optional RGB. */
 typedef struct wfk_frame_view {
   wfk_intrinsics intrinsics;

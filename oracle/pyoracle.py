@@ -12,7 +12,7 @@ import numpy as np
 
 from paper_1603_08161_b200.abi import (
     CORR_DTYPE, CorrespondParams, Energy, ExpansionStats, FusionParams, FusionStats,
-    GeometryBufferView, Intrinsics, MeshView, PcgResult, PointNormalMapView, Pose,
+    GeometryBufferView, IcpParams, IcpResult, Intrinsics, MeshView, PcgResult, PointNormalMapView, Pose,
     SolverParams, TraceEntry, VolumeView, FrameView, Volume, ptr, trace_to_list,
     WFK_OK, WFK_E_CAPACITY, WFK_E_INVALID_ARG, WFK_E_OUT_OF_RANGE, WFK_E_LOGIC,
     EXEC_PARALLEL)
@@ -361,6 +361,27 @@ def find_dense_correspondences(buf, maps, intr, params, vol):
     return out[: n.value].copy()
 
 
+def estimate_global_pose(buf, maps, intr, vol, initial=None, params=None) -> IcpResult:
+    """estimate_global_pose (solver.cpp:536-614)."""
+    res = IcpResult()
+    bv, mv, vv = buf.view(), maps.view(), vol.view()
+    p = params or IcpParams.make()
+    ini = initial or Pose.make()
+    _check(lib().wfo_estimate_global_pose(C.byref(bv), C.byref(mv), C.byref(intr), C.byref(vv), C.byref(ini),
+                                          C.byref(p), C.byref(res)))
+    return res
+
+
+def ldlt_solve(a, b):
+    """Eigen LDLT (symmetric pivoting) restated: solve a x = b, a symmetric n x n, n <= 8."""
+    a = np.ascontiguousarray(a, np.float64)
+    b = np.ascontiguousarray(b, np.float64).reshape(-1)
+    n = b.shape[0]
+    x = np.zeros(n, np.float64)
+    _check(lib().wfo_ldlt_solve(C.c_int(n), ptr(a, C.c_double), ptr(b, C.c_double), ptr(x, C.c_double)))
+    return x
+
+
 def sparse_to_constraints(canonical, target, vol):
     canonical = np.ascontiguousarray(canonical, np.float64).reshape(-1, 3)
     target = np.ascontiguousarray(target, np.float64).reshape(-1, 3)
@@ -443,17 +464,21 @@ def synth_render(intr, center=(0.0, 0.0, 1.2), radius=0.3, pivot=(0.0, 0.0, 1.2)
 class ReconConfig(C.Structure):
     _fields_ = [("dims", C.c_int32 * 3), ("reassociations", C.c_int32), ("voxel_size", C.c_double),
                 ("origin", C.c_double * 3), ("solver", SolverParams), ("correspond", CorrespondParams),
-                ("fusion", FusionParams)]
+                ("fusion", FusionParams), ("estimate_pose", C.c_int32), ("reserved_", C.c_int32),
+                ("icp", IcpParams)]
 
 
 class FrameRecord(C.Structure):
     _fields_ = [("energy", Energy), ("dense_count", C.c_int32), ("sparse_count", C.c_int32),
                 ("anomalies", C.c_int32), ("trace_len", C.c_int32), ("pcg_iterations", C.c_int32),
-                ("reserved_", C.c_int32), ("fusion", FusionStats), ("expansion", ExpansionStats)]
+                ("reserved_", C.c_int32), ("fusion", FusionStats), ("expansion", ExpansionStats),
+                ("pose", Pose), ("icp_degraded", C.c_int32), ("icp_iterations", C.c_int32),
+                ("icp_rms", C.c_double)]
 
 
 class Reconstructor:
-    def __init__(self, dims, voxel, origin, solver=None, correspond=None, fusion=None, reassociations=3):
+    def __init__(self, dims, voxel, origin, solver=None, correspond=None, fusion=None, reassociations=3,
+                 estimate_pose=True, icp=None):
         cfg = ReconConfig()
         cfg.dims[:] = list(dims)
         cfg.voxel_size = voxel
@@ -462,6 +487,8 @@ class Reconstructor:
         cfg.solver = solver or SolverParams.make()
         cfg.correspond = correspond or CorrespondParams.make()
         cfg.fusion = fusion or FusionParams.make()
+        cfg.estimate_pose = 1 if estimate_pose else 0
+        cfg.icp = icp or IcpParams.make()
         self.cfg = cfg
         h = C.c_void_p()
         _check(lib().wfo_recon_create(C.byref(cfg), C.byref(h)))

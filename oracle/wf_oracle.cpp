@@ -1340,6 +1340,176 @@ std::vector<Con> find_dense(const GBuf& buf, const Maps& maps, const wfk_intrins
 }
 
 // ---------------------------------------------------------------------------
+// global pose: estimate_global_pose (solver.cpp:536-614)
+// ---------------------------------------------------------------------------
+// Eigen 3.4 LDLT<MatrixXd> (ldlt_inplace<Lower>::unblocked and _solve_impl),
+// restated: in-place on the lower triangle; at step k the remaining diagonal
+// entry of largest magnitude is moved to k by a symmetric transposition; the
+// k-th row of L is updated against the previous pivots, then column k below
+// the diagonal is divided by the pivot (skipped for a zero pivot).  Solve:
+// permute, unit-lower forward substitution, divide by D (pseudo-inverse: a
+// |D_i| not above the smallest normal double gives 0), unit-upper back
+// substitution with L^T, undo the permutation.
+struct Ldlt {
+  int n = 0;
+  double a[8][8];
+  int tr[8];
+};
+void ldlt_factor(Ldlt& f) {
+  const int n = f.n;
+  double temp[8];
+  for (int k = 0; k < n; ++k) {
+    int big = k;
+    for (int i = k + 1; i < n; ++i)
+      if (std::abs(f.a[i][i]) > std::abs(f.a[big][big])) big = i;
+    f.tr[k] = big;
+    if (big != k) {
+      for (int j = 0; j < k; ++j) std::swap(f.a[k][j], f.a[big][j]);
+      for (int i = big + 1; i < n; ++i) std::swap(f.a[i][k], f.a[i][big]);
+      std::swap(f.a[k][k], f.a[big][big]);
+      for (int i = k + 1; i < big; ++i) {
+        const double t = f.a[i][k];
+        f.a[i][k] = f.a[big][i];
+        f.a[big][i] = t;
+      }
+    }
+    if (k > 0) {
+      for (int j = 0; j < k; ++j) temp[j] = f.a[j][j] * f.a[k][j];
+      double d = 0;
+      for (int j = 0; j < k; ++j) d += f.a[k][j] * temp[j];
+      f.a[k][k] -= d;
+      for (int i = k + 1; i < n; ++i) {
+        double s = 0;
+        for (int j = 0; j < k; ++j) s += f.a[i][j] * temp[j];
+        f.a[i][k] -= s;
+      }
+    }
+    const double akk = f.a[k][k];
+    if (std::abs(akk) > 0)
+      for (int i = k + 1; i < n; ++i) f.a[i][k] /= akk;
+  }
+}
+void ldlt_solve(const Ldlt& f, const double* b, double* x) {
+  const int n = f.n;
+  for (int i = 0; i < n; ++i) x[i] = b[i];
+  for (int k = 0; k < n; ++k) std::swap(x[k], x[f.tr[k]]);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < i; ++j) x[i] -= f.a[i][j] * x[j];
+  for (int i = 0; i < n; ++i) {
+    const double d = f.a[i][i];
+    x[i] = std::abs(d) > std::numeric_limits<double>::min() ? x[i] / d : 0.0;
+  }
+  for (int i = n - 1; i >= 0; --i)
+    for (int j = i + 1; j < n; ++j) x[i] -= f.a[j][i] * x[j];
+  for (int k = n - 1; k >= 0; --k) std::swap(x[k], x[f.tr[k]]);
+}
+
+// orthonormalize (core.cpp:30-40): nearest rotation through the Jacobi SVD
+M3 orthonormalize(const M3& m) {
+  M3 u, v;
+  double sv[3];
+  svd3(m, u, sv, v);
+  M3 r = u * transpose(v);
+  if (det(r) < 0) {
+    M3 flip = M3::identity();
+    flip.a[2][2] = -1;
+    r = u * flip * transpose(v);
+  }
+  return r;
+}
+
+struct IcpOut {
+  Pose pose;
+  bool converged = false, degraded = false;
+  double rms = 0;
+  int iterations = 0;
+};
+IcpOut estimate_global_pose(const GBuf& buf, const Maps& maps, const wfk_intrinsics& K, const Vol& vol,
+                            const Pose& initial, const wfk_icp_params& params) {
+  IcpOut res;
+  res.pose = initial;
+  struct Source {
+    V3 q, n0;
+  };
+  std::vector<Source> sources;
+  const M3 r0t = transpose(initial.r);
+  for (int y = 0; y < buf.h; ++y)  // solver.cpp:549-558
+    for (int x = 0; x < buf.w; ++x) {
+      const size_t p = buf.idx(x, y);
+      if (!std::isfinite(buf.depth[p])) continue;
+      const V3 nrm = buf.get(buf.normal, p);
+      if (sqnorm(nrm) < 0.5) continue;
+      const V3 can = buf.get(buf.canonical, p);
+      if (!vol.contains(can)) continue;
+      sources.push_back({vol.interpolate_deformed(can), r0t * nrm});
+    }
+  double prev_rms = std::numeric_limits<double>::infinity();
+  Pose prev_pose = initial;
+  for (int it = 0; it < params.max_iters; ++it) {
+    double h[6][6] = {}, g[6] = {};
+    double err = 0, wsum = 0;
+    int count = 0;
+    for (const Source& s : sources) {  // solver.cpp:567-589
+      const V3 p = res.pose.apply(s.q);
+      const double ux = K.fx * p.x / p.z + K.cx;
+      const double uy = K.fy * p.y / p.z + K.cy;
+      V3 pa, na;
+      if (!sample_point_normal(maps, ux, uy, pa, na)) continue;
+      const V3 nc = res.pose.r * s.n0;
+      const V3 v = -normalized(p);
+      const double w = dense_confidence(norm(p - pa), dot(nc, na), dot(nc, v), params.corr);
+      if (w <= 0) continue;
+      const V3 c = cross(p, na);
+      const double j[6] = {c.x, c.y, c.z, na.x, na.y, na.z};
+      const double r = dot(na, p - pa);
+      for (int i = 0; i < 6; ++i) {
+        const double wj = w * j[i];
+        for (int k = 0; k < 6; ++k) h[i][k] += wj * j[k];
+        g[i] += wj * r;
+      }
+      err += w * r * r;
+      wsum += w;
+      ++count;
+    }
+    if (count < params.min_correspondences) {  // :590-593
+      res.degraded = true;
+      return res;
+    }
+    res.rms = std::sqrt(err / std::max(wsum, 1e-300));
+    res.iterations = it + 1;
+    if (res.rms > prev_rms * (1.0 - std::max(params.rel_tol, params.min_improvement))) {  // :599-604
+      res.pose = prev_pose;
+      res.rms = prev_rms;
+      res.converged = true;
+      break;
+    }
+    prev_rms = res.rms;
+    prev_pose = res.pose;
+    double dmax = h[0][0];
+    for (int i = 1; i < 6; ++i) dmax = std::max(dmax, h[i][i]);
+    const double damp = 1e-3 * dmax;  // :608
+    Ldlt f;
+    f.n = 6;
+    for (int i = 0; i < 6; ++i)
+      for (int k = 0; k < 6; ++k) f.a[i][k] = h[i][k] + (i == k ? damp : 0.0);
+    ldlt_factor(f);
+    double mg[6], delta[6];
+    for (int i = 0; i < 6; ++i) mg[i] = -g[i];
+    ldlt_solve(f, mg, delta);
+    M3 step = M3::identity();  // I + [omega]_x (:610-613)
+    step.a[0][1] += -delta[2];
+    step.a[0][2] += delta[1];
+    step.a[1][0] += delta[2];
+    step.a[1][2] += -delta[0];
+    step.a[2][0] += -delta[1];
+    step.a[2][1] += delta[0];
+    res.pose.r = orthonormalize(step * res.pose.r);
+    res.pose.t = step * res.pose.t + V3{delta[3], delta[4], delta[5]};
+  }
+  return res;
+}
+
+// ---------------------------------------------------------------------------
 // isosurface.cpp / rasterize.cpp
 // ---------------------------------------------------------------------------
 struct Mesh {
@@ -1893,6 +2063,37 @@ int wfo_find_dense_correspondences(const wfk_geometry_buffer* buf, const wfk_poi
   for (size_t i = 0; i < c.size(); ++i) con_to_c(c[i], out[i]);
   return WFK_OK;
 }
+void pose_to_c(const Pose& q, wfk_pose* o) {
+  for (int i = 0; i < 9; ++i) o->rotation[i] = q.r.a[i / 3][i % 3];
+  o->translation[0] = q.t.x;
+  o->translation[1] = q.t.y;
+  o->translation[2] = q.t.z;
+}
+int wfo_estimate_global_pose(const wfk_geometry_buffer* buf, const wfk_point_normal_map* maps,
+                             const wfk_intrinsics* intr, const wfk_volume_view* view, const wfk_pose* initial,
+                             const wfk_icp_params* params, wfk_icp_result* out) {
+  if (buf->width != maps->width || buf->height != maps->height)
+    return fail(WFK_E_INVALID_ARG, "estimate_global_pose: size mismatch");
+  const IcpOut r = estimate_global_pose(gbuf_of(buf), maps_of(maps), *intr, Vol::borrow(view), pose_of(initial),
+                                        *params);
+  std::memset(out, 0, sizeof(*out));
+  pose_to_c(r.pose, &out->pose);
+  out->converged = r.converged;
+  out->degraded = r.degraded;
+  out->rms = r.rms;
+  out->iterations = r.iterations;
+  return WFK_OK;
+}
+int wfo_ldlt_solve(int n, const double* a, const double* b, double* x) {
+  if (n < 1 || n > 8) return fail(WFK_E_INVALID_ARG, "ldlt: n out of range");
+  Ldlt f;
+  f.n = n;
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < n; ++k) f.a[i][k] = a[i * n + k];
+  ldlt_factor(f);
+  ldlt_solve(f, b, x);
+  return WFK_OK;
+}
 int wfo_sparse_to_constraints(const double* canonical, const double* target, int64_t n,
                               const wfk_volume_view* view, wfk_correspondence* out, int64_t* n_out) {
   const Vol v = Vol::borrow(view);  // correspond.cpp:152-169
@@ -2045,6 +2246,7 @@ int wfo_recon_process_frame(wfo_recon* r, const wfk_frame_view* frame, const wfk
     const FusionStats s = integrate_frame(vol, f, r->pose, boot, par);
     rec->fusion = {s.fused, s.gate, s.frustum, s.occluded};
     compute_active_set(vol);
+    pose_to_c(r->pose, &rec->pose);
     ++r->frames;
     return WFK_OK;
   }
@@ -2060,6 +2262,16 @@ int wfo_recon_process_frame(wfo_recon* r, const wfk_frame_view* frame, const wfk
     compute_normals(mesh);
     rasterize(mesh, frame->intrinsics, par, buf);
   };
+  if (cfg.estimate_pose) {  // pipeline.cpp:174-183
+    wfk_icp_params ip = cfg.icp;
+    ip.corr = cfg.correspond;
+    const IcpOut icp = estimate_global_pose(buf, maps, frame->intrinsics, vol, r->pose, ip);
+    rec->icp_degraded = icp.degraded;
+    rec->icp_rms = icp.rms;
+    rec->icp_iterations = icp.iterations;
+    r->pose = icp.pose;
+    redeform();
+  }
   const auto sparse_c = cons_of(sparse, nsparse);
   auto all_active = [&](const Con& c) {
     for (int a : c.idx)
@@ -2100,6 +2312,7 @@ int wfo_recon_process_frame(wfo_recon* r, const wfk_frame_view* frame, const wfk
   const FusionStats s = integrate_frame(vol, f, r->pose, cfg.fusion, par);  // :254
   rec->fusion = {s.fused, s.gate, s.frustum, s.occluded};
   rec->expansion = expand_grid(vol);  // :255
+  pose_to_c(r->pose, &rec->pose);
   ++r->frames;
   return WFK_OK;
 }

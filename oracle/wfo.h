@@ -90,6 +90,12 @@ int wfo_find_dense_correspondences(const wfk_geometry_buffer* buf,
                                    const wfk_correspond_params* params,
                                    const wfk_volume_view* v, wfk_correspondence* out,
                                    int64_t cap, int64_t* n_out);
+/* solver.cpp:536-614 */
+int wfo_estimate_global_pose(const wfk_geometry_buffer* buf, const wfk_point_normal_map* maps,
+                             const wfk_intrinsics* intr, const wfk_volume_view* v, const wfk_pose* initial,
+                             const wfk_icp_params* params, wfk_icp_result* out);
+/* Eigen LDLT<MatrixXd> (symmetric pivoting) restated, n <= 8: solves A x = b */
+int wfo_ldlt_solve(int n, const double* a, const double* b, double* x);
 int wfo_sparse_to_constraints(const double* canonical, const double* target, int64_t n,
                               const wfk_volume_view* v, wfk_correspondence* out,
                               int64_t* n_out);
@@ -117,6 +123,9 @@ typedef struct wfo_recon_config {
   wfk_solver_params solver;
   wfk_correspond_params correspond;
   wfk_fusion_params fusion;
+  int32_t estimate_pose;
+  int32_t reserved_;
+  wfk_icp_params icp;
 } wfo_recon_config;
 
 typedef struct wfo_frame_record {
@@ -129,6 +138,10 @@ typedef struct wfo_frame_record {
   int32_t reserved_;
   wfk_fusion_stats fusion;
   wfk_expansion_stats expansion;
+  wfk_pose pose;
+  int32_t icp_degraded;
+  int32_t icp_iterations;
+  double icp_rms;
 } wfo_frame_record;
 
 typedef struct wfo_recon wfo_recon;

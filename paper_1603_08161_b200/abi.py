@@ -144,6 +144,22 @@ class CorrespondParams(C.Structure):
         return CorrespondParams(eps_d, eps_n, eps_v)
 
 
+class IcpParams(C.Structure):
+    """wf::IcpParams (solver.hpp:121-131)."""
+    _fields_ = [("corr", CorrespondParams), ("max_iters", C.c_int32), ("min_correspondences", C.c_int32),
+                ("rel_tol", C.c_double), ("min_improvement", C.c_double)]
+
+    @staticmethod
+    def make(max_iters=20, rel_tol=1e-6, min_improvement=0.0, min_correspondences=6, corr=None) -> "IcpParams":
+        return IcpParams(corr or CorrespondParams.make(), max_iters, min_correspondences, rel_tol, min_improvement)
+
+
+class IcpResult(C.Structure):
+    """wf::IcpResult (solver.hpp:133-139)."""
+    _fields_ = [("pose", Pose), ("converged", C.c_int32), ("degraded", C.c_int32), ("rms", C.c_double),
+                ("iterations", C.c_int32), ("reserved_", C.c_int32)]
+
+
 class FrameView(C.Structure):
     _fields_ = [("intrinsics", Intrinsics), ("depth", _fp), ("color", _fp)]
 

@@ -147,7 +147,7 @@ int wfk_create(const wfk_config* cfg, wfk_ctx** out) {
     if (prop.major < 10) throw Error(WFK_E_CUDA, "libwfk is built for sm_100a (B200)");
     c->num_sms = prop.multiProcessorCount;
     WFK_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    WFK_CUDA(cudaMallocHost(&c->h_pinned, 4096));
+    WFK_CUDA(cudaMallocHost(&c->h_pinned, 8192));  // 4 KB readback area + 4 KB ICP state staging
     for (cudaEvent_t& e : c->prof.ev) WFK_CUDA(cudaEventCreate(&e));
     for (cudaEvent_t& e : c->prof.timer) WFK_CUDA(cudaEventCreate(&e));
   } catch (const Error& e) {
@@ -548,8 +548,18 @@ int wfk_process_staged_frame(wfk_ctx* c, int32_t slot, const wfk_pose* pose, con
 }  // extern "C"
 
 namespace {
-void run_frame(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose* pose, const wfk_pipeline_config* cfg,
+void run_frame(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose* pose_in, const wfk_pipeline_config* cfg,
                const wfk_correspondence* sparse, int64_t nsparse, int32_t frame_index, wfk_frame_record* rec) {
+    // the frame's pose (the Reconstructor's pose_), refined by ICP below
+    wfk_pose pose_local;
+    if (pose_in) {
+      pose_local = *pose_in;
+    } else {
+      std::memset(&pose_local, 0, sizeof(pose_local));
+      pose_local.rotation[0] = pose_local.rotation[4] = pose_local.rotation[8] = 1.0;
+    }
+    const wfk_pose* pose = &pose_local;
+    rec->pose = pose_local;
     Prof& pf = c->prof;
     double stage[kStages] = {0, 0, 0, 0, 0, 0};
     auto lap = [&](int k, int a, int b) {
@@ -585,6 +595,20 @@ void run_frame(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose* pose, const 
     if (nt == 0) throw Error(WFK_E_LOGIC, "empty isosurface before frame");
     timed("normals", [&] { assoc_compute_normals(c); });
     timed("raster", [&] { assoc_rasterize(c, K, nullptr); });
+    if (cfg->estimate_pose) {  // pipeline.cpp:174-183
+      wfk_icp_params ip = cfg->icp;
+      ip.corr = cfg->correspond;
+      wfk_icp_result icp;
+      timed("icp", [&] { assoc_estimate_pose(c, K, pose_local, ip, &icp); });
+      rec->icp_degraded = icp.degraded;
+      rec->icp_rms = icp.rms;
+      rec->icp_iterations = icp.iterations;
+      pose_local = icp.pose;
+      rec->pose = pose_local;
+      timed("warp0", [&] { assoc_mesh_warp(c, pose); });  // redeform (pipeline.cpp:167-172)
+      timed("normals0", [&] { assoc_compute_normals(c); });
+      timed("raster0", [&] { assoc_rasterize(c, K, nullptr); });
+    }
     stage_mark(c, 1);
     lap(0, 0, 1);
     std::vector<wfk_trace_entry> trace;
@@ -627,6 +651,14 @@ void run_frame(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose* pose, const 
 }  // namespace
 
 extern "C" {
+
+int wfk_estimate_global_pose(wfk_ctx* c, const wfk_intrinsics* intr, const wfk_pose* initial,
+                             const wfk_icp_params* params, wfk_icp_result* out) {
+  return guard(c, [&] {
+    if (!intr || !initial || !params || !out) throw Error(WFK_E_INVALID_ARG, "null argument");
+    assoc_estimate_pose(c, *intr, *initial, *params, out);
+  });
+}
 
 int wfk_synth_render(wfk_ctx* c, const wfk_synth_scene* s, const wfk_intrinsics* intr, float* depth, float* color) {
   return guard(c, [&] {

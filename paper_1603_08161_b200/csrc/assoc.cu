@@ -24,6 +24,7 @@
 #include "../../include/wfk_mc_cases.h"
 #include "wfk_context.cuh"
 #include "wfk_solver.cuh"
+#include "icp_math.cuh"
 
 namespace wfk {
 
@@ -886,6 +887,197 @@ void assoc_find_dense(wfk_ctx* c, const wfk_intrinsics& K, const wfk_correspond_
   WFK_CUDA(cudaStreamSynchronize(s));
   ci.count = n;
   if (n_out) *n_out = n;
+}
+
+// ---------------------------------------------------------------------------
+// estimate_global_pose (solver.cpp:536-614): dense projective point-to-plane ICP
+// ---------------------------------------------------------------------------
+// Sources (valid buffer samples, solver.cpp:549-558) are compacted in pixel
+// order; each iteration is one accumulation launch (per-block partial sums of
+// the 6x6 normal equations' lower triangle, g, error, weight and count) and
+// one single-warp update launch that sums the partials in fixed block order,
+// applies the reference's degraded / revert-and-converge rules, damps, solves
+// with the restated Eigen LDLT and updates the pose -- all on the device, so a
+// whole ICP costs no host round trip until the result is read.
+WF_D bool icp_source(const AssocArgs& a, int64_t i) {
+  if (!isfinite(a.depth[i])) return false;  // GeometryBuffer::valid
+  if (sqnorm(ld3(a.bnormal, i)) < 0.5) return false;
+  return a.g.contains(ld3(a.bcanon, i));
+}
+__global__ void k_icp_flag(AssocArgs a) {
+  const int64_t npx = int64_t(a.K.width) * a.K.height;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npx; i += int64_t(gridDim.x) * blockDim.x)
+    a.flag[i] = icp_source(a, i) ? 1 : 0;
+}
+// source k: q = interpolate_deformed(canonical) (volume.cpp:61-66), n0 = R0^T n
+__global__ void k_icp_write(AssocArgs a, const int32_t* pos, const double* deformed, M3 r0t, double* src) {
+  const int64_t npx = int64_t(a.K.width) * a.K.height;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npx; i += int64_t(gridDim.x) * blockDim.x) {
+    if (!a.flag[i]) continue;
+    const int64_t k = pos[i];
+    st3(src, 2 * k, a.g.interpolate(deformed, ld3(a.bcanon, i)));
+    st3(src, 2 * k + 1, mul(r0t, ld3(a.bnormal, i)));
+  }
+}
+
+__global__ void k_icp_accumulate(AssocArgs a, const double* src, const int32_t* n_src, const IcpDev* st,
+                                 double* partials) {
+  __shared__ double sm[kIcpVals][kBlock / 32];
+  if (st->done) return;
+  PoseD pose;
+  for (int i = 0; i < 9; ++i) pose.r.a[i / 3][i % 3] = st->R[i];
+  pose.t = V3{st->t[0], st->t[1], st->t[2]};
+  double acc[kIcpVals];
+#pragma unroll
+  for (int v = 0; v < kIcpVals; ++v) acc[v] = 0;
+  const int64_t S = *n_src;
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < S; k += int64_t(gridDim.x) * blockDim.x) {
+    const V3 p = pose.apply(ld3(src, 2 * k));  // solver.cpp:567-589
+    const double ux = a.K.fx * p.x / p.z + a.K.cx;
+    const double uy = a.K.fy * p.y / p.z + a.K.cy;
+    V3 pa, na;
+    if (!sample_pn(a, ux, uy, pa, na)) continue;
+    const V3 nc = mul(pose.r, ld3(src, 2 * k + 1));
+    const double zz = sqnorm(p);
+    const V3 v = -(zz > 0 ? p / sqrt(zz) : p);
+    const double kd = kernel_phi(norm3(p - pa), a.p.eps_d);
+    const double kn = kernel_phi(1.0 - dot(nc, na), a.p.eps_n);
+    const double kv = kernel_phi(1.0 - dot(nc, v), a.p.eps_v);
+    double w = 0.0;
+    if (!(kd < 0 || kn < 0 || kv < 0)) {
+      const double avg = (kd + kn + kv) / 3.0;
+      w = avg * avg;
+    }
+    if (w <= 0) continue;
+    const V3 c = cross(p, na);
+    const double j[6] = {c.x, c.y, c.z, na.x, na.y, na.z};
+    const double r = dot(na, p - pa);
+    int t = 0;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      const double wj = w * j[i];
+#pragma unroll
+      for (int q = 0; q <= i; ++q) acc[t++] += wj * j[q];  // H(i, q), lower triangle
+      acc[21 + i] += wj * r;
+    }
+    acc[27] += w * r * r;
+    acc[28] += w;
+    acc[29] += 1.0;
+  }
+  // fixed-order block sum: warp trees, then the warps in order
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int v = 0; v < kIcpVals; ++v) {
+    const double x = warp_sum(acc[v]);
+    if (lane == 0) sm[v][warp] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < kIcpVals) {
+    double t = 0;
+    for (int w2 = 0; w2 < int(blockDim.x >> 5); ++w2) t += sm[threadIdx.x][w2];
+    partials[size_t(blockIdx.x) * kIcpVals + threadIdx.x] = t;
+  }
+}
+
+__global__ void k_icp_update(const double* partials, int nblk, IcpDev* st, wfk_icp_params prm, double* tot_out) {
+  __shared__ double tot[kIcpVals];
+  const int lane = threadIdx.x;
+  if (lane < kIcpVals) {
+    double t = 0;
+    for (int b = 0; b < nblk; ++b) t += partials[size_t(b) * kIcpVals + lane];
+    tot[lane] = t;
+    if (tot_out) tot_out[lane] = t;
+  }
+  __syncwarp();
+  __shared__ double h[6][6], mg[6], delta[6];
+  if (lane == 0) {
+    IcpDev local = *st;
+    if (!local.done) {
+      icp_step(tot, local, prm, h, mg, delta);
+      *st = local;
+    }
+  }
+}
+
+void assoc_estimate_pose(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose& initial, const wfk_icp_params& prm,
+                         wfk_icp_result* out) {
+  FrameDev& f = c->frame;
+  GBufDev& b = c->gbuf;
+  if (!f.maps_valid) throw Error(WFK_E_INVALID_ARG, "no point/normal maps (call backproject first)");
+  if (!b.valid) throw Error(WFK_E_INVALID_ARG, "no geometry buffer (call rasterize first)");
+  if (b.w != f.K.width || b.h != f.K.height) throw Error(WFK_E_INVALID_ARG, "estimate_global_pose: size mismatch");
+  if (!c->vol.valid) throw Error(WFK_E_INVALID_ARG, "no volume uploaded");
+  cudaStream_t s = c->stream;
+  const int64_t npx = int64_t(b.w) * b.h;
+  AssocArgs a;
+  a.K = K;
+  a.K.width = b.w;
+  a.K.height = b.h;
+  a.p = prm.corr;
+  a.g = c->vol.g;
+  a.depth = b.depth;
+  a.bpoint = b.point;
+  a.bnormal = b.normal;
+  a.bcanon = b.canonical;
+  a.mpoint = f.point;
+  a.mnormal = f.normal;
+  a.pv = f.pvalid;
+  a.nv = f.nvalid;
+  a.active = c->vol.active;
+  a.drop_inactive = 0;
+  a.flag = c->mask.ensure(size_t(std::max<int64_t>(npx, 2 * c->vol.n)) + 1);
+  k_icp_flag<<<grid_for(npx), kBlock, 0, s>>>(a);
+  WFK_CUDA(cudaMemsetAsync(a.flag + npx, 0, 1, s));
+  int32_t* pos = c->icp_pos.ensure(size_t(npx) + 1);
+  thrust::transform_iterator<U8ToInt, const uint8_t*, int32_t> it(a.flag, U8ToInt());
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, it, pos, int(npx + 1), s);
+  c->temp.ensure(tmp);
+  WFK_CUDA(cub::DeviceScan::ExclusiveSum(c->temp.p, tmp, it, pos, int(npx + 1), s));
+  double* src = c->icp_src.ensure(6 * size_t(npx) + 6);
+  M3 r0;
+  for (int i = 0; i < 9; ++i) r0.a[i / 3][i % 3] = initial.rotation[i];
+  k_icp_write<<<grid_for(npx), kBlock, 0, s>>>(a, pos, c->vol.deformed, transpose(r0), src);
+  count_launch(c, 3);
+  // state: pose = initial, prev_rms = +inf
+  IcpDev h0{};
+  for (int i = 0; i < 9; ++i) h0.R[i] = h0.pR[i] = initial.rotation[i];
+  for (int i = 0; i < 3; ++i) h0.t[i] = h0.pt[i] = initial.translation[i];
+  h0.prev_rms = __builtin_huge_val();
+  h0.done = prm.max_iters <= 0 ? 1 : 0;
+  IcpDev* st = reinterpret_cast<IcpDev*>(c->icp_state.ensure(sizeof(IcpDev)));
+  IcpDev* hst = reinterpret_cast<IcpDev*>(c->h_pinned + 1024);  // pinned staging (second 4 KB)
+  *hst = h0;
+  WFK_CUDA(cudaMemcpyAsync(st, hst, sizeof(IcpDev), cudaMemcpyHostToDevice, s));
+  const int nblk = c->num_sms * 2;
+  double* part = c->icp_part.ensure(size_t(nblk) * kIcpVals);
+  static const bool hostcheck = getenv("WFK_ICP_HOSTCHECK") != nullptr;
+  double* tot_dbg = hostcheck ? c->dvec.ensure(64) : nullptr;
+  IcpDev hcheck = h0;
+  for (int i = 0; i < prm.max_iters; ++i) {
+    k_icp_accumulate<<<nblk, kBlock, 0, s>>>(a, src, pos + npx, st, part);
+    k_icp_update<<<1, 32, 0, s>>>(part, nblk, st, prm, tot_dbg);
+    count_launch(c, 2);
+    if (hostcheck) {  // debug: the same step on the host from the device's totals
+      double tot[kIcpVals];
+      IcpDev dev;
+      WFK_CUDA(cudaMemcpyAsync(tot, tot_dbg, sizeof(tot), cudaMemcpyDeviceToHost, s));
+      WFK_CUDA(cudaMemcpyAsync(&dev, st, sizeof(IcpDev), cudaMemcpyDeviceToHost, s));
+      WFK_CUDA(cudaStreamSynchronize(s));
+      if (!hcheck.done) icp_step_host(tot, hcheck, prm);
+      fprintf(stderr, "[icp check] it %d host t %.9g %.9g %.9g dev t %.9g %.9g %.9g host R0 %.9g dev R0 %.9g\n", i,
+              hcheck.t[0], hcheck.t[1], hcheck.t[2], dev.t[0], dev.t[1], dev.t[2], hcheck.R[0], dev.R[0]);
+    }
+  }
+  WFK_CUDA(cudaMemcpyAsync(hst, st, sizeof(IcpDev), cudaMemcpyDeviceToHost, s));
+  WFK_CUDA(cudaStreamSynchronize(s));
+  std::memset(out, 0, sizeof(*out));
+  for (int i = 0; i < 9; ++i) out->pose.rotation[i] = hst->R[i];
+  for (int i = 0; i < 3; ++i) out->pose.translation[i] = hst->t[i];
+  out->converged = hst->converged;
+  out->degraded = hst->degraded;
+  out->rms = hst->rms;
+  out->iterations = hst->iterations;
 }
 
 // ---------------------------------------------------------------------------

@@ -243,7 +243,11 @@ struct wfk_ctx {
   wfk::DevBuf<double> dvec;     // misc double scratch
   wfk::DevBuf<double> eout;     // energy readback
   wfk::DevBuf<uint8_t> mask;    // misc byte scratch
-  int32_t* h_pinned = nullptr;  // small pinned readback area (4 KB)
+  int32_t* h_pinned = nullptr;  // small pinned readback area (8 KB)
+  // global-pose ICP (assoc.cu)
+  wfk::DevBuf<int32_t> icp_pos;
+  wfk::DevBuf<double> icp_src, icp_part;
+  wfk::DevBuf<uint8_t> icp_state;
   int coop_blocks = 0;          // resident blocks for cooperative kernels
 };
 

@@ -16,7 +16,7 @@ import subprocess
 import numpy as np
 
 from .abi import (CORR_DTYPE, CorrespondParams, Energy, ExpansionStats, FrameView, FusionParams,
-                  FusionStats, GeometryBufferView, Intrinsics, MeshView, PcgResult,
+                  FusionStats, GeometryBufferView, IcpParams, IcpResult, Intrinsics, MeshView, PcgResult,
                   PointNormalMapView, Pose, SolverParams, TraceEntry, Volume, VolumeView, ptr,
                   trace_to_list, VOL_ALL, WFK_OK)
 
@@ -40,13 +40,15 @@ class WfkError(RuntimeError):
 
 class PipelineConfig(C.Structure):
     _fields_ = [("solver", SolverParams), ("correspond", CorrespondParams), ("fusion", FusionParams),
-                ("reassociations", C.c_int32), ("reserved_", C.c_int32)]
+                ("reassociations", C.c_int32), ("estimate_pose", C.c_int32), ("icp", IcpParams)]
 
 
 class FrameRecord(C.Structure):
     _fields_ = [("energy", Energy), ("dense_count", C.c_int32), ("sparse_count", C.c_int32),
                 ("anomalies", C.c_int32), ("trace_len", C.c_int32), ("pcg_iterations", C.c_int32),
-                ("bootstrap", C.c_int32), ("fusion", FusionStats), ("expansion", ExpansionStats)]
+                ("bootstrap", C.c_int32), ("fusion", FusionStats), ("expansion", ExpansionStats),
+                ("pose", Pose), ("icp_degraded", C.c_int32), ("icp_iterations", C.c_int32),
+                ("icp_rms", C.c_double)]
 
 
 class NeHost(C.Structure):
@@ -372,6 +374,15 @@ class Context:
                                             C.byref(rec)))
         return rec
 
+    def estimate_global_pose(self, intr, initial: Pose, params=None) -> IcpResult:
+        """estimate_global_pose (solver.cpp:536-614) on the context's geometry
+        buffer, frame maps and volume."""
+        res = IcpResult()
+        p = params or IcpParams.make()
+        self._check(lib().wfk_estimate_global_pose(self.h, C.byref(intr), C.byref(initial), C.byref(p),
+                                                   C.byref(res)))
+        return res
+
     def stage_frame(self, slot: int, frame):
         fv = frame.view()
         self._check(lib().wfk_frame_stage(self.h, C.c_int32(slot), C.byref(fv)))
@@ -412,10 +423,14 @@ class Context:
         return depth, color
 
 
-def pipeline_config(solver=None, correspond=None, fusion=None, reassociations=3) -> PipelineConfig:
+def pipeline_config(solver=None, correspond=None, fusion=None, reassociations=3, estimate_pose=True,
+                    icp=None) -> PipelineConfig:
+    """ReconstructorConfig defaults (config.hpp): ICP on, 3 reassociations."""
     cfg = PipelineConfig()
     cfg.solver = solver or SolverParams.make()
     cfg.correspond = correspond or CorrespondParams.make()
     cfg.fusion = fusion or FusionParams.make()
     cfg.reassociations = reassociations
+    cfg.estimate_pose = 1 if estimate_pose else 0
+    cfg.icp = icp or IcpParams.make()
     return cfg

@@ -45,6 +45,7 @@ STRUCTS = {
     "wfk_point_normal_map": abi.PointNormalMapView, "wfk_geometry_buffer": abi.GeometryBufferView,
     "wfk_mesh_view": abi.MeshView, "wfk_pipeline_config": wfk.PipelineConfig,
     "wfk_frame_record": wfk.FrameRecord, "wfk_synth_scene": wfk.SynthScene, "wfk_config": wfk.Config,
+    "wfk_icp_params": abi.IcpParams, "wfk_icp_result": abi.IcpResult,
     "wfk_ne_host": wfk.NeHost, "wfk_profile": wfk.Profile,
 }
 

@@ -1,7 +1,7 @@
 """End-to-end parity of the per-frame hot path (Reconstructor::process_frame,
-pipeline.cpp:143-262, without ICP / feature front-end): the B200 path
-(wfk_process_frame) against the oracle's restatement on the same synthetic
-bend sequence."""
+pipeline.cpp:143-262, with the global-pose ICP, without the feature front-end):
+the B200 path (wfk_process_frame) against the oracle's restatement on the same
+synthetic bend sequence."""
 import numpy as np
 import pytest
 
@@ -36,24 +36,31 @@ def bend_frames(ctx, K, n_frames, amplitude, frames_total=10):
     return out
 
 
-@pytest.mark.parametrize("n,reassoc,levels", [(32, 1, 1), (48, 2, 3)])
-def test_process_frame_parity(ctx, n, reassoc, levels):
+@pytest.mark.parametrize("n,reassoc,levels,icp", [(32, 1, 1, True), (48, 2, 3, True), (48, 2, 3, False)])
+def test_process_frame_parity(ctx, n, reassoc, levels, icp):
     from paper_1603_08161_b200.wfk import pipeline_config
     K = Intrinsics.make(280, 280, 159.5, 119.5, 320, 240)
     voxel = 0.7 / (n - 1)
     origin = (-0.35, -0.35, 0.85)
     solver = SolverParams.make(levels=levels)
     frames = bend_frames(ctx, K, 4, 1.0)
-    ref = O.Reconstructor((n, n, n), voxel, origin, solver=solver, reassociations=reassoc)
+    ref = O.Reconstructor((n, n, n), voxel, origin, solver=solver, reassociations=reassoc, estimate_pose=icp)
     vol = Volume((n, n, n), voxel, origin)
     ctx.upload_volume(vol)
-    cfg = pipeline_config(solver=solver, reassociations=reassoc)
+    cfg = pipeline_config(solver=solver, reassociations=reassoc, estimate_pose=icp)
+    pose = Pose.make()
     for i, fr in enumerate(frames):
         rr = ref.process_frame(fr)
-        rg = ctx.process_frame(fr, Pose.make(), cfg, i)
+        rg = ctx.process_frame(fr, pose, cfg, i)
+        pose = rg.pose  # the Reconstructor's pose_ carried to the next frame
         if i == 0:
             assert rg.fusion.fused == rr.fusion.fused
             continue
+        if icp:
+            if i == 1:
+                assert rg.icp_iterations == rr.icp_iterations and rg.icp_degraded == rr.icp_degraded
+            np.testing.assert_allclose(rg.pose.matrix(), rr.pose.matrix(), atol=1e-7)
+            np.testing.assert_allclose(rg.pose.vector(), rr.pose.vector(), atol=1e-7)
         if i == 1:  # identical inputs up to this frame's solve: integer work is exact
             assert rg.dense_count == rr.dense_count
             assert rg.trace_len == rr.trace_len
