@@ -9,8 +9,9 @@ deforming sphere (r 0.3 m at z 1.2 m, bend 2.0 rad/m oscillating with
 frequency 2 over a 300-frame sequence).  One step = one
 Reconstructor::process_frame (pipeline.cpp:143-262) with the reference's
 default solver / correspondence / fusion parameters and 3 re-associations.
-The ICP global pose and the SIFT feature front-end are outside the scope of
-this path and are off in both arms.
+The global-pose ICP runs before the solve as in the reference's default
+configuration (config.hpp:45, pipeline.cpp:174-183); the SIFT feature front-end
+is outside the scope of this path and off in both arms.
 
   python bench.py [--gpus N --steps K --warmup W]        B200 arm (libwfk.so)
   python bench.py --impl reference [...]                  CPU arm (the oracle port)
@@ -62,7 +63,8 @@ def workload_config(n_gpus):
         "depth_resolution": [W_PX, H_PX],
         "levels": 3, "flip_flop_iters": 4, "pcg_tol": 1e-4, "pcg_max_iters": 50, "reassociations": 3,
         "scene": "sphere r=0.3 m @ z=1.2 m, bend 2.0 rad/m, oscillating freq 2 over 300 frames",
-        "icp": "off (out of scope)", "sparse_features": "off (front-end out of scope)",
+        "icp": "on (global-pose ICP before the solve, config.hpp:45 default)",
+        "sparse_features": "off (front-end out of scope)",
         "l2": "flushed (256 MB write) before every timed frame",
         "parallelism": f"replicas x{n_gpus}" if n_gpus > 1 else "single GPU",
     }
@@ -249,12 +251,13 @@ def run_b200(args):
     log(f"bootstrap: fused {rec0.fusion.fused}")
     assert rec0.bootstrap == 1
     for f in range(1, 1 + args.warmup):
-        ctx.process_staged_frame(f, pose, cfg, f)
+        pose = ctx.process_staged_frame(f, pose, cfg, f).pose  # the Reconstructor's pose_, refined by ICP
 
-    # checkpoint so the e2e pass repeats exactly the same K frames
+    # checkpoint (volume + pose) so the e2e pass repeats exactly the same K frames
     log("warm-up done")
     ckpt = Volume(dims, voxel, origin)
     ctx.download_volume(ckpt)
+    ckpt_pose = pose
     timed = list(range(1 + args.warmup, n_frames))
 
     # ---- value: inputs resident in HBM ---------------------------------------
@@ -269,6 +272,7 @@ def run_b200(args):
             ctx.timer_mark(0)
             recs.append(ctx.process_staged_frame(f, pose, cfg, f))
             ctx.timer_mark(1)
+            pose = recs[-1].pose
             total_ms += ctx.timer_elapsed_ms(0, 1)
     d.barrier()
     launches = ctx.launch_count - launches0
@@ -278,6 +282,7 @@ def run_b200(args):
     log(f"timed: {total_ms / len(timed):.3f} ms/frame")
     # ---- e2e: same frames through the public call with host buffers -----------
     ctx.upload_volume(ckpt)
+    pose = ckpt_pose
     e2e_ms = 0.0
     d.barrier()
     for f in timed:
@@ -286,6 +291,7 @@ def run_b200(args):
         r = ctx.process_frame(frames[f], pose, cfg, f)   # H2D frame + D2H record inside
         ctx.timer_mark(3)
         e2e_ms += ctx.timer_elapsed_ms(2, 3)
+        pose = r.pose
         _ = (r.energy.total, r.dense_count)
     d.barrier()
 
