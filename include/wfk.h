@@ -122,6 +122,10 @@ int wfk_advance_active_ages(wfk_ctx* ctx);
 /* backproject_depth (correspond.hpp:44, correspond.cpp:7-57) of the uploaded
  * frame; out may be NULL (maps stay on the device). */
 int wfk_backproject_depth(wfk_ctx* ctx, int32_t exec, wfk_point_normal_map* out);
+/* caller-computed PointNormalMap (correspond.hpp:34-42) as the context's frame
+ * maps -- what a drop-in estimate_global_pose / find_dense_correspondences
+ * receives from the reference's caller */
+int wfk_maps_upload(wfk_ctx* ctx, const wfk_point_normal_map* maps);
 /* extract_mesh (isosurface.hpp:49, isosurface.cpp:39-97); sizes returned */
 int wfk_extract_mesh(wfk_ctx* ctx, const wfk_pose* pose, int64_t* nv, int64_t* nt);
 /* re-warp the mesh's canonical vertices through the current field (the

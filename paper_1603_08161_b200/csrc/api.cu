@@ -481,6 +481,28 @@ int wfk_rasterize(wfk_ctx* c, const wfk_intrinsics* intr, int32_t, wfk_geometry_
   });
 }
 
+int wfk_maps_upload(wfk_ctx* c, const wfk_point_normal_map* m) {
+  return guard(c, [&] {
+    if (!m || m->width <= 0 || m->height <= 0 || !m->point || !m->normal || !m->point_valid || !m->normal_valid)
+      throw Error(WFK_E_INVALID_ARG, "bad point/normal map");
+    FrameDev& f = c->frame;
+    const size_t npx = size_t(m->width) * size_t(m->height);
+    f.point.ensure(3 * npx);
+    f.normal.ensure(3 * npx);
+    f.pvalid.ensure(npx);
+    f.nvalid.ensure(npx);
+    cudaStream_t s = c->stream;
+    WFK_CUDA(cudaMemcpyAsync(f.point, m->point, npx * 24, cudaMemcpyHostToDevice, s));
+    WFK_CUDA(cudaMemcpyAsync(f.normal, m->normal, npx * 24, cudaMemcpyHostToDevice, s));
+    WFK_CUDA(cudaMemcpyAsync(f.pvalid, m->point_valid, npx, cudaMemcpyHostToDevice, s));
+    WFK_CUDA(cudaMemcpyAsync(f.nvalid, m->normal_valid, npx, cudaMemcpyHostToDevice, s));
+    WFK_CUDA(cudaStreamSynchronize(s));
+    f.K.width = m->width;
+    f.K.height = m->height;
+    f.maps_valid = true;
+  });
+}
+
 int wfk_gbuffer_upload(wfk_ctx* c, const wfk_geometry_buffer* b) {
   return guard(c, [&] {
     if (!b || b->width <= 0 || b->height <= 0) throw Error(WFK_E_INVALID_ARG, "bad geometry buffer");

@@ -374,6 +374,11 @@ class Context:
                                             C.byref(rec)))
         return rec
 
+    def upload_maps(self, maps):
+        """A host PointNormalMap (e.g. the oracle's) as the context's frame maps."""
+        mv = maps.view()
+        self._check(lib().wfk_maps_upload(self.h, C.byref(mv)))
+
     def estimate_global_pose(self, intr, initial: Pose, params=None) -> IcpResult:
         """estimate_global_pose (solver.cpp:536-614) on the context's geometry
         buffer, frame maps and volume."""

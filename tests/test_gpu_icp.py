@@ -83,3 +83,24 @@ def test_icp_degraded_keeps_pose(ctx):
     ref, got = run_both(ctx, vol, Frame(K, np.zeros((240, 320), np.float32)), init, IcpParams.make())
     assert got.degraded == ref.degraded == 1 and got.iterations == 0
     np.testing.assert_array_equal(got.pose.vector(), init.vector())
+
+
+def test_icp_from_host_buffers(ctx):
+    """The drop-in path: the caller's GeometryBuffer and
+    PointNormalMap uploaded as they are, the volume's field re-used."""
+    vol = fused_volume(jitter=0.001)
+    d1, c1 = O.synth_render(K, center=(0.006, -0.004, 1.207))
+    fr = Frame(K, d1, c1)
+    mesh = O.extract_mesh(vol)
+    mesh.compute_normals()
+    buf = mesh.rasterize(K)
+    maps = O.backproject_depth(fr)
+    params = IcpParams.make()
+    ref = O.estimate_global_pose(buf, maps, K, vol, Pose.make(), params)
+    ctx.upload_volume(vol)
+    ctx.upload_gbuffer(buf)
+    ctx.upload_maps(maps)
+    got = ctx.estimate_global_pose(K, Pose.make(), params)
+    assert got.iterations == ref.iterations and got.converged == ref.converged and not got.degraded
+    np.testing.assert_allclose(got.pose.vector(), ref.pose.vector(), atol=1e-10)
+    np.testing.assert_allclose(got.pose.matrix(), ref.pose.matrix(), atol=1e-10)
