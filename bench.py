@@ -57,8 +57,11 @@ def log(*a):
 
 def workload_config(n_gpus):
     return {
-        "workload": "VolumeDeform per-frame hot path, BASELINE configs[2]: 640x480 depth, 128^3 lattice, "
-                    "3-level coarse-to-fine flip-flop GN/PCG + deformed-TSDF fusion + association",
+        "workload": (f"VolumeDeform per-frame hot path, BASELINE configs[2]: 640x480 depth, 128^3 lattice, "
+                     "3-level coarse-to-fine flip-flop GN/PCG + deformed-TSDF fusion + association"
+                     if N_LATTICE == 128 else
+                     f"VolumeDeform per-frame hot path on the BASELINE configs[3] lattice ({N_LATTICE}^3, "
+                     "one GPU), 640x480 depth, 3-level coarse-to-fine flip-flop GN/PCG + fusion + association"),
         "lattice": [N_LATTICE] * 3,
         "depth_resolution": [W_PX, H_PX],
         "levels": 3, "flip_flop_iters": 4, "pcg_tol": 1e-4, "pcg_max_iters": 50, "reassociations": 3,
@@ -437,14 +440,18 @@ def run_reference(args):
 
 
 def main():
+    global N_LATTICE
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-frames", type=int, default=2)
+    ap.add_argument("--lattice", type=int, default=N_LATTICE,
+                    help="lattice side (default 128 = configs[2]; 256 = the configs[3] lattice on one GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    N_LATTICE = args.lattice
     if args.warmup < 3 and args.impl == "b200":
         print("warning: W >= 3 warm-up steps are required for a valid number", file=sys.stderr)
     if args.impl == "reference":

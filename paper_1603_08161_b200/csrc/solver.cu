@@ -596,6 +596,7 @@ struct FFArgs {
   unsigned long long* sync_ll;  // split-reduction totals (flag-embedded words)
   int meta_rows, meta_cons;     // pipelined matrix-free levels: metadata cached in shared memory
   int asm_smem;                 // pipelined assembled levels: B^T B rows cached in shared memory
+  double* state_spill;          // pipelined PCG row state in global memory (too many rows for shared), or null
   const int32_t* perm;          // pipelined matrix-free levels: row order (decreasing incidences), or null
   int pcg_variant;       // 0 pipelined (one reduction, overlapped), 1 Chronopoulos-Gear
   const double4 *crhs, *cdiag;
@@ -1447,7 +1448,8 @@ __device__ __forceinline__ void for_warp_rows(int N, int skip, int K, const int3
 // padded vector-major layout, 32 bytes per 3-vector).
 enum { kSx, kSr, kSw, kSp, kSs, kSz, kSd, kSn, kSlotVecs };
 struct Slots {
-  double4* sm;  // kSlotVecs x S
+  double4* sm;  // kSlotVecs x S (or this block's part of the global spill area, stride `stride`)
+  size_t stride;  // elements between two component arrays: S in shared memory, G x S in the spill area
   int S;        // slots per block = warps per block x K x RPW
   int K;        // rounds per warp
   int RPW, gw, nw;
@@ -1460,18 +1462,18 @@ struct Slots {
 #if WFK_SLOT_SOA
   // component-major: (vector, component, slot) -- 24 bytes per 3-vector
   __device__ __forceinline__ double4 get(int v, int q) const {
-    const double* b = reinterpret_cast<const double*>(sm) + size_t(3 * v) * S + q;
-    return make_double4(b[0], b[S], b[2 * S], 0.0);
+    const double* b = reinterpret_cast<const double*>(sm) + size_t(3 * v) * stride + q;
+    return make_double4(b[0], b[stride], b[2 * stride], 0.0);
   }
   __device__ __forceinline__ void put(int v, int q, double4 x) const {
-    double* b = reinterpret_cast<double*>(sm) + size_t(3 * v) * S + q;
+    double* b = reinterpret_cast<double*>(sm) + size_t(3 * v) * stride + q;
     b[0] = x.x;
-    b[S] = x.y;
-    b[2 * S] = x.z;
+    b[stride] = x.y;
+    b[2 * stride] = x.z;
   }
 #else
-  __device__ __forceinline__ double4 get(int v, int q) const { return sm[v * S + q]; }
-  __device__ __forceinline__ void put(int v, int q, double4 x) const { sm[v * S + q] = x; }
+  __device__ __forceinline__ double4 get(int v, int q) const { return sm[v * stride + q]; }
+  __device__ __forceinline__ void put(int v, int q, double4 x) const { sm[v * stride + q] = x; }
 #endif
 };
 __host__ __device__ constexpr int pipe_rpw(bool asm_level, bool rows_on_lanes) {
@@ -1488,7 +1490,7 @@ struct PipeLayout {
   size_t rmeta, cmeta, amat, total;  // byte offsets / size
 };
 __host__ __device__ inline PipeLayout pipe_layout(int N, int64_t C, int rpw, int G, int tpb, int skip, bool rows,
-                                                  bool cons, bool amat = false) {
+                                                  bool cons, bool amat = false, bool state_smem = true) {
   PipeLayout l;
   const int wpb = tpb / 32;
   const int nw = G * wpb - skip;
@@ -1497,7 +1499,8 @@ __host__ __device__ inline PipeLayout pipe_layout(int N, int64_t C, int rpw, int
   const int64_t nt = int64_t(G) * tpb - 32 * skip;
   l.KC = cons ? int((C + nt - 1) / nt) : 0;
   l.SC = tpb * l.KC;
-  size_t off = size_t(kSlotVecs) * l.S * (WFK_SLOT_SOA ? 3 * sizeof(double) : sizeof(double4));
+  // row state in shared memory, or (large lattices) in a global spill area
+  size_t off = state_smem ? size_t(kSlotVecs) * l.S * (WFK_SLOT_SOA ? 3 * sizeof(double) : sizeof(double4)) : 0;
   l.rmeta = off;
   if (rows) off += size_t(l.S) * (2 * sizeof(int4) + 2 * sizeof(int));
   off = (off + 31) / 32 * 32;
@@ -1573,10 +1576,19 @@ __device__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, double& relres) {
   sl.sm = dyn_smem;
   sl.RPW = pipe_rpw(ASM, rows_on_lanes);
   const bool amat = ASM && a.asm_smem && !rows_on_lanes;
-  const PipeLayout lay =
-      pipe_layout(a.N, a.C, sl.RPW, gridDim.x, blockDim.x, kSkip, !ASM && a.meta_rows, !ASM && a.meta_cons, amat);
+  const PipeLayout lay = pipe_layout(a.N, a.C, sl.RPW, gridDim.x, blockDim.x, kSkip, !ASM && a.meta_rows,
+                                     !ASM && a.meta_cons, amat, a.state_spill == nullptr);
   sl.K = lay.K;
   sl.S = lay.S;
+  sl.stride = size_t(lay.S);
+  if (a.state_spill) {  // the block's slots in the global spill area
+#if WFK_SLOT_SOA
+    sl.sm = reinterpret_cast<double4*>(a.state_spill + size_t(blockIdx.x) * lay.S);
+#else
+    sl.sm = reinterpret_cast<double4*>(a.state_spill) + size_t(blockIdx.x) * lay.S;
+#endif
+    sl.stride = size_t(lay.S) * gridDim.x;
+  }
   sl.gw = gwarp() - kSkip;
   sl.nw = nwarps() - kSkip;
   const MfMeta mm = mf_meta(reinterpret_cast<char*>(dyn_smem), lay, !ASM && a.meta_rows, !ASM && a.meta_cons);
@@ -2408,16 +2420,24 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   size_t smem = 0;
   a.meta_rows = a.meta_cons = 0;
   a.asm_smem = 0;
+  a.state_spill = nullptr;
   if (a.pcg_variant == 0) {
     const int rpw = pipe_rpw(L.assembled, a.asm_rows_on_lanes);
+    // the row state goes to a global spill area when it does not fit shared memory
+    const PipeLayout base = pipe_layout(L.N, L.C, rpw, G, kCoopBlock, kPipeSkip, false, false);
+    const bool spill = base.total > kPipeSmemMax || getenv("WFK_PIPE_SPILL") != nullptr;  // env: tests
+    if (spill) {
+      const size_t n = size_t(kSlotVecs) * (WFK_SLOT_SOA ? 3 : 4) * size_t(G) * size_t(base.S);
+      a.state_spill = L.state_spill.ensure(n);
+    }
     auto bytes = [&](bool rows, bool cons) {
-      return pipe_layout(L.N, L.C, rpw, G, kCoopBlock, kPipeSkip, rows, cons).total;
+      return pipe_layout(L.N, L.C, rpw, G, kCoopBlock, kPipeSkip, rows, cons, false, !spill).total;
     };
     static const bool no_meta = getenv("WFK_PIPE_NO_META") != nullptr;
     a.asm_smem = 0;
     static const bool no_asm_smem = getenv("WFK_NO_ASM_SMEM") != nullptr;
     if (L.assembled && !a.asm_rows_on_lanes && !no_meta && !no_asm_smem &&
-        pipe_layout(L.N, L.C, rpw, G, kCoopBlock, kPipeSkip, false, false, true).total <= kPipeSmemMax)
+        pipe_layout(L.N, L.C, rpw, G, kCoopBlock, kPipeSkip, false, false, true, !spill).total <= kPipeSmemMax)
       a.asm_smem = 1;
     static const bool cmeta = getenv("WFK_PIPE_CMETA") != nullptr;
     if (!L.assembled && !no_meta && cmeta && bytes(true, true) <= kPipeSmemMax) {
@@ -2425,7 +2445,7 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
     } else if (!L.assembled && !no_meta && bytes(true, false) <= kPipeSmemMax) {
       a.meta_rows = 1;
     }
-    smem = a.asm_smem ? pipe_layout(L.N, L.C, rpw, G, kCoopBlock, kPipeSkip, false, false, true).total
+    smem = a.asm_smem ? pipe_layout(L.N, L.C, rpw, G, kCoopBlock, kPipeSkip, false, false, true, !spill).total
                       : bytes(a.meta_rows, a.meta_cons);
     if (smem > kPipeSmemMax) {
       a.pcg_variant = 1;

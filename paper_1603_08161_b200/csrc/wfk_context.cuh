@@ -105,6 +105,7 @@ struct Level {
   DevBuf<double4> t, x, rhs, r, p, ap, dinv, u, w, crhs, cdiag, z;  // 32 B padded 3-vectors
   DevBuf<double4> mbuf;  // 2 x N: pipelined PCG m = D w, double-buffered
   DevBuf<double4> nbuf;  // N: pipelined PCG n = A m
+  DevBuf<double> state_spill;  // pipelined PCG row state when it does not fit shared memory
   DevBuf<int32_t> perm, perm_key, perm_val;  // matrix-free levels: row order by decreasing incidences
   DevBuf<double> rot;
   // assembled B^T B for rows with many incidences (see kAssembleRatio)

@@ -296,3 +296,24 @@ def test_solve_is_deterministic(ctx):
     assert np.array_equal(out[0][0], out[1][0])
     assert np.array_equal(out[0][1], out[1][1])
     assert out[0][2] == out[1][2]
+
+
+def test_pipelined_pcg_spill_matches_shared(ctx, monkeypatch):
+    """Large lattices keep the pipelined PCG's row state in a global spill area
+    instead of shared memory: same arithmetic, so the same result bit for bit."""
+    v = make_volume(32)
+    cons = random_dense_constraints(v, 2000, seed=9)
+    p = SolverParams.make()
+    out = []
+    for spill in (False, True):
+        if spill:
+            monkeypatch.setenv("WFK_PIPE_SPILL", "1")
+        w = v.copy()
+        ctx.upload_volume(w)
+        ctx.upload_constraints(cons)
+        tr = ctx.solve_coarse_to_fine(Pose.make(), p)
+        ctx.download_volume(w)
+        out.append((w.deformed.copy(), [e["energy"]["total"] for e in tr]))
+    monkeypatch.delenv("WFK_PIPE_SPILL", raising=False)
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1]
