@@ -152,6 +152,14 @@ int wfk_find_dense_correspondences(wfk_ctx* ctx, const wfk_intrinsics* intr,
 int wfk_constraints_append(wfk_ctx* ctx, const wfk_correspondence* c, int64_t n,
                            int32_t drop_inactive, int64_t* kept);
 
+/* ---- batched warp inversion ------------------------------------------------------
+ * DeformableVolume::invert_warp (volume.hpp:89-94, volume.cpp:95-126) for n points
+ * (host arrays, 3n doubles each): canonical x with warp_point(pose, x) == y from
+ * seed, damped Gauss-Newton on the analytic trilinear Jacobian with Eigen's
+ * PartialPivLU; ok[i] = 0 where the reference returns nullopt (x = 0). */
+int wfk_invert_warp(wfk_ctx* ctx, const wfk_pose* pose, int64_t n, const double* y, const double* seed,
+                    int32_t max_iters, double tol, double* x, uint8_t* ok);
+
 /* ---- global pose ---------------------------------------------------------------
  * estimate_global_pose (solver.cpp:536-614; replaces solver.hpp:144-147): dense
  * projective point-to-plane ICP.  Sources are the valid samples of the context's

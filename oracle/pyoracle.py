@@ -372,6 +372,21 @@ def estimate_global_pose(buf, maps, intr, vol, initial=None, params=None) -> Icp
     return res
 
 
+def invert_warp(vol, pose, y, seed, max_iters=20, tol=1e-6):
+    """DeformableVolume::invert_warp (volume.cpp:95-126) for each row of y / seed;
+    returns (x, ok)."""
+    y = np.ascontiguousarray(y, np.float64).reshape(-1, 3)
+    seed = np.ascontiguousarray(seed, np.float64).reshape(-1, 3)
+    n = y.shape[0]
+    x = np.zeros((n, 3), np.float64)
+    ok = np.zeros(n, np.uint8)
+    vv = vol.view()
+    p = pose or Pose.make()
+    _check(lib().wfo_invert_warp(C.byref(vv), C.byref(p), C.c_int64(n), ptr(y, C.c_double), ptr(seed, C.c_double),
+                                 C.c_int32(max_iters), C.c_double(tol), ptr(x, C.c_double), ptr(ok, C.c_uint8)))
+    return x, ok.astype(bool)
+
+
 def ldlt_solve(a, b):
     """Eigen LDLT (symmetric pivoting) restated: solve a x = b, a symmetric n x n, n <= 8."""
     a = np.ascontiguousarray(a, np.float64)

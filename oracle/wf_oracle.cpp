@@ -1340,6 +1340,100 @@ std::vector<Con> find_dense(const GBuf& buf, const Maps& maps, const wfk_intrins
 }
 
 // ---------------------------------------------------------------------------
+// DeformableVolume::invert_warp (volume.cpp:68-126)
+// ---------------------------------------------------------------------------
+// deformed_jacobian (volume.cpp:68-93): analytic d interpolate_deformed / dx
+M3 deformed_jacobian(const Vol& v, const V3& x) {
+  const V3 rel = (x - v.origin) / v.voxel;
+  const int d[3] = {v.nx, v.ny, v.nz};
+  int cell[3];
+  double f[3];
+  for (int k = 0; k < 3; ++k) {
+    int c = static_cast<int>(std::floor(rel[k]));
+    c = std::clamp(c, 0, d[k] - 2);
+    cell[k] = c;
+    f[k] = rel[k] - c;
+  }
+  M3 j;  // zero-initialised
+  for (int dz = 0; dz < 2; ++dz)
+    for (int dy = 0; dy < 2; ++dy)
+      for (int dx = 0; dx < 2; ++dx) {
+        const V3 t = v.deformed(v.lin(cell[0] + dx, cell[1] + dy, cell[2] + dz));
+        const double wx = dx ? f[0] : 1 - f[0];
+        const double wy = dy ? f[1] : 1 - f[1];
+        const double wz = dz ? f[2] : 1 - f[2];
+        const double g[3] = {(dx ? 1.0 : -1.0) * wy * wz, (dy ? 1.0 : -1.0) * wx * wz, (dz ? 1.0 : -1.0) * wx * wy};
+        for (int c = 0; c < 3; ++c) {
+          j.a[0][c] += t.x * g[c];
+          j.a[1][c] += t.y * g[c];
+          j.a[2][c] += t.z * g[c];
+        }
+      }
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) j.a[r][c] = j.a[r][c] / v.voxel;
+  return j;
+}
+
+// Eigen PartialPivLU<Matrix3d>::solve restated: column k takes the row of the
+// largest |entry| at or below the diagonal (first one on ties), the column
+// below the pivot is divided by it and the trailing block takes the rank-1
+// update; solve = row permutation, unit-lower forward, upper back substitution.
+V3 lu3_solve(M3 a, const V3& b) {
+  int perm[3] = {0, 1, 2};
+  for (int k = 0; k < 3; ++k) {
+    int p = k;
+    for (int i = k + 1; i < 3; ++i)
+      if (std::abs(a.a[i][k]) > std::abs(a.a[p][k])) p = i;
+    if (a.a[p][k] != 0) {
+      if (p != k) {
+        for (int c = 0; c < 3; ++c) std::swap(a.a[k][c], a.a[p][c]);
+        std::swap(perm[k], perm[p]);
+      }
+      for (int i = k + 1; i < 3; ++i) a.a[i][k] /= a.a[k][k];
+    }
+    for (int i = k + 1; i < 3; ++i)
+      for (int c = k + 1; c < 3; ++c) a.a[i][c] -= a.a[i][k] * a.a[k][c];
+  }
+  const double bb[3] = {b.x, b.y, b.z};
+  double x[3] = {bb[perm[0]], bb[perm[1]], bb[perm[2]]};
+  for (int i = 1; i < 3; ++i)
+    for (int j = 0; j < i; ++j) x[i] -= a.a[i][j] * x[j];
+  for (int i = 2; i >= 0; --i) {
+    for (int j = 2; j > i; --j) x[i] -= a.a[i][j] * x[j];
+    x[i] /= a.a[i][i];
+  }
+  return {x[0], x[1], x[2]};
+}
+
+bool invert_warp(const Vol& v, const Pose& pose, const V3& y, const V3& seed, int max_iters, double tol, V3& out) {
+  const V3 target = transpose(pose.r) * (y - pose.t);  // GlobalPose::apply_inverse (core.hpp:25-27)
+  V3 x = seed;
+  if (!v.contains(x)) return false;
+  const double hi[3] = {v.origin.x + v.voxel * (v.nx - 1), v.origin.y + v.voxel * (v.ny - 1),
+                        v.origin.z + v.voxel * (v.nz - 1)};
+  const double lo[3] = {v.origin.x, v.origin.y, v.origin.z};
+  for (int it = 0; it < max_iters; ++it) {
+    const V3 r = v.interpolate_deformed(x) - target;
+    if (norm(r) <= tol) {
+      out = x;
+      return true;
+    }
+    const M3 j = deformed_jacobian(v, x);
+    V3 step = std::abs(det(j)) > 1e-12 ? lu3_solve(j, r) : r;  // damped fixed-point fallback
+    const double max_step = v.voxel;
+    if (norm(step) > max_step) step = step * (max_step / norm(step));
+    V3 xn = x - step;
+    for (int k = 0; k < 3; ++k) xn[k] = std::clamp(xn[k], lo[k], hi[k]);  // keep the iterate inside the grid
+    x = xn;
+  }
+  if (norm(v.interpolate_deformed(x) - target) <= tol) {
+    out = x;
+    return true;
+  }
+  return false;
+}
+
+// ---------------------------------------------------------------------------
 // global pose: estimate_global_pose (solver.cpp:536-614)
 // ---------------------------------------------------------------------------
 // Eigen 3.4 LDLT<MatrixXd> (ldlt_inplace<Lower>::unblocked and _solve_impl),
@@ -2082,6 +2176,21 @@ int wfo_estimate_global_pose(const wfk_geometry_buffer* buf, const wfk_point_nor
   out->degraded = r.degraded;
   out->rms = r.rms;
   out->iterations = r.iterations;
+  return WFK_OK;
+}
+int wfo_invert_warp(const wfk_volume_view* view, const wfk_pose* pose, int64_t n, const double* y,
+                    const double* seed, int32_t max_iters, double tol, double* x, uint8_t* ok) {
+  const Vol v = Vol::borrow(view);
+  const Pose p = pose_of(pose);
+  for (int64_t i = 0; i < n; ++i) {
+    V3 o{0, 0, 0};
+    const bool good = invert_warp(v, p, {y[3 * i], y[3 * i + 1], y[3 * i + 2]},
+                                  {seed[3 * i], seed[3 * i + 1], seed[3 * i + 2]}, max_iters, tol, o);
+    ok[i] = good ? 1 : 0;
+    x[3 * i] = o.x;
+    x[3 * i + 1] = o.y;
+    x[3 * i + 2] = o.z;
+  }
   return WFK_OK;
 }
 int wfo_ldlt_solve(int n, const double* a, const double* b, double* x) {

@@ -94,6 +94,9 @@ int wfo_find_dense_correspondences(const wfk_geometry_buffer* buf,
 int wfo_estimate_global_pose(const wfk_geometry_buffer* buf, const wfk_point_normal_map* maps,
                              const wfk_intrinsics* intr, const wfk_volume_view* v, const wfk_pose* initial,
                              const wfk_icp_params* params, wfk_icp_result* out);
+/* DeformableVolume::invert_warp (volume.cpp:95-126) for n points; x = 0, ok = 0 on failure */
+int wfo_invert_warp(const wfk_volume_view* v, const wfk_pose* pose, int64_t n, const double* y, const double* seed,
+                    int32_t max_iters, double tol, double* x, uint8_t* ok);
 /* Eigen LDLT<MatrixXd> (symmetric pivoting) restated, n <= 8: solves A x = b */
 int wfo_ldlt_solve(int n, const double* a, const double* b, double* x);
 int wfo_sparse_to_constraints(const double* canonical, const double* target, int64_t n,

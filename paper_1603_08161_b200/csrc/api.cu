@@ -674,6 +674,14 @@ void run_frame(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose* pose_in, con
 
 extern "C" {
 
+int wfk_invert_warp(wfk_ctx* c, const wfk_pose* pose, int64_t n, const double* y, const double* seed,
+                    int32_t max_iters, double tol, double* x, uint8_t* ok) {
+  return guard(c, [&] {
+    if (n < 0 || (n > 0 && (!y || !seed || !x || !ok))) throw Error(WFK_E_INVALID_ARG, "null argument");
+    volume_invert_warp(c, pose, n, y, seed, max_iters, tol, x, ok);
+  });
+}
+
 int wfk_estimate_global_pose(wfk_ctx* c, const wfk_intrinsics* intr, const wfk_pose* initial,
                              const wfk_icp_params* params, wfk_icp_result* out) {
   return guard(c, [&] {

@@ -374,6 +374,18 @@ class Context:
                                             C.byref(rec)))
         return rec
 
+    def invert_warp(self, pose: Pose, y, seed, max_iters=20, tol=1e-6):
+        """DeformableVolume::invert_warp (volume.cpp:95-126) for each row; returns (x, ok)."""
+        y = np.ascontiguousarray(y, np.float64).reshape(-1, 3)
+        seed = np.ascontiguousarray(seed, np.float64).reshape(-1, 3)
+        n = y.shape[0]
+        x = np.zeros((n, 3), np.float64)
+        ok = np.zeros(n, np.uint8)
+        self._check(lib().wfk_invert_warp(self.h, C.byref(pose), C.c_int64(n), ptr(y, C.c_double),
+                                          ptr(seed, C.c_double), C.c_int32(max_iters), C.c_double(tol),
+                                          ptr(x, C.c_double), ptr(ok, C.c_uint8)))
+        return x, ok.astype(bool)
+
     def upload_maps(self, maps):
         """A host PointNormalMap (e.g. the oracle's) as the context's frame maps."""
         mv = maps.view()
