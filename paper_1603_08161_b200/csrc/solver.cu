@@ -1007,16 +1007,30 @@ __device__ __forceinline__ void row_pass(const FFArgs& a, const double4* v, Sink
         }
       }
       if (live && !frozen) {
+        // branch-free over the lane's slots so all of its gathers are in
+        // flight at once: an absent column gathers the row itself (always
+        // valid) and its terms are masked to zero
+        constexpr int NS = (27 + L - 1) / L;
+        int colv[NS];
+        V3 xs[NS];
 #pragma unroll
-        for (int s = sub; s < 27; s += L) {
-          const int col = cc[s];
-          if (col < 0) continue;
-          const V3 x = ld4(v, col);
+        for (int i = 0; i < NS; ++i) {
+          const int s = sub + L * i;
+          colv[i] = s < 27 ? cc[s] : -1;
+        }
+#pragma unroll
+        for (int i = 0; i < NS; ++i) xs[i] = ld4(v, colv[i] < 0 ? r : colv[i]);
+#pragma unroll
+        for (int i = 0; i < NS; ++i) {
+          const int s = sub + L * i;
+          if (s >= 27) break;
+          const double mk = colv[i] < 0 ? 0.0 : 1.0;
+          const V3 x = xs[i];
           const double* b = bb + s * 6;  // xx xy xz yy yz zz
-          acc.x += b[0] * x.x + b[1] * x.y + b[2] * x.z;
-          acc.y += b[1] * x.x + b[3] * x.y + b[4] * x.z;
-          acc.z += b[2] * x.x + b[4] * x.y + b[5] * x.z;
-          if (s == 4 || s == 10 || s == 12 || s == 14 || s == 16 || s == 22) acc += w2 * (vr - x);
+          acc.x += mk * (b[0] * x.x + b[1] * x.y + b[2] * x.z);
+          acc.y += mk * (b[1] * x.x + b[3] * x.y + b[4] * x.z);
+          acc.z += mk * (b[2] * x.x + b[4] * x.y + b[5] * x.z);
+          if (s == 4 || s == 10 || s == 12 || s == 14 || s == 16 || s == 22) acc += (mk * w2) * (vr - x);
         }
       }
 #pragma unroll
