@@ -35,10 +35,6 @@ namespace wfk {
 // setup kernels
 // ============================================================================
 
-__global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
-    p[i] = v;
-}
 
 __global__ void k_scatter_node_row(const int32_t* rows, int N, int32_t* node_row) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x) node_row[rows[r]] = r;
@@ -203,106 +199,6 @@ __global__ void k_item_write(int N, const int32_t* row_ptr, const int32_t* xptr,
     for (int i = x0, k = 1; i < x1; ++i, ++k)
       xitems[i] = make_int4(r, e0 + k * kItemLen, min(e1, e0 + (k + 1) * kItemLen), 0);
     xrange[r] = make_int2(x0, x1 - x0);
-  }
-}
-
-__global__ void k_heavy_flags(int N, const int32_t* row_ptr, uint8_t* flag) {
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x)
-    flag[r] = row_ptr[r + 1] - row_ptr[r] > kHeavyRow ? 1 : 0;
-}
-
-// Cached B^T B of one (row, stencil slot): sum over the row's incidences of
-// coef a_i a_k (g g^T | I) for the anchor k at that slot (solver.cpp:196-226),
-// symmetric 3x3 stored as 6 values; columns follow solver.cpp:149-160.  One
-// warp per (row, slot): lanes stride the row's incidence list (thousands on
-// the coarse levels), fixed shuffle tree.  Stored slot-major (SoA over rows:
-// blk[(slot * 6 + m) * N + row], cols[slot * N + row]) so the thread-per-row
-// stencil loads are coalesced.
-__global__ void k_assemble_btb(Grid g, int N, const int32_t* rows, const int32_t* node_row, const int32_t* row_ptr,
-                               const int32_t* ent_con, const uint8_t* ent_k, const double* ent_w, const double* c_w,
-                               const double* c_g, const int32_t* c_kind, double* blk, int32_t* cols, int soa) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t t = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; t < int64_t(N) * 27; t += warps) {
-    const int r = int(t / 27), s = int(t % 27);
-    const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = s / 9 - 1;
-    double b[6] = {0, 0, 0, 0, 0, 0};
-    for (int e = row_ptr[r] + lane; e < row_ptr[r + 1]; e += 32) {
-      const int ki = ent_k[e];
-      const int ox = (ki & 1) + dx, oy = ((ki >> 1) & 1) + dy, oz = (ki >> 2) + dz;
-      if (ox < 0 || ox > 1 || oy < 0 || oy > 1 || oz < 0 || oz > 1) continue;
-      const int c = ent_con[e];
-      const int k = ox + 2 * oy + 4 * oz;
-      const double sc = c_g[4 * c + 3] * ent_w[e] * c_w[8 * int64_t(c) + k];
-      if (c_kind[c] == WFK_DENSE_PLANE) {
-        const double gx = c_g[4 * c], gy = c_g[4 * c + 1], gz = c_g[4 * c + 2];
-        b[0] += sc * (gx * gx);
-        b[1] += sc * (gx * gy);
-        b[2] += sc * (gx * gz);
-        b[3] += sc * (gy * gy);
-        b[4] += sc * (gy * gz);
-        b[5] += sc * (gz * gz);
-      } else {
-        b[0] += sc * 1.0;
-        b[3] += sc * 1.0;
-        b[5] += sc * 1.0;
-      }
-    }
-#pragma unroll
-    for (int m = 0; m < 6; ++m) b[m] = warp_sum(b[m]);
-    if (lane == 0) {
-      int x, y, z;
-      g.idx3(rows[r], x, y, z);
-      const int col = g.in_grid(x + dx, y + dy, z + dz) ? node_row[g.lin(x + dx, y + dy, z + dz)] : -1;
-      if (soa) {
-        cols[int64_t(s) * N + r] = col;
-        for (int m = 0; m < 6; ++m) blk[(int64_t(s) * 6 + m) * N + r] = b[m];
-      } else {
-        cols[t] = col;
-        for (int m = 0; m < 6; ++m) blk[t * 6 + m] = b[m];
-      }
-    }
-  }
-}
-
-// Same, one thread per (row, slot) in the reference's accumulation order --
-// for levels whose rows carry few incidences.
-__global__ void k_assemble_btb_thread(Grid g, int N, const int32_t* rows, const int32_t* node_row,
-                                      const int32_t* row_ptr, const int32_t* ent_con, const uint8_t* ent_k,
-                                      const double* ent_w, const double* c_w, const double* c_g,
-                                      const int32_t* c_kind, double* blk, int32_t* cols, int soa) {
-  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < int64_t(N) * 27;
-       t += int64_t(gridDim.x) * blockDim.x) {
-    const int s = int(t / N), r = int(t % N);  // slot-major: consecutive threads, consecutive rows
-    const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = s / 9 - 1;
-    double b[6] = {0, 0, 0, 0, 0, 0};
-    for (int e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
-      const int ki = ent_k[e];
-      const int ox = (ki & 1) + dx, oy = ((ki >> 1) & 1) + dy, oz = (ki >> 2) + dz;
-      if (ox < 0 || ox > 1 || oy < 0 || oy > 1 || oz < 0 || oz > 1) continue;
-      const int c = ent_con[e];
-      const int k = ox + 2 * oy + 4 * oz;
-      const double sc = c_g[4 * c + 3] * ent_w[e] * c_w[8 * int64_t(c) + k];
-      if (c_kind[c] == WFK_DENSE_PLANE) {
-        const double gx = c_g[4 * c], gy = c_g[4 * c + 1], gz = c_g[4 * c + 2];
-        b[0] += sc * (gx * gx);
-        b[1] += sc * (gx * gy);
-        b[2] += sc * (gx * gz);
-        b[3] += sc * (gy * gy);
-        b[4] += sc * (gy * gz);
-        b[5] += sc * (gz * gz);
-      } else {
-        b[0] += sc * 1.0;
-        b[3] += sc * 1.0;
-        b[5] += sc * 1.0;
-      }
-    }
-    int x, y, z;
-    g.idx3(rows[r], x, y, z);
-    const int col = g.in_grid(x + dx, y + dy, z + dz) ? node_row[g.lin(x + dx, y + dy, z + dz)] : -1;
-    const int64_t ta = int64_t(r) * 27 + s;
-    cols[soa ? int64_t(s) * N + r : ta] = col;
-    for (int m = 0; m < 6; ++m) blk[soa ? (int64_t(s) * 6 + m) * N + r : ta * 6 + m] = b[m];
   }
 }
 
@@ -617,8 +513,6 @@ struct FFArgs {
   const int32_t* row_ptr;
   const int4* c_pos;     // 2 per constraint: incidence slot of each corner or -1
   double4* contrib;      // E: a_k u_c per incidence slot (row-sorted)
-  const int32_t* heavy;  // rows with more than kHeavyRow incidences
-  int n_heavy;
   const int4* xitems;    // matrix-free extra work items (row, e_begin, e_end)
   int n_xitems;
   const int2* xrange;    // N: first extra item and count of each row
@@ -919,41 +813,13 @@ __device__ __forceinline__ V3 laplacian(const FFArgs& a, const double4* v, int r
   return acc;
 }
 
-// A*v for one row.  Matrix-free: the row's contiguous incidence
-// contributions.  Assembled (levels whose rows carry many constraints): the
-// cached symmetric B^T B blocks of the 27-point stencil (solver.cpp:163-237).
-template <bool ASM>
-__device__ __forceinline__ V3 matvec_row(const FFArgs& a, const double4* v, int r, V3 vr) {
-  if (a.frozen[r]) return vr;
-  V3 acc{0, 0, 0};
-  if (ASM) {
-    const int64_t n = a.N;
-#pragma unroll 9
-    for (int s = 0; s < 27; ++s) {
-      const int col = a.cols[int64_t(s) * n + r];
-      if (col < 0) continue;
-      const V3 x = ld4(v, col);
-      const double* b = a.blk + int64_t(s) * 6 * n + r;  // xx xy xz yy yz zz, stride N
-      acc.x += b[0] * x.x + b[n] * x.y + b[2 * n] * x.z;
-      acc.y += b[n] * x.x + b[3 * n] * x.y + b[4 * n] * x.z;
-      acc.z += b[2 * n] * x.x + b[4 * n] * x.y + b[5 * n] * x.z;
-    }
-  } else {
-    const int e0 = a.row_ptr[r], e1 = a.row_ptr[r + 1];
-#pragma unroll 4
-    for (int e = e0; e < e1; ++e) acc += ld4(a.contrib, e);
-  }
-  return laplacian(a, v, r, vr, acc);
-}
-
-// (A v)_r for every row, delivered once per row to the group leader as
-// sink(r, v_r, (A v)_r).
-//  * Assembled levels: a group of kAsmLanes lanes per row, each lane a few of
-//    the 27 stencil slots (one parallel round of gathers), folding the ARAP
-//    Laplacian into the six face slots, then a sub-warp shuffle tree.
-//  * Matrix-free levels: one thread per light row summing its contiguous
-//    incidence contributions; rows with more than kHeavyRow incidences go to
-//    a whole warp (coalesced 256-bit loads, lanes 0-5 one face neighbour each).
+// Assembled levels: (A v)_r for every row over the 27-slot B^T B stencil,
+// delivered once per row to the group leader as sink(r, v_r, (A v)_r).
+//  * small levels: a group of kAsmLanes lanes per row, each lane a few of the
+//    27 stencil slots (one parallel round of gathers), folding the ARAP
+//    Laplacian into the six face slots, then a sub-warp shuffle tree;
+//  * large levels (asm_rows_on_lanes): one row per lane over slot-major blocks.
+// (Matrix-free levels: row_pass_mf, or item_pass in the Chronopoulos-Gear PCG.)
 template <bool ASM, class Sink, class Sl = std::nullptr_t>
 __device__ __forceinline__ void row_pass(const FFArgs& a, const double4* v, Sink& sink, int skip = 0,
                                          const Sl* sl = nullptr, const double* smb = nullptr,
@@ -1041,27 +907,6 @@ __device__ __forceinline__ void row_pass(const FFArgs& a, const double4* v, Sink
       }
       if (live && sub == 0) sink(r, vr, frozen ? vr : acc);
     }
-    return;
-  }
-  for (int r = int(gtid()); r < a.N; r += int(gstride())) {
-    if (a.row_ptr[r + 1] - a.row_ptr[r] > kHeavyRow) continue;
-    const V3 vr = ld4(v, r);
-    sink(r, vr, matvec_row<false>(a, v, r, vr));
-  }
-  for (int h = gwarp(); h < a.n_heavy; h += nwarps()) {
-    const int r = a.heavy[h];
-    const int e0 = a.row_ptr[r], e1 = a.row_ptr[r + 1];
-    const V3 vr = ld4(v, r);
-    V3 acc{0, 0, 0};
-    for (int e = e0 + lane; e < e1; e += 32) acc += ld4(a.contrib, e);
-    if (lane < 6) {
-      const int j = a.nbr[int64_t(lane) * a.N + r];
-      if (j >= 0) acc += w2 * (vr - ld4(v, j));
-    }
-    acc.x = warp_sum(acc.x);
-    acc.y = warp_sum(acc.y);
-    acc.z = warp_sum(acc.z);
-    if (lane == 0) sink(r, vr, a.frozen[r] ? vr : acc);
   }
 }
 
@@ -2241,7 +2086,6 @@ static void level_constraints(wfk_ctx* c, Level& L, const PoseD& pose, const wfk
   // assembled once per solve, so the PCG row pass is a fixed 27-block stencil;
   // the same pass produces their constraint cache.
   L.assembled = E8 > int64_t(kAssembleRatio) * N;
-  L.n_heavy = 0;
   L.n_xitems = 0;
   if (!L.assembled) {
     L.contrib.ensure(size_t(std::max<int64_t>(E8, 1)));
@@ -2398,8 +2242,6 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   a.row_ptr = L.row_ptr;
   a.c_pos = reinterpret_cast<const int4*>(L.c_pos.p);
   a.contrib = L.contrib;
-  a.heavy = L.heavy;
-  a.n_heavy = L.n_heavy;
   a.xitems = L.xitems;
   a.n_xitems = L.n_xitems;
   a.xrange = L.xrange;
@@ -2535,8 +2377,8 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
     const char* names_cg[8] = {"A", "Async", "B", "red-", "U", "Usync", "redblk", "redsync"};
     const char* names_pipe[8] = {"A", "Abar", "B", "-", "U", "-", "wait", "bar"};
     const char* const* names = a.pcg_variant == 0 ? names_pipe : names_cg;
-    fprintf(stderr, "[wfk phase] level %d N %d C %lld asm %d heavy %d iters %.0f | cycles/iter mean/max:", level_tag,
-            L.N, (long long)L.C, int(L.assembled), L.n_heavy, it);
+    fprintf(stderr, "[wfk phase] level %d N %d C %lld asm %d iters %.0f | cycles/iter mean/max:", level_tag, L.N,
+            (long long)L.C, int(L.assembled), it);
     for (int k = 0; k < 8; ++k) {
       double m, x;
       stat(k, m, x);

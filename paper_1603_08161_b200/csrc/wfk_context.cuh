@@ -115,8 +115,6 @@ struct Level {
   DevBuf<uint8_t> ent_k;   // corner of the row inside each incident constraint
   DevBuf<int32_t> c_pos;   // 8C: incidence slot of (constraint, corner), -1 if none
   DevBuf<double4> contrib; // E: per-incidence matvec contributions
-  DevBuf<int32_t> heavy;   // rows summed by a whole warp
-  int n_heavy = 0;
   DevBuf<int4> xitems;     // extra work items of the balanced matrix-free row pass
   DevBuf<int32_t> xptr;
   DevBuf<int2> xrange;
