@@ -148,6 +148,42 @@ typedef struct wfk_correspond_params {
   double eps_d, eps_n, eps_v;
 } wfk_correspond_params;
 
+/* wf::FeatureParams (features.hpp:29-45) */
+typedef struct wfk_feature_params {
+  int32_t octaves;          /* 4 */
+  int32_t dog_levels;       /* 3 */
+  double sigma0;            /* 1.6 */
+  double contrast_threshold;/* 0.01 */
+  double edge_ratio;        /* 10 */
+  int32_t max_keypoints;    /* 150 */
+  int32_t max_orientations; /* 2 */
+  double orientation_peak_ratio; /* 0.8 */
+  int32_t max_candidates;   /* 128 */
+  int32_t keep_best;        /* 64 */
+  double tau_descriptor;    /* 0.7 */
+  double tau_pixels;        /* 48 */
+  double tau_3d;            /* 0.10 */
+} wfk_feature_params;
+
+/* wf::Feature (features.hpp:13-22) */
+typedef struct wfk_feature {
+  double canonical_pos[3];
+  double world_pos[3];
+  double pixel[2];
+  double scale;
+  double orientation;
+  float descriptor[128];
+  int32_t frame_id;
+  int32_t reserved_;
+} wfk_feature;
+
+/* wf::FeatureMatch (features.hpp) */
+typedef struct wfk_feature_match {
+  int32_t source_id;  /* store index */
+  int32_t target_id;  /* current-frame feature index */
+  double distance;
+} wfk_feature_match;
+
 /* wf::IcpParams (solver.hpp:121-131) */
 typedef struct wfk_icp_params {
   wfk_correspond_params corr;   /* the pipeline copies its CorrespondenceParams in (pipeline.cpp:176) */

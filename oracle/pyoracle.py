@@ -11,7 +11,8 @@ import subprocess
 import numpy as np
 
 from paper_1603_08161_b200.abi import (
-    CORR_DTYPE, CorrespondParams, Energy, ExpansionStats, FusionParams, FusionStats,
+    CORR_DTYPE, FEATURE_DTYPE, MATCH_DTYPE, CorrespondParams, Energy, ExpansionStats, FeatureParams, FusionParams,
+    FusionStats,
     GeometryBufferView, IcpParams, IcpResult, Intrinsics, MeshView, PcgResult, PointNormalMapView, Pose,
     SolverParams, TraceEntry, VolumeView, FrameView, Volume, ptr, trace_to_list,
     WFK_OK, WFK_E_CAPACITY, WFK_E_INVALID_ARG, WFK_E_OUT_OF_RANGE, WFK_E_LOGIC,
@@ -370,6 +371,52 @@ def estimate_global_pose(buf, maps, intr, vol, initial=None, params=None) -> Icp
     _check(lib().wfo_estimate_global_pose(C.byref(bv), C.byref(mv), C.byref(intr), C.byref(vv), C.byref(ini),
                                           C.byref(p), C.byref(res)))
     return res
+
+
+# --- feature front-end (features.cpp) ---------------------------------------------
+def detect_features(frame, params=None):
+    """build_pyramid + detect_keypoints + extract_descriptors of a frame
+    (pipeline.cpp:97-101); returns (features[FEATURE_DTYPE], n_keypoints)."""
+    p = params or FeatureParams.make()
+    cap = 4 * max(p.max_keypoints, 1)
+    out = np.zeros(cap, FEATURE_DTYPE)
+    n = C.c_int32()
+    nk = C.c_int32()
+    fv = frame.view()
+    _check(lib().wfo_detect_features(C.byref(fv), C.byref(p), _cptr(out), C.c_int32(cap), C.byref(n), C.byref(nk)))
+    return out[: n.value].copy(), nk.value
+
+
+def pyramid_level(frame, o, l, dog=False, params=None):
+    p = params or FeatureParams.make()
+    w, h = C.c_int32(), C.c_int32()
+    fv = frame.view()
+    _check(lib().wfo_pyramid_level(C.byref(fv), C.byref(p), o, l, int(dog), None, C.byref(w), C.byref(h)))
+    out = np.zeros((h.value, w.value), np.float32)
+    _check(lib().wfo_pyramid_level(C.byref(fv), C.byref(p), o, l, int(dog), _cptr(out), C.byref(w), C.byref(h)))
+    return out
+
+
+def descriptor_distance(a, b):
+    a = np.ascontiguousarray(a, np.float32)
+    b = np.ascontiguousarray(b, np.float32)
+    lib().wfo_descriptor_distance.restype = C.c_double
+    return lib().wfo_descriptor_distance(ptr(a, C.c_float), ptr(b, C.c_float))
+
+
+def match_features(current, store, predicted_world, intr, params=None):
+    """match_features (features.cpp:416-433)."""
+    p = params or FeatureParams.make()
+    cur = np.ascontiguousarray(current, FEATURE_DTYPE)
+    st = np.ascontiguousarray(store, FEATURE_DTYPE)
+    pw = np.ascontiguousarray(predicted_world, np.float64).reshape(-1, 3)
+    cap = max(len(st), 1)
+    out = np.zeros(cap, MATCH_DTYPE)
+    n = C.c_int32()
+    _check(lib().wfo_match_features(_cptr(cur), C.c_int32(len(cur)), _cptr(st), C.c_int32(len(st)),
+                                    ptr(pw, C.c_double), C.byref(intr), C.byref(p), _cptr(out), C.c_int32(cap),
+                                    C.byref(n)))
+    return out[: n.value].copy()
 
 
 def invert_warp(vol, pose, y, seed, max_iters=20, tol=1e-6):

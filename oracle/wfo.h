@@ -94,6 +94,16 @@ int wfo_find_dense_correspondences(const wfk_geometry_buffer* buf,
 int wfo_estimate_global_pose(const wfk_geometry_buffer* buf, const wfk_point_normal_map* maps,
                              const wfk_intrinsics* intr, const wfk_volume_view* v, const wfk_pose* initial,
                              const wfk_icp_params* params, wfk_icp_result* out);
+/* feature front-end (features.cpp, wf_features.cpp) */
+int wfo_detect_features(const wfk_frame_view* frame, const wfk_feature_params* p, wfk_feature* out, int32_t cap,
+                        int32_t* n_out, int32_t* n_keypoints);
+int wfo_pyramid_level(const wfk_frame_view* frame, const wfk_feature_params* p, int32_t o, int32_t l,
+                      int32_t dog, float* out, int32_t* w_out, int32_t* h_out);
+double wfo_descriptor_distance(const float* a, const float* b);
+int wfo_match_features(const wfk_feature* cur, int32_t nc, const wfk_feature* store, int32_t ns,
+                       const double* predicted_world, const wfk_intrinsics* K, const wfk_feature_params* p,
+                       wfk_feature_match* out, int32_t cap, int32_t* n_out);
+
 /* DeformableVolume::invert_warp (volume.cpp:95-126) for n points; x = 0, ok = 0 on failure */
 int wfo_invert_warp(const wfk_volume_view* v, const wfk_pose* pose, int64_t n, const double* y, const double* seed,
                     int32_t max_iters, double tol, double* x, uint8_t* ok);

@@ -144,6 +144,31 @@ class CorrespondParams(C.Structure):
         return CorrespondParams(eps_d, eps_n, eps_v)
 
 
+class FeatureParams(C.Structure):
+    """wf::FeatureParams (features.hpp:29-45)."""
+    _fields_ = [("octaves", C.c_int32), ("dog_levels", C.c_int32), ("sigma0", C.c_double),
+                ("contrast_threshold", C.c_double), ("edge_ratio", C.c_double), ("max_keypoints", C.c_int32),
+                ("max_orientations", C.c_int32), ("orientation_peak_ratio", C.c_double),
+                ("max_candidates", C.c_int32), ("keep_best", C.c_int32), ("tau_descriptor", C.c_double),
+                ("tau_pixels", C.c_double), ("tau_3d", C.c_double)]
+
+    @staticmethod
+    def make(**kw) -> "FeatureParams":
+        d = dict(octaves=4, dog_levels=3, sigma0=1.6, contrast_threshold=0.01, edge_ratio=10.0, max_keypoints=150,
+                 max_orientations=2, orientation_peak_ratio=0.8, max_candidates=128, keep_best=64,
+                 tau_descriptor=0.7, tau_pixels=48.0, tau_3d=0.10)
+        d.update(kw)
+        return FeatureParams(**d)
+
+
+# wf::Feature (features.hpp:13-22)
+FEATURE_DTYPE = np.dtype([("canonical_pos", np.float64, 3), ("world_pos", np.float64, 3), ("pixel", np.float64, 2),
+                          ("scale", np.float64), ("orientation", np.float64), ("descriptor", np.float32, 128),
+                          ("frame_id", np.int32), ("reserved_", np.int32)])
+# wf::FeatureMatch
+MATCH_DTYPE = np.dtype([("source_id", np.int32), ("target_id", np.int32), ("distance", np.float64)])
+
+
 class IcpParams(C.Structure):
     """wf::IcpParams (solver.hpp:121-131)."""
     _fields_ = [("corr", CorrespondParams), ("max_iters", C.c_int32), ("min_correspondences", C.c_int32),
