@@ -152,6 +152,19 @@ int wfk_find_dense_correspondences(wfk_ctx* ctx, const wfk_intrinsics* intr,
 int wfk_constraints_append(wfk_ctx* ctx, const wfk_correspondence* c, int64_t n,
                            int32_t drop_inactive, int64_t* kept);
 
+/* ---- feature front-end (features.hpp, features.cpp:12-433) ------------------------
+ * build_pyramid + detect_keypoints + extract_descriptors of the uploaded (or
+ * staged) frame's color and depth, as Reconstructor::add_features / the sparse
+ * term compute them (pipeline.cpp:97-101, 187-193): features with pixel, scale,
+ * orientation and descriptor (positions and frame id are left 0 / -1).  A frame
+ * without color or below 64x64 yields none.  n_keypoints = detect_keypoints'
+ * count before descriptors drop flat / border patches. */
+int wfk_detect_features(wfk_ctx* ctx, const wfk_feature_params* p, wfk_feature* out, int32_t cap,
+                        int32_t* n_out, int32_t* n_keypoints);
+/* one level of the last detection's pyramid (octave o, gaussian level l or DoG level l) */
+int wfk_feature_pyramid_level(wfk_ctx* ctx, int32_t octave, int32_t level, int32_t dog, float* out,
+                              int32_t* width, int32_t* height);
+
 /* ---- batched warp inversion ------------------------------------------------------
  * DeformableVolume::invert_warp (volume.hpp:89-94, volume.cpp:95-126) for n points
  * (host arrays, 3n doubles each): canonical x with warp_point(pose, x) == y from

@@ -674,6 +674,22 @@ void run_frame(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose* pose_in, con
 
 extern "C" {
 
+int wfk_detect_features(wfk_ctx* c, const wfk_feature_params* p, wfk_feature* out, int32_t cap, int32_t* n_out,
+                        int32_t* n_keypoints) {
+  return guard(c, [&] {
+    if (!p || !n_out) throw Error(WFK_E_INVALID_ARG, "null argument");
+    features_detect(c, *p, out, cap, n_out, n_keypoints);
+  });
+}
+
+int wfk_feature_pyramid_level(wfk_ctx* c, int32_t octave, int32_t level, int32_t dog, float* out, int32_t* width,
+                              int32_t* height) {
+  return guard(c, [&] {
+    if (!width || !height) throw Error(WFK_E_INVALID_ARG, "null argument");
+    features_level(c, octave, level, dog, out, width, height);
+  });
+}
+
 int wfk_invert_warp(wfk_ctx* c, const wfk_pose* pose, int64_t n, const double* y, const double* seed,
                     int32_t max_iters, double tol, double* x, uint8_t* ok) {
   return guard(c, [&] {

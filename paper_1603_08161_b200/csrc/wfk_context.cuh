@@ -191,6 +191,22 @@ struct GBufDev {
 
 constexpr int kMaxLevels = 8;
 
+// feature front-end scratch (features.cu)
+constexpr int kFeatOctaves = 8, kFeatLevels = 16;
+struct FeatDev {
+  DevBuf<float> levels[kFeatOctaves][kFeatLevels];  // per octave: L + 1 gaussian, then L DoG levels
+  int L = 0;
+  std::vector<int> ws, hs;
+  DevBuf<float> gray, tmp, base;
+  DevBuf<uint8_t> flag, ok, kp, cur_raw;
+  DevBuf<int32_t> pos, idx, nori, cnt;
+  DevBuf<int4> ext;
+  DevBuf<uint32_t> key;
+  DevBuf<double> ori;
+  std::vector<wfk_feature> host_cur;  // the last detection's features
+  int32_t n_cur = 0;
+};
+
 struct Stats {
   int64_t pcg_iterations = 0;
   int64_t kernel_launches = 0;
@@ -225,6 +241,7 @@ struct wfk_ctx {
   wfk::FrameDev frame;
   wfk::MeshDev mesh;
   wfk::GBufDev gbuf;
+  wfk::FeatDev feat;
   wfk::Stats stats;
   wfk::Prof prof;
   // frames staged in device memory (wfk_frame_stage)

@@ -31,6 +31,9 @@ void assoc_extract_mesh(wfk_ctx* c, const wfk_pose* pose, int64_t* nv, int64_t* 
 void assoc_mesh_warp(wfk_ctx* c, const wfk_pose* pose);
 void assoc_compute_normals(wfk_ctx* c);
 void assoc_rasterize(wfk_ctx* c, const wfk_intrinsics& K, wfk_geometry_buffer* out);
+void features_detect(wfk_ctx* c, const wfk_feature_params& p, wfk_feature* out, int32_t cap, int32_t* n_out,
+                     int32_t* n_kp_out);
+void features_level(wfk_ctx* c, int o, int l, int dog, float* out, int32_t* w, int32_t* h);
 void volume_invert_warp(wfk_ctx* c, const wfk_pose* pose, int64_t n, const double* y, const double* seed,
                         int32_t max_iters, double tol, double* x, uint8_t* ok);
 void assoc_estimate_pose(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose& initial, const wfk_icp_params& prm,

@@ -15,7 +15,7 @@ import subprocess
 
 import numpy as np
 
-from .abi import (CORR_DTYPE, CorrespondParams, Energy, ExpansionStats, FrameView, FusionParams,
+from .abi import (CORR_DTYPE, FEATURE_DTYPE, MATCH_DTYPE, FeatureParams, CorrespondParams, Energy, ExpansionStats, FrameView, FusionParams,
                   FusionStats, GeometryBufferView, IcpParams, IcpResult, Intrinsics, MeshView, PcgResult,
                   PointNormalMapView, Pose, SolverParams, TraceEntry, Volume, VolumeView, ptr,
                   trace_to_list, VOL_ALL, WFK_OK)
@@ -373,6 +373,24 @@ class Context:
                                             C.c_int64(0 if s is None else len(s)), C.c_int32(frame_index),
                                             C.byref(rec)))
         return rec
+
+    def detect_features(self, params=None):
+        """build_pyramid + detect_keypoints + extract_descriptors of the uploaded frame;
+        returns (features[FEATURE_DTYPE], n_keypoints)."""
+        p = params or FeatureParams.make()
+        cap = 4 * max(p.max_keypoints, 1)
+        out = np.zeros(cap, FEATURE_DTYPE)
+        n, nk = C.c_int32(), C.c_int32()
+        self._check(lib().wfk_detect_features(self.h, C.byref(p), _cptr(out), C.c_int32(cap), C.byref(n),
+                                              C.byref(nk)))
+        return out[: n.value].copy(), nk.value
+
+    def feature_pyramid_level(self, o, l, dog=False):
+        w, h = C.c_int32(), C.c_int32()
+        self._check(lib().wfk_feature_pyramid_level(self.h, o, l, int(dog), None, C.byref(w), C.byref(h)))
+        out = np.zeros((h.value, w.value), np.float32)
+        self._check(lib().wfk_feature_pyramid_level(self.h, o, l, int(dog), _cptr(out), C.byref(w), C.byref(h)))
+        return out
 
     def invert_warp(self, pose: Pose, y, seed, max_iters=20, tol=1e-6):
         """DeformableVolume::invert_warp (volume.cpp:95-126) for each row; returns (x, ok)."""

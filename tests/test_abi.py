@@ -45,7 +45,7 @@ STRUCTS = {
     "wfk_point_normal_map": abi.PointNormalMapView, "wfk_geometry_buffer": abi.GeometryBufferView,
     "wfk_mesh_view": abi.MeshView, "wfk_pipeline_config": wfk.PipelineConfig,
     "wfk_frame_record": wfk.FrameRecord, "wfk_synth_scene": wfk.SynthScene, "wfk_config": wfk.Config,
-    "wfk_icp_params": abi.IcpParams, "wfk_icp_result": abi.IcpResult,
+    "wfk_icp_params": abi.IcpParams, "wfk_icp_result": abi.IcpResult, "wfk_feature_params": abi.FeatureParams,
     "wfk_ne_host": wfk.NeHost, "wfk_profile": wfk.Profile,
 }
 
@@ -57,6 +57,8 @@ def test_struct_layouts_match_c(tmp_path):
         for f, _ in st._fields_:
             src.append(f'  printf("{name}.{f} %zu\\n", offsetof({name}, {f}));')
     src.append('  printf("wfk_correspondence %zu\\n", sizeof(wfk_correspondence));')
+    src.append('  printf("wfk_feature %zu\\n", sizeof(wfk_feature));')
+    src.append('  printf("wfk_feature_match %zu\\n", sizeof(wfk_feature_match));')
     for f in abi.CORR_DTYPE.names:
         src.append(f'  printf("wfk_correspondence.{f} %zu\\n", offsetof(wfk_correspondence, {f}));')
     src.append("  return 0; }")
@@ -71,6 +73,8 @@ def test_struct_layouts_match_c(tmp_path):
         for f, _ in st._fields_:
             assert int(got[f"{name}.{f}"]) == getattr(st, f).offset, f"{name}.{f}"
     assert int(got["wfk_correspondence"]) == abi.CORR_DTYPE.itemsize
+    assert int(got["wfk_feature"]) == abi.FEATURE_DTYPE.itemsize
+    assert int(got["wfk_feature_match"]) == abi.MATCH_DTYPE.itemsize
     for f in abi.CORR_DTYPE.names:
         assert int(got[f"wfk_correspondence.{f}"]) == abi.CORR_DTYPE.fields[f][1], f
 
