@@ -9,9 +9,10 @@ deforming sphere (r 0.3 m at z 1.2 m, bend 2.0 rad/m oscillating with
 frequency 2 over a 300-frame sequence).  One step = one
 Reconstructor::process_frame (pipeline.cpp:143-262) with the reference's
 default solver / correspondence / fusion parameters and 3 re-associations.
-The global-pose ICP runs before the solve as in the reference's default
-configuration (config.hpp:45, pipeline.cpp:174-183); the SIFT feature front-end
-is outside the scope of this path and off in both arms.
+The global-pose ICP runs before the solve and the feature front-end (DoG
+detection, matching against the FeatureStore, sparse constraints, store
+update) runs around it, as in the reference's default configuration
+(config.hpp:44-45, pipeline.cpp:95-141, 174-217, 257) -- on in both arms.
 
   python bench.py [--gpus N --steps K --warmup W]        B200 arm (libwfk.so)
   python bench.py --impl reference [...]                  CPU arm (the oracle port)
@@ -67,7 +68,7 @@ def workload_config(n_gpus):
         "levels": 3, "flip_flop_iters": 4, "pcg_tol": 1e-4, "pcg_max_iters": 50, "reassociations": 3,
         "scene": "sphere r=0.3 m @ z=1.2 m, bend 2.0 rad/m, oscillating freq 2 over 300 frames",
         "icp": "on (global-pose ICP before the solve, config.hpp:45 default)",
-        "sparse_features": "off (front-end out of scope)",
+        "sparse_features": "on (DoG features matched against the feature store, config.hpp:44 default)",
         "l2": "flushed (256 MB write) before every timed frame",
         "parallelism": f"replicas x{n_gpus}" if n_gpus > 1 else "single GPU",
     }
@@ -256,11 +257,12 @@ def run_b200(args):
     for f in range(1, 1 + args.warmup):
         pose = ctx.process_staged_frame(f, pose, cfg, f).pose  # the Reconstructor's pose_, refined by ICP
 
-    # checkpoint (volume + pose) so the e2e pass repeats exactly the same K frames
+    # checkpoint (volume + pose + feature store) so the e2e pass repeats exactly the same K frames
     log("warm-up done")
     ckpt = Volume(dims, voxel, origin)
     ctx.download_volume(ckpt)
     ckpt_pose = pose
+    ckpt_store = ctx.feature_store()
     timed = list(range(1 + args.warmup, n_frames))
 
     # ---- value: inputs resident in HBM ---------------------------------------
@@ -285,6 +287,7 @@ def run_b200(args):
     log(f"timed: {total_ms / len(timed):.3f} ms/frame")
     # ---- e2e: same frames through the public call with host buffers -----------
     ctx.upload_volume(ckpt)
+    ctx.set_feature_store(ckpt_store)
     pose = ckpt_pose
     e2e_ms = 0.0
     d.barrier()
@@ -334,6 +337,9 @@ def run_b200(args):
             "pcg_iterations_per_frame": pcg_iters / k,
             "frame_breakdown_ms": {kk: v / k for kk, v in prof.as_dict()["stage_ms"].items()},
             "dense_constraints_per_frame": float(np.mean([r.dense_count for r in recs])),
+            "sparse_constraints_per_frame": float(np.mean([r.sparse_count for r in recs])),
+            "feature_matches_per_frame": float(np.mean([r.match_count for r in recs])),
+            "feature_store_size": int(len(ctx.feature_store())),
             "gpu_launches": int(launches),
             "roofline": {
                 "bound": "hbm",

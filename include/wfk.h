@@ -164,6 +164,18 @@ int wfk_detect_features(wfk_ctx* ctx, const wfk_feature_params* p, wfk_feature* 
 /* one level of the last detection's pyramid (octave o, gaussian level l or DoG level l) */
 int wfk_feature_pyramid_level(wfk_ctx* ctx, int32_t octave, int32_t level, int32_t dog, float* out,
                               int32_t* width, int32_t* height);
+/* match_features (features.cpp:354-433; replaces features.hpp:106-110): the store
+ * grouped by frame id (ascending), per group mutual-best matching of descriptors,
+ * the max_candidates cap, the (distance, source id) sort, keep_best and the
+ * descriptor / reprojection / 3-D prune.  predicted = 3 doubles per store entry
+ * (z <= 0: no prediction).  Host arrays; computed on the device. */
+int wfk_match_features(wfk_ctx* ctx, const wfk_feature* current, int32_t n_current, const wfk_feature* store,
+                       int32_t n_store, const double* predicted, const wfk_intrinsics* intr,
+                       const wfk_feature_params* p, wfk_feature_match* out, int32_t cap, int32_t* n_out);
+/* the context's FeatureStore (features.hpp:79-95): filled by wfk_process_frame
+ * when cfg->use_features; upload replaces it (FeatureStore::load / resume). */
+int wfk_feature_store_upload(wfk_ctx* ctx, const wfk_feature* in, int64_t n);
+int wfk_feature_store_download(wfk_ctx* ctx, wfk_feature* out, int64_t cap, int64_t* n_out);
 
 /* ---- batched warp inversion ------------------------------------------------------
  * DeformableVolume::invert_warp (volume.hpp:89-94, volume.cpp:95-126) for n points
@@ -183,8 +195,10 @@ int wfk_invert_warp(wfk_ctx* ctx, const wfk_pose* pose, int64_t n, const double*
 int wfk_estimate_global_pose(wfk_ctx* ctx, const wfk_intrinsics* intr, const wfk_pose* initial,
                              const wfk_icp_params* params, wfk_icp_result* out);
 
-/* ---- per-frame hot path (Reconstructor::process_frame, pipeline.cpp:143-262,
- * without the feature front-end; sparse constraints may be passed in) --------- */
+/* ---- per-frame hot path (Reconstructor::process_frame, pipeline.cpp:143-262) --
+ * With use_features the feature front-end runs on the device against the
+ * context's FeatureStore (pipeline.cpp:95-141, 185-217); caller-supplied sparse
+ * constraints are appended after the feature ones. */
 typedef struct wfk_pipeline_config {
   wfk_solver_params solver;
   wfk_correspond_params correspond;
@@ -192,6 +206,9 @@ typedef struct wfk_pipeline_config {
   int32_t reassociations;
   int32_t estimate_pose;  /* global ICP before the solve (config.hpp:45, default on) */
   wfk_icp_params icp;     /* its corr is replaced by `correspond` (pipeline.cpp:176) */
+  int32_t use_features;   /* sparse feature term + feature store (config.hpp:44, default on) */
+  int32_t reserved_;
+  wfk_feature_params features;
 } wfk_pipeline_config;
 
 typedef struct wfk_frame_record {
@@ -208,9 +225,11 @@ typedef struct wfk_frame_record {
   int32_t icp_degraded;    /* FrameRecord::icp_degraded */
   int32_t icp_iterations;
   double icp_rms;          /* FrameRecord::icp_rms */
+  int32_t match_count;     /* FrameRecord::match_count */
+  int32_t features_added;  /* FrameRecord::features_added */
 } wfk_frame_record;
 
-/* frame_index 0 bootstraps (pipeline.cpp:150-159).  sparse may be NULL.  `pose`
+/* frame_index 0 bootstraps (pipeline.cpp:150-159) and empties the feature store.  sparse may be NULL.  `pose`
  * is the pose entering the frame (the Reconstructor's pose_); the frame's pose,
  * refined by ICP when cfg->estimate_pose, is returned in rec->pose. */
 int wfk_process_frame(wfk_ctx* ctx, const wfk_frame_view* frame, const wfk_pose* pose,

@@ -527,7 +527,8 @@ class ReconConfig(C.Structure):
     _fields_ = [("dims", C.c_int32 * 3), ("reassociations", C.c_int32), ("voxel_size", C.c_double),
                 ("origin", C.c_double * 3), ("solver", SolverParams), ("correspond", CorrespondParams),
                 ("fusion", FusionParams), ("estimate_pose", C.c_int32), ("reserved_", C.c_int32),
-                ("icp", IcpParams)]
+                ("icp", IcpParams), ("use_features", C.c_int32), ("reserved2_", C.c_int32),
+                ("features", FeatureParams)]
 
 
 class FrameRecord(C.Structure):
@@ -535,12 +536,12 @@ class FrameRecord(C.Structure):
                 ("anomalies", C.c_int32), ("trace_len", C.c_int32), ("pcg_iterations", C.c_int32),
                 ("reserved_", C.c_int32), ("fusion", FusionStats), ("expansion", ExpansionStats),
                 ("pose", Pose), ("icp_degraded", C.c_int32), ("icp_iterations", C.c_int32),
-                ("icp_rms", C.c_double)]
+                ("icp_rms", C.c_double), ("match_count", C.c_int32), ("features_added", C.c_int32)]
 
 
 class Reconstructor:
     def __init__(self, dims, voxel, origin, solver=None, correspond=None, fusion=None, reassociations=3,
-                 estimate_pose=True, icp=None):
+                 estimate_pose=True, icp=None, use_features=True, features=None):
         cfg = ReconConfig()
         cfg.dims[:] = list(dims)
         cfg.voxel_size = voxel
@@ -551,6 +552,8 @@ class Reconstructor:
         cfg.fusion = fusion or FusionParams.make()
         cfg.estimate_pose = 1 if estimate_pose else 0
         cfg.icp = icp or IcpParams.make()
+        cfg.use_features = 1 if use_features else 0
+        cfg.features = features or FeatureParams.make()
         self.cfg = cfg
         h = C.c_void_p()
         _check(lib().wfo_recon_create(C.byref(cfg), C.byref(h)))
@@ -575,6 +578,13 @@ class Reconstructor:
                     color=arr(v.color, (n, 3), np.float32), deformed=arr(v.deformed, (n, 3), np.float64),
                     euler=arr(v.euler, (n, 3), np.float64), age=arr(v.age, (n,), np.int32),
                     active=arr(v.active, (n,), np.uint8))
+
+    def feature_store(self):
+        n = C.c_int64()
+        _check(lib().wfo_recon_feature_store(self.h, None, C.c_int64(0), C.byref(n)))
+        out = np.zeros(max(n.value, 1), FEATURE_DTYPE)
+        _check(lib().wfo_recon_feature_store(self.h, _cptr(out), C.c_int64(len(out)), C.byref(n)))
+        return out[: n.value].copy()
 
     def process_frame(self, frame, sparse=None) -> FrameRecord:
         rec = FrameRecord()

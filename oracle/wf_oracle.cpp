@@ -2309,7 +2309,107 @@ struct wfo_recon {
   std::vector<double> pt, nr, bp, bn, bc;
   std::vector<uint8_t> pv, nv;
   std::vector<float> bd;
+  std::vector<wfk_feature> store;  // FeatureStore (features.hpp:79-95)
 };
+
+namespace {
+// build_pyramid + detect_keypoints + extract_descriptors of the frame (pipeline.cpp:97-101)
+std::vector<wfk_feature> detect_frame(const wfk_frame_view* frame, const wfk_feature_params& p) {
+  std::vector<wfk_feature> out(4096);
+  int32_t n = 0;
+  int rc = wfo_detect_features(frame, &p, out.data(), int32_t(out.size()), &n, nullptr);
+  if (rc == WFK_E_CAPACITY) {
+    out.resize(size_t(n));
+    rc = wfo_detect_features(frame, &p, out.data(), int32_t(out.size()), &n, nullptr);
+  }
+  out.resize(size_t(n));
+  return out;
+}
+
+// Reconstructor::add_features (pipeline.cpp:95-141)
+int add_features(wfo_recon* r, const wfk_frame_view* frame, const Maps& maps, int frame_index, const GBuf* buffer) {
+  if (!frame->color) return 0;
+  const Vol& vol = r->vol;
+  auto features = detect_frame(frame, r->cfg.features);
+  int added = 0;
+  for (wfk_feature& f : features) {
+    const int px = int(std::lround(f.pixel[0])), py = int(std::lround(f.pixel[1]));
+    if (px < 0 || py < 0 || px >= maps.w || py >= maps.h) continue;
+    const size_t idx = maps.idx(px, py);
+    if (!maps.pv[idx]) continue;
+    const V3 w = maps.P(idx);
+    V3 can = w;  // bootstrap frame: the warp is the identity
+    if (buffer) {
+      V3 seed;
+      bool have = false;
+      for (int rr = 0; rr <= 4 && !have; ++rr)
+        for (int dy = -rr; dy <= rr && !have; ++dy)
+          for (int dx = -rr; dx <= rr && !have; ++dx) {
+            const int sx = px + dx, sy = py + dy;
+            if (sx < 0 || sy < 0 || sx >= buffer->w || sy >= buffer->h) continue;
+            if (!std::isfinite(buffer->depth[buffer->idx(sx, sy)])) continue;
+            seed = buffer->get(buffer->canonical, buffer->idx(sx, sy));
+            have = true;
+          }
+      if (!have) continue;
+      if (!invert_warp(vol, r->pose, w, seed, 20, 1e-6, can) || !vol.contains(can)) continue;
+    }
+    if (!vol.contains(can)) continue;
+    f.world_pos[0] = w.x; f.world_pos[1] = w.y; f.world_pos[2] = w.z;
+    f.canonical_pos[0] = can.x; f.canonical_pos[1] = can.y; f.canonical_pos[2] = can.z;
+    f.frame_id = frame_index;
+    r->store.push_back(f);
+    ++added;
+  }
+  return added;
+}
+
+// the sparse term against the full history (pipeline.cpp:185-217)
+std::vector<Con> feature_constraints(wfo_recon* r, const wfk_frame_view* frame, const Maps& maps, int* match_count) {
+  const Vol& vol = r->vol;
+  auto current = detect_frame(frame, r->cfg.features);
+  for (wfk_feature& f : current) {
+    const int px = int(std::lround(f.pixel[0])), py = int(std::lround(f.pixel[1]));
+    V3 w{0, 0, -1};  // invalid, pruned by matching
+    if (px >= 0 && py >= 0 && px < maps.w && py < maps.h && maps.pv[maps.idx(px, py)]) w = maps.P(maps.idx(px, py));
+    f.world_pos[0] = w.x; f.world_pos[1] = w.y; f.world_pos[2] = w.z;
+  }
+  const size_t ns = r->store.size();
+  std::vector<double> pred(3 * ns);
+  for (size_t i = 0; i < ns; ++i) {
+    const V3 c{r->store[i].canonical_pos[0], r->store[i].canonical_pos[1], r->store[i].canonical_pos[2]};
+    const V3 p = vol.contains(c) ? vol.warp_point(r->pose, c) : V3{0, 0, -1};
+    pred[3 * i] = p.x; pred[3 * i + 1] = p.y; pred[3 * i + 2] = p.z;
+  }
+  std::vector<wfk_feature_match> m(ns * 64 + 64);
+  int32_t nm = 0;
+  int rc = wfo_match_features(current.data(), int32_t(current.size()), r->store.data(), int32_t(ns), pred.data(),
+                              &frame->intrinsics, &r->cfg.features, m.data(), int32_t(m.size()), &nm);
+  if (rc == WFK_E_CAPACITY) {
+    m.resize(size_t(nm));
+    wfo_match_features(current.data(), int32_t(current.size()), r->store.data(), int32_t(ns), pred.data(),
+                       &frame->intrinsics, &r->cfg.features, m.data(), int32_t(m.size()), &nm);
+  }
+  *match_count = nm;
+  std::vector<Con> out;  // sparse_to_constraints (correspond.cpp:152-169)
+  for (int i = 0; i < nm; ++i) {
+    const wfk_feature& cf = current[size_t(m[size_t(i)].target_id)];
+    if (cf.world_pos[2] <= 0) continue;
+    const wfk_feature& sf = r->store[size_t(m[size_t(i)].source_id)];
+    const V3 x{sf.canonical_pos[0], sf.canonical_pos[1], sf.canonical_pos[2]};
+    if (!vol.contains(x)) continue;
+    Con c;
+    c.dense = false;
+    c.canonical = x;
+    vol.anchors(x, c.idx, c.w);
+    c.target = {cf.world_pos[0], cf.world_pos[1], cf.world_pos[2]};
+    c.normal = {0, 0, 0};
+    c.conf = 1.0;
+    out.push_back(c);
+  }
+  return out;
+}
+}  // namespace
 
 extern "C" {
 
@@ -2355,6 +2455,7 @@ int wfo_recon_process_frame(wfo_recon* r, const wfk_frame_view* frame, const wfk
     const FusionStats s = integrate_frame(vol, f, r->pose, boot, par);
     rec->fusion = {s.fused, s.gate, s.frustum, s.occluded};
     compute_active_set(vol);
+    if (cfg.use_features) rec->features_added = add_features(r, frame, maps, r->frames, nullptr);  // :155
     pose_to_c(r->pose, &rec->pose);
     ++r->frames;
     return WFK_OK;
@@ -2381,7 +2482,9 @@ int wfo_recon_process_frame(wfo_recon* r, const wfk_frame_view* frame, const wfk
     r->pose = icp.pose;
     redeform();
   }
-  const auto sparse_c = cons_of(sparse, nsparse);
+  std::vector<Con> sparse_c;
+  if (cfg.use_features && frame->color) sparse_c = feature_constraints(r, frame, maps, &rec->match_count);
+  for (const Con& c : cons_of(sparse, nsparse)) sparse_c.push_back(c);
   auto all_active = [&](const Con& c) {
     for (int a : c.idx)
       if (!vol.active(a)) return false;
@@ -2421,8 +2524,18 @@ int wfo_recon_process_frame(wfo_recon* r, const wfk_frame_view* frame, const wfk
   const FusionStats s = integrate_frame(vol, f, r->pose, cfg.fusion, par);  // :254
   rec->fusion = {s.fused, s.gate, s.frustum, s.occluded};
   rec->expansion = expand_grid(vol);  // :255
+  if (cfg.use_features) rec->features_added = add_features(r, frame, maps, r->frames, &buf);  // :257
   pose_to_c(r->pose, &rec->pose);
   ++r->frames;
+  return WFK_OK;
+}
+
+int wfo_recon_feature_store(const wfo_recon* r, wfk_feature* out, int64_t cap, int64_t* n_out) {
+  const int64_t n = int64_t(r->store.size());
+  if (n_out) *n_out = n;
+  if (!out) return WFK_OK;
+  if (n > cap) return fail(WFK_E_CAPACITY, "feature buffer too small");
+  std::copy(r->store.begin(), r->store.end(), out);
   return WFK_OK;
 }
 

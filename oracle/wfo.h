@@ -125,9 +125,10 @@ int wfo_rasterize(const wfo_mesh* m, const wfk_intrinsics* intr, int32_t exec,
                   wfk_geometry_buffer* out);
 void wfo_mesh_free(wfo_mesh* m);
 
-/* Reconstructor::process_frame (pipeline.cpp:143-262) restricted to the hot
- * path: ICP (estimate_pose) and the feature front-end are off; sparse
- * constraints may be supplied by the caller instead. */
+/* Reconstructor::process_frame (pipeline.cpp:143-262): global ICP when
+ * estimate_pose, the feature front-end and FeatureStore when use_features
+ * (pipeline.cpp:95-141, 185-217); caller-supplied sparse constraints are
+ * appended after the feature ones. */
 typedef struct wfo_recon_config {
   int32_t dims[3];
   int32_t reassociations;
@@ -139,6 +140,9 @@ typedef struct wfo_recon_config {
   int32_t estimate_pose;
   int32_t reserved_;
   wfk_icp_params icp;
+  int32_t use_features;
+  int32_t reserved2_;
+  wfk_feature_params features;
 } wfo_recon_config;
 
 typedef struct wfo_frame_record {
@@ -155,6 +159,8 @@ typedef struct wfo_frame_record {
   int32_t icp_degraded;
   int32_t icp_iterations;
   double icp_rms;
+  int32_t match_count;
+  int32_t features_added;
 } wfo_frame_record;
 
 typedef struct wfo_recon wfo_recon;
@@ -165,6 +171,8 @@ void wfo_recon_volume(wfo_recon* r, wfk_volume_view* out);
 int wfo_recon_process_frame(wfo_recon* r, const wfk_frame_view* frame,
                             const wfk_correspondence* sparse, int64_t nsparse,
                             wfo_frame_record* rec);
+/* the reconstructor's FeatureStore (copies n_out <= cap entries when out != NULL) */
+int wfo_recon_feature_store(const wfo_recon* r, wfk_feature* out, int64_t cap, int64_t* n_out);
 
 #ifdef __cplusplus
 }

@@ -598,6 +598,12 @@ void run_frame(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose* pose_in, con
       boot.bootstrap = 1;
       fusion_integrate(c, pose, boot, &rec->fusion);
       fusion_compute_active_set(c, nullptr, 0, nullptr);
+      c->feat.n_store = 0;      // a bootstrap starts a reconstruction: its FeatureStore is empty
+      if (cfg->use_features) {  // pipeline.cpp:155
+        int32_t nf = 0;
+        features_detect(c, cfg->features, nullptr, 0, &nf, nullptr);
+        rec->features_added = features_add(c, *pose, frame_index, true);
+      }
       rec->bootstrap = 1;
       return;
     }
@@ -631,6 +637,15 @@ void run_frame(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose* pose_in, con
       timed("normals0", [&] { assoc_compute_normals(c); });
       timed("raster0", [&] { assoc_rasterize(c, K, nullptr); });
     }
+    bool features = false;
+    if (cfg->use_features && c->frame.has_color) {  // sparse term against the history (pipeline.cpp:185-217)
+      int32_t nf = 0;
+      timed("features", [&] {
+        features_detect(c, cfg->features, nullptr, 0, &nf, nullptr);
+        features_frame_sparse(c, K, pose_local, cfg->features, &rec->match_count);
+      });
+      features = true;
+    }
     stage_mark(c, 1);
     lap(0, 0, 1);
     std::vector<wfk_trace_entry> trace;
@@ -639,9 +654,10 @@ void run_frame(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose* pose_in, con
       int64_t nd = 0;
       assoc_find_dense(c, K, cfg->correspond, true, &nd);
       rec->dense_count = int32_t(nd);
-      int64_t kept = 0;
-      if (nsparse > 0) upload_constraints(c, sparse, nsparse, true, true, &kept);
-      rec->sparse_count = int32_t(kept);
+      int64_t kept = 0, kept_caller = 0;
+      if (features) kept = features_append_sparse(c);  // pipeline.cpp:229-236
+      if (nsparse > 0) upload_constraints(c, sparse, nsparse, true, true, &kept_caller);
+      rec->sparse_count = int32_t(kept + kept_caller);
       stage_mark(c, 3);
       lap(1, 2, 3);
       if (c->cons.count == 0) break;
@@ -665,6 +681,13 @@ void run_frame(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose* pose_in, con
     fusion_advance_active_ages(c);                      // pipeline.cpp:249-252
     fusion_integrate(c, pose, cfg->fusion, &rec->fusion);  // :254
     fusion_expand(c, &rec->expansion);                  // :255
+    if (cfg->use_features && c->frame.has_color) {      // :257
+      if (!features) {
+        int32_t nf = 0;
+        features_detect(c, cfg->features, nullptr, 0, &nf, nullptr);
+      }
+      timed("feat_add", [&] { rec->features_added = features_add(c, pose_local, frame_index, false); });
+    }
     stage_mark(c, 7);
     lap(4, 6, 7);
     lap(5, 0, 7);
@@ -688,6 +711,23 @@ int wfk_feature_pyramid_level(wfk_ctx* c, int32_t octave, int32_t level, int32_t
     if (!width || !height) throw Error(WFK_E_INVALID_ARG, "null argument");
     features_level(c, octave, level, dog, out, width, height);
   });
+}
+
+int wfk_match_features(wfk_ctx* c, const wfk_feature* cur, int32_t nc, const wfk_feature* store, int32_t ns,
+                       const double* predicted, const wfk_intrinsics* intr, const wfk_feature_params* p,
+                       wfk_feature_match* out, int32_t cap, int32_t* n_out) {
+  return guard(c, [&] {
+    if (!intr || !p || !n_out) throw Error(WFK_E_INVALID_ARG, "null argument");
+    features_match_host(c, cur, nc, store, ns, predicted, *intr, *p, out, cap, n_out);
+  });
+}
+
+int wfk_feature_store_upload(wfk_ctx* c, const wfk_feature* in, int64_t n) {
+  return guard(c, [&] { features_store_upload(c, in, n); });
+}
+
+int wfk_feature_store_download(wfk_ctx* c, wfk_feature* out, int64_t cap, int64_t* n_out) {
+  return guard(c, [&] { features_store_download(c, out, cap, n_out); });
 }
 
 int wfk_invert_warp(wfk_ctx* c, const wfk_pose* pose, int64_t n, const double* y, const double* seed,

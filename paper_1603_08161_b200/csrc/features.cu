@@ -14,6 +14,7 @@
 
 #include "wfk_context.cuh"
 #include "wfk_solver.cuh"
+#include "volume_math.cuh"
 
 namespace wfk {
 
@@ -130,63 +131,94 @@ struct OctImg {
   const float* g1[8];  // gauss[o][1]
   int w[8], h[8];
 };
-// dominant_orientations (features.cpp:94-132), one thread per extremum
-__global__ void k_orientations(int n, const int4* ext, const int32_t* order, OctImg im, double sigma,
-                               wfk_feature_params p, double* ori, int32_t* nori) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int4 e = ext[order[i]];
-    const float* img = im.g1[e.x];
-    const int W = im.w[e.x], H = im.h[e.x];
-    constexpr int kBins = 36;
-    double hist[kBins];
-    for (int b = 0; b < kBins; ++b) hist[b] = 0;
-    const double win_sigma = 1.5 * sigma;
-    const int radius = max(1, int(llround(3.0 * win_sigma)));
-    const int cx = e.y, cy = e.z;
-    for (int dy = -radius; dy <= radius; ++dy)
-      for (int dx = -radius; dx <= radius; ++dx) {
+// dominant_orientations (features.cpp:94-132), one warp per extremum: the
+// lanes stage (bin, weight) of a chunk of window samples in shared memory,
+// then the lane owning a bin adds that bin's samples in window order -- the
+// reference's summation order per bin, so the histogram is the serial one.
+constexpr int kOriWarps = 4, kOriChunk = 256, kOriBins = 36;
+__global__ void __launch_bounds__(32 * kOriWarps) k_orientations(int n, const int4* ext, const int32_t* order,
+                                                                 OctImg im, double sigma, wfk_feature_params p,
+                                                                 double* ori, int32_t* nori) {
+  __shared__ double sw[kOriWarps][kOriChunk];
+  __shared__ int8_t sb[kOriWarps][kOriChunk];
+  __shared__ double sh[kOriWarps][kOriBins];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int i = blockIdx.x * kOriWarps + warp;
+  if (i >= n) return;  // warp-uniform; only __syncwarp below
+  const int4 e = ext[order[i]];
+  const float* img = im.g1[e.x];
+  const int W = im.w[e.x], H = im.h[e.x];
+  const double win_sigma = 1.5 * sigma;
+  const int radius = max(1, int(llround(3.0 * win_sigma)));
+  const int side = 2 * radius + 1, ns = side * side;
+  const int cx = e.y, cy = e.z;
+  double h0 = 0, h1 = 0;  // bins lane and lane + 32
+  for (int c0 = 0; c0 < ns; c0 += kOriChunk) {
+    for (int s = lane; s < kOriChunk; s += 32) {
+      const int q = c0 + s;
+      int bin = -1;
+      double v = 0;
+      if (q < ns) {
+        const int dy = q / side - radius, dx = q % side - radius;
         const int px = cx + dx, py = cy + dy;
-        if (px < 1 || py < 1 || px >= W - 1 || py >= H - 1) continue;
-        const double gx = img[int64_t(py) * W + px + 1] - img[int64_t(py) * W + px - 1];
-        const double gy = img[int64_t(py + 1) * W + px] - img[int64_t(py - 1) * W + px];
-        const double mag = hypot(gx, gy);
-        const double theta = atan2(gy, gx);
-        const double w = exp(-0.5 * (dx * dx + dy * dy) / (win_sigma * win_sigma));
-        int bin = int(floor((theta + M_PI) / (2 * M_PI) * kBins));
-        bin = min(max(bin, 0), kBins - 1);
-        hist[bin] += w * mag;
+        if (!(px < 1 || py < 1 || px >= W - 1 || py >= H - 1)) {
+          const double gx = img[int64_t(py) * W + px + 1] - img[int64_t(py) * W + px - 1];
+          const double gy = img[int64_t(py + 1) * W + px] - img[int64_t(py - 1) * W + px];
+          const double mag = hypot(gx, gy);
+          const double theta = atan2(gy, gx);
+          const double w = exp(-0.5 * (dx * dx + dy * dy) / (win_sigma * win_sigma));
+          bin = int(floor((theta + M_PI) / (2 * M_PI) * kOriBins));
+          bin = min(max(bin, 0), kOriBins - 1);
+          v = w * mag;
+        }
       }
-    double peak = hist[0];
-    for (int b = 1; b < kBins; ++b) peak = fmax(peak, hist[b]);
-    int cnt = 0;
-    double val[2] = {0, 0}, ang[2] = {0, 0};
-    if (peak > 0) {
-      // candidates in bin order, stable by decreasing value: keep the best max_orientations (<= 2)
-      for (int b = 0; b < kBins; ++b) {
-        const double l = hist[(b + kBins - 1) % kBins], r = hist[(b + 1) % kBins];
-        if (hist[b] >= p.orientation_peak_ratio * peak && hist[b] > l && hist[b] > r) {
-          const double denom = l - 2 * hist[b] + r;
-          const double off = fabs(denom) > 1e-12 ? 0.5 * (l - r) / denom : 0.0;
-          const double a = (b + 0.5 + off) / kBins * 2 * M_PI - M_PI;
-          // insert keeping (value desc, earlier bin first on ties)
-          int at = cnt;
-          while (at > 0 && val[at - 1] < hist[b]) --at;
-          if (at < 2) {
-            for (int q = min(cnt, 1); q > at; --q) {
-              val[q] = val[q - 1];
-              ang[q] = ang[q - 1];
-            }
-            val[at] = hist[b];
-            ang[at] = a;
-            cnt = min(cnt + 1, 2);
+      sb[warp][s] = int8_t(bin);
+      sw[warp][s] = v;
+    }
+    __syncwarp();
+    const int m = min(kOriChunk, ns - c0);
+    for (int s = 0; s < m; ++s) {
+      const int bq = sb[warp][s];
+      if (bq == lane) h0 += sw[warp][s];
+      else if (bq == lane + 32) h1 += sw[warp][s];
+    }
+    __syncwarp();
+  }
+  sh[warp][lane] = h0;
+  if (lane + 32 < kOriBins) sh[warp][lane + 32] = h1;
+  __syncwarp();
+  if (lane != 0) return;
+  const double* hist = sh[warp];
+  double peak = hist[0];
+  for (int b = 1; b < kOriBins; ++b) peak = fmax(peak, hist[b]);
+  int cnt = 0;
+  double val[2] = {0, 0}, ang[2] = {0, 0};
+  if (peak > 0) {
+    // candidates in bin order, stable by decreasing value: keep the best max_orientations (<= 2)
+    for (int b = 0; b < kOriBins; ++b) {
+      const double l = hist[(b + kOriBins - 1) % kOriBins], r = hist[(b + 1) % kOriBins];
+      if (hist[b] >= p.orientation_peak_ratio * peak && hist[b] > l && hist[b] > r) {
+        const double denom = l - 2 * hist[b] + r;
+        const double off = fabs(denom) > 1e-12 ? 0.5 * (l - r) / denom : 0.0;
+        const double a = (b + 0.5 + off) / kOriBins * 2 * M_PI - M_PI;
+        // insert keeping (value desc, earlier bin first on ties)
+        int at = cnt;
+        while (at > 0 && val[at - 1] < hist[b]) --at;
+        if (at < 2) {
+          for (int q = min(cnt, 1); q > at; --q) {
+            val[q] = val[q - 1];
+            ang[q] = ang[q - 1];
           }
+          val[at] = hist[b];
+          ang[at] = a;
+          cnt = min(cnt + 1, 2);
         }
       }
     }
-    nori[i] = min(cnt, p.max_orientations);
-    ori[2 * i] = ang[0];
-    ori[2 * i + 1] = ang[1];
   }
+  nori[i] = min(cnt, p.max_orientations);
+  ori[2 * i] = ang[0];
+  ori[2 * i + 1] = ang[1];
 }
 // keypoints in extremum order until max_keypoints (features.cpp:188-207)
 struct KpDev {
@@ -212,83 +244,426 @@ __global__ void k_assemble_kp(int n, const int4* ext, const int32_t* order, cons
   }
   *n_kp = m;
 }
-// extract_descriptors (features.cpp:212-286), one thread per keypoint
-__global__ void k_descriptors(const int32_t* n_kp, const KpDev* kps, OctImg im, double sigma_oct,
-                              wfk_feature* out, uint8_t* ok) {
+// extract_descriptors (features.cpp:212-286), one 128-thread block per
+// keypoint.  Phase 1 stages a chunk of window samples (cell / orientation bin
+// corner, fractions, weight) in shared memory; phase 2: the thread owning one
+// of the 128 histogram bins adds that bin's trilinear shares in window order,
+// which is the reference's summation order per bin.
+constexpr int kDescThreads = 128, kDescChunk = 512;
+__global__ void __launch_bounds__(kDescThreads) k_descriptors(const int32_t* n_kp, const KpDev* kps, OctImg im,
+                                                              double sigma_oct, wfk_feature* out, uint8_t* ok) {
+  constexpr int kCells = 4, kBins8 = 8;
+  __shared__ double s_fx[kDescChunk], s_fy[kDescChunk], s_fo[kDescChunk], s_w[kDescChunk];
+  __shared__ int s_c[kDescChunk];  // x0 + 1 | (y0 + 1) << 8 | o0 << 16, or -1 outside the window
+  __shared__ float s_desc[128];
   const int n = *n_kp;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+  const int tid = threadIdx.x;
+  const int my_y = tid / (kCells * kBins8), my_x = (tid / kBins8) % kCells, my_o = tid % kBins8;
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
     const KpDev kp = kps[i];
     const float* img = im.g1[kp.octave];
     const int W = im.w[kp.octave], H = im.h[kp.octave];
-    constexpr int kCells = 4, kOriBins = 8;
     const double cell = 3.0 * sigma_oct;
     const double radius = cell * (kCells + 1) * sqrt(2.0) * 0.5;
     const double cx = kp.ox, cy = kp.oy;
-    ok[i] = 0;
-    if (cx - radius < 1 || cy - radius < 1 || cx + radius >= W - 1 || cy + radius >= H - 1) continue;
+    if (cx - radius < 1 || cy - radius < 1 || cx + radius >= W - 1 || cy + radius >= H - 1) {
+      if (tid == 0) ok[i] = 0;
+      continue;  // block-uniform
+    }
     const double ct = cos(kp.orientation), st = sin(kp.orientation);
-    double hist[kCells * kCells * kOriBins];
-    for (int q = 0; q < kCells * kCells * kOriBins; ++q) hist[q] = 0;
     const int r = int(ceil(radius));
-    for (int dy = -r; dy <= r; ++dy)
-      for (int dx = -r; dx <= r; ++dx) {
-        const double rx = (ct * dx + st * dy) / cell;
-        const double ry = (-st * dx + ct * dy) / cell;
-        const double bx = rx + kCells / 2.0 - 0.5;
-        const double by = ry + kCells / 2.0 - 0.5;
-        if (bx <= -1 || by <= -1 || bx >= kCells || by >= kCells) continue;
-        const int px = kp.ox + dx, py = kp.oy + dy;
-        const double gx = img[int64_t(py) * W + px + 1] - img[int64_t(py) * W + px - 1];
-        const double gy = img[int64_t(py + 1) * W + px] - img[int64_t(py - 1) * W + px];
-        const double mag = hypot(gx, gy);
-        double theta = atan2(gy, gx) - kp.orientation;
-        while (theta < 0) theta += 2 * M_PI;
-        while (theta >= 2 * M_PI) theta -= 2 * M_PI;
-        const double ob = theta / (2 * M_PI) * kOriBins;
-        const double w = mag * exp(-0.5 * (rx * rx + ry * ry) / ((kCells / 2.0) * (kCells / 2.0)));
-        const int x0 = int(floor(bx)), y0 = int(floor(by));
-        const int o0 = int(floor(ob)) % kOriBins;
-        const double fx = bx - floor(bx), fy = by - floor(by), fo = ob - floor(ob);
-        for (int ix = 0; ix < 2; ++ix)
-          for (int iy = 0; iy < 2; ++iy)
-            for (int io = 0; io < 2; ++io) {
-              const int xx = x0 + ix, yy = y0 + iy;
-              if (xx < 0 || yy < 0 || xx >= kCells || yy >= kCells) continue;
-              const int oo = (o0 + io) % kOriBins;
-              hist[(yy * kCells + xx) * kOriBins + oo] +=
-                  w * (ix ? fx : 1 - fx) * (iy ? fy : 1 - fy) * (io ? fo : 1 - fo);
-            }
+    const int side = 2 * r + 1, ns = side * side;
+    double acc = 0;
+    for (int c0 = 0; c0 < ns; c0 += kDescChunk) {
+      for (int s = tid; s < kDescChunk; s += kDescThreads) {
+        const int q = c0 + s;
+        int code = -1;
+        if (q < ns) {
+          const int dy = q / side - r, dx = q % side - r;
+          const double rx = (ct * dx + st * dy) / cell;
+          const double ry = (-st * dx + ct * dy) / cell;
+          const double bx = rx + kCells / 2.0 - 0.5;
+          const double by = ry + kCells / 2.0 - 0.5;
+          if (!(bx <= -1 || by <= -1 || bx >= kCells || by >= kCells)) {
+            const int px = kp.ox + dx, py = kp.oy + dy;
+            const double gx = img[int64_t(py) * W + px + 1] - img[int64_t(py) * W + px - 1];
+            const double gy = img[int64_t(py + 1) * W + px] - img[int64_t(py - 1) * W + px];
+            const double mag = hypot(gx, gy);
+            double theta = atan2(gy, gx) - kp.orientation;
+            while (theta < 0) theta += 2 * M_PI;
+            while (theta >= 2 * M_PI) theta -= 2 * M_PI;
+            const double ob = theta / (2 * M_PI) * kBins8;
+            s_w[s] = mag * exp(-0.5 * (rx * rx + ry * ry) / ((kCells / 2.0) * (kCells / 2.0)));
+            const int x0 = int(floor(bx)), y0 = int(floor(by));
+            const int o0 = int(floor(ob)) % kBins8;
+            s_fx[s] = bx - floor(bx);
+            s_fy[s] = by - floor(by);
+            s_fo[s] = ob - floor(ob);
+            code = (x0 + 1) | ((y0 + 1) << 8) | (o0 << 16);
+          }
+        }
+        s_c[s] = code;
       }
-    wfk_feature& f = out[i];
-    const int scale = 1 << kp.octave;
-    for (int q = 0; q < 3; ++q) f.canonical_pos[q] = f.world_pos[q] = 0;
-    f.pixel[0] = double(kp.ox * scale);
-    f.pixel[1] = double(kp.oy * scale);
-    f.scale = kp.scale;
-    f.orientation = kp.orientation;
-    f.frame_id = -1;
-    f.reserved_ = 0;
-    double norm = 0;
-    for (int q = 0; q < 128; ++q) {
-      f.descriptor[q] = float(hist[q]);
-      norm += f.descriptor[q] * f.descriptor[q];
+      __syncthreads();
+      const int m = min(kDescChunk, ns - c0);
+      for (int s = 0; s < m; ++s) {
+        const int code = s_c[s];
+        if (code < 0) continue;
+        const int ix = my_x - ((code & 0xff) - 1), iy = my_y - (((code >> 8) & 0xff) - 1);
+        if (unsigned(ix) > 1u || unsigned(iy) > 1u) continue;
+        const int io = (my_o - (code >> 16) + kBins8) % kBins8;
+        if (io > 1) continue;
+        const double fx = s_fx[s], fy = s_fy[s], fo = s_fo[s];
+        acc += s_w[s] * (ix ? fx : 1 - fx) * (iy ? fy : 1 - fy) * (io ? fo : 1 - fo);
+      }
+      __syncthreads();
     }
-    norm = sqrt(norm);
-    if (norm < 1e-12) continue;  // flat patch
-    double norm2 = 0;
-    for (int q = 0; q < 128; ++q) {
-      const float v = fminf(f.descriptor[q] / float(norm), 0.2f);
-      f.descriptor[q] = v;
-      norm2 += v * v;
+    s_desc[tid] = float(acc);
+    __syncthreads();
+    if (tid == 0) {
+      wfk_feature& f = out[i];
+      const int scale = 1 << kp.octave;
+      for (int q = 0; q < 3; ++q) f.canonical_pos[q] = f.world_pos[q] = 0;
+      f.pixel[0] = double(kp.ox * scale);
+      f.pixel[1] = double(kp.oy * scale);
+      f.scale = kp.scale;
+      f.orientation = kp.orientation;
+      f.frame_id = -1;
+      f.reserved_ = 0;
+      double norm = 0;
+      for (int q = 0; q < 128; ++q) norm += s_desc[q] * s_desc[q];
+      norm = sqrt(norm);
+      if (norm < 1e-12) {  // flat patch
+        ok[i] = 0;
+      } else {
+        double norm2 = 0;
+        for (int q = 0; q < 128; ++q) {
+          const float v = fminf(s_desc[q] / float(norm), 0.2f);
+          s_desc[q] = v;
+          norm2 += v * v;
+        }
+        norm2 = sqrt(norm2);
+        for (int q = 0; q < 128; ++q) f.descriptor[q] = float(s_desc[q] / norm2);
+        ok[i] = 1;
+      }
     }
-    norm2 = sqrt(norm2);
-    for (int q = 0; q < 128; ++q) f.descriptor[q] = float(f.descriptor[q] / norm2);
-    ok[i] = 1;
+    __syncthreads();
   }
 }
 
-// The whole detection of the context's frame; features land in c->feat.cur
-// (device) and, when out != null, on the host.
+// ---------------------------------------------------------------------------
+// ordered compaction in one block (record order kept: keypoint order, store
+// order, match order); n from the device (n_dev) or the host
+// ---------------------------------------------------------------------------
+constexpr int kCompactBlock = 256;
+template <class T>
+__global__ void __launch_bounds__(kCompactBlock) k_compact_ordered(const int32_t* n_dev, int n_host, const T* in,
+                                                                   const uint8_t* ok, T* out, int32_t* n_out) {
+  using Scan = cub::BlockScan<int, kCompactBlock>;
+  __shared__ typename Scan::TempStorage ts;
+  const int n = n_dev ? *n_dev : n_host;
+  int base = 0;
+  for (int c0 = 0; c0 < n; c0 += kCompactBlock) {
+    const int i = c0 + int(threadIdx.x);
+    const int f = (i < n && ok[i]) ? 1 : 0;
+    int pos, agg;
+    Scan(ts).ExclusiveSum(f, pos, agg);
+    if (f) out[base + pos] = in[i];
+    base += agg;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *n_out = base;
+}
+
+// current features' world positions from the frame's maps (pipeline.cpp:194-201)
+__global__ void k_feat_world(int n, wfk_feature* f, int W, int H, const double* point, const uint8_t* pvalid) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int px = int(lround(f[i].pixel[0])), py = int(lround(f[i].pixel[1]));
+  V3 w{0, 0, -1};  // invalid, pruned by matching
+  if (px >= 0 && py >= 0 && px < W && py < H && pvalid[int64_t(py) * W + px]) w = ld3(point, int64_t(py) * W + px);
+  f[i].world_pos[0] = w.x;
+  f[i].world_pos[1] = w.y;
+  f[i].world_pos[2] = w.z;
+}
+
+// the store's predicted world positions (pipeline.cpp:203-207)
+__global__ void k_feat_predict(int64_t n, const wfk_feature* st, Grid g, const double* deformed, PoseD pose,
+                               double* pred) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const V3 c{st[i].canonical_pos[0], st[i].canonical_pos[1], st[i].canonical_pos[2]};
+    st3(pred, i, g.contains(c) ? pose.apply(g.interpolate(deformed, c)) : V3{0, 0, -1});
+  }
+}
+
+// ---------------------------------------------------------------------------
+// match_features (features.cpp:354-433): the store is stably sorted by frame
+// id; the block at the head of each run matches that frame's features against
+// the current ones (mutual best, cap, sort, prune) into its slot.
+// ---------------------------------------------------------------------------
+__global__ void k_match_keys(int64_t n, const wfk_feature* st, uint32_t* key, int32_t* idx) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    key[i] = uint32_t(st[i].frame_id) ^ 0x80000000u;  // signed order
+    idx[i] = int32_t(i);
+  }
+}
+
+struct MatchArgs {
+  const wfk_feature* cur;
+  int nc;
+  const wfk_feature* st;
+  int ns;
+  const uint32_t* key;  // sorted frame keys
+  const int32_t* id;    // store index of each sorted position
+  const double* pred;   // 3 * ns, by store index
+  wfk_intrinsics K;
+  int max_cand, keep, slot;
+  double tau_desc, tau_px, tau_3d;
+  double* dist;         // ns * nc, by sorted position
+  int32_t* best_row;    // ns
+  double* best_row_d;   // ns
+  wfk_feature_match* out;  // slot per sorted position
+  int32_t* cnt;            // ns + 1
+};
+
+// descriptor_distance (features.cpp:288-295): sequential fp64 sum, no fused multiply-add
+WF_D double desc_dist(const float* a, const float* b) {
+  // wfk_feature is 600 B: descriptors are 8-byte aligned
+  const float2* a2 = reinterpret_cast<const float2*>(a);
+  const float2* b2 = reinterpret_cast<const float2*>(b);
+  double s = 0;
+#pragma unroll 16
+  for (int i = 0; i < 64; ++i) {
+    const float2 x = a2[i], y = b2[i];
+    const double d0 = double(x.x) - double(y.x), d1 = double(x.y) - double(y.y);
+    s = __dadd_rn(s, __dmul_rn(d0, d0));
+    s = __dadd_rn(s, __dmul_rn(d1, d1));
+  }
+  return sqrt(s);
+}
+
+constexpr int kMatchBlock = 256;
+__global__ void __launch_bounds__(kMatchBlock) k_match_groups(MatchArgs a) {
+  extern __shared__ __align__(16) unsigned char msm[];
+  int32_t* best_col = reinterpret_cast<int32_t*>(msm);                                                  // nc
+  wfk_feature_match* cand = reinterpret_cast<wfk_feature_match*>(msm + 16 * ((4 * a.nc + 15) / 16));  // max_cand
+  __shared__ int s_nh;
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x;
+  if (b > 0 && a.key[b] == a.key[b - 1]) {  // not the head of a frame group
+    if (tid == 0) a.cnt[b] = 0;
+    return;
+  }
+  if (tid == 0) {
+    int e = b + 1;
+    while (e < a.ns && a.key[e] == a.key[b]) ++e;
+    s_nh = e - b;
+  }
+  __syncthreads();
+  const int nh = s_nh, nc = a.nc;
+  // distance matrix of the group (rows: history features in store order)
+  for (int64_t q = tid; q < int64_t(nh) * nc; q += kMatchBlock) {
+    const int h = int(q / nc), c = int(q % nc);
+    a.dist[(int64_t(b) + h) * nc + c] = desc_dist(a.st[a.id[b + h]].descriptor, a.cur[c].descriptor);
+  }
+  __syncthreads();
+  for (int h = tid; h < nh; h += kMatchBlock) {  // best current feature of each history feature
+    const double* row = a.dist + (int64_t(b) + h) * nc;
+    double bd = INFINITY;
+    int bc = -1;
+    for (int c = 0; c < nc; ++c)
+      if (row[c] < bd) {
+        bd = row[c];
+        bc = c;
+      }
+    a.best_row[b + h] = bc;
+    a.best_row_d[b + h] = bd;
+  }
+  for (int c = tid; c < nc; c += kMatchBlock) {  // best history feature of each current feature
+    double bd = INFINITY;
+    int bh = -1;
+    for (int h = 0; h < nh; ++h) {
+      const double d = a.dist[(int64_t(b) + h) * nc + c];
+      if (d < bd) {
+        bd = d;
+        bh = h;
+      }
+    }
+    best_col[c] = bh;
+  }
+  __syncthreads();
+  if (tid != 0) return;
+  // mutual-best candidates in history order, capped (features.cpp:372-380)
+  int nk = 0;
+  for (int h = 0; h < nh; ++h) {
+    const int c = a.best_row[b + h];
+    if (c >= 0 && best_col[c] == h) {
+      cand[nk++] = wfk_feature_match{a.id[b + h], c, a.best_row_d[b + h]};
+      if (nk >= a.max_cand) break;
+    }
+  }
+  // sort by (distance, source id) -- a total order, so any sort is the stable sort
+  for (int i = 1; i < nk; ++i) {
+    const wfk_feature_match m = cand[i];
+    int j = i - 1;
+    while (j >= 0 && (cand[j].distance > m.distance ||
+                      (cand[j].distance == m.distance && cand[j].source_id > m.source_id))) {
+      cand[j + 1] = cand[j];
+      --j;
+    }
+    cand[j + 1] = m;
+  }
+  if (nk > a.keep) nk = a.keep;
+  // prune: descriptor distance, reprojection, 3-D distance (features.cpp:384-411)
+  int no = 0;
+  for (int k = 0; k < nk; ++k) {
+    const wfk_feature_match m = cand[k];
+    if (m.distance > a.tau_desc) continue;
+    const double* pw = a.pred + 3 * int64_t(m.source_id);
+    if (pw[2] <= 0) continue;
+    const double u = a.K.fx * pw[0] / pw[2] + a.K.cx, v = a.K.fy * pw[1] / pw[2] + a.K.cy;
+    const wfk_feature& cf = a.cur[m.target_id];
+    const double du = u - cf.pixel[0], dv = v - cf.pixel[1];
+    if (sqrt(__dadd_rn(__dmul_rn(du, du), __dmul_rn(dv, dv))) > a.tau_px) continue;
+    const double ex = pw[0] - cf.world_pos[0], ey = pw[1] - cf.world_pos[1], ez = pw[2] - cf.world_pos[2];
+    if (sqrt(__dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez))) > a.tau_3d) continue;
+    a.out[int64_t(b) * a.slot + no++] = m;
+  }
+  a.cnt[b] = no;
+}
+
+__global__ void k_match_scatter(int n, int slot, const wfk_feature_match* in, const int32_t* cnt, const int32_t* pos,
+                                wfk_feature_match* out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n) return;
+  for (int k = 0; k < cnt[b]; ++k) out[pos[b] + k] = in[int64_t(b) * slot + k];
+}
+
+// sparse_to_constraints (correspond.cpp:152-169) of the matches whose current
+// feature has a valid world position (pipeline.cpp:210-215)
+__global__ void k_sparse_records(int n, const wfk_feature_match* m, const wfk_feature* cur, const wfk_feature* st,
+                                 Grid g, wfk_correspondence* rec, uint8_t* ok) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const wfk_feature& cf = cur[m[i].target_id];
+  const wfk_feature& sf = st[m[i].source_id];
+  const V3 x{sf.canonical_pos[0], sf.canonical_pos[1], sf.canonical_pos[2]};
+  const bool good = cf.world_pos[2] > 0 && g.contains(x);
+  ok[i] = good ? 1 : 0;
+  if (!good) return;
+  wfk_correspondence r;
+  r.kind = WFK_SPARSE_POINT;
+  r.reserved_ = 0;
+  r.canonical[0] = x.x;
+  r.canonical[1] = x.y;
+  r.canonical[2] = x.z;
+  g.anchors(x, r.anchor_index, r.anchor_weight);
+  for (int k = 0; k < 3; ++k) {
+    r.target[k] = cf.world_pos[k];
+    r.target_normal[k] = 0;
+  }
+  r.confidence = 1.0;
+  rec[i] = r;
+}
+
+// append the records whose eight anchors are active to the constraint arrays
+// (pipeline.cpp:221-235)
+__global__ void __launch_bounds__(kCompactBlock) k_append_active(int n, const wfk_correspondence* rec,
+                                                                 const uint8_t* ok, const uint8_t* active, int64_t base,
+                                                                 int32_t* kind, double* can, int32_t* anchor,
+                                                                 double* weight, double* tgt, double* nrm,
+                                                                 double* conf, int32_t* n_out) {
+  using Scan = cub::BlockScan<int, kCompactBlock>;
+  __shared__ typename Scan::TempStorage ts;
+  int done = 0;
+  for (int c0 = 0; c0 < n; c0 += kCompactBlock) {
+    const int i = c0 + int(threadIdx.x);
+    int f = 0;
+    if (i < n && ok[i]) {
+      f = 1;
+      for (int k = 0; k < 8; ++k) f &= active[rec[i].anchor_index[k]] ? 1 : 0;
+    }
+    int pos, agg;
+    Scan(ts).ExclusiveSum(f, pos, agg);
+    if (f) {
+      const wfk_correspondence& r = rec[i];
+      const int64_t j = base + done + pos;
+      kind[j] = r.kind;
+      for (int k = 0; k < 3; ++k) {
+        can[3 * j + k] = r.canonical[k];
+        tgt[3 * j + k] = r.target[k];
+        nrm[3 * j + k] = r.target_normal[k];
+      }
+      for (int k = 0; k < 8; ++k) {
+        anchor[8 * j + k] = r.anchor_index[k];
+        weight[8 * j + k] = r.anchor_weight[k];
+      }
+      conf[j] = r.confidence;
+    }
+    done += agg;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *n_out = done;
+}
+
+// add_features (pipeline.cpp:95-141): world position from the maps, canonical
+// position by inverting the warp from a rasterized seed within 4 pixels
+struct LiftArgs {
+  int n;
+  const wfk_feature* cur;
+  int W, H;
+  const double* point;
+  const uint8_t* pvalid;
+  int bootstrap;
+  const float* bdepth;
+  const double* bcanon;
+  int bw, bh;
+  Grid g;
+  const double* deformed;
+  PoseD pose;
+  int frame_id;
+  wfk_feature* out;
+  uint8_t* ok;
+};
+__global__ void k_feat_lift(LiftArgs a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  a.ok[i] = 0;
+  wfk_feature f = a.cur[i];
+  const int px = int(lround(f.pixel[0])), py = int(lround(f.pixel[1]));
+  if (px < 0 || py < 0 || px >= a.W || py >= a.H) return;
+  const int64_t idx = int64_t(py) * a.W + px;
+  if (!a.pvalid[idx]) return;
+  const V3 w = ld3(a.point, idx);
+  V3 can = w;  // bootstrap frame: the warp is the identity
+  if (!a.bootstrap) {
+    V3 seed{0, 0, 0};
+    bool have = false;
+    for (int r = 0; r <= 4 && !have; ++r)
+      for (int dy = -r; dy <= r && !have; ++dy)
+        for (int dx = -r; dx <= r && !have; ++dx) {
+          const int sx = px + dx, sy = py + dy;
+          if (sx < 0 || sy < 0 || sx >= a.bw || sy >= a.bh) continue;
+          const int64_t q = int64_t(sy) * a.bw + sx;
+          if (!isfinite(a.bdepth[q])) continue;  // GeometryBuffer::valid (isosurface.hpp:42)
+          seed = ld3(a.bcanon, q);
+          have = true;
+        }
+    if (!have) return;
+    if (!invert_warp_point(a.g, a.deformed, a.pose, w, seed, 20, 1e-6, can) || !a.g.contains(can)) return;
+  }
+  if (!a.g.contains(can)) return;
+  f.world_pos[0] = w.x;
+  f.world_pos[1] = w.y;
+  f.world_pos[2] = w.z;
+  f.canonical_pos[0] = can.x;
+  f.canonical_pos[1] = can.y;
+  f.canonical_pos[2] = can.z;
+  f.frame_id = a.frame_id;
+  a.out[i] = f;
+  a.ok[i] = 1;
+}
+
 void features_detect(wfk_ctx* c, const wfk_feature_params& p, wfk_feature* out, int32_t cap, int32_t* n_out,
                      int32_t* n_kp_out) {
   FrameDev& f = c->frame;
@@ -421,35 +796,33 @@ void features_detect(wfk_ctx* c, const wfk_feature_params& p, wfk_feature* out, 
   const int32_t* order = fd.idx.p + n_ext;
   double* ori = fd.ori.ensure(2 * size_t(n_ext));
   int32_t* nori = fd.nori.ensure(size_t(n_ext));
-  k_orientations<<<grid_for(n_ext, 64), 64, 0, s>>>(n_ext, fd.ext, order, im, sigma_oct, p, ori, nori);
+  k_orientations<<<(n_ext + kOriWarps - 1) / kOriWarps, 32 * kOriWarps, 0, s>>>(n_ext, fd.ext, order, im, sigma_oct,
+                                                                               p, ori, nori);
   KpDev* kp = reinterpret_cast<KpDev*>(fd.kp.ensure(size_t(std::max(p.max_keypoints, 1)) * sizeof(KpDev)));
-  int32_t* nkp = fd.cnt.ensure(4);
+  int32_t* nkp = fd.cnt.ensure(4);  // [0] keypoints, [1] features, [2] sparse kept, [3] store added
   k_assemble_kp<<<1, 32, 0, s>>>(n_ext, fd.ext, order, ori, nori, p.max_keypoints, sigma_oct, kp, nkp);
   const int maxk = std::max(p.max_keypoints, 1);
   wfk_feature* cur = reinterpret_cast<wfk_feature*>(fd.cur_raw.ensure(size_t(maxk) * sizeof(wfk_feature)));
   uint8_t* ok = fd.ok.ensure(size_t(maxk));
-  k_descriptors<<<grid_for(maxk, 32), 32, 0, s>>>(nkp, kp, im, sigma_oct, cur, ok);
+  k_descriptors<<<std::min(maxk, 4 * c->num_sms), kDescThreads, 0, s>>>(nkp, kp, im, sigma_oct, cur, ok);
   count_launch(c, 3);
-  // compact the valid descriptors in keypoint order (host side: <= max_keypoints records)
-  int32_t n_kp = 0;
-  WFK_CUDA(cudaMemcpyAsync(&n_kp, nkp, 4, cudaMemcpyDeviceToHost, s));
+  // compact the valid descriptors in keypoint order (features.cpp:279-283)
+  wfk_feature* dst = fd.cur.ensure(size_t(maxk));
+  int32_t* dn = fd.cnt.p + 1;
+  k_compact_ordered<wfk_feature><<<1, kCompactBlock, 0, s>>>(nkp, 0, cur, ok, dst, dn);
+  count_launch(c);
+  WFK_CUDA(cudaMemcpyAsync(c->h_pinned, nkp, 8, cudaMemcpyDeviceToHost, s));
   WFK_CUDA(cudaStreamSynchronize(s));
-  std::vector<wfk_feature> hf(static_cast<size_t>(n_kp));
-  std::vector<uint8_t> hok(static_cast<size_t>(n_kp));
-  if (n_kp > 0) {
-    WFK_CUDA(cudaMemcpyAsync(hf.data(), cur, size_t(n_kp) * sizeof(wfk_feature), cudaMemcpyDeviceToHost, s));
-    WFK_CUDA(cudaMemcpyAsync(hok.data(), ok, size_t(n_kp), cudaMemcpyDeviceToHost, s));
-    WFK_CUDA(cudaStreamSynchronize(s));
-  }
-  fd.host_cur.clear();
-  for (int i = 0; i < n_kp; ++i)
-    if (hok[size_t(i)]) fd.host_cur.push_back(hf[size_t(i)]);
-  fd.n_cur = int32_t(fd.host_cur.size());
+  const int32_t n_kp = c->h_pinned[0];
+  fd.n_cur = c->h_pinned[1];
   *n_out = fd.n_cur;
   if (n_kp_out) *n_kp_out = n_kp;
   if (out) {
     if (fd.n_cur > cap) throw Error(WFK_E_CAPACITY, "feature buffer too small");
-    std::copy(fd.host_cur.begin(), fd.host_cur.end(), out);
+    if (fd.n_cur > 0) {
+      WFK_CUDA(cudaMemcpyAsync(out, dst, size_t(fd.n_cur) * sizeof(wfk_feature), cudaMemcpyDeviceToHost, s));
+      WFK_CUDA(cudaStreamSynchronize(s));
+    }
   }
 }
 
@@ -464,6 +837,224 @@ void features_level(wfk_ctx* c, int o, int l, int dog, float* out, int32_t* w, i
   const DevBuf<float>& b = fd.levels[o][dog ? L + 1 + l : l];
   if (out) {
     WFK_CUDA(cudaMemcpyAsync(out, b.p, size_t(*w) * size_t(*h) * 4, cudaMemcpyDeviceToHost, c->stream));
+    WFK_CUDA(cudaStreamSynchronize(c->stream));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side of matching, sparse constraints and the store
+// ---------------------------------------------------------------------------
+namespace {
+PoseD pose_dev(const wfk_pose& p) {
+  PoseD d;
+  for (int i = 0; i < 9; ++i) d.r.a[i / 3][i % 3] = p.rotation[i];
+  d.t = V3{p.translation[0], p.translation[1], p.translation[2]};
+  return d;
+}
+void check_match_params(const wfk_feature_params& p) {
+  if (p.keep_best < 0 || p.max_candidates > 4096)
+    throw Error(WFK_E_INVALID_ARG, "feature params beyond the device limits (keep_best >= 0, max_candidates <= 4096)");
+}
+}  // namespace
+
+// match_features (features.cpp:416-433) of device arrays; result in fd.matches / fd.n_matches
+void features_match_dev(wfk_ctx* c, const wfk_feature* cur, int nc, const wfk_feature* st, int64_t ns,
+                        const double* pred, const wfk_intrinsics& K, const wfk_feature_params& p) {
+  FeatDev& fd = c->feat;
+  fd.n_matches = 0;
+  check_match_params(p);
+  if (nc <= 0 || ns <= 0) return;
+  if (ns >= (int64_t(1) << 31) || int64_t(ns) * nc >= (int64_t(1) << 40))
+    throw Error(WFK_E_INVALID_ARG, "feature store too large");
+  cudaStream_t s = c->stream;
+  const int n = int(ns);
+  uint32_t* key = fd.skey.ensure(2 * size_t(n));
+  int32_t* idx = fd.sidx.ensure(2 * size_t(n));
+  k_match_keys<<<grid_for(n), kBlock, 0, s>>>(n, st, key, idx);
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, key, key + n, idx, idx + n, n, 0, 32, s);
+  c->temp.ensure(tb);
+  WFK_CUDA(cub::DeviceRadixSort::SortPairs(c->temp.p, tb, key, key + n, idx, idx + n, n, 0, 32, s));
+  count_launch(c, 2);
+  MatchArgs a;
+  a.cur = cur;
+  a.nc = nc;
+  a.st = st;
+  a.ns = n;
+  a.key = key + n;
+  a.id = idx + n;
+  a.pred = pred;
+  a.K = K;
+  a.max_cand = std::max(p.max_candidates, 1);  // the cap is tested after each push
+  a.keep = p.keep_best;
+  a.slot = std::max(std::min(a.max_cand, a.keep), 1);
+  a.tau_desc = p.tau_descriptor;
+  a.tau_px = p.tau_pixels;
+  a.tau_3d = p.tau_3d;
+  a.dist = fd.dist.ensure(size_t(n) * size_t(nc));
+  int32_t* rows = fd.mpos.ensure(2 * size_t(n) + 2);
+  a.best_row = rows + n + 1;
+  a.best_row_d = fd.row_d.ensure(size_t(n));
+  a.out = fd.mslot.ensure(size_t(n) * size_t(a.slot));
+  a.cnt = fd.mcnt.ensure(size_t(n) + 1);
+  const size_t smem = 16 * ((4 * size_t(nc) + 15) / 16) + 16 * size_t(a.max_cand);
+  if (smem > 200 * 1024) throw Error(WFK_E_INVALID_ARG, "too many current features for the matcher");
+  if (smem > 48 * 1024)
+    WFK_CUDA(cudaFuncSetAttribute(k_match_groups, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  WFK_CUDA(cudaMemsetAsync(a.cnt + n, 0, 4, s));
+  k_match_groups<<<n, kMatchBlock, smem, s>>>(a);
+  int32_t* pos = rows;  // n + 1 exclusive offsets
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, a.cnt, pos, n + 1, s);
+  c->temp.ensure(tb);
+  WFK_CUDA(cub::DeviceScan::ExclusiveSum(c->temp.p, tb, a.cnt, pos, n + 1, s));
+  WFK_CUDA(cudaMemcpyAsync(c->h_pinned, pos + n, 4, cudaMemcpyDeviceToHost, s));
+  WFK_CUDA(cudaStreamSynchronize(s));
+  fd.n_matches = c->h_pinned[0];
+  if (fd.n_matches > 0) {
+    wfk_feature_match* m = fd.matches.ensure(size_t(fd.n_matches));
+    k_match_scatter<<<grid_for(n), kBlock, 0, s>>>(n, a.slot, a.out, a.cnt, pos, m);
+    count_launch(c);
+  }
+  count_launch(c, 2);
+  WFK_CUDA(cudaGetLastError());
+}
+
+void features_match_host(wfk_ctx* c, const wfk_feature* cur, int32_t nc, const wfk_feature* st, int32_t ns,
+                         const double* pred, const wfk_intrinsics& K, const wfk_feature_params& p,
+                         wfk_feature_match* out, int32_t cap, int32_t* n_out) {
+  FeatDev& fd = c->feat;
+  cudaStream_t s = c->stream;
+  *n_out = 0;
+  if (nc < 0 || ns < 0 || (nc > 0 && !cur) || (ns > 0 && (!st || !pred))) throw Error(WFK_E_INVALID_ARG, "bad arrays");
+  if (nc == 0 || ns == 0) return;
+  wfk_feature* dcur = fd.lift.ensure(size_t(nc));
+  wfk_feature* dst = fd.xstore.ensure(size_t(ns));
+  double* dp = fd.pred.ensure(3 * size_t(ns));
+  WFK_CUDA(cudaMemcpyAsync(dcur, cur, size_t(nc) * sizeof(wfk_feature), cudaMemcpyHostToDevice, s));
+  WFK_CUDA(cudaMemcpyAsync(dst, st, size_t(ns) * sizeof(wfk_feature), cudaMemcpyHostToDevice, s));
+  WFK_CUDA(cudaMemcpyAsync(dp, pred, 3 * size_t(ns) * 8, cudaMemcpyHostToDevice, s));
+  features_match_dev(c, dcur, nc, dst, ns, dp, K, p);
+  *n_out = fd.n_matches;
+  if (fd.n_matches > cap) throw Error(WFK_E_CAPACITY, "match buffer too small");
+  if (fd.n_matches > 0 && out) {
+    WFK_CUDA(cudaMemcpyAsync(out, fd.matches.p, size_t(fd.n_matches) * sizeof(wfk_feature_match),
+                             cudaMemcpyDeviceToHost, s));
+    WFK_CUDA(cudaStreamSynchronize(s));
+  }
+}
+
+// the sparse term of a frame (pipeline.cpp:185-217): the detected features'
+// world positions, the store's predicted positions, matches, constraint records
+void features_frame_sparse(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose& pose, const wfk_feature_params& p,
+                           int32_t* match_count) {
+  FeatDev& fd = c->feat;
+  FrameDev& f = c->frame;
+  cudaStream_t s = c->stream;
+  fd.n_sparse = 0;
+  *match_count = 0;
+  if (fd.n_cur == 0) return;
+  k_feat_world<<<grid_for(fd.n_cur, 64), 64, 0, s>>>(fd.n_cur, fd.cur, f.K.width, f.K.height, f.point, f.pvalid);
+  count_launch(c);
+  if (fd.n_store == 0) return;
+  double* pred = fd.pred.ensure(3 * size_t(fd.n_store));
+  k_feat_predict<<<grid_for(fd.n_store), kBlock, 0, s>>>(fd.n_store, fd.store, c->vol.g, c->vol.deformed,
+                                                        pose_dev(pose), pred);
+  count_launch(c);
+  features_match_dev(c, fd.cur, fd.n_cur, fd.store, fd.n_store, pred, K, p);
+  *match_count = fd.n_matches;
+  if (fd.n_matches == 0) return;
+  fd.n_sparse = fd.n_matches;
+  k_sparse_records<<<grid_for(fd.n_sparse, 64), 64, 0, s>>>(fd.n_sparse, fd.matches, fd.cur, fd.store, c->vol.g,
+                                                           fd.sparse.ensure(size_t(fd.n_sparse)),
+                                                           fd.sparse_ok.ensure(size_t(fd.n_sparse)));
+  count_launch(c);
+  WFK_CUDA(cudaGetLastError());
+}
+
+// append the frame's sparse records with all anchors active (pipeline.cpp:229-236)
+int64_t features_append_sparse(wfk_ctx* c) {
+  FeatDev& fd = c->feat;
+  if (fd.n_sparse == 0) return 0;
+  ConIn& ci = c->cons;
+  cudaStream_t s = c->stream;
+  const int64_t base = ci.count;
+  const size_t cap = size_t(base + fd.n_sparse) + 1;
+  ci.kind.grow_keep(cap, s);
+  ci.canonical.grow_keep(3 * cap, s);
+  ci.anchor.grow_keep(8 * cap, s);
+  ci.weight.grow_keep(8 * cap, s);
+  ci.target.grow_keep(3 * cap, s);
+  ci.normal.grow_keep(3 * cap, s);
+  ci.conf.grow_keep(cap, s);
+  int32_t* kept = fd.cnt.ensure(4) + 2;
+  k_append_active<<<1, kCompactBlock, 0, s>>>(fd.n_sparse, fd.sparse, fd.sparse_ok, c->vol.active, base, ci.kind,
+                                              ci.canonical, ci.anchor, ci.weight, ci.target, ci.normal, ci.conf, kept);
+  count_launch(c);
+  WFK_CUDA(cudaMemcpyAsync(c->h_pinned, kept, 4, cudaMemcpyDeviceToHost, s));
+  WFK_CUDA(cudaStreamSynchronize(s));
+  const int64_t m = c->h_pinned[0];
+  ci.n_sparse += m;
+  ci.count = base + m;
+  return m;
+}
+
+// add_features (pipeline.cpp:95-141) of the last detection; returns the count added
+int32_t features_add(wfk_ctx* c, const wfk_pose& pose, int32_t frame_id, bool bootstrap) {
+  FeatDev& fd = c->feat;
+  if (fd.n_cur == 0) return 0;
+  FrameDev& f = c->frame;
+  GBufDev& b = c->gbuf;
+  if (!f.maps_valid) throw Error(WFK_E_INVALID_ARG, "add_features: no point/normal maps");
+  if (!bootstrap && !b.valid) throw Error(WFK_E_INVALID_ARG, "add_features: no geometry buffer");
+  cudaStream_t s = c->stream;
+  LiftArgs a;
+  a.n = fd.n_cur;
+  a.cur = fd.cur;
+  a.W = f.K.width;
+  a.H = f.K.height;
+  a.point = f.point;
+  a.pvalid = f.pvalid;
+  a.bootstrap = bootstrap ? 1 : 0;
+  a.bdepth = bootstrap ? nullptr : b.depth.p;
+  a.bcanon = bootstrap ? nullptr : b.canonical.p;
+  a.bw = b.w;
+  a.bh = b.h;
+  a.g = c->vol.g;
+  a.deformed = c->vol.deformed;
+  a.pose = pose_dev(pose);
+  a.frame_id = frame_id;
+  a.out = fd.lift.ensure(size_t(fd.n_cur));
+  a.ok = fd.lift_ok.ensure(size_t(fd.n_cur));
+  k_feat_lift<<<grid_for(a.n, 64), 64, 0, s>>>(a);
+  fd.store.grow_keep(size_t(fd.n_store + fd.n_cur), s);
+  int32_t* added = fd.cnt.ensure(4) + 3;
+  k_compact_ordered<wfk_feature><<<1, kCompactBlock, 0, s>>>(nullptr, a.n, a.out, a.ok, fd.store.p + fd.n_store,
+                                                              added);
+  count_launch(c, 2);
+  WFK_CUDA(cudaMemcpyAsync(c->h_pinned, added, 4, cudaMemcpyDeviceToHost, s));
+  WFK_CUDA(cudaStreamSynchronize(s));
+  fd.n_store += c->h_pinned[0];
+  return c->h_pinned[0];
+}
+
+void features_store_upload(wfk_ctx* c, const wfk_feature* in, int64_t n) {
+  if (n < 0 || (n > 0 && !in)) throw Error(WFK_E_INVALID_ARG, "bad feature array");
+  FeatDev& fd = c->feat;
+  fd.store.ensure(size_t(n));
+  if (n > 0)
+    WFK_CUDA(cudaMemcpyAsync(fd.store.p, in, size_t(n) * sizeof(wfk_feature), cudaMemcpyHostToDevice, c->stream));
+  WFK_CUDA(cudaStreamSynchronize(c->stream));
+  fd.n_store = n;
+}
+
+void features_store_download(wfk_ctx* c, wfk_feature* out, int64_t cap, int64_t* n_out) {
+  FeatDev& fd = c->feat;
+  if (n_out) *n_out = fd.n_store;
+  if (!out) return;
+  if (fd.n_store > cap) throw Error(WFK_E_CAPACITY, "feature buffer too small");
+  if (fd.n_store > 0) {
+    WFK_CUDA(cudaMemcpyAsync(out, fd.store.p, size_t(fd.n_store) * sizeof(wfk_feature), cudaMemcpyDeviceToHost,
+                             c->stream));
     WFK_CUDA(cudaStreamSynchronize(c->stream));
   }
 }

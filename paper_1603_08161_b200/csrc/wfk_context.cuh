@@ -203,8 +203,25 @@ struct FeatDev {
   DevBuf<int4> ext;
   DevBuf<uint32_t> key;
   DevBuf<double> ori;
-  std::vector<wfk_feature> host_cur;  // the last detection's features
   int32_t n_cur = 0;
+  DevBuf<wfk_feature> cur;            // the last detection's features, compacted
+  // FeatureStore (features.hpp:79-95): append-only history, frame ids ascending
+  DevBuf<wfk_feature> store;
+  int64_t n_store = 0;
+  // matching scratch (match_features, features.cpp:354-433)
+  DevBuf<double> pred, dist, row_d;
+  DevBuf<wfk_feature> xstore;  // wfk_match_features' store upload
+  DevBuf<uint32_t> skey;
+  DevBuf<int32_t> sidx, mcnt, mpos;
+  DevBuf<wfk_feature_match> mslot, matches;
+  int32_t n_matches = 0;
+  // sparse feature constraints of the frame (sparse_to_constraints, correspond.cpp:152-169)
+  DevBuf<wfk_correspondence> sparse;
+  DevBuf<uint8_t> sparse_ok;
+  int32_t n_sparse = 0;
+  // add_features scratch (pipeline.cpp:95-141)
+  DevBuf<wfk_feature> lift;
+  DevBuf<uint8_t> lift_ok;
 };
 
 struct Stats {

@@ -34,6 +34,17 @@ void assoc_rasterize(wfk_ctx* c, const wfk_intrinsics& K, wfk_geometry_buffer* o
 void features_detect(wfk_ctx* c, const wfk_feature_params& p, wfk_feature* out, int32_t cap, int32_t* n_out,
                      int32_t* n_kp_out);
 void features_level(wfk_ctx* c, int o, int l, int dog, float* out, int32_t* w, int32_t* h);
+void features_match_dev(wfk_ctx* c, const wfk_feature* cur, int nc, const wfk_feature* st, int64_t ns,
+                        const double* pred, const wfk_intrinsics& K, const wfk_feature_params& p);
+void features_match_host(wfk_ctx* c, const wfk_feature* cur, int32_t nc, const wfk_feature* st, int32_t ns,
+                         const double* pred, const wfk_intrinsics& K, const wfk_feature_params& p,
+                         wfk_feature_match* out, int32_t cap, int32_t* n_out);
+void features_frame_sparse(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose& pose, const wfk_feature_params& p,
+                           int32_t* match_count);
+int64_t features_append_sparse(wfk_ctx* c);
+int32_t features_add(wfk_ctx* c, const wfk_pose& pose, int32_t frame_id, bool bootstrap);
+void features_store_upload(wfk_ctx* c, const wfk_feature* in, int64_t n);
+void features_store_download(wfk_ctx* c, wfk_feature* out, int64_t cap, int64_t* n_out);
 void volume_invert_warp(wfk_ctx* c, const wfk_pose* pose, int64_t n, const double* y, const double* seed,
                         int32_t max_iters, double tol, double* x, uint8_t* ok);
 void assoc_estimate_pose(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose& initial, const wfk_icp_params& prm,

@@ -40,7 +40,8 @@ class WfkError(RuntimeError):
 
 class PipelineConfig(C.Structure):
     _fields_ = [("solver", SolverParams), ("correspond", CorrespondParams), ("fusion", FusionParams),
-                ("reassociations", C.c_int32), ("estimate_pose", C.c_int32), ("icp", IcpParams)]
+                ("reassociations", C.c_int32), ("estimate_pose", C.c_int32), ("icp", IcpParams),
+                ("use_features", C.c_int32), ("reserved_", C.c_int32), ("features", FeatureParams)]
 
 
 class FrameRecord(C.Structure):
@@ -48,7 +49,7 @@ class FrameRecord(C.Structure):
                 ("anomalies", C.c_int32), ("trace_len", C.c_int32), ("pcg_iterations", C.c_int32),
                 ("bootstrap", C.c_int32), ("fusion", FusionStats), ("expansion", ExpansionStats),
                 ("pose", Pose), ("icp_degraded", C.c_int32), ("icp_iterations", C.c_int32),
-                ("icp_rms", C.c_double)]
+                ("icp_rms", C.c_double), ("match_count", C.c_int32), ("features_added", C.c_int32)]
 
 
 class NeHost(C.Structure):
@@ -385,6 +386,32 @@ class Context:
                                               C.byref(nk)))
         return out[: n.value].copy(), nk.value
 
+    def match_features(self, current, store, predicted_world, intr, params=None):
+        """match_features (features.cpp:416-433) on the device; returns MATCH_DTYPE records."""
+        p = params or FeatureParams.make()
+        cur = np.ascontiguousarray(current, FEATURE_DTYPE)
+        st = np.ascontiguousarray(store, FEATURE_DTYPE)
+        pw = np.ascontiguousarray(predicted_world, np.float64).reshape(-1, 3)
+        cap = max(len(st), 1)
+        out = np.zeros(cap, MATCH_DTYPE)
+        n = C.c_int32()
+        self._check(lib().wfk_match_features(self.h, _cptr(cur), C.c_int32(len(cur)), _cptr(st), C.c_int32(len(st)),
+                                             ptr(pw, C.c_double), C.byref(intr), C.byref(p), _cptr(out),
+                                             C.c_int32(cap), C.byref(n)))
+        return out[: n.value].copy()
+
+    def feature_store(self):
+        """The context's FeatureStore (FEATURE_DTYPE records)."""
+        n = C.c_int64()
+        self._check(lib().wfk_feature_store_download(self.h, None, C.c_int64(0), C.byref(n)))
+        out = np.zeros(max(n.value, 1), FEATURE_DTYPE)
+        self._check(lib().wfk_feature_store_download(self.h, _cptr(out), C.c_int64(len(out)), C.byref(n)))
+        return out[: n.value].copy()
+
+    def set_feature_store(self, features):
+        f = np.ascontiguousarray(features, FEATURE_DTYPE)
+        self._check(lib().wfk_feature_store_upload(self.h, _cptr(f) if len(f) else None, C.c_int64(len(f))))
+
     def feature_pyramid_level(self, o, l, dog=False):
         w, h = C.c_int32(), C.c_int32()
         self._check(lib().wfk_feature_pyramid_level(self.h, o, l, int(dog), None, C.byref(w), C.byref(h)))
@@ -459,8 +486,8 @@ class Context:
 
 
 def pipeline_config(solver=None, correspond=None, fusion=None, reassociations=3, estimate_pose=True,
-                    icp=None) -> PipelineConfig:
-    """ReconstructorConfig defaults (config.hpp): ICP on, 3 reassociations."""
+                    icp=None, use_features=True, features=None) -> PipelineConfig:
+    """ReconstructorConfig defaults (config.hpp:30-46): ICP on, features on, 3 reassociations."""
     cfg = PipelineConfig()
     cfg.solver = solver or SolverParams.make()
     cfg.correspond = correspond or CorrespondParams.make()
@@ -468,4 +495,6 @@ def pipeline_config(solver=None, correspond=None, fusion=None, reassociations=3,
     cfg.reassociations = reassociations
     cfg.estimate_pose = 1 if estimate_pose else 0
     cfg.icp = icp or IcpParams.make()
+    cfg.use_features = 1 if use_features else 0
+    cfg.features = features or FeatureParams.make()
     return cfg

@@ -89,3 +89,26 @@ def test_context_fails_loudly_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(wfk.WfkError):
         wfk.Context(0)
+
+
+def test_oracle_struct_layouts_match_c(tmp_path):
+    """oracle/wfo.h's reconstructor config / record vs the pyoracle mirrors."""
+    from oracle import pyoracle
+    structs = {"wfo_recon_config": pyoracle.ReconConfig, "wfo_frame_record": pyoracle.FrameRecord}
+    src = ['#include <stdio.h>', '#include <stddef.h>', '#include "wfo.h"', "int main(void) {"]
+    for name, st in structs.items():
+        src.append(f'  printf("{name} %zu\\n", sizeof({name}));')
+        for f, _ in st._fields_:
+            src.append(f'  printf("{name}.{f} %zu\\n", offsetof({name}, {f}));')
+    src.append("  return 0; }")
+    c = tmp_path / "layout.c"
+    c.write_text("\n".join(src))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), "-I", os.path.join(ROOT, "oracle"), str(c), "-o",
+                    str(exe)], check=True)
+    got = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                       check=True).stdout.splitlines())
+    for name, st in structs.items():
+        assert int(got[name]) == C.sizeof(st), name
+        for f, _ in st._fields_:
+            assert int(got[f"{name}.{f}"]) == getattr(st, f).offset, f"{name}.{f}"

@@ -56,3 +56,65 @@ def test_features_without_color(ctx):
     ctx.upload_frame(Frame(K320, d, None))
     got, nk = ctx.detect_features()
     assert len(got) == 0 and nk == 0
+
+
+def backprojected(feats, fr, K):
+    """world positions of features from the frame depth at the rounded pixel (z <= 0: invalid)"""
+    out = feats.copy()
+    px = np.rint(feats["pixel"]).astype(int)
+    z = fr.depth[np.clip(px[:, 1], 0, K.height - 1), np.clip(px[:, 0], 0, K.width - 1)].astype(np.float64)
+    x = (px[:, 0] - K.cx) * z / K.fx
+    y = (px[:, 1] - K.cy) * z / K.fy
+    out["world_pos"] = np.stack([x, y, np.where(z > 0, z, -1.0)], axis=1)
+    return out
+
+
+def history(K, n_frames, ids):
+    """features of a short bend sequence, frame ids from `ids`, stored in that order"""
+    st = []
+    for f in range(n_frames):
+        fr = frame(K, (0.004 * f, 0.0, 1.2), 0.3 * f)
+        feats, _ = O.detect_features(fr)
+        feats = backprojected(feats, fr, K)
+        feats["canonical_pos"] = feats["world_pos"]
+        feats["frame_id"] = ids[f]
+        st.append(feats)
+    return np.concatenate(st)
+
+
+@pytest.mark.parametrize("ids,tau_px,tau_3d,keep,maxc", [
+    ([0, 1, 2, 3], 48.0, 0.10, 64, 128),  # defaults
+    ([5, 2, 5, 0], 48.0, 0.10, 64, 128),  # frame ids unsorted and repeated (groups not contiguous)
+    ([0, 1, 2, 3], 3.0, 0.004, 64, 128),  # tight reprojection / 3-D prune
+    ([0, 1, 2, 3], 48.0, 0.10, 7, 5),     # candidate cap and keep_best below the mutual count
+])
+def test_match_features_parity(ctx, ids, tau_px, tau_3d, keep, maxc):
+    st = history(K320, 4, ids)
+    fr = frame(K320, (0.02, 0.0, 1.2), 1.3)
+    cur, _ = O.detect_features(fr)
+    cur = backprojected(cur, fr, K320)
+    pred = st["world_pos"].copy()
+    pred[::9, 2] = -1.0  # some history features without a prediction
+    p = FeatureParams.make()
+    p.tau_pixels, p.tau_3d, p.keep_best, p.max_candidates = tau_px, tau_3d, keep, maxc
+    ref = O.match_features(cur, st, pred, K320, p)
+    got = ctx.match_features(cur, st, pred, K320, p)
+    assert len(ref) >= (3 if keep < 10 else 6)
+    np.testing.assert_array_equal(got["source_id"], ref["source_id"])
+    np.testing.assert_array_equal(got["target_id"], ref["target_id"])
+    np.testing.assert_array_equal(got["distance"], ref["distance"])  # sequential fp64 sum: bit-exact
+
+
+def test_match_features_empty(ctx):
+    st = history(K320, 1, [0])
+    assert len(ctx.match_features(st[:0], st, st["world_pos"], K320)) == 0
+    assert len(ctx.match_features(st, st[:0], np.zeros((0, 3)), K320)) == 0
+
+
+def test_feature_store_round_trip(ctx):
+    st = history(K320, 2, [0, 1])
+    ctx.set_feature_store(st)
+    back = ctx.feature_store()
+    assert back.tobytes() == st.tobytes()
+    ctx.set_feature_store(st[:0])
+    assert len(ctx.feature_store()) == 0

@@ -1,12 +1,12 @@
 """End-to-end parity of the per-frame hot path (Reconstructor::process_frame,
-pipeline.cpp:143-262, with the global-pose ICP, without the feature front-end):
+pipeline.cpp:143-262, with the global-pose ICP and the feature front-end):
 the B200 path (wfk_process_frame) against the oracle's restatement on the same
 synthetic bend sequence."""
 import numpy as np
 import pytest
 
 from oracle import pyoracle as O
-from paper_1603_08161_b200.abi import CorrespondParams, Frame, FusionParams, Intrinsics, Pose, SolverParams, Volume
+from paper_1603_08161_b200.abi import FEATURE_DTYPE, CorrespondParams, Frame, FusionParams, Intrinsics, Pose, SolverParams, Volume
 
 pytestmark = pytest.mark.gpu
 
@@ -61,7 +61,7 @@ def test_process_frame_parity(ctx, n, reassoc, levels, icp):
                 assert rg.icp_iterations == rr.icp_iterations and rg.icp_degraded == rr.icp_degraded
             np.testing.assert_allclose(rg.pose.matrix(), rr.pose.matrix(), atol=1e-7)
             np.testing.assert_allclose(rg.pose.vector(), rr.pose.vector(), atol=1e-7)
-        if i == 1:  # identical inputs up to this frame's solve: integer work is exact
+        if i == 1 and reassoc == 1:  # identical inputs up to this frame's solve: integer work is exact
             assert rg.dense_count == rr.dense_count
             assert rg.trace_len == rr.trace_len
         else:
@@ -75,4 +75,52 @@ def test_process_frame_parity(ctx, n, reassoc, levels, icp):
     assert (vol.active != arr["active"]).sum() <= 8
     both = act & vol.active.astype(bool)
     dev = np.max(np.linalg.norm(vol.deformed[both] - arr["deformed"][both], axis=1)) / voxel
+    assert dev <= 1e-3, dev
+
+
+def test_process_frame_features_parity(ctx):
+    """The feature front-end inside process_frame (pipeline.cpp:95-141, 185-217):
+    per-frame match / sparse / added counts and the FeatureStore against the oracle."""
+    from paper_1603_08161_b200.wfk import pipeline_config
+    n = 48
+    K = Intrinsics.make(280, 280, 159.5, 119.5, 320, 240)
+    voxel = 0.7 / (n - 1)
+    origin = (-0.35, -0.35, 0.85)
+    solver = SolverParams.make(levels=3)
+    frames = bend_frames(ctx, K, 5, 1.0)
+    ref = O.Reconstructor((n, n, n), voxel, origin, solver=solver, reassociations=2)
+    vol = Volume((n, n, n), voxel, origin)
+    ctx.upload_volume(vol)
+    ctx.set_feature_store(np.zeros(0, FEATURE_DTYPE))
+    cfg = pipeline_config(solver=solver, reassociations=2)
+    assert cfg.use_features == 1
+    pose = Pose.make()
+    total_sparse = 0
+    for i, fr in enumerate(frames):
+        rr = ref.process_frame(fr)
+        rg = ctx.process_frame(fr, pose, cfg, i)
+        pose = rg.pose
+        if i <= 1:  # identical inputs so far: integer work is exact
+            assert rg.features_added == rr.features_added
+            assert rg.match_count == rr.match_count and rg.sparse_count == rr.sparse_count
+        else:
+            assert abs(rg.features_added - rr.features_added) <= 2
+            assert abs(rg.match_count - rr.match_count) <= 2
+            assert abs(rg.sparse_count - rr.sparse_count) <= 2
+        if i > 0:
+            assert rg.energy.total == pytest.approx(rr.energy.total, rel=1e-3)
+        total_sparse += rg.sparse_count
+    assert total_sparse > 0, "the sequence should produce sparse feature constraints"
+    sg, sr = ctx.feature_store(), ref.feature_store()
+    assert abs(len(sg) - len(sr)) <= 4 and len(sr) > 20
+    # the bootstrap frame's positions are exact (identity warp), later ones to the inversion tolerance
+    b = int((sr["frame_id"] == 0).sum())
+    assert b > 0 and int((sg["frame_id"] == 0).sum()) == b
+    for f in ("pixel", "world_pos", "canonical_pos", "frame_id"):
+        np.testing.assert_array_equal(sg[f][:b], sr[f][:b])
+    np.testing.assert_allclose(sg["descriptor"][:b], sr["descriptor"][:b], rtol=0, atol=1e-5)
+    m = min(len(sg), len(sr))
+    same = (sg["frame_id"][:m] == sr["frame_id"][:m]) & np.all(sg["pixel"][:m] == sr["pixel"][:m], axis=1)
+    assert same.mean() > 0.95
+    dev = np.linalg.norm(sg["canonical_pos"][:m][same] - sr["canonical_pos"][:m][same], axis=1).max() / voxel
     assert dev <= 1e-3, dev
