@@ -47,22 +47,33 @@ __global__ void k_gray(int64_t n, const float* rgb, float* g) {  // to_gray (ima
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     g[i] = (0.299f * rgb[3 * i] + 0.587f * rgb[3 * i + 1] + 0.114f * rgb[3 * i + 2]) / 255.0f;
 }
-template <bool X>
-__global__ void k_blur(int w, int h, const float* in, float* out, Taps t) {
-  const int64_t n = int64_t(w) * h;
-  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < n; p += int64_t(gridDim.x) * blockDim.x) {
-    const int x = int(p % w), y = int(p / w);
+// gaussian_blur (features.cpp:23-46): horizontal then vertical pass with
+// clamped borders, both in one kernel -- a 32x8 output tile keeps its
+// horizontally blurred rows (with the vertical halo) in shared memory; same
+// float operations in the same order as two separate passes.  When `prev` is
+// given the DoG level out - prev (features.cpp:80-86) is written as well.
+constexpr int kBlurTX = 32, kBlurTY = 8, kBlurMaxR = (kMaxTaps - 1) / 2;
+__global__ void __launch_bounds__(kBlurTX* kBlurTY) k_blur(int w, int h, const float* in, float* out, Taps t,
+                                                          const float* prev, float* dog) {
+  __shared__ float tile[kBlurTY + 2 * kBlurMaxR][kBlurTX];
+  const int r = t.radius;
+  const int tx = threadIdx.x % kBlurTX, ty = threadIdx.x / kBlurTX;
+  const int x = blockIdx.x * kBlurTX + tx, y0 = blockIdx.y * kBlurTY;
+  for (int row = ty; row < kBlurTY + 2 * r; row += kBlurTY) {
+    const int yy = min(max(y0 - r + row, 0), h - 1);
     float acc = 0;
-    for (int i = -t.radius; i <= t.radius; ++i) {
-      const float v = X ? in[int64_t(y) * w + min(max(x + i, 0), w - 1)] : in[int64_t(min(max(y + i, 0), h - 1)) * w + x];
-      acc += t.k[i + t.radius] * v;
-    }
-    out[p] = acc;
+    if (x < w)
+      for (int i = -r; i <= r; ++i) acc += t.k[i + r] * in[int64_t(yy) * w + min(max(x + i, 0), w - 1)];
+    tile[row][tx] = acc;
   }
-}
-__global__ void k_sub(int64_t n, const float* a, const float* b, float* out) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
-    out[i] = a[i] - b[i];
+  __syncthreads();
+  const int y = y0 + ty;
+  if (x >= w || y >= h) return;
+  float acc = 0;
+  for (int i = -r; i <= r; ++i) acc += t.k[i + r] * tile[ty + r + i][tx];
+  const int64_t q = int64_t(y) * w + x;
+  out[q] = acc;
+  if (prev) dog[q] = acc - prev[q];
 }
 __global__ void k_down2(int w, int h, const float* in, int wo, int ho, float* out) {
   const int64_t n = int64_t(wo) * ho;
@@ -225,31 +236,43 @@ struct KpDev {
   int octave, ox, oy, pad;
   double scale, orientation;
 };
-__global__ void k_assemble_kp(int n, const int4* ext, const int32_t* order, const double* ori, const int32_t* nori,
-                              int max_kp, double sigma_oct, KpDev* kp, int32_t* n_kp) {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
-  int m = 0;
-  for (int i = 0; i < n && m < max_kp; ++i) {
-    const int4 e = ext[order[i]];
-    for (int q = 0; q < nori[i] && m < max_kp; ++q) {
-      KpDev k;
-      k.octave = e.x;
-      k.ox = e.y;
-      k.oy = e.z;
-      k.pad = 0;
-      k.scale = sigma_oct * double(1 << e.x);
-      k.orientation = ori[2 * i + q];
-      kp[m++] = k;
+constexpr int kAsmBlock = 256;
+__global__ void __launch_bounds__(kAsmBlock) k_assemble_kp(int n, const int4* ext, const int32_t* order,
+                                                           const double* ori, const int32_t* nori, int max_kp,
+                                                           double sigma_oct, KpDev* kp, int32_t* n_kp) {
+  using Scan = cub::BlockScan<int, kAsmBlock>;
+  __shared__ typename Scan::TempStorage ts;
+  int base = 0;
+  for (int c0 = 0; c0 < n && base < max_kp; c0 += kAsmBlock) {  // base is block-uniform
+    const int i = c0 + int(threadIdx.x);
+    const int cnt = i < n ? nori[i] : 0;
+    int pos, agg;
+    Scan(ts).ExclusiveSum(cnt, pos, agg);
+    if (cnt > 0) {
+      const int4 e = ext[order[i]];
+      for (int q = 0; q < cnt && base + pos + q < max_kp; ++q) {
+        KpDev k;
+        k.octave = e.x;
+        k.ox = e.y;
+        k.oy = e.z;
+        k.pad = 0;
+        k.scale = sigma_oct * double(1 << e.x);
+        k.orientation = ori[2 * i + q];
+        kp[base + pos + q] = k;
+      }
     }
+    base += agg;
+    __syncthreads();
   }
-  *n_kp = m;
+  if (threadIdx.x == 0) *n_kp = min(base, max_kp);
 }
-// extract_descriptors (features.cpp:212-286), one 128-thread block per
-// keypoint.  Phase 1 stages a chunk of window samples (cell / orientation bin
-// corner, fractions, weight) in shared memory; phase 2: the thread owning one
-// of the 128 histogram bins adds that bin's trilinear shares in window order,
-// which is the reference's summation order per bin.
-constexpr int kDescThreads = 128, kDescChunk = 512;
+// extract_descriptors (features.cpp:212-286), one 512-thread block per
+// keypoint.  Phase 1 (all threads) stages a chunk of window samples (cell /
+// orientation bin corner, fractions, weight) in shared memory; phase 2: the
+// lane owning one of the 128 histogram bins (warp = cell, lane = orientation)
+// adds that bin's trilinear shares in window order, which is the reference's
+// summation order per bin.
+constexpr int kDescThreads = 512, kDescChunk = 1024;  // 16 warps: one per descriptor cell
 __global__ void __launch_bounds__(kDescThreads) k_descriptors(const int32_t* n_kp, const KpDev* kps, OctImg im,
                                                               double sigma_oct, wfk_feature* out, uint8_t* ok) {
   constexpr int kCells = 4, kBins8 = 8;
@@ -258,7 +281,9 @@ __global__ void __launch_bounds__(kDescThreads) k_descriptors(const int32_t* n_k
   __shared__ float s_desc[128];
   const int n = *n_kp;
   const int tid = threadIdx.x;
-  const int my_y = tid / (kCells * kBins8), my_x = (tid / kBins8) % kCells, my_o = tid % kBins8;
+  // phase 2: warp w owns descriptor cell w (x = w % 4, y = w / 4); lane l < 8 its orientation bin l
+  const int warp = tid / 32, lane = tid % 32;
+  const int my_y = warp / kCells, my_x = warp % kCells, my_o = lane % kBins8;
   for (int i = blockIdx.x; i < n; i += gridDim.x) {
     const KpDev kp = kps[i];
     const float* img = im.g1[kp.octave];
@@ -305,20 +330,29 @@ __global__ void __launch_bounds__(kDescThreads) k_descriptors(const int32_t* n_k
         s_c[s] = code;
       }
       __syncthreads();
+      // only samples whose corner cell is (x - 1 .. x, y - 1 .. y) touch cell (x, y):
+      // a ballot per 32 samples finds them, the warp walks them in window order
       const int m = min(kDescChunk, ns - c0);
-      for (int s = 0; s < m; ++s) {
-        const int code = s_c[s];
-        if (code < 0) continue;
-        const int ix = my_x - ((code & 0xff) - 1), iy = my_y - (((code >> 8) & 0xff) - 1);
-        if (unsigned(ix) > 1u || unsigned(iy) > 1u) continue;
-        const int io = (my_o - (code >> 16) + kBins8) % kBins8;
-        if (io > 1) continue;
-        const double fx = s_fx[s], fy = s_fy[s], fo = s_fo[s];
-        acc += s_w[s] * (ix ? fx : 1 - fx) * (iy ? fy : 1 - fy) * (io ? fo : 1 - fo);
+      for (int s0 = 0; s0 < m; s0 += 32) {
+        const int sl = s0 + lane;
+        const int cl = sl < m ? s_c[sl] : -1;
+        const int xl = (cl & 0xff) - 1, yl = ((cl >> 8) & 0xff) - 1;
+        unsigned mask = __ballot_sync(0xffffffffu, cl >= 0 && unsigned(my_x - xl) <= 1u && unsigned(my_y - yl) <= 1u);
+        while (mask) {
+          const int j = __ffs(mask) - 1;
+          mask &= mask - 1;
+          const int code = __shfl_sync(0xffffffffu, cl, j);
+          const int s = s0 + j;
+          const int ix = my_x - ((code & 0xff) - 1), iy = my_y - (((code >> 8) & 0xff) - 1);
+          const int io = (my_o - (code >> 16) + kBins8) % kBins8;
+          if (io > 1) continue;
+          const double fx = s_fx[s], fy = s_fy[s], fo = s_fo[s];
+          acc += s_w[s] * (ix ? fx : 1 - fx) * (iy ? fy : 1 - fy) * (io ? fo : 1 - fo);
+        }
       }
       __syncthreads();
     }
-    s_desc[tid] = float(acc);
+    if (lane < kBins8) s_desc[warp * kBins8 + lane] = float(acc);
     __syncthreads();
     if (tid == 0) {
       wfk_feature& f = out[i];
@@ -359,8 +393,11 @@ constexpr int kCompactBlock = 256;
 template <class T>
 __global__ void __launch_bounds__(kCompactBlock) k_compact_ordered(const int32_t* n_dev, int n_host, const T* in,
                                                                    const uint8_t* ok, T* out, int32_t* n_out) {
+  static_assert(sizeof(T) % 8 == 0, "records are copied as 8-byte words");
+  constexpr int kWords = int(sizeof(T) / 8);
   using Scan = cub::BlockScan<int, kCompactBlock>;
   __shared__ typename Scan::TempStorage ts;
+  __shared__ int src[kCompactBlock];
   const int n = n_dev ? *n_dev : n_host;
   int base = 0;
   for (int c0 = 0; c0 < n; c0 += kCompactBlock) {
@@ -368,7 +405,13 @@ __global__ void __launch_bounds__(kCompactBlock) k_compact_ordered(const int32_t
     const int f = (i < n && ok[i]) ? 1 : 0;
     int pos, agg;
     Scan(ts).ExclusiveSum(f, pos, agg);
-    if (f) out[base + pos] = in[i];
+    if (f) src[pos] = i;
+    __syncthreads();
+    // the block copies the kept records word by word (coalesced)
+    const uint64_t* a = reinterpret_cast<const uint64_t*>(in);
+    uint64_t* b = reinterpret_cast<uint64_t*>(out + base);
+    for (int q = threadIdx.x; q < agg * kWords; q += kCompactBlock)
+      b[q] = a[int64_t(src[q / kWords]) * kWords + q % kWords];
     base += agg;
     __syncthreads();
   }
@@ -419,34 +462,55 @@ struct MatchArgs {
   wfk_intrinsics K;
   int max_cand, keep, slot;
   double tau_desc, tau_px, tau_3d;
-  double* dist;         // ns * nc, by sorted position
+  double* dist;         // ns * nc, by sorted position (groups whose tile exceeds tile_cap)
+  int tile_cap;         // doubles of shared memory for a group's distance tile
   int32_t* best_row;    // ns
   double* best_row_d;   // ns
   wfk_feature_match* out;  // slot per sorted position
   int32_t* cnt;            // ns + 1
 };
 
-// descriptor_distance (features.cpp:288-295): sequential fp64 sum, no fused multiply-add
-WF_D double desc_dist(const float* a, const float* b) {
-  // wfk_feature is 600 B: descriptors are 8-byte aligned
-  const float2* a2 = reinterpret_cast<const float2*>(a);
-  const float2* b2 = reinterpret_cast<const float2*>(b);
+// descriptor_distance (features.cpp:288-295) against a current descriptor
+// staged transposed in shared memory: sequential fp64 sum, no fused multiply-add
+WF_D double desc_dist_t(const float* a, const float* curT, int ldc, int c) {
+  const float2* a2 = reinterpret_cast<const float2*>(a);  // wfk_feature is 600 B: 8-byte aligned
   double s = 0;
 #pragma unroll 16
   for (int i = 0; i < 64; ++i) {
-    const float2 x = a2[i], y = b2[i];
-    const double d0 = double(x.x) - double(y.x), d1 = double(x.y) - double(y.y);
+    const float2 x = a2[i];
+    const double d0 = double(x.x) - double(curT[(2 * i) * ldc + c]);
+    const double d1 = double(x.y) - double(curT[(2 * i + 1) * ldc + c]);
     s = __dadd_rn(s, __dmul_rn(d0, d0));
     s = __dadd_rn(s, __dmul_rn(d1, d1));
   }
   return sqrt(s);
 }
 
+WF_D bool match_less(const wfk_feature_match& x, const wfk_feature_match& y) {
+  return x.distance != y.distance ? x.distance < y.distance : x.source_id < y.source_id;
+}
+
+// shared-memory plan of k_match_groups (bytes, 16-aligned pieces)
+struct MatchSmem {
+  size_t curT, best_col, rows, cand, sorted, tile, total;
+  int row_cap;
+  static size_t al(size_t x) { return (x + 15) / 16 * 16; }
+  MatchSmem(int nc, int max_cand, int row_cap_, int tile_cap) : row_cap(row_cap_) {
+    curT = 0;
+    best_col = curT + al(size_t(128) * nc * 4);
+    rows = best_col + al(size_t(nc) * 4);
+    cand = rows + al(size_t(row_cap) * 12);
+    sorted = cand + al(size_t(max_cand) * 16);
+    tile = sorted + al(size_t(max_cand) * 16);
+    total = tile + size_t(tile_cap) * 8;
+  }
+};
+
 constexpr int kMatchBlock = 256;
-__global__ void __launch_bounds__(kMatchBlock) k_match_groups(MatchArgs a) {
+__global__ void __launch_bounds__(kMatchBlock) k_match_groups(MatchArgs a, MatchSmem L) {
   extern __shared__ __align__(16) unsigned char msm[];
-  int32_t* best_col = reinterpret_cast<int32_t*>(msm);                                                  // nc
-  wfk_feature_match* cand = reinterpret_cast<wfk_feature_match*>(msm + 16 * ((4 * a.nc + 15) / 16));  // max_cand
+  using Scan = cub::BlockScan<int, kMatchBlock>;
+  __shared__ typename Scan::TempStorage ts;
   __shared__ int s_nh;
   const int b = blockIdx.x;
   const int tid = threadIdx.x;
@@ -454,21 +518,37 @@ __global__ void __launch_bounds__(kMatchBlock) k_match_groups(MatchArgs a) {
     if (tid == 0) a.cnt[b] = 0;
     return;
   }
+  const int nc = a.nc;
+  float* curT = reinterpret_cast<float*>(msm + L.curT);  // [128][nc]
+  int32_t* best_col = reinterpret_cast<int32_t*>(msm + L.best_col);
+  wfk_feature_match* cand = reinterpret_cast<wfk_feature_match*>(msm + L.cand);
+  wfk_feature_match* sorted = reinterpret_cast<wfk_feature_match*>(msm + L.sorted);
   if (tid == 0) {
     int e = b + 1;
     while (e < a.ns && a.key[e] == a.key[b]) ++e;
     s_nh = e - b;
   }
+  for (int q = tid; q < 128 * nc; q += kMatchBlock) {  // stage the current descriptors, transposed
+    const int c = q / 128, i = q % 128;
+    curT[i * nc + c] = a.cur[c].descriptor[i];
+  }
   __syncthreads();
-  const int nh = s_nh, nc = a.nc;
-  // distance matrix of the group (rows: history features in store order)
+  const int nh = s_nh;
+  // per history feature: best current feature and its distance (smem when it fits)
+  int32_t* brow = nh <= L.row_cap ? reinterpret_cast<int32_t*>(msm + L.rows) : a.best_row + b;
+  double* brow_d = nh <= L.row_cap ? reinterpret_cast<double*>(msm + L.rows + 4 * ((L.row_cap + 3) / 4 * 4))
+                                   : a.best_row_d + b;
+  // distance matrix of the group (rows: history features in store order), in
+  // shared memory when it fits
+  double* D = int64_t(nh) * nc <= int64_t(a.tile_cap) ? reinterpret_cast<double*>(msm + L.tile)
+                                                       : a.dist + int64_t(b) * nc;
   for (int64_t q = tid; q < int64_t(nh) * nc; q += kMatchBlock) {
     const int h = int(q / nc), c = int(q % nc);
-    a.dist[(int64_t(b) + h) * nc + c] = desc_dist(a.st[a.id[b + h]].descriptor, a.cur[c].descriptor);
+    D[q] = desc_dist_t(a.st[a.id[b + h]].descriptor, curT, nc, c);
   }
   __syncthreads();
   for (int h = tid; h < nh; h += kMatchBlock) {  // best current feature of each history feature
-    const double* row = a.dist + (int64_t(b) + h) * nc;
+    const double* row = D + int64_t(h) * nc;
     double bd = INFINITY;
     int bc = -1;
     for (int c = 0; c < nc; ++c)
@@ -476,14 +556,14 @@ __global__ void __launch_bounds__(kMatchBlock) k_match_groups(MatchArgs a) {
         bd = row[c];
         bc = c;
       }
-    a.best_row[b + h] = bc;
-    a.best_row_d[b + h] = bd;
+    brow[h] = bc;
+    brow_d[h] = bd;
   }
   for (int c = tid; c < nc; c += kMatchBlock) {  // best history feature of each current feature
     double bd = INFINITY;
     int bh = -1;
     for (int h = 0; h < nh; ++h) {
-      const double d = a.dist[(int64_t(b) + h) * nc + c];
+      const double d = D[int64_t(h) * nc + c];
       if (d < bd) {
         bd = d;
         bh = h;
@@ -492,44 +572,60 @@ __global__ void __launch_bounds__(kMatchBlock) k_match_groups(MatchArgs a) {
     best_col[c] = bh;
   }
   __syncthreads();
-  if (tid != 0) return;
-  // mutual-best candidates in history order, capped (features.cpp:372-380)
-  int nk = 0;
-  for (int h = 0; h < nh; ++h) {
-    const int c = a.best_row[b + h];
-    if (c >= 0 && best_col[c] == h) {
-      cand[nk++] = wfk_feature_match{a.id[b + h], c, a.best_row_d[b + h]};
-      if (nk >= a.max_cand) break;
+  // mutual-best candidates in history order, the first max_cand (features.cpp:372-380)
+  int base = 0;
+  for (int h0 = 0; h0 < nh && base < a.max_cand; h0 += kMatchBlock) {  // base is block-uniform
+    const int h = h0 + tid;
+    int c = -1, f = 0;
+    if (h < nh) {
+      c = brow[h];
+      f = (c >= 0 && best_col[c] == h) ? 1 : 0;
     }
+    int pos, agg;
+    Scan(ts).ExclusiveSum(f, pos, agg);
+    if (f && base + pos < a.max_cand) cand[base + pos] = wfk_feature_match{a.id[b + h], c, brow_d[h]};
+    base += agg;
+    __syncthreads();
   }
-  // sort by (distance, source id) -- a total order, so any sort is the stable sort
-  for (int i = 1; i < nk; ++i) {
-    const wfk_feature_match m = cand[i];
-    int j = i - 1;
-    while (j >= 0 && (cand[j].distance > m.distance ||
-                      (cand[j].distance == m.distance && cand[j].source_id > m.source_id))) {
-      cand[j + 1] = cand[j];
-      --j;
-    }
-    cand[j + 1] = m;
-  }
-  if (nk > a.keep) nk = a.keep;
-  // prune: descriptor distance, reprojection, 3-D distance (features.cpp:384-411)
-  int no = 0;
-  for (int k = 0; k < nk; ++k) {
+  const int nk = min(base, a.max_cand);
+  // sort by (distance, source id): a total order, so the rank of each candidate is its place
+  for (int k = tid; k < nk; k += kMatchBlock) {
     const wfk_feature_match m = cand[k];
-    if (m.distance > a.tau_desc) continue;
-    const double* pw = a.pred + 3 * int64_t(m.source_id);
-    if (pw[2] <= 0) continue;
-    const double u = a.K.fx * pw[0] / pw[2] + a.K.cx, v = a.K.fy * pw[1] / pw[2] + a.K.cy;
-    const wfk_feature& cf = a.cur[m.target_id];
-    const double du = u - cf.pixel[0], dv = v - cf.pixel[1];
-    if (sqrt(__dadd_rn(__dmul_rn(du, du), __dmul_rn(dv, dv))) > a.tau_px) continue;
-    const double ex = pw[0] - cf.world_pos[0], ey = pw[1] - cf.world_pos[1], ez = pw[2] - cf.world_pos[2];
-    if (sqrt(__dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez))) > a.tau_3d) continue;
-    a.out[int64_t(b) * a.slot + no++] = m;
+    int r = 0;
+    for (int j = 0; j < nk; ++j) r += match_less(cand[j], m) ? 1 : 0;
+    sorted[r] = m;
   }
-  a.cnt[b] = no;
+  __syncthreads();
+  // keep_best, then the descriptor / reprojection / 3-D prune (features.cpp:382-411), in order
+  const int nkeep = min(nk, a.keep);
+  int done = 0;
+  for (int k0 = 0; k0 < nkeep; k0 += kMatchBlock) {
+    const int k = k0 + tid;
+    int f = 0;
+    wfk_feature_match m{};
+    if (k < nkeep) {
+      m = sorted[k];
+      f = 1;
+      if (m.distance > a.tau_desc) f = 0;
+      const double* pw = a.pred + 3 * int64_t(m.source_id);
+      if (f && pw[2] <= 0) f = 0;
+      if (f) {
+        const double u = a.K.fx * pw[0] / pw[2] + a.K.cx, v = a.K.fy * pw[1] / pw[2] + a.K.cy;
+        const wfk_feature& cf = a.cur[m.target_id];
+        const double du = u - cf.pixel[0], dv = v - cf.pixel[1];
+        if (sqrt(__dadd_rn(__dmul_rn(du, du), __dmul_rn(dv, dv))) > a.tau_px) f = 0;
+        const double ex = pw[0] - cf.world_pos[0], ey = pw[1] - cf.world_pos[1], ez = pw[2] - cf.world_pos[2];
+        if (f && sqrt(__dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez))) > a.tau_3d)
+          f = 0;
+      }
+    }
+    int pos, agg;
+    Scan(ts).ExclusiveSum(f, pos, agg);
+    if (f) a.out[int64_t(b) * a.slot + done + pos] = m;
+    done += agg;
+    __syncthreads();
+  }
+  if (tid == 0) a.cnt[b] = done;
 }
 
 __global__ void k_match_scatter(int n, int slot, const wfk_feature_match* in, const int32_t* cnt, const int32_t* pos,
@@ -691,7 +787,6 @@ void features_detect(wfk_ctx* c, const wfk_feature_params& p, wfk_feature* out, 
   const double k = std::pow(2.0, 1.0 / L);
   const size_t npx = size_t(W) * H;
   float* gray = fd.gray.ensure(npx);
-  float* tmp = fd.tmp.ensure(npx);
   k_gray<<<grid_for(int64_t(npx)), kBlock, 0, s>>>(int64_t(npx), f.color, gray);
   count_launch(c);
   const float* base = gray;
@@ -707,12 +802,9 @@ void features_detect(wfk_ctx* c, const wfk_feature_params& p, wfk_feature* out, 
       const Taps t = blur_taps(sigma);
       float* dst = G(o, l).ensure(size_t(n));
       const float* src = l == 0 ? base : G(o, l - 1).p;
-      k_blur<true><<<grid_for(n), kBlock, 0, s>>>(w, h, src, tmp, t);
-      k_blur<false><<<grid_for(n), kBlock, 0, s>>>(w, h, tmp, dst, t);
-      count_launch(c, 2);
-    }
-    for (int l = 0; l < L; ++l) {
-      k_sub<<<grid_for(n), kBlock, 0, s>>>(n, G(o, l + 1).p, G(o, l).p, D(o, l).ensure(size_t(n)));
+      const dim3 grid((w + kBlurTX - 1) / kBlurTX, (h + kBlurTY - 1) / kBlurTY);
+      k_blur<<<grid, kBlurTX * kBlurTY, 0, s>>>(w, h, src, dst, t, l == 0 ? nullptr : G(o, l - 1).p,
+                                                l == 0 ? nullptr : D(o, l - 1).ensure(size_t(n)));
       count_launch(c);
     }
     if (o + 1 < p.octaves) {
@@ -800,7 +892,7 @@ void features_detect(wfk_ctx* c, const wfk_feature_params& p, wfk_feature* out, 
                                                                                p, ori, nori);
   KpDev* kp = reinterpret_cast<KpDev*>(fd.kp.ensure(size_t(std::max(p.max_keypoints, 1)) * sizeof(KpDev)));
   int32_t* nkp = fd.cnt.ensure(4);  // [0] keypoints, [1] features, [2] sparse kept, [3] store added
-  k_assemble_kp<<<1, 32, 0, s>>>(n_ext, fd.ext, order, ori, nori, p.max_keypoints, sigma_oct, kp, nkp);
+  k_assemble_kp<<<1, kAsmBlock, 0, s>>>(n_ext, fd.ext, order, ori, nori, p.max_keypoints, sigma_oct, kp, nkp);
   const int maxk = std::max(p.max_keypoints, 1);
   wfk_feature* cur = reinterpret_cast<wfk_feature*>(fd.cur_raw.ensure(size_t(maxk) * sizeof(wfk_feature)));
   uint8_t* ok = fd.ok.ensure(size_t(maxk));
@@ -897,12 +989,16 @@ void features_match_dev(wfk_ctx* c, const wfk_feature* cur, int nc, const wfk_fe
   a.best_row_d = fd.row_d.ensure(size_t(n));
   a.out = fd.mslot.ensure(size_t(n) * size_t(a.slot));
   a.cnt = fd.mcnt.ensure(size_t(n) + 1);
-  const size_t smem = 16 * ((4 * size_t(nc) + 15) / 16) + 16 * size_t(a.max_cand);
-  if (smem > 200 * 1024) throw Error(WFK_E_INVALID_ARG, "too many current features for the matcher");
-  if (smem > 48 * 1024)
-    WFK_CUDA(cudaFuncSetAttribute(k_match_groups, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  // shared memory: transposed current descriptors, best rows of groups up to
+  // 1024 features, candidates, and the group's distance tile when it fits
+  const int row_cap = 1024;
+  const MatchSmem L0(nc, a.max_cand, row_cap, 0);
+  if (L0.total > 160 * 1024) throw Error(WFK_E_INVALID_ARG, "too many current features for the matcher");
+  a.tile_cap = int(std::min<size_t>((200 * 1024 - L0.total) / 8, 16384));
+  const MatchSmem L(nc, a.max_cand, row_cap, a.tile_cap);
+  WFK_CUDA(cudaFuncSetAttribute(k_match_groups, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.total)));
   WFK_CUDA(cudaMemsetAsync(a.cnt + n, 0, 4, s));
-  k_match_groups<<<n, kMatchBlock, smem, s>>>(a);
+  k_match_groups<<<n, kMatchBlock, L.total, s>>>(a, L);
   int32_t* pos = rows;  // n + 1 exclusive offsets
   cub::DeviceScan::ExclusiveSum(nullptr, tb, a.cnt, pos, n + 1, s);
   c->temp.ensure(tb);
