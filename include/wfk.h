@@ -164,7 +164,7 @@ int wfk_detect_features(wfk_ctx* ctx, const wfk_feature_params* p, wfk_feature* 
 /* one level of the last detection's pyramid (octave o, gaussian level l or DoG level l) */
 int wfk_feature_pyramid_level(wfk_ctx* ctx, int32_t octave, int32_t level, int32_t dog, float* out,
                               int32_t* width, int32_t* height);
-/* match_features (features.cpp:354-433; replaces features.hpp:106-110): the store
+/* match_features (features.cpp:354-433; replaces features.hpp:107-110): the store
  * grouped by frame id (ascending), per group mutual-best matching of descriptors,
  * the max_candidates cap, the (distance, source id) sort, keep_best and the
  * descriptor / reprojection / 3-D prune.  predicted = 3 doubles per store entry
