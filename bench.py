@@ -270,6 +270,7 @@ def run_b200(args):
     launches0 = ctx.launch_count
     recs = []
     total_ms = 0.0
+    frame_ms = []
     d.barrier()
     with ClockSampler(d.local) as clocks:
         for f in timed:
@@ -278,7 +279,8 @@ def run_b200(args):
             recs.append(ctx.process_staged_frame(f, pose, cfg, f))
             ctx.timer_mark(1)
             pose = recs[-1].pose
-            total_ms += ctx.timer_elapsed_ms(0, 1)
+            frame_ms.append(ctx.timer_elapsed_ms(0, 1))
+            total_ms += frame_ms[-1]
     d.barrier()
     launches = ctx.launch_count - launches0
     prof = ctx.profile_read()
@@ -290,13 +292,15 @@ def run_b200(args):
     ctx.set_feature_store(ckpt_store)
     pose = ckpt_pose
     e2e_ms = 0.0
+    e2e_frame_ms = []
     d.barrier()
     for f in timed:
         ctx.flush_l2()
         ctx.timer_mark(2)
         r = ctx.process_frame(frames[f], pose, cfg, f)   # H2D frame + D2H record inside
         ctx.timer_mark(3)
-        e2e_ms += ctx.timer_elapsed_ms(2, 3)
+        e2e_frame_ms.append(ctx.timer_elapsed_ms(2, 3))
+        e2e_ms += e2e_frame_ms[-1]
         pose = r.pose
         _ = (r.energy.total, r.dense_count)
     d.barrier()
@@ -336,6 +340,8 @@ def run_b200(args):
             "pcg_iters_per_s": pcg_iters_all / (d.max(total_ms) * 1e-3),
             "pcg_iterations_per_frame": pcg_iters / k,
             "frame_breakdown_ms": {kk: v / k for kk, v in prof.as_dict()["stage_ms"].items()},
+            "frame_ms": [round(x, 3) for x in frame_ms],
+            "e2e_frame_ms": [round(x, 3) for x in e2e_frame_ms],
             "dense_constraints_per_frame": float(np.mean([r.dense_count for r in recs])),
             "sparse_constraints_per_frame": float(np.mean([r.sparse_count for r in recs])),
             "feature_matches_per_frame": float(np.mean([r.match_count for r in recs])),

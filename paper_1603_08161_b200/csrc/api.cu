@@ -599,6 +599,7 @@ void run_frame(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose* pose_in, con
       fusion_integrate(c, pose, boot, &rec->fusion);
       fusion_compute_active_set(c, nullptr, 0, nullptr);
       c->feat.n_store = 0;      // a bootstrap starts a reconstruction: its FeatureStore is empty
+      c->feat.max_group = 0;
       if (cfg->use_features) {  // pipeline.cpp:155
         int32_t nf = 0;
         features_detect(c, cfg->features, nullptr, 0, &nf, nullptr);

@@ -9,6 +9,8 @@
 // and descriptors call device hypot/atan2/exp/cos/sin (glibc's last bits can
 // differ): one thread per keypoint keeps the reference's accumulation order,
 // so results agree to rounding.
+#include <map>
+
 #include <cub/cub.cuh>
 #include <thrust/iterator/transform_iterator.h>
 
@@ -35,6 +37,14 @@ static Taps blur_taps(double sigma) {
   }
   for (int i = 0; i < 2 * t.radius + 1; ++i) t.k[i] /= sum;
   return t;
+}
+
+// capacity for size-varying scratch (extrema, store, matches): powers of two
+// from 16384, so growth (cudaFree synchronises the device) is rare
+static size_t cap_for(size_t n) {
+  size_t c = 16384;
+  while (c < n) c *= 2;
+  return c;
 }
 
 struct FlagToInt {
@@ -858,9 +868,9 @@ void features_detect(wfk_ctx* c, const wfk_feature_params& p, wfk_feature* out, 
     WFK_CUDA(cudaStreamSynchronize(s));
     n_ext = c->h_pinned[0];
     if (n_ext > 0) {
-      int4* ext = fd.ext.ensure(size_t(n_ext));
-      uint32_t* key = fd.key.ensure(2 * size_t(n_ext));
-      int32_t* idx = fd.idx.ensure(2 * size_t(n_ext));
+      int4* ext = fd.ext.ensure(cap_for(size_t(n_ext)));
+      uint32_t* key = fd.key.ensure(2 * cap_for(size_t(n_ext)));
+      int32_t* idx = fd.idx.ensure(2 * cap_for(size_t(n_ext)));
       q = 0;
       for (int o = 0; o < p.octaves; ++o)
         for (int l = 1; l + 1 < L; ++l, ++q) {
@@ -886,8 +896,8 @@ void features_detect(wfk_ctx* c, const wfk_feature_params& p, wfk_feature* out, 
   }
   const double sigma_oct = p.sigma0 * std::pow(k, 1.5);
   const int32_t* order = fd.idx.p + n_ext;
-  double* ori = fd.ori.ensure(2 * size_t(n_ext));
-  int32_t* nori = fd.nori.ensure(size_t(n_ext));
+  double* ori = fd.ori.ensure(2 * cap_for(size_t(n_ext)));
+  int32_t* nori = fd.nori.ensure(cap_for(size_t(n_ext)));
   k_orientations<<<(n_ext + kOriWarps - 1) / kOriWarps, 32 * kOriWarps, 0, s>>>(n_ext, fd.ext, order, im, sigma_oct,
                                                                                p, ori, nori);
   KpDev* kp = reinterpret_cast<KpDev*>(fd.kp.ensure(size_t(std::max(p.max_keypoints, 1)) * sizeof(KpDev)));
@@ -951,7 +961,7 @@ void check_match_params(const wfk_feature_params& p) {
 
 // match_features (features.cpp:416-433) of device arrays; result in fd.matches / fd.n_matches
 void features_match_dev(wfk_ctx* c, const wfk_feature* cur, int nc, const wfk_feature* st, int64_t ns,
-                        const double* pred, const wfk_intrinsics& K, const wfk_feature_params& p) {
+                        const double* pred, const wfk_intrinsics& K, const wfk_feature_params& p, int64_t max_group) {
   FeatDev& fd = c->feat;
   fd.n_matches = 0;
   check_match_params(p);
@@ -960,8 +970,8 @@ void features_match_dev(wfk_ctx* c, const wfk_feature* cur, int nc, const wfk_fe
     throw Error(WFK_E_INVALID_ARG, "feature store too large");
   cudaStream_t s = c->stream;
   const int n = int(ns);
-  uint32_t* key = fd.skey.ensure(2 * size_t(n));
-  int32_t* idx = fd.sidx.ensure(2 * size_t(n));
+  uint32_t* key = fd.skey.ensure(2 * cap_for(size_t(n)));
+  int32_t* idx = fd.sidx.ensure(2 * cap_for(size_t(n)));
   k_match_keys<<<grid_for(n), kBlock, 0, s>>>(n, st, key, idx);
   size_t tb = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tb, key, key + n, idx, idx + n, n, 0, 32, s);
@@ -983,12 +993,12 @@ void features_match_dev(wfk_ctx* c, const wfk_feature* cur, int nc, const wfk_fe
   a.tau_desc = p.tau_descriptor;
   a.tau_px = p.tau_pixels;
   a.tau_3d = p.tau_3d;
-  a.dist = fd.dist.ensure(size_t(n) * size_t(nc));
-  int32_t* rows = fd.mpos.ensure(2 * size_t(n) + 2);
+  a.dist = nullptr;  // set below when a group's distance tile can exceed shared memory
+  int32_t* rows = fd.mpos.ensure(2 * cap_for(size_t(n) + 1));
   a.best_row = rows + n + 1;
-  a.best_row_d = fd.row_d.ensure(size_t(n));
-  a.out = fd.mslot.ensure(size_t(n) * size_t(a.slot));
-  a.cnt = fd.mcnt.ensure(size_t(n) + 1);
+  a.best_row_d = fd.row_d.ensure(cap_for(size_t(n)));
+  a.out = fd.mslot.ensure(cap_for(size_t(n)) * size_t(a.slot));
+  a.cnt = fd.mcnt.ensure(cap_for(size_t(n) + 1));
   // shared memory: transposed current descriptors, best rows of groups up to
   // 1024 features, candidates, and the group's distance tile when it fits
   const int row_cap = 1024;
@@ -996,6 +1006,7 @@ void features_match_dev(wfk_ctx* c, const wfk_feature* cur, int nc, const wfk_fe
   if (L0.total > 160 * 1024) throw Error(WFK_E_INVALID_ARG, "too many current features for the matcher");
   a.tile_cap = int(std::min<size_t>((200 * 1024 - L0.total) / 8, 16384));
   const MatchSmem L(nc, a.max_cand, row_cap, a.tile_cap);
+  if (max_group * nc > a.tile_cap) a.dist = fd.dist.ensure(cap_for(size_t(n) * size_t(nc)));
   WFK_CUDA(cudaFuncSetAttribute(k_match_groups, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.total)));
   WFK_CUDA(cudaMemsetAsync(a.cnt + n, 0, 4, s));
   k_match_groups<<<n, kMatchBlock, L.total, s>>>(a, L);
@@ -1007,7 +1018,7 @@ void features_match_dev(wfk_ctx* c, const wfk_feature* cur, int nc, const wfk_fe
   WFK_CUDA(cudaStreamSynchronize(s));
   fd.n_matches = c->h_pinned[0];
   if (fd.n_matches > 0) {
-    wfk_feature_match* m = fd.matches.ensure(size_t(fd.n_matches));
+    wfk_feature_match* m = fd.matches.ensure(cap_for(size_t(fd.n_matches)));
     k_match_scatter<<<grid_for(n), kBlock, 0, s>>>(n, a.slot, a.out, a.cnt, pos, m);
     count_launch(c);
   }
@@ -1023,13 +1034,16 @@ void features_match_host(wfk_ctx* c, const wfk_feature* cur, int32_t nc, const w
   *n_out = 0;
   if (nc < 0 || ns < 0 || (nc > 0 && !cur) || (ns > 0 && (!st || !pred))) throw Error(WFK_E_INVALID_ARG, "bad arrays");
   if (nc == 0 || ns == 0) return;
-  wfk_feature* dcur = fd.lift.ensure(size_t(nc));
+  wfk_feature* dcur = fd.lift.ensure(cap_for(size_t(nc)));
   wfk_feature* dst = fd.xstore.ensure(size_t(ns));
-  double* dp = fd.pred.ensure(3 * size_t(ns));
+  double* dp = fd.pred.ensure(3 * cap_for(size_t(ns)));
   WFK_CUDA(cudaMemcpyAsync(dcur, cur, size_t(nc) * sizeof(wfk_feature), cudaMemcpyHostToDevice, s));
   WFK_CUDA(cudaMemcpyAsync(dst, st, size_t(ns) * sizeof(wfk_feature), cudaMemcpyHostToDevice, s));
   WFK_CUDA(cudaMemcpyAsync(dp, pred, 3 * size_t(ns) * 8, cudaMemcpyHostToDevice, s));
-  features_match_dev(c, dcur, nc, dst, ns, dp, K, p);
+  std::map<int32_t, int64_t> groups;  // frame id -> entries (sizes the fallback distance area)
+  int64_t max_group = 0;
+  for (int32_t i = 0; i < ns; ++i) max_group = std::max(max_group, ++groups[st[i].frame_id]);
+  features_match_dev(c, dcur, nc, dst, ns, dp, K, p, max_group);
   *n_out = fd.n_matches;
   if (fd.n_matches > cap) throw Error(WFK_E_CAPACITY, "match buffer too small");
   if (fd.n_matches > 0 && out) {
@@ -1052,17 +1066,17 @@ void features_frame_sparse(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose& 
   k_feat_world<<<grid_for(fd.n_cur, 64), 64, 0, s>>>(fd.n_cur, fd.cur, f.K.width, f.K.height, f.point, f.pvalid);
   count_launch(c);
   if (fd.n_store == 0) return;
-  double* pred = fd.pred.ensure(3 * size_t(fd.n_store));
+  double* pred = fd.pred.ensure(3 * cap_for(size_t(fd.n_store)));
   k_feat_predict<<<grid_for(fd.n_store), kBlock, 0, s>>>(fd.n_store, fd.store, c->vol.g, c->vol.deformed,
                                                         pose_dev(pose), pred);
   count_launch(c);
-  features_match_dev(c, fd.cur, fd.n_cur, fd.store, fd.n_store, pred, K, p);
+  features_match_dev(c, fd.cur, fd.n_cur, fd.store, fd.n_store, pred, K, p, fd.max_group);
   *match_count = fd.n_matches;
   if (fd.n_matches == 0) return;
   fd.n_sparse = fd.n_matches;
   k_sparse_records<<<grid_for(fd.n_sparse, 64), 64, 0, s>>>(fd.n_sparse, fd.matches, fd.cur, fd.store, c->vol.g,
-                                                           fd.sparse.ensure(size_t(fd.n_sparse)),
-                                                           fd.sparse_ok.ensure(size_t(fd.n_sparse)));
+                                                           fd.sparse.ensure(cap_for(size_t(fd.n_sparse))),
+                                                           fd.sparse_ok.ensure(cap_for(size_t(fd.n_sparse))));
   count_launch(c);
   WFK_CUDA(cudaGetLastError());
 }
@@ -1119,10 +1133,10 @@ int32_t features_add(wfk_ctx* c, const wfk_pose& pose, int32_t frame_id, bool bo
   a.deformed = c->vol.deformed;
   a.pose = pose_dev(pose);
   a.frame_id = frame_id;
-  a.out = fd.lift.ensure(size_t(fd.n_cur));
-  a.ok = fd.lift_ok.ensure(size_t(fd.n_cur));
+  a.out = fd.lift.ensure(cap_for(size_t(fd.n_cur)));
+  a.ok = fd.lift_ok.ensure(cap_for(size_t(fd.n_cur)));
   k_feat_lift<<<grid_for(a.n, 64), 64, 0, s>>>(a);
-  fd.store.grow_keep(size_t(fd.n_store + fd.n_cur), s);
+  fd.store.grow_keep(cap_for(size_t(fd.n_store + fd.n_cur)), s);
   int32_t* added = fd.cnt.ensure(4) + 3;
   k_compact_ordered<wfk_feature><<<1, kCompactBlock, 0, s>>>(nullptr, a.n, a.out, a.ok, fd.store.p + fd.n_store,
                                                               added);
@@ -1130,6 +1144,7 @@ int32_t features_add(wfk_ctx* c, const wfk_pose& pose, int32_t frame_id, bool bo
   WFK_CUDA(cudaMemcpyAsync(c->h_pinned, added, 4, cudaMemcpyDeviceToHost, s));
   WFK_CUDA(cudaStreamSynchronize(s));
   fd.n_store += c->h_pinned[0];
+  fd.max_group = std::max<int64_t>(fd.max_group, c->h_pinned[0]);
   return c->h_pinned[0];
 }
 
@@ -1141,6 +1156,9 @@ void features_store_upload(wfk_ctx* c, const wfk_feature* in, int64_t n) {
     WFK_CUDA(cudaMemcpyAsync(fd.store.p, in, size_t(n) * sizeof(wfk_feature), cudaMemcpyHostToDevice, c->stream));
   WFK_CUDA(cudaStreamSynchronize(c->stream));
   fd.n_store = n;
+  std::map<int32_t, int64_t> groups;
+  fd.max_group = 0;
+  for (int64_t i = 0; i < n; ++i) fd.max_group = std::max(fd.max_group, ++groups[in[i].frame_id]);
 }
 
 void features_store_download(wfk_ctx* c, wfk_feature* out, int64_t cap, int64_t* n_out) {

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -28,6 +29,12 @@ struct Error : std::runtime_error {
                          std::string(#call) + ": " + cudaGetErrorString(e_));            \
   } while (0)
 
+// WFK_ALLOC_TRACE=1: log every device (re)allocation of a DevBuf to stderr
+inline bool alloc_trace() {
+  static const bool on = std::getenv("WFK_ALLOC_TRACE") != nullptr;
+  return on;
+}
+
 // Growable device buffer (capacity only grows; contents not preserved).
 template <class T>
 struct DevBuf {
@@ -46,6 +53,7 @@ struct DevBuf {
       p = nullptr;
       size_t want = n + n / 4;
       WFK_CUDA(cudaMalloc(&p, want * sizeof(T)));
+      if (alloc_trace()) fprintf(stderr, "[wfk alloc] ensure %zu x %zu B\n", want, sizeof(T));
       cap = want;
     }
     return p;
@@ -56,6 +64,7 @@ struct DevBuf {
     T* q = nullptr;
     size_t want = n + n / 4;
     WFK_CUDA(cudaMalloc(&q, want * sizeof(T)));
+    if (alloc_trace()) fprintf(stderr, "[wfk alloc] grow_keep %zu x %zu B\n", want, sizeof(T));
     if (p) {
       WFK_CUDA(cudaMemcpyAsync(q, p, cap * sizeof(T), cudaMemcpyDeviceToDevice, s));
       WFK_CUDA(cudaStreamSynchronize(s));
@@ -208,6 +217,7 @@ struct FeatDev {
   // FeatureStore (features.hpp:79-95): append-only history, frame ids ascending
   DevBuf<wfk_feature> store;
   int64_t n_store = 0;
+  int64_t max_group = 0;  // largest frame group (sizes the matcher's fallback distance area)
   // matching scratch (match_features, features.cpp:354-433)
   DevBuf<double> pred, dist, row_d;
   DevBuf<wfk_feature> xstore;  // wfk_match_features' store upload

@@ -35,7 +35,8 @@ void features_detect(wfk_ctx* c, const wfk_feature_params& p, wfk_feature* out, 
                      int32_t* n_kp_out);
 void features_level(wfk_ctx* c, int o, int l, int dog, float* out, int32_t* w, int32_t* h);
 void features_match_dev(wfk_ctx* c, const wfk_feature* cur, int nc, const wfk_feature* st, int64_t ns,
-                        const double* pred, const wfk_intrinsics& K, const wfk_feature_params& p);
+                        const double* pred, const wfk_intrinsics& K, const wfk_feature_params& p,
+                        int64_t max_group);
 void features_match_host(wfk_ctx* c, const wfk_feature* cur, int32_t nc, const wfk_feature* st, int32_t ns,
                          const double* pred, const wfk_intrinsics& K, const wfk_feature_params& p,
                          wfk_feature_match* out, int32_t cap, int32_t* n_out);
