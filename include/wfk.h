@@ -97,6 +97,29 @@ int wfk_build_normal_equations(wfk_ctx* ctx, const wfk_pose* pose, const wfk_sol
 int wfk_pcg_solve(wfk_ctx* ctx, int32_t rows, const double* blocks, const int32_t* cols,
                   const double* rhs, double* x, double tol, int32_t max_iters, int32_t exec,
                   wfk_pcg_result* out);
+
+/* ---- slab-partitioned PCG ------------------------------------
+ * pcg_solve with the rows split into contiguous ranges, one per rank (rows are
+ * in lattice order, so a range is a z-slab): per iteration each rank applies A
+ * to its rows, exchanges the halo rows of p with their owners and all-gathers
+ * its partial dots, summed in rank order on every rank.  Every rank passes the
+ * full system and receives the full x.
+ *   wfk_dist_unique_id: an NCCL unique id (rank 0; share it, e.g. through
+ *     torch.distributed); wfk_dist_init: join the communicator (world 1 needs no id).
+ *   wfk_pcg_solve_dist: the partitioned solve over NCCL (one process per GPU).
+ *   wfk_pcg_solve_slabs: the same partition run by one process on its GPU as
+ *     `slabs` slab states with device copies for the halos (single-GPU check).
+ *   wfk_dist_plan: the partition (host only): ranges[2 * world] = {lo, hi} per
+ *     rank, xfers[4 * n] = {src, dst, row_lo, row_hi} halo transfers. */
+int wfk_dist_unique_id(uint8_t* id /* 128 bytes */);
+int wfk_dist_init(wfk_ctx* ctx, int32_t rank, int32_t world, const uint8_t* id);
+int wfk_pcg_solve_dist(wfk_ctx* ctx, int32_t rows, const double* blocks, const int32_t* cols,
+                       const double* rhs, double* x, double tol, int32_t max_iters, wfk_pcg_result* out);
+int wfk_pcg_solve_slabs(wfk_ctx* ctx, int32_t slabs, int32_t rows, const double* blocks,
+                        const int32_t* cols, const double* rhs, double* x, double tol, int32_t max_iters,
+                        wfk_pcg_result* out);
+int wfk_dist_plan(int32_t rows, const int32_t* cols, int32_t world, int32_t* ranges, int32_t* xfers,
+                  int32_t cap, int32_t* n_xfers);
 /* NormalEquations::multiply (solver.cpp:71-89) on an explicit system */
 int wfk_ne_multiply(wfk_ctx* ctx, int32_t rows, const double* blocks, const int32_t* cols,
                     const double* x, double* y);

@@ -162,6 +162,7 @@ void wfk_destroy(wfk_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  wfk::dist_destroy(c);
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   for (cudaEvent_t e : c->prof.ev)
     if (e) cudaEventDestroy(e);
@@ -348,6 +349,50 @@ int wfk_pcg_solve(wfk_ctx* c, int32_t rows, const double* blocks, const int32_t*
   return guard(c, [&] {
     if (rows < 0 || (rows > 0 && (!blocks || !cols || !rhs || !x))) throw Error(WFK_E_INVALID_ARG, "bad system");
     solver_pcg_assembled(c, rows, blocks, cols, rhs, x, tol, max_iters, 0, out, nullptr);
+  });
+}
+
+int wfk_dist_unique_id(uint8_t* out) {
+  if (!out) return WFK_E_INVALID_ARG;
+  try {
+    dist_unique_id(out);
+  } catch (const Error& e) {
+    return e.code;
+  }
+  return WFK_OK;
+}
+
+int wfk_dist_init(wfk_ctx* c, int32_t rank, int32_t world, const uint8_t* id) {
+  return guard(c, [&] {
+    if (world > 1 && !id) throw Error(WFK_E_INVALID_ARG, "null NCCL id");
+    dist_init(c, rank, world, id);
+  });
+}
+
+int wfk_dist_plan(int32_t rows, const int32_t* cols, int32_t world, int32_t* ranges, int32_t* xfers, int32_t cap,
+                  int32_t* n_xfers) {
+  if (!n_xfers) return WFK_E_INVALID_ARG;
+  try {
+    dist_plan(rows, cols, world, ranges, xfers, cap, n_xfers);
+  } catch (const Error& e) {
+    return e.code;
+  }
+  return WFK_OK;
+}
+
+int wfk_pcg_solve_dist(wfk_ctx* c, int32_t rows, const double* blocks, const int32_t* cols, const double* rhs,
+                       double* x, double tol, int32_t max_iters, wfk_pcg_result* out) {
+  return guard(c, [&] {
+    if (rows < 0 || (rows > 0 && (!blocks || !cols || !rhs || !x))) throw Error(WFK_E_INVALID_ARG, "bad system");
+    dist_pcg(c, rows, blocks, cols, rhs, x, tol, max_iters, out);
+  });
+}
+
+int wfk_pcg_solve_slabs(wfk_ctx* c, int32_t slabs, int32_t rows, const double* blocks, const int32_t* cols,
+                        const double* rhs, double* x, double tol, int32_t max_iters, wfk_pcg_result* out) {
+  return guard(c, [&] {
+    if (rows < 0 || (rows > 0 && (!blocks || !cols || !rhs || !x))) throw Error(WFK_E_INVALID_ARG, "bad system");
+    slabs_pcg(c, slabs, rows, blocks, cols, rhs, x, tol, max_iters, out);
   });
 }
 

@@ -16,6 +16,8 @@
 
 namespace wfk {
 
+struct DistComm;  // dist.cu: rank, world, NCCL communicator
+
 struct Error : std::runtime_error {
   int code;
   Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
@@ -292,6 +294,7 @@ struct wfk_ctx {
   wfk::DevBuf<double> icp_src, icp_part;
   wfk::DevBuf<uint8_t> icp_state;
   int coop_blocks = 0;          // resident blocks for cooperative kernels
+  wfk::DistComm* dist = nullptr;  // slab-partitioned PCG (wfk_dist_init)
 };
 
 namespace wfk {

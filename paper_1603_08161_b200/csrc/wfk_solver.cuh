@@ -44,6 +44,14 @@ void features_frame_sparse(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose& 
                            int32_t* match_count);
 int64_t features_append_sparse(wfk_ctx* c);
 int32_t features_add(wfk_ctx* c, const wfk_pose& pose, int32_t frame_id, bool bootstrap);
+void dist_destroy(wfk_ctx* c);
+void dist_unique_id(uint8_t* out);
+void dist_init(wfk_ctx* c, int rank, int world, const uint8_t* id_bytes);
+void dist_plan(int N, const int32_t* cols, int world, int32_t* ranges, int32_t* xfers, int32_t cap, int32_t* n_xfers);
+void dist_pcg(wfk_ctx* c, int N, const double* blocks, const int32_t* cols, const double* rhs, double* x, double tol,
+              int max_iters, wfk_pcg_result* res);
+void slabs_pcg(wfk_ctx* c, int slabs, int N, const double* blocks, const int32_t* cols, const double* rhs, double* x,
+               double tol, int max_iters, wfk_pcg_result* res);
 void features_store_upload(wfk_ctx* c, const wfk_feature* in, int64_t n);
 void features_store_download(wfk_ctx* c, wfk_feature* out, int64_t cap, int64_t* n_out);
 void volume_invert_warp(wfk_ctx* c, const wfk_pose* pose, int64_t n, const double* y, const double* seed,

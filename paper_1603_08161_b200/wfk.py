@@ -107,6 +107,33 @@ def _cptr(a):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
 
 
+def dist_unique_id() -> bytes:
+    """An NCCL unique id for wfk_dist_init (rank 0 creates it and shares it)."""
+    buf = (C.c_uint8 * 128)()
+    rc = lib().wfk_dist_unique_id(buf)
+    if rc != WFK_OK:
+        raise WfkError(rc, "wfk_dist_unique_id failed (NCCL unavailable?)")
+    return bytes(buf)
+
+
+def dist_plan(cols, world: int):
+    """The z-slab partition of a system's rows (host only, no GPU): ranges
+    (world x 2: lo, hi) and the halo transfers (n x 4: src, dst, row_lo, row_hi)."""
+    cols = np.ascontiguousarray(cols, np.int32).reshape(-1, 27)
+    ranges = np.zeros((world, 2), np.int32)
+    n = C.c_int32()
+    rc = lib().wfk_dist_plan(C.c_int32(len(cols)), _cptr(cols), C.c_int32(world), _cptr(ranges), None, 0,
+                             C.byref(n))
+    if rc != WFK_OK:
+        raise WfkError(rc, "wfk_dist_plan failed")
+    xf = np.zeros((max(n.value, 1), 4), np.int32)
+    rc = lib().wfk_dist_plan(C.c_int32(len(cols)), _cptr(cols), C.c_int32(world), _cptr(ranges), _cptr(xf),
+                             C.c_int32(len(xf)), C.byref(n))
+    if rc != WFK_OK:
+        raise WfkError(rc, "wfk_dist_plan failed")
+    return ranges, xf[: n.value]
+
+
 class _Pinned:
     def __init__(self, nbytes):
         p = C.c_void_p()
@@ -256,6 +283,35 @@ class Context:
         self._check(lib().wfk_pcg_solve(self.h, C.c_int32(len(cols)), _cptr(blocks), _cptr(cols), _cptr(rhs),
                                         _cptr(x), C.c_double(tol), C.c_int32(max_iters), C.c_int32(1),
                                         C.byref(res)))
+        return x, res.iterations, res.relative_residual
+
+    # ---- slab-partitioned PCG ----------------------------------
+    def dist_init(self, rank: int, world: int, nccl_id: bytes | None = None):
+        """Join the NCCL communicator of a partitioned solve (world 1: no id needed)."""
+        buf = None if nccl_id is None else (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+        self._check(lib().wfk_dist_init(self.h, C.c_int32(rank), C.c_int32(world), buf))
+
+    def pcg_solve_dist(self, blocks, cols, rhs, x, tol, max_iters):
+        """pcg_solve with this rank's z-slab of the rows; returns the full x."""
+        blocks = np.ascontiguousarray(blocks, np.float64)
+        cols = np.ascontiguousarray(cols, np.int32)
+        rhs = np.ascontiguousarray(rhs, np.float64)
+        x = np.ascontiguousarray(x, np.float64).copy()
+        res = PcgResult()
+        self._check(lib().wfk_pcg_solve_dist(self.h, C.c_int32(len(cols)), _cptr(blocks), _cptr(cols), _cptr(rhs),
+                                             _cptr(x), C.c_double(tol), C.c_int32(max_iters), C.byref(res)))
+        return x, res.iterations, res.relative_residual
+
+    def pcg_solve_slabs(self, slabs, blocks, cols, rhs, x, tol, max_iters):
+        """The same partition run on this GPU as `slabs` slab states (halo copies on the device)."""
+        blocks = np.ascontiguousarray(blocks, np.float64)
+        cols = np.ascontiguousarray(cols, np.int32)
+        rhs = np.ascontiguousarray(rhs, np.float64)
+        x = np.ascontiguousarray(x, np.float64).copy()
+        res = PcgResult()
+        self._check(lib().wfk_pcg_solve_slabs(self.h, C.c_int32(slabs), C.c_int32(len(cols)), _cptr(blocks),
+                                              _cptr(cols), _cptr(rhs), _cptr(x), C.c_double(tol),
+                                              C.c_int32(max_iters), C.byref(res)))
         return x, res.iterations, res.relative_residual
 
     def ne_multiply(self, blocks, cols, x):
