@@ -98,6 +98,28 @@ int wfk_pcg_solve(wfk_ctx* ctx, int32_t rows, const double* blocks, const int32_
                   const double* rhs, double* x, double tol, int32_t max_iters, int32_t exec,
                   wfk_pcg_result* out);
 
+/* ---- snapshot and frame formats -------------------------
+ * DeformableVolume::save / load (volume.cpp:150-217; volume.hpp:99-100): the
+ * "WFVOL01\n" snapshot (60-byte header, one interleaved 73-byte record per
+ * point), packed from / unpacked into the context's lattice on the device.
+ * Load replaces the lattice (dims, voxel, origin, truncation and every field).
+ * pack / unpack: the same byte image in memory (size query: out = NULL). */
+int wfk_volume_save(wfk_ctx* ctx, const char* path);
+int wfk_volume_load(wfk_ctx* ctx, const char* path);
+int wfk_volume_pack(wfk_ctx* ctx, uint8_t* out, int64_t cap, int64_t* n_out);
+int wfk_volume_unpack(wfk_ctx* ctx, const uint8_t* in, int64_t n);
+/* FeatureStore::save / load (features.cpp:306-352; features.hpp:90-91), "WFFEAT1\n" */
+int wfk_feature_store_save(wfk_ctx* ctx, const char* path);
+int wfk_feature_store_load(wfk_ctx* ctx, const char* path);
+/* load_depth_pgm + load_color_ppm (image.cpp:71-121) decoded on the device into
+ * the context's frame (color_ppm may be NULL; the images must be intr's size);
+ * save_depth_pgm / save_color_ppm (image.cpp:55-104) of the context's frame
+ * (either path may be NULL); wfk_frame_download reads the frame back. */
+int wfk_frame_load_pnm(wfk_ctx* ctx, const char* depth_pgm, const char* color_ppm,
+                       const wfk_intrinsics* intr);
+int wfk_frame_save_pnm(wfk_ctx* ctx, const char* depth_pgm, const char* color_ppm);
+int wfk_frame_download(wfk_ctx* ctx, float* depth, float* color);
+
 /* ---- slab-partitioned PCG ------------------------------------
  * pcg_solve with the rows split into contiguous ranges, one per rank (rows are
  * in lattice order, so a range is a z-slab): per iteration each rank applies A

@@ -592,3 +592,58 @@ class Reconstructor:
         fv = frame.view()
         _check(lib().wfo_recon_process_frame(self.h, C.byref(fv), _cptr(s), C.c_int64(n), C.byref(rec)))
         return rec
+
+
+# ---- snapshot / frame formats (wf_formats.cpp) ------------------------------------
+def _bytes_call(fn, *args):
+    n = C.c_int64()
+    _check(fn(*args, None, C.c_int64(0), C.byref(n)))
+    out = np.zeros(n.value, np.uint8)
+    _check(fn(*args, _cptr(out), C.c_int64(n.value), C.byref(n)))
+    return out.tobytes()
+
+
+def volume_save_bytes(vol) -> bytes:
+    """DeformableVolume::save (volume.cpp:150-178) as bytes."""
+    vv = vol.view()
+    return _bytes_call(lib().wfo_volume_save_bytes, C.byref(vv))
+
+
+def volume_load_bytes(image: bytes):
+    """DeformableVolume::load (volume.cpp:180-217) from bytes."""
+    from paper_1603_08161_b200.abi import Volume as _V, VolumeView as _VV
+    buf = np.frombuffer(image, np.uint8)
+    hv = _VV()
+    _check(lib().wfo_volume_load_bytes(_cptr(buf), C.c_int64(len(buf)), C.byref(hv)))
+    v = _V(tuple(hv.dims), hv.voxel_size, tuple(hv.origin))
+    vv = v.view()
+    _check(lib().wfo_volume_load_bytes(_cptr(buf), C.c_int64(len(buf)), C.byref(vv)))
+    v.truncation = vv.truncation
+    return v
+
+
+def feature_store_bytes(features) -> bytes:
+    """FeatureStore::save (features.cpp:306-323) as bytes."""
+    f = np.ascontiguousarray(features, FEATURE_DTYPE)
+    return _bytes_call(lib().wfo_feature_store_bytes, _cptr(f), C.c_int32(len(f)))
+
+
+def pgm_encode(depth) -> bytes:
+    d = np.ascontiguousarray(depth, np.float32)
+    return _bytes_call(lib().wfo_pgm_encode, _cptr(d), C.c_int32(d.shape[1]), C.c_int32(d.shape[0]))
+
+
+def ppm_encode(color) -> bytes:
+    c = np.ascontiguousarray(color, np.float32)
+    return _bytes_call(lib().wfo_ppm_encode, _cptr(c), C.c_int32(c.shape[1]), C.c_int32(c.shape[0]))
+
+
+def pnm_decode(image: bytes, channels: int):
+    buf = np.frombuffer(image, np.uint8)
+    w, h = C.c_int32(), C.c_int32()
+    _check(lib().wfo_pnm_decode(_cptr(buf), C.c_int64(len(buf)), C.c_int32(channels), C.byref(w), C.byref(h), None))
+    shape = (h.value, w.value) if channels == 1 else (h.value, w.value, 3)
+    out = np.zeros(shape, np.float32)
+    _check(lib().wfo_pnm_decode(_cptr(buf), C.c_int64(len(buf)), C.c_int32(channels), C.byref(w), C.byref(h),
+                                _cptr(out)))
+    return out

@@ -174,6 +174,15 @@ int wfo_recon_process_frame(wfo_recon* r, const wfk_frame_view* frame,
 /* the reconstructor's FeatureStore (copies n_out <= cap entries when out != NULL) */
 int wfo_recon_feature_store(const wfo_recon* r, wfk_feature* out, int64_t cap, int64_t* n_out);
 
+/* snapshot / frame formats (wf_formats.cpp): volume.cpp:150-217,
+ * features.cpp:306-352, image.cpp:21-121 */
+int wfo_volume_save_bytes(const wfk_volume_view* v, uint8_t* out, int64_t cap, int64_t* n_out);
+int wfo_volume_load_bytes(const uint8_t* in, int64_t n, wfk_volume_view* v);
+int wfo_feature_store_bytes(const wfk_feature* f, int32_t nf, uint8_t* out, int64_t cap, int64_t* n_out);
+int wfo_pgm_encode(const float* depth, int32_t w, int32_t h, uint8_t* out, int64_t cap, int64_t* n_out);
+int wfo_ppm_encode(const float* color, int32_t w, int32_t h, uint8_t* out, int64_t cap, int64_t* n_out);
+int wfo_pnm_decode(const uint8_t* in, int64_t n, int32_t channels, int32_t* w, int32_t* h, float* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -352,6 +352,37 @@ int wfk_pcg_solve(wfk_ctx* c, int32_t rows, const double* blocks, const int32_t*
   });
 }
 
+int wfk_volume_save(wfk_ctx* c, const char* path) {
+  return guard(c, [&] { volume_save(c, path); });
+}
+int wfk_volume_load(wfk_ctx* c, const char* path) {
+  return guard(c, [&] { volume_load(c, path); });
+}
+int wfk_volume_pack(wfk_ctx* c, uint8_t* out, int64_t cap, int64_t* n_out) {
+  return guard(c, [&] { volume_pack(c, out, cap, n_out); });
+}
+int wfk_volume_unpack(wfk_ctx* c, const uint8_t* in, int64_t n) {
+  return guard(c, [&] { volume_unpack(c, in, n); });
+}
+int wfk_feature_store_save(wfk_ctx* c, const char* path) {
+  return guard(c, [&] { feature_store_save(c, path); });
+}
+int wfk_feature_store_load(wfk_ctx* c, const char* path) {
+  return guard(c, [&] { feature_store_load(c, path); });
+}
+int wfk_frame_load_pnm(wfk_ctx* c, const char* depth_pgm, const char* color_ppm, const wfk_intrinsics* intr) {
+  return guard(c, [&] {
+    if (!depth_pgm || !intr) throw Error(WFK_E_INVALID_ARG, "null argument");
+    frame_load_pnm(c, depth_pgm, color_ppm, *intr);
+  });
+}
+int wfk_frame_save_pnm(wfk_ctx* c, const char* depth_pgm, const char* color_ppm) {
+  return guard(c, [&] { frame_save_pnm(c, depth_pgm, color_ppm); });
+}
+int wfk_frame_download(wfk_ctx* c, float* depth, float* color) {
+  return guard(c, [&] { frame_download(c, depth, color); });
+}
+
 int wfk_dist_unique_id(uint8_t* out) {
   if (!out) return WFK_E_INVALID_ARG;
   try {

@@ -44,6 +44,16 @@ void features_frame_sparse(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose& 
                            int32_t* match_count);
 int64_t features_append_sparse(wfk_ctx* c);
 int32_t features_add(wfk_ctx* c, const wfk_pose& pose, int32_t frame_id, bool bootstrap);
+int64_t volume_image_bytes(wfk_ctx* c);
+void volume_pack(wfk_ctx* c, uint8_t* out, int64_t cap, int64_t* n_out);
+void volume_unpack(wfk_ctx* c, const uint8_t* in, int64_t n);
+void volume_save(wfk_ctx* c, const char* path);
+void volume_load(wfk_ctx* c, const char* path);
+void feature_store_save(wfk_ctx* c, const char* path);
+void feature_store_load(wfk_ctx* c, const char* path);
+void frame_load_pnm(wfk_ctx* c, const char* depth_path, const char* color_path, const wfk_intrinsics& K);
+void frame_save_pnm(wfk_ctx* c, const char* depth_path, const char* color_path);
+void frame_download(wfk_ctx* c, float* depth, float* color);
 void dist_destroy(wfk_ctx* c);
 void dist_unique_id(uint8_t* out);
 void dist_init(wfk_ctx* c, int rank, int world, const uint8_t* id_bytes);

@@ -205,6 +205,52 @@ class Context:
         vv = vol.view()
         self._check(lib().wfk_volume_download(self.h, C.byref(vv), C.c_uint32(fields)))
 
+    # ---- snapshot / frame formats -----------------------
+    def save_volume(self, path: str):
+        """DeformableVolume::save (volume.cpp:150-178) of the device lattice."""
+        self._check(lib().wfk_volume_save(self.h, os.fsencode(path)))
+
+    def load_volume(self, path: str):
+        """DeformableVolume::load (volume.cpp:180-217) into the device lattice."""
+        self._check(lib().wfk_volume_load(self.h, os.fsencode(path)))
+        self.dims = self.volume_dims()
+
+    def volume_dims(self):
+        img = self.pack_volume(header_only=True)
+        return tuple(int(d) for d in np.frombuffer(img[8:20], np.int32))
+
+    def pack_volume(self, header_only: bool = False) -> bytes:
+        n = C.c_int64()
+        self._check(lib().wfk_volume_pack(self.h, None, C.c_int64(0), C.byref(n)))
+        out = np.zeros(n.value, np.uint8)
+        self._check(lib().wfk_volume_pack(self.h, _cptr(out), C.c_int64(n.value), C.byref(n)))
+        return out[:60].tobytes() if header_only else out.tobytes()
+
+    def unpack_volume(self, image: bytes):
+        buf = np.frombuffer(image, np.uint8)
+        self._check(lib().wfk_volume_unpack(self.h, _cptr(buf), C.c_int64(len(buf))))
+        self.dims = self.volume_dims()
+
+    def save_feature_store(self, path: str):
+        self._check(lib().wfk_feature_store_save(self.h, os.fsencode(path)))
+
+    def load_feature_store(self, path: str):
+        self._check(lib().wfk_feature_store_load(self.h, os.fsencode(path)))
+
+    def load_frame_pnm(self, depth_pgm: str, color_ppm, intr):
+        self._check(lib().wfk_frame_load_pnm(self.h, os.fsencode(depth_pgm),
+                                             None if color_ppm is None else os.fsencode(color_ppm), C.byref(intr)))
+
+    def save_frame_pnm(self, depth_pgm, color_ppm):
+        self._check(lib().wfk_frame_save_pnm(self.h, None if depth_pgm is None else os.fsencode(depth_pgm),
+                                             None if color_ppm is None else os.fsencode(color_ppm)))
+
+    def download_frame(self, width: int, height: int, color: bool = True):
+        d = np.zeros((height, width), np.float32)
+        c = np.zeros((height, width, 3), np.float32) if color else None
+        self._check(lib().wfk_frame_download(self.h, _cptr(d), _cptr(c)))
+        return d, c
+
     # ---- solver ------------------------------------------------------------
     def compute_active_set(self, want_list: bool = True):
         n = C.c_int64()
