@@ -140,6 +140,16 @@ int wfk_pcg_solve_dist(wfk_ctx* ctx, int32_t rows, const double* blocks, const i
 int wfk_pcg_solve_slabs(wfk_ctx* ctx, int32_t slabs, int32_t rows, const double* blocks,
                         const int32_t* cols, const double* rhs, double* x, double tol, int32_t max_iters,
                         wfk_pcg_result* out);
+/* solve_coarse_to_fine (solver.cpp:505-534) with every level's PCG partitioned
+ * as above: the replicated lattice, hierarchy, normal-equation assembly,
+ * write-back, Procrustes fit and energy run identically on every rank; the
+ * PCG runs on the rank's slab.  _dist: the context's communicator; _slabs:
+ * `slabs` slab states on this GPU. */
+int wfk_solve_coarse_to_fine_dist(wfk_ctx* ctx, const wfk_pose* pose, const wfk_solver_params* p,
+                                  wfk_trace_entry* trace, int32_t cap, int32_t* n_out);
+int wfk_solve_coarse_to_fine_slabs(wfk_ctx* ctx, int32_t slabs, const wfk_pose* pose,
+                                   const wfk_solver_params* p, wfk_trace_entry* trace, int32_t cap,
+                                   int32_t* n_out);
 int wfk_dist_plan(int32_t rows, const int32_t* cols, int32_t world, int32_t* ranges, int32_t* xfers,
                   int32_t cap, int32_t* n_xfers);
 /* NormalEquations::multiply (solver.cpp:71-89) on an explicit system */

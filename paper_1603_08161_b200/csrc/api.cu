@@ -335,6 +335,30 @@ int wfk_solve_coarse_to_fine(wfk_ctx* c, const wfk_pose* pose, const wfk_solver_
   return export_trace(c, t, trace, cap, n_out);
 }
 
+int wfk_solve_coarse_to_fine_dist(wfk_ctx* c, const wfk_pose* pose, const wfk_solver_params* p,
+                                  wfk_trace_entry* trace, int32_t cap, int32_t* n_out) {
+  std::vector<wfk_trace_entry> t;
+  const int rc = guard(c, [&] {
+    check_params(p);
+    if (!c->dist) throw Error(WFK_E_INVALID_ARG, "wfk_dist_init first");
+    solver_c2f_dist(c, pose, *p, 0, t);
+  });
+  if (rc != WFK_OK) return rc;
+  return export_trace(c, t, trace, cap, n_out);
+}
+
+int wfk_solve_coarse_to_fine_slabs(wfk_ctx* c, int32_t slabs, const wfk_pose* pose, const wfk_solver_params* p,
+                                   wfk_trace_entry* trace, int32_t cap, int32_t* n_out) {
+  std::vector<wfk_trace_entry> t;
+  const int rc = guard(c, [&] {
+    check_params(p);
+    if (slabs < 1) throw Error(WFK_E_INVALID_ARG, "slabs must be >= 1");
+    solver_c2f_dist(c, pose, *p, slabs, t);
+  });
+  if (rc != WFK_OK) return rc;
+  return export_trace(c, t, trace, cap, n_out);
+}
+
 int wfk_build_normal_equations(wfk_ctx* c, const wfk_pose* pose, const wfk_solver_params* p, wfk_ne_host* out,
                                int32_t* rows_out) {
   return guard(c, [&] {

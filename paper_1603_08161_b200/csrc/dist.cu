@@ -372,30 +372,28 @@ struct NcclTransport : Transport {
   }
 };
 
-// one partitioned pcg_solve; `ranks` = the slab indices run here
-void run_dist_pcg(wfk_ctx* c, int N, int world, const std::vector<int>& ranks, const double* blocks_h,
-                  const int32_t* cols_h, const double* rhs_h, double* x_h, double tol, int max_iters,
-                  wfk_pcg_result* res, Transport& tr) {
+// the partition plan of a device system (D2H of each row's column range)
+DistPlan plan_of(wfk_ctx* c, int N, const int32_t* cols_d, int world) {
   cudaStream_t s = c->stream;
-  // the system, replicated on this device (every rank holds the caller's full system)
-  DevBuf<double> B, RHS;
-  DevBuf<int32_t> CL, MN, MX;
-  B.ensure(size_t(N) * 27 * 9);
-  CL.ensure(size_t(N) * 27);
-  RHS.ensure(size_t(N) * 3);
+  DevBuf<int32_t> MN, MX;
   MN.ensure(size_t(N));
   MX.ensure(size_t(N));
-  WFK_CUDA(cudaMemcpyAsync(B.p, blocks_h, size_t(N) * 27 * 9 * 8, cudaMemcpyHostToDevice, s));
-  WFK_CUDA(cudaMemcpyAsync(CL.p, cols_h, size_t(N) * 27 * 4, cudaMemcpyHostToDevice, s));
-  WFK_CUDA(cudaMemcpyAsync(RHS.p, rhs_h, size_t(N) * 3 * 8, cudaMemcpyHostToDevice, s));
-  k_d_col_range<<<grid_for(N), kBlock, 0, s>>>(N, CL.p, MN.p, MX.p);
+  k_d_col_range<<<grid_for(N), kBlock, 0, s>>>(N, cols_d, MN.p, MX.p);
   count_launch(c);
   std::vector<int32_t> mn(static_cast<size_t>(N)), mx(static_cast<size_t>(N));
   WFK_CUDA(cudaMemcpyAsync(mn.data(), MN.p, size_t(N) * 4, cudaMemcpyDeviceToHost, s));
   WFK_CUDA(cudaMemcpyAsync(mx.data(), MX.p, size_t(N) * 4, cudaMemcpyDeviceToHost, s));
   WFK_CUDA(cudaStreamSynchronize(s));
-  const DistPlan plan = make_plan(N, mn.data(), mx.data(), world);
+  return make_plan(N, mn.data(), mx.data(), world);
+}
 
+// one partitioned pcg_solve of a device-resident system; `ranks` = the slab
+// indices run here; x (device, N x 3) is the initial guess on entry and the
+// full solution on return
+void run_dist_pcg_dev(wfk_ctx* c, int N, int world, const std::vector<int>& ranks, const DistPlan& plan,
+                      const double* B, const int32_t* CL, const double* RHS, double* x, double tol, int max_iters,
+                      wfk_pcg_result* res, Transport& tr) {
+  cudaStream_t s = c->stream;
   std::vector<std::unique_ptr<SlabBufs>> bufs;
   std::vector<DSlab> sl;
   for (int q : ranks) {
@@ -403,9 +401,9 @@ void run_dist_pcg(wfk_ctx* c, int N, int world, const std::vector<int>& ranks, c
     DSlab a;
     a.lo = plan.lo[size_t(q)];
     a.hi = plan.hi[size_t(q)];
-    a.blocks = B.p;
-    a.cols = CL.p;
-    a.rhs = RHS.p;
+    a.blocks = B;
+    a.cols = CL;
+    a.rhs = RHS;
     a.x = b->x.ensure(3 * size_t(N));
     a.r = b->r.ensure(3 * size_t(N));
     a.z = b->z.ensure(3 * size_t(N));
@@ -415,7 +413,7 @@ void run_dist_pcg(wfk_ctx* c, int N, int world, const std::vector<int>& ranks, c
     a.part = b->part.ensure(size_t(kDK) * kDMaxBlocks);
     a.gath = b->gath.ensure(size_t(kDK) * world);
     a.st = b->st.ensure(DS_N);
-    WFK_CUDA(cudaMemcpyAsync(a.x, x_h, size_t(N) * 3 * 8, cudaMemcpyHostToDevice, s));  // x0, replicated
+    WFK_CUDA(cudaMemcpyAsync(a.x, x, size_t(N) * 3 * 8, cudaMemcpyDeviceToDevice, s));  // x0, replicated
     WFK_CUDA(cudaMemsetAsync(a.gath, 0, size_t(kDK) * world * 8, s));
     WFK_CUDA(cudaMemsetAsync(a.st, 0, DS_N * 8, s));
     sl.push_back(a);
@@ -457,7 +455,7 @@ void run_dist_pcg(wfk_ctx* c, int N, int world, const std::vector<int>& ranks, c
   }
   tr.final_x(sl, plan);
   double st_h[DS_N];
-  WFK_CUDA(cudaMemcpyAsync(x_h, sl[0].x, size_t(N) * 3 * 8, cudaMemcpyDeviceToHost, s));
+  WFK_CUDA(cudaMemcpyAsync(x, sl[0].x, size_t(N) * 3 * 8, cudaMemcpyDeviceToDevice, s));
   WFK_CUDA(cudaMemcpyAsync(st_h, sl[0].st, DS_N * 8, cudaMemcpyDeviceToHost, s));
   WFK_CUDA(cudaStreamSynchronize(s));
   WFK_CUDA(cudaGetLastError());
@@ -466,7 +464,72 @@ void run_dist_pcg(wfk_ctx* c, int N, int world, const std::vector<int>& ranks, c
     res->relative_residual = st_h[DS_RELRES];
   }
 }
+
+// host-array system: uploaded (every rank holds the caller's full system), solved, x returned
+void run_dist_pcg(wfk_ctx* c, int N, int world, const std::vector<int>& ranks, const double* blocks_h,
+                  const int32_t* cols_h, const double* rhs_h, double* x_h, double tol, int max_iters,
+                  wfk_pcg_result* res, Transport& tr) {
+  cudaStream_t s = c->stream;
+  DevBuf<double> B, RHS, X;
+  DevBuf<int32_t> CL;
+  B.ensure(size_t(N) * 27 * 9);
+  CL.ensure(size_t(N) * 27);
+  RHS.ensure(size_t(N) * 3);
+  X.ensure(size_t(N) * 3);
+  WFK_CUDA(cudaMemcpyAsync(B.p, blocks_h, size_t(N) * 27 * 9 * 8, cudaMemcpyHostToDevice, s));
+  WFK_CUDA(cudaMemcpyAsync(CL.p, cols_h, size_t(N) * 27 * 4, cudaMemcpyHostToDevice, s));
+  WFK_CUDA(cudaMemcpyAsync(RHS.p, rhs_h, size_t(N) * 3 * 8, cudaMemcpyHostToDevice, s));
+  WFK_CUDA(cudaMemcpyAsync(X.p, x_h, size_t(N) * 3 * 8, cudaMemcpyHostToDevice, s));
+  const DistPlan plan = plan_of(c, N, CL.p, world);
+  run_dist_pcg_dev(c, N, world, ranks, plan, B.p, CL.p, RHS.p, X.p, tol, max_iters, res, tr);
+  WFK_CUDA(cudaMemcpyAsync(x_h, X.p, size_t(N) * 3 * 8, cudaMemcpyDeviceToHost, s));
+  WFK_CUDA(cudaStreamSynchronize(s));
+}
 }  // namespace
+
+// partitioned PCG of a device-resident system (the solver's normal equations).
+// slabs > 0: that many slab states on this GPU; slabs == 0: this rank of the
+// context's communicator.  plan_key identifies the system's row structure: the
+// plan is rebuilt when it changes.
+struct PlanCache {
+  const void* key = nullptr;
+  int N = -1, world = 0;
+  DistPlan plan;
+};
+static PlanCache& plan_cache() {
+  static PlanCache pc;
+  return pc;
+}
+
+void dist_pcg_device(wfk_ctx* c, int slabs, int N, const double* blocks, const int32_t* cols, const double* rhs,
+                     double* x, double tol, int max_iters, const void* plan_key, wfk_pcg_result* res) {
+  if (N <= 0) {
+    if (res) *res = wfk_pcg_result{0, 0, 0.0};
+    return;
+  }
+  DistComm* d = c->dist;
+  if (slabs <= 0 && !d) throw Error(WFK_E_INVALID_ARG, "wfk_dist_init first");
+  const int world = slabs > 0 ? slabs : d->world;
+  PlanCache& pc = plan_cache();
+  if (!plan_key || pc.key != plan_key || pc.N != N || pc.world != world) {
+    pc.plan = plan_of(c, N, cols, world);
+    pc.key = plan_key;
+    pc.N = N;
+    pc.world = world;
+  }
+  std::vector<int> ranks;
+  if (slabs > 0) {
+    for (int q = 0; q < slabs; ++q) ranks.push_back(q);
+    SlabsTransport t(c->stream, slabs);
+    run_dist_pcg_dev(c, N, world, ranks, pc.plan, blocks, cols, rhs, x, tol, max_iters, res, t);
+  } else {
+    ranks.push_back(d->rank);
+    NcclTransport tr(c->stream, d);
+    SlabsTransport single(c->stream, 1);
+    Transport& t = d->comm ? static_cast<Transport&>(tr) : static_cast<Transport&>(single);
+    run_dist_pcg_dev(c, N, world, ranks, pc.plan, blocks, cols, rhs, x, tol, max_iters, res, t);
+  }
+}
 
 void dist_plan(int N, const int32_t* cols, int world, int32_t* ranges, int32_t* xfers, int32_t cap,
                int32_t* n_xfers) {

@@ -2184,7 +2184,7 @@ static int coop_blocks(wfk_ctx* c) {
 static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_params& p, int mode, int level_tag,
                       std::vector<wfk_trace_entry>* out, wfk_energy* e_out) {
   cudaStream_t s = c->stream;
-  const int G = coop_blocks(c);
+  const int G = coop_blocks(c);  // one persistent block per SM (fewer blocks measured slower on every level)
 
   FFArgs a;
   a.g = L.g;
@@ -2621,6 +2621,83 @@ void solver_c2f(wfk_ctx* c, const wfk_pose* pose, const wfk_solver_params& p, st
     tr.report();
     g_trace = nullptr;
   }
+}
+
+// --------------------------------------------------------------------------
+// solve_coarse_to_fine with the PCG partitioned into z-slabs
+// (dist.cu).  Every rank holds the same replicated lattice, so the hierarchy,
+// rows, constraint cache, normal-equation assembly (k_ne_assemble), the
+// write-back, the Procrustes fit and the energy are computed identically on
+// every rank; the PCG -- the per-iteration work -- runs on the rank's slab
+// with NCCL halo exchanges, and its solution is broadcast back to all ranks.
+// flip_flop_solve's control flow (solver.cpp:419-453) is restated on the host.
+// slabs > 0: that many slab states on this GPU (single-GPU check); slabs == 0:
+// the context's communicator (wfk_dist_init).
+// --------------------------------------------------------------------------
+__global__ void k_rows_to_x(int N, const double4* t, double* x) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x)
+    st3(x, r, V3{t[r].x, t[r].y, t[r].z});
+}
+__global__ void k_write_back(int N, const int32_t* rows, const uint8_t* frozen, const double* x, double* f_def) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x)
+    if (!frozen[r]) st3(f_def, rows[r], ld3(x, r));
+}
+
+static void dist_flip_flop(wfk_ctx* c, int l, const PoseD& pose, const wfk_solver_params& p, int slabs,
+                           std::vector<wfk_trace_entry>& trace) {
+  Level& L = c->lv[l];
+  level_rows(c, L);
+  level_constraints(c, L, pose, p);
+  wfk_energy prev;
+  run_level(c, L, pose, p, 1, l, nullptr, &prev);  // evaluate_energy
+  if (prev.total == 0) return;
+  const int N = L.N;
+  cudaStream_t s = c->stream;
+  double* blocks = L.ne_blocks.ensure(size_t(std::max(N, 1)) * 27 * 9);
+  int32_t* cols = L.ne_cols.ensure(size_t(std::max(N, 1)) * 27);
+  double* rhs = L.ne_rhs.ensure(size_t(std::max(N, 1)) * 3);
+  double* x = L.ne_x.ensure(size_t(std::max(N, 1)) * 3);
+  for (int it = 0; it < p.flip_flop_iters; ++it) {
+    wfk_pcg_result pr{0, 0, 0.0};
+    if (N > 0) {
+      k_load_rows<<<grid_for(N), kBlock, 0, s>>>(N, L.rows, L.deformed, L.euler, L.t, L.rot);
+      k_ne_assemble<<<grid_for(N), kBlock, 0, s>>>(L.g, N, L.rows, L.node_row, L.nbr, L.frozen, L.row_ptr,
+                                                   L.ent_con, L.ent_w, L.c_node, L.c_w, L.c_kind, L.c_g, L.rot, L.t,
+                                                   L.crhs, p.w_r, blocks, cols, rhs);
+      k_rows_to_x<<<grid_for(N), kBlock, 0, s>>>(N, L.t, x);
+      count_launch(c, 3);
+      // the row structure is fixed within the solve: plan once (key nullptr), then reuse
+      dist_pcg_device(c, slabs, N, blocks, cols, rhs, x, p.pcg_tol, p.pcg_max_iters, it == 0 ? nullptr : &L, &pr);
+      k_write_back<<<grid_for(N), kBlock, 0, s>>>(N, L.rows, L.frozen, x, L.deformed);
+      count_launch(c);
+    }
+    run_level(c, L, pose, p, 2, l, nullptr, nullptr);  // update_rotations
+    wfk_trace_entry e{};
+    e.level = l;
+    e.iteration = it;
+    run_level(c, L, pose, p, 1, l, nullptr, &e.energy);
+    e.pcg_iterations = pr.iterations;
+    e.pcg_residual = pr.relative_residual;
+    e.anomaly = e.energy.total > prev.total + 1e-9 * prev.total ? 1 : 0;
+    trace.push_back(e);
+    const double rel = (prev.total - e.energy.total) / std::max(prev.total, 1e-300);
+    prev = e.energy;
+    if (rel >= 0 && rel < p.flip_flop_rel_tol) break;
+  }
+}
+
+void solver_c2f_dist(wfk_ctx* c, const wfk_pose* pose, const wfk_solver_params& p, int slabs,
+                     std::vector<wfk_trace_entry>& trace) {
+  require_volume(c);
+  bind_level0(c);
+  const PoseD pd = pose_dev(pose);
+  build_hierarchy(c, p.levels);
+  for (int l = p.levels - 1; l >= 1; --l) {
+    dist_flip_flop(c, l, pd, p, slabs, trace);
+    prolong(c, l);
+  }
+  dist_flip_flop(c, 0, pd, p, slabs, trace);
+  sync_check(c);
 }
 
 void solver_hierarchy_info(wfk_ctx* c, int levels, int32_t* dims, int64_t* active) {

@@ -146,6 +146,9 @@ struct Level {
   DevBuf<int32_t> row_ptr, ent_con, key_in, key_out, val_in, val_out;
   DevBuf<double> ent_w;
   DevBuf<int32_t> cnt;
+  // explicit normal equations of the slab-partitioned solve (solver_c2f_dist)
+  DevBuf<double> ne_blocks, ne_rhs, ne_x;
+  DevBuf<int32_t> ne_cols;
 };
 
 struct VolumeDev {

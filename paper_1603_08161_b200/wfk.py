@@ -300,6 +300,14 @@ class Context:
     def solve_coarse_to_fine(self, pose: Pose, params: SolverParams):
         return self._trace(lib().wfk_solve_coarse_to_fine, C.byref(pose), C.byref(params))
 
+    def solve_coarse_to_fine_dist(self, pose: Pose, params: SolverParams):
+        """solve_coarse_to_fine with each level's PCG on this rank's z-slab (wfk_dist_init first)."""
+        return self._trace(lib().wfk_solve_coarse_to_fine_dist, C.byref(pose), C.byref(params))
+
+    def solve_coarse_to_fine_slabs(self, slabs: int, pose: Pose, params: SolverParams):
+        """The same partitioned solve with `slabs` slab states on this GPU."""
+        return self._trace(lib().wfk_solve_coarse_to_fine_slabs, C.c_int32(slabs), C.byref(pose), C.byref(params))
+
     def hierarchy_info(self, levels: int):
         dims = np.zeros((levels, 3), np.int32)
         act = np.zeros(levels, np.int64)

@@ -317,3 +317,21 @@ def test_pipelined_pcg_spill_matches_shared(ctx, monkeypatch):
     monkeypatch.delenv("WFK_PIPE_SPILL", raising=False)
     assert np.array_equal(out[0][0], out[1][0])
     assert out[0][1] == out[1][1]
+
+
+@pytest.mark.parametrize("slabs", [1, 3])
+def test_coarse_to_fine_slab_partition_parity(ctx, slabs):
+    """solve_coarse_to_fine with every level's PCG partitioned into z-slabs
+    (slab states on one GPU) against the oracle"""
+    v = make_volume(32)
+    cons = random_dense_constraints(v, 2000, seed=9)
+    p = SolverParams.make()
+    pose = Pose.make(O.euler_to_matrix((0.0, 0.01, 0.0)), (0.005, 0, 0))
+    ref = v.copy()
+    tr = O.solve_coarse_to_fine(ref, pose, cons, p)
+    ctx.upload_volume(v)
+    ctx.upload_constraints(cons)
+    tg = ctx.solve_coarse_to_fine_slabs(slabs, pose, p)
+    ctx.download_volume(v)
+    compare_solves(v, ref, tg, tr)
+    assert all(e["pcg_iterations"] > 0 for e in tg)
