@@ -379,6 +379,100 @@ def run_b200(args):
     d.close()
 
 
+def run_partitioned(args):
+    """BASELINE configs[3]: the frame-1 solve on a 256^3
+    lattice with every level's PCG slab-partitioned across the N ranks
+    (wfk_solve_coarse_to_fine_dist, NCCL halos + all-gathered dots), repeated
+    from the same checkpoint.  One step = one coarse-to-fine solve; `value` =
+    ms per solve (max over ranks, CUDA events on the context stream);
+    "scaling": "strong" (the lattice is fixed as N grows)."""
+    from paper_1603_08161_b200.abi import CorrespondParams, Frame, Intrinsics, Pose, SolverParams, Volume
+    from paper_1603_08161_b200.wfk import Context, SynthScene, dist_unique_id, pipeline_config
+
+    d = Dist(args.gpus)
+    ctx = Context(d.local)
+    if d.world > 1:
+        idt = d.torch.zeros(128, dtype=d.torch.uint8, device=d.device)
+        if d.rank == 0:
+            idt[:] = d.torch.frombuffer(bytearray(dist_unique_id()), dtype=d.torch.uint8).to(d.device)
+        d.dist.broadcast(idt, 0)
+        ctx.dist_init(d.rank, d.world, bytes(idt.cpu().tolist()))
+    else:
+        ctx.dist_init(0, 1)
+    K = Intrinsics.make(FX, FY, CX, CY, W_PX, H_PX)
+    frames = []
+    for f in range(2):
+        sc = SynthScene()
+        sc.center[:] = [0.0, 0.0, 1.2]
+        sc.radius = 0.3
+        sc.pivot[:] = [0.0, 0.0, 1.2]
+        sc.amplitude = frame_amplitude(f + 3)  # a visible bend between the two frames
+        sc.driver_axis, sc.rot_axis = 0, 1
+        sc.t_min, sc.t_max = 0.05, 6.0
+        sc.texture_seed, sc.texture_scale, sc.dot_radius = 7, 0.06, 0.3
+        depth, color = ctx.synth_render(sc, K)
+        frames.append(Frame(K, depth, color))
+    dims, voxel, origin = lattice_geometry()
+    vol = Volume(dims, voxel, origin)
+    ctx.upload_volume(vol)
+    cfg = pipeline_config(solver=SolverParams.make(), reassociations=1, estimate_pose=False, use_features=False)
+    pose = Pose.make()
+    ctx.process_frame(frames[0], pose, cfg, 0)  # bootstrap
+    # frame 1's dense constraints against the bootstrap surface
+    ctx.upload_frame(frames[1])
+    ctx.backproject_depth(download=False)
+    ctx.extract_mesh(pose)
+    ctx.compute_normals()
+    ctx.rasterize(K, download=False)
+    n_cons = ctx.find_dense_correspondences(K, CorrespondParams.make(), drop_inactive=True)
+    ckpt = Volume(dims, voxel, origin)
+    ctx.download_volume(ckpt)
+    p = SolverParams.make()
+    for _ in range(args.warmup):
+        ctx.upload_volume(ckpt)
+        ctx.solve_coarse_to_fine_dist(pose, p)
+    total_ms, pcg = 0.0, 0
+    for _ in range(args.steps):
+        ctx.upload_volume(ckpt)
+        ctx.flush_l2()
+        d.barrier()
+        ctx.timer_mark(0)
+        tr = ctx.solve_coarse_to_fine_dist(pose, p)
+        ctx.timer_mark(1)
+        total_ms += ctx.timer_elapsed_ms(0, 1)
+        pcg += sum(e["pcg_iterations"] for e in tr)
+    d.barrier()
+    ms = d.max(total_ms) / args.steps
+    fused = None
+    if d.world == 1:  # the fused single-GPU solve of the same system, for reference
+        fms = 0.0
+        for _ in range(max(args.steps, 2)):
+            ctx.upload_volume(ckpt)
+            ctx.flush_l2()
+            ctx.timer_mark(0)
+            ctx.solve_coarse_to_fine(pose, p)
+            ctx.timer_mark(1)
+            fms += ctx.timer_elapsed_ms(0, 1)
+        fused = fms / max(args.steps, 2)
+    _, act = ctx.hierarchy_info(3)
+    if d.rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": ms, "unit": "ms/solve", "n_gpus": d.world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-rendered sphere, frames 0-1)",
+            "config": {"workload": f"BASELINE configs[3]: {N_LATTICE}^3 lattice, frame-1 coarse-to-fine solve, "
+                                   "every level's PCG slab-partitioned (z-slabs, NCCL halos + all-gathered dots)",
+                       "lattice": [N_LATTICE] * 3, "rows_per_level": [int(a) for a in act],
+                       "dense_constraints": int(n_cons), "parallelism": f"z-slab x{d.world}",
+                       "l2": "flushed before every solve"},
+            "pcg_iters_per_s": pcg / (d.max(total_ms) * 1e-3),
+            "fused_single_gpu_ms_per_solve": fused,
+            "gpu_launches": int(ctx.launch_count),
+        }), flush=True)
+    ctx.close()
+    d.close()
+
+
 def cpu_baseline_sample(frames, n_frames):
     """The oracle port on this host's cores, frames 1..n of the same sequence
     after the (untimed) bootstrap frame 0; reports the median ms/frame."""
@@ -462,12 +556,18 @@ def main():
     ap.add_argument("--lattice", type=int, default=N_LATTICE,
                     help="lattice side (default 128 = configs[2]; 256 = the configs[3] lattice on one GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="BASELINE configs[3]: the 256^3 frame-1 solve with the PCG slab-partitioned over the ranks")
     args = ap.parse_args()
     N_LATTICE = args.lattice
     if args.warmup < 3 and args.impl == "b200":
         print("warning: W >= 3 warm-up steps are required for a valid number", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args)
+    elif args.partitioned:
+        if args.lattice == 128 and "--lattice" not in sys.argv:
+            N_LATTICE = 256
+        run_partitioned(args)
     else:
         run_b200(args)
 

@@ -162,6 +162,7 @@ void wfk_destroy(wfk_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  wfk::dist_forget(c);
   wfk::dist_destroy(c);
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   for (cudaEvent_t e : c->prof.ev)

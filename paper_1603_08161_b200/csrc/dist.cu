@@ -19,7 +19,10 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <vector>
 
@@ -230,18 +233,27 @@ __global__ void k_d_zero(DSlab a) {
   for (int r = a.lo + blockIdx.x * kDBlock + threadIdx.x; r < a.hi; r += gridDim.x * kDBlock) st3(a.x, r, V3{0, 0, 0});
 }
 
-// the slab's partials: block partials summed in block order -> gath[rank]
+// the slab's partials: block partials summed in a fixed order -> gath[rank]
+// (one warp per value: every lane loads its strided share, then a fixed tree)
 __global__ void k_d_slab_sum(DSlab a, int nv, int nblocks, int rank) {
-  const int k = threadIdx.x;
+  const int k = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (k >= nv) return;
+  double v[kDMaxBlocks / 32];
+#pragma unroll
+  for (int j = 0; j < kDMaxBlocks / 32; ++j) {
+    const int b = lane + 32 * j;
+    v[j] = b < nblocks ? a.part[k * kDMaxBlocks + b] : 0.0;
+  }
   double s = 0;
-  for (int b = 0; b < nblocks; ++b) s += a.part[k * kDMaxBlocks + b];
-  a.gath[rank * kDK + k] = s;
+#pragma unroll
+  for (int j = 0; j < kDMaxBlocks / 32; ++j) s += v[j];
+  s = warp_sum(s);
+  if (lane == 0) a.gath[rank * kDK + k] = s;
 }
 
 // scalars from the gathered partials, summed in rank order (identical on every rank)
 // phase 0: init, 1: after spmv, 2: after update
-__global__ void k_d_scalars(DSlab a, int world, int phase, double tol, int it) {
+__global__ void k_d_scalars(DSlab a, int world, int phase, double tol) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double t[kDK] = {0, 0, 0, 0};
   for (int q = 0; q < world; ++q)
@@ -273,15 +285,12 @@ __global__ void k_d_scalars(DSlab a, int world, int phase, double tol, int it) {
     st[DS_RZ] = t[0];
     st[DS_RNORM] = sqrt(t[1]);
     st[DS_RELRES] = st[DS_RNORM] / st[DS_BNORM];
-    st[DS_ITERS] = it + 1;
+    st[DS_ITERS] += 1;
+    // the loop test of the next iteration (r_norm > stop); the direction
+    // update that follows is then skipped, as the reference leaves the loop
+    if (!(st[DS_RNORM] > st[DS_STOP])) st[DS_DONE] = 1;
   }
 }
-// the loop test of the next iteration (r_norm > stop), after the direction update
-__global__ void k_d_test(DSlab a) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  if (a.st[DS_DONE] == 0 && !(a.st[DS_RNORM] > a.st[DS_STOP])) a.st[DS_DONE] = 1;
-}
-
 // per-row min / max referenced column (for the plan)
 __global__ void k_d_col_range(int N, const int32_t* cols, int32_t* mn, int32_t* mx) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x) {
@@ -387,65 +396,127 @@ DistPlan plan_of(wfk_ctx* c, int N, const int32_t* cols_d, int world) {
   return make_plan(N, mn.data(), mx.data(), world);
 }
 
-// one partitioned pcg_solve of a device-resident system; `ranks` = the slab
-// indices run here; x (device, N x 3) is the initial guess on entry and the
-// full solution on return
-void run_dist_pcg_dev(wfk_ctx* c, int N, int world, const std::vector<int>& ranks, const DistPlan& plan,
-                      const double* B, const int32_t* CL, const double* RHS, double* x, double tol, int max_iters,
-                      wfk_pcg_result* res, Transport& tr) {
-  cudaStream_t s = c->stream;
+// per-solve work state: slab buffers and the CUDA graph of one PCG iteration,
+// reused while the system (pointers, size, partition) is unchanged
+struct DistWork {
+  const wfk_ctx* ctx = nullptr;
+  int N = -1, world = 0;
+  std::vector<int> ranks;
+  const double *B = nullptr, *RHS = nullptr;
+  const int32_t* CL = nullptr;
+  uint64_t plan_ver = 0;
   std::vector<std::unique_ptr<SlabBufs>> bufs;
   std::vector<DSlab> sl;
-  for (int q : ranks) {
-    auto b = std::make_unique<SlabBufs>();
-    DSlab a;
-    a.lo = plan.lo[size_t(q)];
-    a.hi = plan.hi[size_t(q)];
-    a.blocks = B;
-    a.cols = CL;
-    a.rhs = RHS;
-    a.x = b->x.ensure(3 * size_t(N));
-    a.r = b->r.ensure(3 * size_t(N));
-    a.z = b->z.ensure(3 * size_t(N));
-    a.p = b->p.ensure(3 * size_t(N));
-    a.ap = b->ap.ensure(3 * size_t(N));
-    a.dinv = b->dinv.ensure(3 * size_t(N));
-    a.part = b->part.ensure(size_t(kDK) * kDMaxBlocks);
-    a.gath = b->gath.ensure(size_t(kDK) * world);
-    a.st = b->st.ensure(DS_N);
+  static constexpr int kBatch = 8;
+  cudaGraphExec_t exec = nullptr, exec1 = nullptr;  // kBatch iterations / one iteration
+  int kernels_per_iter = 0;
+  void reset() {  // the slab buffers stay allocated (they only grow)
+    if (exec) cudaGraphExecDestroy(exec);
+    if (exec1) cudaGraphExecDestroy(exec1);
+    exec = exec1 = nullptr;
+    sl.clear();
+  }
+  ~DistWork() { reset(); }
+};
+
+// one partitioned pcg_solve of a device-resident system; `ranks` = the slab
+// indices run here; x (device, N x 3) is the initial guess on entry and the
+// full solution on return.  One iteration (matvec, all-gathered dots, update,
+// direction, halo exchange) is captured once as a CUDA graph -- NCCL calls
+// included -- and replayed.
+void run_dist_pcg_dev(wfk_ctx* c, int N, int world, const std::vector<int>& ranks, const DistPlan& plan,
+                      uint64_t plan_ver, const double* B, const int32_t* CL, const double* RHS, double* x, double tol,
+                      int max_iters, wfk_pcg_result* res, Transport& tr, DistWork& w) {
+  cudaStream_t s = c->stream;
+  const bool reuse = w.exec && w.ctx == c && w.N == N && w.world == world && w.ranks == ranks && w.B == B &&
+                     w.CL == CL && w.RHS == RHS && w.plan_ver == plan_ver;
+  if (!reuse) {
+    w.reset();
+    w.ctx = c;
+    w.N = N;
+    w.world = world;
+    w.ranks = ranks;
+    w.B = B;
+    w.CL = CL;
+    w.RHS = RHS;
+    w.plan_ver = plan_ver;
+    while (w.bufs.size() < ranks.size()) w.bufs.push_back(std::make_unique<SlabBufs>());
+    for (size_t i = 0; i < ranks.size(); ++i) {
+      const int q = ranks[i];
+      SlabBufs* b = w.bufs[i].get();
+      DSlab a;
+      a.lo = plan.lo[size_t(q)];
+      a.hi = plan.hi[size_t(q)];
+      a.blocks = B;
+      a.cols = CL;
+      a.rhs = RHS;
+      a.x = b->x.ensure(3 * size_t(N));
+      a.r = b->r.ensure(3 * size_t(N));
+      a.z = b->z.ensure(3 * size_t(N));
+      a.p = b->p.ensure(3 * size_t(N));
+      a.ap = b->ap.ensure(3 * size_t(N));
+      a.dinv = b->dinv.ensure(3 * size_t(N));
+      a.part = b->part.ensure(size_t(kDK) * kDMaxBlocks);
+      a.gath = b->gath.ensure(size_t(kDK) * world);
+      a.st = b->st.ensure(DS_N);
+      w.sl.push_back(a);
+    }
+  }
+  std::vector<DSlab>& sl = w.sl;
+  for (DSlab& a : sl) {
     WFK_CUDA(cudaMemcpyAsync(a.x, x, size_t(N) * 3 * 8, cudaMemcpyDeviceToDevice, s));  // x0, replicated
     WFK_CUDA(cudaMemsetAsync(a.gath, 0, size_t(kDK) * world * 8, s));
     WFK_CUDA(cudaMemsetAsync(a.st, 0, DS_N * 8, s));
-    sl.push_back(a);
-    bufs.push_back(std::move(b));
-  }
-  auto reduce = [&](int nv, int phase, int it) {
-    for (size_t i = 0; i < sl.size(); ++i)
-      k_d_slab_sum<<<1, 32, 0, s>>>(sl[i], nv, slab_blocks(sl[i]), ranks[i]);
-    tr.allgather(sl);
-    for (DSlab& a : sl) k_d_scalars<<<1, 32, 0, s>>>(a, world, phase, tol, it);
-    count_launch(c, int(2 * sl.size()));
-  };
-  for (DSlab& a : sl) {
     WFK_CUDA(cudaMemsetAsync(a.part, 0, size_t(kDK) * kDMaxBlocks * 8, s));
-    k_d_init<<<slab_blocks(a), kDBlock, 0, s>>>(a);
   }
-  count_launch(c, int(sl.size()));
-  reduce(3, 0, 0);
+  auto reduce = [&](int nv, int phase) {
+    for (size_t i = 0; i < sl.size(); ++i)
+      k_d_slab_sum<<<1, 32 * kDK, 0, s>>>(sl[i], nv, slab_blocks(sl[i]), ranks[i]);
+    tr.allgather(sl);
+    for (DSlab& a : sl) k_d_scalars<<<1, 32, 0, s>>>(a, world, phase, tol);
+  };
+  for (DSlab& a : sl) k_d_init<<<slab_blocks(a), kDBlock, 0, s>>>(a);
+  reduce(3, 0);
   for (DSlab& a : sl) k_d_zero<<<slab_blocks(a), kDBlock, 0, s>>>(a);
+  count_launch(c, int(4 * sl.size()));
   tr.exchange(sl, &DSlab::p, plan);
-  for (int it = 0; it < max_iters; ++it) {
-    for (DSlab& a : sl) k_d_spmv<<<slab_blocks(a), kDBlock, 0, s>>>(a);
-    reduce(1, 1, it);
-    for (DSlab& a : sl) k_d_update<<<slab_blocks(a), kDBlock, 0, s>>>(a);
-    reduce(2, 2, it);
-    for (DSlab& a : sl) {
-      k_d_dir<<<slab_blocks(a), kDBlock, 0, s>>>(a);
-      k_d_test<<<1, 32, 0, s>>>(a);
-    }
-    count_launch(c, int(4 * sl.size()));
-    tr.exchange(sl, &DSlab::p, plan);
-    if ((it & 7) == 7) {  // leave early once converged (the state is identical on every rank)
+  static const bool trace = std::getenv("WFK_DIST_TRACE") != nullptr;
+  auto now = [&] {
+    if (trace) WFK_CUDA(cudaStreamSynchronize(s));
+    return std::chrono::steady_clock::now();
+  };
+  const auto t0 = now();
+  const bool captured = !w.exec;
+  if (!w.exec) {
+    // graphs of kBatch iterations and of one iteration; batches are replayed
+    // one at a time with a convergence check in between (queueing many graph
+    // launches back to back was measured to stall for up to a second)
+    auto capture = [&](int iters, cudaGraphExec_t* out) {
+      cudaGraph_t g = nullptr;
+      WFK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      for (int k = 0; k < iters; ++k) {
+        for (DSlab& a : sl) k_d_spmv<<<slab_blocks(a), kDBlock, 0, s>>>(a);
+        reduce(1, 1);
+        for (DSlab& a : sl) k_d_update<<<slab_blocks(a), kDBlock, 0, s>>>(a);
+        reduce(2, 2);
+        for (DSlab& a : sl) k_d_dir<<<slab_blocks(a), kDBlock, 0, s>>>(a);
+        tr.exchange(sl, &DSlab::p, plan);
+      }
+      WFK_CUDA(cudaStreamEndCapture(s, &g));
+      const cudaError_t e = cudaGraphInstantiate(out, g, 0);
+      cudaGraphDestroy(g);
+      WFK_CUDA(e);
+    };
+    capture(DistWork::kBatch, &w.exec);
+    capture(1, &w.exec1);
+    w.kernels_per_iter = int(7 * sl.size());
+  }
+  for (int it = 0; it < max_iters;) {
+    const int k = max_iters - it >= DistWork::kBatch ? DistWork::kBatch : 1;
+    WFK_CUDA(cudaGraphLaunch(k == 1 ? w.exec1 : w.exec, s));
+    count_launch(c, k * w.kernels_per_iter);
+    it += k;
+    if (it < max_iters) {  // leave early once converged (identical state on every rank)
       WFK_CUDA(cudaMemcpyAsync(c->h_pinned + 64, sl[0].st + DS_DONE, 8, cudaMemcpyDeviceToHost, s));
       WFK_CUDA(cudaStreamSynchronize(s));
       double done;
@@ -453,6 +524,10 @@ void run_dist_pcg_dev(wfk_ctx* c, int N, int world, const std::vector<int>& rank
       if (done != 0) break;
     }
   }
+  const auto t2 = now();
+  if (trace)
+    fprintf(stderr, "[wfk dist] N %d world %d %s loop %.3f ms\n", N, world, captured ? "captured" : "reused",
+            std::chrono::duration<double, std::milli>(t2 - t0).count());
   tr.final_x(sl, plan);
   double st_h[DS_N];
   WFK_CUDA(cudaMemcpyAsync(x, sl[0].x, size_t(N) * 3 * 8, cudaMemcpyDeviceToDevice, s));
@@ -481,7 +556,8 @@ void run_dist_pcg(wfk_ctx* c, int N, int world, const std::vector<int>& ranks, c
   WFK_CUDA(cudaMemcpyAsync(RHS.p, rhs_h, size_t(N) * 3 * 8, cudaMemcpyHostToDevice, s));
   WFK_CUDA(cudaMemcpyAsync(X.p, x_h, size_t(N) * 3 * 8, cudaMemcpyHostToDevice, s));
   const DistPlan plan = plan_of(c, N, CL.p, world);
-  run_dist_pcg_dev(c, N, world, ranks, plan, B.p, CL.p, RHS.p, X.p, tol, max_iters, res, tr);
+  DistWork w;
+  run_dist_pcg_dev(c, N, world, ranks, plan, 0, B.p, CL.p, RHS.p, X.p, tol, max_iters, res, tr, w);
   WFK_CUDA(cudaMemcpyAsync(x_h, X.p, size_t(N) * 3 * 8, cudaMemcpyDeviceToHost, s));
   WFK_CUDA(cudaStreamSynchronize(s));
 }
@@ -490,19 +566,31 @@ void run_dist_pcg(wfk_ctx* c, int N, int world, const std::vector<int>& ranks, c
 // partitioned PCG of a device-resident system (the solver's normal equations).
 // slabs > 0: that many slab states on this GPU; slabs == 0: this rank of the
 // context's communicator.  plan_key identifies the system's row structure: the
-// plan is rebuilt when it changes.
+// plan (and the captured iteration) is rebuilt when it changes or when `fresh`.
 struct PlanCache {
-  const void* key = nullptr;
+  const wfk_ctx* ctx = nullptr;
   int N = -1, world = 0;
+  uint64_t version = 0;
   DistPlan plan;
+  DistWork work;
 };
-static PlanCache& plan_cache() {
-  static PlanCache pc;
-  return pc;
+static bool same_plan(const DistPlan& a, const DistPlan& b) {
+  if (a.world != b.world || a.lo != b.lo || a.hi != b.hi || a.xfers.size() != b.xfers.size()) return false;
+  for (size_t i = 0; i < a.xfers.size(); ++i)
+    if (a.xfers[i].src != b.xfers[i].src || a.xfers[i].dst != b.xfers[i].dst || a.xfers[i].lo != b.xfers[i].lo ||
+        a.xfers[i].hi != b.xfers[i].hi)
+      return false;
+  return true;
+}
+// one cache entry per system key (the solver passes its Level), so each level
+// keeps its plan, slab buffers and captured iteration from solve to solve
+static std::map<const void*, PlanCache>& plan_caches() {
+  static std::map<const void*, PlanCache> m;
+  return m;
 }
 
 void dist_pcg_device(wfk_ctx* c, int slabs, int N, const double* blocks, const int32_t* cols, const double* rhs,
-                     double* x, double tol, int max_iters, const void* plan_key, wfk_pcg_result* res) {
+                     double* x, double tol, int max_iters, const void* plan_key, bool fresh, wfk_pcg_result* res) {
   if (N <= 0) {
     if (res) *res = wfk_pcg_result{0, 0, 0.0};
     return;
@@ -510,10 +598,15 @@ void dist_pcg_device(wfk_ctx* c, int slabs, int N, const double* blocks, const i
   DistComm* d = c->dist;
   if (slabs <= 0 && !d) throw Error(WFK_E_INVALID_ARG, "wfk_dist_init first");
   const int world = slabs > 0 ? slabs : d->world;
-  PlanCache& pc = plan_cache();
-  if (!plan_key || pc.key != plan_key || pc.N != N || pc.world != world) {
-    pc.plan = plan_of(c, N, cols, world);
-    pc.key = plan_key;
+  PlanCache& pc = plan_caches()[plan_key];
+  if (fresh || !plan_key || pc.ctx != c || pc.N != N || pc.world != world) {
+    DistPlan p = plan_of(c, N, cols, world);
+    // an unchanged partition keeps the captured iteration
+    if (pc.ctx != c || pc.N != N || pc.world != world || !same_plan(p, pc.plan)) {
+      pc.plan = std::move(p);
+      ++pc.version;
+    }
+    pc.ctx = c;
     pc.N = N;
     pc.world = world;
   }
@@ -521,13 +614,24 @@ void dist_pcg_device(wfk_ctx* c, int slabs, int N, const double* blocks, const i
   if (slabs > 0) {
     for (int q = 0; q < slabs; ++q) ranks.push_back(q);
     SlabsTransport t(c->stream, slabs);
-    run_dist_pcg_dev(c, N, world, ranks, pc.plan, blocks, cols, rhs, x, tol, max_iters, res, t);
+    run_dist_pcg_dev(c, N, world, ranks, pc.plan, pc.version, blocks, cols, rhs, x, tol, max_iters, res, t, pc.work);
   } else {
     ranks.push_back(d->rank);
     NcclTransport tr(c->stream, d);
     SlabsTransport single(c->stream, 1);
     Transport& t = d->comm ? static_cast<Transport&>(tr) : static_cast<Transport&>(single);
-    run_dist_pcg_dev(c, N, world, ranks, pc.plan, blocks, cols, rhs, x, tol, max_iters, res, t);
+    run_dist_pcg_dev(c, N, world, ranks, pc.plan, pc.version, blocks, cols, rhs, x, tol, max_iters, res, t, pc.work);
+  }
+}
+
+// the context goes away: drop cached work that points into it
+void dist_forget(wfk_ctx* c) {
+  auto& m = plan_caches();
+  for (auto it = m.begin(); it != m.end();) {
+    if (it->second.ctx == c || it->second.work.ctx == c)
+      it = m.erase(it);
+    else
+      ++it;
   }
 }
 

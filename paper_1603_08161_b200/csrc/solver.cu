@@ -19,6 +19,8 @@
 //     Dot products are deterministic two-level reductions (warp shuffle ->
 //     per-block partial -> fixed-order sum).
 #include <cooperative_groups.h>
+#include <chrono>
+
 #include <cub/cub.cuh>
 #include <type_traits>
 #include <thrust/iterator/counting_iterator.h>
@@ -1886,66 +1888,77 @@ __global__ void __launch_bounds__(kCoopBlock, 1) k_pcg_assembled(AsmArgs a) {
 // ============================================================================
 // NormalEquations materialisation (test-facing build_normal_equations)
 // ============================================================================
-__global__ void k_ne_assemble(Grid g, int N, const int32_t* rows, const int32_t* node_row, const int32_t* nbr,
-                              const uint8_t* frozen, const int32_t* row_ptr, const int32_t* ent_con,
-                              const double* ent_w, const int32_t* c_node, const double* c_w, const int32_t* c_kind,
-                              const double* c_g, const double* rot, const double4* t, const double4* crhs,
-                              double w_r, double* blocks, int32_t* cols, double* rhs) {
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x) {
+// build_normal_equations' blocks, cols and rhs (solver.cpp:113-275) with one
+// warp per row: lane s < 27 owns stencil slot s and accumulates its 3x3 block
+// in registers in the reference's order (incidences, then corners, then the
+// ARAP terms); lane 0 builds the rhs.
+__global__ void k_ne_assemble_warp(Grid g, int r0, int r1, const int32_t* rows, const int32_t* node_row,
+                                   const int32_t* nbr, int N, const uint8_t* frozen, const int32_t* row_ptr,
+                                   const int32_t* ent_con, const double* ent_w, const int32_t* c_node,
+                                   const double* c_w, const int32_t* c_kind, const double* c_g, const double* rot,
+                                   const double4* t, const double4* crhs, double w_r, double* blocks, int32_t* cols,
+                                   double* rhs) {
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int r = r0 + warp; r < r1; r += nwarps) {
     const int node = rows[r];
     int x, y, z;
     g.idx3(node, x, y, z);
-    double* B = blocks + int64_t(r) * 27 * 9;
-    for (int s = 0; s < 27 * 9; ++s) B[s] = 0.0;
-    for (int dz = -1; dz <= 1; ++dz)
-      for (int dy = -1; dy <= 1; ++dy)
-        for (int dx = -1; dx <= 1; ++dx) {
-          const int s = stencil_slot(dx, dy, dz);
-          cols[27 * int64_t(r) + s] =
-              g.in_grid(x + dx, y + dy, z + dz) ? node_row[g.lin(x + dx, y + dy, z + dz)] : -1;
-        }
+    double b[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) b[q] = 0.0;
+    if (lane < 27) {
+      const int dx = lane % 3 - 1, dy = (lane / 3) % 3 - 1, dz = lane / 9 - 1;
+      cols[27 * int64_t(r) + lane] = g.in_grid(x + dx, y + dy, z + dz) ? node_row[g.lin(x + dx, y + dy, z + dz)] : -1;
+    }
     if (frozen[r]) {
-      B[kCenter * 9 + 0] = B[kCenter * 9 + 4] = B[kCenter * 9 + 8] = 1.0;
-      st3(rhs, r, V3{t[r].x, t[r].y, t[r].z});
-      continue;
-    }
-    for (int e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
-      const int c = ent_con[e];
-      const double ai = ent_w[e];
-      const double coef = c_g[4 * c + 3];
-      const V3 gg{c_g[4 * c], c_g[4 * c + 1], c_g[4 * c + 2]};
-      for (int k = 0; k < 8; ++k) {
-        int a, b, cz;
-        g.idx3(c_node[8 * c + k], a, b, cz);
-        const int s = stencil_slot(a - x, b - y, cz - z);
-        const double sc = coef * ai * c_w[8 * c + k];
-        if (c_kind[c] == WFK_DENSE_PLANE) {
-          for (int i = 0; i < 3; ++i)
-            for (int j = 0; j < 3; ++j) B[s * 9 + i * 3 + j] += sc * (comp(gg, i) * comp(gg, j));
-        } else {
-          for (int i = 0; i < 3; ++i)
-            for (int j = 0; j < 3; ++j) B[s * 9 + i * 3 + j] += sc * (i == j ? 1.0 : 0.0);
+      if (lane == kCenter) b[0] = b[4] = b[8] = 1.0;
+      if (lane == 0) st3(rhs, r, V3{t[r].x, t[r].y, t[r].z});
+    } else {
+      for (int e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
+        const int c = ent_con[e];
+        const double ai = ent_w[e];
+        const double coef = c_g[4 * c + 3];
+        const double gg[3] = {c_g[4 * c], c_g[4 * c + 1], c_g[4 * c + 2]};
+        const bool dense = c_kind[c] == WFK_DENSE_PLANE;
+        for (int k = 0; k < 8; ++k) {
+          int a, bb, cz;
+          g.idx3(c_node[8 * c + k], a, bb, cz);
+          if (stencil_slot(a - x, bb - y, cz - z) != lane) continue;
+          const double sc = coef * ai * c_w[8 * c + k];
+          if (dense) {
+            for (int i = 0; i < 3; ++i)
+              for (int j = 0; j < 3; ++j) b[i * 3 + j] += sc * (gg[i] * gg[j]);
+          } else {
+            for (int i = 0; i < 3; ++i)
+              for (int j = 0; j < 3; ++j) b[i * 3 + j] += sc * (i == j ? 1.0 : 0.0);
+          }
         }
       }
-    }
-    V3 rv{crhs[r].x, crhs[r].y, crhs[r].z};
-    const M3 ri = ld_m3(rot, r);
-    const V3 can_i = g.canonical(node);
-    const double w2 = 2.0 * w_r;
-    for (int k = 0; k < 6; ++k) {
-      const int j = nbr[int64_t(k) * N + r];
-      if (j < 0) continue;
-      const V3 dij = can_i - g.canonical(rows[j]);
-      for (int i = 0; i < 3; ++i) B[kCenter * 9 + i * 4] += w2 * 1.0;
-      rv += w_r * mul(add(ri, ld_m3(rot, j)), dij);
-      if (frozen[j]) {
-        rv += w2 * V3{t[j].x, t[j].y, t[j].z};
-      } else {
-        const int s = stencil_slot(kFace[k][0], kFace[k][1], kFace[k][2]);
-        for (int i = 0; i < 3; ++i) B[s * 9 + i * 4] -= w2 * 1.0;
+      const double w2 = 2.0 * w_r;
+      V3 rv{crhs[r].x, crhs[r].y, crhs[r].z};
+      const M3 ri = ld_m3(rot, r);
+      const V3 can_i = g.canonical(node);
+      for (int k = 0; k < 6; ++k) {
+        const int j = nbr[int64_t(k) * N + r];
+        if (j < 0) continue;
+        if (lane == kCenter)
+          for (int i = 0; i < 3; ++i) b[i * 4] += w2 * 1.0;
+        if (lane == 0) {
+          const V3 dij = can_i - g.canonical(rows[j]);
+          rv += w_r * mul(add(ri, ld_m3(rot, j)), dij);
+          if (frozen[j]) rv += w2 * V3{t[j].x, t[j].y, t[j].z};
+        }
+        if (!frozen[j] && lane == stencil_slot(kFace[k][0], kFace[k][1], kFace[k][2]))
+          for (int i = 0; i < 3; ++i) b[i * 4] -= w2 * 1.0;
       }
+      if (lane == 0) st3(rhs, r, rv);
     }
-    st3(rhs, r, rv);
+    if (lane < 27) {
+      double* B = blocks + (int64_t(r) * 27 + lane) * 9;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) B[q] = b[q];
+    }
   }
 }
 
@@ -2645,11 +2658,23 @@ __global__ void k_write_back(int N, const int32_t* rows, const uint8_t* frozen, 
 
 static void dist_flip_flop(wfk_ctx* c, int l, const PoseD& pose, const wfk_solver_params& p, int slabs,
                            std::vector<wfk_trace_entry>& trace) {
+  static const bool dtrace = getenv("WFK_DIST_TRACE") != nullptr;
+  auto t_prev = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!dtrace) return;
+    sync_check(c);
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[wfk dist ff] L%d %-10s %.3f ms\n", l, what,
+            std::chrono::duration<double, std::milli>(t - t_prev).count());
+    t_prev = t;
+  };
   Level& L = c->lv[l];
   level_rows(c, L);
   level_constraints(c, L, pose, p);
+  lap("setup");
   wfk_energy prev;
   run_level(c, L, pose, p, 1, l, nullptr, &prev);  // evaluate_energy
+  lap("energy0");
   if (prev.total == 0) return;
   const int N = L.N;
   cudaStream_t s = c->stream;
@@ -2661,21 +2686,25 @@ static void dist_flip_flop(wfk_ctx* c, int l, const PoseD& pose, const wfk_solve
     wfk_pcg_result pr{0, 0, 0.0};
     if (N > 0) {
       k_load_rows<<<grid_for(N), kBlock, 0, s>>>(N, L.rows, L.deformed, L.euler, L.t, L.rot);
-      k_ne_assemble<<<grid_for(N), kBlock, 0, s>>>(L.g, N, L.rows, L.node_row, L.nbr, L.frozen, L.row_ptr,
-                                                   L.ent_con, L.ent_w, L.c_node, L.c_w, L.c_kind, L.c_g, L.rot, L.t,
-                                                   L.crhs, p.w_r, blocks, cols, rhs);
+      k_ne_assemble_warp<<<grid_for(int64_t(N) * 32), kBlock, 0, s>>>(
+          L.g, 0, N, L.rows, L.node_row, L.nbr, N, L.frozen, L.row_ptr, L.ent_con, L.ent_w, L.c_node, L.c_w,
+          L.c_kind, L.c_g, L.rot, L.t, L.crhs, p.w_r, blocks, cols, rhs);
       k_rows_to_x<<<grid_for(N), kBlock, 0, s>>>(N, L.t, x);
       count_launch(c, 3);
-      // the row structure is fixed within the solve: plan once (key nullptr), then reuse
-      dist_pcg_device(c, slabs, N, blocks, cols, rhs, x, p.pcg_tol, p.pcg_max_iters, it == 0 ? nullptr : &L, &pr);
+      lap("assemble");
+      // the row structure is fixed within the solve: plan at the first iteration, then reuse
+      dist_pcg_device(c, slabs, N, blocks, cols, rhs, x, p.pcg_tol, p.pcg_max_iters, &L, it == 0, &pr);
+      lap("pcg");
       k_write_back<<<grid_for(N), kBlock, 0, s>>>(N, L.rows, L.frozen, x, L.deformed);
       count_launch(c);
     }
     run_level(c, L, pose, p, 2, l, nullptr, nullptr);  // update_rotations
+    lap("rotations");
     wfk_trace_entry e{};
     e.level = l;
     e.iteration = it;
     run_level(c, L, pose, p, 1, l, nullptr, &e.energy);
+    lap("energy");
     e.pcg_iterations = pr.iterations;
     e.pcg_residual = pr.relative_residual;
     e.anomaly = e.energy.total > prev.total + 1e-9 * prev.total ? 1 : 0;
@@ -2736,9 +2765,10 @@ int solver_build_ne(wfk_ctx* c, const wfk_pose* pose, const wfk_solver_params& p
   blocks.ensure(size_t(N) * 27 * 9);
   cols.ensure(size_t(N) * 27);
   rhs.ensure(size_t(N) * 3);
-  k_ne_assemble<<<grid_for(N), kBlock, 0, s>>>(L.g, N, L.rows, L.node_row, L.nbr, L.frozen, L.row_ptr, L.ent_con,
-                                               L.ent_w, L.c_node, L.c_w, L.c_kind, L.c_g, L.rot, t, L.crhs, p.w_r,
-                                               blocks, cols, rhs);
+  k_ne_assemble_warp<<<grid_for(int64_t(N) * 32), kBlock, 0, s>>>(L.g, 0, N, L.rows, L.node_row, L.nbr, N, L.frozen,
+                                                                  L.row_ptr, L.ent_con, L.ent_w, L.c_node, L.c_w,
+                                                                  L.c_kind, L.c_g, L.rot, t, L.crhs, p.w_r, blocks,
+                                                                  cols, rhs);
   count_launch(c, 2);
   WFK_CUDA(cudaGetLastError());
   if (out->rows) WFK_CUDA(cudaMemcpyAsync(out->rows, L.rows, size_t(N) * 4, cudaMemcpyDeviceToHost, s));

@@ -55,8 +55,9 @@ void frame_load_pnm(wfk_ctx* c, const char* depth_path, const char* color_path, 
 void frame_save_pnm(wfk_ctx* c, const char* depth_path, const char* color_path);
 void frame_download(wfk_ctx* c, float* depth, float* color);
 void dist_destroy(wfk_ctx* c);
+void dist_forget(wfk_ctx* c);
 void dist_pcg_device(wfk_ctx* c, int slabs, int N, const double* blocks, const int32_t* cols, const double* rhs,
-                     double* x, double tol, int max_iters, const void* plan_key, wfk_pcg_result* res);
+                     double* x, double tol, int max_iters, const void* plan_key, bool fresh, wfk_pcg_result* res);
 void solver_c2f_dist(wfk_ctx* c, const wfk_pose* pose, const wfk_solver_params& p, int slabs,
                      std::vector<wfk_trace_entry>& trace);
 void dist_unique_id(uint8_t* out);
