@@ -24,6 +24,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <vector>
 
 #include "wfk_context.cuh"
@@ -588,6 +589,10 @@ static std::map<const void*, PlanCache>& plan_caches() {
   static std::map<const void*, PlanCache> m;
   return m;
 }
+static std::mutex& plan_mutex() {  // the map is shared by every context of the process
+  static std::mutex m;
+  return m;
+}
 
 void dist_pcg_device(wfk_ctx* c, int slabs, int N, const double* blocks, const int32_t* cols, const double* rhs,
                      double* x, double tol, int max_iters, const void* plan_key, bool fresh, wfk_pcg_result* res) {
@@ -598,7 +603,12 @@ void dist_pcg_device(wfk_ctx* c, int slabs, int N, const double* blocks, const i
   DistComm* d = c->dist;
   if (slabs <= 0 && !d) throw Error(WFK_E_INVALID_ARG, "wfk_dist_init first");
   const int world = slabs > 0 ? slabs : d->world;
-  PlanCache& pc = plan_caches()[plan_key];
+  PlanCache* pcp;
+  {
+    std::lock_guard<std::mutex> lock(plan_mutex());
+    pcp = &plan_caches()[plan_key];  // std::map references stay valid across inserts
+  }
+  PlanCache& pc = *pcp;
   if (fresh || !plan_key || pc.ctx != c || pc.N != N || pc.world != world) {
     DistPlan p = plan_of(c, N, cols, world);
     // an unchanged partition keeps the captured iteration
@@ -626,6 +636,7 @@ void dist_pcg_device(wfk_ctx* c, int slabs, int N, const double* blocks, const i
 
 // the context goes away: drop cached work that points into it
 void dist_forget(wfk_ctx* c) {
+  std::lock_guard<std::mutex> lock(plan_mutex());
   auto& m = plan_caches();
   for (auto it = m.begin(); it != m.end();) {
     if (it->second.ctx == c || it->second.work.ctx == c)
