@@ -522,25 +522,26 @@ __global__ void __launch_bounds__(kMatchBlock) k_match_groups(MatchArgs a, Match
   using Scan = cub::BlockScan<int, kMatchBlock>;
   __shared__ typename Scan::TempStorage ts;
   __shared__ int s_nh;
-  const int b = blockIdx.x;
   const int tid = threadIdx.x;
-  if (b > 0 && a.key[b] == a.key[b - 1]) {  // not the head of a frame group
-    if (tid == 0) a.cnt[b] = 0;
-    return;
-  }
   const int nc = a.nc;
   float* curT = reinterpret_cast<float*>(msm + L.curT);  // [128][nc]
   int32_t* best_col = reinterpret_cast<int32_t*>(msm + L.best_col);
   wfk_feature_match* cand = reinterpret_cast<wfk_feature_match*>(msm + L.cand);
   wfk_feature_match* sorted = reinterpret_cast<wfk_feature_match*>(msm + L.sorted);
+  for (int q = tid; q < 128 * nc; q += kMatchBlock) {  // stage the current descriptors once, transposed
+    const int c = q / 128, i = q % 128;
+    curT[i * nc + c] = a.cur[c].descriptor[i];
+  }
+  // the blocks stride over the sorted store; the position heading a frame group does its matching
+  for (int b = blockIdx.x; b < a.ns; b += gridDim.x) {
+  if (b > 0 && a.key[b] == a.key[b - 1]) {  // not the head of a frame group
+    if (tid == 0) a.cnt[b] = 0;
+    continue;
+  }
   if (tid == 0) {
     int e = b + 1;
     while (e < a.ns && a.key[e] == a.key[b]) ++e;
     s_nh = e - b;
-  }
-  for (int q = tid; q < 128 * nc; q += kMatchBlock) {  // stage the current descriptors, transposed
-    const int c = q / 128, i = q % 128;
-    curT[i * nc + c] = a.cur[c].descriptor[i];
   }
   __syncthreads();
   const int nh = s_nh;
@@ -636,6 +637,8 @@ __global__ void __launch_bounds__(kMatchBlock) k_match_groups(MatchArgs a, Match
     __syncthreads();
   }
   if (tid == 0) a.cnt[b] = done;
+  __syncthreads();  // shared memory is reused by the block's next group
+  }
 }
 
 __global__ void k_match_scatter(int n, int slot, const wfk_feature_match* in, const int32_t* cnt, const int32_t* pos,
@@ -1009,7 +1012,7 @@ void features_match_dev(wfk_ctx* c, const wfk_feature* cur, int nc, const wfk_fe
   if (max_group * nc > a.tile_cap) a.dist = fd.dist.ensure(cap_for(size_t(n) * size_t(nc)));
   WFK_CUDA(cudaFuncSetAttribute(k_match_groups, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.total)));
   WFK_CUDA(cudaMemsetAsync(a.cnt + n, 0, 4, s));
-  k_match_groups<<<n, kMatchBlock, L.total, s>>>(a, L);
+  k_match_groups<<<std::min(n, c->num_sms), kMatchBlock, L.total, s>>>(a, L);
   int32_t* pos = rows;  // n + 1 exclusive offsets
   cub::DeviceScan::ExclusiveSum(nullptr, tb, a.cnt, pos, n + 1, s);
   c->temp.ensure(tb);
