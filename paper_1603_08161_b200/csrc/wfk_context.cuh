@@ -211,7 +211,7 @@ struct FeatDev {
   DevBuf<float> levels[kFeatOctaves][kFeatLevels];  // per octave: L + 1 gaussian, then L DoG levels
   int L = 0;
   std::vector<int> ws, hs;
-  DevBuf<float> gray, tmp, base;
+  DevBuf<float> gray, base;
   DevBuf<uint8_t> flag, ok, kp, cur_raw;
   DevBuf<int32_t> pos, idx, nori, cnt;
   DevBuf<int4> ext;
