@@ -486,10 +486,20 @@ def cpu_baseline_sample(frames, n_frames):
         t0 = time.perf_counter()
         rec.process_frame(frames[f])
         times.append((time.perf_counter() - t0) * 1e3)
-    return {"value": float(np.median(times)), "unit": "ms/frame", "cores": int(O.lib().wfo_num_threads()),
+    cores = int(O.lib().wfo_num_threads())
+    # also the 1-thread figure, on the next frame of the sequence
+    serial = None
+    if 1 + n_frames < len(frames):
+        O.lib().wfo_set_num_threads(1)
+        t0 = time.perf_counter()
+        rec.process_frame(frames[1 + n_frames])
+        serial = (time.perf_counter() - t0) * 1e3
+        O.lib().wfo_set_num_threads(cores)
+    return {"value": float(np.median(times)), "unit": "ms/frame", "cores": cores,
             "kind": "port",
             "sample": f"oracle Reconstructor, frames 1..{n_frames} of the same sequence after the bootstrap "
-                      f"frame (median of {n_frames}), OpenMP threads = {int(O.lib().wfo_num_threads())}"}
+                      f"frame (median of {n_frames}), OpenMP threads = {cores}",
+            "serial_1thread_ms_per_frame": serial}
 
 
 # ---------------------------------------------------------------------------
