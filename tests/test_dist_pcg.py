@@ -223,3 +223,48 @@ def test_dist_pcg_nccl_world1():
         assert itd == its and np.array_equal(xd, xs)
     finally:
         c.close()
+
+
+def test_plan_more_ranks_than_rows():
+    cols = -np.ones((3, 27), np.int32)
+    for r in range(3):
+        cols[r, 13] = r
+        if r > 0:
+            cols[r, 12] = r - 1
+        if r < 2:
+            cols[r, 14] = r + 1
+    ranges, xf = wfk.dist_plan(cols, 5)
+    assert ranges[0, 0] == 0 and ranges[-1, 1] == 3 and np.all(ranges[:, 1] >= ranges[:, 0])
+    for src, dst, a, b in xf:
+        assert ranges[src, 0] <= a < b <= ranges[src, 1]
+
+
+def chain_system(n=10, seed=2):
+    """an SPD 1-D chain: 4 I on the diagonal, -I to each neighbour"""
+    cols = -np.ones((n, 27), np.int32)
+    blocks = np.zeros((n, 27, 3, 3))
+    for r in range(n):
+        cols[r, 13] = r
+        blocks[r, 13] = 4 * np.eye(3)
+        if r > 0:
+            cols[r, 12] = r - 1
+            blocks[r, 12] = -np.eye(3)
+        if r < n - 1:
+            cols[r, 14] = r + 1
+            blocks[r, 14] = -np.eye(3)
+    rhs = np.random.default_rng(seed).normal(size=(n, 3))
+    return blocks, cols, rhs
+
+
+@pytest.mark.gpu
+def test_slab_pcg_more_slabs_than_rows():
+    c = wfk.Context(0)
+    try:
+        blocks, cols, rhs = chain_system(10)
+        x0 = np.zeros((10, 3))
+        xs, its, _ = c.pcg_solve(blocks, cols, rhs, x0, 1e-12, 200)
+        xd, itd, _ = c.pcg_solve_slabs(13, blocks, cols, rhs, x0, 1e-12, 200)
+        assert abs(itd - its) <= 1
+        assert np.max(np.abs(xd - xs)) <= 1e-9 * np.max(np.abs(xs))
+    finally:
+        c.close()
