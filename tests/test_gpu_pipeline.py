@@ -124,3 +124,29 @@ def test_process_frame_features_parity(ctx):
     assert same.mean() > 0.95
     dev = np.linalg.norm(sg["canonical_pos"][:m][same] - sr["canonical_pos"][:m][same], axis=1).max() / voxel
     assert dev <= 1e-3, dev
+
+
+def test_process_frame_features_frame_without_color(ctx):
+    """a frame without color skips the sparse term and add_features (pipeline.cpp:96, 188)"""
+    from paper_1603_08161_b200.wfk import pipeline_config
+    n = 32
+    K = Intrinsics.make(280, 280, 159.5, 119.5, 320, 240)
+    voxel = 0.7 / (n - 1)
+    origin = (-0.35, -0.35, 0.85)
+    solver = SolverParams.make(levels=2)
+    frames = bend_frames(ctx, K, 4, 1.0)
+    frames[2] = Frame(K, frames[2].depth, None)
+    ref = O.Reconstructor((n, n, n), voxel, origin, solver=solver, reassociations=1)
+    vol = Volume((n, n, n), voxel, origin)
+    ctx.upload_volume(vol)
+    cfg = pipeline_config(solver=solver, reassociations=1)
+    pose = Pose.make()
+    for i, fr in enumerate(frames):
+        rr = ref.process_frame(fr)
+        rg = ctx.process_frame(fr, pose, cfg, i)
+        pose = rg.pose
+        if i == 2:
+            assert rg.match_count == rr.match_count == 0 and rg.features_added == rr.features_added == 0
+        else:
+            assert rr.features_added > 0 and abs(rg.features_added - rr.features_added) <= 2
+    assert abs(len(ctx.feature_store()) - len(ref.feature_store())) <= 4
