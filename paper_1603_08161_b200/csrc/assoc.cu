@@ -886,6 +886,7 @@ void assoc_find_dense(wfk_ctx* c, const wfk_intrinsics& K, const wfk_correspond_
   }
   WFK_CUDA(cudaStreamSynchronize(s));
   ci.count = n;
+  ci.n_sparse = 0;  // the dense association replaces every constraint
   if (n_out) *n_out = n;
 }
 
