@@ -980,23 +980,28 @@ __global__ void k_icp_accumulate(AssocArgs a, const double* src, const int32_t* 
   }
 }
 
-__global__ void k_icp_update(const double* partials, int nblk, IcpDev* st, wfk_icp_params prm, double* tot_out) {
+// one warp per accumulated value: lanes sum strided block partials, then a
+// fixed shuffle tree (run-to-run identical); thread 0 takes the step.  After
+// convergence the remaining launches of the fixed-length loop return at once.
+constexpr int kIcpUpdateThreads = 32 * kIcpVals;
+__global__ void __launch_bounds__(kIcpUpdateThreads) k_icp_update(const double* partials, int nblk, IcpDev* st,
+                                                                  wfk_icp_params prm, double* tot_out) {
   __shared__ double tot[kIcpVals];
-  const int lane = threadIdx.x;
-  if (lane < kIcpVals) {
-    double t = 0;
-    for (int b = 0; b < nblk; ++b) t += partials[size_t(b) * kIcpVals + lane];
-    tot[lane] = t;
-    if (tot_out) tot_out[lane] = t;
-  }
-  __syncwarp();
   __shared__ double h[6][6], mg[6], delta[6];
+  if (st->done) return;
+  const int v = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double t = 0;
+  for (int b = lane; b < nblk; b += 32) t += partials[size_t(b) * kIcpVals + v];
+  t = warp_sum(t);
   if (lane == 0) {
+    tot[v] = t;
+    if (tot_out) tot_out[v] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
     IcpDev local = *st;
-    if (!local.done) {
-      icp_step(tot, local, prm, h, mg, delta);
-      *st = local;
-    }
+    icp_step(tot, local, prm, h, mg, delta);
+    *st = local;
   }
 }
 
@@ -1057,7 +1062,7 @@ void assoc_estimate_pose(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose& in
   IcpDev hcheck = h0;
   for (int i = 0; i < prm.max_iters; ++i) {
     k_icp_accumulate<<<nblk, kBlock, 0, s>>>(a, src, pos + npx, st, part);
-    k_icp_update<<<1, 32, 0, s>>>(part, nblk, st, prm, tot_dbg);
+    k_icp_update<<<1, kIcpUpdateThreads, 0, s>>>(part, nblk, st, prm, tot_dbg);
     count_launch(c, 2);
     if (hostcheck) {  // debug: the same step on the host from the device's totals
       double tot[kIcpVals];
