@@ -150,3 +150,72 @@ def test_process_frame_features_frame_without_color(ctx):
         else:
             assert rr.features_added > 0 and abs(rg.features_added - rr.features_added) <= 2
     assert abs(len(ctx.feature_store()) - len(ref.feature_store())) <= 4
+
+
+def test_config2_sequence_parity(ctx):
+    """BASELINE configs[1]: 640x480 depth, 64^3 lattice, depth + ARAP + sparse
+    feature terms, default solver / correspondence / fusion parameters, ICP on:
+    four frames of the bend sequence against the oracle Reconstructor."""
+    from paper_1603_08161_b200.wfk import pipeline_config
+    n = 64
+    K = Intrinsics.make(560, 560, 319.5, 239.5, 640, 480)
+    voxel = 0.7 / (n - 1)
+    origin = (-0.35, -0.35, 0.85)
+    frames = bend_frames(ctx, K, 4, 2.0, frames_total=60)
+    ref = O.Reconstructor((n, n, n), voxel, origin, solver=SolverParams.make(), reassociations=3)
+    vol = Volume((n, n, n), voxel, origin)
+    ctx.upload_volume(vol)
+    cfg = pipeline_config(solver=SolverParams.make(), reassociations=3)
+    pose = Pose.make()
+    sparse = 0
+    for i, fr in enumerate(frames):
+        rr = ref.process_frame(fr)
+        rg = ctx.process_frame(fr, pose, cfg, i)
+        pose = rg.pose
+        if i == 0:
+            assert rg.fusion.fused == rr.fusion.fused and rg.features_added == rr.features_added
+            continue
+        assert rg.energy.total == pytest.approx(rr.energy.total, rel=1e-3)
+        assert abs(rg.dense_count - rr.dense_count) <= max(3, 0.002 * rr.dense_count)
+        assert abs(rg.sparse_count - rr.sparse_count) <= 2
+        np.testing.assert_allclose(rg.pose.vector(), rr.pose.vector(), atol=1e-6)
+        sparse += rg.sparse_count
+    assert sparse > 0
+    ctx.download_volume(vol)
+    arr = ref.volume_arrays()
+    both = arr["active"].astype(bool) & vol.active.astype(bool)
+    assert (vol.active != arr["active"]).sum() <= 16
+    dev = np.max(np.linalg.norm(vol.deformed[both] - arr["deformed"][both], axis=1)) / voxel
+    assert dev <= 1e-3, dev
+
+
+def test_config3_short_sequence_parity(ctx):
+    """BASELINE configs[2] (the bench workload): 640x480, 128^3, defaults --
+    the first three frames against the oracle Reconstructor."""
+    from paper_1603_08161_b200.wfk import pipeline_config
+    n = 128
+    K = Intrinsics.make(560, 560, 319.5, 239.5, 640, 480)
+    voxel = 0.7 / (n - 1)
+    origin = (-0.35, -0.35, 0.85)
+    frames = bend_frames(ctx, K, 3, 2.0, frames_total=300)
+    ref = O.Reconstructor((n, n, n), voxel, origin, solver=SolverParams.make(), reassociations=3)
+    vol = Volume((n, n, n), voxel, origin)
+    ctx.upload_volume(vol)
+    cfg = pipeline_config(solver=SolverParams.make(), reassociations=3)
+    pose = Pose.make()
+    for i, fr in enumerate(frames):
+        rr = ref.process_frame(fr)
+        rg = ctx.process_frame(fr, pose, cfg, i)
+        pose = rg.pose
+        if i == 0:
+            assert rg.fusion.fused == rr.fusion.fused and rg.features_added == rr.features_added
+            continue
+        assert rg.energy.total == pytest.approx(rr.energy.total, rel=1e-3)
+        assert abs(rg.dense_count - rr.dense_count) <= max(3, 0.002 * rr.dense_count)
+        assert rg.pcg_iterations == rr.pcg_iterations
+    ctx.download_volume(vol)
+    arr = ref.volume_arrays()
+    both = arr["active"].astype(bool) & vol.active.astype(bool)
+    assert (vol.active != arr["active"]).sum() <= 16
+    dev = np.max(np.linalg.norm(vol.deformed[both] - arr["deformed"][both], axis=1)) / voxel
+    assert dev <= 1e-3, dev
