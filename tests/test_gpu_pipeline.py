@@ -219,3 +219,35 @@ def test_config3_short_sequence_parity(ctx):
     assert (vol.active != arr["active"]).sum() <= 16
     dev = np.max(np.linalg.norm(vol.deformed[both] - arr["deformed"][both], axis=1)) / voxel
     assert dev <= 1e-3, dev
+
+
+def test_config1_fixed_work_parity(ctx):
+    """BASELINE configs[0] as SURVEY.md 8(d) row 1 states it: 320x240, 32^3,
+    depth + ARAP only (use_features 0), levels 1, one reassociation, 5 GN x 10
+    PCG fixed work (flip_flop_rel_tol 0, pcg_tol 0), 10 frames of the bend."""
+    from paper_1603_08161_b200.wfk import pipeline_config
+    n = 32
+    K = Intrinsics.make(280, 280, 159.5, 119.5, 320, 240)
+    voxel = 0.7 / (n - 1)
+    origin = (-0.35, -0.35, 0.85)
+    solver = SolverParams.make(levels=1, flip_flop_iters=5, flip_flop_rel_tol=0.0, pcg_max_iters=10, pcg_tol=0.0)
+    frames = bend_frames(ctx, K, 10, 1.0)
+    ref = O.Reconstructor((n, n, n), voxel, origin, solver=solver, reassociations=1, use_features=False)
+    vol = Volume((n, n, n), voxel, origin)
+    ctx.upload_volume(vol)
+    cfg = pipeline_config(solver=solver, reassociations=1, use_features=False)
+    pose = Pose.make()
+    for i, fr in enumerate(frames):
+        rr = ref.process_frame(fr)
+        rg = ctx.process_frame(fr, pose, cfg, i)
+        pose = rg.pose
+        if i == 0:
+            continue
+        assert rg.trace_len == rr.trace_len == 5
+        assert rg.pcg_iterations == rr.pcg_iterations == 50  # fixed work
+        assert rg.energy.total == pytest.approx(rr.energy.total, rel=1e-3)
+    ctx.download_volume(vol)
+    arr = ref.volume_arrays()
+    both = arr["active"].astype(bool) & vol.active.astype(bool)
+    dev = np.max(np.linalg.norm(vol.deformed[both] - arr["deformed"][both], axis=1)) / voxel
+    assert dev <= 1e-3, dev
