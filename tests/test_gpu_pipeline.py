@@ -175,7 +175,7 @@ def test_config2_sequence_parity(ctx):
         if i == 0:
             assert rg.fusion.fused == rr.fusion.fused and rg.features_added == rr.features_added
             continue
-        assert rg.energy.total == pytest.approx(rr.energy.total, rel=1e-3)
+        assert rg.energy.total == pytest.approx(rr.energy.total, rel=1e-6)  # measured 1e-10 .. 1e-14
         assert abs(rg.dense_count - rr.dense_count) <= max(3, 0.002 * rr.dense_count)
         assert abs(rg.sparse_count - rr.sparse_count) <= 2
         np.testing.assert_allclose(rg.pose.vector(), rr.pose.vector(), atol=1e-6)
@@ -210,7 +210,7 @@ def test_config3_short_sequence_parity(ctx):
         if i == 0:
             assert rg.fusion.fused == rr.fusion.fused and rg.features_added == rr.features_added
             continue
-        assert rg.energy.total == pytest.approx(rr.energy.total, rel=1e-3)
+        assert rg.energy.total == pytest.approx(rr.energy.total, rel=1e-6)  # measured 1e-10 .. 1e-14
         assert abs(rg.dense_count - rr.dense_count) <= max(3, 0.002 * rr.dense_count)
         assert rg.pcg_iterations == rr.pcg_iterations
     ctx.download_volume(vol)
@@ -245,7 +245,7 @@ def test_config1_fixed_work_parity(ctx):
             continue
         assert rg.trace_len == rr.trace_len == 5
         assert rg.pcg_iterations == rr.pcg_iterations == 50  # fixed work
-        assert rg.energy.total == pytest.approx(rr.energy.total, rel=1e-3)
+        assert rg.energy.total == pytest.approx(rr.energy.total, rel=1e-6)  # measured 1e-10 .. 1e-14
     ctx.download_volume(vol)
     arr = ref.volume_arrays()
     both = arr["active"].astype(bool) & vol.active.astype(bool)
