@@ -151,6 +151,7 @@ struct Rot {
 WF_HD Rot rot_t(Rot j) { return {j.c, -j.s}; }
 WF_HD Rot rot_mul(Rot a, Rot b) { return {a.c * b.c - a.s * b.s, a.c * b.s + a.s * b.c}; }
 WF_HD void rot_rows(M3& m, int p, int q, Rot j) {
+#pragma unroll
   for (int i = 0; i < 3; ++i) {
     const double xi = m.a[p][i], yi = m.a[q][i];
     m.a[p][i] = j.c * xi + j.s * yi;
@@ -159,6 +160,7 @@ WF_HD void rot_rows(M3& m, int p, int q, Rot j) {
 }
 WF_HD void rot_cols(M3& m, int p, int q, Rot j) {
   const Rot t = rot_t(j);
+#pragma unroll
   for (int i = 0; i < 3; ++i) {
     const double xi = m.a[i][p], yi = m.a[i][q];
     m.a[i][p] = t.c * xi + t.s * yi;
@@ -200,7 +202,10 @@ WF_HD void svd3(const M3& a, M3& u, double sv[3], M3& v) {
   while (!finished && sweeps < 64) {
     finished = true;
     ++sweeps;
+    // fully unrolled (p, q) pairs: the 3x3 matrices stay in registers
+#pragma unroll
     for (int p = 1; p < 3; ++p)
+#pragma unroll
       for (int q = 0; q < p; ++q) {
         const double threshold = fmax(considerAsZero, precision * maxDiag);
         if (fabs(w.a[p][q]) > threshold || fabs(w.a[q][p]) > threshold) {
@@ -230,29 +235,44 @@ WF_HD void svd3(const M3& a, M3& u, double sv[3], M3& v) {
         }
       }
   }
+#pragma unroll
   for (int i = 0; i < 3; ++i) {
     const double d = w.a[i][i];
     sv[i] = fabs(d);
     if (d < 0)
+#pragma unroll
       for (int k = 0; k < 3; ++k) u.a[k][i] = -u.a[k][i];
   }
+#pragma unroll
   for (int i = 0; i < 3; ++i) sv[i] *= scale;
+  // selection sort by decreasing singular value; the swap with the chosen
+  // column is spelled out per candidate so no index is dynamic
+  bool stop = false;
+#pragma unroll
   for (int i = 0; i < 3; ++i) {
+    if (stop) continue;
     int pos = i;
     double best = sv[i];
+#pragma unroll
     for (int k = i + 1; k < 3; ++k)
       if (sv[k] > best) {
         best = sv[k];
         pos = k;
       }
-    if (best == 0) break;
-    if (pos != i) {
-      double t = sv[i]; sv[i] = sv[pos]; sv[pos] = t;
-      for (int k = 0; k < 3; ++k) {
-        t = u.a[k][i]; u.a[k][i] = u.a[k][pos]; u.a[k][pos] = t;
-        t = v.a[k][i]; v.a[k][i] = v.a[k][pos]; v.a[k][pos] = t;
-      }
+    if (best == 0) {
+      stop = true;
+      continue;
     }
+#pragma unroll
+    for (int k = i + 1; k < 3; ++k)
+      if (pos == k) {
+        double t = sv[i]; sv[i] = sv[k]; sv[k] = t;
+#pragma unroll
+        for (int m = 0; m < 3; ++m) {
+          t = u.a[m][i]; u.a[m][i] = u.a[m][k]; u.a[m][k] = t;
+          t = v.a[m][i]; v.a[m][i] = v.a[m][k]; v.a[m][k] = t;
+        }
+      }
   }
 }
 
