@@ -118,3 +118,26 @@ def test_feature_store_round_trip(ctx):
     assert back.tobytes() == st.tobytes()
     ctx.set_feature_store(st[:0])
     assert len(ctx.feature_store()) == 0
+
+
+def test_match_features_many_groups(ctx):
+    """more frame groups than SMs: the matcher's blocks stride over the store"""
+    base = history(K320, 2, [0, 1])
+    rng = np.random.default_rng(3)
+    groups = []
+    for g in range(200):
+        f = base.copy()
+        f["frame_id"] = g
+        f["descriptor"] = np.clip(f["descriptor"] + rng.normal(0, 0.01, f["descriptor"].shape), 0, None)
+        groups.append(f)
+    st = np.concatenate(groups)
+    fr = frame(K320, (0.01, 0.0, 1.2), 0.4)
+    cur, _ = O.detect_features(fr)
+    cur = backprojected(cur, fr, K320)
+    pred = st["world_pos"].copy()
+    ref = O.match_features(cur, st, pred, K320)
+    got = ctx.match_features(cur, st, pred, K320)
+    assert len(ref) > 200
+    np.testing.assert_array_equal(got["source_id"], ref["source_id"])
+    np.testing.assert_array_equal(got["target_id"], ref["target_id"])
+    np.testing.assert_array_equal(got["distance"], ref["distance"])
