@@ -141,3 +141,21 @@ def test_match_features_many_groups(ctx):
     np.testing.assert_array_equal(got["source_id"], ref["source_id"])
     np.testing.assert_array_equal(got["target_id"], ref["target_id"])
     np.testing.assert_array_equal(got["distance"], ref["distance"])
+
+
+def test_match_features_large_group(ctx):
+    """a frame group whose distance tile exceeds shared memory (the global fallback)"""
+    st = history(K320, 10, [0] * 10)  # one group of ~10 frames of features
+    fr = frame(K640, (0.01, 0.0, 1.2), 0.4)
+    cur, _ = O.detect_features(fr)
+    cur = backprojected(cur, fr, K640)
+    assert len(st) * len(cur) > 16384
+    pred = st["world_pos"].copy()
+    p = FeatureParams.make()
+    p.tau_pixels, p.tau_3d = 1e9, 1e9  # keep every mutual match
+    ref = O.match_features(cur, st, pred, K640, p)
+    got = ctx.match_features(cur, st, pred, K640, p)
+    assert len(ref) > 5
+    np.testing.assert_array_equal(got["source_id"], ref["source_id"])
+    np.testing.assert_array_equal(got["target_id"], ref["target_id"])
+    np.testing.assert_array_equal(got["distance"], ref["distance"])
