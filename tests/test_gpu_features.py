@@ -159,3 +159,18 @@ def test_match_features_large_group(ctx):
     np.testing.assert_array_equal(got["source_id"], ref["source_id"])
     np.testing.assert_array_equal(got["target_id"], ref["target_id"])
     np.testing.assert_array_equal(got["distance"], ref["distance"])
+
+
+@pytest.mark.parametrize("kw", [dict(max_keypoints=20), dict(max_orientations=1), dict(dog_levels=4, octaves=3),
+                                dict(contrast_threshold=0.03, edge_ratio=5.0)])
+def test_features_parity_params(ctx, kw):
+    fr = frame(K640, (0.02, -0.01, 1.25), 1.0)
+    p = FeatureParams.make(**kw)
+    ref, nk_ref = O.detect_features(fr, p)
+    ctx.upload_frame(fr)
+    got, nk = ctx.detect_features(p)
+    assert nk == nk_ref and len(got) == len(ref) and len(got) > 0
+    np.testing.assert_array_equal(got["pixel"], ref["pixel"])
+    np.testing.assert_array_equal(got["scale"], ref["scale"])
+    np.testing.assert_allclose(got["orientation"], ref["orientation"], rtol=0, atol=1e-9)
+    np.testing.assert_allclose(got["descriptor"], ref["descriptor"], rtol=0, atol=1e-5)
