@@ -291,3 +291,42 @@ def test_synth_render_matches_analytic_sphere(ctx):
     both = (depth > 0) & (ref > 0)
     assert np.array_equal(depth > 0, ref > 0) or abs(int((depth > 0).sum()) - int((ref > 0).sum())) < 20
     assert np.max(np.abs(depth[both] - ref[both])) < 1e-5
+
+
+def test_mesh_warp_bit_exact(ctx):
+    """redeform (pipeline.cpp:167-172): mesh vertices re-warped through a new field and pose"""
+    v = fused_sphere_volume()
+    pose0 = Pose.make()
+    mr = O.extract_mesh(v, pose0)
+    ctx.upload_volume(v)
+    ctx.extract_mesh(pose0)
+    act = v.active.astype(bool)
+    v.deformed[act] += np.random.default_rng(8).uniform(-0.003, 0.003, (act.sum(), 3))
+    pose = Pose.make(O.euler_to_matrix((0.01, -0.02, 0.03)), (0.002, 0.001, -0.004))
+    ctx.upload_volume(v)
+    ctx.mesh_warp(pose)
+    mr.warp(v, pose)
+    m = ctx.download_mesh()
+    assert np.array_equal(m.vertices_deformed, mr.vertices_deformed)
+
+
+def test_constraints_append_drops_inactive(ctx):
+    """wfk_constraints_append: caller records after the dense ones, keeping only
+    those whose eight anchors are active (pipeline.cpp:229-236)"""
+    from tests.fixtures import active_sphere_volume, random_dense_constraints, rigid_motion_constraints
+    v = active_sphere_volume(12, 0.05)
+    dense = random_dense_constraints(v, 50, seed=2)
+    sparse = rigid_motion_constraints(v, np.eye(3), (0.01, 0.0, 0.0))
+    sparse["kind"] = 1  # WFK_SPARSE_POINT
+    # deactivate one anchor of every third record
+    for i in range(0, len(sparse), 3):
+        v.active[sparse["anchor_index"][i][0]] = 0
+    ctx.upload_volume(v)
+    ctx.upload_constraints(dense)
+    kept = ctx.append_constraints(sparse, drop_inactive=True)
+    keep = np.array([all(v.active[a] for a in s["anchor_index"]) for s in sparse])
+    assert kept == keep.sum() and 0 < kept < len(sparse)
+    got = ctx.download_constraints()
+    assert len(got) == len(dense) + kept
+    assert got[: len(dense)].tobytes() == np.ascontiguousarray(dense, CORR_DTYPE).tobytes()
+    assert got[len(dense):].tobytes() == np.ascontiguousarray(sparse[keep], CORR_DTYPE).tobytes()
