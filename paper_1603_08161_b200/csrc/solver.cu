@@ -20,6 +20,7 @@
 //     per-block partial -> fixed-order sum).
 #include <cooperative_groups.h>
 #include <chrono>
+#include <string>
 
 #include <cub/cub.cuh>
 #include <type_traits>
@@ -631,7 +632,7 @@ __device__ __forceinline__ void grid_barrier(const FFArgs& a, Red& rs) {
 }
 
 template <int NV>
-__device__ void grid_reduce(const FFArgs& a, Red& rs, double (&v)[NV], PhaseClock* pc = nullptr) {
+__device__ __forceinline__ void grid_reduce(const FFArgs& a, Red& rs, double (&v)[NV], PhaseClock* pc = nullptr) {
   __shared__ double smem[4 * 32];
   __shared__ double bcast[4];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -697,7 +698,7 @@ WF_D void ld_anchors(const FFArgs& a, int64_t c, int rows[8], double w[8]) {
 }
 
 // E_sparse, E_dense, E_reg partials (solver.cpp:345-383)
-__device__ void energy_partials(const FFArgs& a, double& es, double& ed, double& er, int& bad) {
+__device__ __forceinline__ void energy_partials(const FFArgs& a, double& es, double& ed, double& er, int& bad) {
   es = ed = er = 0;
   for (int64_t c = gtid(); c < a.C; c += gstride()) {
     int rows[8];
@@ -732,7 +733,7 @@ __device__ void energy_partials(const FFArgs& a, double& es, double& ed, double&
   }
 }
 
-__device__ wfk_energy energy(const FFArgs& a, cg::grid_group& grid, Red& rs, bool& logic_error) {
+__device__ __forceinline__ wfk_energy energy(const FFArgs& a, cg::grid_group& grid, Red& rs, bool& logic_error) {
   double es, ed, er;
   int bad = 0;
   energy_partials(a, es, ed, er, bad);
@@ -751,7 +752,7 @@ __device__ wfk_energy energy(const FFArgs& a, cg::grid_group& grid, Red& rs, boo
 // q_c = sum_k a_k v[a_k], and a_k u_c scattered to the incidence slot of each
 // anchor row (row-sorted order), so pass 2 sums a contiguous range per row.
 template <class Meta = std::nullptr_t>
-__device__ void matvec_constraints(const FFArgs& a, const double4* v, int skip = 0, const Meta* mm = nullptr) {
+__device__ __forceinline__ void matvec_constraints(const FFArgs& a, const double4* v, int skip = 0, const Meta* mm = nullptr) {
   const int64_t c0 = gtid() - 32 * skip;
   if (c0 < 0) return;
   int k_round = 0;
@@ -913,7 +914,7 @@ __device__ __forceinline__ void row_pass(const FFArgs& a, const double4* v, Sink
 }
 
 // finish_row (solver.cpp:240-269) + Jacobi diagonal (solver.cpp:289-294)
-__device__ void assemble_rows(const FFArgs& a) {
+__device__ __forceinline__ void assemble_rows(const FFArgs& a) {
   for (int r = int(gtid()); r < a.N; r += int(gstride())) {
     const int node = a.rows[r];
     if (a.frozen[r]) {
@@ -1215,14 +1216,14 @@ __device__ __forceinline__ unsigned long long* split_totals(const FFArgs& a, uns
   return a.sync_ll + (seq & 1) * 8;
 }
 // block sum of v -> partials[seq], then a grid barrier (publishes all writes)
-__device__ void split_arrive(const FFArgs& a, Red& rs, double (&v)[kSplitNV], unsigned seq) {
+__device__ __forceinline__ void split_arrive(const FFArgs& a, Red& rs, double (&v)[kSplitNV], unsigned seq) {
   __shared__ double smem[kSplitNV * 32];
   block_sum<kSplitNV>(v, smem);
   if (threadIdx.x < kSplitNV) split_partials(a, seq)[threadIdx.x * gridDim.x + blockIdx.x] = v[threadIdx.x];
   grid_barrier(a, rs);
 }
 // global warp 0 only, after split_arrive's barrier
-__device__ void split_total(const FFArgs& a, unsigned seq) {
+__device__ __forceinline__ void split_total(const FFArgs& a, unsigned seq) {
   const int lane = threadIdx.x & 31;
   const double* part = split_partials(a, seq);
   double t[kSplitNV];
@@ -1259,7 +1260,7 @@ __device__ void split_total(const FFArgs& a, unsigned seq) {
   }
 }
 // every block: wait for the totals of reduction seq
-__device__ void split_wait(const FFArgs& a, unsigned seq, double (&v)[kSplitNV]) {
+__device__ __forceinline__ void split_wait(const FFArgs& a, unsigned seq, double (&v)[kSplitNV]) {
   __shared__ double bc[kSplitNV];
   const int lane = threadIdx.x & 31;
   if (threadIdx.x < 32) {
@@ -1305,22 +1306,24 @@ __device__ __forceinline__ void for_warp_rows(int N, int skip, int K, const int3
 // apart) are always the same, so their Krylov state lives in the block's
 // shared memory for the whole solve: slot (warp-in-block, round, row-in-round),
 // stored component-major (vector, component, slot): consecutive lanes hit
-// consecutive 8-byte words, 24 bytes per 3-vector (WFK_SLOT_SOA=0 selects the
-// padded vector-major layout, 32 bytes per 3-vector).
+// consecutive 8-byte words, 24 bytes per 3-vector.
 enum { kSx, kSr, kSw, kSp, kSs, kSz, kSd, kSn, kSlotVecs };
-struct Slots {
-  double4* sm;  // kSlotVecs x S (or this block's part of the global spill area, stride `stride`)
-  size_t stride;  // elements between two component arrays: S in shared memory, G x S in the spill area
-  int S;        // slots per block = warps per block x K x RPW
-  int K;        // rounds per warp
+// NSM (compile time): kSlotVecs -- the row state lives in shared memory and
+// is addressed through the shared window; kSlotsSpill -- levels too large for
+// shared memory keep it in a global spill area (this block's part, component
+// arrays G x S apart), addressed through a generic pointer.  Specialising the
+// shared case lets the compiler use 32-bit shared addressing in the hot loops.
+constexpr int kSlotsSpill = -1;
+template <int NSM>
+struct SlotsT {
+  double4* sm;    // shared memory, or the spill area (kSlotsSpill)
+  size_t stride;  // S in shared memory, G x S in the spill area
+  int S;          // slots per block = warps per block x K x RPW
+  int K;          // rounds per warp
   int RPW, gw, nw;
   __device__ __forceinline__ int of(int r) const {
     return int(threadIdx.x >> 5) * K * RPW + ((r / RPW - gw) / nw) * RPW + r % RPW;
   }
-#ifndef WFK_SLOT_SOA
-#define WFK_SLOT_SOA 1
-#endif
-#if WFK_SLOT_SOA
   // component-major: (vector, component, slot) -- 24 bytes per 3-vector
   __device__ __forceinline__ double4 get(int v, int q) const {
     const double* b = reinterpret_cast<const double*>(sm) + size_t(3 * v) * stride + q;
@@ -1332,10 +1335,6 @@ struct Slots {
     b[stride] = x.y;
     b[2 * stride] = x.z;
   }
-#else
-  __device__ __forceinline__ double4 get(int v, int q) const { return sm[v * stride + q]; }
-  __device__ __forceinline__ void put(int v, int q, double4 x) const { sm[v * stride + q] = x; }
-#endif
 };
 __host__ __device__ constexpr int pipe_rpw(bool asm_level, bool rows_on_lanes) {
   return rows_on_lanes ? 32 : 32 / (asm_level ? kAsmLanes : kMfLanes);
@@ -1351,7 +1350,7 @@ struct PipeLayout {
   size_t rmeta, cmeta, amat, total;  // byte offsets / size
 };
 __host__ __device__ inline PipeLayout pipe_layout(int N, int64_t C, int rpw, int G, int tpb, int skip, bool rows,
-                                                  bool cons, bool amat = false, bool state_smem = true) {
+                                                  bool cons, bool amat = false, int state_vecs = kSlotVecs) {
   PipeLayout l;
   const int wpb = tpb / 32;
   const int nw = G * wpb - skip;
@@ -1360,8 +1359,8 @@ __host__ __device__ inline PipeLayout pipe_layout(int N, int64_t C, int rpw, int
   const int64_t nt = int64_t(G) * tpb - 32 * skip;
   l.KC = cons ? int((C + nt - 1) / nt) : 0;
   l.SC = tpb * l.KC;
-  // row state in shared memory, or (large lattices) in a global spill area
-  size_t off = state_smem ? size_t(kSlotVecs) * l.S * (WFK_SLOT_SOA ? 3 * sizeof(double) : sizeof(double4)) : 0;
+  // row state in shared memory (state_vecs of the kSlotVecs vectors; the rest spill)
+  size_t off = size_t(state_vecs) * l.S * 3 * sizeof(double);
   l.rmeta = off;
   if (rows) off += size_t(l.S) * (2 * sizeof(int4) + 2 * sizeof(int));
   off = (off + 31) / 32 * 32;
@@ -1423,8 +1422,8 @@ constexpr size_t kPipeSmemMax = 220 * 1024;  // dynamic shared memory for the ro
 // Only m (gathered by neighbours) lives in global memory; x, r, w, p, s, z,
 // D^-1 and n stay in the shared-memory slots of the warp that owns the row.
 // Stopping rule, breakdown test and iteration count are the reference's.
-template <bool ASM>
-__device__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, double& relres) {
+template <bool ASM, int NSM>
+__device__ __forceinline__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, double& relres) {
   extern __shared__ double4 dyn_smem[];
   iters = 0;
   relres = 0;
@@ -1433,21 +1432,17 @@ __device__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, double& relres) {
   const bool comm = gwarp() == 0;
   constexpr int LM = ASM ? kAsmLanes : kMfLanes;
   const bool rows_on_lanes = ASM && a.asm_rows_on_lanes;
-  Slots sl;
+  SlotsT<NSM> sl;
   sl.sm = dyn_smem;
   sl.RPW = pipe_rpw(ASM, rows_on_lanes);
   const bool amat = ASM && a.asm_smem && !rows_on_lanes;
   const PipeLayout lay = pipe_layout(a.N, a.C, sl.RPW, gridDim.x, blockDim.x, kSkip, !ASM && a.meta_rows,
-                                     !ASM && a.meta_cons, amat, a.state_spill == nullptr);
+                                     !ASM && a.meta_cons, amat, a.state_spill ? 0 : kSlotVecs);
   sl.K = lay.K;
   sl.S = lay.S;
   sl.stride = size_t(lay.S);
-  if (a.state_spill) {  // the block's slots in the global spill area
-#if WFK_SLOT_SOA
+  if (NSM == kSlotsSpill && a.state_spill) {  // the block's slots in the global spill area
     sl.sm = reinterpret_cast<double4*>(a.state_spill + size_t(blockIdx.x) * lay.S);
-#else
-    sl.sm = reinterpret_cast<double4*>(a.state_spill) + size_t(blockIdx.x) * lay.S;
-#endif
     sl.stride = size_t(lay.S) * gridDim.x;
   }
   sl.gw = gwarp() - kSkip;
@@ -1649,7 +1644,7 @@ __device__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, double& relres) {
 }
 
 // update_rotations (solver.cpp:385-417) for every row; rot[] follows euler.
-__device__ void rotations(const FFArgs& a) {
+__device__ __forceinline__ void rotations(const FFArgs& a) {
   for (int r = int(gtid()); r < a.N; r += int(gstride())) {
     const int node = a.rows[r];
     const V3 can_i = a.g.canonical(node);
@@ -1682,7 +1677,7 @@ __device__ void rotations(const FFArgs& a) {
 // One instantiation per (PCG variant, level kind): each carries only the PCG
 // code it runs, so the register allocation of one variant does not spill
 // another's hot loops.
-template <int V, bool ASM>
+template <int V, bool ASM, int NSM = kSlotVecs>
 __global__ void __launch_bounds__(kCoopBlock, 1) k_flip_flop(FFArgs a) {
   cg::grid_group grid = cg::this_grid();
   Red rs;
@@ -1725,7 +1720,7 @@ __global__ void __launch_bounds__(kCoopBlock, 1) k_flip_flop(FFArgs a) {
       if (V == 1)
         pcg<ASM>(a, grid, rs, iters, relres);
       else
-        pcg_pipe<ASM>(a, rs, iters, relres);
+        pcg_pipe<ASM, NSM>(a, rs, iters, relres);
       total_pcg += iters;
       pc.lap(9);
       // write back non-frozen rows (solver.cpp:436-437)
@@ -2287,6 +2282,7 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   // pipelined PCG keeps the row state in shared memory; levels too large for
   // it use the Chronopoulos-Gear variant (state in global memory)
   size_t smem = 0;
+  int nsm = kSlotVecs;  // kSlotVecs: row state in shared memory; 0: spilled (pipelined PCG)
   a.meta_rows = a.meta_cons = 0;
   a.asm_smem = 0;
   a.state_spill = nullptr;
@@ -2296,17 +2292,17 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
     const PipeLayout base = pipe_layout(L.N, L.C, rpw, G, kCoopBlock, kPipeSkip, false, false);
     const bool spill = base.total > kPipeSmemMax || getenv("WFK_PIPE_SPILL") != nullptr;  // env: tests
     if (spill) {
-      const size_t n = size_t(kSlotVecs) * (WFK_SLOT_SOA ? 3 : 4) * size_t(G) * size_t(base.S);
-      a.state_spill = L.state_spill.ensure(n);
+      nsm = 0;
+      a.state_spill = L.state_spill.ensure(size_t(kSlotVecs) * 3 * size_t(G) * size_t(base.S));
     }
     auto bytes = [&](bool rows, bool cons) {
-      return pipe_layout(L.N, L.C, rpw, G, kCoopBlock, kPipeSkip, rows, cons, false, !spill).total;
+      return pipe_layout(L.N, L.C, rpw, G, kCoopBlock, kPipeSkip, rows, cons, false, nsm).total;
     };
     static const bool no_meta = getenv("WFK_PIPE_NO_META") != nullptr;
     a.asm_smem = 0;
     static const bool no_asm_smem = getenv("WFK_NO_ASM_SMEM") != nullptr;
     if (L.assembled && !a.asm_rows_on_lanes && !no_meta && !no_asm_smem &&
-        pipe_layout(L.N, L.C, rpw, G, kCoopBlock, kPipeSkip, false, false, true, !spill).total <= kPipeSmemMax)
+        pipe_layout(L.N, L.C, rpw, G, kCoopBlock, kPipeSkip, false, false, true, nsm).total <= kPipeSmemMax)
       a.asm_smem = 1;
     static const bool cmeta = getenv("WFK_PIPE_CMETA") != nullptr;
     if (!L.assembled && !no_meta && cmeta && bytes(true, true) <= kPipeSmemMax) {
@@ -2314,7 +2310,7 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
     } else if (!L.assembled && !no_meta && bytes(true, false) <= kPipeSmemMax) {
       a.meta_rows = 1;
     }
-    smem = a.asm_smem ? pipe_layout(L.N, L.C, rpw, G, kCoopBlock, kPipeSkip, false, false, true, !spill).total
+    smem = a.asm_smem ? pipe_layout(L.N, L.C, rpw, G, kCoopBlock, kPipeSkip, false, false, true, nsm).total
                       : bytes(a.meta_rows, a.meta_cons);
     if (smem > kPipeSmemMax) {
       a.pcg_variant = 1;
@@ -2335,12 +2331,15 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   const bool asm_k = L.assembled;
   if (a.pcg_variant == 1)
     kern = asm_k ? k_flip_flop<1, true> : k_flip_flop<1, false>;
-  else
+  else if (nsm == kSlotVecs)
     kern = asm_k ? k_flip_flop<0, true> : k_flip_flop<0, false>;
+  else
+    kern = asm_k ? k_flip_flop<0, true, kSlotsSpill> : k_flip_flop<0, false, kSlotsSpill>;
   static bool smem_attr = false;
   if (!smem_attr) {
     for (void (*k)(FFArgs) : {k_flip_flop<0, false>, k_flip_flop<0, true>, k_flip_flop<1, false>,
-                              k_flip_flop<1, true>})
+                              k_flip_flop<1, true>, k_flip_flop<0, false, kSlotsSpill>,
+                              k_flip_flop<0, true, kSlotsSpill>})
     {
       WFK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPipeSmemMax)));
       static const int carve = getenv("WFK_CARVEOUT") ? atoi(getenv("WFK_CARVEOUT")) : -1;
