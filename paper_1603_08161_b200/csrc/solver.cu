@@ -1677,8 +1677,8 @@ __device__ __forceinline__ void rotations(const FFArgs& a) {
 // One instantiation per (PCG variant, level kind): each carries only the PCG
 // code it runs, so the register allocation of one variant does not spill
 // another's hot loops.
-template <int V, bool ASM, int NSM = kSlotVecs>
-__global__ void __launch_bounds__(kCoopBlock, 1) k_flip_flop(FFArgs a) {
+template <int V, bool ASM, int NSM = kSlotVecs, int TPB = kCoopBlock>
+__global__ void __launch_bounds__(TPB, 1) k_flip_flop(FFArgs a) {
   cg::grid_group grid = cg::this_grid();
   Red rs;
   // load the row state from the field
@@ -2283,26 +2283,32 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   // it use the Chronopoulos-Gear variant (state in global memory)
   size_t smem = 0;
   int nsm = kSlotVecs;  // kSlotVecs: row state in shared memory; 0: spilled (pipelined PCG)
+  int tpb = kCoopBlock;  // threads per block of the launch
   a.meta_rows = a.meta_cons = 0;
   a.asm_smem = 0;
   a.state_spill = nullptr;
   if (a.pcg_variant == 0) {
     const int rpw = pipe_rpw(L.assembled, a.asm_rows_on_lanes);
     // the row state goes to a global spill area when it does not fit shared memory
-    const PipeLayout base = pipe_layout(L.N, L.C, rpw, G, kCoopBlock, kPipeSkip, false, false);
+    // shared-memory row state runs with kCoopBlockShared threads per block
+    // (more registers per thread: no spills); the spill variant with kCoopBlock
+    tpb = kCoopBlockShared;
+    PipeLayout base = pipe_layout(L.N, L.C, rpw, G, tpb, kPipeSkip, false, false);
     const bool spill = base.total > kPipeSmemMax || getenv("WFK_PIPE_SPILL") != nullptr;  // env: tests
     if (spill) {
       nsm = 0;
+      tpb = kCoopBlock;
+      base = pipe_layout(L.N, L.C, rpw, G, tpb, kPipeSkip, false, false);
       a.state_spill = L.state_spill.ensure(size_t(kSlotVecs) * 3 * size_t(G) * size_t(base.S));
     }
     auto bytes = [&](bool rows, bool cons) {
-      return pipe_layout(L.N, L.C, rpw, G, kCoopBlock, kPipeSkip, rows, cons, false, nsm).total;
+      return pipe_layout(L.N, L.C, rpw, G, tpb, kPipeSkip, rows, cons, false, nsm).total;
     };
     static const bool no_meta = getenv("WFK_PIPE_NO_META") != nullptr;
     a.asm_smem = 0;
     static const bool no_asm_smem = getenv("WFK_NO_ASM_SMEM") != nullptr;
     if (L.assembled && !a.asm_rows_on_lanes && !no_meta && !no_asm_smem &&
-        pipe_layout(L.N, L.C, rpw, G, kCoopBlock, kPipeSkip, false, false, true, nsm).total <= kPipeSmemMax)
+        pipe_layout(L.N, L.C, rpw, G, tpb, kPipeSkip, false, false, true, nsm).total <= kPipeSmemMax)
       a.asm_smem = 1;
     static const bool cmeta = getenv("WFK_PIPE_CMETA") != nullptr;
     if (!L.assembled && !no_meta && cmeta && bytes(true, true) <= kPipeSmemMax) {
@@ -2310,12 +2316,13 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
     } else if (!L.assembled && !no_meta && bytes(true, false) <= kPipeSmemMax) {
       a.meta_rows = 1;
     }
-    smem = a.asm_smem ? pipe_layout(L.N, L.C, rpw, G, kCoopBlock, kPipeSkip, false, false, true, nsm).total
+    smem = a.asm_smem ? pipe_layout(L.N, L.C, rpw, G, tpb, kPipeSkip, false, false, true, nsm).total
                       : bytes(a.meta_rows, a.meta_cons);
     if (smem > kPipeSmemMax) {
       a.pcg_variant = 1;
       a.meta_rows = a.meta_cons = 0;
       smem = 0;
+      tpb = kCoopBlock;
     }
   }
   static const bool no_perm = getenv("WFK_NO_PERM") != nullptr;
@@ -2332,12 +2339,13 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   if (a.pcg_variant == 1)
     kern = asm_k ? k_flip_flop<1, true> : k_flip_flop<1, false>;
   else if (nsm == kSlotVecs)
-    kern = asm_k ? k_flip_flop<0, true> : k_flip_flop<0, false>;
+    kern = asm_k ? k_flip_flop<0, true, kSlotVecs, kCoopBlockShared> : k_flip_flop<0, false, kSlotVecs, kCoopBlockShared>;
   else
     kern = asm_k ? k_flip_flop<0, true, kSlotsSpill> : k_flip_flop<0, false, kSlotsSpill>;
   static bool smem_attr = false;
   if (!smem_attr) {
-    for (void (*k)(FFArgs) : {k_flip_flop<0, false>, k_flip_flop<0, true>, k_flip_flop<1, false>,
+    for (void (*k)(FFArgs) : {k_flip_flop<0, false, kSlotVecs, kCoopBlockShared>,
+                              k_flip_flop<0, true, kSlotVecs, kCoopBlockShared>, k_flip_flop<1, false>,
                               k_flip_flop<1, true>, k_flip_flop<0, false, kSlotsSpill>,
                               k_flip_flop<0, true, kSlotsSpill>})
     {
@@ -2350,7 +2358,7 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   void* args[] = {&a};
   Prof& pf = c->prof;
   if (pf.on) WFK_CUDA(cudaEventRecord(pf.ev[0], s));
-  WFK_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(G), dim3(kCoopBlock), args, smem, s));
+  WFK_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(G), dim3(tpb), args, smem, s));
   if (pf.on) WFK_CUDA(cudaEventRecord(pf.ev[1], s));
   count_launch(c);
   int32_t st[4];
