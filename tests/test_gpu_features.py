@@ -174,3 +174,26 @@ def test_features_parity_params(ctx, kw):
     np.testing.assert_array_equal(got["scale"], ref["scale"])
     np.testing.assert_allclose(got["orientation"], ref["orientation"], rtol=0, atol=1e-9)
     np.testing.assert_allclose(got["descriptor"], ref["descriptor"], rtol=0, atol=1e-5)
+
+
+def test_match_pruning_gates_device(ctx):  # test_features.cpp:135-181
+    from tests.feature_kats import K as KK, pruning_cases
+    for name, store, cur, pred, exp in pruning_cases():
+        m = ctx.match_features(cur, store, pred, KK)
+        assert [(int(a), int(b)) for a, b in zip(m["source_id"], m["target_id"])] == exp, name
+
+
+def test_descriptors_match_across_translation_device(ctx):  # test_features.cpp:103-133
+    from tests.feature_kats import K as KK, blob_frame, with_world
+    ctx.upload_frame(blob_frame())
+    f0, _ = ctx.detect_features()
+    ctx.upload_frame(blob_frame(12, 8))
+    f1, _ = ctx.detect_features()
+    assert len(f0) >= 4 and len(f1) >= 4
+    st = with_world(f0)
+    st["frame_id"] = 0
+    cur = with_world(f1)
+    m = ctx.match_features(cur, st, st["world_pos"], KK)
+    assert len(m) >= 4
+    off = cur["pixel"][m["target_id"]] - st["pixel"][m["source_id"]]
+    assert np.all(np.abs(off[:, 0] - 12) < 1.5) and np.all(np.abs(off[:, 1] - 8) < 1.5)

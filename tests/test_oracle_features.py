@@ -73,3 +73,25 @@ def test_descriptor_distance():
     b = np.zeros(128, np.float32)
     a[3], b[3] = 0.5, -0.5
     assert O.descriptor_distance(a, b) == pytest.approx(1.0)
+
+
+def test_match_pruning_gates():  # test_features.cpp:135-181
+    from tests.feature_kats import K as KK, pruning_cases
+    for name, store, cur, pred, exp in pruning_cases():
+        m = O.match_features(cur, store, pred, KK)
+        assert [(int(a), int(b)) for a, b in zip(m["source_id"], m["target_id"])] == exp, name
+
+
+def test_descriptors_match_across_translation():  # test_features.cpp:103-133
+    from tests.feature_kats import K as KK, blob_frame, with_world
+    f0, _ = O.detect_features(blob_frame())
+    f1, _ = O.detect_features(blob_frame(12, 8))
+    assert len(f0) >= 4 and len(f1) >= 4
+    st = with_world(f0)
+    st["frame_id"] = 0
+    cur = with_world(f1)
+    m = O.match_features(cur, st, st["world_pos"], KK)
+    assert len(m) >= 4
+    off = cur["pixel"][m["target_id"]] - st["pixel"][m["source_id"]]
+    assert np.all(np.abs(off[:, 0] - 12) < 1.5) and np.all(np.abs(off[:, 1] - 8) < 1.5)
+    assert np.all(m["distance"] <= FeatureParams.make().tau_descriptor)
