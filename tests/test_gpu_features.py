@@ -197,3 +197,17 @@ def test_descriptors_match_across_translation_device(ctx):  # test_features.cpp:
     assert len(m) >= 4
     off = cur["pixel"][m["target_id"]] - st["pixel"][m["source_id"]]
     assert np.all(np.abs(off[:, 0] - 12) < 1.5) and np.all(np.abs(off[:, 1] - 8) < 1.5)
+
+
+def test_blobs_detected_near_centers_device(ctx):  # test_features.cpp:82-101
+    from tests.feature_kats import CENTERS, blob_frame
+    fr = blob_frame()
+    ctx.upload_frame(fr)
+    f, nk = ctx.detect_features()
+    assert nk > 0
+    near = [np.min(np.linalg.norm(f["pixel"] - np.array(c), axis=1)) < 3.0 for c in CENTERS]
+    assert sum(near) >= len(CENTERS) - 1  # features: one blob may fail the descriptor tests
+    fr.depth[:] = 0
+    ctx.upload_frame(fr)
+    f, nk = ctx.detect_features()
+    assert nk == 0 and len(f) == 0

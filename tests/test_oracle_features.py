@@ -95,3 +95,20 @@ def test_descriptors_match_across_translation():  # test_features.cpp:103-133
     off = cur["pixel"][m["target_id"]] - st["pixel"][m["source_id"]]
     assert np.all(np.abs(off[:, 0] - 12) < 1.5) and np.all(np.abs(off[:, 1] - 8) < 1.5)
     assert np.all(m["distance"] <= FeatureParams.make().tau_descriptor)
+
+
+def test_blobs_detected_near_centers():  # test_features.cpp:82-101
+    from tests.feature_kats import CENTERS, blob_frame
+    fr = blob_frame()
+    f, nk = O.detect_features(fr)
+    assert nk > 0
+    px = f["pixel"]
+    # the reference checks its keypoints; these are the features that survive
+    # extract_descriptors, so one blob may lose its feature to the descriptor tests
+    near = [np.min(np.linalg.norm(px - np.array(c), axis=1)) < 3.0 for c in CENTERS]
+    assert sum(near) >= len(CENTERS) - 1
+    for p, s in zip(px, f["scale"]):
+        assert np.min(np.linalg.norm(np.array(CENTERS) - p, axis=1)) < 4.0 * s + 4.0
+    fr.depth[:] = 0  # without valid depth nothing may be detected
+    f, nk = O.detect_features(fr)
+    assert nk == 0 and len(f) == 0
