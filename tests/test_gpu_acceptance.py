@@ -1,0 +1,123 @@
+"""Acceptance criterion 7 of the reference (acceptance.cpp:616-656): feature
+ablation on a tangentially sliding textured plane.  Point-to-plane terms
+cannot see motion along the plane; the sparse feature term can, so with the
+feature front-end on, the drift of tracked material points must stay below
+half of the dense-only drift.  Run on the B200 path (wfk_process_frame) with
+the drift tracker of acceptance.cpp:188-214 (wfk_invert_warp).
+
+The scene is rendered here in numpy (test infrastructure): plane z = 1.3 m
+facing the camera inside the bounds |x|, |y| <= 0.25 m, the Dots texture of
+synthcam.cpp:98-119 (scale 0.03 m, seed 7, dot radius 0.3) on the material
+point, rigid translation 2 mm per frame along x, 30 frames at 320x240.
+"""
+import numpy as np
+import pytest
+
+from paper_1603_08161_b200.abi import Frame, Intrinsics, Pose, SolverParams, Volume
+
+pytestmark = pytest.mark.gpu
+
+K = Intrinsics.make(280.0, 280.0, 159.5, 119.5, 320, 240)
+M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def splitmix64(x):
+    x = (x + np.uint64(0x9E3779B97F4A7C15)) & M64
+    x = ((x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)) & M64
+    x = ((x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)) & M64
+    return x ^ (x >> np.uint64(31))
+
+
+def hash_cell(ix, iy, iz, seed):
+    h = np.full(ix.shape, np.uint64(seed))
+    for v in (ix, iy, iz):
+        h = splitmix64(h ^ v.astype(np.int64).view(np.uint64))
+    return h
+
+
+def rand01(h):
+    return (h >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+
+
+def dots_color(p, scale=0.03, seed=7, dot_radius=0.3):
+    """texture_color (synthcam.cpp:98-119), Dots, at material points p (n x 3)"""
+    cell = p / scale
+    f = np.floor(cell)
+    h = hash_cell(f[:, 0], f[:, 1], f[:, 2], seed)
+    margin = dot_radius + 0.05
+    h1 = splitmix64(h)
+    h2 = splitmix64(h1)
+    center = f + margin + np.stack([rand01(h), rand01(h1), rand01(h2)], 1) * (1 - 2 * margin)
+    inside = np.linalg.norm(cell - center, axis=1) < dot_radius
+    hc = splitmix64(h ^ np.uint64(0xD0D5))
+    hc1 = splitmix64(hc)
+    hc2 = splitmix64(hc1)
+    rgb = np.stack([20 + 160 * rand01(hc), 20 + 160 * rand01(hc1), 20 + 160 * rand01(hc2)], 1)
+    out = np.full(p.shape, 210.0)
+    out[inside] = rgb[inside]
+    return out.astype(np.float32)
+
+
+def shift(f):
+    return np.array([0.002 * f, 0.0, 0.0])  # WarpType::Rigid, trans_per_frame
+
+
+def render(f, z=1.3, half=0.25):
+    v, u = np.mgrid[0:K.height, 0:K.width].astype(np.float64)
+    p = np.stack([(u - K.cx) / K.fx * z, (v - K.cy) / K.fy * z, np.full(u.shape, z)], -1).reshape(-1, 3)
+    inside = (np.abs(p[:, 0]) <= half) & (np.abs(p[:, 1]) <= half)
+    depth = np.where(inside, z, 0.0).astype(np.float32).reshape(K.height, K.width)
+    color = dots_color(p - shift(f)).reshape(K.height, K.width, 3)
+    color[~inside.reshape(K.height, K.width)] = 0
+    return Frame(K, depth, color)
+
+
+def truth_samples(z=1.3, half=0.25, n=17, cap=200):
+    """truth_surface_samples (acceptance.cpp:153-186) for the plane: grid points projected onto it"""
+    g = np.linspace(-half, half, n)
+    pts = [(x, y, z) for y in g for x in g]
+    return np.array(pts[:cap])
+
+
+def tangential_drift(ctx, use_features, frames=30):
+    from paper_1603_08161_b200.wfk import pipeline_config
+    n, voxel, origin = 64, 0.01, (-0.315, -0.315, 1.0)
+    vol = Volume((n, n, n), voxel, origin)
+    ctx.upload_volume(vol)
+    cfg = pipeline_config(solver=SolverParams.make(), use_features=use_features)
+    pose = Pose.make()
+    pts = truth_samples()
+    last = pts.copy()
+    ref = np.zeros_like(pts)
+    has = np.zeros(len(pts), bool)
+    total, count = 0.0, 0
+    for f in range(frames):
+        rec = ctx.process_frame(render(f), pose, cfg, f)
+        pose = rec.pose
+        y = pts + shift(f)  # the material points' current world positions
+        c, ok = ctx.invert_warp(pose, y, last)
+        ok = ok.astype(bool)
+        last[ok] = c[ok]
+        first = ok & ~has
+        ref[first] = c[first]
+        again = ok & has
+        total += np.linalg.norm(c[again] - ref[again], axis=1).sum()
+        count += int(again.sum())
+        has |= ok
+    return total / count if count else -1.0
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_1603_08161_b200.wfk import Context
+    c = Context(0)
+    yield c
+    c.close()
+
+
+def test_feature_ablation_tangential_drift(ctx):  # acceptance criterion 7
+    both = tangential_drift(ctx, True)
+    dense_only = tangential_drift(ctx, False)
+    print(f"drift sparse+dense {both:.5f} m, dense-only {dense_only:.5f} m, ratio {both / dense_only:.3f}")
+    assert both >= 0 and dense_only > 0
+    assert both < 0.5 * dense_only
