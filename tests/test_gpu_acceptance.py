@@ -1,4 +1,10 @@
-"""Acceptance criterion 7 of the reference (acceptance.cpp:616-656): feature
+"""Acceptance criteria of the reference run on the B200 path.
+
+Criterion 3 (acceptance.cpp:399-457): ten identical frames of a large spherical
+cap leave the deformation at the identity, the TSDF equal to the analytic
+projective TSDF and the canonical mesh on the sphere.
+
+Criterion 7 (acceptance.cpp:616-656): feature
 ablation on a tangentially sliding textured plane.  Point-to-plane terms
 cannot see motion along the plane; the sparse feature term can, so with the
 feature front-end on, the drift of tracked material points must stay below
@@ -121,3 +127,52 @@ def test_feature_ablation_tangential_drift(ctx):  # acceptance criterion 7
     print(f"drift sparse+dense {both:.5f} m, dense-only {dense_only:.5f} m, ratio {both / dense_only:.3f}")
     assert both >= 0 and dense_only > 0
     assert both < 0.5 * dense_only
+
+
+def test_static_sequence_identity(ctx):  # acceptance criterion 3 (acceptance.cpp:399-457)
+    """ten identical frames of a large face-on spherical cap: the deformation
+    stays the identity, the TSDF matches the analytic projective TSDF and the
+    canonical mesh lies on the sphere"""
+    from paper_1603_08161_b200.wfk import SynthScene, pipeline_config
+    center, radius = np.array([0.0, 0.0, 2.2]), 1.0
+    s = SynthScene()
+    s.center[:] = center
+    s.radius = radius
+    s.pivot[:] = center
+    s.amplitude = 0.0
+    s.driver_axis, s.rot_axis = 0, 1
+    s.t_min, s.t_max = 0.05, 6.0
+    s.texture_seed, s.texture_scale, s.dot_radius = 7, 0.06, 0.3
+    depth, color = ctx.synth_render(s, K)
+    fr = Frame(K, depth, color)
+    n, voxel, origin = 64, 0.01, (-0.315, -0.315, 1.05)
+    vol = Volume((n, n, n), voxel, origin)
+    ctx.upload_volume(vol)
+    cfg = pipeline_config(solver=SolverParams.make())
+    pose = Pose.make()
+    for f in range(10):
+        pose = ctx.process_frame(fr, pose, cfg, f).pose
+    ctx.download_volume(vol)
+    act = vol.active.astype(bool)
+    can = vol.canonical_positions()
+    max_deform = np.max(np.linalg.norm(vol.deformed[act] - can[act], axis=1))
+    # analytic projective TSDF along each voxel's camera ray
+    w = vol.weight > 0
+    p = can[w]
+    d = p / np.linalg.norm(p, axis=1, keepdims=True)
+    b = d @ center
+    disc = b * b - center @ center + radius * radius
+    ok = disc >= 0
+    sdf = (b - np.sqrt(np.where(ok, disc, 0))) * d[:, 2] - p[:, 2]
+    trunc = 4 * voxel
+    ok &= sdf >= -trunc
+    sdf = np.minimum(sdf, trunc)
+    tsdf_err = np.max(np.abs(vol.tsdf[w][ok] - sdf[ok]))
+    nv, nt = ctx.extract_mesh(Pose.make())
+    m = ctx.download_mesh()
+    mesh_err = np.max(np.abs(np.linalg.norm(m.vertices_canonical - center, axis=1) - radius))
+    print(f"max deform {max_deform:.2e} m, tsdf err {tsdf_err:.2e}, mesh err {mesh_err:.2e}")
+    assert nt > 0
+    assert max_deform < 1e-4
+    assert tsdf_err < voxel / 4
+    assert mesh_err < voxel / 2
