@@ -4,6 +4,9 @@ Criterion 3 (acceptance.cpp:399-457): ten identical frames of a large spherical
 cap leave the deformation at the identity, the TSDF equal to the analytic
 projective TSDF and the canonical mesh on the sphere.
 
+Criterion 4 (acceptance.cpp:460-502): the global-pose ICP tracks a camera
+moving rigidly in a five-wall room corner to < 0.1 degree and < 1 mm.
+
 Criterion 7 (acceptance.cpp:616-656): feature
 ablation on a tangentially sliding textured plane.  Point-to-plane terms
 cannot see motion along the plane; the sparse feature term can, so with the
@@ -176,3 +179,55 @@ def test_static_sequence_identity(ctx):  # acceptance criterion 3 (acceptance.cp
     assert max_deform < 1e-4
     assert tsdf_err < voxel / 4
     assert mesh_err < voxel / 2
+
+
+def axis_angle(axis, angle):
+    a = np.asarray(axis, np.float64)
+    a = a / np.linalg.norm(a)
+    kx = np.array([[0, -a[2], a[1]], [a[2], 0, -a[0]], [-a[1], a[0], 0]])
+    return np.eye(3) + np.sin(angle) * kx + (1 - np.cos(angle)) * kx @ kx
+
+
+def room_frame(R, t):
+    """the five-wall room of acceptance.cpp:463-478 seen from camera pose (R, t)
+    (world -> camera), walls n . p = offset, free space n . p > offset"""
+    walls = [((0, 0, -1), -1.45), ((1, 0, 0), -0.26), ((-1, 0, 0), -0.26), ((0, 1, 0), -0.26), ((0, -1, 0), -0.26)]
+    v, u = np.mgrid[0:K.height, 0:K.width].astype(np.float64)
+    d_cam = np.stack([(u - K.cx) / K.fx, (v - K.cy) / K.fy, np.ones_like(u)], -1).reshape(-1, 3)
+    o_w = -R.T @ t
+    d_w = d_cam @ R  # R^T d for each row
+    best = np.full(len(d_w), np.inf)
+    for n, off in walls:
+        n = np.array(n, np.float64)
+        nd = d_w @ n
+        with np.errstate(divide="ignore", invalid="ignore"):
+            th = (off - n @ o_w) / nd
+        ok = (nd < 0) & (th > 0)
+        best = np.where(ok & (th < best), th, best)
+    hit = np.isfinite(best)
+    depth = np.where(hit, best, 0.0).astype(np.float32).reshape(K.height, K.width)
+    p_w = o_w + best[:, None] * d_w
+    color = np.zeros((len(d_w), 3), np.float32)
+    color[hit] = dots_color(p_w[hit], scale=0.06)
+    return Frame(K, depth, color.reshape(K.height, K.width, 3))
+
+
+def test_rigid_tracking_room_corner(ctx):  # acceptance criterion 4 (acceptance.cpp:460-502)
+    from paper_1603_08161_b200.wfk import pipeline_config
+    n, voxel, origin = 64, 0.01, (-0.315, -0.315, 0.95)
+    vol = Volume((n, n, n), voxel, origin)
+    ctx.upload_volume(vol)
+    cfg = pipeline_config(solver=SolverParams.make())
+    pose = Pose.make()
+    worst_rot = worst_trans = 0.0
+    for f in range(30):
+        R = axis_angle((0.2, 1.0, 0.1), np.deg2rad(0.25) * f)
+        t = np.array([0.0015, 0.001, 0.001]) * f
+        rec = ctx.process_frame(room_frame(R, t), pose, cfg, f)
+        pose = rec.pose
+        Rg, tg = rec.pose.matrix(), rec.pose.vector()
+        cosang = np.clip((np.trace(Rg.T @ R) - 1) / 2, -1, 1)
+        worst_rot = max(worst_rot, np.rad2deg(np.arccos(cosang)))
+        worst_trans = max(worst_trans, np.linalg.norm(tg - t))
+    print(f"worst pose error {worst_rot:.4f} deg, {worst_trans * 1e3:.3f} mm")
+    assert worst_rot < 0.1 and worst_trans < 0.001
