@@ -589,8 +589,8 @@ WF_D void st4w(double4* p, int64_t i, double4 v) { reinterpret_cast<D4*>(p)[i] =
 // ---- grid synchronisation of the persistent kernel -------------------------
 // One arrival counter and one generation word (separate 128 B lines).  A block
 // arrives with a single acq_rel atomic from thread 0 after a block barrier; the
-// last of the G arrivals resets the counter and releases the next generation;
-// the others poll the generation word.
+// others poll the counter until it reaches G (gen + 1), and the last arrival
+// raises the generation word (monotonically, red.max) for grid_reduce.
 //
 // grid_reduce fuses that barrier with a deterministic sum: every block
 // publishes its partials before arriving, and ONLY the last arriving block
@@ -606,6 +606,11 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
 __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// monotonic release of the generation word: plain-barrier and reduction
+// releases can land out of order, the word must never move backwards
+__device__ __forceinline__ void atom_max_release_u32(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.max.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ unsigned atom_add_acq_rel_u32(unsigned* p, unsigned v) {
   unsigned old;
   asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
@@ -619,11 +624,14 @@ __device__ __forceinline__ void grid_barrier(const FFArgs& a, Red& rs) {
     // generation g reads G (g + 1) - 1.  The acq_rel arrival releases the
     // block's writes (ordered before it by the block barrier) and, for the
     // last block, acquires everyone else's.
+    const unsigned target = gridDim.x * (rs.gen + 1);
     const unsigned old = atom_add_acq_rel_u32(a.sync_count, 1u);
-    if (old == gridDim.x * (rs.gen + 1) - 1) {
-      st_release_u32(a.sync_gen, rs.gen + 1);
+    if (old == target - 1) {
+      atom_max_release_u32(a.sync_gen, rs.gen + 1);
     } else {
-      while (ld_acquire_u32(a.sync_gen) == rs.gen) {
+      // poll the arrival counter itself: the last arrival's RMW is visible
+      // one L2 round trip earlier than the generation word it then writes
+      while (ld_acquire_u32(a.sync_count) < target) {
       }
     }
   }
@@ -660,10 +668,12 @@ __device__ __forceinline__ void grid_reduce(const FFArgs& a, Red& rs, double (&v
       if (lane == 0) {
 #pragma unroll
         for (int k = 0; k < NV; ++k) a.sync_total[k] = s[k];
-        st_release_u32(a.sync_gen, rs.gen + 1);
+        atom_max_release_u32(a.sync_gen, rs.gen + 1);
       }
     } else if (lane == 0) {
-      while (ld_acquire_u32(a.sync_gen) == rs.gen) {
+      // the generation word may still lag (a plain barrier's last arrival
+      // raises it after the others have left): wait until it reaches ours
+      while (int(ld_acquire_u32(a.sync_gen) - (rs.gen + 1)) < 0) {
       }
     }
     if (lane == 0)
