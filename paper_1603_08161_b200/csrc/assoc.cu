@@ -17,6 +17,7 @@
 //    one 64-bit atomicMin on (float depth bits, triangle index) per covered
 //    pixel, then the winner's attributes are resolved per pixel;
 //  * association compacts per-pixel candidates in row-major order.
+#include <mutex>
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
@@ -40,10 +41,15 @@ struct McTables {
   int8_t corner_off[8][3];
 };
 __constant__ McTables c_mc;
-static bool g_mc_ready = false;
+// __constant__ memory is per device: upload once per device, under a lock
+static std::mutex g_mc_mu;
+static unsigned long long g_mc_ready = 0;  // bit d: tables uploaded to device d
 
 static void mc_tables_init() {
-  if (g_mc_ready) return;
+  int dev = 0;
+  WFK_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_mc_mu);
+  if (g_mc_ready & (1ull << (dev & 63))) return;
   McTables t;
   for (int c = 0; c < 256; ++c) {
     const char* s = kWfMcCases[c];
@@ -70,7 +76,7 @@ static void mc_tables_init() {
   for (int c = 0; c < 8; ++c)
     for (int k = 0; k < 3; ++k) t.corner_off[c][k] = int8_t(kWfMcCornerOffset[c][k]);
   WFK_CUDA(cudaMemcpyToSymbol(c_mc, &t, sizeof(t)));
-  g_mc_ready = true;
+  g_mc_ready |= 1ull << (dev & 63);
 }
 
 // ---------------------------------------------------------------------------

@@ -90,7 +90,12 @@ struct DistComm {
   }
 };
 
+void dist_forget(wfk_ctx* c);
+
+// drops the communicator AND every captured iteration of this context: the
+// graphs hold NCCL nodes bound to the communicator being destroyed
 void dist_destroy(wfk_ctx* c) {
+  dist_forget(c);
   delete c->dist;
   c->dist = nullptr;
 }
@@ -326,6 +331,7 @@ struct Transport {
   virtual void exchange(std::vector<DSlab>& s, double* DSlab::*vec, const DistPlan& plan) = 0;
   virtual void allgather(std::vector<DSlab>& s) = 0;
   virtual void final_x(std::vector<DSlab>& s, const DistPlan& plan) = 0;
+  virtual const void* id() const { return nullptr; }  // communicator a captured graph binds to
 };
 
 struct SlabsTransport : Transport {
@@ -358,6 +364,7 @@ struct NcclTransport : Transport {
   cudaStream_t st;
   DistComm* d;
   NcclTransport(cudaStream_t s, DistComm* dc) : st(s), d(dc) {}
+  const void* id() const override { return d->comm; }
   void exchange(std::vector<DSlab>& s, double* DSlab::*vec, const DistPlan& plan) override {
     NcclApi& n = nccl();
     double* v = s[0].*vec;
@@ -406,6 +413,7 @@ struct DistWork {
   const double *B = nullptr, *RHS = nullptr;
   const int32_t* CL = nullptr;
   uint64_t plan_ver = 0;
+  const void* transport_id = nullptr;  // the communicator (or null for in-process slabs) the graph captured
   std::vector<std::unique_ptr<SlabBufs>> bufs;
   std::vector<DSlab> sl;
   static constexpr int kBatch = 8;
@@ -430,9 +438,10 @@ void run_dist_pcg_dev(wfk_ctx* c, int N, int world, const std::vector<int>& rank
                       int max_iters, wfk_pcg_result* res, Transport& tr, DistWork& w) {
   cudaStream_t s = c->stream;
   const bool reuse = w.exec && w.ctx == c && w.N == N && w.world == world && w.ranks == ranks && w.B == B &&
-                     w.CL == CL && w.RHS == RHS && w.plan_ver == plan_ver;
+                     w.CL == CL && w.RHS == RHS && w.plan_ver == plan_ver && w.transport_id == tr.id();
   if (!reuse) {
     w.reset();
+    w.transport_id = tr.id();
     w.ctx = c;
     w.N = N;
     w.world = world;

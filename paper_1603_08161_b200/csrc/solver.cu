@@ -20,6 +20,7 @@
 //     per-block partial -> fixed-order sum).
 #include <cooperative_groups.h>
 #include <chrono>
+#include <mutex>
 #include <string>
 
 #include <cub/cub.cuh>
@@ -631,7 +632,7 @@ __device__ __forceinline__ void grid_barrier(const FFArgs& a, Red& rs) {
     } else {
       // poll the arrival counter itself: the last arrival's RMW is visible
       // one L2 round trip earlier than the generation word it then writes
-      while (ld_acquire_u32(a.sync_count) < target) {
+      while (int(ld_acquire_u32(a.sync_count) - target) < 0) {
       }
     }
   }
@@ -2234,13 +2235,9 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   a.m0 = L.mbuf.p;
   a.m1 = L.mbuf.p + std::max(L.N, 1);
   a.nbuf = L.nbuf.p;
-  static const int pcg_variant = [] {
-    const char* v = getenv("WFK_PCG");
-    if (v && std::string(v) == "cg") return 1;
-    if (v && std::string(v) == "pipe") return 0;
-    return 0;
-  }();
-  a.pcg_variant = pcg_variant;
+  // read per call so tests can force the Chronopoulos-Gear variant
+  const char* pcg_env = getenv("WFK_PCG");
+  a.pcg_variant = (pcg_env && std::string(pcg_env) == "cg") ? 1 : 0;
   a.assembled = L.assembled ? 1 : 0;
   a.asm_rows_on_lanes = L.N >= kAsmThreadRows ? 1 : 0;
   a.blk = L.blk;
@@ -2304,7 +2301,7 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
     // (more registers per thread: no spills); the spill variant with kCoopBlock
     tpb = kCoopBlockShared;
     PipeLayout base = pipe_layout(L.N, L.C, rpw, G, tpb, kPipeSkip, false, false);
-    const bool spill = base.total > kPipeSmemMax || getenv("WFK_PIPE_SPILL") != nullptr;  // env: tests
+    const bool spill = base.total > kPipeSmemMax || getenv("WFK_PIPE_SPILL") != nullptr;  // env (any value): tests force the spill area
     if (spill) {
       nsm = 0;
       tpb = kCoopBlock;
@@ -2352,8 +2349,12 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
     kern = asm_k ? k_flip_flop<0, true, kSlotVecs, kCoopBlockShared> : k_flip_flop<0, false, kSlotVecs, kCoopBlockShared>;
   else
     kern = asm_k ? k_flip_flop<0, true, kSlotsSpill> : k_flip_flop<0, false, kSlotsSpill>;
-  static bool smem_attr = false;
-  if (!smem_attr) {
+  // kernel attributes are per device: set once per device, under a lock
+  static std::mutex attr_mu;
+  static unsigned long long attr_done = 0;  // bit d: device d configured
+  {
+  std::lock_guard<std::mutex> attr_lock(attr_mu);
+  if (!(attr_done & (1ull << (c->device & 63)))) {
     for (void (*k)(FFArgs) : {k_flip_flop<0, false, kSlotVecs, kCoopBlockShared>,
                               k_flip_flop<0, true, kSlotVecs, kCoopBlockShared>, k_flip_flop<1, false>,
                               k_flip_flop<1, true>, k_flip_flop<0, false, kSlotsSpill>,
@@ -2363,7 +2364,8 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
       static const int carve = getenv("WFK_CARVEOUT") ? atoi(getenv("WFK_CARVEOUT")) : -1;
       if (carve >= 0) WFK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     }
-    smem_attr = true;
+    attr_done |= 1ull << (c->device & 63);
+  }
   }
   void* args[] = {&a};
   Prof& pf = c->prof;
