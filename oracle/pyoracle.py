@@ -1,7 +1,17 @@
 """ORACLE -- test infrastructure only (tests/, __graft_entry__.smoke(), bench.py's
-CPU-baseline leg).  ctypes front end of oracle/_build/liboracle.so, the CPU
-restatement of the reference hot path (oracle/wf_oracle.cpp).  Never imported
-by the product package."""
+CPU-baseline leg).  ctypes front end of the wfo_* C ABI (oracle/wfo.h), served
+by one of two CPU backends:
+
+* "ref"  -- oracle/_ref/libwfref.so: the UNMODIFIED reference sources
+  (/root/reference/proj/src) compiled against the Eigen/doctest shims
+  (oracle/ref/Makefile), behind a conversion-only C ABI (oracle/ref/capi.cpp);
+* "port" -- oracle/_build/liboracle.so: the line-by-line restatement
+  (oracle/wf_oracle.cpp), kept as the checker where the reference has no
+  public entry point and as a cross-check of the reference build.
+
+WF_ORACLE=ref|port picks the backend (default: "ref" when libwfref.so is
+built, else "port"); set_backend() switches it at run time.  Never imported by
+the product package."""
 from __future__ import annotations
 
 import ctypes as C
@@ -20,6 +30,8 @@ from paper_1603_08161_b200.abi import (
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_build", "liboracle.so")
+REF_LIB_PATH = os.path.join(HERE, "_ref", "libwfref.so")
+REFERENCE_SRC = "/root/reference/proj"
 
 
 def build(force: bool = False) -> str:
@@ -28,16 +40,50 @@ def build(force: bool = False) -> str:
     return LIB_PATH
 
 
-_lib = None
+def build_ref(force: bool = False) -> str | None:
+    """Compile the reference into oracle/_ref (only where /root/reference is
+    mounted; the GPU box uses the prebuilt files)."""
+    if (force or not os.path.exists(REF_LIB_PATH)) and os.path.isdir(REFERENCE_SRC):
+        subprocess.run(["make", "-s", "-j8", "-C", os.path.join(HERE, "ref")], check=True)
+    return REF_LIB_PATH if os.path.exists(REF_LIB_PATH) else None
 
 
-def lib():
-    global _lib
-    if _lib is None:
-        build()
-        _lib = C.CDLL(LIB_PATH)
-        _declare(_lib)
-    return _lib
+def ref_available() -> bool:
+    return os.path.exists(REF_LIB_PATH)
+
+
+_libs: dict = {}
+_backend = os.environ.get("WF_ORACLE") or ("ref" if os.path.exists(REF_LIB_PATH) else "port")
+
+
+def backend() -> str:
+    return _backend
+
+
+def set_backend(kind: str) -> str:
+    """Switch the wfo_* backend ("ref" or "port"); returns the previous one.
+    Handles (normal equations, meshes, reconstructors) belong to the backend
+    that made them."""
+    global _backend
+    if kind not in ("ref", "port"):
+        raise ValueError(kind)
+    prev, _backend = _backend, kind
+    return prev
+
+
+def lib(kind: str | None = None):
+    kind = kind or _backend
+    if kind not in _libs:
+        if kind == "ref":
+            path = build_ref()
+            if path is None:
+                raise OracleError(WFK_E_INVALID_ARG, "reference build oracle/_ref/libwfref.so is missing")
+        else:
+            path = build()
+        l = C.CDLL(path)
+        _declare(l)
+        _libs[kind] = l
+    return _libs[kind]
 
 
 def _declare(l):
