@@ -15,7 +15,8 @@ update) runs around it, as in the reference's default configuration
 (config.hpp:44-45, pipeline.cpp:95-141, 174-217, 257) -- on in both arms.
 
   python bench.py [--gpus N --steps K --warmup W]        B200 arm (libwfk.so)
-  python bench.py --impl reference [...]                  CPU arm (the oracle port)
+  python bench.py --impl reference [...]                  CPU arm (the reference's own code,
+                                                          oracle/_ref, on the host cores)
 
 Frame 0 bootstraps the volume (untimed); W warm-up frames follow; K frames
 are timed.  `value` times K frames whose inputs are staged in HBM beforehand;
@@ -31,7 +32,6 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import subprocess
 import sys
@@ -74,9 +74,36 @@ def workload_config(n_gpus):
     }
 
 
-def frame_amplitude(f):
-    # SyntheticScene::warp_phase with frequency > 0 (synthcam.cpp:131-136)
-    return AMPLITUDE * math.sin(2 * math.pi * FREQUENCY * f / FRAMES_TOTAL)
+def scene(K):
+    """The configs' synthetic sequence: tools/synthscene, the
+    reference's SyntheticScene restated bit for bit (tests/test_synthscene.py),
+    rendered on the host -- both arms consume identical frames."""
+    from tools import synthscene as S
+    return S.bend_sphere(K, frames=FRAMES_TOTAL, amplitude=AMPLITUDE, frequency=FREQUENCY)
+
+
+def render_frames(K, indices, pinned=False):
+    from tools import synthscene as S
+    from paper_1603_08161_b200.abi import Frame
+    sc = scene(K)
+    out = []
+    for f in indices:
+        depth, color = S.render(sc, f)
+        if pinned:
+            from paper_1603_08161_b200.wfk import pinned_array
+            pd = pinned_array(depth.shape, np.float32)
+            pc = pinned_array(color.shape, np.float32)
+            pd[:] = depth
+            pc[:] = color
+            depth, color = pd, pc
+        out.append(Frame(K, depth, color))
+    return out
+
+
+REF_DESC = ("the reference itself: unmodified /root/reference/proj/src compiled with -O3 -fopenmp "
+            "-ffp-contract=off against the Eigen/doctest subset shims (oracle/_ref/libwfref.so)")
+DATA = ("synthetic (tools/synthscene: the reference's SyntheticScene restated and checked bit for bit against it; "
+        "host-rendered, identical frames in both arms)")
 
 
 def lattice_geometry():
@@ -215,31 +242,16 @@ class Dist:
 # B200 arm
 # ---------------------------------------------------------------------------
 def run_b200(args):
-    from paper_1603_08161_b200.abi import Frame, Intrinsics, Pose, SolverParams, Volume
-    from paper_1603_08161_b200.wfk import Context, SynthScene, pinned_array, pipeline_config
+    from paper_1603_08161_b200.abi import Intrinsics, Pose, SolverParams, Volume
+    from paper_1603_08161_b200.wfk import Context, pipeline_config
 
     d = Dist(args.gpus)
     ctx = Context(d.local)
     K = Intrinsics.make(FX, FY, CX, CY, W_PX, H_PX)
     n_frames = 1 + args.warmup + args.steps
 
-    # synthetic input sequence, rendered on the device, kept in pinned host memory
-    frames = []
-    for f in range(n_frames):
-        s = SynthScene()
-        s.center[:] = [0.0, 0.0, 1.2]
-        s.radius = 0.3
-        s.pivot[:] = [0.0, 0.0, 1.2]
-        s.amplitude = frame_amplitude(f)
-        s.driver_axis, s.rot_axis = 0, 1
-        s.t_min, s.t_max = 0.05, 6.0
-        s.texture_seed, s.texture_scale, s.dot_radius = 7, 0.06, 0.3
-        depth, color = ctx.synth_render(s, K)
-        pd = pinned_array((H_PX, W_PX), np.float32)
-        pc = pinned_array((H_PX, W_PX, 3), np.float32)
-        pd[:] = depth
-        pc[:] = color
-        frames.append(Frame(K, pd, pc))
+    # synthetic input sequence, rendered on the host, kept in pinned host memory
+    frames = render_frames(K, range(n_frames), pinned=True)
     log(f"rendered {n_frames} frames; valid depth px of frame 1: {int((frames[min(1, n_frames - 1)].depth > 0).sum())}")
 
     dims, voxel, origin = lattice_geometry()
@@ -335,7 +347,7 @@ def run_b200(args):
             "scaling": "weak",
             "vs_baseline": None,
             "dtype": "f64",
-            "data": "synthetic (device-rendered deforming sphere sequence)",
+            "data": DATA,
             "config": workload_config(d.world),
             "pcg_iters_per_s": pcg_iters_all / (d.max(total_ms) * 1e-3),
             "pcg_iterations_per_frame": pcg_iters / k,
@@ -386,8 +398,8 @@ def run_partitioned(args):
     from the same checkpoint.  One step = one coarse-to-fine solve; `value` =
     ms per solve (max over ranks, CUDA events on the context stream);
     "scaling": "strong" (the lattice is fixed as N grows)."""
-    from paper_1603_08161_b200.abi import CorrespondParams, Frame, Intrinsics, Pose, SolverParams, Volume
-    from paper_1603_08161_b200.wfk import Context, SynthScene, dist_unique_id, pipeline_config
+    from paper_1603_08161_b200.abi import CorrespondParams, Intrinsics, Pose, SolverParams, Volume
+    from paper_1603_08161_b200.wfk import Context, dist_unique_id, pipeline_config
 
     d = Dist(args.gpus)
     ctx = Context(d.local)
@@ -400,18 +412,7 @@ def run_partitioned(args):
     else:
         ctx.dist_init(0, 1)
     K = Intrinsics.make(FX, FY, CX, CY, W_PX, H_PX)
-    frames = []
-    for f in range(2):
-        sc = SynthScene()
-        sc.center[:] = [0.0, 0.0, 1.2]
-        sc.radius = 0.3
-        sc.pivot[:] = [0.0, 0.0, 1.2]
-        sc.amplitude = frame_amplitude(f + 3)  # a visible bend between the two frames
-        sc.driver_axis, sc.rot_axis = 0, 1
-        sc.t_min, sc.t_max = 0.05, 6.0
-        sc.texture_seed, sc.texture_scale, sc.dot_radius = 7, 0.06, 0.3
-        depth, color = ctx.synth_render(sc, K)
-        frames.append(Frame(K, depth, color))
+    frames = render_frames(K, [3, 4])  # a visible bend between the two frames
     dims, voxel, origin = lattice_geometry()
     vol = Volume(dims, voxel, origin)
     ctx.upload_volume(vol)
@@ -459,7 +460,7 @@ def run_partitioned(args):
         print(json.dumps({
             "metric": METRIC, "value": ms, "unit": "ms/solve", "n_gpus": d.world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-rendered sphere, frames 0-1)",
+            "vs_baseline": None, "dtype": "f64", "data": DATA + ", frames 3-4",
             "config": {"workload": f"BASELINE configs[3]: {N_LATTICE}^3 lattice, frame-1 coarse-to-fine solve, "
                                    "every level's PCG slab-partitioned (z-slabs, NCCL halos + all-gathered dots)",
                        "lattice": [N_LATTICE] * 3, "rows_per_level": [int(a) for a in act],
@@ -487,6 +488,7 @@ def cpu_baseline_sample(frames, n_frames):
         rec.process_frame(frames[f])
         times.append((time.perf_counter() - t0) * 1e3)
     cores = int(O.lib().wfo_num_threads())
+    kind = "reference" if O.backend() == "ref" else "port"
     # also the 1-thread figure, on the next frame of the sequence
     serial = None
     if 1 + n_frames < len(frames):
@@ -496,9 +498,10 @@ def cpu_baseline_sample(frames, n_frames):
         serial = (time.perf_counter() - t0) * 1e3
         O.lib().wfo_set_num_threads(cores)
     return {"value": float(np.median(times)), "unit": "ms/frame", "cores": cores,
-            "kind": "port",
-            "sample": f"oracle Reconstructor, frames 1..{n_frames} of the same sequence after the bootstrap "
-                      f"frame (median of {n_frames}), OpenMP threads = {cores}",
+            "kind": kind,
+            "sample": (f"{REF_DESC if kind == 'reference' else 'oracle port (oracle/wf_oracle.cpp)'}: "
+                       f"Reconstructor::process_frame on frames 1..{n_frames} of the same sequence after the "
+                       f"bootstrap frame (median of {n_frames}), OpenMP threads = {cores}"),
             "serial_1thread_ms_per_frame": serial}
 
 
@@ -511,13 +514,10 @@ def run_reference(args):
     if rank != 0:
         return
     from oracle import pyoracle as O
-    from paper_1603_08161_b200.abi import Frame, Intrinsics, SolverParams
+    from paper_1603_08161_b200.abi import Intrinsics, SolverParams
     K = Intrinsics.make(FX, FY, CX, CY, W_PX, H_PX)
     n_frames = 1 + args.warmup + args.steps
-    frames = []
-    for f in range(n_frames):
-        depth, color = O.synth_render(K, amplitude=frame_amplitude(f))
-        frames.append(Frame(K, depth, color))
+    frames = render_frames(K, range(n_frames))
     dims, voxel, origin = lattice_geometry()
     rec = O.Reconstructor(dims, voxel, origin, solver=SolverParams.make(), reassociations=3)
     rec.process_frame(frames[0])
@@ -531,6 +531,8 @@ def run_reference(args):
     dt = time.perf_counter() - t0
     ms = dt * 1e3 / args.steps
     cores = int(O.lib().wfo_num_threads())
+    kind = "reference" if O.backend() == "ref" else "port"
+    what = REF_DESC if kind == "reference" else "oracle port of the reference path (oracle/wf_oracle.cpp)"
     out = {
         "impl": "reference",
         "metric": METRIC,
@@ -544,12 +546,12 @@ def run_reference(args):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (CPU-rendered deforming sphere sequence)",
+        "data": DATA,
         "config": workload_config(1),
         "pcg_iters_per_s": pcg / dt,
-        "cpu_baseline": {"value": ms, "unit": "ms/frame", "cores": cores, "kind": "port",
-                         "sample": f"oracle port of the reference path (oracle/wf_oracle.cpp, OpenMP {cores} "
-                                   f"threads), {args.steps} full frames after bootstrap + {args.warmup} warm-up"},
+        "cpu_baseline": {"value": ms, "unit": "ms/frame", "cores": cores, "kind": kind,
+                         "sample": f"{what}, OpenMP {cores} threads, wf::Reconstructor::process_frame on "
+                                   f"{args.steps} full frames after bootstrap + {args.warmup} warm-up"},
         "e2e": {"value": ms, "unit": "ms/frame", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)

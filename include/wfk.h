@@ -322,25 +322,6 @@ int wfk_flush_l2(wfk_ctx* ctx);
 int wfk_host_alloc(size_t bytes, void** out);
 void wfk_host_free(void* p);
 
-/* ---- synthetic test-bed (NOT the hot path) --------------------------------------
- * Sphere-traced depth + color of a sphere under the reference's bend warp
- * (synthcam.cpp:141-159, 252-316), rendered on the device for benchmarks. */
-typedef struct wfk_synth_scene {
-  double center[3];
-  double radius;
-  double pivot[3];
-  double amplitude;      /* rad/m, already multiplied by the warp phase */
-  int32_t driver_axis;
-  int32_t rot_axis;
-  double t_min, t_max;
-  uint32_t texture_seed;
-  int32_t reserved_;
-  double texture_scale;
-  double dot_radius;
-} wfk_synth_scene;
-int wfk_synth_render(wfk_ctx* ctx, const wfk_synth_scene* s, const wfk_intrinsics* intr,
-                     float* depth_out, float* color_out);
-
 #ifdef __cplusplus
 }
 #endif

@@ -236,19 +236,20 @@ class NormalEquations:
         _check(lib().wfo_build_normal_equations(C.byref(vv), C.byref(pose), _cptr(c), C.c_int64(n),
                                                 C.byref(params), C.byref(h)))
         self.h = h
-        nr = lib().wfo_ne_num_rows(h)
+        self._l = lib()  # handles belong to the backend that made them
+        nr = self._l.wfo_ne_num_rows(h)
         self.rows = np.zeros(nr, np.int32)
         self.node_row = np.zeros(vol.num_points, np.int32)
         self.blocks = np.zeros((nr, 27, 3, 3))
         self.cols = np.zeros((nr, 27), np.int32)
         self.rhs = np.zeros((nr, 3))
         self.frozen = np.zeros(nr, np.uint8)
-        lib().wfo_ne_export(h, *(_cptr(a) for a in (self.rows, self.node_row, self.blocks, self.cols,
+        self._l.wfo_ne_export(h, *(_cptr(a) for a in (self.rows, self.node_row, self.blocks, self.cols,
                                                      self.rhs, self.frozen)))
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().wfo_ne_free(self.h)
+            self._l.wfo_ne_free(self.h)
             self.h = None
 
     @property
@@ -258,16 +259,16 @@ class NormalEquations:
     def multiply(self, x, exec_=EXEC_PARALLEL):
         x = np.ascontiguousarray(x, np.float64)
         y = np.zeros_like(x)
-        lib().wfo_ne_multiply(self.h, ptr(x, C.c_double), ptr(y, C.c_double), exec_)
+        self._l.wfo_ne_multiply(self.h, ptr(x, C.c_double), ptr(y, C.c_double), exec_)
         return y
 
     def symmetry_error(self):
-        return lib().wfo_ne_symmetry_error(self.h)
+        return self._l.wfo_ne_symmetry_error(self.h)
 
     def pcg_solve(self, x, tol, max_iters, exec_=EXEC_PARALLEL):
         x = np.ascontiguousarray(x, np.float64)
         res = PcgResult()
-        _check(lib().wfo_ne_pcg_solve(self.h, ptr(x, C.c_double), float(tol), int(max_iters), exec_,
+        _check(self._l.wfo_ne_pcg_solve(self.h, ptr(x, C.c_double), float(tol), int(max_iters), exec_,
                                       C.byref(res)))
         return x, res.iterations, res.relative_residual
 
@@ -506,11 +507,12 @@ class Mesh:
 
     def __init__(self, handle):
         self.h = handle
+        self._l = lib()  # handles belong to the backend that made them
         self.refresh()
 
     def refresh(self):
         nv, nt = C.c_int64(), C.c_int64()
-        lib().wfo_mesh_sizes(self.h, C.byref(nv), C.byref(nt))
+        self._l.wfo_mesh_sizes(self.h, C.byref(nv), C.byref(nt))
         V, T = nv.value, nt.value
         self.vertices_canonical = np.zeros((V, 3))
         self.vertices_deformed = np.zeros((V, 3))
@@ -520,26 +522,26 @@ class Mesh:
         mv = MeshView(V, T, ptr(self.vertices_canonical, C.c_double), ptr(self.vertices_deformed, C.c_double),
                       ptr(self.normals_deformed, C.c_double), ptr(self.colors, C.c_float),
                       ptr(self.triangles, C.c_int32))
-        lib().wfo_mesh_export(self.h, C.byref(mv))
+        self._l.wfo_mesh_export(self.h, C.byref(mv))
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().wfo_mesh_free(self.h)
+            self._l.wfo_mesh_free(self.h)
             self.h = None
 
     def compute_normals(self):
-        lib().wfo_compute_normals(self.h)
+        self._l.wfo_compute_normals(self.h)
         self.refresh()
 
     def warp(self, vol, pose):
         vv = vol.view()
-        _check(lib().wfo_mesh_warp(self.h, C.byref(vv), C.byref(pose)))
+        _check(self._l.wfo_mesh_warp(self.h, C.byref(vv), C.byref(pose)))
         self.refresh()
 
     def rasterize(self, intr, exec_=EXEC_PARALLEL) -> GeometryBuffer:
         b = GeometryBuffer(intr.width, intr.height)
         bv = b.view()
-        _check(lib().wfo_rasterize(self.h, C.byref(intr), exec_, C.byref(bv)))
+        _check(self._l.wfo_rasterize(self.h, C.byref(intr), exec_, C.byref(bv)))
         return b
 
 
@@ -602,17 +604,18 @@ class Reconstructor:
         cfg.features = features or FeatureParams.make()
         self.cfg = cfg
         h = C.c_void_p()
-        _check(lib().wfo_recon_create(C.byref(cfg), C.byref(h)))
+        self._l = lib()  # handles belong to the backend that made them
+        _check(self._l.wfo_recon_create(C.byref(cfg), C.byref(h)))
         self.h = h
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().wfo_recon_free(self.h)
+            self._l.wfo_recon_free(self.h)
             self.h = None
 
     def volume_view(self) -> VolumeView:
         v = VolumeView()
-        lib().wfo_recon_volume(self.h, C.byref(v))
+        self._l.wfo_recon_volume(self.h, C.byref(v))
         return v
 
     def volume_arrays(self) -> dict:
@@ -627,16 +630,16 @@ class Reconstructor:
 
     def feature_store(self):
         n = C.c_int64()
-        _check(lib().wfo_recon_feature_store(self.h, None, C.c_int64(0), C.byref(n)))
+        _check(self._l.wfo_recon_feature_store(self.h, None, C.c_int64(0), C.byref(n)))
         out = np.zeros(max(n.value, 1), FEATURE_DTYPE)
-        _check(lib().wfo_recon_feature_store(self.h, _cptr(out), C.c_int64(len(out)), C.byref(n)))
+        _check(self._l.wfo_recon_feature_store(self.h, _cptr(out), C.c_int64(len(out)), C.byref(n)))
         return out[: n.value].copy()
 
     def process_frame(self, frame, sparse=None) -> FrameRecord:
         rec = FrameRecord()
         s, n = _cons(sparse)
         fv = frame.view()
-        _check(lib().wfo_recon_process_frame(self.h, C.byref(fv), _cptr(s), C.c_int64(n), C.byref(rec)))
+        _check(self._l.wfo_recon_process_frame(self.h, C.byref(fv), _cptr(s), C.c_int64(n), C.byref(rec)))
         return rec
 
 

@@ -23,6 +23,7 @@
 #include <unistd.h>
 #include <vector>
 
+#include "../../tools/synthscene.h"
 #include "../wfo.h"
 #include "wf/correspond.hpp"
 #include "wf/features.hpp"
@@ -932,6 +933,58 @@ int wfo_synth_render(const double center[3], double radius, const double pivot[3
     const SyntheticScene scene(s);
     const Frame f = scene.render_frame(1);
     const size_t n = size_t(K->width) * size_t(K->height);
+    std::memcpy(depth, f.depth.data.data(), n * sizeof(float));
+    for (size_t i = 0; i < n; ++i)
+      for (int k = 0; k < 3; ++k) color[3 * i + size_t(k)] = f.color.data[i][k];
+    return WFK_OK;
+  });
+}
+
+// the reference's SyntheticScene for a tools/synthscene.h scene description
+// (checks tools/synthscene.cpp bit for bit, tests/test_synthscene.py)
+static Vec3 sv(const double* p) { return Vec3(p[0], p[1], p[2]); }
+int wfo_ref_render_scene(const ss_scene* q, int32_t frame, float* depth, float* color) {
+  return guarded([&]() -> int {
+    SceneSpec s;
+    s.frames = q->frames;
+    s.intrinsics = Intrinsics{q->fx, q->fy, q->cx, q->cy, q->width, q->height};
+    s.shapes.clear();
+    for (int i = 0; i < q->num_shapes; ++i) {
+      const ss_shape& a = q->shapes[i];
+      ShapeSpec b;
+      b.type = ShapeType(a.type);
+      b.center = sv(a.center);
+      b.radius = a.radius;
+      b.half_extents = sv(a.half_extents);
+      b.normal = sv(a.normal);
+      b.offset = a.offset;
+      b.axis = sv(a.axis);
+      b.half_height = a.half_height;
+      s.shapes.push_back(b);
+    }
+    s.texture.type = TextureType(q->tex_type);
+    s.texture.seed = q->tex_seed;
+    s.texture.scale = q->tex_scale;
+    s.texture.dot_radius = q->dot_radius;
+    s.warp.type = WarpType(q->warp_type);
+    s.warp.driver_axis = q->driver_axis;
+    s.warp.rot_axis = q->rot_axis;
+    s.warp.amplitude = q->amplitude;
+    s.warp.frequency = q->frequency;
+    s.warp.pivot = sv(q->pivot);
+    s.warp.rotation_axis = sv(q->rotation_axis);
+    s.warp.deg_per_frame = q->deg_per_frame;
+    s.warp.trans_per_frame = sv(q->trans_per_frame);
+    s.camera.rot_axis = sv(q->cam_rot_axis);
+    s.camera.deg_per_frame = q->cam_deg_per_frame;
+    s.camera.trans_per_frame = sv(q->cam_trans_per_frame);
+    s.t_min = q->t_min;
+    s.t_max = q->t_max;
+    s.noise_sigma = q->noise_sigma;
+    s.noise_seed = q->noise_seed;
+    const SyntheticScene scene(s);
+    const Frame f = scene.render_frame(frame);
+    const size_t n = size_t(q->width) * size_t(q->height);
     std::memcpy(depth, f.depth.data.data(), n * sizeof(float));
     for (size_t i = 0; i < n; ++i)
       for (int k = 0; k < 3; ++k) color[3 * i + size_t(k)] = f.color.data[i][k];

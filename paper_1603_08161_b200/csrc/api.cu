@@ -848,13 +848,6 @@ int wfk_estimate_global_pose(wfk_ctx* c, const wfk_intrinsics* intr, const wfk_p
   });
 }
 
-int wfk_synth_render(wfk_ctx* c, const wfk_synth_scene* s, const wfk_intrinsics* intr, float* depth, float* color) {
-  return guard(c, [&] {
-    if (!s || !intr || !depth) throw Error(WFK_E_INVALID_ARG, "null argument");
-    synth_render(c, *s, *intr, depth, color);
-  });
-}
-
 }  // extern "C"
 
 extern "C" {

@@ -1092,157 +1092,4 @@ void assoc_estimate_pose(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose& in
   out->iterations = hst->iterations;
 }
 
-// ---------------------------------------------------------------------------
-// synthetic test-bed renderer (synthcam.cpp:141-159, 252-316), sphere + bend
-// ---------------------------------------------------------------------------
-struct SynthArgs {
-  wfk_synth_scene s;
-  wfk_intrinsics K;
-  float* depth;
-  float* color;
-};
-
-WF_D M3 axis_angle_unit(int axis, double ang) {
-  M3 r = m3_identity();
-  const double c = cos(ang), s = sin(ang);
-  if (axis == 0) {
-    r.a[1][1] = c; r.a[1][2] = -s; r.a[2][1] = s; r.a[2][2] = c;
-  } else if (axis == 1) {
-    r.a[0][0] = c; r.a[0][2] = s; r.a[2][0] = -s; r.a[2][2] = c;
-  } else {
-    r.a[0][0] = c; r.a[0][1] = -s; r.a[1][0] = s; r.a[1][1] = c;
-  }
-  return r;
-}
-
-WF_D V3 synth_inverse_warp(const wfk_synth_scene& s, V3 world) {
-  const double a = s.amplitude;
-  const V3 pv{s.pivot[0], s.pivot[1], s.pivot[2]};
-  const V3 p = world - pv;
-  if (a == 0) return world;
-  const int d = s.driver_axis, e = s.rot_axis;
-  auto g = [&](double t) { return comp(mul(transpose(axis_angle_unit(e, a * t)), p), d) - t; };
-  double t = comp(p, d);
-  bool ok = false;
-  for (int it = 0; it < 50; ++it) {
-    const double gs = g(t);
-    if (fabs(gs) < 1e-12) {
-      ok = true;
-      break;
-    }
-    const double h = 1e-7;
-    const double dg = (g(t + h) - g(t - h)) / (2 * h);
-    if (fabs(dg) < 1e-12) break;
-    t -= gs / dg;
-  }
-  if (!ok && fabs(g(t)) > 1e-10) {
-    double lo = -(norm3(p) + 1), hi = norm3(p) + 1;
-    for (int it = 0; it < 200; ++it) {
-      const double mid = 0.5 * (lo + hi);
-      if (g(lo) * g(mid) <= 0)
-        hi = mid;
-      else
-        lo = mid;
-    }
-    t = 0.5 * (lo + hi);
-  }
-  return pv + mul(axis_angle_unit(e, -a * t), p);
-}
-
-WF_D uint64_t splitmix64(uint64_t x) {
-  x += 0x9e3779b97f4a7c15ull;
-  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
-  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
-  return x ^ (x >> 31);
-}
-WF_D uint64_t hash_cell(int64_t x, int64_t y, int64_t z, uint32_t seed) {
-  uint64_t h = seed;
-  h = splitmix64(h ^ uint64_t(x));
-  h = splitmix64(h ^ uint64_t(y));
-  h = splitmix64(h ^ uint64_t(z));
-  return h;
-}
-WF_D double rand01(uint64_t h) { return double(h >> 11) * (1.0 / 9007199254740992.0); }
-
-// Dots texture (synthcam.cpp:98-112)
-WF_D void dots_color(const wfk_synth_scene& s, V3 can, float out[3]) {
-  const V3 cell = can / s.texture_scale;
-  const V3 f{floor(cell.x), floor(cell.y), floor(cell.z)};
-  const uint64_t h = hash_cell(int64_t(f.x), int64_t(f.y), int64_t(f.z), s.texture_seed);
-  const double margin = s.dot_radius + 0.05;
-  const V3 jit{margin + rand01(h) * (1 - 2 * margin), margin + rand01(splitmix64(h)) * (1 - 2 * margin),
-               margin + rand01(splitmix64(splitmix64(h))) * (1 - 2 * margin)};
-  const V3 center = f + jit;
-  if (norm3(cell - center) < s.dot_radius) {
-    const uint64_t hc = splitmix64(h ^ 0xd0d5u);
-    out[0] = 20 + 160 * float(rand01(hc));
-    out[1] = 20 + 160 * float(rand01(splitmix64(hc)));
-    out[2] = 20 + 160 * float(rand01(splitmix64(splitmix64(hc))));
-    return;
-  }
-  out[0] = out[1] = out[2] = 210.f;
-}
-
-__global__ void k_synth(SynthArgs a) {
-  const int W = a.K.width, H = a.K.height;
-  const int64_t npx = int64_t(W) * H;
-  const V3 center{a.s.center[0], a.s.center[1], a.s.center[2]};
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npx; i += int64_t(gridDim.x) * blockDim.x) {
-    const int x = int(i % W), y = int(i / W);
-    const V3 ray{(double(x) - a.K.cx) / a.K.fx, (double(y) - a.K.cy) / a.K.fy, 1.0};
-    const V3 dir = ray / norm3(ray);
-    auto field = [&](double t) { return norm3(synth_inverse_warp(a.s, t * dir) - center) - a.s.radius; };
-    double t = a.s.t_min;
-    double f = field(t);
-    a.depth[i] = 0.f;
-    a.color[3 * i] = a.color[3 * i + 1] = a.color[3 * i + 2] = 0.f;
-    if (f <= 0) continue;
-    double hit = -1;
-    for (int it = 0; it < 2000 && t < a.s.t_max; ++it) {
-      const double step = clampd(0.7 * f, 5e-5, 0.25);
-      const double tn = t + step;
-      const double fn = field(tn);
-      if (fn <= 1e-7) {
-        if (fn < 0) {
-          double lo = t, hi = tn;
-          for (int b = 0; b < 60; ++b) {
-            const double mid = 0.5 * (lo + hi);
-            if (field(mid) > 0)
-              lo = mid;
-            else
-              hi = mid;
-          }
-          hit = 0.5 * (lo + hi);
-        } else {
-          hit = tn;
-        }
-        break;
-      }
-      t = tn;
-      f = fn;
-    }
-    if (hit < 0) continue;
-    const V3 pc = hit * dir;
-    a.depth[i] = float(pc.z);
-    float col[3];
-    dots_color(a.s, synth_inverse_warp(a.s, pc), col);
-    a.color[3 * i] = col[0];
-    a.color[3 * i + 1] = col[1];
-    a.color[3 * i + 2] = col[2];
-  }
-}
-
-void synth_render(wfk_ctx* c, const wfk_synth_scene& s, const wfk_intrinsics& K, float* depth, float* color) {
-  const int64_t npx = int64_t(K.width) * K.height;
-  DevBuf<float> d, col;
-  d.ensure(size_t(npx));
-  col.ensure(3 * size_t(npx));
-  SynthArgs a{s, K, d, col};
-  k_synth<<<grid_for(npx, 128), 128, 0, c->stream>>>(a);
-  WFK_CUDA(cudaGetLastError());
-  WFK_CUDA(cudaMemcpyAsync(depth, d.p, size_t(npx) * 4, cudaMemcpyDeviceToHost, c->stream));
-  if (color) WFK_CUDA(cudaMemcpyAsync(color, col.p, 3 * size_t(npx) * 4, cudaMemcpyDeviceToHost, c->stream));
-  WFK_CUDA(cudaStreamSynchronize(c->stream));
-}
-
 }  // namespace wfk

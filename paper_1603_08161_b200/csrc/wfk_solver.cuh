@@ -75,6 +75,5 @@ void assoc_estimate_pose(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose& in
                          wfk_icp_result* out);
 void assoc_find_dense(wfk_ctx* c, const wfk_intrinsics& K, const wfk_correspond_params& p, bool drop_inactive,
                       int64_t* n_out);
-void synth_render(wfk_ctx* c, const wfk_synth_scene& s, const wfk_intrinsics& K, float* depth, float* color);
 
 }  // namespace wfk

@@ -57,13 +57,6 @@ class NeHost(C.Structure):
                 ("cols", C.c_void_p), ("rhs", C.c_void_p), ("frozen", C.c_void_p)]
 
 
-class SynthScene(C.Structure):
-    _fields_ = [("center", C.c_double * 3), ("radius", C.c_double), ("pivot", C.c_double * 3),
-                ("amplitude", C.c_double), ("driver_axis", C.c_int32), ("rot_axis", C.c_int32),
-                ("t_min", C.c_double), ("t_max", C.c_double), ("texture_seed", C.c_uint32),
-                ("reserved_", C.c_int32), ("texture_scale", C.c_double), ("dot_radius", C.c_double)]
-
-
 class Profile(C.Structure):
     _fields_ = [("flip_flop_launches", C.c_int64), ("pcg_iterations", C.c_int64), ("flip_flop_ms", C.c_double),
                 ("flip_flop_bytes", C.c_double), ("flip_flop_bytes_impl", C.c_double),
@@ -587,13 +580,6 @@ class Context:
 
     def flush_l2(self):
         self._check(lib().wfk_flush_l2(self.h))
-
-    def synth_render(self, scene: SynthScene, intr: Intrinsics):
-        depth = np.zeros((intr.height, intr.width), np.float32)
-        color = np.zeros((intr.height, intr.width, 3), np.float32)
-        self._check(lib().wfk_synth_render(self.h, C.byref(scene), C.byref(intr), _cptr(depth), _cptr(color)))
-        return depth, color
-
 
 def pipeline_config(solver=None, correspond=None, fusion=None, reassociations=3, estimate_pose=True,
                     icp=None, use_features=True, features=None) -> PipelineConfig:

@@ -44,7 +44,7 @@ STRUCTS = {
     "wfk_correspond_params": abi.CorrespondParams, "wfk_frame_view": abi.FrameView,
     "wfk_point_normal_map": abi.PointNormalMapView, "wfk_geometry_buffer": abi.GeometryBufferView,
     "wfk_mesh_view": abi.MeshView, "wfk_pipeline_config": wfk.PipelineConfig,
-    "wfk_frame_record": wfk.FrameRecord, "wfk_synth_scene": wfk.SynthScene, "wfk_config": wfk.Config,
+    "wfk_frame_record": wfk.FrameRecord, "wfk_config": wfk.Config,
     "wfk_icp_params": abi.IcpParams, "wfk_icp_result": abi.IcpResult, "wfk_feature_params": abi.FeatureParams,
     "wfk_ne_host": wfk.NeHost, "wfk_profile": wfk.Profile,
 }

@@ -136,17 +136,11 @@ def test_static_sequence_identity(ctx):  # acceptance criterion 3 (acceptance.cp
     """ten identical frames of a large face-on spherical cap: the deformation
     stays the identity, the TSDF matches the analytic projective TSDF and the
     canonical mesh lies on the sphere"""
-    from paper_1603_08161_b200.wfk import SynthScene, pipeline_config
+    from paper_1603_08161_b200.wfk import pipeline_config
+    from tools import synthscene as S
     center, radius = np.array([0.0, 0.0, 2.2]), 1.0
-    s = SynthScene()
-    s.center[:] = center
-    s.radius = radius
-    s.pivot[:] = center
-    s.amplitude = 0.0
-    s.driver_axis, s.rot_axis = 0, 1
-    s.t_min, s.t_max = 0.05, 6.0
-    s.texture_seed, s.texture_scale, s.dot_radius = 7, 0.06, 0.3
-    depth, color = ctx.synth_render(s, K)
+    s = S.Scene.make(K, frames=1).add_shape(S.SPHERE, center=tuple(center), radius=radius)  # acceptance.cpp:406-412
+    depth, color = S.render(s, 0)
     fr = Frame(K, depth, color)
     n, voxel, origin = 64, 0.01, (-0.315, -0.315, 1.05)
     vol = Volume((n, n, n), voxel, origin)

@@ -275,24 +275,6 @@ def test_dense_association_plane_kat(ctx):  # test_correspond.cpp:78-107
     assert np.max(np.linalg.norm(c["target"] - c["canonical"], axis=1)) < 1e-6
 
 
-def test_synth_render_matches_analytic_sphere(ctx):
-    from paper_1603_08161_b200.wfk import SynthScene
-    K = Intrinsics.make(280, 280, 159.5, 119.5, 320, 240)
-    s = SynthScene()
-    s.center[:] = [0.0, 0.0, 1.2]
-    s.radius = 0.3
-    s.pivot[:] = [0.0, 0.0, 1.2]
-    s.amplitude = 0.0
-    s.driver_axis, s.rot_axis = 0, 1
-    s.t_min, s.t_max = 0.05, 6.0
-    s.texture_seed, s.texture_scale, s.dot_radius = 7, 0.06, 0.3
-    depth, color = ctx.synth_render(s, K)
-    ref = sphere_frame(K, center=(0, 0, 1.2), radius=0.3, holes=False).depth
-    both = (depth > 0) & (ref > 0)
-    assert np.array_equal(depth > 0, ref > 0) or abs(int((depth > 0).sum()) - int((ref > 0).sum())) < 20
-    assert np.max(np.abs(depth[both] - ref[both])) < 1e-5
-
-
 def test_mesh_warp_bit_exact(ctx):
     """redeform (pipeline.cpp:167-172): mesh vertices re-warped through a new field and pose"""
     v = fused_sphere_volume()

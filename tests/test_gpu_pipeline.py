@@ -19,21 +19,13 @@ def ctx():
     c.close()
 
 
-def bend_frames(ctx, K, n_frames, amplitude, frames_total=10):
-    from paper_1603_08161_b200.wfk import SynthScene
-    out = []
-    for f in range(n_frames):
-        s = SynthScene()
-        s.center[:] = [0.0, 0.0, 1.2]
-        s.radius = 0.3
-        s.pivot[:] = [0.0, 0.0, 1.2]
-        s.amplitude = amplitude * (f / (frames_total - 1))  # linear ramp (synthcam.cpp:131-136)
-        s.driver_axis, s.rot_axis = 0, 1
-        s.t_min, s.t_max = 0.05, 6.0
-        s.texture_seed, s.texture_scale, s.dot_radius = 7, 0.06, 0.3
-        depth, color = ctx.synth_render(s, K)
-        out.append(Frame(K, depth, color))
-    return out
+def bend_frames(ctx, K, n_frames, amplitude, frames_total=10, frequency=0.0, start=0):
+    """frames of the bend-sphere sequence (linear ramp over frames_total when
+    frequency is 0, synthcam.cpp:138-143), rendered by tools/synthscene --
+    bit-identical to the reference's SyntheticScene -- and fed to both sides"""
+    from tools import synthscene as S
+    sc = S.bend_sphere(K, frames=frames_total, amplitude=amplitude, frequency=frequency)
+    return [Frame(K, *S.render(sc, f)) for f in range(start, start + n_frames)]
 
 
 @pytest.mark.parametrize("n,reassoc,levels,icp", [(32, 1, 1, True), (48, 2, 3, True), (48, 2, 3, False)])
