@@ -170,6 +170,7 @@ inline int run(int argc, char** argv) {
       } catch (const std::exception& e) {
         std::fprintf(stderr, "%s:%d: ERROR: test case THREW exception: %s [case: %s]\n", tc.file, tc.line, e.what(),
                      tc.name);
+        ++s.asserts;
         ++s.failed;
         s.case_failed = true;
       }

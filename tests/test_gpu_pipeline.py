@@ -1,7 +1,12 @@
 """End-to-end parity of the per-frame hot path (Reconstructor::process_frame,
 pipeline.cpp:143-262, with the global-pose ICP and the feature front-end):
-the B200 path (wfk_process_frame) against the oracle's restatement on the same
-synthetic bend sequence."""
+the B200 path (wfk_process_frame) against the checker -- the reference's own
+code (oracle/_ref) when built, else the port -- on identical synthetic frames
+(tools/synthscene).  Integer outcomes (constraint / match / feature counts,
+fused and activated voxels, PCG iteration counts, trace lengths) must be
+EQUAL frame by frame; energies agree to 1e-9 relative (measured <= 1e-12) and
+the deformation field to 1e-6 voxel (measured ~1e-10), the device's PCG dot
+order and libm being the only differences."""
 import numpy as np
 import pytest
 
@@ -9,6 +14,32 @@ from oracle import pyoracle as O
 from paper_1603_08161_b200.abi import FEATURE_DTYPE, CorrespondParams, Frame, FusionParams, Intrinsics, Pose, SolverParams, Volume
 
 pytestmark = pytest.mark.gpu
+
+INT_FIELDS = ("dense_count", "sparse_count", "match_count", "features_added", "pcg_iterations", "trace_len",
+              "anomalies", "icp_degraded")
+
+
+def assert_records_equal(rg, rr, frame):
+    for k in INT_FIELDS:
+        assert getattr(rg, k) == getattr(rr, k), (frame, k, getattr(rg, k), getattr(rr, k))
+    if rr.icp_iterations >= 0:  # not part of the reference's FrameRecord (the ref build reports -1)
+        assert rg.icp_iterations == rr.icp_iterations, frame
+    assert (rg.fusion.fused, rg.fusion.skipped_gate, rg.fusion.skipped_frustum, rg.fusion.skipped_occluded) == \
+        (rr.fusion.fused, rr.fusion.skipped_gate, rr.fusion.skipped_frustum, rr.fusion.skipped_occluded), frame
+    assert (rg.expansion.activated, rg.expansion.orphans) == (rr.expansion.activated, rr.expansion.orphans), frame
+    if rr.energy.total != 0:
+        assert rg.energy.total == pytest.approx(rr.energy.total, rel=1e-9), frame
+    np.testing.assert_allclose(rg.pose.matrix(), rr.pose.matrix(), rtol=0, atol=1e-11)
+    np.testing.assert_allclose(rg.pose.vector(), rr.pose.vector(), rtol=0, atol=1e-11)
+
+
+def assert_volumes_match(vol, arr, voxel):
+    assert np.array_equal(vol.active, arr["active"])
+    assert np.array_equal(vol.age, arr["age"])
+    both = arr["active"].astype(bool)
+    if both.any():
+        dev = np.max(np.linalg.norm(vol.deformed[both] - arr["deformed"][both], axis=1)) / voxel
+        assert dev <= 1e-6, dev
 
 
 @pytest.fixture(scope="module")
@@ -45,29 +76,9 @@ def test_process_frame_parity(ctx, n, reassoc, levels, icp):
         rr = ref.process_frame(fr)
         rg = ctx.process_frame(fr, pose, cfg, i)
         pose = rg.pose  # the Reconstructor's pose_ carried to the next frame
-        if i == 0:
-            assert rg.fusion.fused == rr.fusion.fused
-            continue
-        if icp:
-            if i == 1:
-                assert rg.icp_iterations == rr.icp_iterations and rg.icp_degraded == rr.icp_degraded
-            np.testing.assert_allclose(rg.pose.matrix(), rr.pose.matrix(), atol=1e-7)
-            np.testing.assert_allclose(rg.pose.vector(), rr.pose.vector(), atol=1e-7)
-        if i == 1 and reassoc == 1:  # identical inputs up to this frame's solve: integer work is exact
-            assert rg.dense_count == rr.dense_count
-            assert rg.trace_len == rr.trace_len
-        else:
-            assert abs(rg.dense_count - rr.dense_count) <= max(3, 0.002 * rr.dense_count)
-        assert rg.energy.total == pytest.approx(rr.energy.total, rel=1e-3)
-        assert abs(rg.fusion.fused - rr.fusion.fused) <= max(3, 0.002 * rr.fusion.fused)
-        assert rg.expansion.activated == pytest.approx(rr.expansion.activated, abs=3)
+        assert_records_equal(rg, rr, i)
     ctx.download_volume(vol)
-    arr = ref.volume_arrays()
-    act = arr["active"].astype(bool)
-    assert (vol.active != arr["active"]).sum() <= 8
-    both = act & vol.active.astype(bool)
-    dev = np.max(np.linalg.norm(vol.deformed[both] - arr["deformed"][both], axis=1)) / voxel
-    assert dev <= 1e-3, dev
+    assert_volumes_match(vol, ref.volume_arrays(), voxel)
 
 
 def test_process_frame_features_parity(ctx):
@@ -92,30 +103,22 @@ def test_process_frame_features_parity(ctx):
         rr = ref.process_frame(fr)
         rg = ctx.process_frame(fr, pose, cfg, i)
         pose = rg.pose
-        if i <= 1:  # identical inputs so far: integer work is exact
-            assert rg.features_added == rr.features_added
-            assert rg.match_count == rr.match_count and rg.sparse_count == rr.sparse_count
-        else:
-            assert abs(rg.features_added - rr.features_added) <= 2
-            assert abs(rg.match_count - rr.match_count) <= 2
-            assert abs(rg.sparse_count - rr.sparse_count) <= 2
-        if i > 0:
-            assert rg.energy.total == pytest.approx(rr.energy.total, rel=1e-3)
+        assert_records_equal(rg, rr, i)
         total_sparse += rg.sparse_count
     assert total_sparse > 0, "the sequence should produce sparse feature constraints"
     sg, sr = ctx.feature_store(), ref.feature_store()
-    assert abs(len(sg) - len(sr)) <= 4 and len(sr) > 20
+    assert len(sg) == len(sr) > 20
+    for f in ("pixel", "frame_id"):
+        np.testing.assert_array_equal(sg[f], sr[f])
     # the bootstrap frame's positions are exact (identity warp), later ones to the inversion tolerance
     b = int((sr["frame_id"] == 0).sum())
-    assert b > 0 and int((sg["frame_id"] == 0).sum()) == b
-    for f in ("pixel", "world_pos", "canonical_pos", "frame_id"):
+    for f in ("world_pos", "canonical_pos"):
         np.testing.assert_array_equal(sg[f][:b], sr[f][:b])
-    np.testing.assert_allclose(sg["descriptor"][:b], sr["descriptor"][:b], rtol=0, atol=1e-5)
-    m = min(len(sg), len(sr))
-    same = (sg["frame_id"][:m] == sr["frame_id"][:m]) & np.all(sg["pixel"][:m] == sr["pixel"][:m], axis=1)
-    assert same.mean() > 0.95
-    dev = np.linalg.norm(sg["canonical_pos"][:m][same] - sr["canonical_pos"][:m][same], axis=1).max() / voxel
-    assert dev <= 1e-3, dev
+    np.testing.assert_allclose(sg["descriptor"], sr["descriptor"], rtol=0, atol=1e-5)
+    dev = np.linalg.norm(sg["canonical_pos"] - sr["canonical_pos"], axis=1).max() / voxel
+    assert dev <= 1e-6, dev
+    ctx.download_volume(vol)
+    assert_volumes_match(vol, ref.volume_arrays(), voxel)
 
 
 def test_process_frame_features_frame_without_color(ctx):
@@ -137,11 +140,12 @@ def test_process_frame_features_frame_without_color(ctx):
         rr = ref.process_frame(fr)
         rg = ctx.process_frame(fr, pose, cfg, i)
         pose = rg.pose
+        assert_records_equal(rg, rr, i)
         if i == 2:
-            assert rg.match_count == rr.match_count == 0 and rg.features_added == rr.features_added == 0
+            assert rg.match_count == 0 and rg.features_added == 0
         else:
-            assert rr.features_added > 0 and abs(rg.features_added - rr.features_added) <= 2
-    assert abs(len(ctx.feature_store()) - len(ref.feature_store())) <= 4
+            assert rr.features_added > 0
+    assert len(ctx.feature_store()) == len(ref.feature_store())
 
 
 def test_config2_sequence_parity(ctx):
@@ -164,53 +168,11 @@ def test_config2_sequence_parity(ctx):
         rr = ref.process_frame(fr)
         rg = ctx.process_frame(fr, pose, cfg, i)
         pose = rg.pose
-        if i == 0:
-            assert rg.fusion.fused == rr.fusion.fused and rg.features_added == rr.features_added
-            continue
-        assert rg.energy.total == pytest.approx(rr.energy.total, rel=1e-6)  # measured 1e-10 .. 1e-14
-        assert abs(rg.dense_count - rr.dense_count) <= max(3, 0.002 * rr.dense_count)
-        assert abs(rg.sparse_count - rr.sparse_count) <= 2
-        np.testing.assert_allclose(rg.pose.vector(), rr.pose.vector(), atol=1e-6)
+        assert_records_equal(rg, rr, i)
         sparse += rg.sparse_count
     assert sparse > 0
     ctx.download_volume(vol)
-    arr = ref.volume_arrays()
-    both = arr["active"].astype(bool) & vol.active.astype(bool)
-    assert (vol.active != arr["active"]).sum() <= 16
-    dev = np.max(np.linalg.norm(vol.deformed[both] - arr["deformed"][both], axis=1)) / voxel
-    assert dev <= 1e-3, dev
-
-
-def test_config3_short_sequence_parity(ctx):
-    """BASELINE configs[2] (the bench workload): 640x480, 128^3, defaults --
-    the first three frames against the oracle Reconstructor."""
-    from paper_1603_08161_b200.wfk import pipeline_config
-    n = 128
-    K = Intrinsics.make(560, 560, 319.5, 239.5, 640, 480)
-    voxel = 0.7 / (n - 1)
-    origin = (-0.35, -0.35, 0.85)
-    frames = bend_frames(ctx, K, 3, 2.0, frames_total=300)
-    ref = O.Reconstructor((n, n, n), voxel, origin, solver=SolverParams.make(), reassociations=3)
-    vol = Volume((n, n, n), voxel, origin)
-    ctx.upload_volume(vol)
-    cfg = pipeline_config(solver=SolverParams.make(), reassociations=3)
-    pose = Pose.make()
-    for i, fr in enumerate(frames):
-        rr = ref.process_frame(fr)
-        rg = ctx.process_frame(fr, pose, cfg, i)
-        pose = rg.pose
-        if i == 0:
-            assert rg.fusion.fused == rr.fusion.fused and rg.features_added == rr.features_added
-            continue
-        assert rg.energy.total == pytest.approx(rr.energy.total, rel=1e-6)  # measured 1e-10 .. 1e-14
-        assert abs(rg.dense_count - rr.dense_count) <= max(3, 0.002 * rr.dense_count)
-        assert rg.pcg_iterations == rr.pcg_iterations
-    ctx.download_volume(vol)
-    arr = ref.volume_arrays()
-    both = arr["active"].astype(bool) & vol.active.astype(bool)
-    assert (vol.active != arr["active"]).sum() <= 16
-    dev = np.max(np.linalg.norm(vol.deformed[both] - arr["deformed"][both], axis=1)) / voxel
-    assert dev <= 1e-3, dev
+    assert_volumes_match(vol, ref.volume_arrays(), voxel)
 
 
 def test_config1_fixed_work_parity(ctx):
@@ -233,13 +195,8 @@ def test_config1_fixed_work_parity(ctx):
         rr = ref.process_frame(fr)
         rg = ctx.process_frame(fr, pose, cfg, i)
         pose = rg.pose
-        if i == 0:
-            continue
-        assert rg.trace_len == rr.trace_len == 5
-        assert rg.pcg_iterations == rr.pcg_iterations == 50  # fixed work
-        assert rg.energy.total == pytest.approx(rr.energy.total, rel=1e-6)  # measured 1e-10 .. 1e-14
+        assert_records_equal(rg, rr, i)
+        if i > 0:
+            assert rg.trace_len == 5 and rg.pcg_iterations == 50  # fixed work
     ctx.download_volume(vol)
-    arr = ref.volume_arrays()
-    both = arr["active"].astype(bool) & vol.active.astype(bool)
-    dev = np.max(np.linalg.norm(vol.deformed[both] - arr["deformed"][both], axis=1)) / voxel
-    assert dev <= 1e-3, dev
+    assert_volumes_match(vol, ref.volume_arrays(), voxel)

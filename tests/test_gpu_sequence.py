@@ -7,15 +7,15 @@ timed frames) run through libwfk (wfk_process_frame) and through the checker
 (the reference's own code, oracle/_ref, when built) on IDENTICAL frames
 (tools/synthscene, bit-identical to the reference's renderer).
 
-Bars (north star): per-frame energy within 1e-4 relative, the deformation
-field within 1e-3 voxel at the end.  Integer counts are tracked frame by frame
-and written to gpurun_out/sequence_parity.json.  Why they can drift at all:
-every kernel's integer work is bit-exact on identical inputs (kernel tests),
-but the device PCG sums its dot products in a different (fixed) order than the
-reference's serial loop and the device's cos/sin/atan2 differ from glibc's in
-the last ulp, so the deformation field differs at the 1e-12 level; a pixel
-whose raster coverage or association test sits within that distance of its
-threshold can flip in a later frame."""
+Integer outcomes are compared frame by frame and written to
+gpurun_out/sequence_parity.json.  Every kernel's integer work is bit-exact on
+identical inputs (kernel tests); the device PCG sums its dot products in a
+different (fixed) order than the reference's serial loop and the device's
+cos/sin/atan2 can differ from glibc's in the last ulp, so the deformation
+field differs at the 1e-12 level.  A pixel whose raster or association test
+sat within that distance of its threshold would flip an integer count in a
+later frame; over these 30 frames none does (measured), and the test holds
+the path to that."""
 import json
 import os
 
@@ -89,9 +89,11 @@ def test_config3_thirty_frames(ctx):
     with open(os.path.join(ROOT, "gpurun_out", "sequence_parity.json"), "w") as fh:
         json.dump(summary, fh, indent=1)
     print(json.dumps({k: v for k, v in summary.items() if k != "per_frame"}))
-    assert worst_e <= 1e-4, worst_e
-    assert dev <= 1e-3, dev
-    # integer drift stays a handful of threshold-straddling pixels / voxels
-    assert summary["max_dense_count_diff"] <= max(8, 0.002 * 66000)
-    assert summary["max_fused_diff"] <= 0.002 * max(r["fused"][1] for r in rows)
-    assert active_diff <= 0.001 * int(arr["active"].sum()) + 8
+    # north-star bars: energy 1e-4 relative, deformation 1e-3 voxel; measured
+    # (profiles/r02_sequence_parity_30f.json): 3e-13 and 1e-10, every integer
+    # outcome equal on every frame -- asserted as such
+    assert worst_e <= 1e-9, worst_e
+    assert dev <= 1e-6, dev
+    assert active_diff == 0
+    mismatched = [(r["frame"], k) for r in rows for k, v in r.items() if isinstance(v, list) and v[0] != v[1]]
+    assert not mismatched, mismatched
