@@ -1,7 +1,13 @@
 /* Plain-old-data types crossing the C ABI of the B200 non-rigid solver
  * (libwfk.so, include/wfk.h).  Every struct is the C image of one type of the
- * reference's wf:: interface; field order follows the reference so that a C++
- * adapter can pass std::vector storage straight through.
+ * reference's wf:: interface.  Layout-compatible with the reference (storage
+ * may cross without conversion; pinned by static_asserts in
+ * integration/wf_b200_adapter.cpp): wfk_correspondence == wf::Correspondence,
+ * and the volume / point-map / geometry-buffer / mesh arrays are the
+ * reference's std::vector<Vec3/Vec3f/Vec3i/float/uint8_t> storage.  The other
+ * structs (wfk_fusion_params, wfk_trace_entry, wfk_solver_params, ...) carry
+ * the same fields in a C-friendly order and are converted field by field by
+ * the adapter.
  *
  * No torch / CUDA / Eigen types appear here: plain pointers, sizes and
  * fixed-width integers only. */

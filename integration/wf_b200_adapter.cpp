@@ -20,6 +20,7 @@
 // each one uploads what it reads and downloads what it writes; the resident,
 // per-frame fast path is wfk_process_frame (bench.py's e2e number).
 #include <cstddef>
+#include <cstdio>
 #include <cstring>
 #include <optional>
 #include <stdexcept>
@@ -56,6 +57,8 @@ wfk_ctx* ctx() {  // one context per thread (the reference calls from its main t
     wfk_ctx* h = nullptr;
     wfk_config cfg{};
     if (wfk_create(&cfg, &h) != WFK_OK) throw std::runtime_error("libwfk: no B200 available");
+    // one line per process so a log shows the hot path ran through libwfk
+    std::fprintf(stderr, "[wf_b200] libwfk context created (device %d): wf:: hot path on the GPU\n", cfg.device);
     return h;
   }();
   return c;

@@ -634,7 +634,8 @@ int wfk_find_dense_correspondences(wfk_ctx* c, const wfk_intrinsics* intr, const
   });
 }
 
-// Reconstructor::process_frame (pipeline.cpp:143-262) without ICP/features
+// Reconstructor::process_frame (pipeline.cpp:143-262): global-pose ICP, feature front-end, association,
+// coarse-to-fine solve, fusion and expansion
 int wfk_process_frame(wfk_ctx* c, const wfk_frame_view* frame, const wfk_pose* pose, const wfk_pipeline_config* cfg,
                       const wfk_correspondence* sparse, int64_t nsparse, int32_t frame_index, wfk_frame_record* rec) {
   const int rc0 = wfk_frame_upload(c, frame);

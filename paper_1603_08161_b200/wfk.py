@@ -1,8 +1,9 @@
 """ctypes front end of libwfk.so (include/wfk.h) -- the B200 path.
 
 ``Context`` owns one device (its CUDA stream, the device-resident lattice and
-work buffers).  Its methods are one-to-one with the C ABI; ``paper_1603_08161_b200.wf``
-layers the reference's stateless ``wf::`` functions on top.
+work buffers).  Its methods are one-to-one with the C ABI; the reference's
+stateless ``wf::`` functions are layered on top in C++ by
+integration/wf_b200_adapter.cpp.
 
 There is no CPU fallback: if libwfk.so is missing or no B200 is visible the
 constructor raises.
