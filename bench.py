@@ -474,6 +474,109 @@ def run_partitioned(args):
     d.close()
 
 
+# ---------------------------------------------------------------------------
+# BASELINE configs[3] / configs[4] on one GPU: the frame-1 solve, repeated
+# ---------------------------------------------------------------------------
+SOLVE_CONFIGS = {
+    # 256^3 sphere, 640x480, frame-1 solve (bend), levels 3
+    3: dict(n=256, K=(560.0, 560.0, 319.5, 239.5, 640, 480), voxel=0.7 / 255, origin=(-0.35, -0.35, 0.85),
+            scene="sphere", desc="BASELINE configs[3]: 256^3 lattice, 640x480, bend sphere, frame-1 coarse-to-fine "
+                                 "solve (3 levels) on one GPU"),
+    # 512^3, 1280x720, acceptance C4 five-wall room + sphere r 0.12 at (0, 0, 1.2),
+    # voxel 0.63/511, origin (-0.315, -0.315, 0.95) (acceptance.cpp:466-486 scaled), frame-1 solve
+    4: dict(n=512, K=(1120.0, 1120.0, 639.5, 359.5, 1280, 720), voxel=0.63 / 511, origin=(-0.315, -0.315, 0.95),
+            scene="room", desc="BASELINE configs[4] (north-star stress): 512^3 lattice, 1280x720, five-wall room + "
+                               "sphere, frame-1 coarse-to-fine solve (3 levels) on one GPU"),
+}
+
+
+def run_solve(args):
+    """One step = the frame-1 solve_coarse_to_fine of a BASELINE solve config,
+    from identical state every time (device-side checkpoint of the volume
+    after the bootstrap frame): constraints from the frame-1 association at
+    the ICP pose, as process_frame builds them (pipeline.cpp:174-240).  Inputs
+    are HBM-resident; `value` = ms per solve (CUDA events, L2 flushed before
+    each solve).  The roofline is the SURVEY.md 8(d) byte model of every
+    k_flip_flop launch of the timed solves."""
+    from paper_1603_08161_b200.abi import CorrespondParams, Frame, Intrinsics, Pose, SolverParams
+    from paper_1603_08161_b200.wfk import Context, pipeline_config
+    from tools import synthscene as S
+    cfg_s = SOLVE_CONFIGS[args.solve_config]
+    n = cfg_s["n"]
+    K = Intrinsics.make(*cfg_s["K"])
+    if cfg_s["scene"] == "room":
+        sc = S.room_corner(K, frames=30, sphere_radius=0.12)
+        frames_idx = [0, 1]
+    else:
+        sc = S.bend_sphere(K, frames=FRAMES_TOTAL, amplitude=AMPLITUDE, frequency=FREQUENCY)
+        frames_idx = [3, 4]  # a visible bend between the two frames
+    frames = [Frame(K, *S.render(sc, f)) for f in frames_idx]
+    ctx = Context(0)
+    t0 = time.perf_counter()
+    ctx.create_volume((n, n, n), cfg_s["voxel"], cfg_s["origin"])
+    cfg = pipeline_config(solver=SolverParams.make(), reassociations=1)
+    rec0 = ctx.process_frame(frames[0], Pose.make(), cfg, 0)  # bootstrap: fusion + active set
+    ctx.checkpoint_volume()
+    rec1 = ctx.process_frame(frames[1], Pose.make(), cfg, 1)  # the frame's ICP pose (and a full frame, untimed)
+    pose = rec1.pose
+    ctx.checkpoint_volume(restore=True)
+    log(f"setup {time.perf_counter() - t0:.1f}s: bootstrap fused {rec0.fusion.fused}, frame-1 ICP pose found")
+    # frame-1 dense constraints against the bootstrap surface at that pose (pipeline.cpp:161-240)
+    ctx.upload_frame(frames[1])
+    ctx.backproject_depth(download=False)
+    ctx.extract_mesh(pose)
+    ctx.compute_normals()
+    ctx.rasterize(K, download=False)
+    n_cons = ctx.find_dense_correspondences(K, CorrespondParams.make(), drop_inactive=True)
+    p = SolverParams.make()
+    for _ in range(args.warmup):
+        ctx.checkpoint_volume(restore=True)
+        ctx.solve_coarse_to_fine(pose, p)
+    ctx.profile_enable(True)
+    launches0 = ctx.launch_count
+    total_ms, pcg, times = 0.0, 0, []
+    with ClockSampler(0) as clocks:
+        for _ in range(args.steps):
+            ctx.checkpoint_volume(restore=True)
+            ctx.flush_l2()
+            ctx.timer_mark(0)
+            tr = ctx.solve_coarse_to_fine(pose, p)
+            ctx.timer_mark(1)
+            times.append(ctx.timer_elapsed_ms(0, 1))
+            total_ms += times[-1]
+            pcg += sum(e["pcg_iterations"] for e in tr)
+    launches = ctx.launch_count - launches0
+    prof = ctx.profile_read()
+    ctx.profile_enable(False)
+    dims, act = ctx.hierarchy_info(3)
+    ms = total_ms / args.steps
+    peak, peak_src = measured_peak()
+    achieved = prof.flip_flop_bytes / (prof.flip_flop_ms * 1e-3) / 1e9 if prof.flip_flop_ms > 0 else 0.0
+    achieved_impl = prof.flip_flop_bytes_impl / (prof.flip_flop_ms * 1e-3) / 1e9 if prof.flip_flop_ms > 0 else 0.0
+    out = {
+        "metric": METRIC, "value": ms, "unit": "ms/solve", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": DATA + f", frames {frames_idx[0]}-{frames_idx[1]}",
+        "config": {"workload": cfg_s["desc"], "lattice": [n] * 3, "depth_resolution": list(cfg_s["K"][4:]),
+                   "rows_per_level": [int(x) for x in act], "dense_constraints": int(n_cons),
+                   "l2": "flushed (256 MB write) before every solve", "parallelism": "single GPU"},
+        "pcg_iters_per_s": pcg / (total_ms * 1e-3), "pcg_iterations_per_solve": pcg / args.steps,
+        "solve_ms": [round(x, 3) for x in times], "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": "k_flip_flop", "achieved": achieved, "peak": peak,
+                     "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
+                     "bytes_model": "SURVEY.md 8(d): PCG 160 N + 32 C_d + 20 C_s per iteration, rhs/diag 52 N, "
+                                    "rotation 28 N, energy 28 N + 44 C",
+                     "achieved_fp64_layout": achieved_impl, "frac_fp64_layout": achieved_impl / peak,
+                     "launches": prof.flip_flop_launches,
+                     "avg_launch_ms": prof.flip_flop_ms / max(prof.flip_flop_launches, 1),
+                     "share_of_solve": prof.flip_flop_ms / max(total_ms, 1e-9)},
+        "clocks": clocks.summary(),
+        "energy_final": tr[-1]["energy"]["total"] if tr else None,
+    }
+    print(json.dumps(out), flush=True)
+    ctx.close()
+
+
 def cpu_baseline_sample(frames, n_frames):
     """The oracle port on this host's cores, frames 1..n of the same sequence
     after the (untimed) bootstrap frame 0; reports the median ms/frame."""
@@ -568,6 +671,8 @@ def main():
     ap.add_argument("--lattice", type=int, default=N_LATTICE,
                     help="lattice side (default 128 = configs[2]; 256 = the configs[3] lattice on one GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--solve-config", type=int, choices=[3, 4], default=None,
+                    help="BASELINE configs[3] (256^3) or configs[4] (512^3, 1280x720 room): the frame-1 solve x K")
     ap.add_argument("--partitioned", action="store_true",
                     help="BASELINE configs[3]: the 256^3 frame-1 solve with the PCG slab-partitioned over the ranks")
     args = ap.parse_args()
@@ -576,6 +681,8 @@ def main():
         print("warning: W >= 3 warm-up steps are required for a valid number", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args)
+    elif args.solve_config:
+        run_solve(args)
     elif args.partitioned:
         if args.lattice == 128 and "--lattice" not in sys.argv:
             N_LATTICE = 256

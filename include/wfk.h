@@ -49,6 +49,13 @@ int64_t wfk_pcg_iteration_count(const wfk_ctx* ctx);
  * `fields` (WFK_VOL_* mask). */
 int wfk_volume_upload(wfk_ctx* ctx, const wfk_volume_view* v, uint32_t fields);
 int wfk_volume_download(wfk_ctx* ctx, wfk_volume_view* v, uint32_t fields);
+/* a DeformableVolume in its constructor state (volume.cpp:8-25) created on the
+ * device (truncation 4 x voxel) -- no host lattice needed for large volumes */
+int wfk_volume_create(wfk_ctx* ctx, const int32_t dims[3], double voxel_size, const double origin[3]);
+/* device-side checkpoint of the fields a solve or an expansion mutates
+ * (deformed, euler, age, active): restore = 0 saves, 1 restores (e.g. to
+ * repeat one frame's solve from identical state without host traffic) */
+int wfk_volume_checkpoint(wfk_ctx* ctx, int32_t restore);
 
 /* ---- solver (proj/include/wf/solver.hpp) ------------------------------------- */
 /* compute_active_set (solver.hpp:40, solver.cpp:32-69): grow-only.  Writes the

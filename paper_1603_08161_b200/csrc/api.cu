@@ -222,6 +222,85 @@ int wfk_volume_upload(wfk_ctx* c, const wfk_volume_view* v, uint32_t fields) {
   });
 }
 
+namespace wfk {
+// DeformableVolume's constructor state (volume.cpp:8-25) on the device:
+// empty TSDF, t_i = canonical position, identity rotations, age 0, inactive
+__global__ void k_volume_init(Grid g, float* tsdf, float* weight, float* color, double* def, double* eul,
+                              int32_t* age, uint8_t* active) {
+  const int64_t n = g.n();
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const V3 c = g.canonical(int(i));
+    tsdf[i] = 0.f;
+    weight[i] = 0.f;
+    color[3 * i] = color[3 * i + 1] = color[3 * i + 2] = 0.f;
+    def[3 * i] = c.x;
+    def[3 * i + 1] = c.y;
+    def[3 * i + 2] = c.z;
+    eul[3 * i] = eul[3 * i + 1] = eul[3 * i + 2] = 0.0;
+    age[i] = 0;
+    active[i] = 0;
+  }
+}
+}  // namespace wfk
+
+int wfk_volume_create(wfk_ctx* c, const int32_t dims[3], double voxel_size, const double origin[3]) {
+  return guard(c, [&] {
+    if (!dims || !origin) throw Error(WFK_E_INVALID_ARG, "null argument");
+    if (dims[0] < 2 || dims[1] < 2 || dims[2] < 2)
+      throw Error(WFK_E_INVALID_ARG, "DeformableVolume: each dim must be >= 2");
+    if (!(voxel_size > 0)) throw Error(WFK_E_INVALID_ARG, "DeformableVolume: voxel_size must be > 0");
+    VolumeDev& d = c->vol;
+    const Grid g{dims[0], dims[1], dims[2], voxel_size, origin[0], origin[1], origin[2]};
+    const int64_t n = g.n();
+    if (n >= (int64_t(1) << 31)) throw Error(WFK_E_INVALID_ARG, "lattice too large for 32-bit indices");
+    d.g = g;
+    d.n = n;
+    d.mu = 4.0 * voxel_size;  // volume.cpp:14
+    d.tsdf.ensure(size_t(n));
+    d.weight.ensure(size_t(n));
+    d.color.ensure(3 * size_t(n));
+    d.deformed.ensure(3 * size_t(n));
+    d.euler.ensure(3 * size_t(n));
+    d.age.ensure(size_t(n));
+    d.active.ensure(size_t(n));
+    k_volume_init<<<c->num_sms * 8, kBlock, 0, c->stream>>>(g, d.tsdf, d.weight, d.color, d.deformed, d.euler, d.age,
+                                                         d.active);
+    count_launch(c);
+    WFK_CUDA(cudaGetLastError());
+    ++d.active_gen;
+    WFK_CUDA(cudaStreamSynchronize(c->stream));
+    d.valid = true;
+  });
+}
+
+int wfk_volume_checkpoint(wfk_ctx* c, int32_t restore) {
+  return guard(c, [&] {
+    VolumeDev& d = c->vol;
+    if (!d.valid) throw Error(WFK_E_INVALID_ARG, "no volume uploaded");
+    const size_t n = size_t(d.n);
+    cudaStream_t s = c->stream;
+    if (!restore) {
+      d.bk_deformed.ensure(3 * n);
+      d.bk_euler.ensure(3 * n);
+      d.bk_age.ensure(n);
+      d.bk_active.ensure(n);
+      WFK_CUDA(cudaMemcpyAsync(d.bk_deformed, d.deformed, 24 * n, cudaMemcpyDeviceToDevice, s));
+      WFK_CUDA(cudaMemcpyAsync(d.bk_euler, d.euler, 24 * n, cudaMemcpyDeviceToDevice, s));
+      WFK_CUDA(cudaMemcpyAsync(d.bk_age, d.age, 4 * n, cudaMemcpyDeviceToDevice, s));
+      WFK_CUDA(cudaMemcpyAsync(d.bk_active, d.active, n, cudaMemcpyDeviceToDevice, s));
+      d.bk_valid = true;
+    } else {
+      if (!d.bk_valid) throw Error(WFK_E_INVALID_ARG, "no checkpoint saved");
+      WFK_CUDA(cudaMemcpyAsync(d.deformed, d.bk_deformed, 24 * n, cudaMemcpyDeviceToDevice, s));
+      WFK_CUDA(cudaMemcpyAsync(d.euler, d.bk_euler, 24 * n, cudaMemcpyDeviceToDevice, s));
+      WFK_CUDA(cudaMemcpyAsync(d.age, d.bk_age, 4 * n, cudaMemcpyDeviceToDevice, s));
+      WFK_CUDA(cudaMemcpyAsync(d.active, d.bk_active, n, cudaMemcpyDeviceToDevice, s));
+      ++d.active_gen;
+    }
+    WFK_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
 int wfk_volume_download(wfk_ctx* c, wfk_volume_view* v, uint32_t fields) {
   return guard(c, [&] {
     VolumeDev& d = c->vol;

@@ -161,6 +161,11 @@ struct VolumeDev {
   DevBuf<uint8_t> active;
   uint64_t active_gen = 1;  // bumped whenever the active mask may change
   bool valid = false;
+  // device-side checkpoint of the fields a solve / expansion mutates (wfk_volume_checkpoint)
+  DevBuf<double> bk_deformed, bk_euler;
+  DevBuf<int32_t> bk_age;
+  DevBuf<uint8_t> bk_active;
+  bool bk_valid = false;
 };
 
 struct FrameDev {

@@ -199,6 +199,16 @@ class Context:
         vv = vol.view()
         self._check(lib().wfk_volume_download(self.h, C.byref(vv), C.c_uint32(fields)))
 
+    def create_volume(self, dims, voxel: float, origin):
+        """DeformableVolume(dims, voxel, origin) constructed on the device"""
+        d = (C.c_int32 * 3)(*dims)
+        o = (C.c_double * 3)(*origin)
+        self._check(lib().wfk_volume_create(self.h, d, C.c_double(voxel), o))
+
+    def checkpoint_volume(self, restore: bool = False):
+        """device-side save / restore of deformed, euler, age and active"""
+        self._check(lib().wfk_volume_checkpoint(self.h, C.c_int32(1 if restore else 0)))
+
     # ---- snapshot / frame formats (SURVEY.md 8(f) rank 3) -----------------------
     def save_volume(self, path: str):
         """DeformableVolume::save (volume.cpp:150-178) of the device lattice."""
