@@ -1415,6 +1415,7 @@ __device__ inline MfMeta mf_meta(char* base, const PipeLayout& l, bool rows, boo
   return m;
 }
 constexpr int kPipeSkip = 1;  // global warp 0 sums the split reductions
+constexpr int kCgMinRows = 500000;  // spilled levels from this size run the Chronopoulos-Gear PCG
 constexpr size_t kPipeSmemMax = 220 * 1024;  // dynamic shared memory for the row slots
 
 // pcg_solve (solver.cpp:282-343) as pipelined Jacobi-PCG (Ghysels & Vanroose
@@ -2294,6 +2295,16 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   a.meta_rows = a.meta_cons = 0;
   a.asm_smem = 0;
   a.state_spill = nullptr;
+  // Levels far too large for shared memory (the row state would spill to
+  // global) are HBM-bound, not latency-bound: there the Chronopoulos-Gear PCG,
+  // which streams fewer vectors per iteration, beats the pipelined one
+  // (512^3 frame-1 solve 138 vs 173 ms; at 256^3, 215 K rows, the pipelined
+  // spill variant still wins, 13.7 vs 14.5 ms).  WFK_PCG=pipe forces pipelined.
+  if (a.pcg_variant == 0 && L.N >= kCgMinRows && !(pcg_env && std::string(pcg_env) == "pipe")) {
+    const PipeLayout probe = pipe_layout(L.N, L.C, pipe_rpw(L.assembled, a.asm_rows_on_lanes), G, kCoopBlockShared,
+                                         kPipeSkip, false, false);
+    if (probe.total > kPipeSmemMax) a.pcg_variant = 1;
+  }
   if (a.pcg_variant == 0) {
     const int rpw = pipe_rpw(L.assembled, a.asm_rows_on_lanes);
     // the row state goes to a global spill area when it does not fit shared memory
