@@ -355,3 +355,41 @@ def test_chronopoulos_gear_variant_parity(ctx, monkeypatch):
     ctx.download_volume(v)
     monkeypatch.delenv("WFK_PCG", raising=False)
     compare_solves(v, ref, tg, tr)
+
+
+def test_frame_solve_determinism_stress(ctx):
+    """The reference's race proxy is Serial == Parallel bitwise
+    (test_solver.cpp:132-142); the device has no serial mode, so the stand-in
+    is run-to-run identity under the persistent kernel's hand-rolled grid
+    barrier and split reduction: 50 repeats of one frame's coarse-to-fine solve
+    (a configs[2]-sized system: 640x480 dense association against a 128^3
+    bootstrap, 3 levels) must produce bit-identical traces and fields."""
+    from paper_1603_08161_b200.abi import CorrespondParams, Frame, Intrinsics
+    from paper_1603_08161_b200.wfk import pipeline_config
+    from tools import synthscene as S
+    K = Intrinsics.make(560, 560, 319.5, 239.5, 640, 480)
+    sc = S.bend_sphere(K, frames=300, amplitude=2.0, frequency=2.0)
+    f0, f1 = (Frame(K, *S.render(sc, f)) for f in (0, 7))
+    n = 128
+    ctx.create_volume((n, n, n), 0.7 / (n - 1), (-0.35, -0.35, 0.85))
+    cfg = pipeline_config(solver=SolverParams.make(), reassociations=1)
+    ctx.process_frame(f0, Pose.make(), cfg, 0)
+    ctx.checkpoint_volume()
+    ctx.upload_frame(f1)
+    ctx.backproject_depth(download=False)
+    ctx.extract_mesh(Pose.make())
+    ctx.compute_normals()
+    ctx.rasterize(K, download=False)
+    assert ctx.find_dense_correspondences(K, CorrespondParams.make(), drop_inactive=True) > 50000
+    p = SolverParams.make()
+    ref_trace, ref_field = None, None
+    v = Volume((n, n, n), 0.7 / (n - 1), (-0.35, -0.35, 0.85))
+    for rep in range(50):
+        ctx.checkpoint_volume(restore=True)
+        tr = ctx.solve_coarse_to_fine(Pose.make(), p)
+        ctx.download_volume(v, 1 << 3)  # WFK_VOL_DEFORMED
+        if ref_trace is None:
+            ref_trace, ref_field = tr, v.deformed.copy()
+            continue
+        assert tr == ref_trace, rep
+        assert np.array_equal(v.deformed, ref_field), rep
