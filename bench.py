@@ -512,6 +512,8 @@ def run_solve(args):
         frames_idx = [3, 4]  # a visible bend between the two frames
     frames = [Frame(K, *S.render(sc, f)) for f in frames_idx]
     ctx = Context(0)
+    if args.fast:
+        ctx.set_precision(1)  # WFK_PRECISION_FAST: fp32 Krylov vectors on levels that run the CG variant
     t0 = time.perf_counter()
     ctx.create_volume((n, n, n), cfg_s["voxel"], cfg_s["origin"])
     cfg = pipeline_config(solver=SolverParams.make(), reassociations=1)
@@ -555,9 +557,12 @@ def run_solve(args):
     achieved_impl = prof.flip_flop_bytes_impl / (prof.flip_flop_ms * 1e-3) / 1e9 if prof.flip_flop_ms > 0 else 0.0
     out = {
         "metric": METRIC, "value": ms, "unit": "ms/solve", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "ms_per_step": ms, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64+f32 (mixed)" if args.fast else "f64",
         "data": DATA + f", frames {frames_idx[0]}-{frames_idx[1]}",
-        "config": {"workload": cfg_s["desc"], "lattice": [n] * 3, "depth_resolution": list(cfg_s["K"][4:]),
+        "config": {"workload": cfg_s["desc"] + (" [WFK_PRECISION_FAST]" if args.fast else ""),
+                   "precision": "fast (fp32 Krylov vectors on CG levels)" if args.fast else "fp64",
+                   "lattice": [n] * 3, "depth_resolution": list(cfg_s["K"][4:]),
                    "rows_per_level": [int(x) for x in act], "dense_constraints": int(n_cons),
                    "l2": "flushed (256 MB write) before every solve", "parallelism": "single GPU"},
         "pcg_iters_per_s": pcg / (total_ms * 1e-3), "pcg_iterations_per_solve": pcg / args.steps,
@@ -673,6 +678,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--solve-config", type=int, choices=[3, 4], default=None,
                     help="BASELINE configs[3] (256^3) or configs[4] (512^3, 1280x720 room): the frame-1 solve x K")
+    ap.add_argument("--fast", action="store_true",
+                    help="with --solve-config: WFK_PRECISION_FAST (fp32 Krylov vectors on the large CG levels)")
     ap.add_argument("--partitioned", action="store_true",
                     help="BASELINE configs[3]: the 256^3 frame-1 solve with the PCG slab-partitioned over the ranks")
     args = ap.parse_args()

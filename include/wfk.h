@@ -30,13 +30,24 @@ extern "C" {
 typedef struct wfk_ctx wfk_ctx;
 
 typedef struct wfk_config {
-  int32_t device;   /* CUDA ordinal */
-  int32_t reserved_[7];
+  int32_t device;     /* CUDA ordinal */
+  int32_t precision;  /* WFK_PRECISION_FP64 (default: the reference's arithmetic) or WFK_PRECISION_FAST */
+  int32_t reserved_[6];
 } wfk_config;
+
+/* Precision of the context ("fp64 parity / fp32 fast").
+ * FAST stores the Krylov vectors of the Chronopoulos-Gear PCG -- the variant
+ * that runs levels too large for shared memory (>= 500 K rows) -- in fp32
+ * (arithmetic, dot products, the initial residual and the solution stay fp64;
+ * the solution is carried as x0 + an fp32 increment).  Levels that fit keep
+ * fp64 either way.  Parity then holds to tolerance, not bit for bit. */
+enum { WFK_PRECISION_FP64 = 0, WFK_PRECISION_FAST = 1 };
 
 /* ---- context ------------------------------------------------------------- */
 int wfk_create(const wfk_config* cfg, wfk_ctx** out);
 void wfk_destroy(wfk_ctx* ctx);
+/* change the context's precision (WFK_PRECISION_*) for subsequent solves */
+int wfk_set_precision(wfk_ctx* ctx, int32_t precision);
 const char* wfk_last_error(const wfk_ctx* ctx);
 int wfk_version(void);
 /* kernel launches issued by this context so far (for bench accounting) */

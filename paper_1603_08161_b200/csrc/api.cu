@@ -137,6 +137,7 @@ int wfk_create(const wfk_config* cfg, wfk_ctx** out) {
   *out = nullptr;
   auto* c = new wfk_ctx;
   c->device = cfg ? cfg->device : 0;
+  c->precision = cfg ? cfg->precision : 0;
   try {
     int n = 0;
     WFK_CUDA(cudaGetDeviceCount(&n));
@@ -156,6 +157,14 @@ int wfk_create(const wfk_config* cfg, wfk_ctx** out) {
   }
   *out = c;
   return WFK_OK;
+}
+
+int wfk_set_precision(wfk_ctx* c, int32_t precision) {
+  return guard(c, [&] {
+    if (precision != WFK_PRECISION_FP64 && precision != WFK_PRECISION_FAST)
+      throw Error(WFK_E_INVALID_ARG, "unknown precision");
+    c->precision = precision;
+  });
 }
 
 void wfk_destroy(wfk_ctx* c) {

@@ -521,6 +521,9 @@ struct FFArgs {
   int n_xitems;
   const int2* xrange;    // N: first extra item and count of each row
   double4* wpart;        // per-item partial (A v): rows first, then extra items
+  // WFK_PRECISION_FAST Chronopoulos-Gear PCG (V = 2): fp32 Krylov vectors, packed xyz
+  float *f_r, *f_p, *f_s, *f_u, *f_d, *f_dinv, *f_contrib, *f_wpart;
+  int item2;  // Chronopoulos-Gear item pass with two items in flight per thread
   // outputs
   double* partials;  // 4 slots x gridDim
   unsigned* sync_count;  // grid barrier arrival counter (own 128 B line)
@@ -961,6 +964,21 @@ __device__ __forceinline__ void assemble_rows(const FFArgs& a) {
 // (stored after the first N).  Each item writes its partial (A v) to
 // wpart[item]; the update phase adds a row's items in order, and the w.u dot
 // is accumulated per item (it is linear), so no row waits on a long list.
+WF_D V3 ldf3(const float* p, int64_t i) { return {double(p[3 * i]), double(p[3 * i + 1]), double(p[3 * i + 2])}; }
+WF_D void stf3(float* p, int64_t i, V3 v) {
+  p[3 * i] = float(v.x);
+  p[3 * i + 1] = float(v.y);
+  p[3 * i + 2] = float(v.z);
+}
+WF_D V3 rnd3(V3 v) { return {double(float(v.x)), double(float(v.y)), double(float(v.z))}; }
+// storage-generic access for the two-in-flight item pass: fp64 padded 32-byte
+// vectors (double4) or fp32 packed xyz (float)
+WF_D V3 ldv(const double4* p, int64_t i) { return ld4(p, i); }
+WF_D V3 ldv(const float* p, int64_t i) { return ldf3(p, i); }
+WF_D void stv(double4* p, int64_t i, V3 v) { st4(p, i, v); }
+WF_D void stv(float* p, int64_t i, V3 v) { stf3(p, i, v); }
+WF_D V3 sink_round(const double4*, V3 v) { return v; }
+WF_D V3 sink_round(const float*, V3 v) { return rnd3(v); }
 template <class Sink>
 __device__ __forceinline__ void item_pass(const FFArgs& a, const double4* v, Sink& sink) {
   const double w2 = 2.0 * a.w_r;
@@ -1006,6 +1024,207 @@ WF_D V3 row_from_items(const FFArgs& a, int r) {
   const int2 xr = a.xrange[r];
   for (int i = 0; i < xr.y; ++i) acc += ld4(a.wpart, a.N + xr.x + i);
   return acc;
+}
+
+// ---- WFK_PRECISION_FAST: the Chronopoulos-Gear PCG with fp32 vectors --------
+// Only for matrix-free levels too large for shared memory, which are
+// HBM-bound (configs[4]: 3.6 M rows, ~580 B per row per iteration in fp64 with
+// 32-byte padded vectors).  Storage of r, u, p, s = A p, the solution
+// increment d = x - x0, D^-1, the constraint contributions and the item
+// partials is fp32 packed xyz (12 B); every multiply / add, the three dot
+// products and the initial residual r0 = b - A x0 stay fp64, and x = x0 + d
+// is formed in fp64 at the end, so the rounding is relative to the update,
+// not to the absolute positions.
+// matvec pass 1 (see matvec_constraints) on an fp32 vector
+__device__ __forceinline__ void matvec_constraints_f32(const FFArgs& a, const float* v) {
+  for (int64_t c = gtid(); c < a.C; c += gstride()) {
+    int rows[8];
+    double w[8];
+    ld_anchors(a, c, rows, w);
+    const double4 gc = ld4w(a.c_g, c);
+    V3 q{0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (rows[k] >= 0) q += w[k] * ldf3(v, rows[k]);
+    V3 u;
+    if (a.c_kind[c] == WFK_DENSE_PLANE) {
+      const V3 g{gc.x, gc.y, gc.z};
+      u = (gc.w * dot(g, q)) * g;
+    } else {
+      u = gc.w * q;
+    }
+    const int4 p0 = a.c_pos[2 * c], p1 = a.c_pos[2 * c + 1];
+    const int pos[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (pos[k] >= 0) stf3(a.f_contrib, pos[k], w[k] * u);
+  }
+}
+// matvec pass 2 (see item_pass) on an fp32 vector, two items in flight per
+// thread: at ~47 items per thread (3.6 M rows) the pass is a chain of
+// dependent loads (item -> neighbour table -> gathers), so every load of both
+// items is issued before any of their arithmetic.
+template <class VT, class Sink>
+__device__ __forceinline__ void item_pass2(const FFArgs& a, const VT* v, VT* contrib, VT* wpart,
+                                           Sink& sink) {
+  const double w2 = 2.0 * a.w_r;
+  const int total = a.N + a.n_xitems;
+  const int st = int(gstride());
+  for (int i0 = int(gtid()); i0 < total; i0 += 2 * st) {
+    int r[2], e0[2], e1[2], nb[2][6];
+    bool live[2], first[2], frz[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = i0 + h * st;
+      live[h] = i < total;
+      first[h] = live[h] && i < a.N;
+      r[h] = 0;
+      e0[h] = e1[h] = 0;
+      frz[h] = false;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) nb[h][k] = -1;
+      if (!live[h]) continue;
+      if (first[h]) {
+        r[h] = i;
+        e0[h] = a.row_ptr[i];
+        e1[h] = min(a.row_ptr[i + 1], e0[h] + kItemLen);
+        frz[h] = a.frozen[i];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) nb[h][k] = a.nbr[int64_t(k) * a.N + i];
+      } else {
+        const int4 it = a.xitems[i - a.N];
+        r[h] = it.x;
+        e0[h] = it.y;
+        e1[h] = it.z;
+      }
+    }
+    // item_pass's order: the contributions in incidence order, then the six
+    // Laplacian terms in face order (bit-identical fp64 results); the two
+    // items' loads are interleaved step by step
+    V3 vr[2], acc[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      vr[h] = live[h] ? ldv(v, r[h]) : V3{0, 0, 0};
+      acc[h] = V3{0, 0, 0};
+      if (live[h] && !(first[h] && frz[h]))
+        for (int e = e0[h]; e < e1[h]; ++e) acc[h] += ldv(contrib, e);
+    }
+#pragma unroll
+    for (int k = 0; k < 6; ++k)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (first[h] && !frz[h] && nb[h][k] >= 0) acc[h] += w2 * (vr[h] - ldv(v, nb[h][k]));
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (!live[h]) continue;
+      if (first[h] && frz[h]) acc[h] = vr[h];  // frozen rows: A = I (solver.cpp:241-246)
+      stv(wpart, i0 + h * st, acc[h]);
+      sink(r[h], vr[h], sink_round(v, acc[h]));
+    }
+  }
+}
+template <class Sink>
+__device__ __forceinline__ void item_pass_f32(const FFArgs& a, const float* v, Sink& sink) {
+  item_pass2(a, v, a.f_contrib, a.f_wpart, sink);
+}
+WF_D V3 row_from_items_f32(const FFArgs& a, int r) {
+  V3 acc = ldf3(a.f_wpart, r);
+  const int2 xr = a.xrange[r];
+  for (int i = 0; i < xr.y; ++i) acc += ldf3(a.f_wpart, a.N + xr.x + i);
+  return acc;
+}
+__device__ void pcg_f32(const FFArgs& a, Red& rs, int& iters, double& relres) {
+  iters = 0;
+  relres = 0;
+  PhaseClock pc(a.dbg);
+  auto none = [](int, V3, V3) {};
+  // r0 = b - A x0 in fp64 (the fp64 matvec of x0), then rounded into storage
+  double acc_rr = 0, acc_bb = 0;
+  matvec_constraints(a, a.x);
+  grid_barrier(a, rs);
+  item_pass(a, a.x, none);
+  grid_barrier(a, rs);
+  for (int r = int(gtid()); r < a.N; r += int(gstride())) {
+    const V3 b = ld4(a.rhs, r);
+    const V3 rr = rnd3(b - row_from_items(a, r));
+    const V3 d = rnd3(ld4(a.dinv, r));
+    stf3(a.f_r, r, rr);
+    stf3(a.f_dinv, r, d);
+    stf3(a.f_u, r, cmul(d, rr));
+    stf3(a.f_p, r, V3{0, 0, 0});
+    stf3(a.f_s, r, V3{0, 0, 0});
+    stf3(a.f_d, r, V3{0, 0, 0});
+    acc_rr += dot(rr, rr);
+    acc_bb += sqnorm(b);
+  }
+  grid_barrier(a, rs);
+  // w0 = A u0
+  double v4[4] = {0, 0, acc_rr, acc_bb};
+  matvec_constraints_f32(a, a.f_u);
+  grid_barrier(a, rs);
+  auto w_sink = [&](int, V3 ur, V3 wpart) { v4[1] += dot(wpart, ur); };
+  item_pass_f32(a, a.f_u, w_sink);
+  for (int r = int(gtid()); r < a.N; r += int(gstride())) v4[0] += dot(ldf3(a.f_r, r), ldf3(a.f_u, r));
+  grid_reduce<4>(a, rs, v4);
+  double gamma = v4[0], delta = v4[1];
+  double r_norm = sqrt(v4[2]);
+  const double b_norm = sqrt(v4[3]);
+  if (b_norm == 0) {
+    for (int r = int(gtid()); r < a.N; r += int(gstride())) st4(a.x, r, V3{0, 0, 0});
+    grid_barrier(a, rs);
+    return;
+  }
+  relres = r_norm / b_norm;
+  const double stop = fmax(a.pcg_tol * r_norm, 1e-13 * b_norm);
+  double gamma_prev = 0, alpha_prev = 0;
+  pc.lap(12);
+  for (int it = 0; it < a.pcg_max && r_norm > stop; ++it) {
+    const double beta = it == 0 ? 0.0 : gamma / gamma_prev;
+    const double pap = it == 0 ? delta : delta - beta * gamma / alpha_prev;
+    if (pap <= 0) break;  // solver.cpp:327
+    const double alpha = gamma / pap;
+    double v3[3] = {0, 0, 0};
+    // one row per thread in flight here: two (as in item_pass_f32) spill at
+    // 512 threads and measured slower (U 238 K vs 205 K cycles per level-0 iteration)
+    for (int r = int(gtid()); r < a.N; r += int(gstride())) {
+      const V3 w = row_from_items_f32(a, r);
+      const V3 p = rnd3(ldf3(a.f_u, r) + beta * ldf3(a.f_p, r));
+      const V3 sv = rnd3(w + beta * ldf3(a.f_s, r));
+      const V3 d = ldf3(a.f_d, r) + alpha * p;
+      const V3 rr = rnd3(ldf3(a.f_r, r) - alpha * sv);
+      const V3 u = rnd3(cmul(ldf3(a.f_dinv, r), rr));
+      stf3(a.f_p, r, p);
+      stf3(a.f_s, r, sv);
+      stf3(a.f_d, r, d);
+      stf3(a.f_r, r, rr);
+      stf3(a.f_u, r, u);
+      v3[0] += dot(rr, u);
+      v3[2] += dot(rr, rr);
+    }
+    pc.lap(4);
+    grid_barrier(a, rs);
+    pc.lap(5);
+    matvec_constraints_f32(a, a.f_u);
+    pc.lap(0);
+    grid_barrier(a, rs);
+    pc.lap(1);
+    auto w_sink2 = [&](int, V3 ur, V3 wpart) { v3[1] += dot(wpart, ur); };
+    item_pass_f32(a, a.f_u, w_sink2);
+    pc.lap(2);
+    grid_reduce<3>(a, rs, v3, &pc);
+    pc.lap(3);
+    pc.count(15);
+    gamma_prev = gamma;
+    alpha_prev = alpha;
+    gamma = v3[0];
+    delta = v3[1];
+    r_norm = sqrt(v3[2]);
+    relres = r_norm / b_norm;
+    iters = it + 1;
+  }
+  // x = x0 + d in fp64 (a.x still holds x0 = t)
+  for (int r = int(gtid()); r < a.N; r += int(gstride())) st4(a.x, r, ld4(a.x, r) + ldf3(a.f_d, r));
+  grid_barrier(a, rs);
 }
 
 // pcg_solve (solver.cpp:282-343) in the Chronopoulos-Gear arrangement: the
@@ -1113,7 +1332,10 @@ __device__ void pcg(const FFArgs& a, cg::grid_group& grid, Red& rs, int& iters, 
       grid_barrier(a, rs);
       pc.lap(1);
       auto w_sink2 = [&](int, V3 ur, V3 wpart) { v3[1] += dot(wpart, ur); };
-      item_pass(a, a.u, w_sink2);
+      if (a.item2)
+        item_pass2(a, static_cast<const double4*>(a.u), a.contrib, a.wpart, w_sink2);
+      else
+        item_pass(a, a.u, w_sink2);
     }
     pc.lap(2);
     grid_reduce<3>(a, rs, v3, &pc);
@@ -1416,6 +1638,7 @@ __device__ inline MfMeta mf_meta(char* base, const PipeLayout& l, bool rows, boo
 }
 constexpr int kPipeSkip = 1;  // global warp 0 sums the split reductions
 constexpr int kCgMinRows = 500000;  // spilled levels from this size run the Chronopoulos-Gear PCG
+constexpr int kFastBlock = 512;      // threads per block of the WFK_PRECISION_FAST CG kernel
 constexpr size_t kPipeSmemMax = 220 * 1024;  // dynamic shared memory for the row slots
 
 // pcg_solve (solver.cpp:282-343) as pipelined Jacobi-PCG (Ghysels & Vanroose
@@ -1729,7 +1952,9 @@ __global__ void __launch_bounds__(TPB, 1) k_flip_flop(FFArgs a) {
       pc.lap(8);
       int iters;
       double relres;
-      if (V == 1)
+      if (V == 2) {
+        if constexpr (!ASM) pcg_f32(a, rs, iters, relres);
+      } else if (V == 1)
         pcg<ASM>(a, grid, rs, iters, relres);
       else
         pcg_pipe<ASM, NSM>(a, rs, iters, relres);
@@ -2354,7 +2579,28 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   }
   void (*kern)(FFArgs) = nullptr;
   const bool asm_k = L.assembled;
-  if (a.pcg_variant == 1)
+  // WFK_PRECISION_FAST: the CG variant of a matrix-free level with fp32 vectors
+  const bool fast = c->precision == WFK_PRECISION_FAST && a.pcg_variant == 1 && !asm_k && L.N > 0 && mode == 0;
+  a.f_r = a.f_p = a.f_s = a.f_u = a.f_d = a.f_dinv = a.f_contrib = a.f_wpart = nullptr;
+  static const bool item1 = getenv("WFK_ITEM1") != nullptr;  // A/B: one item per thread in flight
+  a.item2 = item1 ? 0 : 1;
+  if (fast) {
+    const size_t n3 = 3 * size_t(L.N);
+    a.f_r = L.f_r.ensure(n3);
+    a.f_p = L.f_p.ensure(n3);
+    a.f_s = L.f_s.ensure(n3);
+    a.f_u = L.f_u.ensure(n3);
+    a.f_d = L.f_d.ensure(n3);
+    a.f_dinv = L.f_dinv.ensure(n3);
+    a.f_contrib = L.f_contrib.ensure(3 * size_t(std::max<int64_t>(L.E, 1)));
+    a.f_wpart = L.f_wpart.ensure(3 * (size_t(L.N) + size_t(L.n_xitems) + 1));
+  }
+  if (fast) {
+    // two items in flight per thread need the registers of a 256-thread block
+    kern = k_flip_flop<2, false, kSlotVecs, kFastBlock>;
+    tpb = kFastBlock;
+  }
+  else if (a.pcg_variant == 1)
     kern = asm_k ? k_flip_flop<1, true> : k_flip_flop<1, false>;
   else if (nsm == kSlotVecs)
     kern = asm_k ? k_flip_flop<0, true, kSlotVecs, kCoopBlockShared> : k_flip_flop<0, false, kSlotVecs, kCoopBlockShared>;

@@ -146,6 +146,8 @@ struct Level {
   DevBuf<int32_t> row_ptr, ent_con, key_in, key_out, val_in, val_out;
   DevBuf<double> ent_w;
   DevBuf<int32_t> cnt;
+  // WFK_PRECISION_FAST Chronopoulos-Gear PCG: fp32 Krylov vectors (packed xyz)
+  DevBuf<float> f_r, f_p, f_s, f_u, f_d, f_dinv, f_contrib, f_wpart;
   // explicit normal equations of the slab-partitioned solve (solver_c2f_dist)
   DevBuf<double> ne_blocks, ne_rhs, ne_x;
   DevBuf<int32_t> ne_cols;
@@ -272,6 +274,7 @@ struct wfk_ctx {
   int num_sms = 0;
   cudaStream_t stream = nullptr;
   std::string err;
+  int precision = 0;  // WFK_PRECISION_FP64 | WFK_PRECISION_FAST
   wfk::VolumeDev vol;
   wfk::ConIn cons;
   wfk::Level lv[wfk::kMaxLevels];

@@ -72,7 +72,7 @@ class Profile(C.Structure):
 
 
 class Config(C.Structure):
-    _fields_ = [("device", C.c_int32), ("reserved_", C.c_int32 * 7)]
+    _fields_ = [("device", C.c_int32), ("precision", C.c_int32), ("reserved_", C.c_int32 * 6)]
 
 
 _lib = None
@@ -160,15 +160,20 @@ _PINNED_KEEP = []
 class Context:
     """One libwfk context on one CUDA device (wfk_create / wfk_destroy)."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, precision: int = 0):
         cfg = Config()
         cfg.device = device
+        cfg.precision = precision
         h = C.c_void_p()
         rc = lib().wfk_create(C.byref(cfg), C.byref(h))
         if rc != WFK_OK:
             raise WfkError(rc, "wfk_create failed (no B200 / CUDA device visible?)")
         self.h = h
         self.dims = None
+
+    def set_precision(self, precision: int):
+        """WFK_PRECISION_FP64 (0, default) or WFK_PRECISION_FAST (1)"""
+        self._check(lib().wfk_set_precision(self.h, C.c_int32(precision)))
 
     def close(self):
         if getattr(self, "h", None):

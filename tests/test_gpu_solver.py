@@ -393,3 +393,31 @@ def test_frame_solve_determinism_stress(ctx):
             continue
         assert tr == ref_trace, rep
         assert np.array_equal(v.deformed, ref_field), rep
+
+
+def test_fast_precision_cg_parity(ctx, monkeypatch):
+    """WFK_PRECISION_FAST (fp32 Krylov vectors in the Chronopoulos-Gear PCG of
+    matrix-free levels; fp64 arithmetic, dots, initial residual, x = x0 + d):
+    parity by tolerance against the reference -- the north-star bars, 1e-4
+    relative energy and 1e-3 voxel (measured at configs[4]: 9e-7, 1.5e-5)."""
+    v = make_volume(32)
+    cons = random_dense_constraints(v, 3000, seed=13)
+    p = SolverParams.make()
+    pose = Pose.make(O.euler_to_matrix((0.0, 0.01, 0.0)), (0.005, 0, 0))
+    ref = v.copy()
+    tr = O.solve_coarse_to_fine(ref, pose, cons, p)
+    monkeypatch.setenv("WFK_PCG", "cg")  # below 500 K rows the CG variant (and so FAST) must be forced
+    ctx.set_precision(1)
+    try:
+        ctx.upload_volume(v)
+        ctx.upload_constraints(cons)
+        tg = ctx.solve_coarse_to_fine(pose, p)
+        ctx.download_volume(v)
+    finally:
+        ctx.set_precision(0)
+    assert len(tg) == len(tr)
+    for a, b in zip(tg, tr):
+        assert a["energy"]["total"] == pytest.approx(b["energy"]["total"], rel=1e-4)
+    act = ref.active.astype(bool)
+    dev = np.max(np.linalg.norm(v.deformed[act] - ref.deformed[act], axis=1)) / v.voxel_size
+    assert dev <= 1e-3, dev

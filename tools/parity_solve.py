@@ -36,6 +36,8 @@ def main(cfg_id: int):
                                 frequency=bench.FREQUENCY), [3, 4]
     frames = [Frame(K, *S.render(sc, f)) for f in idx]
     ctx = Context(0)
+    if os.environ.get("WF_FAST"):
+        ctx.set_precision(1)  # WFK_PRECISION_FAST
     ctx.create_volume((n, n, n), c["voxel"], c["origin"])
     cfg = pipeline_config(solver=SolverParams.make(), reassociations=1)
     ctx.process_frame(frames[0], Pose.make(), cfg, 0)
@@ -70,6 +72,7 @@ def main(cfg_id: int):
            "worst_energy_rel": max(e_rel), "final_energy": [tg[-1]["energy"]["total"], tr[-1]["energy"]["total"]],
            "deformation_dev_voxel": dev, "gpu_solve_s_incl_sync": t_gpu, "reference_solve_s": t_ref,
            "reference_threads": int(O.lib().wfo_num_threads()),
+           "precision": "fast" if os.environ.get("WF_FAST") else "fp64",
            "env": {k: v for k, v in os.environ.items() if k.startswith("WFK_")}}
     print(json.dumps(out))
 
