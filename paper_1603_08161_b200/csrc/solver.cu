@@ -524,6 +524,7 @@ struct FFArgs {
   // WFK_PRECISION_FAST Chronopoulos-Gear PCG (V = 2): fp32 Krylov vectors, packed xyz
   float *f_r, *f_p, *f_s, *f_u, *f_d, *f_dinv, *f_contrib, *f_wpart;
   int item2;  // Chronopoulos-Gear item pass with two items in flight per thread
+  int cluster2;  // launched in 2-CTA clusters: one grid-barrier arrival per cluster
   // outputs
   double* partials;  // 4 slots x gridDim
   unsigned* sync_count;  // grid barrier arrival counter (own 128 B line)
@@ -621,16 +622,31 @@ __device__ __forceinline__ unsigned atom_add_acq_rel_u32(unsigned* p, unsigned v
   return old;
 }
 
+// 2-CTA clusters (a.cluster2): the pair meets at a cluster barrier (release /
+// acquire at cluster scope) and only cluster rank 0 arrives on the grid
+// counter -- its gpu-scope release is cumulative over its partner's writes --
+// so the counter sees G / 2 arrivals per generation; both CTAs poll it.
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned arrivals_per_gen(const FFArgs& a) { return a.cluster2 ? gridDim.x / 2 : gridDim.x; }
+
 __device__ __forceinline__ void grid_barrier(const FFArgs& a, Red& rs) {
   __syncthreads();
+  if (a.cluster2) cluster_sync_all();
   if (threadIdx.x == 0) {
     // the arrival counter only grows (reset at launch): the last arrival of
-    // generation g reads G (g + 1) - 1.  The acq_rel arrival releases the
-    // block's writes (ordered before it by the block barrier) and, for the
-    // last block, acquires everyone else's.
-    const unsigned target = gridDim.x * (rs.gen + 1);
-    const unsigned old = atom_add_acq_rel_u32(a.sync_count, 1u);
-    if (old == target - 1) {
+    // generation g reads A (g + 1) - 1 (A arrivals per generation).  The
+    // acq_rel arrival releases the block's writes (ordered before it by the
+    // block barrier) and, for the last block, acquires everyone else's.
+    const unsigned target = arrivals_per_gen(a) * (rs.gen + 1);
+    const unsigned old = (a.cluster2 && cluster_rank() != 0) ? 0u : atom_add_acq_rel_u32(a.sync_count, 1u);
+    if ((!a.cluster2 || cluster_rank() == 0) && old == target - 1) {
       atom_max_release_u32(a.sync_gen, rs.gen + 1);
     } else {
       // poll the arrival counter itself: the last arrival's RMW is visible
@@ -655,16 +671,20 @@ __device__ __forceinline__ void grid_reduce(const FFArgs& a, Red& rs, double (&v
     for (int k = 0; k < NV; ++k) smem[k * 32 + warp] = v[k];
   __syncthreads();
   if (pc) pc->lap(6);
+  double s[NV];
   if (warp == 0) {
-    double s[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) s[k] = warp_sum(lane < nw ? smem[k * 32 + lane] : 0.0);
-    unsigned last = 0;
-    if (lane == 0) {
+    if (lane == 0)
 #pragma unroll
       for (int k = 0; k < NV; ++k) a.partials[size_t(k) * gridDim.x + blockIdx.x] = s[k];
-      last = atom_add_acq_rel_u32(a.sync_count, 1u) == gridDim.x * (rs.gen + 1) - 1 ? 1u : 0u;
-    }
+  }
+  // 2-CTA clusters: the partner's partials are released to rank 0 here
+  if (a.cluster2) cluster_sync_all();
+  if (warp == 0) {
+    unsigned last = 0;
+    if (lane == 0 && (!a.cluster2 || cluster_rank() == 0))
+      last = atom_add_acq_rel_u32(a.sync_count, 1u) == arrivals_per_gen(a) * (rs.gen + 1) - 1 ? 1u : 0u;
     last = __shfl_sync(0xffffffffu, last, 0);
     if (last) {
 #pragma unroll
@@ -2627,7 +2647,27 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   void* args[] = {&a};
   Prof& pf = c->prof;
   if (pf.on) WFK_CUDA(cudaEventRecord(pf.ev[0], s));
-  WFK_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(G), dim3(tpb), args, smem, s));
+  static const bool cluster2 = getenv("WFK_CLUSTER2") != nullptr;  // experiment: 2-CTA cluster arrivals
+  a.cluster2 = (cluster2 && G % 2 == 0) ? 1 : 0;
+  if (a.cluster2) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(G);
+    lc.blockDim = dim3(tpb);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = 2;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 2;
+    WFK_CUDA(cudaLaunchKernelExC(&lc, (const void*)kern, args));
+  } else {
+    WFK_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(G), dim3(tpb), args, smem, s));
+  }
   if (pf.on) WFK_CUDA(cudaEventRecord(pf.ev[1], s));
   count_launch(c);
   int32_t st[4];
