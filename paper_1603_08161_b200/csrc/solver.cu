@@ -472,6 +472,22 @@ __global__ void k_prolong(Grid fine, Grid coarse, const uint8_t* f_act, double* 
 // the cooperative flip-flop kernel
 // ============================================================================
 
+// Krylov storage of the packed Chronopoulos-Gear PCG (pcg_pk): xyz triples,
+// 12 B (fp32) or 24 B (fp64) per row instead of 32-byte padded double4
+template <class S>
+struct AlignedOf {  // the gathered vector u stays one aligned load: double4 / float4
+  using type = double4;
+};
+template <>
+struct AlignedOf<float> {
+  using type = float4;
+};
+template <class S>
+struct PackVecs {
+  S *r, *p, *s, *d, *dinv, *contrib, *wpart;
+  typename AlignedOf<S>::type* u;  // gathered by both matvec passes: aligned, not packed
+};
+
 struct FFArgs {
   Grid g;
   int N;
@@ -521,8 +537,10 @@ struct FFArgs {
   int n_xitems;
   const int2* xrange;    // N: first extra item and count of each row
   double4* wpart;        // per-item partial (A v): rows first, then extra items
-  // WFK_PRECISION_FAST Chronopoulos-Gear PCG (V = 2): fp32 Krylov vectors, packed xyz
-  float *f_r, *f_p, *f_s, *f_u, *f_d, *f_dinv, *f_contrib, *f_wpart;
+  // packed-storage Chronopoulos-Gear PCG of large matrix-free levels: fp32
+  // (V = 2, WFK_PRECISION_FAST) or fp64 (V = 3) Krylov vectors, packed xyz
+  PackVecs<float> fv;
+  PackVecs<double> dv;
   int item2;  // Chronopoulos-Gear item pass with two items in flight per thread
   int cluster2;  // launched in 2-CTA clusters: one grid-barrier arrival per cluster
   // outputs
@@ -995,10 +1013,23 @@ WF_D V3 rnd3(V3 v) { return {double(float(v.x)), double(float(v.y)), double(floa
 // vectors (double4) or fp32 packed xyz (float)
 WF_D V3 ldv(const double4* p, int64_t i) { return ld4(p, i); }
 WF_D V3 ldv(const float* p, int64_t i) { return ldf3(p, i); }
+WF_D V3 ldv(const double* p, int64_t i) { return {p[3 * i], p[3 * i + 1], p[3 * i + 2]}; }
 WF_D void stv(double4* p, int64_t i, V3 v) { st4(p, i, v); }
 WF_D void stv(float* p, int64_t i, V3 v) { stf3(p, i, v); }
+WF_D void stv(double* p, int64_t i, V3 v) {
+  p[3 * i] = v.x;
+  p[3 * i + 1] = v.y;
+  p[3 * i + 2] = v.z;
+}
 WF_D V3 sink_round(const double4*, V3 v) { return v; }
 WF_D V3 sink_round(const float*, V3 v) { return rnd3(v); }
+WF_D V3 sink_round(const double*, V3 v) { return v; }
+WF_D V3 ldv(const float4* p, int64_t i) {
+  const float4 f = p[i];
+  return {double(f.x), double(f.y), double(f.z)};
+}
+WF_D void stv(float4* p, int64_t i, V3 v) { p[i] = make_float4(float(v.x), float(v.y), float(v.z), 0.f); }
+WF_D V3 sink_round(const float4*, V3 v) { return rnd3(v); }
 template <class Sink>
 __device__ __forceinline__ void item_pass(const FFArgs& a, const double4* v, Sink& sink) {
   const double w2 = 2.0 * a.w_r;
@@ -1055,8 +1086,9 @@ WF_D V3 row_from_items(const FFArgs& a, int r) {
 // products and the initial residual r0 = b - A x0 stay fp64, and x = x0 + d
 // is formed in fp64 at the end, so the rounding is relative to the update,
 // not to the absolute positions.
-// matvec pass 1 (see matvec_constraints) on an fp32 vector
-__device__ __forceinline__ void matvec_constraints_f32(const FFArgs& a, const float* v) {
+// matvec pass 1 (see matvec_constraints) on a packed vector
+template <class VT, class S>
+__device__ __forceinline__ void matvec_constraints_pk(const FFArgs& a, const VT* v, S* contrib) {
   for (int64_t c = gtid(); c < a.C; c += gstride()) {
     int rows[8];
     double w[8];
@@ -1065,7 +1097,7 @@ __device__ __forceinline__ void matvec_constraints_f32(const FFArgs& a, const fl
     V3 q{0, 0, 0};
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-      if (rows[k] >= 0) q += w[k] * ldf3(v, rows[k]);
+      if (rows[k] >= 0) q += w[k] * ldv(v, rows[k]);
     V3 u;
     if (a.c_kind[c] == WFK_DENSE_PLANE) {
       const V3 g{gc.x, gc.y, gc.z};
@@ -1077,16 +1109,15 @@ __device__ __forceinline__ void matvec_constraints_f32(const FFArgs& a, const fl
     const int pos[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-      if (pos[k] >= 0) stf3(a.f_contrib, pos[k], w[k] * u);
+      if (pos[k] >= 0) stv(contrib, pos[k], w[k] * u);
   }
 }
 // matvec pass 2 (see item_pass) on an fp32 vector, two items in flight per
 // thread: at ~47 items per thread (3.6 M rows) the pass is a chain of
 // dependent loads (item -> neighbour table -> gathers), so every load of both
 // items is issued before any of their arithmetic.
-template <class VT, class Sink>
-__device__ __forceinline__ void item_pass2(const FFArgs& a, const VT* v, VT* contrib, VT* wpart,
-                                           Sink& sink) {
+template <class VT, class CT, class Sink>
+__device__ __forceinline__ void item_pass2(const FFArgs& a, const VT* v, CT* contrib, CT* wpart, Sink& sink) {
   const double w2 = 2.0 * a.w_r;
   const int total = a.N + a.n_xitems;
   const int st = int(gstride());
@@ -1143,17 +1174,30 @@ __device__ __forceinline__ void item_pass2(const FFArgs& a, const VT* v, VT* con
     }
   }
 }
-template <class Sink>
-__device__ __forceinline__ void item_pass_f32(const FFArgs& a, const float* v, Sink& sink) {
-  item_pass2(a, v, a.f_contrib, a.f_wpart, sink);
-}
-WF_D V3 row_from_items_f32(const FFArgs& a, int r) {
-  V3 acc = ldf3(a.f_wpart, r);
+template <class S>
+WF_D V3 row_from_items_pk(const FFArgs& a, const S* wpart, int r) {
+  V3 acc = ldv(wpart, r);
   const int2 xr = a.xrange[r];
-  for (int i = 0; i < xr.y; ++i) acc += ldf3(a.f_wpart, a.N + xr.x + i);
+  for (int i = 0; i < xr.y; ++i) acc += ldv(wpart, a.N + xr.x + i);
   return acc;
 }
-__device__ void pcg_f32(const FFArgs& a, Red& rs, int& iters, double& relres) {
+template <class S>
+WF_D V3 rnd_s(V3 v) {
+  if constexpr (std::is_same<S, float>::value)
+    return rnd3(v);
+  else
+    return v;
+}
+template <class S>
+__device__ __forceinline__ const PackVecs<S>& pack_of(const FFArgs& a) {
+  if constexpr (std::is_same<S, float>::value)
+    return a.fv;
+  else
+    return a.dv;
+}
+template <class S>
+__device__ void pcg_pk(const FFArgs& a, Red& rs, int& iters, double& relres) {
+  const PackVecs<S>& pv = pack_of<S>(a);
   iters = 0;
   relres = 0;
   PhaseClock pc(a.dbg);
@@ -1166,25 +1210,25 @@ __device__ void pcg_f32(const FFArgs& a, Red& rs, int& iters, double& relres) {
   grid_barrier(a, rs);
   for (int r = int(gtid()); r < a.N; r += int(gstride())) {
     const V3 b = ld4(a.rhs, r);
-    const V3 rr = rnd3(b - row_from_items(a, r));
-    const V3 d = rnd3(ld4(a.dinv, r));
-    stf3(a.f_r, r, rr);
-    stf3(a.f_dinv, r, d);
-    stf3(a.f_u, r, cmul(d, rr));
-    stf3(a.f_p, r, V3{0, 0, 0});
-    stf3(a.f_s, r, V3{0, 0, 0});
-    stf3(a.f_d, r, V3{0, 0, 0});
+    const V3 rr = rnd_s<S>(b - row_from_items(a, r));
+    const V3 d = rnd_s<S>(ld4(a.dinv, r));
+    stv(pv.r, r, rr);
+    stv(pv.dinv, r, d);
+    stv(pv.u, r, cmul(d, rr));
+    stv(pv.p, r, V3{0, 0, 0});
+    stv(pv.s, r, V3{0, 0, 0});
+    stv(pv.d, r, V3{0, 0, 0});
     acc_rr += dot(rr, rr);
     acc_bb += sqnorm(b);
   }
   grid_barrier(a, rs);
   // w0 = A u0
   double v4[4] = {0, 0, acc_rr, acc_bb};
-  matvec_constraints_f32(a, a.f_u);
+  matvec_constraints_pk(a, pv.u, pv.contrib);
   grid_barrier(a, rs);
   auto w_sink = [&](int, V3 ur, V3 wpart) { v4[1] += dot(wpart, ur); };
-  item_pass_f32(a, a.f_u, w_sink);
-  for (int r = int(gtid()); r < a.N; r += int(gstride())) v4[0] += dot(ldf3(a.f_r, r), ldf3(a.f_u, r));
+  item_pass2(a, pv.u, pv.contrib, pv.wpart, w_sink);
+  for (int r = int(gtid()); r < a.N; r += int(gstride())) v4[0] += dot(ldv(pv.r, r), ldv(pv.u, r));
   grid_reduce<4>(a, rs, v4);
   double gamma = v4[0], delta = v4[1];
   double r_norm = sqrt(v4[2]);
@@ -1207,29 +1251,29 @@ __device__ void pcg_f32(const FFArgs& a, Red& rs, int& iters, double& relres) {
     // one row per thread in flight here: two (as in item_pass_f32) spill at
     // 512 threads and measured slower (U 238 K vs 205 K cycles per level-0 iteration)
     for (int r = int(gtid()); r < a.N; r += int(gstride())) {
-      const V3 w = row_from_items_f32(a, r);
-      const V3 p = rnd3(ldf3(a.f_u, r) + beta * ldf3(a.f_p, r));
-      const V3 sv = rnd3(w + beta * ldf3(a.f_s, r));
-      const V3 d = ldf3(a.f_d, r) + alpha * p;
-      const V3 rr = rnd3(ldf3(a.f_r, r) - alpha * sv);
-      const V3 u = rnd3(cmul(ldf3(a.f_dinv, r), rr));
-      stf3(a.f_p, r, p);
-      stf3(a.f_s, r, sv);
-      stf3(a.f_d, r, d);
-      stf3(a.f_r, r, rr);
-      stf3(a.f_u, r, u);
+      const V3 w = row_from_items_pk(a, static_cast<const S*>(pv.wpart), r);
+      const V3 p = rnd_s<S>(ldv(pv.u, r) + beta * ldv(pv.p, r));
+      const V3 sv = rnd_s<S>(w + beta * ldv(pv.s, r));
+      const V3 d = ldv(pv.d, r) + alpha * p;
+      const V3 rr = rnd_s<S>(ldv(pv.r, r) - alpha * sv);
+      const V3 u = rnd_s<S>(cmul(ldv(pv.dinv, r), rr));
+      stv(pv.p, r, p);
+      stv(pv.s, r, sv);
+      stv(pv.d, r, d);
+      stv(pv.r, r, rr);
+      stv(pv.u, r, u);
       v3[0] += dot(rr, u);
       v3[2] += dot(rr, rr);
     }
     pc.lap(4);
     grid_barrier(a, rs);
     pc.lap(5);
-    matvec_constraints_f32(a, a.f_u);
+    matvec_constraints_pk(a, pv.u, pv.contrib);
     pc.lap(0);
     grid_barrier(a, rs);
     pc.lap(1);
     auto w_sink2 = [&](int, V3 ur, V3 wpart) { v3[1] += dot(wpart, ur); };
-    item_pass_f32(a, a.f_u, w_sink2);
+    item_pass2(a, pv.u, pv.contrib, pv.wpart, w_sink2);
     pc.lap(2);
     grid_reduce<3>(a, rs, v3, &pc);
     pc.lap(3);
@@ -1243,7 +1287,7 @@ __device__ void pcg_f32(const FFArgs& a, Red& rs, int& iters, double& relres) {
     iters = it + 1;
   }
   // x = x0 + d in fp64 (a.x still holds x0 = t)
-  for (int r = int(gtid()); r < a.N; r += int(gstride())) st4(a.x, r, ld4(a.x, r) + ldf3(a.f_d, r));
+  for (int r = int(gtid()); r < a.N; r += int(gstride())) st4(a.x, r, ld4(a.x, r) + ldv(pv.d, r));
   grid_barrier(a, rs);
 }
 
@@ -1972,8 +2016,13 @@ __global__ void __launch_bounds__(TPB, 1) k_flip_flop(FFArgs a) {
       pc.lap(8);
       int iters;
       double relres;
-      if (V == 2) {
-        if constexpr (!ASM) pcg_f32(a, rs, iters, relres);
+      if (V == 2 || V == 3) {
+        if constexpr (!ASM) {
+          if constexpr (V == 2)
+            pcg_pk<float>(a, rs, iters, relres);
+          else
+            pcg_pk<double>(a, rs, iters, relres);
+        }
       } else if (V == 1)
         pcg<ASM>(a, grid, rs, iters, relres);
       else
@@ -2599,25 +2648,36 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   }
   void (*kern)(FFArgs) = nullptr;
   const bool asm_k = L.assembled;
-  // WFK_PRECISION_FAST: the CG variant of a matrix-free level with fp32 vectors
-  const bool fast = c->precision == WFK_PRECISION_FAST && a.pcg_variant == 1 && !asm_k && L.N > 0 && mode == 0;
-  a.f_r = a.f_p = a.f_s = a.f_u = a.f_d = a.f_dinv = a.f_contrib = a.f_wpart = nullptr;
+  // Matrix-free levels that run the CG variant keep their Krylov vectors
+  // packed (pcg_pk) with WFK_PRECISION_FAST: fp32 xyz (V = 2).  The same code
+  // in fp64 (V = 3, 24-byte vectors; WFK_PACK=1) was measured at configs[4]
+  // and is not faster than the padded fp64 CG (V = 1): the update phase
+  // shrinks (379 K -> 295 K cycles per level-0 iteration) but the unaligned
+  // 24-byte contribution stores and gathers grow the constraint pass
+  // (58 K -> 100 K), 129.7-133.5 vs 130.8 ms -- so fp64 stays padded.
+  static const char* pack_env = getenv("WFK_PACK");
+  const bool cg_mf = a.pcg_variant == 1 && !asm_k && L.N > 0 && mode == 0;
+  const bool fast = c->precision == WFK_PRECISION_FAST && cg_mf;
+  const bool packed64 = !fast && cg_mf && pack_env && pack_env[0] == '1';
   static const bool item1 = getenv("WFK_ITEM1") != nullptr;  // A/B: one item per thread in flight
   a.item2 = item1 ? 0 : 1;
-  if (fast) {
+  a.fv = PackVecs<float>{};
+  a.dv = PackVecs<double>{};
+  auto bind_pack = [&](auto& pv, auto& r, auto& pp, auto& sv, auto& u, auto& d, auto& di, auto& ct, auto& wp) {
     const size_t n3 = 3 * size_t(L.N);
-    a.f_r = L.f_r.ensure(n3);
-    a.f_p = L.f_p.ensure(n3);
-    a.f_s = L.f_s.ensure(n3);
-    a.f_u = L.f_u.ensure(n3);
-    a.f_d = L.f_d.ensure(n3);
-    a.f_dinv = L.f_dinv.ensure(n3);
-    a.f_contrib = L.f_contrib.ensure(3 * size_t(std::max<int64_t>(L.E, 1)));
-    a.f_wpart = L.f_wpart.ensure(3 * (size_t(L.N) + size_t(L.n_xitems) + 1));
-  }
-  if (fast) {
-    // two items in flight per thread need the registers of a 256-thread block
-    kern = k_flip_flop<2, false, kSlotVecs, kFastBlock>;
+    pv.r = r.ensure(n3);
+    pv.p = pp.ensure(n3);
+    pv.s = sv.ensure(n3);
+    pv.u = reinterpret_cast<decltype(pv.u)>(u.ensure(4 * size_t(L.N)));
+    pv.d = d.ensure(n3);
+    pv.dinv = di.ensure(n3);
+    pv.contrib = ct.ensure(3 * size_t(std::max<int64_t>(L.E, 1)));
+    pv.wpart = wp.ensure(3 * (size_t(L.N) + size_t(L.n_xitems) + 1));
+  };
+  if (fast) bind_pack(a.fv, L.f_r, L.f_p, L.f_s, L.f_u, L.f_d, L.f_dinv, L.f_contrib, L.f_wpart);
+  if (packed64) bind_pack(a.dv, L.d_r, L.d_p, L.d_s, L.d_u, L.d_d, L.d_dinv, L.d_contrib, L.d_wpart);
+  if (fast || packed64) {
+    kern = fast ? k_flip_flop<2, false, kSlotVecs, kFastBlock> : k_flip_flop<3, false, kSlotVecs, kFastBlock>;
     tpb = kFastBlock;
   }
   else if (a.pcg_variant == 1)

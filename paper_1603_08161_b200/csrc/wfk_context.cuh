@@ -148,6 +148,8 @@ struct Level {
   DevBuf<int32_t> cnt;
   // WFK_PRECISION_FAST Chronopoulos-Gear PCG: fp32 Krylov vectors (packed xyz)
   DevBuf<float> f_r, f_p, f_s, f_u, f_d, f_dinv, f_contrib, f_wpart;
+  // the same packed in fp64 (the default for large CG levels)
+  DevBuf<double> d_r, d_p, d_s, d_u, d_d, d_dinv, d_contrib, d_wpart;
   // explicit normal equations of the slab-partitioned solve (solver_c2f_dist)
   DevBuf<double> ne_blocks, ne_rhs, ne_x;
   DevBuf<int32_t> ne_cols;

@@ -421,3 +421,22 @@ def test_fast_precision_cg_parity(ctx, monkeypatch):
     act = ref.active.astype(bool)
     dev = np.max(np.linalg.norm(v.deformed[act] - ref.deformed[act], axis=1)) / v.voxel_size
     assert dev <= 1e-3, dev
+
+
+def test_packed_fp64_cg_parity(ctx, monkeypatch):
+    """The packed fp64 Chronopoulos-Gear PCG (24-byte xyz vectors; WFK_PACK=1,
+    an option -- measured no faster than the padded fp64 CG at configs[4])
+    against the reference: fp64 throughout, so the fp64 parity bars apply."""
+    v = make_volume(32)
+    cons = random_dense_constraints(v, 3000, seed=13)
+    p = SolverParams.make()
+    pose = Pose.make(O.euler_to_matrix((0.0, 0.01, 0.0)), (0.005, 0, 0))
+    ref = v.copy()
+    tr = O.solve_coarse_to_fine(ref, pose, cons, p)
+    monkeypatch.setenv("WFK_PCG", "cg")
+    monkeypatch.setenv("WFK_PACK", "1")
+    ctx.upload_volume(v)
+    ctx.upload_constraints(cons)
+    tg = ctx.solve_coarse_to_fine(pose, p)
+    ctx.download_volume(v)
+    compare_solves(v, ref, tg, tr)
