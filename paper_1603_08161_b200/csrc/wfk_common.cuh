@@ -21,7 +21,10 @@ constexpr int kBlock = 256;
 constexpr int kCoopBlock = 512;     // persistent cooperative kernels: 1 block / SM
 constexpr int kCoopBlockShared = 384;  // the flip-flop kernel with its row state in shared memory
 constexpr int kAssembleRatio = 32; // incidences per row above which B^T B is assembled
-constexpr int kAsmLanes = 8;        // lanes per row on small assembled levels (27 stencil slots)
+#ifndef WFK_ASM_LANES
+#define WFK_ASM_LANES 8
+#endif
+constexpr int kAsmLanes = WFK_ASM_LANES;  // lanes per row on small assembled levels (27 stencil slots)
 constexpr int kAsmThreadRows = 16384;  // rows from which assembled levels put one row per lane
 #ifndef WFK_MF_LANES
 #define WFK_MF_LANES 2
