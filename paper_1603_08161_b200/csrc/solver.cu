@@ -220,15 +220,34 @@ __global__ void __launch_bounds__(W * 32) k_assemble_rows(
     const int32_t* c_kind, double* blk, int32_t* cols, int soa, double4* crhs, double4* cdiag) {
   struct Stage {
     double sc[32], a[32], gx[32], gy[32], gz[32], cb[32];
+    double ggt[6][32];  // g g^T (xx xy xz yy yz zz) of the staged incidences, formed once
     double w[8][33];
     int k[32], dense[32];
   };
-  __shared__ Stage st_all[W];
-  __shared__ double part[W][28][6];
+  // the warps' partial blocks reuse the staging memory once every warp is done
+  // with its chunks (48 KB static shared memory at W = 8)
+  union Smem {
+    Stage st[W];
+    double part[W][28][6];
+  };
+  __shared__ Smem sm;
+  auto& part = sm.part;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  Stage& st = st_all[warp];
+  Stage& st = sm.st[warp];
   const int s = lane;
   const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = s / 9 - 1;
+  // per corner ki of the row inside an incidence: does stencil slot s pair it
+  // with a corner of the same cell, and which (bit k of vmask, 3-bit field k
+  // of widx)
+  unsigned vmask = 0, widx = 0;
+#pragma unroll
+  for (int ki = 0; ki < 8; ++ki) {
+    const int ox = (ki & 1) + dx, oy = ((ki >> 1) & 1) + dy, oz = (ki >> 2) + dz;
+    if (ox >= 0 && ox <= 1 && oy >= 0 && oy <= 1 && oz >= 0 && oz <= 1) {
+      vmask |= 1u << ki;
+      widx |= unsigned(ox + 2 * oy + 4 * oz) << (3 * ki);
+    }
+  }
   for (int r = blockIdx.x; r < N; r += gridDim.x) {
     double b[6] = {0, 0, 0, 0, 0, 0};  // slot block (s < 27) | rhs xyz, diag xyz (s == 27)
     const int e0 = row_ptr[r], e1 = row_ptr[r + 1];
@@ -245,6 +264,15 @@ __global__ void __launch_bounds__(W * 32) k_assemble_rows(
         st.gz[lane] = c_g[4 * c + 2];
         st.cb[lane] = c_b[c];
         st.dense[lane] = c_kind[c] == WFK_DENSE_PLANE;
+        {
+          const double gx = st.gx[lane], gy = st.gy[lane], gz = st.gz[lane];
+          st.ggt[0][lane] = gx * gx;
+          st.ggt[1][lane] = gx * gy;
+          st.ggt[2][lane] = gx * gz;
+          st.ggt[3][lane] = gy * gy;
+          st.ggt[4][lane] = gy * gz;
+          st.ggt[5][lane] = gz * gz;
+        }
 #pragma unroll
         for (int k = 0; k < 8; ++k) st.w[k][lane] = c_w[8 * int64_t(c) + k];
       }
@@ -253,17 +281,15 @@ __global__ void __launch_bounds__(W * 32) k_assemble_rows(
       if (s < 27) {
         for (int j = 0; j < cnt; ++j) {
           const int ki = st.k[j];
-          const int ox = (ki & 1) + dx, oy = ((ki >> 1) & 1) + dy, oz = (ki >> 2) + dz;
-          if (ox < 0 || ox > 1 || oy < 0 || oy > 1 || oz < 0 || oz > 1) continue;
-          const double sc = st.sc[j] * st.w[ox + 2 * oy + 4 * oz][j];
+          if (!((vmask >> ki) & 1u)) continue;
+          const double sc = st.sc[j] * st.w[(widx >> (3 * ki)) & 7u][j];
           if (st.dense[j]) {
-            const double gx = st.gx[j], gy = st.gy[j], gz = st.gz[j];
-            b[0] += sc * (gx * gx);
-            b[1] += sc * (gx * gy);
-            b[2] += sc * (gx * gz);
-            b[3] += sc * (gy * gy);
-            b[4] += sc * (gy * gz);
-            b[5] += sc * (gz * gz);
+            b[0] += sc * st.ggt[0][j];
+            b[1] += sc * st.ggt[1][j];
+            b[2] += sc * st.ggt[2][j];
+            b[3] += sc * st.ggt[3][j];
+            b[4] += sc * st.ggt[4][j];
+            b[5] += sc * st.ggt[5][j];
           } else {
             b[0] += sc * 1.0;
             b[3] += sc * 1.0;
@@ -295,6 +321,7 @@ __global__ void __launch_bounds__(W * 32) k_assemble_rows(
       }
       __syncwarp();
     }
+    __syncthreads();  // every warp is done with the staging memory
     if (s < 28)
 #pragma unroll
       for (int m = 0; m < 6; ++m) part[warp][s][m] = b[m];
@@ -2343,6 +2370,7 @@ static void level_rows(wfk_ctx* c, Level& L) {
 // rows, frozen rows, incidence transpose and the constraint cache.  No host
 // synchronisation: the incidence count E stays on the device (row_ptr[N]) and
 // every launch is sized by the bound 8C.
+static void trace_mark(const char* n);
 static void level_constraints(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_params& p) {
   cudaStream_t s = c->stream;
   const int64_t C = L.C;
@@ -2375,6 +2403,7 @@ static void level_constraints(wfk_ctx* c, Level& L, const PoseD& pose, const wfk
     WFK_CUDA(cudaMemsetAsync(L.row_ptr.p, 0, sizeof(int32_t), s));
     return;
   }
+  trace_mark(" prep");
   k_frozen<<<grid_for(N), kBlock, 0, s>>>(N, L.uf, L.comp_flag, L.frozen);
   count_launch(c);
   if (C > 0) {
@@ -2395,6 +2424,7 @@ static void level_constraints(wfk_ctx* c, Level& L, const PoseD& pose, const wfk
   } else {
     WFK_CUDA(cudaMemsetAsync(L.row_ptr.p, 0, size_t(N + 1) * sizeof(int32_t), s));
   }
+  trace_mark(" sort");
   // Rows carrying many constraint incidences (coarse levels, where every
   // constraint of the frame lands on a few thousand nodes) get their B^T B
   // assembled once per solve, so the PCG row pass is a fixed 27-block stencil;
