@@ -207,143 +207,230 @@ __global__ void k_item_write(int N, const int32_t* row_ptr, const int32_t* xptr,
 }
 
 // Assembled levels: B^T B (solver.cpp:196-226) and the ConstraintCache
-// (solver.hpp:66-70) of one row per block.  Warp w takes the row's incidence
-// chunks w, w + 8, ... (32 incidences each): its lanes stage a chunk in shared
-// memory (corner, coef a_i, a_i, g, c_b, kind, the constraint's 8 weights),
-// then lane s < 27 accumulates stencil slot s and lane 27 the cache terms over
-// the staged incidences in incidence order; the 8 warps' partials are summed
-// in warp order (deterministic).  The row's incidence data is read once.
-template <int W>
-__global__ void __launch_bounds__(W * 32) k_assemble_rows(
+// (solver.hpp:66-70).  A block of kAsmWarps warps takes its rows in groups
+// of kAsmWarps: a row with at most kAsmLong incidences is summed by one warp,
+// a longer one by all warps of the block on contiguous segments whose
+// partials are added in segment order (deterministic).  Inside a segment every
+// value is summed sequentially in incidence order (cell order,
+// solver.cpp:185-195).  The incidences are sorted by the row's corner ki
+// inside the cell, so a run of equal ki touches the same 8 stencil slots:
+// lane 3j + p (j < 8, p < 3) owns values 2p, 2p + 1 of the slot pairing the
+// row with cell corner j, keeps them in registers for the run and swaps them
+// through the warp's slot table when ki changes; lanes 24..29 own the six
+// cache terms (rhs xyz, diagonal xyz).  Every lane runs the same
+// instruction stream -- acc += (P w) Q with P, w, Q picked from the staged
+// incidence by a per-lane column (1.0 / 0.0 columns stand for the terms a
+// kind does not have) -- and the next chunk's incidences are loaded while
+// the current one is summed.
+constexpr int kAsmWarps = 8;
+constexpr int kAsmLong = 128;  // rows above this many incidences are split over the block
+enum { kTsc, kTsd, kTnf, kTggt, kTg = kTggt + 6, kTone = kTg + 3, kTzero, kTcols };
+struct AsmStage {
+  double t[kTcols][33];  // sc = coef a, sd = coef a^2, -coef a c_b, g g^T, g, 1, 0
+  double w[9][33];       // the constraint's 8 corner weights, 1
+  int k[32], dense[32];
+  double acc[28][6];     // the segment's slot blocks (27) and cache terms (row 27)
+};
+constexpr size_t kAsmSmem = sizeof(AsmStage) * kAsmWarps;
+__device__ __forceinline__ int asm_slot(int ki, int j) {
+  return ((j & 1) - (ki & 1) + 1) + 3 * (((j >> 1) & 1) - ((ki >> 1) & 1) + 1) + 9 * ((j >> 2) - (ki >> 2) + 1);
+}
+struct AsmCon {  // one incidence's constraint data in flight
+  int k, dense;
+  double a, coef, cb, g[3], w[8];
+};
+struct AsmIn {
+  const int32_t* ent_con;
+  const uint8_t* ent_k;
+  const double *ent_w, *c_w, *c_g, *c_b;
+  const int32_t* c_kind;
+};
+__device__ __forceinline__ void asm_load(const AsmIn& in, int e, int c, AsmCon& x) {
+  x.k = in.ent_k[e];
+  x.a = in.ent_w[e];
+  x.g[0] = in.c_g[4 * c];
+  x.g[1] = in.c_g[4 * c + 1];
+  x.g[2] = in.c_g[4 * c + 2];
+  x.coef = in.c_g[4 * c + 3];
+  x.cb = in.c_b[c];
+  x.dense = in.c_kind[c] == WFK_DENSE_PLANE;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x.w[k] = in.c_w[8 * int64_t(c) + k];
+}
+// Sums incidences [s0, s1) of one row into st.acc (zeroed here).
+__device__ __forceinline__ void asm_segment(const AsmIn& in, AsmStage& st, int s0, int s1) {
+  const int L = threadIdx.x & 31;
+  const int j = L / 3, pm = L % 3, cm = L - 24;
+  // per-lane columns: (P, w, Q0, Q1) for a dense-plane and for a point incidence
+  int pD, pN, wc, q0D, q0N, q1D, q1N;
+  if (L < 24) {
+    pD = pN = kTsc;
+    wc = j;
+    q0D = kTggt + 2 * pm;
+    q1D = kTggt + 2 * pm + 1;
+    q0N = pm == 0 ? kTone : kTzero;  // point: B^T B gains coef a_i a_j I (xx, yy, zz)
+    q1N = pm == 0 ? kTzero : kTone;
+  } else if (cm < 3) {
+    pD = kTnf;
+    pN = kTsc;
+    wc = 8;
+    q0D = q0N = kTg + cm;
+    q1D = q1N = kTzero;
+  } else if (cm < 6) {
+    pD = pN = kTsd;
+    wc = 8;
+    q0D = kTggt + (cm == 3 ? 0 : cm == 4 ? 3 : 5);
+    q0N = kTone;
+    q1D = q1N = kTzero;
+  } else {
+    pD = pN = kTzero;
+    wc = 8;
+    q0D = q0N = q1D = q1N = kTzero;
+  }
+  for (int t = L; t < 28 * 6; t += 32) (&st.acc[0][0])[t] = 0.0;
+  double a0 = 0, a1 = 0;
+  int cur = -1;
+  AsmCon nx;
+  int c_next = -1;
+  if (s0 + L < s1) {
+    asm_load(in, s0 + L, in.ent_con[s0 + L], nx);
+  }
+  if (s0 + 32 + L < s1) c_next = in.ent_con[s0 + 32 + L];
+  for (int base = s0; base < s1; base += 32) {
+    __syncwarp();
+    if (base + L < s1) {  // stage this chunk
+      const double sc = nx.coef * nx.a;
+      st.k[L] = nx.k;
+      st.dense[L] = nx.dense;
+      st.t[kTsc][L] = sc;
+      st.t[kTsd][L] = sc * nx.a;
+      st.t[kTnf][L] = -(sc * nx.cb);
+      st.t[kTggt + 0][L] = nx.g[0] * nx.g[0];
+      st.t[kTggt + 1][L] = nx.g[0] * nx.g[1];
+      st.t[kTggt + 2][L] = nx.g[0] * nx.g[2];
+      st.t[kTggt + 3][L] = nx.g[1] * nx.g[1];
+      st.t[kTggt + 4][L] = nx.g[1] * nx.g[2];
+      st.t[kTggt + 5][L] = nx.g[2] * nx.g[2];
+      st.t[kTg + 0][L] = nx.g[0];
+      st.t[kTg + 1][L] = nx.g[1];
+      st.t[kTg + 2][L] = nx.g[2];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) st.w[k][L] = nx.w[k];
+    }
+    // the next chunk's data in flight while this one is summed
+    if (base + 32 + L < s1) asm_load(in, base + 32 + L, c_next, nx);
+    if (base + 64 + L < s1) c_next = in.ent_con[base + 64 + L];
+    __syncwarp();
+    const int n = min(32, s1 - base);
+    // runs of equal ki inside the chunk (the incidences are sorted by ki)
+    const unsigned brk = __ballot_sync(0xffffffffu, L < n && (L == 0 || st.k[L] != st.k[L - 1])) | (n < 32 ? 1u << n : 0u);
+    for (int i = 0; i < n;) {
+      const int ki = st.k[i];
+      const unsigned rest = brk & ~((2u << i) - 1u);
+      const int iend = rest ? __ffs(rest) - 1 : 32;
+      if (ki != cur) {  // warp-uniform: a new run of the row's corner
+        if (cur >= 0 && L < 24) {
+          double* q = st.acc[asm_slot(cur, j)];
+          q[2 * pm] = a0;
+          q[2 * pm + 1] = a1;
+        }
+        __syncwarp();
+        if (L < 24) {
+          const double* q = st.acc[asm_slot(ki, j)];
+          a0 = q[2 * pm];
+          a1 = q[2 * pm + 1];
+        }
+        cur = ki;
+      }
+#pragma unroll 4
+      for (int ii = i; ii < iend; ++ii) {
+        const bool dn = st.dense[ii] != 0;
+        const double P = st.t[dn ? pD : pN][ii] * st.w[wc][ii];
+        a0 += P * st.t[dn ? q0D : q0N][ii];
+        a1 += P * st.t[dn ? q1D : q1N][ii];
+      }
+      i = iend;
+    }
+  }
+  __syncwarp();
+  if (L < 24) {
+    if (cur >= 0) {
+      double* q = st.acc[asm_slot(cur, j)];
+      q[2 * pm] = a0;
+      q[2 * pm + 1] = a1;
+    }
+  } else if (cm < 6) {
+    st.acc[27][cm] = a0;
+  }
+  __syncwarp();
+}
+// acc (28 x 6, summed over `nseg` stage tables in order) -> the row's outputs;
+// threads [0, nthr) of the caller take part
+__device__ __forceinline__ void asm_write(const AsmStage* stages, int nseg, int tid, int nthr, const Grid& g, int N,
+                                          int r, const int32_t* rows, const int32_t* node_row, double* blk,
+                                          int32_t* cols, int soa, double4* crhs, double4* cdiag) {
+  for (int t = tid; t < 28 * 6; t += nthr) {
+    const int s = t / 6, m = t % 6;
+    double v = stages[0].acc[s][m];
+    for (int w = 1; w < nseg; ++w) v += stages[w].acc[s][m];
+    if (s < 27) {
+      blk[soa ? (int64_t(s) * 6 + m) * N + r : int64_t(r) * 27 * 6 + t] = v;
+    } else {
+      double* out = reinterpret_cast<double*>(m < 3 ? &crhs[r] : &cdiag[r]);
+      out[m % 3] = v;
+      if (m % 3 == 0) out[3] = 0.0;
+    }
+  }
+  if (tid < 27) {
+    const int dx = tid % 3 - 1, dy = (tid / 3) % 3 - 1, dz = tid / 9 - 1;
+    int x, y, z;
+    g.idx3(rows[r], x, y, z);
+    const int col = g.in_grid(x + dx, y + dy, z + dz) ? node_row[g.lin(x + dx, y + dy, z + dz)] : -1;
+    cols[soa ? int64_t(tid) * N + r : int64_t(r) * 27 + tid] = col;
+  }
+}
+__global__ void __launch_bounds__(kAsmWarps * 32, 2) k_assemble_rows(
     Grid g, int N, const int32_t* rows, const int32_t* node_row, const int32_t* row_ptr, const int32_t* ent_con,
     const uint8_t* ent_k, const double* ent_w, const double* c_w, const double* c_g, const double* c_b,
     const int32_t* c_kind, double* blk, int32_t* cols, int soa, double4* crhs, double4* cdiag) {
-  struct Stage {
-    double sc[32], a[32], gx[32], gy[32], gz[32], cb[32];
-    double ggt[6][32];  // g g^T (xx xy xz yy yz zz) of the staged incidences, formed once
-    double w[8][33];
-    int k[32], dense[32];
-  };
-  // the warps' partial blocks reuse the staging memory once every warp is done
-  // with its chunks (48 KB static shared memory at W = 8)
-  union Smem {
-    Stage st[W];
-    double part[W][28][6];
-  };
-  __shared__ Smem sm;
-  auto& part = sm.part;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  Stage& st = sm.st[warp];
-  const int s = lane;
-  const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = s / 9 - 1;
-  // per corner ki of the row inside an incidence: does stencil slot s pair it
-  // with a corner of the same cell, and which (bit k of vmask, 3-bit field k
-  // of widx)
-  unsigned vmask = 0, widx = 0;
-#pragma unroll
-  for (int ki = 0; ki < 8; ++ki) {
-    const int ox = (ki & 1) + dx, oy = ((ki >> 1) & 1) + dy, oz = (ki >> 2) + dz;
-    if (ox >= 0 && ox <= 1 && oy >= 0 && oy <= 1 && oz >= 0 && oz <= 1) {
-      vmask |= 1u << ki;
-      widx |= unsigned(ox + 2 * oy + 4 * oz) << (3 * ki);
-    }
+  extern __shared__ double4 asm_smem[];
+  AsmStage* stages = reinterpret_cast<AsmStage*>(asm_smem);
+  __shared__ int grp[kAsmWarps][2];
+  const int warp = threadIdx.x >> 5, L = threadIdx.x & 31;
+  AsmStage& st = stages[warp];
+  const AsmIn in{ent_con, ent_k, ent_w, c_w, c_g, c_b, c_kind};
+  for (int k = L; k < 32; k += 32) {  // constant columns
+    st.t[kTone][k] = 1.0;
+    st.t[kTzero][k] = 0.0;
+    st.w[8][k] = 1.0;
   }
-  for (int r = blockIdx.x; r < N; r += gridDim.x) {
-    double b[6] = {0, 0, 0, 0, 0, 0};  // slot block (s < 27) | rhs xyz, diag xyz (s == 27)
-    const int e0 = row_ptr[r], e1 = row_ptr[r + 1];
-    for (int base = e0 + 32 * warp; base < e1; base += 32 * W) {
-      const int e = base + lane;
-      if (e < e1) {
-        const int c = ent_con[e];
-        const double ai = ent_w[e];
-        st.k[lane] = ent_k[e];
-        st.a[lane] = ai;
-        st.sc[lane] = c_g[4 * c + 3] * ai;
-        st.gx[lane] = c_g[4 * c];
-        st.gy[lane] = c_g[4 * c + 1];
-        st.gz[lane] = c_g[4 * c + 2];
-        st.cb[lane] = c_b[c];
-        st.dense[lane] = c_kind[c] == WFK_DENSE_PLANE;
-        {
-          const double gx = st.gx[lane], gy = st.gy[lane], gz = st.gz[lane];
-          st.ggt[0][lane] = gx * gx;
-          st.ggt[1][lane] = gx * gy;
-          st.ggt[2][lane] = gx * gz;
-          st.ggt[3][lane] = gy * gy;
-          st.ggt[4][lane] = gy * gz;
-          st.ggt[5][lane] = gz * gz;
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) st.w[k][lane] = c_w[8 * int64_t(c) + k];
-      }
-      __syncwarp();
-      const int cnt = min(32, e1 - base);
-      if (s < 27) {
-        for (int j = 0; j < cnt; ++j) {
-          const int ki = st.k[j];
-          if (!((vmask >> ki) & 1u)) continue;
-          const double sc = st.sc[j] * st.w[(widx >> (3 * ki)) & 7u][j];
-          if (st.dense[j]) {
-            b[0] += sc * st.ggt[0][j];
-            b[1] += sc * st.ggt[1][j];
-            b[2] += sc * st.ggt[2][j];
-            b[3] += sc * st.ggt[3][j];
-            b[4] += sc * st.ggt[4][j];
-            b[5] += sc * st.ggt[5][j];
-          } else {
-            b[0] += sc * 1.0;
-            b[3] += sc * 1.0;
-            b[5] += sc * 1.0;
-          }
-        }
-      } else if (s == 27) {
-        // cache_term (solver.cpp:203-226): coef a^2 diag, rhs
-        for (int j = 0; j < cnt; ++j) {
-          const double coef_a = st.sc[j], sd = coef_a * st.a[j];
-          const double gx = st.gx[j], gy = st.gy[j], gz = st.gz[j];
-          if (st.dense[j]) {
-            b[3] += sd * (gx * gx);
-            b[4] += sd * (gy * gy);
-            b[5] += sd * (gz * gz);
-            const double f = coef_a * st.cb[j];
-            b[0] -= f * gx;
-            b[1] -= f * gy;
-            b[2] -= f * gz;
-          } else {
-            b[3] += sd * 1.0;
-            b[4] += sd * 1.0;
-            b[5] += sd * 1.0;
-            b[0] += coef_a * gx;
-            b[1] += coef_a * gy;
-            b[2] += coef_a * gz;
-          }
-        }
-      }
-      __syncwarp();
-    }
-    __syncthreads();  // every warp is done with the staging memory
-    if (s < 28)
-#pragma unroll
-      for (int m = 0; m < 6; ++m) part[warp][s][m] = b[m];
+  // rows b, b + G, b + 2G, ... in groups of kAsmWarps
+  for (int g0 = blockIdx.x; g0 < N; g0 += gridDim.x * kAsmWarps) {
     __syncthreads();
-    if (warp == 0 && s < 28) {
-      double t[6] = {0, 0, 0, 0, 0, 0};
-      for (int w = 0; w < W; ++w)
-#pragma unroll
-        for (int m = 0; m < 6; ++m) t[m] += part[w][s][m];
-      if (s < 27) {
-        int x, y, z;
-        g.idx3(rows[r], x, y, z);
-        const int col = g.in_grid(x + dx, y + dy, z + dz) ? node_row[g.lin(x + dx, y + dy, z + dz)] : -1;
-        const int64_t ta = int64_t(r) * 27 + s;
-        cols[soa ? int64_t(s) * N + r : ta] = col;
-        for (int m = 0; m < 6; ++m) blk[soa ? (int64_t(s) * 6 + m) * N + r : ta * 6 + m] = t[m];
-      } else {
-        crhs[r] = make_double4(t[0], t[1], t[2], 0.0);
-        cdiag[r] = make_double4(t[3], t[4], t[5], 0.0);
-      }
+    if (threadIdx.x < kAsmWarps) {
+      const int r = g0 + int(threadIdx.x) * gridDim.x;
+      grp[threadIdx.x][0] = r < N ? row_ptr[r] : 0;
+      grp[threadIdx.x][1] = r < N ? row_ptr[r + 1] : 0;
     }
     __syncthreads();
+    // long rows of the group: every warp one segment
+    for (int q = 0; q < kAsmWarps; ++q) {
+      const int r = g0 + q * gridDim.x;
+      const int e0 = grp[q][0], e1 = grp[q][1];
+      if (r >= N || e1 - e0 <= kAsmLong) continue;  // block-uniform
+      const int seglen = (e1 - e0 + kAsmWarps - 1) / kAsmWarps;
+      asm_segment(in, st, min(e1, e0 + warp * seglen), min(e1, e0 + (warp + 1) * seglen));
+      __syncthreads();
+      asm_write(stages, kAsmWarps, threadIdx.x, blockDim.x, g, N, r, rows, node_row, blk, cols, soa, crhs, cdiag);
+      __syncthreads();
+    }
+    // short rows: warp q sums row q of the group alone
+    const int r = g0 + warp * gridDim.x;
+    const int e0 = grp[warp][0], e1 = grp[warp][1];
+    if (r < N && e1 - e0 <= kAsmLong) {
+      asm_segment(in, st, e0, e1);
+      asm_write(&st, 1, L, 32, g, N, r, rows, node_row, blk, cols, soa, crhs, cdiag);
+    }
   }
 }
 
@@ -2457,21 +2544,14 @@ static void level_constraints(wfk_ctx* c, Level& L, const PoseD& pose, const wfk
     const int soa = N >= kAsmThreadRows ? 1 : 0;  // rows on lanes read slot-major blocks
     L.blk.ensure(size_t(N) * 27 * 6);
     L.cols.ensure(size_t(N) * 27);
-    // warps per row ~ incidence chunks per row (bound 8C / N)
-    const int64_t chunks = (E8 / std::max(N, 1) + 31) / 32;
-    auto launch = [&](auto kern, int W) {
-      kern<<<std::min(N, c->num_sms * (64 / W)), W * 32, 0, s>>>(L.g, N, L.rows, L.node_row, L.row_ptr, L.ent_con,
-                                                                 L.ent_k, L.ent_w, L.c_w, L.c_g, L.c_b, L.c_kind,
-                                                                 L.blk, L.cols, soa, L.crhs, L.cdiag);
-    };
-    if (chunks <= 1)
-      launch(k_assemble_rows<1>, 1);
-    else if (chunks <= 2)
-      launch(k_assemble_rows<2>, 2);
-    else if (chunks <= 4)
-      launch(k_assemble_rows<4>, 4);
-    else
-      launch(k_assemble_rows<8>, 8);
+    static unsigned long long asm_attr = 0;  // bit d: device d configured
+    if (!(asm_attr & (1ull << (c->device & 63)))) {
+      WFK_CUDA(cudaFuncSetAttribute(k_assemble_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kAsmSmem)));
+      asm_attr |= 1ull << (c->device & 63);
+    }
+    k_assemble_rows<<<std::min((N + kAsmWarps - 1) / kAsmWarps, c->num_sms * 2), kAsmWarps * 32, kAsmSmem, s>>>(
+        L.g, N, L.rows, L.node_row, L.row_ptr, L.ent_con, L.ent_k, L.ent_w, L.c_w, L.c_g, L.c_b, L.c_kind, L.blk,
+        L.cols, soa, L.crhs, L.cdiag);
     count_launch(c);
   }
   WFK_CUDA(cudaGetLastError());
