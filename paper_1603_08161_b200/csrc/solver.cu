@@ -598,8 +598,11 @@ struct AlignedOf<float> {
 };
 template <class S>
 struct PackVecs {
-  S *r, *p, *s, *d, *dinv, *contrib, *wpart;
-  typename AlignedOf<S>::type* u;  // gathered by both matvec passes: aligned, not packed
+  S *r, *p, *s, *d, *dinv, *wpart;  // streamed row by row: packed xyz
+  typename AlignedOf<S>::type* u;   // gathered by both matvec passes: aligned, not packed
+  // scattered by the constraint pass (one store per incidence): aligned, so
+  // each store is one sector
+  typename AlignedOf<S>::type* contrib;
 };
 
 struct FFArgs {
@@ -1230,8 +1233,8 @@ __device__ __forceinline__ void matvec_constraints_pk(const FFArgs& a, const VT*
 // thread: at ~47 items per thread (3.6 M rows) the pass is a chain of
 // dependent loads (item -> neighbour table -> gathers), so every load of both
 // items is issued before any of their arithmetic.
-template <class VT, class CT, class Sink>
-__device__ __forceinline__ void item_pass2(const FFArgs& a, const VT* v, CT* contrib, CT* wpart, Sink& sink) {
+template <class VT, class CT, class WT, class Sink>
+__device__ __forceinline__ void item_pass2(const FFArgs& a, const VT* v, CT* contrib, WT* wpart, Sink& sink) {
   const double w2 = 2.0 * a.w_r;
   const int total = a.N + a.n_xitems;
   const int st = int(gstride());
@@ -2758,17 +2761,18 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   }
   void (*kern)(FFArgs) = nullptr;
   const bool asm_k = L.assembled;
-  // Matrix-free levels that run the CG variant keep their Krylov vectors
-  // packed (pcg_pk) with WFK_PRECISION_FAST: fp32 xyz (V = 2).  The same code
-  // in fp64 (V = 3, 24-byte vectors; WFK_PACK=1) was measured at configs[4]
-  // and is not faster than the padded fp64 CG (V = 1): the update phase
-  // shrinks (379 K -> 295 K cycles per level-0 iteration) but the unaligned
-  // 24-byte contribution stores and gathers grow the constraint pass
-  // (58 K -> 100 K), 129.7-133.5 vs 130.8 ms -- so fp64 stays padded.
-  static const char* pack_env = getenv("WFK_PACK");
+  // Matrix-free levels that run the CG variant keep their streamed Krylov
+  // vectors packed (pcg_pk): fp64 xyz, 24 B (V = 3), or fp32 xyz, 12 B, with
+  // WFK_PRECISION_FAST (V = 2); the gathered u and the scattered constraint
+  // contributions stay aligned (double4 / float4), one sector per access.
+  // configs[4] level-0 iteration, fp64: padded V = 1 A 58 K, B 264 K,
+  // U 379 K cycles -> packed A 58 K, B 203 K, U 309 K (130.6 -> 119.3 ms per
+  // frame-1 solve); fast: A 67 K -> 50 K with aligned contributions
+  // (108.5 -> 102.8 ms).  WFK_PACK=0 selects the padded fp64 CG.
+  const char* pack_env = getenv("WFK_PACK");  // per call: tests switch it
   const bool cg_mf = a.pcg_variant == 1 && !asm_k && L.N > 0 && mode == 0;
   const bool fast = c->precision == WFK_PRECISION_FAST && cg_mf;
-  const bool packed64 = !fast && cg_mf && pack_env && pack_env[0] == '1';
+  const bool packed64 = !fast && cg_mf && !(pack_env && pack_env[0] == '0');
   static const bool item1 = getenv("WFK_ITEM1") != nullptr;  // A/B: one item per thread in flight
   a.item2 = item1 ? 0 : 1;
   a.fv = PackVecs<float>{};
@@ -2781,7 +2785,7 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
     pv.u = reinterpret_cast<decltype(pv.u)>(u.ensure(4 * size_t(L.N)));
     pv.d = d.ensure(n3);
     pv.dinv = di.ensure(n3);
-    pv.contrib = ct.ensure(3 * size_t(std::max<int64_t>(L.E, 1)));
+    pv.contrib = reinterpret_cast<decltype(pv.contrib)>(ct.ensure(4 * size_t(std::max<int64_t>(L.E, 1))));
     pv.wpart = wp.ensure(3 * (size_t(L.N) + size_t(L.n_xitems) + 1));
   };
   if (fast) bind_pack(a.fv, L.f_r, L.f_p, L.f_s, L.f_u, L.f_d, L.f_dinv, L.f_contrib, L.f_wpart);

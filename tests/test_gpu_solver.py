@@ -423,10 +423,12 @@ def test_fast_precision_cg_parity(ctx, monkeypatch):
     assert dev <= 1e-3, dev
 
 
-def test_packed_fp64_cg_parity(ctx, monkeypatch):
-    """The packed fp64 Chronopoulos-Gear PCG (24-byte xyz vectors; WFK_PACK=1,
-    an option -- measured no faster than the padded fp64 CG at configs[4])
-    against the reference: fp64 throughout, so the fp64 parity bars apply."""
+@pytest.mark.parametrize("pack", ["1", "0"])
+def test_packed_fp64_cg_parity(ctx, monkeypatch, pack):
+    """The Chronopoulos-Gear PCG of matrix-free levels in both fp64 storages --
+    packed 24-byte xyz vectors (the default, WFK_PACK unset or 1) and 32-byte
+    padded ones (WFK_PACK=0) -- against the reference: fp64 throughout, so the
+    fp64 parity bars apply."""
     v = make_volume(32)
     cons = random_dense_constraints(v, 3000, seed=13)
     p = SolverParams.make()
@@ -434,7 +436,7 @@ def test_packed_fp64_cg_parity(ctx, monkeypatch):
     ref = v.copy()
     tr = O.solve_coarse_to_fine(ref, pose, cons, p)
     monkeypatch.setenv("WFK_PCG", "cg")
-    monkeypatch.setenv("WFK_PACK", "1")
+    monkeypatch.setenv("WFK_PACK", pack)
     ctx.upload_volume(v)
     ctx.upload_constraints(cons)
     tg = ctx.solve_coarse_to_fine(pose, p)
