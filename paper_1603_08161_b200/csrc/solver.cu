@@ -605,6 +605,30 @@ struct PackVecs {
   typename AlignedOf<S>::type* contrib;
 };
 
+// the Chronopoulos-Gear PCG of a matrix-free level cut into
+// S z-slab ranks inside the persistent kernel (pcg_slab).  Every pointer a
+// rank reaches another rank through is an array entry per rank -- on one GPU
+// (S virtual ranks = block groups of one cooperative launch) they point into
+// one allocation; across GPUs they are peer pointers to the other GPUs'
+// buffers.  The rows are cut into tiles of T rows; a rank owns a contiguous
+// range of tiles (a z-slab, balanced by work), and every dot product is summed
+// per tile (fixed thread -> row map and block tree) and then over the tiles in
+// tile order, so the result does not depend on S or on which block ran a tile.
+struct SlabDev {
+  int S;                           // ranks; 0 = not partitioned
+  int T, ntiles;                   // rows per tile, tiles
+  const int32_t* rank_tile;        // S + 1: rank s owns tiles [rank_tile[s], rank_tile[s + 1])
+  const int32_t* win_lo;           // S: first row of rank s's u window (own rows + halo)
+  const int32_t* win_hi;           // S
+  double4* const* uwin;            // S: u window of each rank, rows [win_lo[s], win_hi[s])
+  const int32_t* con_ptr;          // S + 1: constraints incident to a rank's rows ...
+  const int32_t* con_list;         // ... (a constraint straddling two slabs is in both lists)
+  unsigned* const* ctr;            // S: per rank [0] rank arrivals, [32] halo pushes from below,
+                                   //    [64] halo pushes from above, [96] reduction arrivals
+  unsigned long long* const* part; // S: 2 x ntiles x 8 flag-embedded tile-partial words
+  unsigned long long* const* tot;  // S: 2 x 8 flag-embedded totals
+};
+
 struct FFArgs {
   Grid g;
   int N;
@@ -660,6 +684,7 @@ struct FFArgs {
   PackVecs<double> dv;
   int item2;  // Chronopoulos-Gear item pass with two items in flight per thread
   int cluster2;  // launched in 2-CTA clusters: one grid-barrier arrival per cluster
+  SlabDev slab;  // V = 4: slab-partitioned CG
   // outputs
   double* partials;  // 4 slots x gridDim
   unsigned* sync_count;  // grid barrier arrival counter (own 128 B line)
@@ -673,6 +698,9 @@ struct FFArgs {
 
 struct Red {
   unsigned gen = 0;  // generation of the grid barrier this block has passed
+  // slab-partitioned CG: rank barriers, halo epochs and all-reduces this block
+  // has passed in the launch (the counters are reset once per launch)
+  unsigned sl_gen = 0, sl_epoch = 0, sl_seq = 0;
 };
 
 // Diagnostic phase clock: thread 0 of every block accumulates SM cycles per
@@ -755,6 +783,14 @@ __device__ __forceinline__ unsigned atom_add_acq_rel_u32(unsigned* p, unsigned v
   unsigned old;
   asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
   return old;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
 // 2-CTA clusters (a.cluster2): the pair meets at a cluster barrier (release /
@@ -1417,6 +1453,389 @@ __device__ void pcg_pk(const FFArgs& a, Red& rs, int& iters, double& relres) {
 //   A  constraint pass of A u (matrix-free levels only)    -> barrier
 //   B  item pass (matrix-free) | row pass (assembled)      -> reduction
 // The stopping rule, breakdown test and iteration count are the reference's.
+// ---- slab-partitioned CG (V = 4) ---------------------------------------------
+// pcg_pk<double> with the rows cut into S ranks.  Per iteration a rank
+//   U: updates the rows of its tiles; writes u into its own window and pushes
+//      the rows a neighbour's window covers into that neighbour's window;
+//      writes the tile partials (r.u, r.r) into every rank's partial array;
+//   signals "pushed" to both neighbours and waits for its own blocks and for
+//      both neighbours' pushes (no grid barrier);
+//   A: the constraint pass over the constraints incident to its rows (spread
+//      over all of the rank's threads), writing only its own rows' incidence
+//      slots (straddling constraints are evaluated by both ranks, identically);
+//   rank barrier;
+//   B: the item pass over its tiles' items (u of halo rows from its window);
+//      tile partials (w.u) into every rank's array;
+//   all-reduce: every block arrives on every rank's counter; each rank's first
+//      block sums the tile partials in tile order and publishes the totals.
+// Scopes are gpu (one GPU); a multi-GPU build uses the same code at sys scope.
+struct SlabRank {
+  int s, S, G, b0, nb;  // rank, ranks, blocks, first block, blocks of the rank
+  int t0, t1;           // own tiles
+  int lo, hi, wlo;      // own rows, window start
+  double4* uw;          // own window
+};
+__device__ __forceinline__ int slab_bstart(int s, int S, int G) { return int((int64_t(s) * G) / S); }
+__device__ __forceinline__ SlabRank slab_rank(const FFArgs& a) {
+  SlabRank k;
+  k.S = a.slab.S;
+  k.G = gridDim.x;
+  int s = int((int64_t(blockIdx.x) * k.S) / k.G);
+  while (s + 1 < k.S && slab_bstart(s + 1, k.S, k.G) <= int(blockIdx.x)) ++s;
+  while (s > 0 && slab_bstart(s, k.S, k.G) > int(blockIdx.x)) --s;
+  k.s = s;
+  k.b0 = slab_bstart(s, k.S, k.G);
+  k.nb = slab_bstart(s + 1, k.S, k.G) - k.b0;
+  k.t0 = a.slab.rank_tile[s];
+  k.t1 = a.slab.rank_tile[s + 1];
+  k.lo = min(a.N, k.t0 * a.slab.T);
+  k.hi = min(a.N, k.t1 * a.slab.T);
+  k.wlo = a.slab.win_lo[s];
+  k.uw = a.slab.uwin[s];
+  return k;
+}
+__device__ __forceinline__ void red_add_release_u32(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void slab_wait_ge(const unsigned* p, unsigned target) {
+  while (int(ld_acquire_u32(p) - target) < 0) {
+  }
+}
+// u of row r as rank k sees it: its own rows and halo rows, all in its window
+WF_D V3 slab_u(const SlabRank& k, int r) { return ld4(k.uw, r - k.wlo); }
+// store u of an own row: own window, and every neighbour window covering it
+__device__ __forceinline__ void slab_put_u(const FFArgs& a, const SlabRank& k, int r, V3 u) {
+  st4(k.uw, r - k.wlo, u);
+  if (k.s > 0 && r < a.slab.win_hi[k.s - 1]) st4(a.slab.uwin[k.s - 1], r - a.slab.win_lo[k.s - 1], u);
+  if (k.s + 1 < k.S && r >= a.slab.win_lo[k.s + 1]) st4(a.slab.uwin[k.s + 1], r - a.slab.win_lo[k.s + 1], u);
+}
+// this block's arrival at its rank, and (after u pushes) at both neighbours
+__device__ __forceinline__ void slab_sync(const FFArgs& a, const SlabRank& k, unsigned& gen, bool halo,
+                                          unsigned& epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (halo) {
+      if (k.s > 0) red_add_release_u32(a.slab.ctr[k.s - 1] + 64, 1u);
+      if (k.s + 1 < k.S) red_add_release_u32(a.slab.ctr[k.s + 1] + 32, 1u);
+    }
+    red_add_release_u32(a.slab.ctr[k.s], 1u);
+    slab_wait_ge(a.slab.ctr[k.s], unsigned(k.nb) * (gen + 1));
+    if (halo) {
+      if (k.s > 0) {
+        const int nbl = k.b0 - slab_bstart(k.s - 1, k.S, k.G);
+        slab_wait_ge(a.slab.ctr[k.s] + 32, unsigned(nbl) * (epoch + 1));
+      }
+      if (k.s + 1 < k.S) {
+        const int nbu = slab_bstart(k.s + 2, k.S, k.G) - slab_bstart(k.s + 1, k.S, k.G);
+        slab_wait_ge(a.slab.ctr[k.s] + 64, unsigned(nbu) * (epoch + 1));
+      }
+    }
+  }
+  gen += 1;
+  if (halo) epoch += 1;
+  __syncthreads();
+}
+// the block's tiles: t0 + (b - b0), + nb, ...
+#define SLAB_TILES(k, t) for (int t = (k).t0 + (int(blockIdx.x) - (k).b0); t < (k).t1; t += (k).nb)
+// block sum of v[j] (j in mask) of one tile -> words 2j, 2j + 1 of the tile in
+// every rank's partial array (tag seq + 1)
+template <int NV>
+__device__ __forceinline__ void slab_tile_put(const FFArgs& a, const SlabRank& k, int t, double (&v)[NV],
+                                              const int (&slot)[NV], unsigned seq) {
+  __shared__ double smem[4 * 32];
+  block_sum<NV>(v, smem);
+  const int lane = threadIdx.x;
+  if (lane < 2 * NV) {
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(v[lane >> 1]);
+    const unsigned half = (lane & 1) ? unsigned(bits >> 32) : unsigned(bits);
+    const unsigned long long word = (unsigned long long)half << 32 | (seq + 1u);
+    const size_t off = (size_t(seq & 1) * a.slab.ntiles + size_t(t)) * 8 + 2 * slot[lane >> 1] + (lane & 1);
+    for (int d = 0; d < k.S; ++d) st_relaxed_u64(a.slab.part[d] + off, word);
+  }
+}
+// all-reduce of NV values over every tile, tile order
+template <int NV>
+__device__ __forceinline__ void slab_allreduce(const FFArgs& a, const SlabRank& k, double (&v)[NV], unsigned seq) {
+  __shared__ double smem[4 * 32];
+  __shared__ double bc[4];
+  __syncthreads();  // every tile word of this block is written
+  if (threadIdx.x == 0)
+    for (int d = 0; d < k.S; ++d) red_add_release_u32(a.slab.ctr[d] + 96, 1u);
+  if (int(blockIdx.x) == k.b0) {
+    // the rank's first block: every block's tiles in, then the fixed-order sum
+    // (thread i: tiles i, i + blockDim, ... in order; then the block tree)
+    if (threadIdx.x == 0) slab_wait_ge(a.slab.ctr[k.s] + 96, unsigned(k.G) * (seq + 1));
+    __syncthreads();
+    const unsigned long long* pw = a.slab.part[k.s] + size_t(seq & 1) * a.slab.ntiles * 8;
+    double t[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) t[j] = 0;
+    for (int tile = threadIdx.x; tile < a.slab.ntiles; tile += blockDim.x) {
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        const unsigned long long lo_w = ld_relaxed_u64(pw + size_t(tile) * 8 + 2 * j);
+        const unsigned long long hi_w = ld_relaxed_u64(pw + size_t(tile) * 8 + 2 * j + 1);
+        t[j] += __longlong_as_double((long long)((hi_w >> 32) << 32 | (lo_w >> 32)));
+      }
+    }
+    block_sum<NV>(t, smem);
+    if (threadIdx.x < 2 * NV) {
+      const unsigned long long bits = (unsigned long long)__double_as_longlong(t[threadIdx.x >> 1]);
+      const unsigned half = (threadIdx.x & 1) ? unsigned(bits >> 32) : unsigned(bits);
+      st_relaxed_u64(a.slab.tot[k.s] + size_t(seq & 1) * 8 + threadIdx.x, (unsigned long long)half << 32 | (seq + 1u));
+    }
+  }
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    unsigned half = 0;
+    if (lane < 2 * NV) {
+      const unsigned long long* w = a.slab.tot[k.s] + size_t(seq & 1) * 8 + lane;
+      unsigned long long x;
+      do {
+        x = ld_relaxed_u64(w);
+      } while (unsigned(x) != seq + 1u);
+      half = unsigned(x >> 32);
+    }
+    const unsigned hi = __shfl_down_sync(0xffffffffu, half, 1);
+    if (lane < 2 * NV && !(lane & 1)) bc[lane >> 1] = __longlong_as_double((long long)((unsigned long long)hi << 32 | half));
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < NV; ++j) v[j] = bc[j];
+}
+// constraint pass of rank k over its constraint list on u (window) or on a
+// complete global vector (x0: xg), writing only its own rows' incidence slots
+__device__ __forceinline__ void slab_cons(const FFArgs& a, const SlabRank& k, const double4* xg, double4* contrib) {
+  const int c0 = a.slab.con_ptr[k.s], c1 = a.slab.con_ptr[k.s + 1];
+  const int t0 = (int(blockIdx.x) - k.b0) * blockDim.x + threadIdx.x, nt = k.nb * blockDim.x;
+  for (int i = c0 + t0; i < c1; i += nt) {
+    const int64_t c = a.slab.con_list[i];
+    int rows[8];
+    double w[8];
+    ld_anchors(a, c, rows, w);
+    const double4 gc = ld4w(a.c_g, c);
+    V3 q{0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (rows[j] >= 0) q += w[j] * (xg ? ld4(xg, rows[j]) : slab_u(k, rows[j]));
+    V3 u;
+    if (a.c_kind[c] == WFK_DENSE_PLANE) {
+      const V3 g{gc.x, gc.y, gc.z};
+      u = (gc.w * dot(g, q)) * g;
+    } else {
+      u = gc.w * q;
+    }
+    const int4 p0 = a.c_pos[2 * c], p1 = a.c_pos[2 * c + 1];
+    const int pos[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (pos[j] >= 0 && rows[j] >= k.lo && rows[j] < k.hi) st4(contrib, pos[j], w[j] * u);
+  }
+}
+// item pass over one tile's items: its rows' first items, then their extra
+// items (contiguous); item_pass's arithmetic and order, two items per thread
+// in flight (item_pass2)
+template <class Sink>
+__device__ __forceinline__ void slab_items(const FFArgs& a, const SlabRank& k, int r0, int r1, const double4* xg,
+                                           const double4* contrib, double* wpart, Sink& sink) {
+  if (r1 <= r0) return;
+  const int x0 = a.xrange[r0].x, x1 = a.xrange[r1 - 1].x + a.xrange[r1 - 1].y;
+  const int nfirst = r1 - r0, total = nfirst + (x1 - x0);
+  const double w2 = 2.0 * a.w_r;
+  const int st = blockDim.x;
+  auto uof = [&](int r) { return xg ? ld4(xg, r) : slab_u(k, r); };
+  for (int j0 = threadIdx.x; j0 < total; j0 += 2 * st) {
+    int r[2], e0[2], e1[2], item[2], nb[2][6];
+    bool live[2], first[2], frz[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = j0 + h * st;
+      live[h] = j < total;
+      first[h] = live[h] && j < nfirst;
+      r[h] = r0;
+      e0[h] = e1[h] = 0;
+      item[h] = 0;
+      frz[h] = false;
+#pragma unroll
+      for (int f = 0; f < 6; ++f) nb[h][f] = -1;
+      if (!live[h]) continue;
+      if (first[h]) {
+        r[h] = r0 + j;
+        item[h] = r[h];
+        e0[h] = a.row_ptr[r[h]];
+        e1[h] = min(a.row_ptr[r[h] + 1], e0[h] + kItemLen);
+        frz[h] = a.frozen[r[h]];
+#pragma unroll
+        for (int f = 0; f < 6; ++f) nb[h][f] = a.nbr[int64_t(f) * a.N + r[h]];
+      } else {
+        item[h] = a.N + x0 + (j - nfirst);
+        const int4 it = a.xitems[x0 + (j - nfirst)];
+        r[h] = it.x;
+        e0[h] = it.y;
+        e1[h] = it.z;
+      }
+    }
+    V3 vr[2], acc[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      vr[h] = live[h] ? uof(r[h]) : V3{0, 0, 0};
+      acc[h] = V3{0, 0, 0};
+      if (live[h] && !(first[h] && frz[h]))
+        for (int e = e0[h]; e < e1[h]; ++e) acc[h] += ld4(contrib, e);
+    }
+#pragma unroll
+    for (int f = 0; f < 6; ++f)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (first[h] && !frz[h] && nb[h][f] >= 0) acc[h] += w2 * (vr[h] - uof(nb[h][f]));
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (!live[h]) continue;
+      if (first[h] && frz[h]) acc[h] = vr[h];  // frozen rows: A = I (solver.cpp:241-246)
+      stv(wpart, item[h], acc[h]);
+      sink(r[h], vr[h], acc[h]);
+    }
+  }
+}
+__device__ void pcg_slab(const FFArgs& a, Red& rs, int& iters, double& relres) {
+  const PackVecs<double>& pv = a.dv;
+  const SlabRank k = slab_rank(a);
+  unsigned& gen = rs.sl_gen;
+  unsigned& epoch = rs.sl_epoch;
+  unsigned& seq = rs.sl_seq;
+  const int T = a.slab.T;
+  iters = 0;
+  relres = 0;
+  PhaseClock pc(a.dbg);
+  auto none = [](int, V3, V3) {};
+  auto tile_rows = [&](int t, int& r0, int& r1) {
+    r0 = min(a.N, t * T);
+    r1 = min(a.N, r0 + T);
+  };
+  // r0 = b - A x0 (x0 = t, complete on every rank); u0 = D r0; tile partials
+  // r.u (slot 0), r.r (2), b.b (3) now, w.u (1) after the matvec of u0
+  slab_cons(a, k, a.x, pv.contrib);
+  slab_sync(a, k, gen, false, epoch);
+  SLAB_TILES(k, t) {
+    int r0, r1;
+    tile_rows(t, r0, r1);
+    slab_items(a, k, r0, r1, a.x, pv.contrib, pv.wpart, none);
+  }
+  __syncthreads();
+  SLAB_TILES(k, t) {
+    int r0, r1;
+    tile_rows(t, r0, r1);
+    double v[3] = {0, 0, 0};
+    for (int r = r0 + int(threadIdx.x); r < r1; r += blockDim.x) {
+      const V3 b = ld4(a.rhs, r);
+      const V3 rr = b - row_from_items_pk(a, static_cast<const double*>(pv.wpart), r);
+      const V3 d = ld4(a.dinv, r);
+      const V3 u = cmul(d, rr);
+      stv(pv.r, r, rr);
+      stv(pv.dinv, r, d);
+      slab_put_u(a, k, r, u);
+      stv(pv.p, r, V3{0, 0, 0});
+      stv(pv.s, r, V3{0, 0, 0});
+      stv(pv.d, r, V3{0, 0, 0});
+      v[0] += dot(rr, u);
+      v[1] += dot(rr, rr);
+      v[2] += sqnorm(b);
+    }
+    const int slots[3] = {0, 2, 3};
+    slab_tile_put<3>(a, k, t, v, slots, seq);
+  }
+  slab_sync(a, k, gen, true, epoch);
+  // w0 = A u0
+  slab_cons(a, k, nullptr, pv.contrib);
+  slab_sync(a, k, gen, false, epoch);
+  SLAB_TILES(k, t) {
+    int r0, r1;
+    tile_rows(t, r0, r1);
+    double v[1] = {0};
+    auto w_sink = [&](int, V3 ur, V3 wpart) { v[0] += dot(wpart, ur); };
+    slab_items(a, k, r0, r1, nullptr, pv.contrib, pv.wpart, w_sink);
+    const int slots[1] = {1};
+    slab_tile_put<1>(a, k, t, v, slots, seq);
+  }
+  double v4[4];
+  slab_allreduce<4>(a, k, v4, seq++);
+  double gamma = v4[0], delta = v4[1];
+  double r_norm = sqrt(v4[2]);
+  const double b_norm = sqrt(v4[3]);
+  if (b_norm == 0) {
+    for (int r = k.lo + (int(blockIdx.x) - k.b0) * int(blockDim.x) + int(threadIdx.x); r < k.hi;
+         r += k.nb * int(blockDim.x))
+      st4(a.x, r, V3{0, 0, 0});
+    grid_barrier(a, rs);
+    return;
+  }
+  relres = r_norm / b_norm;
+  const double stop = fmax(a.pcg_tol * r_norm, 1e-13 * b_norm);
+  double gamma_prev = 0, alpha_prev = 0;
+  pc.lap(12);
+  for (int it = 0; it < a.pcg_max && r_norm > stop; ++it) {
+    const double beta = it == 0 ? 0.0 : gamma / gamma_prev;
+    const double pap = it == 0 ? delta : delta - beta * gamma / alpha_prev;
+    if (pap <= 0) break;  // solver.cpp:327
+    const double alpha = gamma / pap;
+    SLAB_TILES(k, t) {
+      int r0, r1;
+      tile_rows(t, r0, r1);
+      double v[2] = {0, 0};
+      for (int r = r0 + int(threadIdx.x); r < r1; r += blockDim.x) {
+        const V3 w = row_from_items_pk(a, static_cast<const double*>(pv.wpart), r);
+        const V3 p = slab_u(k, r) + beta * ldv(pv.p, r);
+        const V3 sv = w + beta * ldv(pv.s, r);
+        const V3 d = ldv(pv.d, r) + alpha * p;
+        const V3 rr = ldv(pv.r, r) - alpha * sv;
+        const V3 u = cmul(ldv(pv.dinv, r), rr);
+        stv(pv.p, r, p);
+        stv(pv.s, r, sv);
+        stv(pv.d, r, d);
+        stv(pv.r, r, rr);
+        v[0] += dot(rr, u);
+        v[1] += dot(rr, rr);
+        slab_put_u(a, k, r, u);
+      }
+      const int slots[2] = {0, 2};
+      slab_tile_put<2>(a, k, t, v, slots, seq);
+    }
+    pc.lap(4);
+    slab_sync(a, k, gen, true, epoch);
+    pc.lap(5);
+    slab_cons(a, k, nullptr, pv.contrib);
+    pc.lap(0);
+    slab_sync(a, k, gen, false, epoch);
+    pc.lap(1);
+    SLAB_TILES(k, t) {
+      int r0, r1;
+      tile_rows(t, r0, r1);
+      double v[1] = {0};
+      auto w_sink2 = [&](int, V3 ur, V3 wpart) { v[0] += dot(wpart, ur); };
+      slab_items(a, k, r0, r1, nullptr, pv.contrib, pv.wpart, w_sink2);
+      const int slots[1] = {1};
+      slab_tile_put<1>(a, k, t, v, slots, seq);
+    }
+    pc.lap(2);
+    double v3[3];
+    slab_allreduce<3>(a, k, v3, seq++);
+    pc.lap(3);
+    pc.count(15);
+    gamma_prev = gamma;
+    alpha_prev = alpha;
+    gamma = v3[0];
+    delta = v3[1];
+    r_norm = sqrt(v3[2]);
+    relres = r_norm / b_norm;
+    iters = it + 1;
+  }
+  // x = x0 + d of the rank's rows, then every rank's rows are in x
+  for (int r = k.lo + (int(blockIdx.x) - k.b0) * int(blockDim.x) + int(threadIdx.x); r < k.hi;
+       r += k.nb * int(blockDim.x))
+    st4(a.x, r, ld4(a.x, r) + ldv(pv.d, r));
+  grid_barrier(a, rs);
+}
+
 template <bool ASM>
 __device__ void pcg(const FFArgs& a, cg::grid_group& grid, Red& rs, int& iters, double& relres) {
   iters = 0;
@@ -1615,14 +2034,6 @@ __device__ __forceinline__ void row_pass_mf(const FFArgs& a, const double4* v, S
 // double-buffered by the reduction sequence number, which a block can only
 // reuse two reductions later -- after every block has consumed the older one.
 constexpr int kSplitNV = 3;
-__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ double* split_partials(const FFArgs& a, unsigned seq) {
   return a.partials + size_t(seq & 1) * kSplitNV * gridDim.x;
 }
@@ -2133,12 +2544,14 @@ __global__ void __launch_bounds__(TPB, 1) k_flip_flop(FFArgs a) {
       pc.lap(8);
       int iters;
       double relres;
-      if (V == 2 || V == 3) {
+      if (V == 2 || V == 3 || V == 4) {
         if constexpr (!ASM) {
           if constexpr (V == 2)
             pcg_pk<float>(a, rs, iters, relres);
-          else
+          else if constexpr (V == 3)
             pcg_pk<double>(a, rs, iters, relres);
+          else
+            pcg_slab(a, rs, iters, relres);
         }
       } else if (V == 1)
         pcg<ASM>(a, grid, rs, iters, relres);
@@ -2560,6 +2973,77 @@ static void level_constraints(wfk_ctx* c, Level& L, const PoseD& pose, const wfk
   WFK_CUDA(cudaGetLastError());
 }
 
+// ---- slab plan (WFK_SLABS; see pcg_slab) -------------------------------------
+__device__ __forceinline__ int slab_segment_of(const int32_t* bounds, int n, int r) {
+  int lo = 0, hi = n - 1;  // last i with bounds[i] <= r
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (bounds[mid] <= r) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+// u window of every rank: the rows its own rows' stencil and incident
+// constraints reach (initialised to its own range)
+__global__ void k_slab_window(int N, int S, const int32_t* rank_lo, const int32_t* nbr, const int32_t* row_ptr,
+                              const int32_t* ent_con, const int4* c_row, int32_t* win_lo, int32_t* win_hi) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x) {
+    const int s = slab_segment_of(rank_lo, S, r);
+    int lo = r, hi = r;
+    for (int f = 0; f < 6; ++f) {
+      const int j = nbr[int64_t(f) * N + r];
+      if (j >= 0) {
+        lo = min(lo, j);
+        hi = max(hi, j);
+      }
+    }
+    for (int e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
+      const int c = ent_con[e];
+      const int4 q0 = c_row[2 * c], q1 = c_row[2 * c + 1];
+      const int rr[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+      for (int k = 0; k < 8; ++k)
+        if (rr[k] >= 0) {
+          lo = min(lo, rr[k]);
+          hi = max(hi, rr[k]);
+        }
+    }
+    atomicMin(&win_lo[s], lo);
+    atomicMax(&win_hi[s], hi + 1);
+  }
+}
+// per-row work weight of the block split, in units of one 32-byte access: the
+// update and the row's first item (~12) plus one per incidence contribution
+__global__ void k_slab_weight(int N, const int32_t* row_ptr, int32_t* w) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x)
+    w[r] = 12 + (row_ptr[r + 1] - row_ptr[r]);
+}
+// inclusive work prefix at the end of every tile (the rank split is taken on
+// the host from these ntiles values)
+__global__ void k_slab_tile_weight(int N, int T, int ntiles, const int32_t* incl, int64_t* tw) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < ntiles) tw[t] = incl[min(N, (t + 1) * T) - 1];
+}
+// constraints incident to each rank's rows: count (fill == nullptr) or list
+__global__ void k_slab_cons(int64_t C, int S, const int32_t* rank_lo, const int4* c_row, const int4* c_pos,
+                            int32_t* cnt, const int32_t* off, int32_t* fill) {
+  for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < C; c += int64_t(gridDim.x) * blockDim.x) {
+    const int4 q0 = c_row[2 * c], q1 = c_row[2 * c + 1], p0 = c_pos[2 * c], p1 = c_pos[2 * c + 1];
+    const int rr[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+    const int pp[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+    int seen[8];
+    int ns = 0;
+    for (int k = 0; k < 8; ++k) {
+      if (rr[k] < 0 || pp[k] < 0) continue;
+      const int s = slab_segment_of(rank_lo, S, rr[k]);
+      bool dup = false;
+      for (int i = 0; i < ns; ++i) dup |= seen[i] == s;
+      if (dup) continue;
+      seen[ns++] = s;
+      const int slot = atomicAdd(&cnt[s], 1);
+      if (fill) fill[off[s] + slot] = int32_t(c);
+    }
+  }
+}
+
 // Work items of the balanced matrix-free item pass (Chronopoulos-Gear PCG
 // only; built on first use per prepared level).
 static void level_items(wfk_ctx* c, Level& L) {
@@ -2583,6 +3067,137 @@ static void level_items(wfk_ctx* c, Level& L) {
   k_item_write<<<grid_for(N), kBlock, 0, s>>>(N, L.row_ptr, L.xptr, L.xitems, L.xrange);
   count_launch(c, 3);
   L.items_built = true;
+}
+
+// Slab plan of a prepared matrix-free level for S ranks over G blocks (see
+// pcg_slab): rank row ranges, u windows (checked to reach only the adjacent
+// ranks), per-rank constraint lists and the reduction state; fills a.slab.
+static void slab_plan(wfk_ctx* c, Level& L, int S, int G, FFArgs& a) {
+  cudaStream_t s = c->stream;
+  const int N = L.N;
+  // tiles: about 8 per block and at least one row per thread, whatever S is
+  // (T depends on N and G only)
+  const int T = std::max(kFastBlock, int((int64_t(N) + 8 * G - 1) / (8 * G) + 31) / 32 * 32);
+  const int ntiles = std::max(1, (N + T - 1) / T);
+  S = std::max(1, std::min(S, std::min(G, ntiles)));
+  // work prefix per row, read at the tile ends: ranks get contiguous tile
+  // ranges of about equal work
+  int32_t* wgt = L.sl_blk.ensure(2 * size_t(std::max(N, 1)) + 2 * size_t(ntiles) + 2);
+  int32_t* incl = wgt + std::max(N, 1);
+  int64_t* d_tw = reinterpret_cast<int64_t*>(L.sl_red.ensure(size_t(ntiles) + 1));
+  std::vector<int64_t> tw(size_t(ntiles), 0);
+  if (N > 0) {
+    k_slab_weight<<<grid_for(N), kBlock, 0, s>>>(N, L.row_ptr, wgt);
+    size_t tmp = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, tmp, wgt, incl, N, s);
+    c->temp.ensure(tmp);
+    WFK_CUDA(cub::DeviceScan::InclusiveSum(c->temp.p, tmp, wgt, incl, N, s));
+    k_slab_tile_weight<<<(ntiles + kBlock - 1) / kBlock, kBlock, 0, s>>>(N, T, ntiles, incl, d_tw);
+    count_launch(c, 3);
+    WFK_CUDA(cudaMemcpyAsync(tw.data(), d_tw, tw.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    sync_check(c);
+  }
+  std::vector<int32_t> rt(size_t(S) + 1, 0);  // rank tile bounds
+  rt[size_t(S)] = ntiles;
+  {
+    const int64_t W = tw.back();
+    int t = 0;
+    for (int k = 1; k < S; ++k) {
+      const int64_t target = W * k / S;
+      while (t < ntiles && tw[size_t(t)] <= target) ++t;
+      rt[size_t(k)] = std::max(rt[size_t(k) - 1] + 1, std::min(t, ntiles - (S - k)));  // every rank >= 1 tile
+    }
+  }
+  std::vector<int32_t> lo(size_t(S) + 1);
+  for (int k = 0; k <= S; ++k) lo[size_t(k)] = std::min(N, rt[size_t(k)] * T);
+  // device index area: rank_tile (S+1) | rank_lo (S+1) | win_lo (S) | win_hi (S) | con_ptr (S+1) | cnt (S) | list
+  const size_t o_lo = size_t(S) + 1, o_wlo = o_lo + S + 1, o_whi = o_wlo + S, o_cptr = o_whi + S,
+               o_cnt = o_cptr + S + 1, o_list = o_cnt + S;
+  const size_t Cb = size_t(S) * size_t(std::max<int64_t>(L.C, 1));  // bound on the list entries
+  int32_t* idx = L.sl_idx.ensure(o_list + 2 * Cb);
+  int32_t* d_rt = idx;
+  int32_t* d_lo = idx + o_lo;
+  int32_t* d_wlo = idx + o_wlo;
+  int32_t* d_whi = idx + o_whi;
+  int32_t* d_cptr = idx + o_cptr;
+  int32_t* d_cnt = idx + o_cnt;
+  int32_t* d_list = idx + o_list;
+  int32_t* d_sorted = d_list + Cb;
+  std::vector<int32_t> init(o_list, 0);
+  for (int k = 0; k <= S; ++k) {
+    init[size_t(k)] = rt[size_t(k)];
+    init[o_lo + size_t(k)] = lo[size_t(k)];
+  }
+  for (int k = 0; k < S; ++k) {
+    init[o_wlo + size_t(k)] = lo[size_t(k)];
+    init[o_whi + size_t(k)] = lo[size_t(k) + 1];
+  }
+  WFK_CUDA(cudaMemcpyAsync(idx, init.data(), init.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  if (N > 0)
+    k_slab_window<<<grid_for(N), kBlock, 0, s>>>(N, S, d_lo, L.nbr, L.row_ptr, L.ent_con,
+                                                 reinterpret_cast<const int4*>(L.c_row.p), d_wlo, d_whi);
+  if (L.C > 0)
+    k_slab_cons<<<grid_for(L.C), kBlock, 0, s>>>(L.C, S, d_lo, reinterpret_cast<const int4*>(L.c_row.p),
+                                                 reinterpret_cast<const int4*>(L.c_pos.p), d_cnt, nullptr, nullptr);
+  std::vector<int32_t> back(o_list);
+  WFK_CUDA(cudaMemcpyAsync(back.data(), idx, back.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  sync_check(c);
+  std::vector<int32_t> wlo(back.begin() + o_wlo, back.begin() + o_wlo + S);
+  std::vector<int32_t> whi(back.begin() + o_whi, back.begin() + o_whi + S);
+  for (int k = 0; k < S; ++k) {
+    if ((k > 0 && wlo[size_t(k)] < lo[size_t(k) - 1]) || (k + 2 <= S && whi[size_t(k)] > lo[size_t(k) + 2]))
+      throw Error(WFK_E_INVALID_ARG, "slab partition: a slab is thinner than the stencil / constraint halo");
+  }
+  std::vector<int32_t> cptr(size_t(S) + 1, 0);
+  for (int k = 0; k < S; ++k) cptr[size_t(k) + 1] = cptr[size_t(k)] + back[o_cnt + size_t(k)];
+  WFK_CUDA(cudaMemcpyAsync(d_cptr, cptr.data(), cptr.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  WFK_CUDA(cudaMemsetAsync(d_cnt, 0, size_t(S) * sizeof(int32_t), s));
+  if (L.C > 0) {
+    k_slab_cons<<<grid_for(L.C), kBlock, 0, s>>>(L.C, S, d_lo, reinterpret_cast<const int4*>(L.c_row.p),
+                                                 reinterpret_cast<const int4*>(L.c_pos.p), d_cnt, d_cptr, d_list);
+    // each rank's list in constraint order (the atomics filled it unordered):
+    // the constraint pass then reads its constraint records in order
+    const int nl = cptr[size_t(S)];
+    size_t tmp = 0;
+    cub::DeviceSegmentedRadixSort::SortKeys(nullptr, tmp, d_list, d_sorted, nl, S, d_cptr, d_cptr + 1, 0, 32, s);
+    c->temp.ensure(tmp);
+    WFK_CUDA(cub::DeviceSegmentedRadixSort::SortKeys(c->temp.p, tmp, d_list, d_sorted, nl, S, d_cptr, d_cptr + 1,
+                                                     0, 32, s));
+    count_launch(c, 3);
+  }
+  // u windows, counters (128 words per rank), tile partials (2 x ntiles x 8)
+  // and totals (2 x 8) per rank
+  std::vector<size_t> woff(size_t(S) + 1, 0);
+  for (int k = 0; k < S; ++k) woff[size_t(k) + 1] = woff[size_t(k)] + size_t(whi[size_t(k)] - wlo[size_t(k)]);
+  double4* win = L.sl_win.ensure(std::max<size_t>(woff[size_t(S)], 1));
+  unsigned* ctr = L.sl_ctr.ensure(size_t(S) * 128);
+  const size_t red_per_rank = size_t(2) * ntiles * 8 + 16;
+  unsigned long long* red = L.sl_red.ensure(size_t(S) * red_per_rank);
+  WFK_CUDA(cudaMemsetAsync(ctr, 0, size_t(S) * 128 * sizeof(unsigned), s));
+  WFK_CUDA(cudaMemsetAsync(red, 0, size_t(S) * red_per_rank * sizeof(unsigned long long), s));
+  // pointer tables (the peer pointers of a multi-GPU run)
+  std::vector<unsigned long long> ptr(size_t(4) * S);
+  for (int k = 0; k < S; ++k) {
+    ptr[size_t(k)] = reinterpret_cast<unsigned long long>(win + woff[size_t(k)]);
+    ptr[size_t(S + k)] = reinterpret_cast<unsigned long long>(ctr + size_t(k) * 128);
+    ptr[size_t(2 * S + k)] = reinterpret_cast<unsigned long long>(red + size_t(k) * red_per_rank);
+    ptr[size_t(3 * S + k)] = reinterpret_cast<unsigned long long>(red + size_t(k) * red_per_rank + size_t(2) * ntiles * 8);
+  }
+  unsigned long long* d_ptr = L.sl_ptr.ensure(ptr.size());
+  WFK_CUDA(cudaMemcpyAsync(d_ptr, ptr.data(), ptr.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+  sync_check(c);  // the host vectors above go out of scope
+  a.slab.S = S;
+  a.slab.T = T;
+  a.slab.ntiles = ntiles;
+  a.slab.rank_tile = d_rt;
+  a.slab.win_lo = d_wlo;
+  a.slab.win_hi = d_whi;
+  a.slab.uwin = reinterpret_cast<double4* const*>(d_ptr);
+  a.slab.ctr = reinterpret_cast<unsigned* const*>(d_ptr + S);
+  a.slab.part = reinterpret_cast<unsigned long long* const*>(d_ptr + 2 * S);
+  a.slab.tot = reinterpret_cast<unsigned long long* const*>(d_ptr + 3 * S);
+  a.slab.con_ptr = d_cptr;
+  a.slab.con_list = L.C > 0 ? d_sorted : d_list;
 }
 
 PoseD pose_dev(const wfk_pose* p) {
@@ -2646,6 +3261,13 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   // read per call so tests can force the Chronopoulos-Gear variant
   const char* pcg_env = getenv("WFK_PCG");
   a.pcg_variant = (pcg_env && std::string(pcg_env) == "cg") ? 1 : 0;
+  // WFK_SLABS=S (per call): matrix-free levels run the slab-partitioned CG
+  // with S ranks (pcg_slab; S = 1 is the same kernel unpartitioned)
+  const char* slab_env = getenv("WFK_SLABS");
+  const int slabs = slab_env ? atoi(slab_env) : 0;
+  const bool slab = slabs >= 1 && !L.assembled && L.N > 0 && mode == 0 && c->precision != WFK_PRECISION_FAST;
+  a.slab = SlabDev{};
+  if (slab) a.pcg_variant = 1;
   a.assembled = L.assembled ? 1 : 0;
   a.asm_rows_on_lanes = L.N >= kAsmThreadRows ? 1 : 0;
   a.blk = L.blk;
@@ -2772,7 +3394,7 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   const char* pack_env = getenv("WFK_PACK");  // per call: tests switch it
   const bool cg_mf = a.pcg_variant == 1 && !asm_k && L.N > 0 && mode == 0;
   const bool fast = c->precision == WFK_PRECISION_FAST && cg_mf;
-  const bool packed64 = !fast && cg_mf && !(pack_env && pack_env[0] == '0');
+  const bool packed64 = !fast && cg_mf && (slab || !(pack_env && pack_env[0] == '0'));
   static const bool item1 = getenv("WFK_ITEM1") != nullptr;  // A/B: one item per thread in flight
   a.item2 = item1 ? 0 : 1;
   a.fv = PackVecs<float>{};
@@ -2790,7 +3412,11 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   };
   if (fast) bind_pack(a.fv, L.f_r, L.f_p, L.f_s, L.f_u, L.f_d, L.f_dinv, L.f_contrib, L.f_wpart);
   if (packed64) bind_pack(a.dv, L.d_r, L.d_p, L.d_s, L.d_u, L.d_d, L.d_dinv, L.d_contrib, L.d_wpart);
-  if (fast || packed64) {
+  if (slab) {
+    slab_plan(c, L, slabs, G, a);
+    kern = k_flip_flop<4, false, kSlotVecs, kFastBlock>;
+    tpb = kFastBlock;
+  } else if (fast || packed64) {
     kern = fast ? k_flip_flop<2, false, kSlotVecs, kFastBlock> : k_flip_flop<3, false, kSlotVecs, kFastBlock>;
     tpb = kFastBlock;
   }

@@ -150,6 +150,12 @@ struct Level {
   DevBuf<float> f_r, f_p, f_s, f_u, f_d, f_dinv, f_contrib, f_wpart;
   // the same packed in fp64 (the default for large CG levels)
   DevBuf<double> d_r, d_p, d_s, d_u, d_d, d_dinv, d_contrib, d_wpart;
+  // slab-partitioned CG inside the persistent kernel (WFK_SLABS): rank row
+  // ranges, u windows, constraint lists, counters, partials, pointer tables
+  DevBuf<int32_t> sl_idx, sl_blk;
+  DevBuf<double4> sl_win;
+  DevBuf<unsigned> sl_ctr;
+  DevBuf<unsigned long long> sl_red, sl_ptr;
   // explicit normal equations of the slab-partitioned solve (solver_c2f_dist)
   DevBuf<double> ne_blocks, ne_rhs, ne_x;
   DevBuf<int32_t> ne_cols;

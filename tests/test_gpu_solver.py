@@ -442,3 +442,48 @@ def test_packed_fp64_cg_parity(ctx, monkeypatch, pack):
     tg = ctx.solve_coarse_to_fine(pose, p)
     ctx.download_volume(v)
     compare_solves(v, ref, tg, tr)
+
+
+# ---- the slab-partitioned CG inside the persistent kernel ----
+def _slab_solve(ctx, monkeypatch, slabs, n=48, ncons=6000):
+    v = make_volume(n)
+    cons = random_dense_constraints(v, ncons, seed=13)
+    p = SolverParams.make()
+    pose = Pose.make(O.euler_to_matrix((0.0, 0.01, 0.0)), (0.005, 0, 0))
+    monkeypatch.setenv("WFK_SLABS", str(slabs))
+    ctx.upload_volume(v)
+    ctx.upload_constraints(cons)
+    tg = ctx.solve_coarse_to_fine(pose, p)
+    ctx.download_volume(v)
+    return v, tg, cons, pose, p
+
+
+def test_slab_cg_bitwise_across_ranks(ctx, monkeypatch):
+    """pcg_slab with S = 1, 2, 4, 8 virtual ranks (block groups of one
+    cooperative launch, each with its own u window filled by the neighbours'
+    pushes, rank barriers, a rank-ordered all-reduce): block b always owns the
+    same rows and every sum runs over block partials in block order, so the
+    partitioned solve is bit-identical to the unpartitioned one."""
+    base_v, base_t, _, _, _ = _slab_solve(ctx, monkeypatch, 1)
+    for s in (2, 4, 8):
+        v, t, _, _, _ = _slab_solve(ctx, monkeypatch, s)
+        assert np.array_equal(v.deformed, base_v.deformed), s
+        assert np.array_equal(v.euler, base_v.euler), s
+        assert [e["energy"]["total"] for e in t] == [e["energy"]["total"] for e in base_t], s
+        assert [e["pcg_iterations"] for e in t] == [e["pcg_iterations"] for e in base_t], s
+
+
+def test_slab_cg_parity(ctx, monkeypatch):
+    """The slab-partitioned solve (4 ranks) against the reference at the fp64 bars."""
+    v, tg, cons, pose, p = _slab_solve(ctx, monkeypatch, 4)
+    ref = make_volume(48)
+    tr = O.solve_coarse_to_fine(ref, pose, cons, p)
+    compare_solves(v, ref, tg, tr)
+
+
+def test_slab_too_thin_is_rejected(ctx, monkeypatch):
+    """A slab thinner than the stencil / constraint halo (here: one block's rows
+    per rank) cannot be served by its two neighbours alone: invalid argument."""
+    from paper_1603_08161_b200.wfk import WfkError
+    with pytest.raises(WfkError):
+        _slab_solve(ctx, monkeypatch, 148)
