@@ -511,6 +511,10 @@ def run_solve(args):
         sc = S.bend_sphere(K, frames=FRAMES_TOTAL, amplitude=AMPLITUDE, frequency=FREQUENCY)
         frames_idx = [3, 4]  # a visible bend between the two frames
     frames = [Frame(K, *S.render(sc, f)) for f in frames_idx]
+    if args.slabs:
+        # the matrix-free levels' CG cut into z-slab ranks inside the persistent
+        # kernel (pcg_slab; virtual ranks on this GPU; read per solve call)
+        os.environ["WFK_SLABS"] = str(args.slabs)
     ctx = Context(0)
     if args.fast:
         ctx.set_precision(1)  # WFK_PRECISION_FAST: fp32 Krylov vectors on levels that run the CG variant
@@ -564,7 +568,9 @@ def run_solve(args):
                    "precision": "fast (fp32 Krylov vectors on CG levels)" if args.fast else "fp64",
                    "lattice": [n] * 3, "depth_resolution": list(cfg_s["K"][4:]),
                    "rows_per_level": [int(x) for x in act], "dense_constraints": int(n_cons),
-                   "l2": "flushed (256 MB write) before every solve", "parallelism": "single GPU"},
+                   "l2": "flushed (256 MB write) before every solve",
+                   "parallelism": (f"single GPU; matrix-free levels' CG slab-partitioned into {args.slabs} ranks "
+                                   "(block groups of one cooperative launch)") if args.slabs else "single GPU"},
         "pcg_iters_per_s": pcg / (total_ms * 1e-3), "pcg_iterations_per_solve": pcg / args.steps,
         "solve_ms": [round(x, 3) for x in times], "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": "k_flip_flop", "achieved": achieved, "peak": peak,
@@ -577,6 +583,7 @@ def run_solve(args):
                      "share_of_solve": prof.flip_flop_ms / max(total_ms, 1e-9)},
         "clocks": clocks.summary(),
         "energy_final": tr[-1]["energy"]["total"] if tr else None,
+        "energy_final_hex": float(tr[-1]["energy"]["total"]).hex() if tr else None,
     }
     print(json.dumps(out), flush=True)
     ctx.close()
@@ -680,6 +687,9 @@ def main():
                     help="BASELINE configs[3] (256^3) or configs[4] (512^3, 1280x720 room): the frame-1 solve x K")
     ap.add_argument("--fast", action="store_true",
                     help="with --solve-config: WFK_PRECISION_FAST (fp32 Krylov vectors on the large CG levels)")
+    ap.add_argument("--slabs", type=int, default=0,
+                    help="with --solve-config: run the matrix-free levels' CG slab-partitioned into this many ranks "
+                         "inside the persistent kernel (WFK_SLABS)")
     ap.add_argument("--partitioned", action="store_true",
                     help="BASELINE configs[3]: the 256^3 frame-1 solve with the PCG slab-partitioned over the ranks")
     args = ap.parse_args()
