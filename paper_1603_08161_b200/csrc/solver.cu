@@ -1535,23 +1535,64 @@ __device__ __forceinline__ void slab_sync(const FFArgs& a, const SlabRank& k, un
   if (halo) epoch += 1;
   __syncthreads();
 }
-// the block's tiles: t0 + (b - b0), + nb, ...
-#define SLAB_TILES(k, t) for (int t = (k).t0 + (int(blockIdx.x) - (k).b0); t < (k).t1; t += (k).nb)
-// block sum of v[j] (j in mask) of one tile -> words 2j, 2j + 1 of the tile in
-// every rank's partial array (tag seq + 1)
+// Tile partials: after each tile every warp reduces its lanes' sums (fixed
+// butterfly) into a shared slot; after a batch of tiles one block barrier,
+// then the warps' sums of each tile are added in warp order (fixed) and
+// written as words 2j, 2j + 1 of the tile into every rank's partial array
+// (tag seq + 1).  No block barrier between the tiles of a batch.
+constexpr int kSlabBatch = 16;
+struct SlabTileSm {
+  double v[kSlabBatch][32][4];
+};
 template <int NV>
-__device__ __forceinline__ void slab_tile_put(const FFArgs& a, const SlabRank& k, int t, double (&v)[NV],
-                                              const int (&slot)[NV], unsigned seq) {
-  __shared__ double smem[4 * 32];
-  block_sum<NV>(v, smem);
-  const int lane = threadIdx.x;
-  if (lane < 2 * NV) {
-    const unsigned long long bits = (unsigned long long)__double_as_longlong(v[lane >> 1]);
-    const unsigned half = (lane & 1) ? unsigned(bits >> 32) : unsigned(bits);
-    const unsigned long long word = (unsigned long long)half << 32 | (seq + 1u);
-    const size_t off = (size_t(seq & 1) * a.slab.ntiles + size_t(t)) * 8 + 2 * slot[lane >> 1] + (lane & 1);
-    for (int d = 0; d < k.S; ++d) st_relaxed_u64(a.slab.part[d] + off, word);
+__device__ __forceinline__ void slab_tile_stash(SlabTileSm& sm, int tl, double (&v)[NV]) {
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const double w = warp_sum(v[j]);
+    if ((threadIdx.x & 31) == 0) sm.v[tl][threadIdx.x >> 5][j] = w;
   }
+}
+template <int NV>
+__device__ __forceinline__ void slab_tile_flush(const FFArgs& a, const SlabRank& k, SlabTileSm& sm, int n, int t_first,
+                                                const int (&slot)[NV], unsigned seq) {
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  for (int idx = threadIdx.x; idx < n * NV; idx += blockDim.x) {
+    const int tl = idx / NV, j = idx % NV;
+    double v = 0;
+    for (int w = 0; w < nw; ++w) v += sm.v[tl][w][j];
+    const int t = t_first + tl * k.nb;
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+    const size_t off = (size_t(seq & 1) * a.slab.ntiles + size_t(t)) * 8 + 2 * slot[j];
+    const unsigned long long w0 = (unsigned long long)unsigned(bits) << 32 | (seq + 1u);
+    const unsigned long long w1 = (bits >> 32) << 32 | (seq + 1u);
+    for (int d = 0; d < k.S; ++d) {
+      st_relaxed_u64(a.slab.part[d] + off, w0);
+      st_relaxed_u64(a.slab.part[d] + off + 1, w1);
+    }
+  }
+  __syncthreads();
+}
+// runs f(t, r0, r1, v) over this block's tiles with per-tile partials v[NV]
+template <int NV, class F>
+__device__ __forceinline__ void slab_for_tiles(const FFArgs& a, const SlabRank& k, SlabTileSm& sm,
+                                               const int (&slot)[NV], unsigned seq, F f) {
+  const int T = a.slab.T;
+  int tl = 0, t_first = k.t0 + (int(blockIdx.x) - k.b0);
+  for (int t = t_first; t < k.t1; t += k.nb) {
+    const int r0 = min(a.N, t * T), r1 = min(a.N, r0 + T);
+    double v[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) v[j] = 0;
+    f(r0, r1, v);
+    slab_tile_stash<NV>(sm, tl, v);
+    if (++tl == kSlabBatch) {
+      slab_tile_flush<NV>(a, k, sm, tl, t_first, slot, seq);
+      t_first += kSlabBatch * k.nb;
+      tl = 0;
+    }
+  }
+  if (tl) slab_tile_flush<NV>(a, k, sm, tl, t_first, slot, seq);
 }
 // all-reduce of NV values over every tile, tile order
 template <int NV>
@@ -1708,54 +1749,46 @@ __device__ void pcg_slab(const FFArgs& a, Red& rs, int& iters, double& relres) {
   relres = 0;
   PhaseClock pc(a.dbg);
   auto none = [](int, V3, V3) {};
-  auto tile_rows = [&](int t, int& r0, int& r1) {
-    r0 = min(a.N, t * T);
-    r1 = min(a.N, r0 + T);
-  };
+  __shared__ SlabTileSm tsm;
   // r0 = b - A x0 (x0 = t, complete on every rank); u0 = D r0; tile partials
   // r.u (slot 0), r.r (2), b.b (3) now, w.u (1) after the matvec of u0
   slab_cons(a, k, a.x, pv.contrib);
   slab_sync(a, k, gen, false, epoch);
-  SLAB_TILES(k, t) {
-    int r0, r1;
-    tile_rows(t, r0, r1);
+  for (int t = k.t0 + (int(blockIdx.x) - k.b0); t < k.t1; t += k.nb) {
+    const int r0 = min(a.N, t * T), r1 = min(a.N, r0 + T);
     slab_items(a, k, r0, r1, a.x, pv.contrib, pv.wpart, none);
   }
   __syncthreads();
-  SLAB_TILES(k, t) {
-    int r0, r1;
-    tile_rows(t, r0, r1);
-    double v[3] = {0, 0, 0};
-    for (int r = r0 + int(threadIdx.x); r < r1; r += blockDim.x) {
-      const V3 b = ld4(a.rhs, r);
-      const V3 rr = b - row_from_items_pk(a, static_cast<const double*>(pv.wpart), r);
-      const V3 d = ld4(a.dinv, r);
-      const V3 u = cmul(d, rr);
-      stv(pv.r, r, rr);
-      stv(pv.dinv, r, d);
-      slab_put_u(a, k, r, u);
-      stv(pv.p, r, V3{0, 0, 0});
-      stv(pv.s, r, V3{0, 0, 0});
-      stv(pv.d, r, V3{0, 0, 0});
-      v[0] += dot(rr, u);
-      v[1] += dot(rr, rr);
-      v[2] += sqnorm(b);
-    }
+  {
     const int slots[3] = {0, 2, 3};
-    slab_tile_put<3>(a, k, t, v, slots, seq);
+    slab_for_tiles<3>(a, k, tsm, slots, seq, [&](int r0, int r1, double (&v)[3]) {
+      for (int r = r0 + int(threadIdx.x); r < r1; r += blockDim.x) {
+        const V3 b = ld4(a.rhs, r);
+        const V3 rr = b - row_from_items_pk(a, static_cast<const double*>(pv.wpart), r);
+        const V3 d = ld4(a.dinv, r);
+        const V3 u = cmul(d, rr);
+        stv(pv.r, r, rr);
+        stv(pv.dinv, r, d);
+        slab_put_u(a, k, r, u);
+        stv(pv.p, r, V3{0, 0, 0});
+        stv(pv.s, r, V3{0, 0, 0});
+        stv(pv.d, r, V3{0, 0, 0});
+        v[0] += dot(rr, u);
+        v[1] += dot(rr, rr);
+        v[2] += sqnorm(b);
+      }
+    });
   }
   slab_sync(a, k, gen, true, epoch);
   // w0 = A u0
   slab_cons(a, k, nullptr, pv.contrib);
   slab_sync(a, k, gen, false, epoch);
-  SLAB_TILES(k, t) {
-    int r0, r1;
-    tile_rows(t, r0, r1);
-    double v[1] = {0};
-    auto w_sink = [&](int, V3 ur, V3 wpart) { v[0] += dot(wpart, ur); };
-    slab_items(a, k, r0, r1, nullptr, pv.contrib, pv.wpart, w_sink);
+  {
     const int slots[1] = {1};
-    slab_tile_put<1>(a, k, t, v, slots, seq);
+    slab_for_tiles<1>(a, k, tsm, slots, seq, [&](int r0, int r1, double (&v)[1]) {
+      auto w_sink = [&](int, V3 ur, V3 wpart) { v[0] += dot(wpart, ur); };
+      slab_items(a, k, r0, r1, nullptr, pv.contrib, pv.wpart, w_sink);
+    });
   }
   double v4[4];
   slab_allreduce<4>(a, k, v4, seq++);
@@ -1778,27 +1811,25 @@ __device__ void pcg_slab(const FFArgs& a, Red& rs, int& iters, double& relres) {
     const double pap = it == 0 ? delta : delta - beta * gamma / alpha_prev;
     if (pap <= 0) break;  // solver.cpp:327
     const double alpha = gamma / pap;
-    SLAB_TILES(k, t) {
-      int r0, r1;
-      tile_rows(t, r0, r1);
-      double v[2] = {0, 0};
-      for (int r = r0 + int(threadIdx.x); r < r1; r += blockDim.x) {
-        const V3 w = row_from_items_pk(a, static_cast<const double*>(pv.wpart), r);
-        const V3 p = slab_u(k, r) + beta * ldv(pv.p, r);
-        const V3 sv = w + beta * ldv(pv.s, r);
-        const V3 d = ldv(pv.d, r) + alpha * p;
-        const V3 rr = ldv(pv.r, r) - alpha * sv;
-        const V3 u = cmul(ldv(pv.dinv, r), rr);
-        stv(pv.p, r, p);
-        stv(pv.s, r, sv);
-        stv(pv.d, r, d);
-        stv(pv.r, r, rr);
-        v[0] += dot(rr, u);
-        v[1] += dot(rr, rr);
-        slab_put_u(a, k, r, u);
-      }
+    {
       const int slots[2] = {0, 2};
-      slab_tile_put<2>(a, k, t, v, slots, seq);
+      slab_for_tiles<2>(a, k, tsm, slots, seq, [&](int r0, int r1, double (&v)[2]) {
+        for (int r = r0 + int(threadIdx.x); r < r1; r += blockDim.x) {
+          const V3 w = row_from_items_pk(a, static_cast<const double*>(pv.wpart), r);
+          const V3 p = slab_u(k, r) + beta * ldv(pv.p, r);
+          const V3 sv = w + beta * ldv(pv.s, r);
+          const V3 d = ldv(pv.d, r) + alpha * p;
+          const V3 rr = ldv(pv.r, r) - alpha * sv;
+          const V3 u = cmul(ldv(pv.dinv, r), rr);
+          stv(pv.p, r, p);
+          stv(pv.s, r, sv);
+          stv(pv.d, r, d);
+          stv(pv.r, r, rr);
+          v[0] += dot(rr, u);
+          v[1] += dot(rr, rr);
+          slab_put_u(a, k, r, u);
+        }
+      });
     }
     pc.lap(4);
     slab_sync(a, k, gen, true, epoch);
@@ -1807,14 +1838,12 @@ __device__ void pcg_slab(const FFArgs& a, Red& rs, int& iters, double& relres) {
     pc.lap(0);
     slab_sync(a, k, gen, false, epoch);
     pc.lap(1);
-    SLAB_TILES(k, t) {
-      int r0, r1;
-      tile_rows(t, r0, r1);
-      double v[1] = {0};
-      auto w_sink2 = [&](int, V3 ur, V3 wpart) { v[0] += dot(wpart, ur); };
-      slab_items(a, k, r0, r1, nullptr, pv.contrib, pv.wpart, w_sink2);
+    {
       const int slots[1] = {1};
-      slab_tile_put<1>(a, k, t, v, slots, seq);
+      slab_for_tiles<1>(a, k, tsm, slots, seq, [&](int r0, int r1, double (&v)[1]) {
+        auto w_sink2 = [&](int, V3 ur, V3 wpart) { v[0] += dot(wpart, ur); };
+        slab_items(a, k, r0, r1, nullptr, pv.contrib, pv.wpart, w_sink2);
+      });
     }
     pc.lap(2);
     double v3[3];
