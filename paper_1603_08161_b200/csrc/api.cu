@@ -524,6 +524,29 @@ int wfk_dist_plan(int32_t rows, const int32_t* cols, int32_t world, int32_t* ran
   return WFK_OK;
 }
 
+int wfk_slab_plan(int32_t rows, const int32_t* row_work, int32_t blocks, int32_t block_threads, int32_t ranks,
+                  int32_t* tile_rows, int32_t* rank_tiles) {
+  if (rows < 0 || blocks < 1 || block_threads < 1 || ranks < 1 || !tile_rows || !rank_tiles ||
+      (rows > 0 && !row_work))
+    return WFK_E_INVALID_ARG;
+  try {
+    const int T = slab_tile_rows(rows, blocks, block_threads);
+    const int ntiles = std::max(1, (rows + T - 1) / T);
+    if (ranks > std::min(blocks, ntiles)) return WFK_E_INVALID_ARG;
+    std::vector<int64_t> prefix(size_t(ntiles), 0);
+    int64_t acc = 0;
+    for (int r = 0, t = 0; r < rows; ++r) {
+      acc += row_work[r];
+      if (r + 1 == std::min(rows, (t + 1) * T)) prefix[size_t(t++)] = acc;
+    }
+    slab_split(ntiles, prefix.data(), ranks, rank_tiles);
+    *tile_rows = T;
+  } catch (const Error& e) {
+    return e.code;
+  }
+  return WFK_OK;
+}
+
 int wfk_pcg_solve_dist(wfk_ctx* c, int32_t rows, const double* blocks, const int32_t* cols, const double* rhs,
                        double* x, double tol, int32_t max_iters, wfk_pcg_result* out) {
   return guard(c, [&] {

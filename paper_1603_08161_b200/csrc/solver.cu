@@ -3101,12 +3101,31 @@ static void level_items(wfk_ctx* c, Level& L) {
 // Slab plan of a prepared matrix-free level for S ranks over G blocks (see
 // pcg_slab): rank row ranges, u windows (checked to reach only the adjacent
 // ranks), per-rank constraint lists and the reduction state; fills a.slab.
+// Host side of the slab plan, shared with wfk_slab_plan (tests): rows per
+// tile -- about 8 tiles per block and at least one row per thread, from N and
+// G only -- and the rank split: contiguous tile ranges of about equal work,
+// every rank at least one tile.
+int slab_tile_rows(int N, int G, int tpb) {
+  return std::max(tpb, int((int64_t(N) + 8 * G - 1) / (8 * G) + 31) / 32 * 32);
+}
+void slab_split(int ntiles, const int64_t* tile_prefix, int S, int32_t* rank_tile) {
+  rank_tile[0] = 0;
+  rank_tile[S] = ntiles;
+  const int64_t W = ntiles > 0 ? tile_prefix[ntiles - 1] : 0;
+  int t = 0;
+  for (int k = 1; k < S; ++k) {
+    const int64_t target = W * k / S;
+    while (t < ntiles && tile_prefix[t] <= target) ++t;
+    rank_tile[k] = std::max(rank_tile[k - 1] + 1, std::min(t, ntiles - (S - k)));
+  }
+}
+
 static void slab_plan(wfk_ctx* c, Level& L, int S, int G, FFArgs& a) {
   cudaStream_t s = c->stream;
   const int N = L.N;
   // tiles: about 8 per block and at least one row per thread, whatever S is
   // (T depends on N and G only)
-  const int T = std::max(kFastBlock, int((int64_t(N) + 8 * G - 1) / (8 * G) + 31) / 32 * 32);
+  const int T = slab_tile_rows(N, G, kFastBlock);
   const int ntiles = std::max(1, (N + T - 1) / T);
   S = std::max(1, std::min(S, std::min(G, ntiles)));
   // work prefix per row, read at the tile ends: ranks get contiguous tile
@@ -3127,16 +3146,7 @@ static void slab_plan(wfk_ctx* c, Level& L, int S, int G, FFArgs& a) {
     sync_check(c);
   }
   std::vector<int32_t> rt(size_t(S) + 1, 0);  // rank tile bounds
-  rt[size_t(S)] = ntiles;
-  {
-    const int64_t W = tw.back();
-    int t = 0;
-    for (int k = 1; k < S; ++k) {
-      const int64_t target = W * k / S;
-      while (t < ntiles && tw[size_t(t)] <= target) ++t;
-      rt[size_t(k)] = std::max(rt[size_t(k) - 1] + 1, std::min(t, ntiles - (S - k)));  // every rank >= 1 tile
-    }
-  }
+  slab_split(ntiles, tw.data(), S, rt.data());
   std::vector<int32_t> lo(size_t(S) + 1);
   for (int k = 0; k <= S; ++k) lo[size_t(k)] = std::min(N, rt[size_t(k)] * T);
   // device index area: rank_tile (S+1) | rank_lo (S+1) | win_lo (S) | win_hi (S) | con_ptr (S+1) | cnt (S) | list

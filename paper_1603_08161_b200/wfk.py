@@ -128,6 +128,19 @@ def dist_plan(cols, world: int):
     return ranges, xf[: n.value]
 
 
+def slab_plan(row_work, blocks: int, block_threads: int, ranks: int):
+    """The in-kernel slab partition's host plan (wfk_slab_plan, no GPU): rows
+    per tile and the rank tile bounds (ranks + 1)."""
+    w = np.ascontiguousarray(row_work, np.int32)
+    t = C.c_int32()
+    rt = np.zeros(ranks + 1, np.int32)
+    rc = lib().wfk_slab_plan(C.c_int32(len(w)), _cptr(w), C.c_int32(blocks), C.c_int32(block_threads),
+                             C.c_int32(ranks), C.byref(t), _cptr(rt))
+    if rc != WFK_OK:
+        raise WfkError(rc, "wfk_slab_plan failed")
+    return t.value, rt
+
+
 class _Pinned:
     def __init__(self, nbytes):
         p = C.c_void_p()
