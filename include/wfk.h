@@ -171,12 +171,14 @@ int wfk_solve_coarse_to_fine_slabs(wfk_ctx* ctx, int32_t slabs, const wfk_pose* 
 int wfk_dist_plan(int32_t rows, const int32_t* cols, int32_t world, int32_t* ranges, int32_t* xfers,
                   int32_t cap, int32_t* n_xfers);
 /* The in-kernel slab partition of the matrix-free levels' CG (WFK_SLABS=S;
- * no reference counterpart -- SURVEY.md 8(e)): host part of its plan.  Rows
- * are cut into tiles of *tile_rows rows (about 8 per block, at least
- * block_threads); rank s owns tiles [rank_tiles[s], rank_tiles[s + 1]) of
- * about equal summed row_work.  ranks <= min(blocks, tiles). */
+ * no reference counterpart -- SURVEY.md 8(e)): host part of its plan.  The
+ * rows are cut into *n_tiles tiles (blocks x clamp(rows / (blocks x
+ * block_threads), 1, 8)) of about equal summed row_work: tile t = rows
+ * [tile_rows[t], tile_rows[t + 1]) (tile_rows: 8 blocks + 1 entries); rank s
+ * owns tiles [rank_tiles[s], rank_tiles[s + 1]) (ranks + 1 entries, equal
+ * tile counts).  ranks <= blocks. */
 int wfk_slab_plan(int32_t rows, const int32_t* row_work, int32_t blocks, int32_t block_threads, int32_t ranks,
-                  int32_t* tile_rows, int32_t* rank_tiles);
+                  int32_t* n_tiles, int32_t* tile_rows, int32_t* rank_tiles);
 /* NormalEquations::multiply (solver.cpp:71-89) on an explicit system */
 int wfk_ne_multiply(wfk_ctx* ctx, int32_t rows, const double* blocks, const int32_t* cols,
                     const double* x, double* y);

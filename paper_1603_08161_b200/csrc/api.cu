@@ -525,22 +525,22 @@ int wfk_dist_plan(int32_t rows, const int32_t* cols, int32_t world, int32_t* ran
 }
 
 int wfk_slab_plan(int32_t rows, const int32_t* row_work, int32_t blocks, int32_t block_threads, int32_t ranks,
-                  int32_t* tile_rows, int32_t* rank_tiles) {
-  if (rows < 0 || blocks < 1 || block_threads < 1 || ranks < 1 || !tile_rows || !rank_tiles ||
-      (rows > 0 && !row_work))
+                  int32_t* n_tiles, int32_t* tile_rows, int32_t* rank_tiles) {
+  if (rows < 0 || blocks < 1 || block_threads < 1 || ranks < 1 || ranks > blocks || !n_tiles || !tile_rows ||
+      !rank_tiles || (rows > 0 && !row_work))
     return WFK_E_INVALID_ARG;
   try {
-    const int T = slab_tile_rows(rows, blocks, block_threads);
-    const int ntiles = std::max(1, (rows + T - 1) / T);
-    if (ranks > std::min(blocks, ntiles)) return WFK_E_INVALID_ARG;
-    std::vector<int64_t> prefix(size_t(ntiles), 0);
+    const int nt = slab_tile_count(rows, blocks, block_threads);
+    std::vector<int32_t> incl(size_t(std::max(rows, 1)), 0);
     int64_t acc = 0;
-    for (int r = 0, t = 0; r < rows; ++r) {
+    for (int r = 0; r < rows; ++r) {
       acc += row_work[r];
-      if (r + 1 == std::min(rows, (t + 1) * T)) prefix[size_t(t++)] = acc;
+      if (row_work[r] < 0 || acc > INT32_MAX) return WFK_E_INVALID_ARG;
+      incl[size_t(r)] = int32_t(acc);
     }
-    slab_split(ntiles, prefix.data(), ranks, rank_tiles);
-    *tile_rows = T;
+    for (int t = 0; t <= nt; ++t) tile_rows[t] = slab_tile_bound_host(t, nt, rows, incl.data());
+    slab_split(nt, ranks, rank_tiles);
+    *n_tiles = nt;
   } catch (const Error& e) {
     return e.code;
   }

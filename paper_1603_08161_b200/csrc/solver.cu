@@ -610,13 +610,14 @@ struct PackVecs {
 // rank reaches another rank through is an array entry per rank -- on one GPU
 // (S virtual ranks = block groups of one cooperative launch) they point into
 // one allocation; across GPUs they are peer pointers to the other GPUs'
-// buffers.  The rows are cut into tiles of T rows; a rank owns a contiguous
-// range of tiles (a z-slab, balanced by work), and every dot product is summed
+// buffers.  The rows are cut into tiles of about equal work; a rank owns a
+// contiguous range of tiles (a z-slab), and every dot product is summed
 // per tile (fixed thread -> row map and block tree) and then over the tiles in
 // tile order, so the result does not depend on S or on which block ran a tile.
 struct SlabDev {
   int S;                           // ranks; 0 = not partitioned
-  int T, ntiles;                   // rows per tile, tiles
+  int ntiles;                      // tiles
+  const int32_t* tile_row;         // ntiles + 1: tile t = rows [tile_row[t], tile_row[t + 1])
   const int32_t* rank_tile;        // S + 1: rank s owns tiles [rank_tile[s], rank_tile[s + 1])
   const int32_t* win_lo;           // S: first row of rank s's u window (own rows + halo)
   const int32_t* win_hi;           // S
@@ -1488,8 +1489,8 @@ __device__ __forceinline__ SlabRank slab_rank(const FFArgs& a) {
   k.nb = slab_bstart(s + 1, k.S, k.G) - k.b0;
   k.t0 = a.slab.rank_tile[s];
   k.t1 = a.slab.rank_tile[s + 1];
-  k.lo = min(a.N, k.t0 * a.slab.T);
-  k.hi = min(a.N, k.t1 * a.slab.T);
+  k.lo = a.slab.tile_row[k.t0];
+  k.hi = a.slab.tile_row[k.t1];
   k.wlo = a.slab.win_lo[s];
   k.uw = a.slab.uwin[s];
   return k;
@@ -1577,10 +1578,9 @@ __device__ __forceinline__ void slab_tile_flush(const FFArgs& a, const SlabRank&
 template <int NV, class F>
 __device__ __forceinline__ void slab_for_tiles(const FFArgs& a, const SlabRank& k, SlabTileSm& sm,
                                                const int (&slot)[NV], unsigned seq, F f) {
-  const int T = a.slab.T;
   int tl = 0, t_first = k.t0 + (int(blockIdx.x) - k.b0);
   for (int t = t_first; t < k.t1; t += k.nb) {
-    const int r0 = min(a.N, t * T), r1 = min(a.N, r0 + T);
+    const int r0 = a.slab.tile_row[t], r1 = a.slab.tile_row[t + 1];
     double v[NV];
 #pragma unroll
     for (int j = 0; j < NV; ++j) v[j] = 0;
@@ -1744,7 +1744,6 @@ __device__ void pcg_slab(const FFArgs& a, Red& rs, int& iters, double& relres) {
   unsigned& gen = rs.sl_gen;
   unsigned& epoch = rs.sl_epoch;
   unsigned& seq = rs.sl_seq;
-  const int T = a.slab.T;
   iters = 0;
   relres = 0;
   PhaseClock pc(a.dbg);
@@ -1755,8 +1754,7 @@ __device__ void pcg_slab(const FFArgs& a, Red& rs, int& iters, double& relres) {
   slab_cons(a, k, a.x, pv.contrib);
   slab_sync(a, k, gen, false, epoch);
   for (int t = k.t0 + (int(blockIdx.x) - k.b0); t < k.t1; t += k.nb) {
-    const int r0 = min(a.N, t * T), r1 = min(a.N, r0 + T);
-    slab_items(a, k, r0, r1, a.x, pv.contrib, pv.wpart, none);
+    slab_items(a, k, a.slab.tile_row[t], a.slab.tile_row[t + 1], a.x, pv.contrib, pv.wpart, none);
   }
   __syncthreads();
   {
@@ -3045,11 +3043,22 @@ __global__ void k_slab_weight(int N, const int32_t* row_ptr, int32_t* w) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x)
     w[r] = 12 + (row_ptr[r + 1] - row_ptr[r]);
 }
-// inclusive work prefix at the end of every tile (the rank split is taken on
-// the host from these ntiles values)
-__global__ void k_slab_tile_weight(int N, int T, int ntiles, const int32_t* incl, int64_t* tw) {
+// Tile t starts at the first row whose inclusive work prefix exceeds
+// t W / ntiles (host and device share the rule: wfk_slab_plan, k_slab_tiles).
+__host__ __device__ inline int slab_tile_bound(int t, int ntiles, int N, const int32_t* incl) {
+  if (t <= 0 || N == 0) return 0;
+  if (t >= ntiles) return N;
+  const int64_t target = int64_t(t) * incl[N - 1] / ntiles;
+  int lo = 0, hi = N;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (incl[mid] > target) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+__global__ void k_slab_tiles(int N, int ntiles, const int32_t* incl, int32_t* tile_row) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < ntiles) tw[t] = incl[min(N, (t + 1) * T) - 1];
+  if (t <= ntiles) tile_row[t] = slab_tile_bound(t, ntiles, N, incl);
 }
 // constraints incident to each rank's rows: count (fill == nullptr) or list
 __global__ void k_slab_cons(int64_t C, int S, const int32_t* rank_lo, const int4* c_row, const int4* c_pos,
@@ -3101,54 +3110,45 @@ static void level_items(wfk_ctx* c, Level& L) {
 // Slab plan of a prepared matrix-free level for S ranks over G blocks (see
 // pcg_slab): rank row ranges, u windows (checked to reach only the adjacent
 // ranks), per-rank constraint lists and the reduction state; fills a.slab.
-// Host side of the slab plan, shared with wfk_slab_plan (tests): rows per
-// tile -- about 8 tiles per block and at least one row per thread, from N and
-// G only -- and the rank split: contiguous tile ranges of about equal work,
-// every rank at least one tile.
-int slab_tile_rows(int N, int G, int tpb) {
-  return std::max(tpb, int((int64_t(N) + 8 * G - 1) / (8 * G) + 31) / 32 * 32);
+// Host side of the slab plan, shared with wfk_slab_plan (tests): the tile
+// count -- one tile per block per blockDim rows, between 1 and 8 per block,
+// from N and G only -- and the rank split: rank s owns tiles
+// [s ntiles / S, (s + 1) ntiles / S) (tiles carry about equal work).
+int slab_tile_count(int N, int G, int tpb) {
+  const int64_t per_block = int64_t(N) / (int64_t(G) * tpb);
+  return G * int(std::max<int64_t>(1, std::min<int64_t>(8, per_block)));
 }
-void slab_split(int ntiles, const int64_t* tile_prefix, int S, int32_t* rank_tile) {
-  rank_tile[0] = 0;
-  rank_tile[S] = ntiles;
-  const int64_t W = ntiles > 0 ? tile_prefix[ntiles - 1] : 0;
-  int t = 0;
-  for (int k = 1; k < S; ++k) {
-    const int64_t target = W * k / S;
-    while (t < ntiles && tile_prefix[t] <= target) ++t;
-    rank_tile[k] = std::max(rank_tile[k - 1] + 1, std::min(t, ntiles - (S - k)));
-  }
+void slab_split(int ntiles, int S, int32_t* rank_tile) {
+  for (int k = 0; k <= S; ++k) rank_tile[k] = int32_t((int64_t(k) * ntiles) / S);
 }
+int slab_tile_bound_host(int t, int ntiles, int N, const int32_t* incl) { return slab_tile_bound(t, ntiles, N, incl); }
 
 static void slab_plan(wfk_ctx* c, Level& L, int S, int G, FFArgs& a) {
   cudaStream_t s = c->stream;
   const int N = L.N;
-  // tiles: about 8 per block and at least one row per thread, whatever S is
-  // (T depends on N and G only)
-  const int T = slab_tile_rows(N, G, kFastBlock);
-  const int ntiles = std::max(1, (N + T - 1) / T);
-  S = std::max(1, std::min(S, std::min(G, ntiles)));
-  // work prefix per row, read at the tile ends: ranks get contiguous tile
-  // ranges of about equal work
-  int32_t* wgt = L.sl_blk.ensure(2 * size_t(std::max(N, 1)) + 2 * size_t(ntiles) + 2);
+  // tiles of about equal work (12 units per row + 1 per incidence), their
+  // count from N and G only; ranks take equal numbers of consecutive tiles
+  const int ntiles = slab_tile_count(N, G, kFastBlock);
+  S = std::max(1, std::min(S, G));
+  int32_t* wgt = L.sl_blk.ensure(2 * size_t(std::max(N, 1)) + size_t(ntiles) + 1);
   int32_t* incl = wgt + std::max(N, 1);
-  int64_t* d_tw = reinterpret_cast<int64_t*>(L.sl_red.ensure(size_t(ntiles) + 1));
-  std::vector<int64_t> tw(size_t(ntiles), 0);
+  int32_t* d_trow = incl + std::max(N, 1);
   if (N > 0) {
     k_slab_weight<<<grid_for(N), kBlock, 0, s>>>(N, L.row_ptr, wgt);
     size_t tmp = 0;
     cub::DeviceScan::InclusiveSum(nullptr, tmp, wgt, incl, N, s);
     c->temp.ensure(tmp);
     WFK_CUDA(cub::DeviceScan::InclusiveSum(c->temp.p, tmp, wgt, incl, N, s));
-    k_slab_tile_weight<<<(ntiles + kBlock - 1) / kBlock, kBlock, 0, s>>>(N, T, ntiles, incl, d_tw);
-    count_launch(c, 3);
-    WFK_CUDA(cudaMemcpyAsync(tw.data(), d_tw, tw.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    sync_check(c);
   }
+  k_slab_tiles<<<(ntiles + 1 + kBlock - 1) / kBlock, kBlock, 0, s>>>(N, ntiles, incl, d_trow);
+  count_launch(c, 3);
+  std::vector<int32_t> trow(size_t(ntiles) + 1);
+  WFK_CUDA(cudaMemcpyAsync(trow.data(), d_trow, trow.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  sync_check(c);
   std::vector<int32_t> rt(size_t(S) + 1, 0);  // rank tile bounds
-  slab_split(ntiles, tw.data(), S, rt.data());
+  slab_split(ntiles, S, rt.data());
   std::vector<int32_t> lo(size_t(S) + 1);
-  for (int k = 0; k <= S; ++k) lo[size_t(k)] = std::min(N, rt[size_t(k)] * T);
+  for (int k = 0; k <= S; ++k) lo[size_t(k)] = trow[size_t(rt[size_t(k)])];
   // device index area: rank_tile (S+1) | rank_lo (S+1) | win_lo (S) | win_hi (S) | con_ptr (S+1) | cnt (S) | list
   const size_t o_lo = size_t(S) + 1, o_wlo = o_lo + S + 1, o_whi = o_wlo + S, o_cptr = o_whi + S,
                o_cnt = o_cptr + S + 1, o_list = o_cnt + S;
@@ -3226,8 +3226,8 @@ static void slab_plan(wfk_ctx* c, Level& L, int S, int G, FFArgs& a) {
   WFK_CUDA(cudaMemcpyAsync(d_ptr, ptr.data(), ptr.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
   sync_check(c);  // the host vectors above go out of scope
   a.slab.S = S;
-  a.slab.T = T;
   a.slab.ntiles = ntiles;
+  a.slab.tile_row = d_trow;
   a.slab.rank_tile = d_rt;
   a.slab.win_lo = d_wlo;
   a.slab.win_hi = d_whi;

@@ -14,10 +14,11 @@ void solver_energy(wfk_ctx* c, const wfk_pose* pose, const wfk_solver_params& p,
 void solver_rotations(wfk_ctx* c);
 void solver_c2f(wfk_ctx* c, const wfk_pose* pose, const wfk_solver_params& p, std::vector<wfk_trace_entry>& trace);
 void solver_hierarchy_info(wfk_ctx* c, int levels, int32_t* dims, int64_t* active);
-// slab plan of the in-kernel partitioned CG (host part): rows per tile and
-// the rank split over the tiles' work prefix (solver.cu)
-int slab_tile_rows(int N, int G, int tpb);
-void slab_split(int ntiles, const int64_t* tile_prefix, int S, int32_t* rank_tile);
+// slab plan of the in-kernel partitioned CG (host part, solver.cu): tile
+// count, tile bounds from the inclusive row-work prefix, rank split
+int slab_tile_count(int N, int G, int tpb);
+int slab_tile_bound_host(int t, int ntiles, int N, const int32_t* incl);
+void slab_split(int ntiles, int S, int32_t* rank_tile);
 int solver_build_ne(wfk_ctx* c, const wfk_pose* pose, const wfk_solver_params& p, wfk_ne_host* out);
 void solver_pcg_assembled(wfk_ctx* c, int N, const double* blocks, const int32_t* cols, const double* rhs, double* x,
                           double tol, int max_iters, int mode, wfk_pcg_result* res, double* y);

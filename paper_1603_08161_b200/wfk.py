@@ -129,16 +129,17 @@ def dist_plan(cols, world: int):
 
 
 def slab_plan(row_work, blocks: int, block_threads: int, ranks: int):
-    """The in-kernel slab partition's host plan (wfk_slab_plan, no GPU): rows
-    per tile and the rank tile bounds (ranks + 1)."""
+    """The in-kernel slab partition's host plan (wfk_slab_plan, no GPU): the
+    tile row bounds (n_tiles + 1) and the rank tile bounds (ranks + 1)."""
     w = np.ascontiguousarray(row_work, np.int32)
-    t = C.c_int32()
+    nt = C.c_int32()
+    tr = np.zeros(8 * blocks + 1, np.int32)
     rt = np.zeros(ranks + 1, np.int32)
     rc = lib().wfk_slab_plan(C.c_int32(len(w)), _cptr(w), C.c_int32(blocks), C.c_int32(block_threads),
-                             C.c_int32(ranks), C.byref(t), _cptr(rt))
+                             C.c_int32(ranks), C.byref(nt), _cptr(tr), _cptr(rt))
     if rc != WFK_OK:
         raise WfkError(rc, "wfk_slab_plan failed")
-    return t.value, rt
+    return tr[: nt.value + 1], rt
 
 
 class _Pinned:

@@ -4,8 +4,8 @@ SURVEY.md 8(e)) on the CPU.
 The device kernel runs the ranks as block groups of one cooperative launch;
 what makes it a multi-GPU design is its plan and its protocol, and those are
 what these tests exercise across real process boundaries:
-  * the host plan (`wfk_slab_plan`, libwfk's own code): tiles of T rows and
-    the rank split into contiguous tile ranges of about equal work;
+  * the host plan (`wfk_slab_plan`, libwfk's own code): tiles of about equal
+    work and the rank split into contiguous, equal tile ranges;
   * each rank's u window (its rows plus the rows its rows' stencil reaches)
     lies within its two neighbours' rows;
   * the per-iteration protocol over two gloo processes: a rank updates only
@@ -30,7 +30,7 @@ from paper_1603_08161_b200.abi import Pose, SolverParams
 from tests.fixtures import active_sphere_volume, rigid_motion_constraints
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-BLOCKS, THREADS = 16, 32   # a small virtual grid: T = max(32, N / 128)
+BLOCKS, THREADS = 16, 32   # a small virtual grid: 16 x clamp(N / 512, 1, 8) tiles
 
 
 def system(n=12, voxel=0.05):
@@ -57,10 +57,9 @@ def windows(cols, lo):
 
 
 def plan(cols, ranks):
-    n = len(cols)
-    T, rt = wfk.slab_plan(row_work(cols), BLOCKS, THREADS, ranks)
-    lo = [min(n, int(t) * T) for t in rt]
-    return T, rt, lo, windows(cols, lo)
+    tr, rt = wfk.slab_plan(row_work(cols), BLOCKS, THREADS, ranks)
+    lo = [int(tr[t]) for t in rt]
+    return tr, rt, lo, windows(cols, lo)
 
 
 @pytest.mark.parametrize("ranks", [1, 2, 3, 4])
@@ -68,15 +67,15 @@ def test_plan_split_and_windows(ranks):
     ne = system()
     cols = ne.cols
     n = len(cols)
-    T, rt, lo, win = plan(cols, ranks)
-    assert T >= THREADS and T % 32 == 0
-    ntiles = (n + T - 1) // T
+    tr, rt, lo, win = plan(cols, ranks)
+    ntiles = len(tr) - 1
+    assert ntiles % BLOCKS == 0 and BLOCKS <= ntiles <= 8 * BLOCKS
+    assert tr[0] == 0 and tr[-1] == n and np.all(np.diff(tr) >= 0)
     assert rt[0] == 0 and rt[-1] == ntiles and np.all(np.diff(rt) >= 1)
-    # about equal work per rank: within one tile's work of the mean
+    # tiles of about equal work: within one row's work of the mean
     w = row_work(cols)
-    per = [int(w[lo[s]:lo[s + 1]].sum()) for s in range(ranks)]
-    tile_max = max(int(w[t * T:(t + 1) * T].sum()) for t in range(ntiles))
-    assert max(per) - min(per) <= 2 * tile_max
+    tw = np.array([int(w[tr[t]:tr[t + 1]].sum()) for t in range(ntiles)])
+    assert tw.max() - tw.min() <= 2 * int(w.max())
     for s, (a, b) in enumerate(win):
         assert a >= (lo[s - 1] if s > 0 else 0), "halo beyond the lower neighbour"
         assert b <= (lo[s + 2] if s + 2 <= ranks else n), "halo beyond the upper neighbour"
@@ -84,7 +83,7 @@ def test_plan_split_and_windows(ranks):
 
 def test_plan_rejects_bad_arguments():
     with pytest.raises(wfk.WfkError):
-        wfk.slab_plan(np.full(64, 12, np.int32), 4, 32, 3)   # 2 tiles, 3 ranks
+        wfk.slab_plan(np.full(64, 12, np.int32), 4, 32, 5)   # more ranks than blocks
 
 
 def _apply(blocks, cols, v_of, r0, r1):
@@ -103,10 +102,10 @@ def slab_cg(ne, ranks, rank, comm, iters):
     callbacks (None for a single rank).  Returns (d of own rows, lo, hi)."""
     blocks, cols, rhs = ne.blocks, ne.cols, ne.rhs
     n = len(cols)
-    T, rt, lo_all, win = plan(cols, ranks)
+    tr, rt, lo_all, win = plan(cols, ranks)
     lo, hi = lo_all[rank], lo_all[rank + 1]
     wlo, whi = win[rank]
-    ntiles = (n + T - 1) // T
+    ntiles = len(tr) - 1
     my_tiles = range(rt[rank], rt[rank + 1])
     u_win = np.zeros((whi - wlo, 3))            # own rows + halo
     u_of = lambda idx: u_win[idx - wlo]          # noqa: E731
@@ -121,7 +120,7 @@ def slab_cg(ne, ranks, rank, comm, iters):
     def tile_sums(terms):  # terms[j] : (n,) per-row values of own rows
         part = np.zeros((ntiles, len(terms)))
         for t in my_tiles:
-            a, b = t * T, min(n, (t + 1) * T)
+            a, b = tr[t], tr[t + 1]
             for j, v in enumerate(terms):
                 part[t, j] = np.sum(v[a:b])
         if comm is not None:
@@ -199,7 +198,7 @@ def _rank_main(rank, world, port, ne_arrays, iters, out):
                         reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(u_win[a - wlo:b - wlo])), nb))
             for nb in (rank - 1, rank + 1):
                 if 0 <= nb < world:
-                    T, rt, lo_all, _ = plan(ne.cols, world)
+                    _, _, lo_all, _ = plan(ne.cols, world)
                     a, b = max(lo_all[nb], win[rank][0]), min(lo_all[nb + 1], win[rank][1])
                     if b > a:
                         buf = torch.zeros((b - a, 3), dtype=torch.float64)
