@@ -2987,10 +2987,15 @@ static void level_constraints(wfk_ctx* c, Level& L, const PoseD& pose, const wfk
     const int soa = N >= kAsmThreadRows ? 1 : 0;  // rows on lanes read slot-major blocks
     L.blk.ensure(size_t(N) * 27 * 6);
     L.cols.ensure(size_t(N) * 27);
-    static unsigned long long asm_attr = 0;  // bit d: device d configured
-    if (!(asm_attr & (1ull << (c->device & 63)))) {
-      WFK_CUDA(cudaFuncSetAttribute(k_assemble_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kAsmSmem)));
-      asm_attr |= 1ull << (c->device & 63);
+    {
+      // per device, under a lock (contexts on several devices / threads)
+      static std::mutex asm_mu;
+      static unsigned long long asm_attr = 0;  // bit d: device d configured
+      std::lock_guard<std::mutex> lock(asm_mu);
+      if (!(asm_attr & (1ull << (c->device & 63)))) {
+        WFK_CUDA(cudaFuncSetAttribute(k_assemble_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kAsmSmem)));
+        asm_attr |= 1ull << (c->device & 63);
+      }
     }
     k_assemble_rows<<<std::min((N + kAsmWarps - 1) / kAsmWarps, c->num_sms * 2), kAsmWarps * 32, kAsmSmem, s>>>(
         L.g, N, L.rows, L.node_row, L.row_ptr, L.ent_con, L.ent_k, L.ent_w, L.c_w, L.c_g, L.c_b, L.c_kind, L.blk,
