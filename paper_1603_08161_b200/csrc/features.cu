@@ -40,9 +40,11 @@ static Taps blur_taps(double sigma) {
 }
 
 // capacity for size-varying scratch (extrema, store, matches): powers of two
-// from 16384, so growth (cudaFree synchronises the device) is rare
+// from 65536, so growth (cudaMalloc / cudaFree synchronise the device: one
+// 47 ms frame where the configs[2] store passed 16 K entries at frame 298) is
+// rare -- the 300-frame sequence's store ends at 16.4 K entries
 static size_t cap_for(size_t n) {
-  size_t c = 16384;
+  size_t c = 65536;
   while (c < n) c *= 2;
   return c;
 }

@@ -653,7 +653,8 @@ struct FFArgs {
   double4* nbuf;         // pipelined PCG: n = A m of the rows a thread leads
   unsigned long long* sync_ll;  // split-reduction totals (flag-embedded words)
   int meta_rows, meta_cons;     // pipelined matrix-free levels: metadata cached in shared memory
-  int asm_smem;                 // pipelined assembled levels: B^T B rows cached in shared memory
+  int asm_smem;                 // pipelined assembled levels: row slots whose B^T B is cached in shared
+                                // memory (round-major: a partial last round may stay in global), or 0
   double* state_spill;          // pipelined PCG row state in global memory (too many rows for shared), or null
   const int32_t* perm;          // pipelined matrix-free levels: row order (decreasing incidences), or null
   int pcg_variant;       // 0 pipelined (one reduction, overlapped), 1 Chronopoulos-Gear
@@ -1029,7 +1030,7 @@ __device__ __forceinline__ V3 laplacian(const FFArgs& a, const double4* v, int r
 //    Laplacian into the six face slots, then a sub-warp shuffle tree;
 //  * large levels (asm_rows_on_lanes): one row per lane over slot-major blocks.
 // (Matrix-free levels: row_pass_mf, or item_pass in the Chronopoulos-Gear PCG.)
-template <bool ASM, class Sink, class Sl = std::nullptr_t>
+template <bool ASM, int AL = kAsmLanes, class Sink, class Sl = std::nullptr_t>
 __device__ __forceinline__ void row_pass(const FFArgs& a, const double4* v, Sink& sink, int skip = 0,
                                          const Sl* sl = nullptr, const double* smb = nullptr,
                                          const int* smc = nullptr) {
@@ -1064,7 +1065,7 @@ __device__ __forceinline__ void row_pass(const FFArgs& a, const double4* v, Sink
     return;
   }
   if (ASM) {
-    constexpr int L = kAsmLanes, RPW = 32 / L;
+    constexpr int L = AL, RPW = 32 / L;
     const int sub = lane % L, grp = lane / L;
     for (int base = (gwarp() - skip) * RPW; base < a.N; base += (nwarps() - skip) * RPW) {
       const int r = base + grp;
@@ -1076,9 +1077,11 @@ __device__ __forceinline__ void row_pass(const FFArgs& a, const double4* v, Sink
       const int* cc = a.cols + int64_t(r) * 27;
       if constexpr (!std::is_same<Sl, std::nullptr_t>::value) {
         if (smb && live) {  // the solve's blocks of this warp's rows, cached in shared memory
-          const int q = sl->of(r);
-          bb = smb + q * 27 * 6;
-          cc = smc + q * 27;
+          const int q = sl->amat_of(r);
+          if (q < a.asm_smem) {
+            bb = smb + q * 27 * 6;
+            cc = smc + q * 27;
+          }
         }
       }
       if (live && !frozen) {
@@ -2032,7 +2035,19 @@ __device__ __forceinline__ void row_pass_mf(const FFArgs& a, const double4* v, S
     const V3 vr = live ? ld4(v, r) : V3{0, 0, 0};
     V3 acc{0, 0, 0};
     if (live && !frozen) {
-      for (int e = e0 + sub; e < e1; e += L) acc += ld4(a.contrib, e);
+      // the row's contributions in incidence order, eight loads in flight
+      // before their (sequential, order-preserving) adds: a heavy row late in
+      // a sequence (hundreds of incidences on two lanes) otherwise pays one
+      // L2 round trip per few contributions
+      int e = e0 + sub;
+      for (; e + 7 * L < e1; e += 8 * L) {
+        V3 t[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) t[i] = ld4(a.contrib, e + i * L);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc += t[i];
+      }
+      for (; e < e1; e += L) acc += ld4(a.contrib, e);
 #pragma unroll
       for (int k2 = sub; k2 < 6; k2 += L) {
         const int j = nb[k2];
@@ -2176,6 +2191,11 @@ struct SlotsT {
   __device__ __forceinline__ int of(int r) const {
     return int(threadIdx.x >> 5) * K * RPW + ((r / RPW - gw) / nw) * RPW + r % RPW;
   }
+  // round-major slot of the cached B^T B (assembled levels): the first rounds
+  // first, so a partial last round is what stays in global memory
+  __device__ __forceinline__ int amat_of(int r) const {
+    return ((r / RPW - gw) / nw) * int(blockDim.x >> 5) * RPW + int(threadIdx.x >> 5) * RPW + r % RPW;
+  }
   // component-major: (vector, component, slot) -- 24 bytes per 3-vector
   __device__ __forceinline__ double4 get(int v, int q) const {
     const double* b = reinterpret_cast<const double*>(sm) + size_t(3 * v) * stride + q;
@@ -2188,8 +2208,8 @@ struct SlotsT {
     b[2 * stride] = x.z;
   }
 };
-__host__ __device__ constexpr int pipe_rpw(bool asm_level, bool rows_on_lanes) {
-  return rows_on_lanes ? 32 : 32 / (asm_level ? kAsmLanes : kMfLanes);
+__host__ __device__ constexpr int pipe_rpw(bool asm_level, bool rows_on_lanes, int asm_lanes = kAsmLanes) {
+  return rows_on_lanes ? 32 : 32 / (asm_level ? asm_lanes : kMfLanes);
 }
 // Shared-memory layout of one pipelined solve (host and device compute it
 // alike): the row-state slots; on matrix-free levels optionally each row
@@ -2202,7 +2222,7 @@ struct PipeLayout {
   size_t rmeta, cmeta, amat, total;  // byte offsets / size
 };
 __host__ __device__ inline PipeLayout pipe_layout(int N, int64_t C, int rpw, int G, int tpb, int skip, bool rows,
-                                                  bool cons, bool amat = false, int state_vecs = kSlotVecs) {
+                                                  bool cons, int amat_slots = 0, int state_vecs = kSlotVecs) {
   PipeLayout l;
   const int wpb = tpb / 32;
   const int nw = G * wpb - skip;
@@ -2219,8 +2239,8 @@ __host__ __device__ inline PipeLayout pipe_layout(int N, int64_t C, int rpw, int
   l.cmeta = off;
   if (cons) off += size_t(l.SC) * (4 * sizeof(int4) + 3 * sizeof(double4) + sizeof(int));
   off = (off + 31) / 32 * 32;
-  l.amat = off;  // assembled levels: 27 x 6 block values + 27 columns per row slot
-  if (amat) off += size_t(l.S) * 27 * (6 * sizeof(double) + sizeof(int));
+  l.amat = off;  // assembled levels: 27 x 6 block values + 27 columns per cached row slot
+  off += size_t(amat_slots) * 27 * (6 * sizeof(double) + sizeof(int));
   l.total = off;
   return l;
 }
@@ -2276,7 +2296,7 @@ constexpr size_t kPipeSmemMax = 220 * 1024;  // dynamic shared memory for the ro
 // Only m (gathered by neighbours) lives in global memory; x, r, w, p, s, z,
 // D^-1 and n stay in the shared-memory slots of the warp that owns the row.
 // Stopping rule, breakdown test and iteration count are the reference's.
-template <bool ASM, int NSM>
+template <bool ASM, int NSM, int AL = kAsmLanes>
 __device__ __forceinline__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, double& relres) {
   extern __shared__ double4 dyn_smem[];
   iters = 0;
@@ -2284,14 +2304,14 @@ __device__ __forceinline__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, d
   PhaseClock pc(a.dbg);
   constexpr int kSkip = kPipeSkip;
   const bool comm = gwarp() == 0;
-  constexpr int LM = ASM ? kAsmLanes : kMfLanes;
+  constexpr int LM = ASM ? AL : kMfLanes;
   const bool rows_on_lanes = ASM && a.asm_rows_on_lanes;
   SlotsT<NSM> sl;
   sl.sm = dyn_smem;
-  sl.RPW = pipe_rpw(ASM, rows_on_lanes);
-  const bool amat = ASM && a.asm_smem && !rows_on_lanes;
+  sl.RPW = pipe_rpw(ASM, rows_on_lanes, AL);
+  const bool amat = ASM && a.asm_smem > 0 && !rows_on_lanes;
   const PipeLayout lay = pipe_layout(a.N, a.C, sl.RPW, gridDim.x, blockDim.x, kSkip, !ASM && a.meta_rows,
-                                     !ASM && a.meta_cons, amat, a.state_spill ? 0 : kSlotVecs);
+                                     !ASM && a.meta_cons, amat ? a.asm_smem : 0, a.state_spill ? 0 : kSlotVecs);
   sl.K = lay.K;
   sl.S = lay.S;
   sl.stride = size_t(lay.S);
@@ -2304,7 +2324,7 @@ __device__ __forceinline__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, d
   const MfMeta mm = mf_meta(reinterpret_cast<char*>(dyn_smem), lay, !ASM && a.meta_rows, !ASM && a.meta_cons);
   const MfMeta* mmp = ASM ? nullptr : &mm;
   double* smb = amat ? reinterpret_cast<double*>(reinterpret_cast<char*>(dyn_smem) + lay.amat) : nullptr;
-  int* smc = amat ? reinterpret_cast<int*>(reinterpret_cast<char*>(dyn_smem) + lay.amat + size_t(lay.S) * 27 * 48)
+  int* smc = amat ? reinterpret_cast<int*>(reinterpret_cast<char*>(dyn_smem) + lay.amat + size_t(a.asm_smem) * 27 * 48)
                   : nullptr;
   if (amat && gwarp() >= kSkip) {
     // this warp's rows of B^T B into shared memory (fixed for the whole solve)
@@ -2312,7 +2332,8 @@ __device__ __forceinline__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, d
     for (int idx = 0; idx < sl.K * sl.RPW; ++idx) {
       const int r = (sl.gw + (idx / sl.RPW) * sl.nw) * sl.RPW + idx % sl.RPW;
       if (r >= a.N) break;
-      const int q = sl.of(r);
+      const int q = sl.amat_of(r);
+      if (q >= a.asm_smem) continue;  // beyond the cached slots: read from global in the row pass
       for (int t = lane; t < 27 * 6; t += 32) smb[q * 27 * 6 + t] = a.blk[int64_t(r) * 27 * 6 + t];
       if (lane < 27) smc[q * 27 + lane] = a.cols[int64_t(r) * 27 + lane];
     }
@@ -2323,9 +2344,9 @@ __device__ __forceinline__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, d
     if (ASM) {
       auto sink3 = [&](int r, V3 vr, V3 av) { sink4(r, sl.of(r), vr, av); };
       if (amat)
-        row_pass<true>(a, v, sink3, kSkip, &sl, smb, smc);
+        row_pass<true, AL>(a, v, sink3, kSkip, &sl, smb, smc);
       else
-        row_pass<true>(a, v, sink3, kSkip);
+        row_pass<true, AL>(a, v, sink3, kSkip);
     } else {
       matvec_constraints(a, v, kSkip, mmp);
       grid_barrier(a, rs);
@@ -2531,7 +2552,7 @@ __device__ __forceinline__ void rotations(const FFArgs& a) {
 // One instantiation per (PCG variant, level kind): each carries only the PCG
 // code it runs, so the register allocation of one variant does not spill
 // another's hot loops.
-template <int V, bool ASM, int NSM = kSlotVecs, int TPB = kCoopBlock>
+template <int V, bool ASM, int NSM = kSlotVecs, int TPB = kCoopBlock, int AL = kAsmLanes>
 __global__ void __launch_bounds__(TPB, 1) k_flip_flop(FFArgs a) {
   cg::grid_group grid = cg::this_grid();
   Red rs;
@@ -2583,7 +2604,7 @@ __global__ void __launch_bounds__(TPB, 1) k_flip_flop(FFArgs a) {
       } else if (V == 1)
         pcg<ASM>(a, grid, rs, iters, relres);
       else
-        pcg_pipe<ASM, NSM>(a, rs, iters, relres);
+        pcg_pipe<ASM, NSM, AL>(a, rs, iters, relres);
       total_pcg += iters;
       pc.lap(9);
       // write back non-frozen rows (solver.cpp:436-437)
@@ -3365,6 +3386,7 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   size_t smem = 0;
   int nsm = kSlotVecs;  // kSlotVecs: row state in shared memory; 0: spilled (pipelined PCG)
   int tpb = kCoopBlock;  // threads per block of the launch
+  int asm_lanes = kAsmLanes;  // lanes per row of a pipelined assembled level (8 or 4)
   a.meta_rows = a.meta_cons = 0;
   a.asm_smem = 0;
   a.state_spill = nullptr;
@@ -3379,7 +3401,17 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
     if (probe.total > kPipeSmemMax) a.pcg_variant = 1;
   }
   if (a.pcg_variant == 0) {
-    const int rpw = pipe_rpw(L.assembled, a.asm_rows_on_lanes);
+    // assembled levels: 8 lanes per row (one slot gather per lane per 3-4
+    // slots), or 4 when that saves a whole round of rows -- a level just past
+    // a round boundary (e.g. 128^3 level 1 late in the sequence: 14.8 K rows,
+    // 3 rounds at 8 lanes, 2 at 4) pays a full extra round of gathers
+    if (L.assembled && !a.asm_rows_on_lanes) {
+      const int64_t nw = int64_t(G) * (kCoopBlockShared / 32) - kPipeSkip;
+      const int64_t r8 = (L.N + nw * 4 - 1) / (nw * 4), r4 = (L.N + nw * 8 - 1) / (nw * 8);
+      static const char* lanes_env = getenv("WFK_ASM_LANES_RT");  // A/B: force 8 or 4
+      asm_lanes = lanes_env ? (atoi(lanes_env) == 4 ? 4 : 8) : (r4 < r8 ? 4 : 8);
+    }
+    int rpw = pipe_rpw(L.assembled, a.asm_rows_on_lanes, asm_lanes);
     // the row state goes to a global spill area when it does not fit shared memory
     // shared-memory row state runs with kCoopBlockShared threads per block
     // (more registers per thread: no spills); the spill variant with kCoopBlock
@@ -3387,6 +3419,8 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
     PipeLayout base = pipe_layout(L.N, L.C, rpw, G, tpb, kPipeSkip, false, false);
     const bool spill = base.total > kPipeSmemMax || getenv("WFK_PIPE_SPILL") != nullptr;  // env (any value): tests force the spill area
     if (spill) {
+      asm_lanes = kAsmLanes;  // the spill variant is instantiated with the default lanes
+      rpw = pipe_rpw(L.assembled, a.asm_rows_on_lanes, asm_lanes);
       nsm = 0;
       tpb = kCoopBlock;
       base = pipe_layout(L.N, L.C, rpw, G, tpb, kPipeSkip, false, false);
@@ -3398,16 +3432,21 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
     static const bool no_meta = getenv("WFK_PIPE_NO_META") != nullptr;
     a.asm_smem = 0;
     static const bool no_asm_smem = getenv("WFK_NO_ASM_SMEM") != nullptr;
-    if (L.assembled && !a.asm_rows_on_lanes && !no_meta && !no_asm_smem &&
-        pipe_layout(L.N, L.C, rpw, G, tpb, kPipeSkip, false, false, true, nsm).total <= kPipeSmemMax)
-      a.asm_smem = 1;
+    if (L.assembled && !a.asm_rows_on_lanes && !no_meta && !no_asm_smem) {
+      // as many row slots' B^T B as fit (the rest of a partial last round is
+      // read from global memory)
+      const PipeLayout b0 = pipe_layout(L.N, L.C, rpw, G, tpb, kPipeSkip, false, false, 0, nsm);
+      const size_t per = size_t(27) * (6 * sizeof(double) + sizeof(int));
+      const size_t fit = b0.total < kPipeSmemMax ? (kPipeSmemMax - b0.total) / per : 0;
+      a.asm_smem = int(std::min<size_t>(size_t(b0.S), fit));
+    }
     static const bool cmeta = getenv("WFK_PIPE_CMETA") != nullptr;
     if (!L.assembled && !no_meta && cmeta && bytes(true, true) <= kPipeSmemMax) {
       a.meta_rows = a.meta_cons = 1;
     } else if (!L.assembled && !no_meta && bytes(true, false) <= kPipeSmemMax) {
       a.meta_rows = 1;
     }
-    smem = a.asm_smem ? pipe_layout(L.N, L.C, rpw, G, tpb, kPipeSkip, false, false, true, nsm).total
+    smem = a.asm_smem ? pipe_layout(L.N, L.C, rpw, G, tpb, kPipeSkip, false, false, a.asm_smem, nsm).total
                       : bytes(a.meta_rows, a.meta_cons);
     if (smem > kPipeSmemMax) {
       a.pcg_variant = 1;
@@ -3467,7 +3506,9 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   else if (a.pcg_variant == 1)
     kern = asm_k ? k_flip_flop<1, true> : k_flip_flop<1, false>;
   else if (nsm == kSlotVecs)
-    kern = asm_k ? k_flip_flop<0, true, kSlotVecs, kCoopBlockShared> : k_flip_flop<0, false, kSlotVecs, kCoopBlockShared>;
+    kern = asm_k ? (asm_lanes == 4 ? k_flip_flop<0, true, kSlotVecs, kCoopBlockShared, 4>
+                                   : k_flip_flop<0, true, kSlotVecs, kCoopBlockShared>)
+                 : k_flip_flop<0, false, kSlotVecs, kCoopBlockShared>;
   else
     kern = asm_k ? k_flip_flop<0, true, kSlotsSpill> : k_flip_flop<0, false, kSlotsSpill>;
   // kernel attributes are per device: set once per device, under a lock
@@ -3477,7 +3518,8 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   std::lock_guard<std::mutex> attr_lock(attr_mu);
   if (!(attr_done & (1ull << (c->device & 63)))) {
     for (void (*k)(FFArgs) : {k_flip_flop<0, false, kSlotVecs, kCoopBlockShared>,
-                              k_flip_flop<0, true, kSlotVecs, kCoopBlockShared>, k_flip_flop<1, false>,
+                              k_flip_flop<0, true, kSlotVecs, kCoopBlockShared>,
+                              k_flip_flop<0, true, kSlotVecs, kCoopBlockShared, 4>, k_flip_flop<1, false>,
                               k_flip_flop<1, true>, k_flip_flop<0, false, kSlotsSpill>,
                               k_flip_flop<0, true, kSlotsSpill>})
     {
