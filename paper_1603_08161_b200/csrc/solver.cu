@@ -1987,15 +1987,35 @@ __device__ void pcg(const FFArgs& a, cg::grid_group& grid, Red& rs, int& iters, 
 __device__ __forceinline__ int mf_round(int k, int gw, int nw, bool snake) {
   return k * nw + ((snake && (k & 1)) ? nw - 1 - gw : gw);
 }
+// Position (in the row order) of row-in-round grp of round k of warp gw.  With
+// the decreasing-incidence order (perm) the rounds are dealt in snake order.
+// When the level's heaviest row is very heavy (`hybrid`: more than kHeavyDeal
+// incidences -- late in the configs[2] sequence the sparse term concentrates
+// incidences on a few rows), round 0 is dealt differently: every warp's first
+// row is one of the nw heaviest rows (warp gw takes position gw) and its other
+// RPW - 1 rows are consecutive positions after those; dealing round 0's RPW
+// heaviest rows to warp 0 held every block at the barrier (that warp's row
+// pass 21 K cycles against 9 K on average).  The heaviest kHeavyRows rows are
+// then summed by their whole warp (row_pass_mf).  Without perm: RPW
+// consecutive rows per warp and round.
+__device__ __forceinline__ int mf_pos(int k, int grp, int gw, int nw, int RPW, bool sorted, bool hybrid) {
+  if (hybrid && k == 0) return grp == 0 ? gw : nw + gw * (RPW - 1) + (grp - 1);
+  return mf_round(k, gw, nw, sorted) * RPW + grp;
+}
+constexpr int kHeavyDeal = 96;   // heaviest-row incidences from which round 0 is dealt one heavy row per warp
+constexpr int kHeavyRows = 1024; // that many of the heaviest rows (all in round 0, row 0 of a warp, for any
+                                 // block shape) are summed by their whole warp when above kHeavyRow
+constexpr int kHeavyRow = 32;   // ... incidences
 
 // Matrix-free row pass with kMfLanes lanes per row: the row's contiguous
 // incidence contributions and its six face neighbours are strided over the
 // lanes, a sub-warp shuffle tree sums them (fixed order), and the group
 // leader receives (A v)_r -- so a row is complete inside one warp and its
 // update can follow without another grid barrier.
-template <class Sink, class Meta = std::nullptr_t, class Sl = std::nullptr_t>
+template <bool HY = false, class Sink, class Meta = std::nullptr_t, class Sl = std::nullptr_t>
 __device__ __forceinline__ void row_pass_mf(const FFArgs& a, const double4* v, Sink& sink, int skip = 0,
                                             const Meta* mm = nullptr, const Sl* sl = nullptr) {
+  constexpr bool hybrid = HY;  // a separate instantiation: the common case keeps its code
   constexpr int L = kMfLanes, RPW = 32 / L;
   const int lane = threadIdx.x & 31;
   const int sub = lane % L, grp = lane / L;
@@ -2003,8 +2023,11 @@ __device__ __forceinline__ void row_pass_mf(const FFArgs& a, const double4* v, S
   if (gwarp() < skip) return;
   const int gw = gwarp() - skip, nw = nwarps() - skip;
   for (int k = 0;; ++k) {
-    const int pos = mf_round(k, gw, nw, a.perm != nullptr) * RPW + grp;
-    if (pos - grp >= a.N) break;  // rounds only grow with k
+    const bool sorted = a.perm != nullptr;
+    const int pos = mf_pos(k, grp, gw, nw, RPW, sorted, hybrid);
+    // rounds only grow with k: the warp's round start (hybrid round 0 is not
+    // contiguous: every position of round k is >= k nw RPW)
+    if ((HY ? k * nw * RPW : pos - grp) >= a.N) break;
     const bool live = pos < a.N;
     const int q = int(threadIdx.x >> 5) * (sl ? sl->K : 0) * RPW + k * RPW + grp;  // row slot
     int r = pos, e0 = 0, e1 = 0, nb[6] = {-1, -1, -1, -1, -1, -1};
@@ -2034,20 +2057,39 @@ __device__ __forceinline__ void row_pass_mf(const FFArgs& a, const double4* v, S
     }
     const V3 vr = live ? ld4(v, r) : V3{0, 0, 0};
     V3 acc{0, 0, 0};
-    if (live && !frozen) {
-      // the row's contributions in incidence order, eight loads in flight
-      // before their (sequential, order-preserving) adds: a heavy row late in
-      // a sequence (hundreds of incidences on two lanes) otherwise pays one
-      // L2 round trip per few contributions
-      int e = e0 + sub;
-      for (; e + 7 * L < e1; e += 8 * L) {
-        V3 t[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) t[i] = ld4(a.contrib, e + i * L);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc += t[i];
+    // round 0's first row (one of the heaviest): its contributions summed by
+    // all 32 lanes (butterfly tree) when it has more than kHeavyRow of them
+    bool heavy = false;
+    V3 hsum{0, 0, 0};
+    if constexpr (HY) {
+    if (k == 0 && gw < kHeavyRows) {
+      const int he0 = __shfl_sync(0xffffffffu, e0, 0), he1 = __shfl_sync(0xffffffffu, e1, 0);
+      const int hl = __shfl_sync(0xffffffffu, (live && !frozen) ? 1 : 0, 0);
+      if (hl && he1 - he0 > kHeavyRow) {  // warp-uniform
+        for (int e = he0 + lane; e < he1; e += 32) hsum += ld4(a.contrib, e);
+        hsum.x = warp_sum(hsum.x);
+        hsum.y = warp_sum(hsum.y);
+        hsum.z = warp_sum(hsum.z);
+        heavy = grp == 0;
       }
-      for (; e < e1; e += L) acc += ld4(a.contrib, e);
+    }
+    }
+    if (live && !frozen) {
+      if (heavy) {
+        if (sub == 0) acc = hsum;
+      } else {
+        // the row's contributions in incidence order, eight loads in flight
+        // before their (sequential, order-preserving) adds
+        int e = e0 + sub;
+        for (; e + 7 * L < e1; e += 8 * L) {
+          V3 t[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) t[i] = ld4(a.contrib, e + i * L);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc += t[i];
+        }
+        for (; e < e1; e += L) acc += ld4(a.contrib, e);
+      }
 #pragma unroll
       for (int k2 = sub; k2 < 6; k2 += L) {
         const int j = nb[k2];
@@ -2154,15 +2196,20 @@ __device__ __forceinline__ void split_wait(const FFArgs& a, unsigned seq, double
 // takes row l % RPW of round l / RPW, 32 / RPW rounds per step.  The matvec
 // results were stored by lanes of the same warp, so a __syncwarp orders them.
 template <int L, class F>
-__device__ __forceinline__ void for_warp_rows(int N, int skip, int K, const int32_t* perm, const int* rid, F f) {
+__device__ __forceinline__ void for_warp_rows(int N, int skip, int K, const int32_t* perm, const int* rid, F f,
+                                              bool hybrid = false) {
   constexpr int RPW = 32 / L, RPS = 32 / RPW;
   if (gwarp() < skip) return;
   __syncwarp();
   const int lane = threadIdx.x & 31;
   const int gw = gwarp() - skip, nw = nwarps() - skip;
   for (int k = lane / RPW;; k += RPS) {
-    const int pos = mf_round(k, gw, nw, perm != nullptr) * RPW + lane % RPW;
-    if (pos >= N) break;  // positions grow with k
+    const int pos = mf_pos(k, lane % RPW, gw, nw, RPW, perm != nullptr, hybrid);
+    if (!hybrid && pos >= N) break;  // positions grow with k
+    if (hybrid) {                     // hybrid round 0 is not contiguous
+      if (k * nw * RPW >= N) break;
+      if (pos >= N) continue;
+    }
     const int q = int(threadIdx.x >> 5) * K * RPW + k * RPW + lane % RPW;
     f(rid ? rid[q] : perm ? perm[pos] : pos, q);
   }
@@ -2306,6 +2353,12 @@ __device__ __forceinline__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, d
   const bool comm = gwarp() == 0;
   constexpr int LM = ASM ? AL : kMfLanes;
   const bool rows_on_lanes = ASM && a.asm_rows_on_lanes;
+  // round 0 dealt one heavy row per warp when the level's heaviest row is very heavy (mf_pos)
+  bool hybrid = false;
+  if (!ASM && a.perm && a.N > 0) {
+    const int r0 = a.perm[0];
+    hybrid = a.row_ptr[r0 + 1] - a.row_ptr[r0] > kHeavyDeal;
+  }
   SlotsT<NSM> sl;
   sl.sm = dyn_smem;
   sl.RPW = pipe_rpw(ASM, rows_on_lanes, AL);
@@ -2350,7 +2403,10 @@ __device__ __forceinline__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, d
     } else {
       matvec_constraints(a, v, kSkip, mmp);
       grid_barrier(a, rs);
-      row_pass_mf(a, v, sink4, kSkip, mmp, &sl);
+      if (hybrid)
+        row_pass_mf<true>(a, v, sink4, kSkip, mmp, &sl);
+      else
+        row_pass_mf<false>(a, v, sink4, kSkip, mmp, &sl);
     }
   };
   const int* rid_sm = (!ASM && mm.rows) ? mm.rid : nullptr;
@@ -2358,7 +2414,7 @@ __device__ __forceinline__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, d
     if (rows_on_lanes)
       for_warp_rows<1>(a.N, kSkip, sl.K, nullptr, nullptr, f);
     else
-      for_warp_rows<LM>(a.N, kSkip, sl.K, ASM ? nullptr : a.perm, rid_sm, f);
+      for_warp_rows<LM>(a.N, kSkip, sl.K, ASM ? nullptr : a.perm, rid_sm, f, hybrid);
   };
   if (!ASM && (mm.rows || mm.cons)) {
     // the solve's fixed row / constraint metadata into shared memory
@@ -2371,7 +2427,7 @@ __device__ __forceinline__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, d
         const_cast<int4*>(mm.rm)[q] = make_int4(a.row_ptr[r], a.row_ptr[r + 1], a.frozen[r], nb[0]);
         const_cast<int4*>(mm.rn)[q] = make_int4(nb[1], nb[2], nb[3], nb[4]);
         const_cast<int*>(mm.rn5)[q] = nb[5];
-      });
+      }, hybrid);
     if (mm.cons) {
       const int64_t c0 = gtid() - 32 * kSkip;
       if (c0 >= 0)
@@ -2451,7 +2507,10 @@ __device__ __forceinline__ void pcg_pipe(const FFArgs& a, Red& rs, int& iters, d
       pc.lap(0);
       grid_barrier(a, rs);
       pc.lap(1);
-      row_pass_mf(a, mcur, n_sink, kSkip, mmp, &sl);
+      if (hybrid)
+        row_pass_mf<true>(a, mcur, n_sink, kSkip, mmp, &sl);
+      else
+        row_pass_mf<false>(a, mcur, n_sink, kSkip, mmp, &sl);
     }
     pc.lap(2);
     if (pending) {
@@ -3592,8 +3651,15 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
     const char* names_cg[8] = {"A", "Async", "B", "red-", "U", "Usync", "redblk", "redsync"};
     const char* names_pipe[8] = {"A", "Abar", "B", "-", "U", "-", "wait", "bar"};
     const char* const* names = a.pcg_variant == 0 ? names_pipe : names_cg;
-    fprintf(stderr, "[wfk phase] level %d N %d C %lld asm %d iters %.0f | cycles/iter mean/max:", level_tag, L.N,
-            (long long)L.C, int(L.assembled), it);
+    int maxinc = 0;
+    if (a.perm && L.N > 0) {  // incidences of the heaviest row (the row order's first)
+      int32_t r0 = 0, rp[2] = {0, 0};
+      WFK_CUDA(cudaMemcpy(&r0, a.perm, sizeof(int32_t), cudaMemcpyDeviceToHost));
+      WFK_CUDA(cudaMemcpy(rp, L.row_ptr.p + r0, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost));
+      maxinc = rp[1] - rp[0];
+    }
+    fprintf(stderr, "[wfk phase] level %d N %d C %lld asm %d maxinc %d iters %.0f | cycles/iter mean/max:", level_tag,
+            L.N, (long long)L.C, int(L.assembled), maxinc, it);
     for (int k = 0; k < 8; ++k) {
       double m, x;
       stat(k, m, x);
