@@ -345,6 +345,17 @@ int wfk_timer_mark(wfk_ctx* ctx, int32_t slot);
 int wfk_timer_elapsed_ms(wfk_ctx* ctx, int32_t a, int32_t b, double* ms);
 /* write 256 MB on the context's stream so the next call starts with a cold L2 */
 int wfk_flush_l2(wfk_ctx* ctx);
+/* ---- checked mode -------------------------------------------------------------
+ * With WFK_CHECK=1 in the environment when the library loads, every device
+ * buffer is poisoned (0xff bytes) when allocated and carries a 256-byte canary
+ * tail that every call verifies before it returns: a write past the end of any
+ * device buffer fails that call with WFK_E_CUDA (the stand-in for
+ * compute-sanitizer memcheck / initcheck, which the GPU pool does not offer).
+ * wfk_check_enabled: 1 in checked mode.  wfk_debug_overrun: self-test of the
+ * detector -- a kernel writes `past_end` bytes beyond the end of a context
+ * scratch buffer (0: within it, and the buffer's canary is renewed). */
+int wfk_check_enabled(void);
+int wfk_debug_overrun(wfk_ctx* ctx, int32_t past_end);
 /* page-locked host memory for frame buffers (cudaMallocHost) */
 int wfk_host_alloc(size_t bytes, void** out);
 void wfk_host_free(void* p);

@@ -10,6 +10,40 @@
 
 using namespace wfk;
 
+// checked mode (WFK_CHECK=1, wfk_context.cuh): the canary registry of every
+// live DevBuf allocation
+namespace wfk {
+std::mutex& guard_mutex() {
+  static std::mutex m;
+  return m;
+}
+std::map<const void*, GuardEntry>& guard_table() {
+  static std::map<const void*, GuardEntry> t;
+  return t;
+}
+int guard_verify(std::string* what) {
+  std::lock_guard<std::mutex> lock(guard_mutex());
+  int broken = 0;
+  unsigned char tail[kGuardBytes];
+  for (const auto& kv : guard_table()) {
+    WFK_CUDA(cudaMemcpy(tail, static_cast<const char*>(kv.first) + kv.second.bytes, kGuardBytes,
+                        cudaMemcpyDeviceToHost));
+    size_t first = kGuardBytes;
+    for (size_t i = 0; i < kGuardBytes; ++i)
+      if (tail[i] != kGuardByte) {
+        first = i;
+        break;
+      }
+    if (first == kGuardBytes) continue;
+    if (broken++ == 0 && what)
+      *what = "WFK_CHECK: write past the end of a " + std::to_string(kv.second.bytes) +
+              "-byte device buffer (canary byte " + std::to_string(first) + " overwritten, device " +
+              std::to_string(kv.second.device) + ")";
+  }
+  return broken;
+}
+}  // namespace wfk
+
 namespace {
 
 template <class F>
@@ -18,6 +52,12 @@ int guard(wfk_ctx* c, F&& f) {
   try {
     WFK_CUDA(cudaSetDevice(c->device));
     f();
+    if (check_mode()) {
+      // every kernel of the call has finished before the canaries are read
+      WFK_CUDA(cudaDeviceSynchronize());
+      std::string what;
+      if (guard_verify(&what) > 0) throw Error(WFK_E_CUDA, what);
+    }
     return WFK_OK;
   } catch (const Error& e) {
     c->err = e.what();
@@ -1003,6 +1043,29 @@ int wfk_timer_elapsed_ms(wfk_ctx* c, int32_t a, int32_t b, double* ms) {
     float f = 0;
     WFK_CUDA(cudaEventElapsedTime(&f, c->prof.timer[a], c->prof.timer[b]));
     *ms = f;
+  });
+}
+
+int wfk_check_enabled(void) { return check_mode() ? 1 : 0; }
+
+__global__ void k_debug_fill(uint8_t* p, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    p[i] = 0x5a;
+}
+
+int wfk_debug_overrun(wfk_ctx* c, int32_t past_end) {
+  if (past_end < 0 || size_t(past_end) > kGuardBytes) {
+    if (c) c->err = "past_end must be in [0, 256]";
+    return WFK_E_INVALID_ARG;
+  }
+  return guard(c, [&] {
+    dev_free(c->debug_buf.p);  // a fresh buffer (and canary) every call
+    c->debug_buf.p = nullptr;
+    c->debug_buf.cap = 0;
+    uint8_t* p = c->debug_buf.ensure(4000);
+    k_debug_fill<<<4, 256, 0, c->stream>>>(p, int64_t(c->debug_buf.cap) + past_end);
+    WFK_CUDA(cudaGetLastError());
+    WFK_CUDA(cudaStreamSynchronize(c->stream));
   });
 }
 

@@ -7,6 +7,8 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -37,6 +39,69 @@ inline bool alloc_trace() {
   return on;
 }
 
+// ---- checked mode (WFK_CHECK=1) ---------------------------------------------
+// compute-sanitizer is not available on the GPU pool, so the library carries
+// its own memcheck / initcheck stand-ins, switched on by the environment when
+// the process starts:
+//  * every DevBuf allocation is filled with 0xff bytes before use (NaN doubles
+//    and floats, -1 integers), so a kernel that reads memory nothing wrote
+//    feeds NaNs / -1 indices into results the parity tests compare with the
+//    reference -- instead of the zeros a fresh cudaMalloc usually returns;
+//  * every DevBuf carries a kGuardBytes canary tail (0xa5) past its capacity,
+//    verified after every C-ABI call (guard_verify in api.cu's guard()): a kernel
+//    writing past the end of any buffer fails the call with WFK_E_CUDA naming
+//    the buffer's size.
+// Off (the default), allocations are exactly as before: no fill, no tail.
+inline bool check_mode() {
+  static const bool on = [] {
+    const char* v = std::getenv("WFK_CHECK");
+    return v && *v && *v != '0';
+  }();
+  return on;
+}
+constexpr size_t kGuardBytes = 256;
+constexpr unsigned char kGuardByte = 0xa5;
+constexpr unsigned char kPoisonByte = 0xff;
+struct GuardEntry {
+  size_t bytes;  // usable bytes; the canary starts here
+  int device;
+};
+std::mutex& guard_mutex();
+std::map<const void*, GuardEntry>& guard_table();
+inline void guard_add(const void* p, size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(guard_mutex());
+  guard_table()[p] = GuardEntry{bytes, dev};
+}
+inline void guard_drop(const void* p) {
+  std::lock_guard<std::mutex> lock(guard_mutex());
+  guard_table().erase(p);
+}
+// allocation of `bytes` usable bytes (+ the canary in checked mode); poisoned
+// and synchronised in checked mode so the fill is ordered before any stream
+inline void* dev_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (!check_mode()) {
+    WFK_CUDA(cudaMalloc(&p, bytes));
+    return p;
+  }
+  WFK_CUDA(cudaMalloc(&p, bytes + kGuardBytes));
+  WFK_CUDA(cudaMemset(p, kPoisonByte, bytes));
+  WFK_CUDA(cudaMemset(static_cast<char*>(p) + bytes, kGuardByte, kGuardBytes));
+  WFK_CUDA(cudaDeviceSynchronize());
+  guard_add(p, bytes);
+  return p;
+}
+inline void dev_free(void* p) {
+  if (!p) return;
+  if (check_mode()) guard_drop(p);
+  cudaFree(p);
+}
+// verifies every live canary (checked mode); returns the number broken and
+// describes the first in *what
+int guard_verify(std::string* what);
+
 // Growable device buffer (capacity only grows; contents not preserved).
 template <class T>
 struct DevBuf {
@@ -45,16 +110,14 @@ struct DevBuf {
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  ~DevBuf() {
-    if (p) cudaFree(p);
-  }
+  ~DevBuf() { dev_free(p); }
   T* ensure(size_t n) {
     if (n == 0) n = 1;
     if (n > cap) {
-      if (p) cudaFree(p);
+      dev_free(p);
       p = nullptr;
       size_t want = n + n / 4;
-      WFK_CUDA(cudaMalloc(&p, want * sizeof(T)));
+      p = static_cast<T*>(dev_alloc(want * sizeof(T)));
       if (alloc_trace()) fprintf(stderr, "[wfk alloc] ensure %zu x %zu B\n", want, sizeof(T));
       cap = want;
     }
@@ -63,14 +126,13 @@ struct DevBuf {
   // exact-size ensure keeping the old contents
   T* grow_keep(size_t n, cudaStream_t s) {
     if (n <= cap) return p;
-    T* q = nullptr;
     size_t want = n + n / 4;
-    WFK_CUDA(cudaMalloc(&q, want * sizeof(T)));
+    T* q = static_cast<T*>(dev_alloc(want * sizeof(T)));
     if (alloc_trace()) fprintf(stderr, "[wfk alloc] grow_keep %zu x %zu B\n", want, sizeof(T));
     if (p) {
       WFK_CUDA(cudaMemcpyAsync(q, p, cap * sizeof(T), cudaMemcpyDeviceToDevice, s));
       WFK_CUDA(cudaStreamSynchronize(s));
-      cudaFree(p);
+      dev_free(p);
     }
     p = q;
     cap = want;
@@ -314,6 +376,7 @@ struct wfk_ctx {
   wfk::DevBuf<uint8_t> icp_state;
   int coop_blocks = 0;          // resident blocks for cooperative kernels
   wfk::DistComm* dist = nullptr;  // slab-partitioned PCG (wfk_dist_init)
+  wfk::DevBuf<uint8_t> debug_buf;  // wfk_debug_overrun (checked-mode self-test)
 };
 
 namespace wfk {

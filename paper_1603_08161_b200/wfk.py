@@ -611,6 +611,16 @@ class Context:
     def flush_l2(self):
         self._check(lib().wfk_flush_l2(self.h))
 
+    def debug_overrun(self, past_end: int):
+        """Checked-mode self-test (include/wfk.h): a kernel writes `past_end`
+        bytes beyond a scratch buffer; raises WfkError when WFK_CHECK caught it."""
+        self._check(lib().wfk_debug_overrun(self.h, C.c_int32(past_end)))
+
+
+def check_enabled() -> bool:
+    """True when the library runs in checked mode (WFK_CHECK=1 at load)."""
+    return bool(lib().wfk_check_enabled())
+
 def pipeline_config(solver=None, correspond=None, fusion=None, reassociations=3, estimate_pose=True,
                     icp=None, use_features=True, features=None) -> PipelineConfig:
     """ReconstructorConfig defaults (config.hpp:30-46): ICP on, features on, 3 reassociations."""

@@ -1,5 +1,6 @@
 """Small workload for compute-sanitizer (memcheck / initcheck / racecheck /
-synccheck): one coarse-to-fine flip-flop solve on a 12^3 jittered sphere
+synccheck, where offered) and for libwfk's checked mode (WFK_CHECK=1,
+tests/test_gpu_checked.py): one coarse-to-fine flip-flop solve on a 12^3 jittered sphere
 (pipelined PCG, and the Chronopoulos-Gear variant when WFK_PCG=cg), one
 fusion step, and one 32^3 process_frame (association, ICP, features, solve,
 fusion).  Run by tools/sanitize.sh; exits non-zero on a parity failure."""
