@@ -13,13 +13,14 @@ using namespace wfk;
 // checked mode (WFK_CHECK=1, wfk_context.cuh): the canary registry of every
 // live DevBuf allocation
 namespace wfk {
+// never destroyed: a DevBuf freed during static destruction still finds them
 std::mutex& guard_mutex() {
-  static std::mutex m;
-  return m;
+  static std::mutex* m = new std::mutex;
+  return *m;
 }
 std::map<const void*, GuardEntry>& guard_table() {
-  static std::map<const void*, GuardEntry> t;
-  return t;
+  static auto* t = new std::map<const void*, GuardEntry>;
+  return *t;
 }
 int guard_verify(std::string* what) {
   std::lock_guard<std::mutex> lock(guard_mutex());
