@@ -569,8 +569,10 @@ def run_solve(args):
                    "lattice": [n] * 3, "depth_resolution": list(cfg_s["K"][4:]),
                    "rows_per_level": [int(x) for x in act], "dense_constraints": int(n_cons),
                    "l2": "flushed (256 MB write) before every solve",
-                   "parallelism": (f"single GPU; matrix-free levels' CG slab-partitioned into {args.slabs} ranks "
-                                   "(block groups of one cooperative launch)") if args.slabs else "single GPU"},
+                   "parallelism": (f"single GPU; matrix-free levels of >= {os.environ.get('WFK_SLAB_MIN_ROWS', 100000)} "
+                                   f"rows: CG slab-partitioned into {args.slabs} ranks (block groups of one "
+                                   "cooperative launch); smaller levels unpartitioned (replicated across ranks)")
+                                  if args.slabs else "single GPU"},
         "pcg_iters_per_s": pcg / (total_ms * 1e-3), "pcg_iterations_per_solve": pcg / args.steps,
         "solve_ms": [round(x, 3) for x in times], "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": "k_flip_flop", "achieved": achieved, "peak": peak,

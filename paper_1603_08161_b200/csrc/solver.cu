@@ -2325,6 +2325,11 @@ __device__ inline MfMeta mf_meta(char* base, const PipeLayout& l, bool rows, boo
 }
 constexpr int kPipeSkip = 1;  // global warp 0 sums the split reductions
 constexpr int kCgMinRows = 500000;  // spilled levels from this size run the Chronopoulos-Gear PCG
+// WFK_SLABS: matrix-free levels from this size are slab-partitioned; smaller
+// levels (latency-bound, a few thousand rows per SM) run the unpartitioned
+// fused PCG, replicated on every rank of a multi-GPU solve the way dist.cu
+// replicates assembly.  WFK_SLAB_MIN_ROWS overrides (tests: 0 = every level).
+constexpr int kSlabMinRows = 100000;
 constexpr int kFastBlock = 512;      // threads per block of the WFK_PRECISION_FAST CG kernel
 constexpr size_t kPipeSmemMax = 220 * 1024;  // dynamic shared memory for the row slots
 
@@ -3386,11 +3391,15 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   // read per call so tests can force the Chronopoulos-Gear variant
   const char* pcg_env = getenv("WFK_PCG");
   a.pcg_variant = (pcg_env && std::string(pcg_env) == "cg") ? 1 : 0;
-  // WFK_SLABS=S (per call): matrix-free levels run the slab-partitioned CG
-  // with S ranks (pcg_slab; S = 1 is the same kernel unpartitioned)
+  // WFK_SLABS=S (per call): matrix-free levels of >= kSlabMinRows rows run
+  // the slab-partitioned CG with S ranks (pcg_slab; S = 1 is the same kernel
+  // unpartitioned)
   const char* slab_env = getenv("WFK_SLABS");
   const int slabs = slab_env ? atoi(slab_env) : 0;
-  const bool slab = slabs >= 1 && !L.assembled && L.N > 0 && mode == 0 && c->precision != WFK_PRECISION_FAST;
+  const char* slab_min_env = getenv("WFK_SLAB_MIN_ROWS");
+  const int64_t slab_min = slab_min_env ? atoll(slab_min_env) : kSlabMinRows;
+  const bool slab = slabs >= 1 && !L.assembled && L.N > 0 && int64_t(L.N) >= slab_min && mode == 0 &&
+                    c->precision != WFK_PRECISION_FAST;
   a.slab = SlabDev{};
   if (slab) a.pcg_variant = 1;
   a.assembled = L.assembled ? 1 : 0;

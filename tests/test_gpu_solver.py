@@ -451,6 +451,7 @@ def _slab_solve(ctx, monkeypatch, slabs, n=48, ncons=6000):
     p = SolverParams.make()
     pose = Pose.make(O.euler_to_matrix((0.0, 0.01, 0.0)), (0.005, 0, 0))
     monkeypatch.setenv("WFK_SLABS", str(slabs))
+    monkeypatch.setenv("WFK_SLAB_MIN_ROWS", "0")  # partition every matrix-free level of the small fixture
     ctx.upload_volume(v)
     ctx.upload_constraints(cons)
     tg = ctx.solve_coarse_to_fine(pose, p)
@@ -479,6 +480,24 @@ def test_slab_cg_parity(ctx, monkeypatch):
     ref = make_volume(48)
     tr = O.solve_coarse_to_fine(ref, pose, cons, p)
     compare_solves(v, ref, tg, tr)
+
+
+def test_slab_partition_skips_small_levels(ctx, monkeypatch):
+    """Under WFK_SLABS only matrix-free levels of >= kSlabMinRows (100 K) rows
+    are partitioned; the fixture's levels are all smaller, so the solve is the
+    fused one, bit for bit."""
+    base_v, base_t, _, _, _ = _slab_solve(ctx, monkeypatch, 0)
+    monkeypatch.delenv("WFK_SLAB_MIN_ROWS")
+    v = make_volume(48)
+    cons = random_dense_constraints(v, 6000, seed=13)
+    pose = Pose.make(O.euler_to_matrix((0.0, 0.01, 0.0)), (0.005, 0, 0))
+    ctx.upload_volume(v)
+    ctx.upload_constraints(cons)
+    monkeypatch.setenv("WFK_SLABS", "4")
+    t = ctx.solve_coarse_to_fine(pose, SolverParams.make())
+    ctx.download_volume(v)
+    assert np.array_equal(v.deformed, base_v.deformed)
+    assert [e["energy"]["total"] for e in t] == [e["energy"]["total"] for e in base_t]
 
 
 def test_slab_too_thin_is_rejected(ctx, monkeypatch):

@@ -14,5 +14,5 @@ python - <<'PY'
 import json
 for line in open("gpurun_out/slab_sweep.jsonl"):
     d = json.loads(line)
-    print(d["config"]["lattice"][0], d["config"]["parallelism"][:60], round(d["value"], 2), d["energy_final_hex"])
+    print(d["config"]["lattice"][0], d["config"]["parallelism"][:110], round(d["value"], 2), d["energy_final_hex"])
 PY
