@@ -2325,6 +2325,11 @@ __device__ inline MfMeta mf_meta(char* base, const PipeLayout& l, bool rows, boo
 }
 constexpr int kPipeSkip = 1;  // global warp 0 sums the split reductions
 constexpr int kCgMinRows = 500000;  // spilled levels from this size run the Chronopoulos-Gear PCG
+// ... and from this size when they carry fewer than 4 constraint incidences
+// per row (256^3 level 0: 214 K rows, 2.3 per row, frame-1 solve 13.57 ->
+// 13.21 ms; 512^3 level 2: 205 K rows, 12.6 per row, stays pipelined: 119.9
+// vs 121.0 ms with CG)
+constexpr int kCgMinRowsSparse = 200000;
 // WFK_SLABS: matrix-free levels from this size are slab-partitioned; smaller
 // levels (latency-bound, a few thousand rows per SM) run the unpartitioned
 // fused PCG, replicated on every rank of a multi-GPU solve the way dist.cu
@@ -3464,7 +3469,10 @@ static void run_level(wfk_ctx* c, Level& L, const PoseD& pose, const wfk_solver_
   // which streams fewer vectors per iteration, beats the pipelined one
   // (512^3 frame-1 solve 138 vs 173 ms; at 256^3, 215 K rows, the pipelined
   // spill variant still wins, 13.7 vs 14.5 ms).  WFK_PCG=pipe forces pipelined.
-  if (a.pcg_variant == 0 && L.N >= kCgMinRows && !(pcg_env && std::string(pcg_env) == "pipe")) {
+  const char* cg_min_env = getenv("WFK_CG_MIN_ROWS");  // A/B: one plain row threshold
+  const bool cg_size = cg_min_env ? int64_t(L.N) >= atoll(cg_min_env)
+                                  : (L.N >= kCgMinRows || (L.N >= kCgMinRowsSparse && L.E < 4 * int64_t(L.N)));
+  if (a.pcg_variant == 0 && cg_size && !(pcg_env && std::string(pcg_env) == "pipe")) {
     const PipeLayout probe = pipe_layout(L.N, L.C, pipe_rpw(L.assembled, a.asm_rows_on_lanes), G, kCoopBlockShared,
                                          kPipeSkip, false, false);
     if (probe.total > kPipeSmemMax) a.pcg_variant = 1;
