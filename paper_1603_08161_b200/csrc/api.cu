@@ -223,6 +223,12 @@ void wfk_destroy(wfk_ctx* c) {
     if (p) cudaFree(p);
   for (float* p : c->staged_color)
     if (p) cudaFree(p);
+  for (wfk::Level& L : c->lv) {
+    if (L.setup_stream) cudaStreamSynchronize(L.setup_stream);
+    if (L.setup_done) cudaEventDestroy(L.setup_done);
+    if (L.setup_stream) cudaStreamDestroy(L.setup_stream);
+  }
+  if (c->setup_ready) cudaEventDestroy(c->setup_ready);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }

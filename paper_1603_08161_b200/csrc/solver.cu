@@ -3899,6 +3899,54 @@ void solver_rotations(wfk_ctx* c) {
   L.C = Csave;
 }
 
+// Every level's setup -- rows (level_rows), constraint incidences, frozen
+// rows, B^T B / constraint cache (level_constraints) -- depends only on the
+// hierarchy (activity, re-anchored constraints) and the frame's constraints,
+// never on a coarser level's solution.  So after build_hierarchy the levels'
+// setups, chains of small latency-bound kernels, are issued on one stream per
+// level and overlap one another; the context stream waits for all of them
+// before the first flip-flop launch.  Each level uses its own cub scratch and
+// count word while its setup runs (swapped in for the context's); the kernels
+// and their inputs are the serial path's, so results are bit-identical
+// (WFK_SERIAL_SETUP=1 restores the serial order for A/B runs).
+template <class T>
+static void swap_buf(DevBuf<T>& a, DevBuf<T>& b) {
+  std::swap(a.p, b.p);
+  std::swap(a.cap, b.cap);
+}
+struct SetupScope {
+  wfk_ctx* c;
+  Level& L;
+  cudaStream_t saved;
+  SetupScope(wfk_ctx* c_, Level& L_) : c(c_), L(L_), saved(c_->stream) {
+    c->stream = L.setup_stream;
+    swap_buf(c->temp, L.setup_temp);
+    swap_buf(c->ivec, L.setup_ivec);
+  }
+  ~SetupScope() {
+    swap_buf(c->ivec, L.setup_ivec);
+    swap_buf(c->temp, L.setup_temp);
+    c->stream = saved;
+  }
+};
+static void setup_levels(wfk_ctx* c, int levels, const PoseD& pd, const wfk_solver_params& p) {
+  if (!c->setup_ready) WFK_CUDA(cudaEventCreateWithFlags(&c->setup_ready, cudaEventDisableTiming));
+  WFK_CUDA(cudaEventRecord(c->setup_ready, c->stream));
+  for (int l = levels - 1; l >= 0; --l) {
+    Level& L = c->lv[l];
+    if (!L.setup_stream) WFK_CUDA(cudaStreamCreateWithFlags(&L.setup_stream, cudaStreamNonBlocking));
+    if (!L.setup_done) WFK_CUDA(cudaEventCreateWithFlags(&L.setup_done, cudaEventDisableTiming));
+    WFK_CUDA(cudaStreamWaitEvent(L.setup_stream, c->setup_ready, 0));
+    {
+      SetupScope scope(c, L);
+      level_rows(c, L);
+      level_constraints(c, L, pd, p);
+    }
+    WFK_CUDA(cudaEventRecord(L.setup_done, L.setup_stream));
+  }
+  for (int l = levels - 1; l >= 0; --l) WFK_CUDA(cudaStreamWaitEvent(c->stream, c->lv[l].setup_done, 0));
+}
+
 void solver_c2f(wfk_ctx* c, const wfk_pose* pose, const wfk_solver_params& p, std::vector<wfk_trace_entry>& trace) {
   require_volume(c);
   bind_level0(c);
@@ -3913,12 +3961,25 @@ void solver_c2f(wfk_ctx* c, const wfk_pose* pose, const wfk_solver_params& p, st
   }
   build_hierarchy(c, p.levels);
   trace_mark("hier");
+  static const bool serial_setup = getenv("WFK_SERIAL_SETUP") != nullptr;
+  if (!serial_setup) {
+    setup_levels(c, p.levels, pd, p);
+    trace_mark("setup");
+  }
+  auto solve = [&](int l) {
+    if (serial_setup) {
+      solve_level(c, l, pd, p, 0, &trace, nullptr);
+    } else {
+      run_level(c, c->lv[l], pd, p, 0, l, &trace, nullptr);
+      trace_mark(l == 0 ? "L0ff" : l == 1 ? "L1ff" : "L2ff");
+    }
+  };
   for (int l = p.levels - 1; l >= 1; --l) {
-    solve_level(c, l, pd, p, 0, &trace, nullptr);
+    solve(l);
     prolong(c, l);
     trace_mark("prolong");
   }
-  solve_level(c, 0, pd, p, 0, &trace, nullptr);
+  solve(0);
   if (tracing) {
     tr.report();
     g_trace = nullptr;

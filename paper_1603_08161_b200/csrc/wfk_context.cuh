@@ -203,6 +203,12 @@ struct Level {
   DevBuf<double> c_b;       // 3C: constraint rhs vector before alpha
   DevBuf<double> c_u;       // 3C: matvec scratch
   DevBuf<int32_t> c_kind;   // C
+  // concurrent setup (solver_c2f): the level's own stream, completion event,
+  // cub scratch and count words while its setup runs beside the other levels'
+  cudaStream_t setup_stream = nullptr;
+  cudaEvent_t setup_done = nullptr;
+  DevBuf<uint8_t> setup_temp;
+  DevBuf<int32_t> setup_ivec;
   // CSR transpose: row -> (constraint, alpha)
   int64_t E = 0;
   DevBuf<int32_t> row_ptr, ent_con, key_in, key_out, val_in, val_out;
@@ -377,6 +383,7 @@ struct wfk_ctx {
   int coop_blocks = 0;          // resident blocks for cooperative kernels
   wfk::DistComm* dist = nullptr;  // slab-partitioned PCG (wfk_dist_init)
   wfk::DevBuf<uint8_t> debug_buf;  // wfk_debug_overrun (checked-mode self-test)
+  cudaEvent_t setup_ready = nullptr;  // solver_c2f: hierarchy built, level setups may start
 };
 
 namespace wfk {
