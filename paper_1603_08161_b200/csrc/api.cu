@@ -163,6 +163,23 @@ void upload_constraints(wfk_ctx* c, const wfk_correspondence* h, int64_t n, bool
 void run_frame(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose* pose, const wfk_pipeline_config* cfg,
                const wfk_correspondence* sparse, int64_t nsparse, int32_t frame_index, wfk_frame_record* rec);
 
+// the context's stream and cub scratch swapped for the side stream's while
+// the feature detection is queued there (run_frame)
+struct SideScope {
+  wfk_ctx* c;
+  cudaStream_t saved;
+  explicit SideScope(wfk_ctx* c_) : c(c_), saved(c_->stream) {
+    c->stream = c->side_stream;
+    std::swap(c->temp.p, c->side_temp.p);
+    std::swap(c->temp.cap, c->side_temp.cap);
+  }
+  ~SideScope() {
+    std::swap(c->temp.p, c->side_temp.p);
+    std::swap(c->temp.cap, c->side_temp.cap);
+    c->stream = saved;
+  }
+};
+
 void stage_mark(wfk_ctx* c, int k) {
   if (c->prof.on) WFK_CUDA(cudaEventRecord(c->prof.ev[2 + k], c->stream));
 }
@@ -229,6 +246,10 @@ void wfk_destroy(wfk_ctx* c) {
     if (L.setup_stream) cudaStreamDestroy(L.setup_stream);
   }
   if (c->setup_ready) cudaEventDestroy(c->setup_ready);
+  if (c->side_stream) cudaStreamSynchronize(c->side_stream);
+  if (c->side_ready) cudaEventDestroy(c->side_ready);
+  if (c->side_done) cudaEventDestroy(c->side_done);
+  if (c->side_stream) cudaStreamDestroy(c->side_stream);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -880,6 +901,21 @@ void run_frame(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose* pose_in, con
       fprintf(stderr, "[wfk stage] frame %d %-10s %8.3f ms  (V %lld T %lld)\n", frame_index, name, ms, (long long)nv,
               (long long)nt);
     };
+    // The feature detection (pyramid, DoG, extrema, orientations, descriptors)
+    // reads only the frame's colour image: it runs on a side stream beside
+    // the mesh / raster / ICP chain, queued after the ICP launches so its own
+    // count readbacks do not hold that chain back; the matching and lifting,
+    // which need the ICP pose, wait for it on the context stream.
+    // WFK_NO_SIDE_FEATURES=1 keeps it in line (A/B).
+    static const bool no_side = getenv("WFK_NO_SIDE_FEATURES") != nullptr;
+    const bool want_features = cfg->use_features && c->frame.has_color;
+    const bool side = want_features && cfg->estimate_pose && !dbg && !no_side;
+    if (side) {
+      if (!c->side_stream) WFK_CUDA(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
+      if (!c->side_ready) WFK_CUDA(cudaEventCreateWithFlags(&c->side_ready, cudaEventDisableTiming));
+      if (!c->side_done) WFK_CUDA(cudaEventCreateWithFlags(&c->side_done, cudaEventDisableTiming));
+      WFK_CUDA(cudaEventRecord(c->side_ready, c->stream));  // frame image uploaded
+    }
     timed("mc", [&] { assoc_extract_mesh(c, pose, &nv, &nt); });
     if (nt == 0) throw Error(WFK_E_LOGIC, "empty isosurface before frame");
     timed("normals", [&] { assoc_compute_normals(c); });
@@ -888,7 +924,19 @@ void run_frame(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose* pose_in, con
       wfk_icp_params ip = cfg->icp;
       ip.corr = cfg->correspond;
       wfk_icp_result icp;
-      timed("icp", [&] { assoc_estimate_pose(c, K, pose_local, ip, &icp); });
+      if (side) {
+        assoc_estimate_pose_begin(c, K, pose_local, ip);
+        {
+          SideScope scope(c);
+          WFK_CUDA(cudaStreamWaitEvent(c->stream, c->side_ready, 0));
+          int32_t nf = 0;
+          features_detect(c, cfg->features, nullptr, 0, &nf, nullptr);
+          WFK_CUDA(cudaEventRecord(c->side_done, c->stream));
+        }
+        assoc_estimate_pose_end(c, &icp);
+      } else {
+        timed("icp", [&] { assoc_estimate_pose(c, K, pose_local, ip, &icp); });
+      }
       rec->icp_degraded = icp.degraded;
       rec->icp_rms = icp.rms;
       rec->icp_iterations = icp.iterations;
@@ -899,10 +947,13 @@ void run_frame(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose* pose_in, con
       timed("raster0", [&] { assoc_rasterize(c, K, nullptr); });
     }
     bool features = false;
-    if (cfg->use_features && c->frame.has_color) {  // sparse term against the history (pipeline.cpp:185-217)
+    if (want_features) {  // sparse term against the history (pipeline.cpp:185-217)
       int32_t nf = 0;
       timed("features", [&] {
-        features_detect(c, cfg->features, nullptr, 0, &nf, nullptr);
+        if (side)
+          WFK_CUDA(cudaStreamWaitEvent(c->stream, c->side_done, 0));
+        else
+          features_detect(c, cfg->features, nullptr, 0, &nf, nullptr);
         features_frame_sparse(c, K, pose_local, cfg->features, &rec->match_count);
       });
       features = true;

@@ -1011,8 +1011,22 @@ __global__ void __launch_bounds__(kIcpUpdateThreads) k_icp_update(const double* 
   }
 }
 
+// Split in two so wfk_process_frame can queue other work (the feature
+// detection on a side stream) between the ICP launches and the readback of
+// the pose: begin enqueues every ICP kernel and the asynchronous state
+// readback, end waits for it.
+void assoc_estimate_pose_begin(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose& initial,
+                               const wfk_icp_params& prm);
+void assoc_estimate_pose_end(wfk_ctx* c, wfk_icp_result* out);
+
 void assoc_estimate_pose(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose& initial, const wfk_icp_params& prm,
                          wfk_icp_result* out) {
+  assoc_estimate_pose_begin(c, K, initial, prm);
+  assoc_estimate_pose_end(c, out);
+}
+
+void assoc_estimate_pose_begin(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose& initial,
+                               const wfk_icp_params& prm) {
   FrameDev& f = c->frame;
   GBufDev& b = c->gbuf;
   if (!f.maps_valid) throw Error(WFK_E_INVALID_ARG, "no point/normal maps (call backproject first)");
@@ -1082,7 +1096,11 @@ void assoc_estimate_pose(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose& in
     }
   }
   WFK_CUDA(cudaMemcpyAsync(hst, st, sizeof(IcpDev), cudaMemcpyDeviceToHost, s));
-  WFK_CUDA(cudaStreamSynchronize(s));
+}
+
+void assoc_estimate_pose_end(wfk_ctx* c, wfk_icp_result* out) {
+  const IcpDev* hst = reinterpret_cast<const IcpDev*>(c->h_pinned + 1024);
+  WFK_CUDA(cudaStreamSynchronize(c->stream));
   std::memset(out, 0, sizeof(*out));
   for (int i = 0; i < 9; ++i) out->pose.rotation[i] = hst->R[i];
   for (int i = 0; i < 3; ++i) out->pose.translation[i] = hst->t[i];

@@ -384,6 +384,10 @@ struct wfk_ctx {
   wfk::DistComm* dist = nullptr;  // slab-partitioned PCG (wfk_dist_init)
   wfk::DevBuf<uint8_t> debug_buf;  // wfk_debug_overrun (checked-mode self-test)
   cudaEvent_t setup_ready = nullptr;  // solver_c2f: hierarchy built, level setups may start
+  // wfk_process_frame: feature detection on a side stream beside mesh / raster / ICP
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t side_ready = nullptr, side_done = nullptr;
+  wfk::DevBuf<uint8_t> side_temp;
 };
 
 namespace wfk {

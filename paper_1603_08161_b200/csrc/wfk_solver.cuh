@@ -78,6 +78,9 @@ void volume_invert_warp(wfk_ctx* c, const wfk_pose* pose, int64_t n, const doubl
                         int32_t max_iters, double tol, double* x, uint8_t* ok);
 void assoc_estimate_pose(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose& initial, const wfk_icp_params& prm,
                          wfk_icp_result* out);
+void assoc_estimate_pose_begin(wfk_ctx* c, const wfk_intrinsics& K, const wfk_pose& initial,
+                               const wfk_icp_params& prm);
+void assoc_estimate_pose_end(wfk_ctx* c, wfk_icp_result* out);
 void assoc_find_dense(wfk_ctx* c, const wfk_intrinsics& K, const wfk_correspond_params& p, bool drop_inactive,
                       int64_t* n_out);
 
